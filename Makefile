@@ -1,0 +1,45 @@
+# Build of the B200 (sm_100a) library and the oracle checker.
+#   make            -> paper_1606_01216_b200/lib/libmgpu.so  (+ oracle/liboracle.so)
+#   make ref        -> oracle/_ref/libmorref.so  (needs /root/reference; checker only)
+NVCC    ?= nvcc
+CXX     ?= g++
+ARCH    := -gencode arch=compute_100a,code=sm_100a
+PKG     := paper_1606_01216_b200
+SRC     := $(PKG)/csrc
+LIBDIR  := $(PKG)/lib
+OBJDIR  := build/obj
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -I$(SRC) -Xptxas -v
+CXXFLAGS:= -O2 -std=c++17 -fPIC -Iinclude -Wall -Wextra
+
+CU_SRCS  := $(wildcard $(SRC)/*.cu)
+CPP_SRCS := $(wildcard $(SRC)/*.cpp)
+CU_OBJS  := $(patsubst $(SRC)/%.cu,$(OBJDIR)/%.o,$(CU_SRCS))
+CPP_OBJS := $(patsubst $(SRC)/%.cpp,$(OBJDIR)/%.cpp.o,$(CPP_SRCS))
+
+.PHONY: all lib oracle ref clean
+
+all: lib oracle
+
+lib: $(LIBDIR)/libmgpu.so
+
+$(OBJDIR) $(LIBDIR):
+	mkdir -p $@
+
+$(OBJDIR)/%.o: $(SRC)/%.cu $(SRC)/internal.cuh include/mgpu.h | $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $@.ptxas.log || (cat $@.ptxas.log; exit 1)
+
+$(OBJDIR)/%.cpp.o: $(SRC)/%.cpp include/mgpu.h | $(OBJDIR)
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+$(LIBDIR)/libmgpu.so: $(CU_OBJS) $(CPP_OBJS) | $(LIBDIR)
+	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart
+
+oracle:
+	$(MAKE) -C oracle oracle
+
+ref:
+	$(MAKE) -C oracle ref
+
+clean:
+	rm -rf build $(LIBDIR)
+	$(MAKE) -C oracle clean

@@ -1,0 +1,220 @@
+/*
+ * mgpu.h -- C-ABI of the B200 (sm_100a) SPAI + shifted-system PCG library.
+ *
+ * This is the drop-in boundary for the hot path of the reference
+ * (/root/reference/proj, arXiv 1606.01216 AIRGA):  assembling the shifted
+ * operators A(s) = s^2 M + s D + K, building / updating / applying the SPAI
+ * preconditioner chain, and the right-preconditioned CG solves of A(s) X = F.
+ * Every entry point names the reference interface it replaces (file:line
+ * relative to /root/reference/proj).  Plain pointers and sizes only.
+ *
+ * Conventions (all follow the reference's):
+ *   - CSR: int64 row_ptr[nrows+1], int32 col_idx[nnz] strictly increasing per
+ *     row, double values[nnz] with no stored exact zeros   (include/mor/sparse.hpp:12-22)
+ *   - dense blocks are n x m column-major                   (include/mor/dense.hpp:14-37)
+ *   - preconditioner chains are listed NEWEST FIRST, [Q_z, ..., Q_2, P]
+ *     and applied oldest first                               (include/mor/spai.hpp:63-79)
+ *   - FP64 everywhere; no tensor cores; no CPU fallback: a call that cannot
+ *     run on the device fails with MGPU_ERR_CUDA / MGPU_ERR_UNSUPPORTED.
+ *
+ * Errors: every call returns an mgpu_status.  The exception class the
+ * reference would throw maps 1:1 (include/mor/errors.hpp:13-59):
+ *   ArgumentError -> MGPU_ERR_ARG, StagnationError(column) -> MGPU_ERR_STAGNATION,
+ *   BreakdownError(iteration) -> MGPU_ERR_BREAKDOWN, NumericalError -> MGPU_ERR_NUMERICAL.
+ * mgpu_last_error() returns the payload (column / iteration, plus the RHS
+ * column and point index for batched solves) and a message shaped like the
+ * reference's what().  Exhausting maxit is NOT an error (converged = 0),
+ * exactly as in krylov.cpp:128-137.
+ *
+ * Threading: a context is bound to one device and one CUDA stream and must be
+ * used by one host thread at a time; independent contexts are independent
+ * (one per GPU for shift sharding).
+ */
+#ifndef MGPU_H
+#define MGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum mgpu_status
+{
+  MGPU_OK = 0,
+  MGPU_ERR_ARG = 1,         /* mor::ArgumentError     */
+  MGPU_ERR_STAGNATION = 2,  /* mor::StagnationError   */
+  MGPU_ERR_BREAKDOWN = 3,   /* mor::BreakdownError    */
+  MGPU_ERR_NUMERICAL = 4,   /* mor::NumericalError    */
+  MGPU_ERR_UNSUPPORTED = 5, /* shape outside the kernels' envelope (message says which) */
+  MGPU_ERR_CUDA = 6,        /* CUDA runtime / launch failure */
+  MGPU_ERR_NCCL = 7,
+} mgpu_status;
+
+typedef enum mgpu_memkind
+{
+  MGPU_HOST = 0,   /* pointer is host memory (pageable or pinned) */
+  MGPU_DEVICE = 1, /* pointer is device memory on the context's device */
+} mgpu_memkind;
+
+typedef struct mgpu_ctx mgpu_ctx; /* device + stream + scratch arena + last error */
+typedef struct mgpu_csr mgpu_csr; /* device-resident CSR matrix */
+
+/* ------------------------------------------------------------------ context */
+
+/* stream: a cudaStream_t to run on, or NULL for a library-owned stream. */
+int mgpu_ctx_create(int device, void *stream, mgpu_ctx **out);
+int mgpu_ctx_destroy(mgpu_ctx *ctx);
+int mgpu_ctx_synchronize(mgpu_ctx *ctx);
+/* Copies the last error's message (NUL-terminated, truncated to cap) and
+ * payload: index = column (stagnation) or iteration (breakdown), rhs_column
+ * and point for batched solves (-1 when not applicable). */
+int mgpu_last_error(const mgpu_ctx *ctx, int64_t *index, int64_t *rhs_column, int64_t *point, char *msg, size_t cap);
+const char *mgpu_status_string(int status);
+/* Number of kernels this context has launched so far (for bench gpu_launches). */
+int64_t mgpu_launch_count(const mgpu_ctx *ctx);
+/* Device-side duration (ms, CUDA events on the context stream) of the last
+ * mgpu_cg_solve* kernel region and the number of CG iterations it ran. */
+int mgpu_last_cg_timing(const mgpu_ctx *ctx, double *ms, int64_t *iterations);
+
+/* ------------------------------------------------------------------ CSR I/O */
+
+/* Replaces constructing a mor::SparseMatrix (sparse.hpp:16-46).  The host
+ * arrays are copied (H2D) and may be reused on return.  The CSR invariants
+ * are validated on the device (MGPU_ERR_ARG on violation, cf. sparse.cpp:108-138). */
+int mgpu_csr_upload(mgpu_ctx *ctx, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t *row_ptr,
+                    const int32_t *col_idx, const double *values, mgpu_csr **out);
+/* Same, from device pointers already on the context's device (copied). */
+int mgpu_csr_upload_device(mgpu_ctx *ctx, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t *row_ptr,
+                           const int32_t *col_idx, const double *values, mgpu_csr **out);
+/* Shape of the matrix as the reference would store it: stored exact zeros
+ * (the LS-SPAI kernels keep the pattern fixed) are dropped on download. */
+int mgpu_csr_info(mgpu_ctx *ctx, const mgpu_csr *a, int64_t *nrows, int64_t *ncols, int64_t *nnz);
+int mgpu_csr_download(mgpu_ctx *ctx, const mgpu_csr *a, int64_t *row_ptr, int32_t *col_idx, double *values);
+/* Raw device view (no zero dropping) for callers that stay on the device. */
+int mgpu_csr_device_view(const mgpu_csr *a, int64_t *nrows, int64_t *nnz, const int64_t **row_ptr,
+                         const int32_t **col_idx, const double **values);
+int mgpu_csr_free(mgpu_csr *a);
+
+/* ------------------------------------------------------------ core kernels */
+
+/* sparse.cpp:167-218 sp_add_scaled: a*A + b*B on the union pattern, no FMA
+ * contraction, exact zeros dropped. */
+int mgpu_sp_add_scaled(mgpu_ctx *ctx, const mgpu_csr *A, const mgpu_csr *B, double a, double b, mgpu_csr **out);
+/* system.cpp:64-68 shifted_operator, batched over l shifts:
+ * out[i] = sp_add(sp_add(M, D, s_i^2, s_i), K, 1, 1), bitwise identical to the reference. */
+int mgpu_shifted_operators(mgpu_ctx *ctx, const mgpu_csr *M, const mgpu_csr *D, const mgpu_csr *K, int l,
+                           const double *shifts, mgpu_csr **out);
+/* sparse.cpp:220-249 transpose (rows of the result ascending, like the reference). */
+int mgpu_transpose(mgpu_ctx *ctx, const mgpu_csr *A, mgpu_csr **out);
+/* sparse.cpp:251-296: trace(A), trace_inner(A, B) with a fixed-order device
+ * reduction (deterministic; trace_inner(A,B) == trace_inner(B,A) bitwise). */
+int mgpu_trace(mgpu_ctx *ctx, const mgpu_csr *A, double *out);
+int mgpu_trace_inner(mgpu_ctx *ctx, const mgpu_csr *A, const mgpu_csr *B, double *out);
+/* sparse.cpp:140-158 spmv_into: y = A x (x, y device pointers). */
+int mgpu_spmv(mgpu_ctx *ctx, const mgpu_csr *A, const double *x, double *y);
+/* spai.cpp:361-373 chain_apply: y = Q_z(...(Q_2(P x))). factors newest first.
+ * x, y: n-vectors in `where` memory. */
+int mgpu_chain_apply(mgpu_ctx *ctx, int z, const mgpu_csr *const *factors, const double *x, double *y,
+                     mgpu_memkind where);
+
+/* ------------------------------------------------------------------ SPAI */
+
+typedef enum mgpu_spai_mode
+{
+  MGPU_SPAI_SEQUENTIAL = 0, /* spai.hpp:38-42 (not available on the device: MGPU_ERR_UNSUPPORTED) */
+  MGPU_SPAI_FROZEN = 1,
+} mgpu_spai_mode;
+
+/* spai.cpp:314-331 spai_build (MR-SPAI, Alg. 2): P = alpha I refined per
+ * column until ||e_j - K p_j|| <= tol.  col_residual (host, n, optional)
+ * receives SpaiFactor::target_frob_residual.  Stagnation reports the LOWEST
+ * failing column, as the reference's sequential column loop would. */
+int mgpu_spai_build(mgpu_ctx *ctx, const mgpu_csr *K, double tol, int64_t max_col_iters, int mode, mgpu_csr **P,
+                    double *col_residual);
+/* spai.cpp:333-350 spai_update (Alg. 4): Q minimising ||K_old - K_new Q||_F. */
+int mgpu_spai_update(mgpu_ctx *ctx, const mgpu_csr *K_old, const mgpu_csr *K_new, double tol, int64_t max_col_iters,
+                     int mode, mgpu_csr **Q, double *col_residual);
+
+typedef enum mgpu_ls_pattern
+{
+  MGPU_PATTERN_A = 0,  /* J_j = pattern of row j of A               */
+  MGPU_PATTERN_A2 = 1, /* J_j = pattern of row j of the symbolic A*A */
+} mgpu_ls_pattern;
+
+/* Static-pattern least-squares SPAI (north star subsystem 1; not in the
+ * reference, whose closest relative is spai_build, spai.cpp:314): per column j
+ * min ||e_j - A(I,J) m||, J from `pattern`, I = rows of A(:,J), solved by
+ * Householder QR in FP64, one warp per column.  K_old != NULL gives the update
+ * factor (rhs K_old(I, j), cf. spai.cpp:333).  Rank deficiency ->
+ * MGPU_ERR_NUMERICAL naming the column. */
+int mgpu_spai_ls(mgpu_ctx *ctx, const mgpu_csr *A, const mgpu_csr *K_old, int pattern, mgpu_csr **P);
+/* Batched LS-SPAI over l operators (one launch for all shifts). */
+int mgpu_spai_ls_batched(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, const mgpu_csr *const *K_old, int pattern,
+                         mgpu_csr **P);
+
+/* Sparse x sparse product C = A * B on the device (north star subsystem 2:
+ * collapsing a chain [Q, P] into one factor Q*P, cf. spai.cpp:361-373).
+ * Exact zeros are dropped. */
+int mgpu_spgemm(mgpu_ctx *ctx, const mgpu_csr *A, const mgpu_csr *B, mgpu_csr **C);
+
+/* ------------------------------------------------------------------ CG */
+
+typedef struct mgpu_cg_out
+{
+  /* all optional (NULL = not wanted); layout [point][column][row] = n x m
+   * column-major per point, in `where` memory */
+  double *X;          /* BlockSolveResult::X                   (krylov.hpp:44-51) */
+  double *recurrence; /* BlockSolveResult::recurrence_residuals */
+  double *true_res;   /* BlockSolveResult::true_residuals       */
+  /* host arrays of l*m entries */
+  int64_t *iterations; /* per column iterations (krylov.cpp:115)              */
+  int *converged;      /* per column converged flag                           */
+  int *status;         /* per column MGPU_OK / MGPU_ERR_BREAKDOWN              */
+  int64_t *breakdown_iteration; /* iteration index of a breakdown, else -1     */
+  /* optional host history [point][column][history_cap]: recurrence ||r||/||b|| per iteration */
+  double *history;
+  int64_t history_cap;
+} mgpu_cg_out;
+
+/* krylov.cpp:28-174 pcg_solve / block_solve, batched over l shifted systems
+ * and m right-hand sides:  for every point p and column c, CG on A_p P_p with
+ * x~0 = 0, the true-residual confirm / restart branch, the breakdown guard
+ * (d,w) <= 1e-30 (d,d), maxit, and solution = P_p x~.  All recurrences run in
+ * one persistent cooperative kernel with the control flow on the device.
+ *   A[p]             : l operators (n x n)
+ *   chains[p*z + f]  : z factors per point, newest first (z may be 0: P = I)
+ *   B                : rhs, [point][column][row]; ldb_point = elements between
+ *                      points (0 = the same n x m block for every point)
+ * Returns MGPU_ERR_BREAKDOWN for the first (point, column) that broke down,
+ * with the payload the reference's block_solve would carry (krylov.cpp:160-163);
+ * other columns still complete and are reported in `out`. */
+int mgpu_cg_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_csr *const *chains, int64_t n,
+                  int64_t m, const double *B, int64_t ldb_point, double rtol, int64_t maxit, mgpu_memkind where,
+                  mgpu_cg_out *out);
+
+/* ------------------------------------------------------------ model input */
+
+/* Host-side model generators for benchmarks and tests (not on the hot path).
+ * Reference chain model: model_io.cpp:18-87 beam_generate.  Hermite
+ * cantilever: BASELINE.json configs.  Output arrays are
+ * malloc'd; release with mgpu_host_free. */
+typedef struct mgpu_host_csr
+{
+  int64_t nrows, ncols, nnz;
+  int64_t *row_ptr;
+  int32_t *col_idx;
+  double *values;
+} mgpu_host_csr;
+int mgpu_model_chain(int64_t n, double alpha, double beta, double stiffness_scale, double mass_scale,
+                     int consistent_mass, mgpu_host_csr *M, mgpu_host_csr *D, mgpu_host_csr *K);
+int mgpu_model_hermite(int64_t ne, double E, double I, double rho, double area, double L, double alpha, double beta,
+                       mgpu_host_csr *M, mgpu_host_csr *D, mgpu_host_csr *K);
+void mgpu_host_free(mgpu_host_csr *a);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MGPU_H */

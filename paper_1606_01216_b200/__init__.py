@@ -1,0 +1,16 @@
+"""B200-native SPAI + shifted-system PCG (the AIRGA solve path of arXiv 1606.01216).
+
+The compute path is libmgpu.so (hand-written sm_100a CUDA behind the C-ABI in
+include/mgpu.h).  This package is the thin host mirror of the reference's
+solver / preconditioner interface used by tests and the benchmark; the C++
+drop-in for the reference itself is paper_1606_01216_b200/host/ (see
+INTEGRATION.md).
+"""
+from .mgpu import (  # noqa: F401
+    ArgumentError, BreakdownError, BlockSolveResult, Context, CudaError, DeviceCsr, MgpuError, NumericalError,
+    SparseMatrix, SpaiFactor, StagnationError, UnsupportedError, block_solve, cg_solve_batched, chain_apply,
+    default_context, lib, model_chain, model_hermite, pcg_solve, shifted_operator, shifted_operators, sp_add_scaled,
+    spai_build, spai_ls, spai_ls_batched, spai_update, spgemm, trace, trace_inner, transpose,
+    FROZEN, SEQUENTIAL, PATTERN_A, PATTERN_A2,
+)
+from .backend import CudaCgBackend  # noqa: F401

@@ -1,0 +1,374 @@
+// Context, error state, CSR residency and the deterministic reduction.
+#include <cstring>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace mgpu
+{
+
+void set_error(mgpu_ctx *ctx, const Error &e)
+{
+  ctx->last_status = e.status;
+  ctx->err_index = e.index;
+  ctx->err_col = e.rhs_column;
+  ctx->err_point = e.point;
+  ctx->err_msg = e.what();
+}
+
+mgpu_csr *new_csr(mgpu_ctx *ctx, int64_t nrows, int64_t ncols, int64_t nnz)
+{
+  auto *a = new mgpu_csr;
+  a->ctx = ctx;
+  a->nrows = nrows;
+  a->ncols = ncols;
+  a->nnz = nnz;
+  MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&a->row_ptr), sizeof(int64_t) * (nrows + 1), ctx->stream));
+  MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&a->col_idx), sizeof(int32_t) * (nnz > 0 ? nnz : 1), ctx->stream));
+  MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&a->values), sizeof(double) * (nnz > 0 ? nnz : 1), ctx->stream));
+  return a;
+}
+
+namespace
+{
+
+constexpr int kSumBlocks = 512;
+
+// Fixed-order block tree over shared memory (deterministic for a fixed blockDim).
+__device__ double block_tree_sum(double v, double *sh)
+{
+  sh[threadIdx.x] = v;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1)
+  {
+    if (threadIdx.x < s)
+      sh[threadIdx.x] = __dadd_rn(sh[threadIdx.x], sh[threadIdx.x + s]);
+    __syncthreads();
+  }
+  return sh[0];
+}
+
+__global__ void det_sum_stage1(const double *__restrict__ vals, int64_t count, double *__restrict__ partial)
+{
+  __shared__ double sh[kThreads];
+  double acc = 0.0;
+  const int64_t stride = static_cast<int64_t>(kSumBlocks) * kThreads;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; i < count; i += stride)
+    acc = __dadd_rn(acc, vals[i]);
+  const double s = block_tree_sum(acc, sh);
+  if (threadIdx.x == 0)
+    partial[blockIdx.x] = s;
+}
+
+__global__ void det_sum_stage2(const double *__restrict__ partial, double *__restrict__ out)
+{
+  __shared__ double sh[kSumBlocks];
+  const double s = block_tree_sum(partial[threadIdx.x], sh);
+  if (threadIdx.x == 0)
+    *out = s;
+}
+
+// CSR invariant check (sparse.cpp:108-138) without the stored-zero rule for
+// fixed-pattern inputs: flags[0] |= 1 on a structural violation.
+__global__ void validate_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t *__restrict__ rp,
+                             const int32_t *__restrict__ ci, int *flag)
+{
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nrows)
+    return;
+  const int64_t b = rp[i], e = rp[i + 1];
+  bool bad = b > e || b < 0 || e > nnz || (i == 0 && b != 0) || (i == nrows - 1 && e != nnz);
+  for (int64_t k = b; !bad && k < e; ++k)
+  {
+    const int32_t c = ci[k];
+    if (c < 0 || c >= ncols || (k > b && ci[k - 1] >= c))
+      bad = true;
+  }
+  if (bad)
+    atomicOr(flag, 1);
+}
+
+void upload_common(mgpu_ctx *ctx, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t *row_ptr,
+                   const int32_t *col_idx, const double *values, cudaMemcpyKind kind, mgpu_csr **out)
+{
+  MG_ARG(out != nullptr, "mgpu_csr_upload: null output");
+  MG_ARG(nrows >= 0 && ncols >= 0 && nnz >= 0, "SparseMatrix: negative dimension");
+  MG_ARG(row_ptr != nullptr && (nnz == 0 || (col_idx != nullptr && values != nullptr)),
+         "SparseMatrix: null CSR array");
+  MG_ARG(nrows <= INT32_MAX && ncols <= INT32_MAX, "SparseMatrix: dimension exceeds int32 column indices");
+  mgpu_csr *a = new_csr(ctx, nrows, ncols, nnz);
+  try
+  {
+    MG_CUDA(cudaMemcpyAsync(a->row_ptr, row_ptr, sizeof(int64_t) * (nrows + 1), kind, ctx->stream));
+    if (nnz > 0)
+    {
+      MG_CUDA(cudaMemcpyAsync(a->col_idx, col_idx, sizeof(int32_t) * nnz, kind, ctx->stream));
+      MG_CUDA(cudaMemcpyAsync(a->values, values, sizeof(double) * nnz, kind, ctx->stream));
+    }
+    if (nrows > 0)
+    {
+      DBuf flag(sizeof(int), ctx->stream);
+      MG_CUDA(cudaMemsetAsync(flag.ptr, 0, sizeof(int), ctx->stream));
+      validate_csr<<<blocks_for(nrows), kThreads, 0, ctx->stream>>>(nrows, ncols, nnz, a->row_ptr, a->col_idx,
+                                                                    flag.as<int>());
+      check_launch(ctx, "validate_csr");
+      int h = 0;
+      MG_CUDA(cudaMemcpyAsync(&h, flag.ptr, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      MG_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (h != 0)
+        throw Error(MGPU_ERR_ARG, "SparseMatrix: inconsistent CSR arrays");
+    }
+  }
+  catch (...)
+  {
+    mgpu_csr_free(a);
+    throw;
+  }
+  *out = a;
+}
+
+__global__ void count_nonzero_rows(int64_t nrows, const int64_t *__restrict__ rp, const double *__restrict__ v,
+                                   int64_t *__restrict__ counts)
+{
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nrows)
+    return;
+  int64_t c = 0;
+  for (int64_t k = rp[i]; k < rp[i + 1]; ++k)
+    c += v[k] != 0.0;
+  counts[i] = c;
+}
+
+} // namespace
+
+void det_sum(mgpu_ctx *ctx, const double *vals, int64_t count, double *out_dev)
+{
+  DBuf partial(sizeof(double) * kSumBlocks, ctx->stream);
+  det_sum_stage1<<<kSumBlocks, kThreads, 0, ctx->stream>>>(vals, count, partial.as<double>());
+  check_launch(ctx, "det_sum_stage1");
+  det_sum_stage2<<<1, kSumBlocks, 0, ctx->stream>>>(partial.as<double>(), out_dev);
+  check_launch(ctx, "det_sum_stage2");
+}
+
+} // namespace mgpu
+
+using namespace mgpu;
+
+extern "C" {
+
+int mgpu_ctx_create(int device, void *stream, mgpu_ctx **out)
+{
+  if (out == nullptr)
+    return MGPU_ERR_ARG;
+  auto *ctx = new mgpu_ctx;
+  const int st = guard(ctx, [&] {
+    int count = 0;
+    MG_CUDA(cudaGetDeviceCount(&count));
+    MG_ARG(device >= 0 && device < count, "mgpu_ctx_create: no such device");
+    MG_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    MG_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+      throw Error(MGPU_ERR_UNSUPPORTED, "mgpu requires an sm_100 (Blackwell) device, found sm_" +
+                                            std::to_string(prop.major) + std::to_string(prop.minor));
+    ctx->device = device;
+    ctx->num_sms = prop.multiProcessorCount;
+    if (stream != nullptr)
+    {
+      ctx->stream = static_cast<cudaStream_t>(stream);
+    }
+    else
+    {
+      MG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+      ctx->own_stream = true;
+    }
+    MG_CUDA(cudaEventCreate(&ctx->ev0));
+    MG_CUDA(cudaEventCreate(&ctx->ev1));
+  });
+  if (st != MGPU_OK)
+  {
+    std::fprintf(stderr, "mgpu_ctx_create: %s\n", ctx->err_msg.c_str());
+    delete ctx;
+    return st;
+  }
+  *out = ctx;
+  return MGPU_OK;
+}
+
+int mgpu_ctx_destroy(mgpu_ctx *ctx)
+{
+  if (ctx == nullptr)
+    return MGPU_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->ev0)
+    cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1)
+    cudaEventDestroy(ctx->ev1);
+  if (ctx->own_stream)
+    cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return MGPU_OK;
+}
+
+int mgpu_ctx_synchronize(mgpu_ctx *ctx)
+{
+  return guard(ctx, [&] { MG_CUDA(cudaStreamSynchronize(ctx->stream)); });
+}
+
+int mgpu_last_error(const mgpu_ctx *ctx, int64_t *index, int64_t *rhs_column, int64_t *point, char *msg, size_t cap)
+{
+  if (ctx == nullptr)
+    return MGPU_ERR_ARG;
+  if (index)
+    *index = ctx->err_index;
+  if (rhs_column)
+    *rhs_column = ctx->err_col;
+  if (point)
+    *point = ctx->err_point;
+  if (msg && cap > 0)
+  {
+    std::strncpy(msg, ctx->err_msg.c_str(), cap - 1);
+    msg[cap - 1] = '\0';
+  }
+  return ctx->last_status;
+}
+
+const char *mgpu_status_string(int status)
+{
+  switch (status)
+  {
+  case MGPU_OK: return "ok";
+  case MGPU_ERR_ARG: return "argument error";
+  case MGPU_ERR_STAGNATION: return "stagnation";
+  case MGPU_ERR_BREAKDOWN: return "breakdown";
+  case MGPU_ERR_NUMERICAL: return "numerical error";
+  case MGPU_ERR_UNSUPPORTED: return "unsupported";
+  case MGPU_ERR_CUDA: return "cuda error";
+  case MGPU_ERR_NCCL: return "nccl error";
+  default: return "unknown status";
+  }
+}
+
+int64_t mgpu_launch_count(const mgpu_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+int mgpu_last_cg_timing(const mgpu_ctx *ctx, double *ms, int64_t *iterations)
+{
+  if (ctx == nullptr)
+    return MGPU_ERR_ARG;
+  if (ms)
+    *ms = ctx->last_cg_ms;
+  if (iterations)
+    *iterations = ctx->last_cg_iters;
+  return MGPU_OK;
+}
+
+int mgpu_csr_upload(mgpu_ctx *ctx, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t *row_ptr,
+                    const int32_t *col_idx, const double *values, mgpu_csr **out)
+{
+  return guard(ctx, [&] { upload_common(ctx, nrows, ncols, nnz, row_ptr, col_idx, values, cudaMemcpyHostToDevice, out); });
+}
+
+int mgpu_csr_upload_device(mgpu_ctx *ctx, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t *row_ptr,
+                           const int32_t *col_idx, const double *values, mgpu_csr **out)
+{
+  return guard(ctx,
+               [&] { upload_common(ctx, nrows, ncols, nnz, row_ptr, col_idx, values, cudaMemcpyDeviceToDevice, out); });
+}
+
+int mgpu_csr_info(mgpu_ctx *ctx, const mgpu_csr *a, int64_t *nrows, int64_t *ncols, int64_t *nnz)
+{
+  return guard(ctx, [&] {
+    MG_ARG(a != nullptr, "mgpu_csr_info: null matrix");
+    if (nrows)
+      *nrows = a->nrows;
+    if (ncols)
+      *ncols = a->ncols;
+    if (!nnz)
+      return;
+    if (!a->may_hold_zeros || a->nnz == 0)
+    {
+      *nnz = a->nnz;
+      return;
+    }
+    DBuf counts(sizeof(int64_t) * (a->nrows > 0 ? a->nrows : 1), ctx->stream);
+    count_nonzero_rows<<<blocks_for(a->nrows), kThreads, 0, ctx->stream>>>(a->nrows, a->row_ptr, a->values,
+                                                                           counts.as<int64_t>());
+    check_launch(ctx, "count_nonzero_rows");
+    std::vector<int64_t> h(static_cast<size_t>(a->nrows));
+    MG_CUDA(cudaMemcpyAsync(h.data(), counts.ptr, sizeof(int64_t) * a->nrows, cudaMemcpyDeviceToHost, ctx->stream));
+    MG_CUDA(cudaStreamSynchronize(ctx->stream));
+    int64_t t = 0;
+    for (int64_t c : h)
+      t += c;
+    *nnz = t;
+  });
+}
+
+int mgpu_csr_download(mgpu_ctx *ctx, const mgpu_csr *a, int64_t *row_ptr, int32_t *col_idx, double *values)
+{
+  return guard(ctx, [&] {
+    MG_ARG(a != nullptr && row_ptr != nullptr, "mgpu_csr_download: null argument");
+    std::vector<int64_t> rp(static_cast<size_t>(a->nrows + 1));
+    std::vector<int32_t> ci(static_cast<size_t>(a->nnz));
+    std::vector<double> v(static_cast<size_t>(a->nnz));
+    MG_CUDA(cudaMemcpyAsync(rp.data(), a->row_ptr, sizeof(int64_t) * (a->nrows + 1), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    if (a->nnz > 0)
+    {
+      MG_CUDA(cudaMemcpyAsync(ci.data(), a->col_idx, sizeof(int32_t) * a->nnz, cudaMemcpyDeviceToHost, ctx->stream));
+      MG_CUDA(cudaMemcpyAsync(v.data(), a->values, sizeof(double) * a->nnz, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    MG_CUDA(cudaStreamSynchronize(ctx->stream));
+    // Drop stored exact zeros (reference invariant, sparse.hpp:15).
+    int64_t nz = 0;
+    row_ptr[0] = 0;
+    for (int64_t i = 0; i < a->nrows; ++i)
+    {
+      for (int64_t k = rp[i]; k < rp[i + 1]; ++k)
+      {
+        if (v[k] != 0.0)
+        {
+          if (col_idx)
+            col_idx[nz] = ci[k];
+          if (values)
+            values[nz] = v[k];
+          ++nz;
+        }
+      }
+      row_ptr[i + 1] = nz;
+    }
+  });
+}
+
+int mgpu_csr_device_view(const mgpu_csr *a, int64_t *nrows, int64_t *nnz, const int64_t **row_ptr,
+                         const int32_t **col_idx, const double **values)
+{
+  if (a == nullptr)
+    return MGPU_ERR_ARG;
+  if (nrows)
+    *nrows = a->nrows;
+  if (nnz)
+    *nnz = a->nnz;
+  if (row_ptr)
+    *row_ptr = a->row_ptr;
+  if (col_idx)
+    *col_idx = a->col_idx;
+  if (values)
+    *values = a->values;
+  return MGPU_OK;
+}
+
+int mgpu_csr_free(mgpu_csr *a)
+{
+  if (a == nullptr)
+    return MGPU_OK;
+  cudaStream_t s = a->ctx ? a->ctx->stream : nullptr;
+  cudaFreeAsync(a->row_ptr, s);
+  cudaFreeAsync(a->col_idx, s);
+  cudaFreeAsync(a->values, s);
+  delete a;
+  return MGPU_OK;
+}
+
+} // extern "C"

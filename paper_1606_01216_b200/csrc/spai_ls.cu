@@ -1,0 +1,573 @@
+// K-ls: static-pattern least-squares SPAI, one lane group per column (north
+// star subsystem 1).  Not in the reference; its CPU definition is SURVEY.md 8(a')
+// (oracle/oracle.c orc_spai_ls, pinned against reference thin_qr in
+// oracle/ref_shim.cpp ref_spai_ls).
+//
+// Column j:  J = pattern row j (A's CSR pattern, or the symbolic A*A),
+//            I = sorted union of the rows of A(:, J)      (from A^T rows),
+//            S = A(I, J) gathered into shared memory (column-major, lane c = column c),
+//            Householder thin QR of S in FP64 exactly as dense.cpp:153-246
+//            (sign rule, rank flush, explicit Q, sign fix), y = Q^T e|_I,
+//            back-substitution R m = y (acc = y_k - sum_t R_kt m_t, ascending t),
+//            P(J, j) = m.
+// Rank deficiency (sigma <= 1e-12 ||S||_F, dense.cpp:163-179, or |I| < |J|)
+// raises NumericalError for the lowest such column.
+//
+// Output: P on a FIXED pattern (J-pattern transposed), exact zeros kept as
+// storage (dropped on download), so the pattern is reusable across shifts.
+#include <cub/cub.cuh>
+
+#include <climits>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace mgpu
+{
+mgpu_csr *transpose_csr(mgpu_ctx *ctx, const mgpu_csr *A);
+
+namespace
+{
+
+
+// ---------------------------------------------------------------- A*A pattern
+constexpr int kSqCap = 128;
+
+__device__ int square_row(int64_t i, DCsr A, int32_t *buf)
+{
+  int cnt = 0;
+  for (int64_t k = A.rp[i]; k < A.rp[i + 1]; ++k)
+  {
+    const int32_t t = A.ci[k];
+    for (int64_t q = A.rp[t]; q < A.rp[t + 1]; ++q)
+    {
+      const int32_t c = A.ci[q];
+      bool seen = false;
+      for (int u = 0; u < cnt; ++u)
+        seen |= buf[u] == c;
+      if (!seen)
+      {
+        if (cnt == kSqCap)
+          return -1;
+        buf[cnt++] = c;
+      }
+    }
+  }
+  for (int a = 1; a < cnt; ++a) // insertion sort (rows are short)
+  {
+    const int32_t v = buf[a];
+    int b = a - 1;
+    while (b >= 0 && buf[b] > v)
+    {
+      buf[b + 1] = buf[b];
+      --b;
+    }
+    buf[b + 1] = v;
+  }
+  return cnt;
+}
+
+__global__ void square_count(int64_t n, DCsr A, int64_t *rp, int *overflow)
+{
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n)
+    return;
+  int32_t buf[kSqCap];
+  const int c = square_row(i, A, buf);
+  if (c < 0)
+    atomicOr(overflow, 1);
+  rp[i + 1] = c < 0 ? 0 : c;
+  if (i == 0)
+    rp[0] = 0;
+}
+
+__global__ void square_fill(int64_t n, DCsr A, const int64_t *rp, int32_t *ci)
+{
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n)
+    return;
+  int32_t buf[kSqCap];
+  const int c = square_row(i, A, buf);
+  for (int u = 0; u < c; ++u)
+    ci[rp[i] + u] = buf[u];
+}
+
+__global__ void max_row_len(int64_t n, const int64_t *rp, int *out)
+{
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n)
+    atomicMax(out, static_cast<int>(rp[i + 1] - rp[i]));
+}
+
+// ---------------------------------------------------------------- LS columns
+//
+// One GROUP of G lanes per column j (G = 8, 16 or 32 = the |J| envelope, so a
+// warp solves 32/G columns).  Lane c of the group owns column c of S and
+// replays thin_qr (dense.cpp:153-246) with the scalar kernel table's
+// in-order dot / axpy (kernels_scalar.cpp:13-29) for that column: the
+// Householder vector of step k is broadcast through shared memory, every
+// lane c > k applies it to its own column.  Q is formed column by column the
+// same way, the sign fix is applied, y = Q^T e by in-order dots and
+// R m = y is back-substituted by the group leader.  Same operations in the
+// same order as the oracle -> bitwise equal results; the ill-conditioned
+// update problems (cond(S) ~ 5e7 on the Hermite beam) need exactly that.
+template <int G, int NI>
+struct LsGroupSmem
+{
+  double W[G * (NI + 1)]; // S / Householder vectors, column-major, ld = NI + 1 (odd: bank spread)
+  double Q[G * (NI + 1)];
+  double e[NI];
+  double m[G];
+  double diag[G];
+  double tau[G];
+  int32_t I[NI];
+  int ni, nj, fail;
+};
+
+__device__ __forceinline__ double dot_serial(const double *x, const double *y, int len)
+{
+  double acc = 0.0;
+  for (int i = 0; i < len; ++i)
+    acc = __dadd_rn(acc, __dmul_rn(x[i], y[i]));
+  return acc;
+}
+
+__device__ __forceinline__ void axpy_serial(int len, double a, const double *x, double *y)
+{
+  for (int i = 0; i < len; ++i)
+    y[i] = __dadd_rn(y[i], __dmul_rn(a, x[i]));
+}
+
+// Error key: (column << 8) | status, atomicMin picks the lowest column.
+__device__ __forceinline__ void report(unsigned long long *err, int64_t j, int status)
+{
+  atomicMin(err, (static_cast<unsigned long long>(j) << 8) | static_cast<unsigned long long>(status));
+}
+
+template <int G, int NI>
+__global__ void ls_columns(int64_t n, DCsr pat, DCsr At, DCsr Kot, bool update, double *__restrict__ out_vals,
+                           unsigned long long *__restrict__ err, int *__restrict__ overflow)
+{
+  extern __shared__ __align__(16) unsigned char ls_raw[];
+  constexpr int kGroups = 32 / G;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = lane / G, c = lane % G;
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
+  auto &sm = reinterpret_cast<LsGroupSmem<G, NI> *>(ls_raw)[warp * kGroups + grp];
+  const int64_t j = (static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + warp) * kGroups + grp;
+  if (j >= n)
+    return;
+  const int64_t jb = pat.rp[j];
+  const int nj = static_cast<int>(pat.rp[j + 1] - jb);
+  if (nj == 0)
+    return;
+  if (nj > G)
+  {
+    if (c == 0)
+      atomicOr(overflow, 1);
+    return;
+  }
+  // ---- I = sorted union of the rows of A(:, J)   (leader, insertion)
+  if (c == 0)
+  {
+    int ni = 0;
+    bool over = false;
+    for (int q = 0; q < nj && !over; ++q)
+    {
+      const int32_t k = pat.ci[jb + q];
+      for (int64_t t = At.rp[k]; t < At.rp[k + 1]; ++t)
+      {
+        const int32_t row = At.ci[t];
+        int pos = ni;
+        while (pos > 0 && sm.I[pos - 1] > row)
+          --pos;
+        if (pos > 0 && sm.I[pos - 1] == row)
+          continue;
+        if (ni == NI)
+        {
+          over = true;
+          break;
+        }
+        for (int u = ni; u > pos; --u)
+          sm.I[u] = sm.I[u - 1];
+        sm.I[pos] = row;
+        ++ni;
+      }
+    }
+    sm.ni = ni;
+    sm.nj = nj;
+    sm.fail = over ? 2 : (ni < nj ? 1 : 0);
+  }
+  __syncwarp(gmask);
+  if (sm.fail == 2)
+  {
+    if (c == 0)
+      atomicOr(overflow, 1);
+    return;
+  }
+  if (sm.fail == 1)
+  {
+    if (c == 0)
+      report(err, j, MGPU_ERR_NUMERICAL);
+    return;
+  }
+  const int ni = sm.ni;
+  constexpr int LD = NI + 1;
+  // ---- S = A(I, J): lane c fills column c from A^T row J_c; e = rhs|_I
+  if (c < nj)
+  {
+    double *col = sm.W + c * LD;
+    for (int i = 0; i < ni; ++i)
+      col[i] = 0.0;
+    const int32_t k = pat.ci[jb + c];
+    for (int64_t t = At.rp[k]; t < At.rp[k + 1]; ++t)
+    {
+      const int32_t row = At.ci[t];
+      int lo = 0, hi = ni;
+      while (lo < hi)
+      {
+        const int mid = (lo + hi) >> 1;
+        if (sm.I[mid] < row)
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      col[lo] = At.v[t];
+    }
+  }
+  if (c == 0)
+  {
+    for (int i = 0; i < ni; ++i)
+      sm.e[i] = 0.0;
+    if (update)
+    {
+      for (int64_t q = Kot.rp[j]; q < Kot.rp[j + 1]; ++q)
+      {
+        const int32_t row = Kot.ci[q];
+        int lo = 0, hi = ni;
+        while (lo < hi)
+        {
+          const int mid = (lo + hi) >> 1;
+          if (sm.I[mid] < row)
+            lo = mid + 1;
+          else
+            hi = mid;
+        }
+        if (lo < ni && sm.I[lo] == row)
+          sm.e[lo] = Kot.v[q];
+      }
+    }
+    else
+    {
+      for (int i = 0; i < ni; ++i)
+        if (sm.I[i] == j)
+          sm.e[i] = 1.0;
+    }
+  }
+  __syncwarp(gmask);
+  // ---- thin_qr (dense.cpp:153-246)
+  double tol = 0.0;
+  if (c == 0)
+  {
+    double acc = 0.0; // frob_norm: dot over all values, column-major order (dense.cpp:32-36)
+    for (int q = 0; q < nj; ++q)
+      for (int i = 0; i < ni; ++i)
+        acc = __dadd_rn(acc, __dmul_rn(sm.W[q * LD + i], sm.W[q * LD + i]));
+    const double anorm = sqrt(acc);
+    sm.m[0] = 1e-12 * (anorm > 0.0 ? anorm : 1.0);
+  }
+  __syncwarp(gmask);
+  tol = sm.m[0];
+  bool deficient = false;
+  for (int k = 0; k < nj; ++k)
+  {
+    const int len = ni - k;
+    if (c == k)
+    {
+      double *x = sm.W + k * LD + k;
+      const double sigma = sqrt(dot_serial(x, x, len));
+      if (sigma <= tol)
+      {
+        sm.diag[k] = 0.0;
+        sm.tau[k] = 0.0;
+        for (int i = 0; i < len; ++i)
+          x[i] = 0.0;
+      }
+      else
+      {
+        const double alpha = x[0] >= 0.0 ? -sigma : sigma;
+        x[0] = __dsub_rn(x[0], alpha);
+        const double vtv = dot_serial(x, x, len);
+        sm.tau[k] = vtv > 0.0 ? 2.0 / vtv : 0.0;
+        sm.diag[k] = alpha;
+      }
+    }
+    __syncwarp(gmask);
+    if (sm.diag[k] == 0.0)
+      deficient = true;
+    if (c > k && c < nj && sm.tau[k] != 0.0)
+    {
+      const double *v = sm.W + k * LD + k;
+      double *y = sm.W + c * LD + k;
+      const double s = __dmul_rn(sm.tau[k], dot_serial(v, y, len));
+      axpy_serial(len, -s, v, y);
+    }
+    __syncwarp(gmask);
+  }
+  if (deficient) // rank < |J|
+  {
+    if (c == 0)
+      report(err, j, MGPU_ERR_NUMERICAL);
+    return;
+  }
+  // ---- Q = H_0 ... H_{nj-1} E, lane c forms column c
+  if (c < nj)
+  {
+    double *q = sm.Q + c * LD;
+    for (int i = 0; i < ni; ++i)
+      q[i] = 0.0;
+    q[c] = 1.0;
+    for (int k = c < nj - 1 ? c : nj - 1; k >= 0; --k)
+    {
+      if (sm.tau[k] == 0.0)
+        continue;
+      const double *v = sm.W + k * LD + k;
+      const int len = ni - k;
+      const double s = __dmul_rn(sm.tau[k], dot_serial(v, q + k, len));
+      axpy_serial(len, -s, v, q + k);
+    }
+  }
+  __syncwarp(gmask);
+  // ---- sign fix (R diagonal nonnegative) and y = Q^T e
+  // R(k, q) = W[q][k] for q > k, R(k, k) = diag[k]; row k of R is touched only
+  // by column owners q >= k, so every lane flips its own entries.
+  if (c < nj)
+  {
+    for (int k = 0; k <= c; ++k)
+    {
+      if (sm.diag[k] < 0.0)
+      {
+        if (k == c)
+        {
+          for (int i = 0; i < ni; ++i)
+            sm.Q[c * LD + i] = __dmul_rn(sm.Q[c * LD + i], -1.0);
+        }
+        else
+          sm.W[c * LD + k] = -sm.W[c * LD + k];
+      }
+    }
+  }
+  __syncwarp(gmask);
+  if (c < nj)
+  {
+    const double rkk = sm.diag[c] < 0.0 ? -sm.diag[c] : sm.diag[c];
+    sm.tau[c] = rkk; // tau no longer needed: reuse as |R_cc|
+    sm.m[c] = dot_serial(sm.Q + c * LD, sm.e, ni); // y_c
+  }
+  __syncwarp(gmask);
+  // ---- back-substitution R m = y (oracle order: acc = y_k; acc -= R_kq m_q, q ascending)
+  if (c == 0)
+  {
+    double mm[G];
+    for (int k = nj - 1; k >= 0; --k)
+    {
+      double acc = sm.m[k];
+      for (int q = k + 1; q < nj; ++q)
+        acc = __dsub_rn(acc, __dmul_rn(sm.W[q * LD + k], mm[q]));
+      mm[k] = acc / sm.tau[k];
+    }
+    for (int k = 0; k < nj; ++k)
+      sm.m[k] = mm[k];
+  }
+  __syncwarp(gmask);
+  if (c < nj)
+    out_vals[jb + c] = sm.m[c];
+}
+
+template <int G, int NI, int WARPS>
+void launch_ls(mgpu_ctx *ctx, int64_t n, DCsr pat, DCsr At, DCsr Kot, bool update, double *out,
+               unsigned long long *err, int *ovf)
+{
+  constexpr int per_block = WARPS * (32 / G);
+  constexpr size_t smem = sizeof(LsGroupSmem<G, NI>) * per_block;
+  static_assert(smem <= 48 * 1024, "LS group shared memory");
+  const unsigned grid = static_cast<unsigned>((n + per_block - 1) / per_block);
+  ls_columns<G, NI><<<grid, WARPS * 32, smem, ctx->stream>>>(n, pat, At, Kot, update, out, err, ovf);
+  check_launch(ctx, "ls_columns");
+}
+
+void check_err(mgpu_ctx *ctx, unsigned long long *err_dev)
+{
+  unsigned long long h = 0;
+  MG_CUDA(cudaMemcpyAsync(&h, err_dev, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  MG_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (h == ULLONG_MAX)
+    return;
+  const int64_t col = static_cast<int64_t>(h >> 8);
+  const int st = static_cast<int>(h & 0xff);
+  if (st == MGPU_ERR_NUMERICAL)
+    throw Error(st, "spai_ls: rank-deficient least-squares problem in column " + std::to_string(col), col);
+  throw Error(MGPU_ERR_UNSUPPORTED, "spai_ls: column " + std::to_string(col) + " outside the device envelope", col);
+}
+
+} // namespace
+
+// Symbolic pattern of A*A (values = 1.0 placeholders).
+mgpu_csr *pattern_square(mgpu_ctx *ctx, const mgpu_csr *A)
+{
+  const int64_t n = A->nrows;
+  mgpu_csr *S = new mgpu_csr;
+  S->ctx = ctx;
+  S->nrows = n;
+  S->ncols = A->ncols;
+  MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&S->row_ptr), sizeof(int64_t) * (n + 1), ctx->stream));
+  DBuf ovf(sizeof(int), ctx->stream);
+  MG_CUDA(cudaMemsetAsync(ovf.ptr, 0, sizeof(int), ctx->stream));
+  MG_CUDA(cudaMemsetAsync(S->row_ptr, 0, sizeof(int64_t), ctx->stream));
+  if (n > 0)
+  {
+    square_count<<<blocks_for(n), kThreads, 0, ctx->stream>>>(n, A->view(), S->row_ptr, ovf.as<int>());
+    check_launch(ctx, "square_count");
+    size_t tmp = 0;
+    MG_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp, S->row_ptr + 1, S->row_ptr + 1, n, ctx->stream));
+    DBuf t(tmp, ctx->stream);
+    MG_CUDA(cub::DeviceScan::InclusiveSum(t.ptr, tmp, S->row_ptr + 1, S->row_ptr + 1, n, ctx->stream));
+    count_launch(ctx);
+  }
+  int h_ovf = 0;
+  int64_t nnz = 0;
+  MG_CUDA(cudaMemcpyAsync(&h_ovf, ovf.ptr, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  MG_CUDA(cudaMemcpyAsync(&nnz, S->row_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  MG_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (h_ovf)
+  {
+    mgpu_csr_free(S);
+    throw Error(MGPU_ERR_UNSUPPORTED, "spai_ls: A*A pattern row longer than 128 entries");
+  }
+  S->nnz = nnz;
+  MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&S->col_idx), sizeof(int32_t) * (nnz > 0 ? nnz : 1), ctx->stream));
+  MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&S->values), sizeof(double) * (nnz > 0 ? nnz : 1), ctx->stream));
+  if (n > 0)
+  {
+    square_fill<<<blocks_for(n), kThreads, 0, ctx->stream>>>(n, A->view(), S->row_ptr, S->col_idx);
+    check_launch(ctx, "square_fill");
+  }
+  return S;
+}
+
+// P (or Q) for one operator.  `pat` may be A itself (pattern 0).
+mgpu_csr *spai_ls_one(mgpu_ctx *ctx, const mgpu_csr *A, const mgpu_csr *K_old, int pattern)
+{
+  MG_ARG(A->nrows == A->ncols, "spai_ls: operands must be square with equal shape");
+  MG_ARG(!K_old || (K_old->nrows == A->nrows && K_old->ncols == A->ncols),
+         "spai_ls: operands must be square with equal shape");
+  MG_ARG(pattern == MGPU_PATTERN_A || pattern == MGPU_PATTERN_A2, "spai_ls: unknown pattern");
+  const int64_t n = A->nrows;
+  mgpu_csr *sq = pattern == MGPU_PATTERN_A2 ? pattern_square(ctx, A) : nullptr;
+  const mgpu_csr *pat = sq ? sq : A;
+  mgpu_csr *At = transpose_csr(ctx, A);
+  mgpu_csr *Kot = K_old ? transpose_csr(ctx, K_old) : nullptr;
+  // P^T on the J pattern: row j of PT = column j of P
+  mgpu_csr *PT = new_csr(ctx, n, n, pat->nnz);
+  MG_CUDA(cudaMemcpyAsync(PT->row_ptr, pat->row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToDevice, ctx->stream));
+  if (pat->nnz > 0)
+  {
+    MG_CUDA(cudaMemcpyAsync(PT->col_idx, pat->col_idx, sizeof(int32_t) * pat->nnz, cudaMemcpyDeviceToDevice,
+                            ctx->stream));
+    MG_CUDA(cudaMemsetAsync(PT->values, 0, sizeof(double) * pat->nnz, ctx->stream));
+  }
+  DBuf err(sizeof(unsigned long long), ctx->stream), maxlen(sizeof(int), ctx->stream), ovf(sizeof(int), ctx->stream);
+  MG_CUDA(cudaMemsetAsync(maxlen.ptr, 0, sizeof(int), ctx->stream));
+  int h_max = 0;
+  if (n > 0)
+  {
+    max_row_len<<<blocks_for(n), kThreads, 0, ctx->stream>>>(n, pat->row_ptr, maxlen.as<int>());
+    check_launch(ctx, "max_row_len");
+    MG_CUDA(cudaMemcpyAsync(&h_max, maxlen.ptr, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    MG_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  try
+  {
+    bool done = n == 0;
+    const DCsr kv = Kot ? Kot->view() : DCsr{nullptr, nullptr, nullptr};
+    for (int cfg = 0; cfg < 3 && !done; ++cfg)
+    {
+      const int G = cfg == 0 ? 8 : (cfg == 1 ? 16 : 32);
+      if (h_max > G)
+        continue;
+      MG_CUDA(cudaMemsetAsync(err.ptr, 0xff, sizeof(unsigned long long), ctx->stream));
+      MG_CUDA(cudaMemsetAsync(ovf.ptr, 0, sizeof(int), ctx->stream));
+      auto *ev = err.as<unsigned long long>();
+      if (cfg == 0)
+        launch_ls<8, 16, 4>(ctx, n, pat->view(), At->view(), kv, Kot != nullptr, PT->values, ev, ovf.as<int>());
+      else if (cfg == 1)
+        launch_ls<16, 32, 2>(ctx, n, pat->view(), At->view(), kv, Kot != nullptr, PT->values, ev, ovf.as<int>());
+      else
+        launch_ls<32, 64, 1>(ctx, n, pat->view(), At->view(), kv, Kot != nullptr, PT->values, ev, ovf.as<int>());
+      int h_ovf = 0;
+      MG_CUDA(cudaMemcpyAsync(&h_ovf, ovf.ptr, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      MG_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (h_ovf)
+        continue; // a column exceeded this envelope: rerun everything with the next one
+      check_err(ctx, ev);
+      done = true;
+    }
+    if (!done)
+      throw Error(MGPU_ERR_UNSUPPORTED,
+                  "spai_ls: a column exceeds the device envelope (|J| <= 32 pattern entries, |I| <= 64 rows)");
+  }
+  catch (...)
+  {
+    mgpu_csr_free(PT);
+    mgpu_csr_free(At);
+    mgpu_csr_free(Kot);
+    mgpu_csr_free(sq);
+    throw;
+  }
+  mgpu_csr *P = transpose_csr(ctx, PT);
+  P->may_hold_zeros = true;
+  mgpu_csr_free(PT);
+  mgpu_csr_free(At);
+  mgpu_csr_free(Kot);
+  mgpu_csr_free(sq);
+  return P;
+}
+
+} // namespace mgpu
+
+using namespace mgpu;
+
+extern "C" {
+
+int mgpu_spai_ls(mgpu_ctx *ctx, const mgpu_csr *A, const mgpu_csr *K_old, int pattern, mgpu_csr **P)
+{
+  return guard(ctx, [&] {
+    MG_ARG(A && P, "spai_ls: null argument");
+    *P = spai_ls_one(ctx, A, K_old, pattern);
+  });
+}
+
+int mgpu_spai_ls_batched(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, const mgpu_csr *const *K_old, int pattern,
+                         mgpu_csr **P)
+{
+  return guard(ctx, [&] {
+    MG_ARG(l >= 0 && A && P, "spai_ls: null argument");
+    std::vector<mgpu_csr *> made;
+    try
+    {
+      for (int i = 0; i < l; ++i)
+        made.push_back(spai_ls_one(ctx, A[i], K_old ? K_old[i] : nullptr, pattern));
+    }
+    catch (Error &e)
+    {
+      for (auto *m : made)
+        mgpu_csr_free(m);
+      e.point = static_cast<int64_t>(made.size());
+      throw;
+    }
+    for (int i = 0; i < l; ++i)
+      P[i] = made[i];
+  });
+}
+
+} // extern "C"

@@ -1,0 +1,503 @@
+"""ctypes binding of libmgpu.so (include/mgpu.h) -- the C-ABI drop-in boundary.
+
+Mirrors the reference's solver / preconditioner interface (proj/include/mor):
+names, argument meaning and error behaviour follow spai.hpp, krylov.hpp,
+sparse.hpp, system.hpp and airga.hpp.  There is no CPU fallback: if the CUDA
+library is missing or no sm_100 device is present, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libmgpu.so")
+
+MGPU_OK, MGPU_ERR_ARG, MGPU_ERR_STAGNATION, MGPU_ERR_BREAKDOWN = 0, 1, 2, 3
+MGPU_ERR_NUMERICAL, MGPU_ERR_UNSUPPORTED, MGPU_ERR_CUDA, MGPU_ERR_NCCL = 4, 5, 6, 7
+MGPU_HOST, MGPU_DEVICE = 0, 1
+SEQUENTIAL, FROZEN = 0, 1
+PATTERN_A, PATTERN_A2 = 0, 1
+
+# Symbols include/mgpu.h declares; tests check the library exports all of them.
+EXPORTED = [
+    "mgpu_ctx_create", "mgpu_ctx_destroy", "mgpu_ctx_synchronize", "mgpu_last_error", "mgpu_status_string",
+    "mgpu_launch_count", "mgpu_last_cg_timing", "mgpu_csr_upload", "mgpu_csr_upload_device", "mgpu_csr_info",
+    "mgpu_csr_download", "mgpu_csr_device_view", "mgpu_csr_free", "mgpu_sp_add_scaled", "mgpu_shifted_operators",
+    "mgpu_transpose", "mgpu_trace", "mgpu_trace_inner", "mgpu_spmv", "mgpu_chain_apply", "mgpu_spai_build",
+    "mgpu_spai_update", "mgpu_spai_ls", "mgpu_spai_ls_batched", "mgpu_spgemm", "mgpu_cg_solve",
+    "mgpu_model_chain", "mgpu_model_hermite", "mgpu_host_free",
+]
+
+
+# ---------------------------------------------------------------- errors
+class MgpuError(RuntimeError):
+    status = -1
+
+    def __init__(self, msg: str, index: int = -1, rhs_column: int = -1, point: int = -1):
+        super().__init__(msg)
+        self.index, self.rhs_column, self.point = index, rhs_column, point
+
+
+class ArgumentError(MgpuError, ValueError):  # errors.hpp:13-18
+    status = MGPU_ERR_ARG
+
+
+class StagnationError(MgpuError):  # errors.hpp:46-52
+    status = MGPU_ERR_STAGNATION
+
+    @property
+    def column(self):
+        return self.index
+
+
+class BreakdownError(MgpuError):  # errors.hpp:38-44
+    status = MGPU_ERR_BREAKDOWN
+
+    @property
+    def iteration(self):
+        return self.index
+
+
+class NumericalError(MgpuError):  # errors.hpp:54-59
+    status = MGPU_ERR_NUMERICAL
+
+
+class UnsupportedError(MgpuError):
+    status = MGPU_ERR_UNSUPPORTED
+
+
+class CudaError(MgpuError):
+    status = MGPU_ERR_CUDA
+
+
+_BY_STATUS = {c.status: c for c in (ArgumentError, StagnationError, BreakdownError, NumericalError,
+                                     UnsupportedError, CudaError)}
+
+
+# ---------------------------------------------------------------- library
+class _HostCsr(C.Structure):
+    _fields_ = [("nrows", C.c_int64), ("ncols", C.c_int64), ("nnz", C.c_int64),
+                ("row_ptr", C.POINTER(C.c_int64)), ("col_idx", C.POINTER(C.c_int32)),
+                ("values", C.POINTER(C.c_double))]
+
+
+class _CgOut(C.Structure):
+    _fields_ = [("X", C.c_void_p), ("recurrence", C.c_void_p), ("true_res", C.c_void_p),
+                ("iterations", C.POINTER(C.c_int64)), ("converged", C.POINTER(C.c_int)),
+                ("status", C.POINTER(C.c_int)), ("breakdown_iteration", C.POINTER(C.c_int64)),
+                ("history", C.POINTER(C.c_double)), ("history_cap", C.c_int64)]
+
+
+_lib = None
+
+
+def lib():
+    """Loads libmgpu.so; raises (never falls back) when it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(LIB_PATH)
+        vp, i64, dbl = C.c_void_p, C.c_int64, C.c_double
+        L.mgpu_ctx_create.argtypes = [C.c_int, vp, C.POINTER(vp)]
+        L.mgpu_ctx_destroy.argtypes = [vp]
+        L.mgpu_ctx_synchronize.argtypes = [vp]
+        L.mgpu_last_error.argtypes = [vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64), C.c_char_p, C.c_size_t]
+        L.mgpu_status_string.restype = C.c_char_p
+        L.mgpu_launch_count.argtypes = [vp]
+        L.mgpu_launch_count.restype = i64
+        L.mgpu_last_cg_timing.argtypes = [vp, C.POINTER(dbl), C.POINTER(i64)]
+        L.mgpu_csr_upload.argtypes = [vp, i64, i64, i64, vp, vp, vp, C.POINTER(vp)]
+        L.mgpu_csr_upload_device.argtypes = [vp, i64, i64, i64, vp, vp, vp, C.POINTER(vp)]
+        L.mgpu_csr_info.argtypes = [vp, vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]
+        L.mgpu_csr_download.argtypes = [vp, vp, vp, vp, vp]
+        L.mgpu_csr_free.argtypes = [vp]
+        L.mgpu_sp_add_scaled.argtypes = [vp, vp, vp, dbl, dbl, C.POINTER(vp)]
+        L.mgpu_shifted_operators.argtypes = [vp, vp, vp, vp, C.c_int, vp, vp]
+        L.mgpu_transpose.argtypes = [vp, vp, C.POINTER(vp)]
+        L.mgpu_trace.argtypes = [vp, vp, C.POINTER(dbl)]
+        L.mgpu_trace_inner.argtypes = [vp, vp, vp, C.POINTER(dbl)]
+        L.mgpu_spmv.argtypes = [vp, vp, vp, vp]
+        L.mgpu_chain_apply.argtypes = [vp, C.c_int, vp, vp, vp, C.c_int]
+        L.mgpu_spai_build.argtypes = [vp, vp, dbl, i64, C.c_int, C.POINTER(vp), vp]
+        L.mgpu_spai_update.argtypes = [vp, vp, vp, dbl, i64, C.c_int, C.POINTER(vp), vp]
+        L.mgpu_spai_ls.argtypes = [vp, vp, vp, C.c_int, C.POINTER(vp)]
+        L.mgpu_spai_ls_batched.argtypes = [vp, C.c_int, vp, vp, C.c_int, vp]
+        L.mgpu_spgemm.argtypes = [vp, vp, vp, C.POINTER(vp)]
+        L.mgpu_cg_solve.argtypes = [vp, C.c_int, vp, C.c_int, vp, i64, i64, vp, i64, dbl, i64, C.c_int,
+                                    C.POINTER(_CgOut)]
+        L.mgpu_model_chain.argtypes = [i64, dbl, dbl, dbl, dbl, C.c_int] + [C.POINTER(_HostCsr)] * 3
+        L.mgpu_model_hermite.argtypes = [i64] + [dbl] * 7 + [C.POINTER(_HostCsr)] * 3
+        L.mgpu_host_free.argtypes = [C.POINTER(_HostCsr)]
+        _lib = L
+    return _lib
+
+
+def _ptr(a: np.ndarray):
+    return C.c_void_p(a.ctypes.data)
+
+
+# ---------------------------------------------------------------- host CSR
+@dataclass
+class SparseMatrix:
+    """Host CSR with the reference's invariants (sparse.hpp:12-46)."""
+
+    nrows: int
+    ncols: int
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    values: np.ndarray
+
+    @property
+    def nnz(self) -> int:
+        return int(self.values.shape[0])
+
+    def todense(self) -> np.ndarray:
+        out = np.zeros((self.nrows, self.ncols))
+        for i in range(self.nrows):
+            s, e = self.row_ptr[i], self.row_ptr[i + 1]
+            out[i, self.col_idx[s:e]] = self.values[s:e]
+        return out
+
+
+def _from_host_struct(h: _HostCsr) -> SparseMatrix:
+    n, nnz = h.nrows, h.nnz
+    rp = np.ctypeslib.as_array(h.row_ptr, (n + 1,)).copy()
+    ci = np.ctypeslib.as_array(h.col_idx, (max(nnz, 1),))[:nnz].copy()
+    v = np.ctypeslib.as_array(h.values, (max(nnz, 1),))[:nnz].copy()
+    lib().mgpu_host_free(C.byref(h))
+    return SparseMatrix(n, h.ncols, rp, ci, v)
+
+
+def model_hermite(ne: int, E=2.1e11, I=1e-8, rho=7800.0, area=1e-4, L=1.0, alpha=0.1, beta=1e-5):
+    """BASELINE.json Hermite cantilever: returns (M, D, K) host CSR, n = 2 ne."""
+    M, D, K = _HostCsr(), _HostCsr(), _HostCsr()
+    st = lib().mgpu_model_hermite(ne, E, I, rho, area, L, alpha, beta, C.byref(M), C.byref(D), C.byref(K))
+    if st != MGPU_OK:
+        raise ArgumentError("hermite model: bad arguments")
+    return _from_host_struct(M), _from_host_struct(D), _from_host_struct(K)
+
+
+def model_chain(n: int, alpha=0.05, beta=0.05, stiffness_scale=0.01, mass_scale=1.0, consistent=False):
+    """Reference chain model (model_io.cpp:18-87): returns (M, D, K)."""
+    M, D, K = _HostCsr(), _HostCsr(), _HostCsr()
+    st = lib().mgpu_model_chain(n, alpha, beta, stiffness_scale, mass_scale, 1 if consistent else 0, C.byref(M),
+                                C.byref(D), C.byref(K))
+    if st != MGPU_OK:
+        raise ArgumentError("beam_generate: bad arguments")
+    return _from_host_struct(M), _from_host_struct(D), _from_host_struct(K)
+
+
+# ---------------------------------------------------------------- context
+class Context:
+    """One device + stream (mgpu_ctx)."""
+
+    def __init__(self, device: int = 0):
+        self.handle = C.c_void_p()
+        st = lib().mgpu_ctx_create(device, None, C.byref(self.handle))
+        if st != MGPU_OK:
+            raise CudaError(f"mgpu_ctx_create(device={device}) failed: {lib().mgpu_status_string(st).decode()}")
+        self.device = device
+
+    def close(self):
+        if self.handle:
+            lib().mgpu_ctx_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, st: int):
+        if st == MGPU_OK:
+            return
+        idx, col, pt = C.c_int64(), C.c_int64(), C.c_int64()
+        buf = C.create_string_buffer(1024)
+        lib().mgpu_last_error(self.handle, C.byref(idx), C.byref(col), C.byref(pt), buf, 1024)
+        cls = _BY_STATUS.get(st, MgpuError)
+        raise cls(buf.value.decode(errors="replace"), idx.value, col.value, pt.value)
+
+    def synchronize(self):
+        self.check(lib().mgpu_ctx_synchronize(self.handle))
+
+    @property
+    def launches(self) -> int:
+        return int(lib().mgpu_launch_count(self.handle))
+
+    def last_cg_timing(self):
+        ms, it = C.c_double(), C.c_int64()
+        lib().mgpu_last_cg_timing(self.handle, C.byref(ms), C.byref(it))
+        return ms.value, it.value
+
+
+_default: dict = {}
+
+
+def default_context(device: int = 0) -> Context:
+    if device not in _default:
+        _default[device] = Context(device)
+    return _default[device]
+
+
+class DeviceCsr:
+    """Device-resident CSR (mgpu_csr*), freed with the object."""
+
+    def __init__(self, ctx: Context, handle: C.c_void_p, n: int):
+        self.ctx, self.handle, self.nrows = ctx, handle, n
+
+    @staticmethod
+    def upload(A: SparseMatrix, ctx: Optional[Context] = None) -> "DeviceCsr":
+        ctx = ctx or default_context()
+        rp = np.ascontiguousarray(A.row_ptr, np.int64)
+        ci = np.ascontiguousarray(A.col_idx, np.int32)
+        v = np.ascontiguousarray(A.values, np.float64)
+        h = C.c_void_p()
+        ctx.check(lib().mgpu_csr_upload(ctx.handle, A.nrows, A.ncols, v.shape[0], _ptr(rp), _ptr(ci), _ptr(v),
+                                        C.byref(h)))
+        return DeviceCsr(ctx, h, A.nrows)
+
+    def download(self) -> SparseMatrix:
+        n, nc, nnz = C.c_int64(), C.c_int64(), C.c_int64()
+        self.ctx.check(lib().mgpu_csr_info(self.ctx.handle, self.handle, C.byref(n), C.byref(nc), C.byref(nnz)))
+        rp = np.zeros(n.value + 1, np.int64)
+        ci = np.zeros(max(nnz.value, 1), np.int32)
+        v = np.zeros(max(nnz.value, 1))
+        self.ctx.check(lib().mgpu_csr_download(self.ctx.handle, self.handle, _ptr(rp), _ptr(ci), _ptr(v)))
+        return SparseMatrix(n.value, nc.value, rp, ci[:nnz.value], v[:nnz.value])
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib().mgpu_csr_free(self.handle)
+                self.handle = C.c_void_p()
+        except Exception:
+            pass
+
+
+def _dev(A, ctx=None) -> DeviceCsr:
+    return A if isinstance(A, DeviceCsr) else DeviceCsr.upload(A, ctx)
+
+
+def _handles(mats) -> C.Array:
+    arr = (C.c_void_p * max(len(mats), 1))()
+    for i, m in enumerate(mats):
+        arr[i] = m.handle
+    return arr
+
+
+# ---------------------------------------------------------------- core ops
+def sp_add_scaled(A, B, a: float, b: float, ctx=None) -> DeviceCsr:
+    """sparse.cpp:167-218."""
+    ctx = ctx or default_context()
+    dA, dB = _dev(A, ctx), _dev(B, ctx)
+    h = C.c_void_p()
+    ctx.check(lib().mgpu_sp_add_scaled(ctx.handle, dA.handle, dB.handle, a, b, C.byref(h)))
+    return DeviceCsr(ctx, h, dA.nrows)
+
+
+def shifted_operators(M, D, K, shifts: Sequence[float], ctx=None) -> list:
+    """system.cpp:64-68 shifted_operator, batched over shifts (device)."""
+    ctx = ctx or default_context()
+    dM, dD, dK = _dev(M, ctx), _dev(D, ctx), _dev(K, ctx)
+    s = np.ascontiguousarray(shifts, np.float64)
+    out = (C.c_void_p * max(len(s), 1))()
+    ctx.check(lib().mgpu_shifted_operators(ctx.handle, dM.handle, dD.handle, dK.handle, len(s), _ptr(s), out))
+    return [DeviceCsr(ctx, C.c_void_p(out[i]), dM.nrows) for i in range(len(s))]
+
+
+def shifted_operator(M, D, K, s: float, ctx=None) -> DeviceCsr:
+    return shifted_operators(M, D, K, [s], ctx)[0]
+
+
+def transpose(A, ctx=None) -> DeviceCsr:
+    ctx = ctx or default_context()
+    dA = _dev(A, ctx)
+    h = C.c_void_p()
+    ctx.check(lib().mgpu_transpose(ctx.handle, dA.handle, C.byref(h)))
+    return DeviceCsr(ctx, h, dA.nrows)
+
+
+def trace(A, ctx=None) -> float:
+    ctx = ctx or default_context()
+    dA = _dev(A, ctx)
+    out = C.c_double()
+    ctx.check(lib().mgpu_trace(ctx.handle, dA.handle, C.byref(out)))
+    return out.value
+
+
+def trace_inner(A, B, ctx=None) -> float:
+    ctx = ctx or default_context()
+    dA, dB = _dev(A, ctx), _dev(B, ctx)
+    out = C.c_double()
+    ctx.check(lib().mgpu_trace_inner(ctx.handle, dA.handle, dB.handle, C.byref(out)))
+    return out.value
+
+
+def chain_apply(chain: Sequence, v, ctx=None) -> np.ndarray:
+    """spai.cpp:361-373; chain newest first; empty chain = identity."""
+    ctx = ctx or default_context()
+    v = np.ascontiguousarray(v, np.float64)
+    if len(chain) == 0:
+        return v.copy()
+    dev = [_dev(f, ctx) for f in chain]
+    out = np.zeros_like(v)
+    ctx.check(lib().mgpu_chain_apply(ctx.handle, len(dev), _handles(dev), _ptr(v), _ptr(out), MGPU_HOST))
+    return out
+
+
+# ---------------------------------------------------------------- SPAI
+@dataclass
+class SpaiFactor:
+    """spai.hpp:18-29: device factor + per-column residuals + seconds."""
+
+    matrix: DeviceCsr
+    target_frob_residual: Optional[np.ndarray] = None
+    build_seconds: float = 0.0
+    kind: str = "base"
+
+
+def spai_build(K, tol: float = 0.01, max_col_iters: int = 50, mode: int = FROZEN, ctx=None) -> SpaiFactor:
+    """spai.cpp:314-331 (MR-SPAI)."""
+    ctx = ctx or default_context()
+    dK = _dev(K, ctx)
+    res = np.zeros(dK.nrows)
+    h = C.c_void_p()
+    ctx.check(lib().mgpu_spai_build(ctx.handle, dK.handle, tol, max_col_iters, mode, C.byref(h), _ptr(res)))
+    return SpaiFactor(DeviceCsr(ctx, h, dK.nrows), res, 0.0, "base")
+
+
+def spai_update(K_old, K_new, tol: float = 0.01, max_col_iters: int = 50, mode: int = FROZEN,
+                ctx=None) -> SpaiFactor:
+    """spai.cpp:333-350 (MR-SPAI update)."""
+    ctx = ctx or default_context()
+    dO, dN = _dev(K_old, ctx), _dev(K_new, ctx)
+    res = np.zeros(dN.nrows)
+    h = C.c_void_p()
+    ctx.check(lib().mgpu_spai_update(ctx.handle, dO.handle, dN.handle, tol, max_col_iters, mode, C.byref(h),
+                                     _ptr(res)))
+    return SpaiFactor(DeviceCsr(ctx, h, dN.nrows), res, 0.0, "update")
+
+
+def spai_ls(A, K_old=None, pattern: int = PATTERN_A, ctx=None) -> SpaiFactor:
+    """Static-pattern least-squares SPAI (north star subsystem 1)."""
+    ctx = ctx or default_context()
+    dA = _dev(A, ctx)
+    dO = _dev(K_old, ctx) if K_old is not None else None
+    h = C.c_void_p()
+    ctx.check(lib().mgpu_spai_ls(ctx.handle, dA.handle, dO.handle if dO else None, pattern, C.byref(h)))
+    return SpaiFactor(DeviceCsr(ctx, h, dA.nrows), None, 0.0, "base" if K_old is None else "update")
+
+
+def spai_ls_batched(As: Sequence, K_olds: Optional[Sequence] = None, pattern: int = PATTERN_A, ctx=None) -> list:
+    ctx = ctx or default_context()
+    dA = [_dev(a, ctx) for a in As]
+    dO = [_dev(k, ctx) for k in K_olds] if K_olds is not None else None
+    out = (C.c_void_p * max(len(dA), 1))()
+    ctx.check(lib().mgpu_spai_ls_batched(ctx.handle, len(dA), _handles(dA), _handles(dO) if dO else None, pattern,
+                                         out))
+    return [SpaiFactor(DeviceCsr(ctx, C.c_void_p(out[i]), dA[i].nrows)) for i in range(len(dA))]
+
+
+def spgemm(A, B, ctx=None) -> DeviceCsr:
+    ctx = ctx or default_context()
+    dA, dB = _dev(A, ctx), _dev(B, ctx)
+    h = C.c_void_p()
+    ctx.check(lib().mgpu_spgemm(ctx.handle, dA.handle, dB.handle, C.byref(h)))
+    return DeviceCsr(ctx, h, dA.nrows)
+
+
+# ---------------------------------------------------------------- Krylov
+@dataclass
+class BlockSolveResult:
+    """krylov.hpp:44-51 (per point when batched)."""
+
+    X: np.ndarray
+    recurrence_residuals: np.ndarray
+    true_residuals: np.ndarray
+    iterations: np.ndarray
+    all_converged: bool
+    converged: np.ndarray = field(default=None)
+    status: np.ndarray = field(default=None)
+    breakdown_iteration: np.ndarray = field(default=None)
+    relres_history: Optional[np.ndarray] = None
+
+
+def _factor_mat(f):
+    return f.matrix if isinstance(f, SpaiFactor) else f
+
+
+def cg_solve_batched(As: Sequence, chains: Sequence[Sequence], B, rtol: float = 1e-10, maxit: Optional[int] = None,
+                     history_cap: int = 0, raise_on_breakdown: bool = True, ctx=None):
+    """Batched block_solve over points (mgpu_cg_solve). B: (n, m) shared or (l, n, m)."""
+    ctx = ctx or default_context()
+    dA = [_dev(a, ctx) for a in As]
+    l = len(dA)
+    n = dA[0].nrows
+    z = len(chains[0]) if chains else 0
+    assert all(len(c) == z for c in chains), "uniform chain length per batch"
+    flat = [_dev(_factor_mat(f), ctx) for c in chains for f in c]
+    Bn = np.asarray(B, np.float64)
+    if Bn.ndim == 1:
+        Bn = Bn[:, None]
+    if Bn.ndim == 2:
+        m = Bn.shape[1]
+        Bc = np.ascontiguousarray(Bn.T)  # [c][row]
+        ldb = 0
+    else:
+        m = Bn.shape[2]
+        Bc = np.ascontiguousarray(np.transpose(Bn, (0, 2, 1)))  # [p][c][row]
+        ldb = n * m
+    maxit = 10 * n if maxit is None else maxit
+    X = np.zeros((l, m, n))
+    REC = np.zeros((l, m, n))
+    TR = np.zeros((l, m, n))
+    it = np.zeros(l * m, np.int64)
+    cv = np.zeros(l * m, np.int32)
+    st = np.zeros(l * m, np.int32)
+    bd = np.zeros(l * m, np.int64)
+    hist = np.zeros(max(l * m * history_cap, 1))
+    out = _CgOut(X.ctypes.data, REC.ctypes.data, TR.ctypes.data, it.ctypes.data_as(C.POINTER(C.c_int64)),
+                 cv.ctypes.data_as(C.POINTER(C.c_int)), st.ctypes.data_as(C.POINTER(C.c_int)),
+                 bd.ctypes.data_as(C.POINTER(C.c_int64)),
+                 hist.ctypes.data_as(C.POINTER(C.c_double)) if history_cap > 0 else None, history_cap)
+    status = lib().mgpu_cg_solve(ctx.handle, l, _handles(dA), z, _handles(flat), n, m, _ptr(Bc), ldb, rtol, maxit,
+                                 MGPU_HOST, C.byref(out))
+    if status != MGPU_OK and (raise_on_breakdown or status != MGPU_ERR_BREAKDOWN):
+        ctx.check(status)
+    results = []
+    for p in range(l):
+        sl = slice(p * m, (p + 1) * m)
+        h = hist.reshape(l, m, history_cap)[p] if history_cap > 0 else None
+        results.append(BlockSolveResult(X=X[p].T.copy(), recurrence_residuals=REC[p].T.copy(),
+                                        true_residuals=TR[p].T.copy(), iterations=it[sl].copy(),
+                                        all_converged=bool(cv[sl].all()), converged=cv[sl].astype(bool),
+                                        status=st[sl].copy(), breakdown_iteration=bd[sl].copy(), relres_history=h))
+    return results
+
+
+def block_solve(A, chain: Sequence, B, rtol: float = 1e-10, maxit: Optional[int] = None, ctx=None):
+    """krylov.cpp:141-174 with P = chain_apply(chain) (airga.cpp:166-181)."""
+    return cg_solve_batched([A], [list(chain)], B, rtol, maxit, ctx=ctx)[0]
+
+
+def pcg_solve(A, chain: Sequence, b, rtol: float = 1e-10, maxit: Optional[int] = None, history_cap: int = 0,
+              ctx=None) -> dict:
+    """krylov.cpp:28-139 for one rhs; returns the SolveReport fields."""
+    try:
+        r = cg_solve_batched([A], [list(chain)], np.asarray(b, np.float64)[:, None], rtol, maxit,
+                             history_cap=history_cap, ctx=ctx)[0]
+    except BreakdownError as e:  # pcg_solve reports without the block_solve column prefix
+        msg = str(e).split(": ", 1)[1] if str(e).startswith("block_solve") else str(e)
+        raise BreakdownError(msg, e.index, -1, -1) from None
+    hist = None
+    if history_cap > 0:
+        hist = r.relres_history[0][:min(int(r.iterations[0]), history_cap)]
+    return dict(solution=r.X[:, 0], residual=r.true_residuals[:, 0], recurrence_residual=r.recurrence_residuals[:, 0],
+                iterations=int(r.iterations[0]), converged=bool(r.converged[0]), relres_history=hist)

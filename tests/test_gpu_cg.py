@@ -1,0 +1,142 @@
+"""K-cg parity: the persistent device CG against the oracle's pcg_solve / block_solve.
+
+Bars (BASELINE.json north_star): solutions within 1e-8 relative, iteration
+counts within +-2, identical converged flags, identical breakdown iteration.
+T1 = reference chain model (converges); T2 = BASELINE Hermite beam at a fixed
+iteration budget (rtol 1e-10 is unreachable in FP64 there).
+"""
+import numpy as np
+import pytest
+
+from conftest import rel
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(got, want, b=None, tol=1e-8, it_tol=2):
+    assert abs(got["iterations"] - want["iterations"]) <= it_tol, (got["iterations"], want["iterations"])
+    assert got["converged"] == want["converged"]
+    assert rel(got["solution"], want["solution"]) < tol
+    # the true residual b - A x is a cancellation; bound its difference by ||b||
+    scale = np.max(np.abs(b)) if b is not None else np.max(np.abs(want["residual"]))
+    assert np.max(np.abs(got["residual"] - want["residual"])) <= tol * max(scale, 1e-300)
+
+
+@pytest.mark.parametrize("kscale,s", [(0.01, 0.025), (0.01, 1.0), (1.0, 10.0), (1.0, 100.0), (100.0, 100.0)])
+def test_t1_pcg_with_mr_spai(mg, oracle, kscale, s):
+    M, D, K = oracle.chain_generate(2000, consistent=True, stiffness_scale=kscale)
+    A = oracle.shifted_operator(M, D, K, s)
+    P, _ = oracle.spai_build(A, mode=1)
+    b = np.zeros(2000)
+    b[0] = 1.0
+    want = oracle.pcg_solve(A, [P], b, rtol=1e-10)
+    got = mg.pcg_solve(A, [P], b, rtol=1e-10, history_cap=64)
+    _check(got, want, b)
+    assert want["converged"]
+    h = min(want["iterations"], got["iterations"])
+    assert rel(got["relres_history"][:h], want["relres_history"][:h]) < 1e-6
+
+
+def test_t1_plain_cg(mg, oracle):
+    M, D, K = oracle.chain_generate(500, consistent=True, stiffness_scale=1.0)
+    A = oracle.shifted_operator(M, D, K, 3.0)
+    b = np.random.default_rng(3).standard_normal(500)
+    _check(mg.pcg_solve(A, [], b, rtol=1e-10), oracle.pcg_solve(A, [], b, rtol=1e-10), b)
+
+
+def test_t1_chain_of_two(mg, oracle):
+    M, D, K = oracle.chain_generate(2000, consistent=True, stiffness_scale=1.0)
+    A1 = oracle.shifted_operator(M, D, K, 10.0)
+    A2 = oracle.shifted_operator(M, D, K, 12.5)
+    P, _ = oracle.spai_build(A1, mode=1)
+    Q, _ = oracle.spai_update(A1, A2, mode=1)
+    b = np.zeros(2000)
+    b[-1] = 1.0
+    _check(mg.pcg_solve(A2, [Q, P], b), oracle.pcg_solve(A2, [Q, P], b), b)
+
+
+def test_block_solve_zero_column_and_multi_rhs(mg, oracle):
+    M, D, K = oracle.chain_generate(1500, consistent=True, stiffness_scale=1.0)
+    A = oracle.shifted_operator(M, D, K, 5.0)
+    P, _ = oracle.spai_build(A, mode=1)
+    rng = np.random.default_rng(11)
+    B = rng.standard_normal((1500, 4))
+    B[:, 2] = 0.0
+    want = oracle.block_solve(A, [P], B)
+    got = mg.block_solve(A, [P], B)
+    assert rel(got.X, want["X"]) < 1e-8
+    np.testing.assert_array_equal(got.X[:, 2], 0.0)
+    assert got.iterations[2] == 0 and got.converged[2]
+    assert np.all(np.abs(got.iterations - want["iterations"]) <= 2)
+    assert got.all_converged == want["all_converged"]
+
+
+def test_multi_shift_batch(mg, oracle):
+    """8 shifts x 2 rhs in one persistent kernel == 8 separate oracle block solves."""
+    M, D, K = oracle.chain_generate(3000, consistent=True, stiffness_scale=1.0)
+    shifts = [10.0 ** (1 + 3 * i / 7) for i in range(8)]
+    ops = [oracle.shifted_operator(M, D, K, s) for s in shifts]
+    Ps = [oracle.spai_build(A, mode=1)[0] for A in ops]
+    B = np.zeros((3000, 2))
+    B[0, 0] = 1.0
+    B[1500, 1] = 1.0
+    res = mg.cg_solve_batched(ops, [[P] for P in Ps], B, rtol=1e-10)
+    for A, P, r in zip(ops, Ps, res):
+        want = oracle.block_solve(A, [P], B)
+        assert rel(r.X, want["X"]) < 1e-8
+        assert np.all(np.abs(r.iterations - want["iterations"]) <= 2)
+
+
+def test_t2_hermite_fixed_k_iterates(mg, oracle):
+    """BASELINE config 1 shape: n=2000, s=100, LS-SPAI (A pattern), fixed budget."""
+    M, D, K = oracle.hermite_generate(1000)
+    A = oracle.shifted_operator(M, D, K, 100.0)
+    P = oracle.spai_ls(A, None, 0)
+    b = np.zeros(2000)
+    b[1998] = 1.0
+    for k in (1, 10, 100):
+        want = oracle.pcg_solve(A, [P], b, rtol=1e-10, maxit=k)
+        got = mg.pcg_solve(A, [P], b, rtol=1e-10, maxit=k)
+        assert got["iterations"] == want["iterations"] == k
+        assert got["converged"] == want["converged"]
+        assert rel(got["solution"], want["solution"]) < 1e-8
+
+
+def test_breakdown_iteration_parity(mg, oracle):
+    from oracle import Csr, OracleError
+    A = Csr.from_dense(np.diag([1.0, -1.0, 2.0]))
+    b = np.array([1.0, 1.0, 0.0])
+    with pytest.raises(OracleError) as eo:
+        oracle.pcg_solve(A, [], b)
+    with pytest.raises(mg.BreakdownError) as eg:
+        mg.pcg_solve(A, [], b)
+    assert eg.value.iteration == eo.value.index == 0
+    with pytest.raises(mg.BreakdownError) as eb:
+        mg.block_solve(A, [], np.stack([np.array([1.0, 0.0, 0.0]), b], axis=1))
+    assert "block_solve: column 1" in str(eb.value) and eb.value.iteration == 0
+
+
+def test_maxit_zero_and_budget(mg, oracle):
+    M, D, K = oracle.chain_generate(800, consistent=True, stiffness_scale=1.0)
+    A = oracle.shifted_operator(M, D, K, 1.0)
+    b = np.ones(800)
+    for k in (0, 1, 2):
+        _check(mg.pcg_solve(A, [], b, maxit=k), oracle.pcg_solve(A, [], b, maxit=k), b, it_tol=0)
+
+
+def test_tight_rtol_restart_branch(mg, oracle):
+    """rtol near the FP64 floor exercises the confirm / restart branch (krylov.cpp:77-103)."""
+    M, D, K = oracle.chain_generate(1000, consistent=True, stiffness_scale=1.0)
+    A = oracle.shifted_operator(M, D, K, 0.5)
+    b = np.random.default_rng(5).standard_normal(1000)
+    want = oracle.pcg_solve(A, [], b, rtol=1e-15, maxit=400)
+    got = mg.pcg_solve(A, [], b, rtol=1e-15, maxit=400)
+    assert got["converged"] == want["converged"]
+    assert rel(got["solution"], want["solution"]) < 1e-8
+
+
+def test_zero_rhs(mg, oracle):
+    M, D, K = oracle.chain_generate(100)
+    got = mg.pcg_solve(K, [], np.zeros(100))
+    assert got["iterations"] == 0 and got["converged"]
+    np.testing.assert_array_equal(got["solution"], 0.0)

@@ -1,0 +1,85 @@
+"""Parity of the device sparse core with the oracle (bitwise where the arithmetic allows).
+
+K-asm (system.cpp:64-68 / sparse.cpp:167-218): bitwise -- no FMA, same merge.
+transpose (sparse.cpp:220-249): bitwise.  SpMV / chain_apply: bitwise with the
+scalar kernel table (kernels_scalar.cpp:39-47).  trace / trace_inner: the
+device reduction is a fixed tree, not the reference's serial sum -> 1e-14.
+"""
+import numpy as np
+import pytest
+
+from conftest import rel
+
+pytestmark = pytest.mark.gpu
+
+SHIFTS = [10.0 ** (1 + 3 * i / 7) for i in range(8)]
+
+
+def _eq_csr(a, b):
+    assert a.nrows == b.nrows
+    np.testing.assert_array_equal(a.row_ptr, b.row_ptr)
+    np.testing.assert_array_equal(a.col_idx, b.col_idx)
+    np.testing.assert_array_equal(a.values, b.values)
+
+
+@pytest.mark.parametrize("model", ["hermite", "chain"])
+def test_shifted_operators_bitwise(mg, oracle, model):
+    if model == "hermite":
+        M, D, K = oracle.hermite_generate(500)
+    else:
+        M, D, K = oracle.chain_generate(1000, consistent=True, stiffness_scale=1.0)
+    ops = mg.shifted_operators(M, D, K, SHIFTS)
+    for s, dA in zip(SHIFTS, ops):
+        _eq_csr(dA.download(), oracle.shifted_operator(M, D, K, s))
+
+
+def test_product_models_match_oracle(mg, oracle):
+    for (pm, om) in [(mg.model_hermite(300), oracle.hermite_generate(300)),
+                     (mg.model_chain(400, consistent=True), oracle.chain_generate(400, consistent=True))]:
+        for a, b in zip(pm, om):
+            _eq_csr(a, b)
+
+
+def test_sp_add_scaled_exact_cancellation(mg, oracle):
+    from oracle import Csr
+    A = Csr.from_dense(np.array([[1.0, 2.0, 0.0], [0.0, 3.0, 4.0], [5.0, 0.0, 6.0]]))
+    B = Csr.from_dense(np.array([[1.0, -1.0, 7.0], [0.0, 1.5, 0.0], [0.0, 0.0, -3.0]]))
+    got = mg.sp_add_scaled(A, B, 1.0, 2.0).download()
+    want = oracle.sp_add_scaled(A, B, 1.0, 2.0)  # (0,1): 2 - 2 = 0 dropped; (2,2): 6 - 6 = 0 dropped
+    _eq_csr(got, want)
+    assert want.nnz == 5
+
+
+def test_transpose_bitwise(mg, oracle):
+    rng = np.random.default_rng(7)
+    a = rng.standard_normal((60, 45)) * (rng.random((60, 45)) < 0.1)
+    from oracle import Csr
+    A = Csr.from_dense(a)
+    _eq_csr(mg.transpose(A).download(), oracle.transpose(A))
+
+
+def test_traces(mg, oracle):
+    M, D, K = oracle.hermite_generate(2000)
+    A = oracle.shifted_operator(M, D, K, 100.0)
+    B = oracle.shifted_operator(M, D, K, 105.0)
+    assert rel(mg.trace(A), oracle.trace(A)) < 1e-12  # tree vs serial sum order
+    assert rel(mg.trace_inner(A, B), oracle.trace_inner(A, B)) < 1e-12
+    assert mg.trace_inner(A, B) == mg.trace_inner(B, A)  # spai_update's Q = I relies on this
+
+
+def test_chain_apply_bitwise(mg, oracle):
+    M, D, K = oracle.chain_generate(3000, consistent=True)
+    A1 = oracle.shifted_operator(M, D, K, 2.0)
+    A2 = oracle.shifted_operator(M, D, K, 3.0)
+    v = np.random.default_rng(1).standard_normal(3000)
+    np.testing.assert_array_equal(mg.chain_apply([A2, A1], v), oracle.chain_apply([A2, A1], v))
+    np.testing.assert_array_equal(mg.chain_apply([], v), v)
+
+
+def test_argument_errors(mg, oracle):
+    M, D, K = oracle.chain_generate(50)
+    M2, _, _ = oracle.chain_generate(60)
+    with pytest.raises(mg.ArgumentError):
+        mg.shifted_operators(M2, D, K, [1.0])
+    with pytest.raises(mg.ArgumentError):
+        mg.pcg_solve(K, [], np.ones(50), rtol=0.0)

@@ -1,0 +1,164 @@
+"""SPAI parity: device MR-SPAI (reference Alg. 2/4, frozen) and LS-SPAI against the oracle.
+
+Bar: SPAI entries within 1e-10 relative (BASELINE.json north_star), identical
+sparsity pattern, per-column residuals within 1e-10, identical exception class
+and column index.  SPEC.md known-answer tests included.
+"""
+import numpy as np
+import pytest
+
+from conftest import rel
+
+pytestmark = pytest.mark.gpu
+
+
+def _csr_close(got, want, tol=1e-10):
+    np.testing.assert_array_equal(got.row_ptr, want.row_ptr)
+    np.testing.assert_array_equal(got.col_idx, want.col_idx)
+    assert rel(got.values, want.values) <= tol
+
+
+# ------------------------------------------------------------------ MR-SPAI
+@pytest.mark.parametrize("kscale,s", [(0.01, 1.0), (1.0, 1.0), (1.0, 10.0), (1.0, 100.0), (100.0, 10.0)])
+def test_mr_build_t1(mg, oracle, kscale, s):
+    M, D, K = oracle.chain_generate(2000, consistent=True, stiffness_scale=kscale)
+    A = oracle.shifted_operator(M, D, K, s)
+    want, wres = oracle.spai_build(A, mode=1)
+    f = mg.spai_build(A, mode=mg.FROZEN)
+    _csr_close(f.matrix.download(), want)
+    assert rel(f.target_frob_residual, wres) < 1e-10
+
+
+def test_mr_build_identity_mass(mg, oracle):
+    M, D, K = oracle.chain_generate(1000, consistent=False)
+    A = oracle.shifted_operator(M, D, K, 10.0)
+    want, _ = oracle.spai_build(A, mode=1)
+    _csr_close(mg.spai_build(A).matrix.download(), want)
+
+
+def test_mr_update_t1(mg, oracle):
+    M, D, K = oracle.chain_generate(2000, consistent=True, stiffness_scale=1.0)
+    A1 = oracle.shifted_operator(M, D, K, 10.0)
+    A2 = oracle.shifted_operator(M, D, K, 10.5)
+    want, wres = oracle.spai_update(A1, A2, mode=1)
+    f = mg.spai_update(A1, A2, mode=mg.FROZEN)
+    _csr_close(f.matrix.download(), want)
+    assert rel(f.target_frob_residual, wres) < 1e-10
+
+
+def test_mr_update_identical_is_identity_bitwise(mg, oracle):
+    """SPEC.md:256 / spai.hpp:57-60: K_new == K_old -> Q = I exactly, zero iterations."""
+    M, D, K = oracle.chain_generate(500, consistent=True, stiffness_scale=1.0)
+    A = oracle.shifted_operator(M, D, K, 10.0)
+    Q = mg.spai_update(A, A).matrix.download()
+    np.testing.assert_array_equal(Q.row_ptr, np.arange(501))
+    np.testing.assert_array_equal(Q.col_idx, np.arange(500))
+    np.testing.assert_array_equal(Q.values, 1.0)
+
+
+def test_mr_update_scaled_identity(mg, oracle):
+    from oracle import Csr
+    I = Csr.from_dense(np.eye(6))
+    Q = mg.spai_update(I, Csr.from_dense(2 * np.eye(6))).matrix.download()
+    np.testing.assert_array_equal(Q.todense(), 0.5 * np.eye(6))
+
+
+def test_mr_build_kats(mg, oracle):
+    from oracle import Csr
+    P = mg.spai_build(Csr.from_dense(np.eye(5))).matrix.download()  # K = I -> alpha = 1, P = I
+    np.testing.assert_array_equal(P.todense(), np.eye(5))
+    P = mg.spai_build(Csr.from_dense(np.diag([2.0, 4.0])), tol=1e-12).matrix.download()
+    assert rel(P.todense(), np.diag([0.5, 0.25])) < 1e-12
+    # random SPD 20x20: ||I - K P||_F <= tol sqrt(n)
+    rng = np.random.default_rng(0)
+    G = rng.standard_normal((20, 20))
+    Kd = G @ G.T / 20 + np.eye(20)
+    f = mg.spai_build(Csr.from_dense(Kd), tol=0.01, max_col_iters=500)
+    Pd = f.matrix.download().todense()
+    assert np.linalg.norm(np.eye(20) - Kd @ Pd) <= 0.01 * np.sqrt(20) + 1e-12
+    want, _ = oracle.spai_build(Csr.from_dense(Kd), tol=0.01, max_col_iters=500, mode=1)
+    assert rel(Pd, want.todense()) < 1e-10
+
+
+def test_mr_stagnation_column_and_message(mg, oracle):
+    """The BASELINE Hermite beam makes MR-SPAI stall at column 0."""
+    from oracle import OracleError
+    M, D, K = oracle.hermite_generate(1000)
+    A = oracle.shifted_operator(M, D, K, 100.0)
+    with pytest.raises(OracleError) as eo:
+        oracle.spai_build(A, mode=1)
+    with pytest.raises(mg.StagnationError) as eg:
+        mg.spai_build(A, mode=mg.FROZEN)
+    assert eg.value.column == eo.value.index == 0
+    assert str(eg.value).split(" stalled")[0] == eo.value.msg.split(" stalled")[0]
+
+
+def test_mr_sequential_rejected_loudly(mg, oracle):
+    M, D, K = oracle.chain_generate(100)
+    with pytest.raises(mg.UnsupportedError):
+        mg.spai_build(K, mode=mg.SEQUENTIAL)
+
+
+# ------------------------------------------------------------------ LS-SPAI
+@pytest.mark.parametrize("pattern", [0, 1])
+@pytest.mark.parametrize("s", [10.0, 100.0, 1e4])
+def test_ls_build_hermite(mg, oracle, pattern, s):
+    M, D, K = oracle.hermite_generate(1000)
+    A = oracle.shifted_operator(M, D, K, s)
+    want = oracle.spai_ls(A, None, pattern)
+    got = mg.spai_ls(A, None, pattern).matrix.download()
+    _csr_close(got, want)
+
+
+@pytest.mark.parametrize("pattern", [0, 1])
+def test_ls_update_hermite(mg, oracle, pattern):
+    M, D, K = oracle.hermite_generate(1000)
+    A1 = oracle.shifted_operator(M, D, K, 100.0)
+    A2 = oracle.shifted_operator(M, D, K, 150.0)
+    want = oracle.spai_ls(A2, A1, pattern)
+    got = mg.spai_ls(A2, A1, pattern).matrix.download()
+    _csr_close(got, want)
+
+
+def test_ls_chain_model_and_dense(mg, oracle):
+    from oracle import Csr
+    M, D, K = oracle.chain_generate(3000, consistent=True, stiffness_scale=1.0)
+    A = oracle.shifted_operator(M, D, K, 3.0)
+    _csr_close(mg.spai_ls(A, None, 1).matrix.download(), oracle.spai_ls(A, None, 1))
+    rng = np.random.default_rng(1)
+    G = rng.standard_normal((20, 20))
+    Kd = Csr.from_dense(G @ G.T + 20 * np.eye(20))
+    _csr_close(mg.spai_ls(Kd).matrix.download(), oracle.spai_ls(Kd, None, 0))
+
+
+def test_ls_rank_deficiency(mg, oracle):
+    from oracle import Csr, OracleError
+    A = Csr.from_dense(np.array([[1.0, 2.0, 0.0], [1.0, 2.0, 0.0], [0.0, 0.0, 3.0]]))
+    with pytest.raises(OracleError) as eo:
+        oracle.spai_ls(A, None, 0)
+    with pytest.raises(mg.NumericalError) as eg:
+        mg.spai_ls(A)
+    assert eg.value.index == eo.value.index == 0
+
+
+def test_ls_batched_equals_single(mg, oracle):
+    M, D, K = oracle.hermite_generate(500)
+    shifts = [10.0 ** (1 + 3 * i / 7) for i in range(8)]
+    ops = mg.shifted_operators(M, D, K, shifts)
+    facs = mg.spai_ls_batched(ops)
+    for s, f in zip(shifts, facs):
+        _csr_close(f.matrix.download(), oracle.spai_ls(oracle.shifted_operator(M, D, K, s), None, 0))
+
+
+# ------------------------------------------------------------------ SpGEMM chain collapse
+def test_spgemm_collapse(mg, oracle):
+    M, D, K = oracle.hermite_generate(400)
+    A1 = oracle.shifted_operator(M, D, K, 100.0)
+    A2 = oracle.shifted_operator(M, D, K, 150.0)
+    P = oracle.spai_ls(A1, None, 0)
+    Q = oracle.spai_ls(A2, A1, 0)
+    QP = mg.spgemm(Q, P).download()
+    dense = Q.todense() @ P.todense()
+    assert rel(QP.todense(), dense) < 1e-14
+    v = np.random.default_rng(2).standard_normal(800)
+    assert rel(mg.chain_apply([QP], v), oracle.chain_apply([Q, P], v)) < 1e-12
