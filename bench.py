@@ -1,0 +1,399 @@
+#!/usr/bin/env python
+"""Benchmark of the SPAI + shifted-system PCG path (BASELINE.json metric, configs[1]).
+
+Workload ("config1", the default; BASELINE.json configs[1]):
+  clamped Euler-Bernoulli Hermite beam, ne = 10,000 elements (n = 20,000),
+  8 real shifts log-spaced in [10, 1e4] per GPU, m = 1 rhs (unit tip load, dof n-2).
+  One STEP = the whole hot path for that batch:
+    assemble the 8 shifted operators A(s) = s^2 M + s D + K   (device, one call)
+    build 8 LS-SPAI factors on A's pattern                    (device, batched)
+    8 right-preconditioned CG solves, rtol 1e-10              (one persistent kernel)
+  rtol 1e-10 is unreachable in FP64 on this beam (cond ~1e13), so
+  the CG runs its fixed budget (--budget, default 1000 iterations) in both arms.
+
+Arms:
+  default           this library (libmgpu.so, sm_100a).  `value` is measured with
+                    M, D, K and the rhs resident in HBM; `e2e` runs the same step
+                    through the public API from pinned host buffers, H2D of the
+                    system + rhs and D2H of X / residual blocks inside the timed region.
+  --impl reference  the reference's own CPU path (oracle/_ref: the unmodified
+                    reference library; LS-SPAI from reference thin_qr), shifts run
+                    concurrently on all host cores, rank 0 only.
+Multi-GPU (torchrun): each rank solves its own 8 shifts (weak scaling, no
+collective on the data path); time = max over ranks of CUDA-event time.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "shifted-system PCG solves/s + SPAI build time (FP64), % of HBM roofline"
+UNIT = "solves/s"
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="mgpu", choices=["mgpu", "reference"])
+    ap.add_argument("--budget", type=int, default=1000, help="CG iterations per solve (fixed budget)")
+    ap.add_argument("--workload", default="config1", choices=["config0", "config1", "config3"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def workload(name: str, world: int, rank: int):
+    """(ne, m, shifts for this rank, all shifts, pattern, description)."""
+    if name == "config0":
+        ne, m, per, pattern = 1000, 1, 1, 0
+        all_shifts = [100.0] * world
+    elif name == "config1":
+        ne, m, per, pattern = 10000, 1, 8, 0
+        tot = per * world
+        all_shifts = [10.0 ** (1 + 3 * i / (tot - 1)) for i in range(tot)]
+    else:
+        ne, m, per, pattern = 500000, 4, 16, 1
+        tot = per * world
+        all_shifts = [10.0 ** (1 + 3 * i / (tot - 1)) for i in range(tot)]
+    return ne, m, all_shifts[rank::world], all_shifts, pattern
+
+
+def rhs_block(n: int, m: int) -> np.ndarray:
+    """Unit loads on tip-deflection dofs: m=1 -> dof n-2; m=4 -> w at 25/50/75/100 % of L."""
+    B = np.zeros((n, m))
+    if m == 1:
+        B[n - 2, 0] = 1.0
+    else:
+        ne = n // 2
+        for c in range(m):
+            node = (c + 1) * ne // m
+            B[2 * node - 2, c] = 1.0
+    return B
+
+
+def peak_hbm():
+    try:
+        with open(PEAKS) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.t0 = self.t1 = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.index), "-lms", "100"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def mark(self, which):
+        setattr(self, which, time.time())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        rows = []
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 10:
+                continue
+            try:
+                ts = time.mktime(time.strptime(f[0].split(".")[0], "%Y/%m/%d %H:%M:%S"))
+                rows.append((ts, float(f[2]), float(f[3]), f[6:10]))
+            except Exception:
+                continue
+        if not rows:
+            return None
+        inside = [r for r in rows if self.t0 - 1 <= r[0] <= self.t1 + 1] or rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in inside for i, v in enumerate(r[3]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[1] for r in inside), "sm_max_mhz": max(r[2] for r in inside),
+                "reasons": reasons, "samples": len(inside)}
+
+
+# ------------------------------------------------------------------ CPU (reference) path
+def cpu_step_fn(kind: str, M, D, K, shifts, B, pattern, budget):
+    """One step of the reference CPU path; shifts run concurrently (ctypes releases the GIL)."""
+    from oracle import Oracle, Reference, reference_available
+    lib = Reference() if (kind == "reference" and reference_available()) else Oracle()
+    threads = min(len(shifts), os.cpu_count() or 1)
+
+    def one(s):
+        A = lib.shifted_operator(M, D, K, s)
+        P = lib.spai_ls(A, None, pattern)
+        for c in range(B.shape[1]):
+            lib.pcg_solve(A, [P], B[:, c], rtol=1e-10, maxit=budget, history_cap=1)
+
+    def step():
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(one, shifts))
+
+    return step, threads, lib.kind
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    from oracle import Oracle, reference_available
+    ne, m, _, all_shifts, pattern = workload(args.workload, world, 0)
+    M, D, K = Oracle().hermite_generate(ne)
+    B = rhs_block(M.nrows, m)
+    kind = "reference" if reference_available() else "port"
+    step, threads, kind = cpu_step_fn(kind, M, D, K, all_shifts, B, pattern, args.budget)
+    for _ in range(args.warmup):
+        step()
+    times = []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t)
+    total = sum(times)
+    solves = len(all_shifts) * m * args.steps
+    value = solves / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (deterministic Hermite beam, BASELINE configs)",
+        "config": config_dict(args, ne, m, all_shifts, pattern, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"full steps: {len(all_shifts)} shifts x {m} rhs, {args.budget} CG iterations each"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_dict(args, ne, m, shifts, pattern, world):
+    return {"workload": f"BASELINE.json configs[{ {'config0': 0, 'config1': 1, 'config3': 3}[args.workload] }]: "
+                        f"Hermite cantilever ne={ne} (n={2 * ne}), {len(shifts)} shifts log-spaced in [10,1e4], "
+                        f"m={m}, LS-SPAI on the {'A' if pattern == 0 else 'A^2'} pattern, right-preconditioned CG, "
+                        f"rtol 1e-10, fixed budget {args.budget} iterations",
+            "n": 2 * ne, "shifts_total": len(shifts), "rhs": m, "cg_budget": args.budget,
+            "spai": "ls-" + ("A" if pattern == 0 else "A2"), "parallelism": f"shift-sharded x{world}",
+            "l2": "flushed between timed steps (256 MiB write)"}
+
+
+# ------------------------------------------------------------------ GPU path
+def run_mgpu(args, rank, world, local_rank):
+    import torch
+    import paper_1606_01216_b200 as mg
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    else:
+        torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.Stream(device=dev)
+    ctx = mg.Context(local_rank, stream=stream.cuda_stream)
+
+    ne, m, shifts, all_shifts, pattern = workload(args.workload, world, rank)
+    M, D, K = mg.model_hermite(ne)
+    n = M.nrows
+    l = len(shifts)
+    B = rhs_block(n, m)
+    budget = args.budget
+
+    # device-resident inputs (value)
+    dM, dD, dK = (mg.DeviceCsr.upload(x, ctx) for x in (M, D, K))
+    B_dev = torch.tensor(B.T.copy(), dtype=torch.float64, device=dev).contiguous()  # (m, n) shared
+    X_dev = torch.empty((l, m, n), dtype=torch.float64, device=dev)
+    R_dev = torch.empty_like(X_dev)
+    T_dev = torch.empty_like(X_dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    # pinned host inputs / outputs (e2e)
+    def pinned(a, dtype):
+        t = torch.empty(a.shape, dtype=dtype, pin_memory=True)
+        t.numpy()[...] = a
+        return t
+
+    host_sys = []
+    for x in (M, D, K):
+        host_sys.append(mg.SparseMatrix(x.nrows, x.ncols, pinned(x.row_ptr, torch.int64).numpy(),
+                                        pinned(x.col_idx, torch.int32).numpy(), pinned(x.values, torch.float64).numpy()))
+    B_host = pinned(np.ascontiguousarray(B.T), torch.float64)
+    X_host, R_host, T_host = (torch.empty((l, m, n), dtype=torch.float64, pin_memory=True) for _ in range(3))
+    csr_bytes = sum(8 * (x.nrows + 1) + 12 * x.nnz for x in (M, D, K))
+    h2d_bytes = csr_bytes + 8 * n * m
+    d2h_bytes = 3 * 8 * n * m * l + l * m * (8 + 4 + 4 + 8)
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+    info = {}
+
+    def step_device(record):
+        e0, e1, e2, e3 = ev(), ev(), ev(), ev()
+        e0.record(stream)
+        ops = mg.shifted_operators(dM, dD, dK, shifts, ctx=ctx)
+        e1.record(stream)
+        facs = mg.spai_ls_batched(ops, None, pattern, ctx=ctx)
+        e2.record(stream)
+        it, cv, st, bd = mg.cg_solve_device(ops, [[f.matrix] for f in facs], B_dev, X_dev, R_dev, T_dev, rtol=1e-10,
+                                            maxit=budget, ctx=ctx)
+        e3.record(stream)
+        if record is not None:
+            cg_ms, loops = ctx.last_cg_timing()
+            bytes_iter = sum(8 * o.stored_nnz + 8 * f.matrix.stored_nnz + 48 * n * m for o, f in zip(ops, facs))
+            record.append(dict(ev=(e0, e1, e2, e3), cg_ms=cg_ms, loops=loops, bytes=bytes_iter * loops,
+                               iters=int(it.max()), breakdowns=int((st != 0).sum())))
+
+    def step_e2e(record):
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        hM, hD, hK = (mg.DeviceCsr.upload(x, ctx) for x in host_sys)
+        ops = mg.shifted_operators(hM, hD, hK, shifts, ctx=ctx)
+        facs = mg.spai_ls_batched(ops, None, pattern, ctx=ctx)
+        flat = [f.matrix for f in facs]
+        status, it, cv, st, bd, _ = mg.cg_solve_raw(ctx, ops, flat, 1, n, m, B_host.data_ptr(), 0, 1e-10, budget,
+                                                    mg.mgpu.MGPU_HOST, X_host.data_ptr(), R_host.data_ptr(),
+                                                    T_host.data_ptr())
+        e1.record(stream)
+        if record is not None:
+            record.append((e0, e1))
+
+    def timed(fn):
+        for _ in range(args.warmup):
+            fn(None)
+        stream.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        recs = []
+        launches0 = ctx.launches
+        sampler.mark("t0")
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()  # L2 flush between timed steps (outside the event pair)
+            fn(recs)
+        stream.synchronize()
+        sampler.mark("t1")
+        launches = ctx.launches - launches0
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        return recs, launches
+
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    recs, launches = timed(step_device)
+    clocks = sampler.stop()
+    step_ms = [r["ev"][0].elapsed_time(r["ev"][3]) for r in recs]
+    asm_ms = [r["ev"][0].elapsed_time(r["ev"][1]) for r in recs]
+    spai_ms = [r["ev"][1].elapsed_time(r["ev"][2]) for r in recs]
+    cg_ms = [r["cg_ms"] for r in recs]
+    total_ms = float(sum(step_ms))
+    e2e_recs, _ = timed(step_e2e)
+    e2e_ms = float(sum(a.elapsed_time(b) for a, b in e2e_recs))
+
+    if dist:
+        t = torch.tensor([total_ms, e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, e2e_ms = float(t[0]), float(t[1])
+
+    solves = len(all_shifts) * m * args.steps
+    value = solves / (total_ms / 1e3)
+    e2e_value = solves / (e2e_ms / 1e3)
+    peak, peak_kind = peak_hbm()
+    achieved = sum(r["bytes"] for r in recs) / (sum(cg_ms) / 1e3) / 1e9
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "cg_dram_traffic.json")
+    if os.path.exists(tfile):
+        try:
+            with open(tfile) as f:
+                traffic = json.load(f).get(args.workload)
+        except Exception:
+            traffic = None
+    loops = recs[-1]["loops"]
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle import Oracle, reference_available
+            orc = Oracle()
+            hM, hD, hK = orc.hermite_generate(ne)
+            kind = "reference" if reference_available() else "port"
+            sample_shifts = shifts if args.workload != "config3" else shifts[:1]
+            sample_budget = budget if args.workload != "config3" else 5
+            step, threads, kind = cpu_step_fn(kind, hM, hD, hK, sample_shifts, B, pattern, sample_budget)
+            t = time.perf_counter()
+            step()
+            dt = time.perf_counter() - t
+            cpu = {"value": len(sample_shifts) * m / dt * (sample_budget / budget), "unit": UNIT, "cores": threads,
+                   "kind": kind,
+                   "sample": f"one step: {len(sample_shifts)} shifts x {m} rhs, assemble + LS-SPAI + "
+                             f"{sample_budget} CG iterations (value scaled to the {budget}-iteration budget)",
+                   "seconds": dt}
+        except Exception as e:  # reported, never silently replaced
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable", "sample": repr(e)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (deterministic Hermite beam, BASELINE configs)",
+            "config": config_dict(args, ne, m, all_shifts, pattern, world),
+            "step_ms_min_med_max": [min(step_ms), statistics.median(step_ms), max(step_ms)],
+            "spai_build_ms": statistics.median(spai_ms), "assemble_ms": statistics.median(asm_ms),
+            "cg_ms": statistics.median(cg_ms), "cg_us_per_iteration": 1e3 * statistics.median(cg_ms) / max(loops, 1),
+            "cg_iterations": loops, "breakdowns": recs[-1]["breakdowns"],
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "peak_source": peak_kind, "kernel": "cg_persistent",
+                         "bytes_model": "per iteration, per shift: 8 nnz(A) + 8 nnz(P) + 48 n m"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d_bytes,
+                    "d2h_bytes_per_step": d2h_bytes},
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world == 1 and args.gpus > 1:
+        print(json.dumps({"error": "use torchrun for --gpus > 1"}), file=sys.stderr)
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_mgpu(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

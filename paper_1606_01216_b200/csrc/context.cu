@@ -173,6 +173,13 @@ int mgpu_ctx_create(int device, void *stream, mgpu_ctx **out)
                                             std::to_string(prop.major) + std::to_string(prop.minor));
     ctx->device = device;
     ctx->num_sms = prop.multiProcessorCount;
+    // Keep freed stream-ordered memory in the pool: the default threshold (0)
+    // returns it to the OS at every synchronisation, so each solve would
+    // re-map its work vectors.
+    cudaMemPool_t pool;
+    MG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = UINT64_MAX;
+    MG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     if (stream != nullptr)
     {
       ctx->stream = static_cast<cudaStream_t>(stream);

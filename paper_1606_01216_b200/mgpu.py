@@ -117,6 +117,7 @@ def lib():
         L.mgpu_csr_info.argtypes = [vp, vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]
         L.mgpu_csr_download.argtypes = [vp, vp, vp, vp, vp]
         L.mgpu_csr_free.argtypes = [vp]
+        L.mgpu_csr_device_view.argtypes = [vp, C.POINTER(i64), C.POINTER(i64), vp, vp, vp]
         L.mgpu_sp_add_scaled.argtypes = [vp, vp, vp, dbl, dbl, C.POINTER(vp)]
         L.mgpu_shifted_operators.argtypes = [vp, vp, vp, vp, C.c_int, vp, vp]
         L.mgpu_transpose.argtypes = [vp, vp, C.POINTER(vp)]
@@ -197,9 +198,10 @@ def model_chain(n: int, alpha=0.05, beta=0.05, stiffness_scale=0.01, mass_scale=
 class Context:
     """One device + stream (mgpu_ctx)."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, stream: Optional[int] = None):
+        """stream: a cudaStream_t handle (e.g. torch.cuda.Stream().cuda_stream) or None (library-owned)."""
         self.handle = C.c_void_p()
-        st = lib().mgpu_ctx_create(device, None, C.byref(self.handle))
+        st = lib().mgpu_ctx_create(device, C.c_void_p(stream) if stream else None, C.byref(self.handle))
         if st != MGPU_OK:
             raise CudaError(f"mgpu_ctx_create(device={device}) failed: {lib().mgpu_status_string(st).decode()}")
         self.device = device
@@ -262,6 +264,13 @@ class DeviceCsr:
         ctx.check(lib().mgpu_csr_upload(ctx.handle, A.nrows, A.ncols, v.shape[0], _ptr(rp), _ptr(ci), _ptr(v),
                                         C.byref(h)))
         return DeviceCsr(ctx, h, A.nrows)
+
+    @property
+    def stored_nnz(self) -> int:
+        """Entries stored on the device (fixed-pattern factors may store exact zeros)."""
+        n, nnz = C.c_int64(), C.c_int64()
+        lib().mgpu_csr_device_view(self.handle, C.byref(n), C.byref(nnz), None, None, None)
+        return nnz.value
 
     def download(self) -> SparseMatrix:
         n, nc, nnz = C.c_int64(), C.c_int64(), C.c_int64()
@@ -433,9 +442,31 @@ def _factor_mat(f):
     return f.matrix if isinstance(f, SpaiFactor) else f
 
 
+def cg_solve_raw(ctx: Context, dA: Sequence[DeviceCsr], flat_chain: Sequence[DeviceCsr], z: int, n: int, m: int,
+                 B_ptr: int, ldb: int, rtol: float, maxit: int, where: int, X_ptr: int, REC_ptr: int, TR_ptr: int,
+                 history_cap: int = 0):
+    """Direct mgpu_cg_solve call: pointers are host (where=MGPU_HOST) or device (MGPU_DEVICE).
+    Returns (status, iterations, converged, status_per_column, breakdown_iteration, history)."""
+    l = len(dA)
+    it = np.zeros(l * m, np.int64)
+    cv = np.zeros(l * m, np.int32)
+    st = np.zeros(l * m, np.int32)
+    bd = np.zeros(l * m, np.int64)
+    hist = np.zeros(max(l * m * history_cap, 1))
+    out = _CgOut(X_ptr, REC_ptr, TR_ptr, it.ctypes.data_as(C.POINTER(C.c_int64)),
+                 cv.ctypes.data_as(C.POINTER(C.c_int)), st.ctypes.data_as(C.POINTER(C.c_int)),
+                 bd.ctypes.data_as(C.POINTER(C.c_int64)),
+                 hist.ctypes.data_as(C.POINTER(C.c_double)) if history_cap > 0 else None, history_cap)
+    status = lib().mgpu_cg_solve(ctx.handle, l, _handles(dA), z, _handles(flat_chain), n, m, C.c_void_p(B_ptr), ldb,
+                                 rtol, maxit, where, C.byref(out))
+    return status, it, cv, st, bd, (hist.reshape(l, m, history_cap) if history_cap > 0 else None)
+
+
 def cg_solve_batched(As: Sequence, chains: Sequence[Sequence], B, rtol: float = 1e-10, maxit: Optional[int] = None,
-                     history_cap: int = 0, raise_on_breakdown: bool = True, ctx=None):
-    """Batched block_solve over points (mgpu_cg_solve). B: (n, m) shared or (l, n, m)."""
+                     history_cap: int = 0, raise_on_breakdown: bool = True, ctx=None, host_out=None):
+    """Batched block_solve over points (mgpu_cg_solve), host buffers.
+    B: (n,) / (n, m) shared by every point, or (l, n, m).  host_out: optional dict of
+    preallocated (l, m, n) float64 arrays X / REC / TR (e.g. pinned memory)."""
     ctx = ctx or default_context()
     dA = [_dev(a, ctx) for a in As]
     l = len(dA)
@@ -455,31 +486,42 @@ def cg_solve_batched(As: Sequence, chains: Sequence[Sequence], B, rtol: float = 
         Bc = np.ascontiguousarray(np.transpose(Bn, (0, 2, 1)))  # [p][c][row]
         ldb = n * m
     maxit = 10 * n if maxit is None else maxit
-    X = np.zeros((l, m, n))
-    REC = np.zeros((l, m, n))
-    TR = np.zeros((l, m, n))
-    it = np.zeros(l * m, np.int64)
-    cv = np.zeros(l * m, np.int32)
-    st = np.zeros(l * m, np.int32)
-    bd = np.zeros(l * m, np.int64)
-    hist = np.zeros(max(l * m * history_cap, 1))
-    out = _CgOut(X.ctypes.data, REC.ctypes.data, TR.ctypes.data, it.ctypes.data_as(C.POINTER(C.c_int64)),
-                 cv.ctypes.data_as(C.POINTER(C.c_int)), st.ctypes.data_as(C.POINTER(C.c_int)),
-                 bd.ctypes.data_as(C.POINTER(C.c_int64)),
-                 hist.ctypes.data_as(C.POINTER(C.c_double)) if history_cap > 0 else None, history_cap)
-    status = lib().mgpu_cg_solve(ctx.handle, l, _handles(dA), z, _handles(flat), n, m, _ptr(Bc), ldb, rtol, maxit,
-                                 MGPU_HOST, C.byref(out))
+    if host_out is None:
+        X, REC, TR = (np.zeros((l, m, n)) for _ in range(3))
+    else:
+        X, REC, TR = host_out["X"], host_out["REC"], host_out["TR"]
+    status, it, cv, st, bd, hist = cg_solve_raw(ctx, dA, flat, z, n, m, Bc.ctypes.data, ldb, rtol, maxit, MGPU_HOST,
+                                                X.ctypes.data, REC.ctypes.data, TR.ctypes.data, history_cap)
     if status != MGPU_OK and (raise_on_breakdown or status != MGPU_ERR_BREAKDOWN):
         ctx.check(status)
     results = []
     for p in range(l):
         sl = slice(p * m, (p + 1) * m)
-        h = hist.reshape(l, m, history_cap)[p] if history_cap > 0 else None
         results.append(BlockSolveResult(X=X[p].T.copy(), recurrence_residuals=REC[p].T.copy(),
                                         true_residuals=TR[p].T.copy(), iterations=it[sl].copy(),
                                         all_converged=bool(cv[sl].all()), converged=cv[sl].astype(bool),
-                                        status=st[sl].copy(), breakdown_iteration=bd[sl].copy(), relres_history=h))
+                                        status=st[sl].copy(), breakdown_iteration=bd[sl].copy(),
+                                        relres_history=hist[p] if hist is not None else None))
     return results
+
+
+def cg_solve_device(As: Sequence, chains: Sequence[Sequence], B_dev, X_dev, REC_dev=None, TR_dev=None,
+                    rtol: float = 1e-10, maxit: Optional[int] = None, shared_rhs: bool = True, ctx=None):
+    """Device-resident batched solve.  B_dev / X_dev / ...: torch CUDA float64 tensors laid out
+    [point][column][row] (B_dev may be one (m, n) block shared by every point)."""
+    ctx = ctx or default_context()
+    dA = [_dev(a, ctx) for a in As]
+    n = dA[0].nrows
+    z = len(chains[0]) if chains else 0
+    flat = [_dev(_factor_mat(f), ctx) for c in chains for f in c]
+    m = int(B_dev.shape[-2]) if B_dev.dim() >= 2 else 1
+    maxit = 10 * n if maxit is None else maxit
+    ptr = lambda t: t.data_ptr() if t is not None else 0
+    status, it, cv, st, bd, _ = cg_solve_raw(ctx, dA, flat, z, n, m, B_dev.data_ptr(), 0 if shared_rhs else n * m,
+                                             rtol, maxit, MGPU_DEVICE, ptr(X_dev), ptr(REC_dev), ptr(TR_dev))
+    if status != MGPU_OK and status != MGPU_ERR_BREAKDOWN:
+        ctx.check(status)
+    return it, cv, st, bd
 
 
 def block_solve(A, chain: Sequence, B, rtol: float = 1e-10, maxit: Optional[int] = None, ctx=None):
