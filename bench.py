@@ -57,18 +57,17 @@ def parse():
 
 def workload(name: str, world: int, rank: int):
     """(ne, m, shifts for this rank, all shifts, pattern, description)."""
+    from paper_1606_01216_b200 import sharding
     if name == "config0":
         ne, m, per, pattern = 1000, 1, 1, 0
         all_shifts = [100.0] * world
     elif name == "config1":
         ne, m, per, pattern = 10000, 1, 8, 0
-        tot = per * world
-        all_shifts = [10.0 ** (1 + 3 * i / (tot - 1)) for i in range(tot)]
+        all_shifts = sharding.log_shifts(per * world)
     else:
         ne, m, per, pattern = 500000, 4, 16, 1
-        tot = per * world
-        all_shifts = [10.0 ** (1 + 3 * i / (tot - 1)) for i in range(tot)]
-    return ne, m, all_shifts[rank::world], all_shifts, pattern
+        all_shifts = sharding.log_shifts(per * world)
+    return ne, m, sharding.shard(all_shifts, rank, world), all_shifts, pattern
 
 
 def rhs_block(n: int, m: int) -> np.ndarray:
@@ -316,10 +315,8 @@ def run_mgpu(args, rank, world, local_rank):
     e2e_recs, _ = timed(step_e2e)
     e2e_ms = float(sum(a.elapsed_time(b) for a, b in e2e_recs))
 
-    if dist:
-        t = torch.tensor([total_ms, e2e_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms, e2e_ms = float(t[0]), float(t[1])
+    from paper_1606_01216_b200 import sharding
+    total_ms, e2e_ms = sharding.max_over_ranks([total_ms, e2e_ms], dist, dev)
 
     solves = len(all_shifts) * m * args.steps
     value = solves / (total_ms / 1e3)
