@@ -16,6 +16,8 @@
 //     (in-order rows, no FMA); only the dot-product summation order differs.
 #include <cooperative_groups.h>
 
+#include <algorithm>
+#include <climits>
 #include <cmath>
 #include <vector>
 
@@ -684,6 +686,655 @@ __global__ void __launch_bounds__(kCgThreads) cg_persistent(CgParams P)
   }
 }
 
+// =====================================================================
+// Banded fast path (all operators of the batch have bandwidth <= kMaxHalo):
+// TWO grid barriers per iteration.
+//   phase A: d_new = r + beta d_old (halo rows recomputed in shared memory),
+//            t = P_chain d_new on shrinking halos, w = A t on owned rows,
+//            partials (d_new, w), (d_new, d_new);
+//   phase B: x~ += alpha d_new, r -= alpha w, partial (r, r).
+// Work split: the flattened rows of all points (each point padded to a
+// multiple of 32) are cut into one balanced, 32-row aligned range per block;
+// a block processes its range in chunks of TB * RPT rows (one chunk for the
+// L2-resident configurations), RPT rows per thread for memory-level
+// parallelism.  Dot products: per thread in row order, fixed warp butterfly,
+// fixed warp-order combine, chunks in order -> one partial per (block, point);
+// after the barrier every block sums the per-block partials in block order.
+// Deterministic for a given grid (one block per SM), no atomics.
+// =====================================================================
+constexpr int kMaxZ = 8;
+constexpr int kMaxHalo = 64;
+constexpr int kMaxRpt = 4;
+constexpr int kMaxSeg = 8; // row segments per block
+
+struct Seg
+{
+  int p, rs, re, pad; // rows [rs, re) of point p
+};
+
+struct BandParams
+{
+  int l, m, z, rpt;
+  int64_t n, npad;
+  int halo[kMaxZ + 1]; // halo rows needed by stage q (q = 0 .. z); halo[z] = bw(A)
+  int hmax;            // halo[0]
+  const DCsr *A, *F;
+  double rtol;
+  int64_t maxit;
+  const double *b;
+  double *xt, *r, *dbuf0, *dbuf1, *w, *sol;
+  double *partial; // [l][2*kMaxM][gridDim]
+  const Seg *seg;  // [gridDim][kMaxSeg], p = -1 terminates
+  const int2 *pblk; // [l]: blocks [x, y) that own rows of point p
+  double *X, *REC, *TR;
+  int64_t *iters;
+  int *conv, *status;
+  int64_t *bd_iter;
+  double *hist;
+  int64_t hist_cap;
+  int64_t *loop_iters;
+};
+
+template <int TB>
+struct BandShared
+{
+  double rho[kMaxSys], target[kMaxSys], alpha[kMaxSys], beta[kMaxSys], bnorm[kMaxSys];
+  double tot[kMaxSys * 2];
+  int state[kMaxSys];
+  int fresh[kMaxSys];
+  int64_t sit[kMaxSys];
+  int pmask[kMaxPoints];
+  Seg seg[kMaxSeg];
+  int nseg;
+  double wsum[TB / 32][2 * kMaxM];
+  double acc[2 * kMaxM];
+  int flag;
+};
+
+// Iterate this block's row segments [rs, re) of point p (host plan in shared memory).
+template <class S, class F>
+__device__ __forceinline__ void for_segments(const BandParams &, const S &sh, F &&fn)
+{
+  for (int q = 0; q < sh.nseg; ++q)
+  {
+    const Seg g = sh.seg[q];
+    if (sh.pmask[g.p])
+      fn(g.p, static_cast<int64_t>(g.rs), static_cast<int64_t>(g.re));
+  }
+}
+
+// Adds this chunk's per-thread values (NV of them, nv used) to the block's
+// running partials in a fixed order.
+template <int TB, int NV>
+__device__ __forceinline__ void chunk_sum(BandShared<TB> &sh, double (&v)[NV], int nv)
+{
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+  {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1)
+      v[k] = __dadd_rn(v[k], __shfl_xor_sync(0xffffffffu, v[k], off));
+  }
+  if (lane == 0)
+  {
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+      sh.wsum[warp][k] = v[k];
+  }
+  __syncthreads();
+  if (warp == 0)
+  {
+    for (int k = 0; k < nv; ++k)
+    {
+      double x = lane < TB / 32 ? sh.wsum[lane][k] : 0.0;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1)
+        x = __dadd_rn(x, __shfl_xor_sync(0xffffffffu, x, off));
+      if (lane == 0)
+        sh.acc[k] = __dadd_rn(sh.acc[k], x);
+    }
+  }
+  __syncthreads();
+}
+
+template <int TB>
+__device__ __forceinline__ void begin_point(BandShared<TB> &sh)
+{
+  if (threadIdx.x < 2 * kMaxM)
+    sh.acc[threadIdx.x] = 0.0;
+  __syncthreads();
+}
+
+template <int TB>
+__device__ __forceinline__ void end_point(const BandParams &P, BandShared<TB> &sh, int p, int nv)
+{
+  if (threadIdx.x < nv)
+    P.partial[(static_cast<int64_t>(p) * 2 * kMaxM + threadIdx.x) * gridDim.x + blockIdx.x] = sh.acc[threadIdx.x];
+  __syncthreads();
+}
+
+// After a barrier: tot[p][k] = sum over blocks (fixed order) for live points.
+template <int TB>
+__device__ void reduce_blocks(const BandParams &P, BandShared<TB> &sh, int nk)
+{
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int npairs = P.l * nk;
+  for (int q = warp; q < npairs; q += TB / 32)
+  {
+    const int p = q / nk, k = q % nk;
+    if (!sh.pmask[p])
+      continue;
+    const double *src = P.partial + (static_cast<int64_t>(p) * 2 * kMaxM + k) * gridDim.x;
+    const int2 br = P.pblk[p];
+    double a = 0.0;
+    for (int t = br.x + lane; t < br.y; t += 32)
+      a = __dadd_rn(a, __ldcg(src + t));
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1)
+      a = __dadd_rn(a, __shfl_xor_sync(0xffffffffu, a, off));
+    if (lane == 0)
+      sh.tot[p * 2 * kMaxM + k] = a;
+  }
+  __syncthreads();
+}
+
+// Phase A.  kCheck: source = x~, outputs sol (own rows) and res = b - A sol (in w);
+// otherwise source = d_new = fresh ? r : r + beta d_old, output w.
+template <int TB, int MT, int RPT, bool kCheck>
+__device__ void band_phase_a(const BandParams &P, BandShared<TB> &sh, double *smem, const double *d_old,
+                             double *d_new)
+{
+  const int m = P.m;
+  const int H0 = P.hmax;
+  constexpr int CH = TB * RPT;
+  const int stride = (CH + 2 * H0) * m;
+  double *buf0 = smem, *buf1 = smem + stride;
+  for_segments(P, sh, [&](int p, int64_t rs, int64_t re) {
+    begin_point(sh);
+    const int64_t base = static_cast<int64_t>(p) * P.n * m;
+    double be[MT];
+    bool fr[MT];
+#pragma unroll
+    for (int c = 0; c < MT; ++c)
+    {
+      const int s = p * m + c;
+      fr[c] = c < m && sh.fresh[s];
+      be[c] = (c < m) ? sh.beta[s] : 0.0;
+    }
+    const DCsr A = P.A[p];
+    for (int64_t c0 = rs; c0 < re; c0 += CH)
+    {
+      const int64_t c1 = min(re, c0 + CH);
+      // ---- stage 0 on [c0 - H0, c1 + H0)
+      const int span0 = static_cast<int>(c1 - c0) + 2 * H0;
+      for (int q = threadIdx.x; q < span0; q += TB)
+      {
+        const int64_t i = c0 - H0 + q;
+        if (i < 0 || i >= P.n)
+          continue;
+#pragma unroll
+        for (int c = 0; c < MT; ++c)
+        {
+          if (c >= m)
+            break;
+          const int64_t v = base + i * m + c;
+          double x;
+          if (kCheck)
+            x = __ldcg(P.xt + v);
+          else
+          {
+            const double rv = __ldcg(P.r + v);
+            x = fr[c] ? rv : __dadd_rn(rv, __dmul_rn(be[c], __ldcg(d_old + v)));
+            if (i >= c0 && i < c1)
+              __stcg(d_new + v, x);
+          }
+          buf0[q * m + c] = x;
+        }
+      }
+      __syncthreads();
+      // ---- chain stages (oldest factor first), shrinking halos
+      double *src = buf0, *dst = buf1;
+      int hs = H0;
+      for (int st = 0; st < P.z; ++st)
+      {
+        const DCsr F = P.F[p * P.z + (P.z - 1 - st)];
+        const int hd = P.halo[st + 1];
+        const int span = static_cast<int>(c1 - c0) + 2 * hd;
+        const int64_t shift = static_cast<int64_t>(hs) - c0; // col k -> src row k + shift
+        for (int q = threadIdx.x; q < span; q += TB)
+        {
+          const int64_t i = c0 - hd + q;
+          if (i < 0 || i >= P.n)
+            continue;
+          double acc[MT];
+#pragma unroll
+          for (int c = 0; c < MT; ++c)
+            acc[c] = 0.0;
+          const int64_t e = __ldg(F.rp + i + 1);
+          for (int64_t k = __ldg(F.rp + i); k < e; ++k)
+          {
+            const double fv = __ldg(F.v + k);
+            const int loc = static_cast<int>(__ldg(F.ci + k) + shift) * m;
+#pragma unroll
+            for (int c = 0; c < MT; ++c)
+              if (c < m)
+                acc[c] = __dadd_rn(acc[c], __dmul_rn(fv, src[loc + c]));
+          }
+#pragma unroll
+          for (int c = 0; c < MT; ++c)
+            if (c < m)
+              dst[q * m + c] = acc[c];
+        }
+        __syncthreads();
+        double *tmp = src;
+        src = dst;
+        dst = tmp;
+        hs = hd;
+      }
+      // ---- y = A t on own rows, RPT rows per thread
+      double pk[2 * MT];
+#pragma unroll
+      for (int q = 0; q < 2 * MT; ++q)
+        pk[q] = 0.0;
+      const int64_t shiftA = static_cast<int64_t>(hs) - c0;
+#pragma unroll
+      for (int j = 0; j < RPT; ++j)
+      {
+        const int lr = threadIdx.x + j * TB; // local row
+        const int64_t i = c0 + lr;
+        if (i >= c1)
+          break;
+        double acc[MT];
+#pragma unroll
+        for (int c = 0; c < MT; ++c)
+          acc[c] = 0.0;
+        const int64_t e = __ldg(A.rp + i + 1);
+        for (int64_t k = __ldg(A.rp + i); k < e; ++k)
+        {
+          const double av = __ldg(A.v + k);
+          const int loc = static_cast<int>(__ldg(A.ci + k) + shiftA) * m;
+#pragma unroll
+          for (int c = 0; c < MT; ++c)
+            if (c < m)
+              acc[c] = __dadd_rn(acc[c], __dmul_rn(av, src[loc + c]));
+        }
+#pragma unroll
+        for (int c = 0; c < MT; ++c)
+        {
+          if (c >= m)
+            break;
+          const int64_t v = base + i * m + c;
+          if (kCheck)
+          {
+            const double res = __dsub_rn(__ldg(P.b + v), acc[c]);
+            __stcg(P.w + v, res);
+            __stcg(P.sol + v, src[(hs + lr) * m + c]);
+            pk[c] = __dadd_rn(pk[c], __dmul_rn(res, res));
+          }
+          else
+          {
+            const double dn = buf0[(H0 + lr) * m + c];
+            __stcg(P.w + v, acc[c]);
+            pk[c] = __dadd_rn(pk[c], __dmul_rn(dn, acc[c]));
+            pk[MT + c] = __dadd_rn(pk[MT + c], __dmul_rn(dn, dn));
+          }
+        }
+      }
+      // pack (k, c) -> k * m + c
+      double pv[2 * MT];
+#pragma unroll
+      for (int q = 0; q < 2 * MT; ++q)
+        pv[q] = 0.0;
+#pragma unroll
+      for (int c = 0; c < MT; ++c)
+        if (c < m)
+        {
+          pv[c] = pk[c];
+          pv[m + c] = pk[MT + c];
+        }
+      chunk_sum<TB, 2 * MT>(sh, pv, kCheck ? m : 2 * m); // its barriers also guard buf reuse
+    }
+    end_point(P, sh, p, kCheck ? m : 2 * m);
+  });
+}
+
+// Phase B: x~ += alpha d_new; r -= alpha w; partial (r, r) for running columns.
+template <int TB, int MT, int RPT>
+__device__ void band_phase_b(const BandParams &P, BandShared<TB> &sh, const double *d_new)
+{
+  const int m = P.m;
+  constexpr int CH = TB * RPT;
+  for_segments(P, sh, [&](int p, int64_t rs, int64_t re) {
+    begin_point(sh);
+    const int64_t base = static_cast<int64_t>(p) * P.n * m;
+    bool run[MT];
+    double al[MT];
+#pragma unroll
+    for (int c = 0; c < MT; ++c)
+    {
+      run[c] = c < m && sh.state[p * m + c] == kRun;
+      al[c] = run[c] ? sh.alpha[p * m + c] : 0.0;
+    }
+    for (int64_t c0 = rs; c0 < re; c0 += CH)
+    {
+      const int64_t c1 = min(re, c0 + CH);
+      double pk[MT];
+#pragma unroll
+      for (int c = 0; c < MT; ++c)
+        pk[c] = 0.0;
+#pragma unroll
+      for (int j = 0; j < RPT; ++j)
+      {
+        const int64_t i = c0 + threadIdx.x + j * TB;
+        if (i >= c1)
+          break;
+#pragma unroll
+        for (int c = 0; c < MT; ++c)
+          if (run[c])
+          {
+            const int64_t v = base + i * m + c;
+            const double xn = __dadd_rn(__ldcg(P.xt + v), __dmul_rn(al[c], __ldcg(d_new + v)));
+            const double rn = __dadd_rn(__ldcg(P.r + v), __dmul_rn(-al[c], __ldcg(P.w + v)));
+            __stcg(P.xt + v, xn);
+            __stcg(P.r + v, rn);
+            pk[c] = __dadd_rn(pk[c], __dmul_rn(rn, rn));
+          }
+      }
+      chunk_sum<TB, MT>(sh, pk, m);
+    }
+    end_point(P, sh, p, m);
+  });
+}
+
+// Copy phase after a confirmation check (finish converged / restart others).
+template <int TB>
+__device__ void band_finish_copy(const BandParams &P, BandShared<TB> &sh)
+{
+  const int m = P.m;
+  for_segments(P, sh, [&](int p, int64_t rs, int64_t re) {
+    const int64_t base = static_cast<int64_t>(p) * P.n * m;
+    for (int64_t i = rs + threadIdx.x; i < re; i += TB)
+      for (int c = 0; c < m; ++c)
+      {
+        const int s = p * m + c;
+        const int64_t v = base + i * m + c, o = static_cast<int64_t>(s) * P.n + i;
+        if (sh.state[s] == kPendingConv || sh.state[s] == kMaxed)
+        {
+          if (P.X)
+            P.X[o] = __ldcg(P.sol + v);
+          if (P.TR)
+            P.TR[o] = __ldcg(P.w + v);
+        }
+        else if (sh.state[s] == kPendingRestart)
+          __stcg(P.r + v, __ldcg(P.w + v));
+      }
+  });
+}
+
+template <int TB, int MT, int RPT>
+__global__ void __launch_bounds__(TB, 1) cg_banded(BandParams P)
+{
+  cgrp::grid_group grid = cgrp::this_grid();
+  extern __shared__ double smem_dyn[];
+  __shared__ BandShared<TB> sh;
+  const int m = P.m;
+  const int S = P.l * m;
+
+  // ---- segment plan, phase 0: ||b||^2
+  if (threadIdx.x == 0)
+  {
+    int q = 0;
+    while (q < kMaxSeg && P.seg[blockIdx.x * kMaxSeg + q].p >= 0)
+    {
+      sh.seg[q] = P.seg[blockIdx.x * kMaxSeg + q];
+      ++q;
+    }
+    sh.nseg = q;
+  }
+  for (int p = threadIdx.x; p < P.l; p += TB)
+    sh.pmask[p] = 1;
+  __syncthreads();
+  for_segments(P, sh, [&](int p, int64_t rs, int64_t re) {
+    begin_point(sh);
+    const int64_t base = static_cast<int64_t>(p) * P.n * m;
+    for (int64_t c0 = rs; c0 < re; c0 += TB * RPT)
+    {
+      const int64_t c1 = min(re, c0 + TB * RPT);
+      double pk[MT];
+#pragma unroll
+      for (int c = 0; c < MT; ++c)
+        pk[c] = 0.0;
+#pragma unroll
+      for (int j = 0; j < RPT; ++j)
+      {
+        const int64_t i = c0 + threadIdx.x + j * TB;
+        if (i >= c1)
+          break;
+#pragma unroll
+        for (int c = 0; c < MT; ++c)
+          if (c < m)
+          {
+            const double bv = __ldg(P.b + base + i * m + c);
+            pk[c] = __dadd_rn(pk[c], __dmul_rn(bv, bv));
+          }
+      }
+      chunk_sum<TB, MT>(sh, pk, m);
+    }
+    end_point(P, sh, p, m);
+  });
+  grid.sync();
+  reduce_blocks<TB>(P, sh, m);
+  for (int s = threadIdx.x; s < S; s += TB)
+  {
+    const double bb = sh.tot[(s / m) * 2 * kMaxM + s % m];
+    const double bn = sqrt(bb);
+    sh.bnorm[s] = bn;
+    sh.rho[s] = bb;
+    sh.target[s] = P.rtol * bn;
+    sh.state[s] = bn == 0.0 ? kZeroRhs : kRun;
+    sh.fresh[s] = 1;
+    sh.beta[s] = 0.0;
+    sh.sit[s] = 0;
+  }
+  __syncthreads();
+
+  int cur = 0; // d_old = dbuf[cur], d_new = dbuf[cur ^ 1]
+  int64_t it = 0;
+  for (;;)
+  {
+    if (it >= P.maxit)
+      break;
+    // ---- confirm on the true residual (krylov.cpp:77-103)
+    if (threadIdx.x == 0)
+      sh.flag = 0;
+    __syncthreads();
+    for (int p = threadIdx.x; p < P.l; p += TB)
+    {
+      int need = 0;
+      for (int c = 0; c < m; ++c)
+      {
+        const int s = p * m + c;
+        need |= sh.state[s] == kRun && sqrt(sh.rho[s]) <= sh.target[s];
+      }
+      sh.pmask[p] = need;
+      if (need)
+        atomicOr(&sh.flag, 1);
+    }
+    __syncthreads();
+    if (sh.flag)
+    {
+      band_phase_a<TB, MT, RPT, true>(P, sh, smem_dyn, nullptr, nullptr);
+      grid.sync();
+      reduce_blocks<TB>(P, sh, m);
+      for (int s = threadIdx.x; s < S; s += TB)
+      {
+        if (!(sh.state[s] == kRun && sqrt(sh.rho[s]) <= sh.target[s]))
+          continue;
+        const double tt = sh.tot[(s / m) * 2 * kMaxM + s % m];
+        if (sqrt(tt) <= sh.target[s])
+        {
+          sh.state[s] = kPendingConv;
+          sh.sit[s] = it;
+        }
+        else
+        {
+          sh.rho[s] = tt;
+          if (sqrt(tt) <= sh.target[s])
+          {
+            sh.state[s] = kPendingConv;
+            sh.sit[s] = it;
+          }
+          else
+          {
+            sh.state[s] = kPendingRestart;
+            sh.fresh[s] = 1; // d = r (the true residual)
+          }
+        }
+      }
+      __syncthreads();
+      band_finish_copy<TB>(P, sh);
+      grid.sync();
+      for (int s = threadIdx.x; s < S; s += TB)
+      {
+        if (sh.state[s] == kPendingConv)
+          sh.state[s] = kConverged;
+        else if (sh.state[s] == kPendingRestart)
+          sh.state[s] = kRun;
+      }
+      __syncthreads();
+    }
+    // ---- live points
+    if (threadIdx.x == 0)
+      sh.flag = 0;
+    __syncthreads();
+    for (int p = threadIdx.x; p < P.l; p += TB)
+    {
+      int live = 0;
+      for (int c = 0; c < m; ++c)
+        live |= sh.state[p * m + c] == kRun;
+      sh.pmask[p] = live;
+      if (live)
+        atomicOr(&sh.flag, 1);
+    }
+    __syncthreads();
+    if (!sh.flag)
+      break;
+    double *d_old = cur ? P.dbuf1 : P.dbuf0;
+    double *d_new = cur ? P.dbuf0 : P.dbuf1;
+    // ---- phase A: d_new, w = A P d_new, (d, w), (d, d)
+    band_phase_a<TB, MT, RPT, false>(P, sh, smem_dyn, d_old, d_new);
+    grid.sync();
+    reduce_blocks<TB>(P, sh, 2 * m);
+    for (int s = threadIdx.x; s < S; s += TB)
+    {
+      if (sh.state[s] != kRun)
+        continue;
+      const int p = s / m, c = s % m;
+      const double curv = sh.tot[p * 2 * kMaxM + c];
+      const double dd = sh.tot[p * 2 * kMaxM + m + c];
+      if (!(curv > 1e-30 * dd))
+      {
+        sh.state[s] = kBreakdown;
+        sh.sit[s] = it;
+      }
+      else
+        sh.alpha[s] = sh.rho[s] / curv;
+    }
+    __syncthreads();
+    // ---- phase B
+    band_phase_b<TB, MT, RPT>(P, sh, d_new);
+    grid.sync();
+    reduce_blocks<TB>(P, sh, m);
+    ++it;
+    for (int s = threadIdx.x; s < S; s += TB)
+    {
+      if (sh.state[s] != kRun)
+        continue;
+      const double rn = sh.tot[(s / m) * 2 * kMaxM + s % m];
+      if (P.hist && blockIdx.x == 0 && it - 1 < P.hist_cap)
+        P.hist[static_cast<int64_t>(s) * P.hist_cap + (it - 1)] = sqrt(rn) / sh.bnorm[s];
+      sh.beta[s] = rn / sh.rho[s];
+      sh.rho[s] = rn;
+      sh.fresh[s] = 0;
+    }
+    __syncthreads();
+    cur ^= 1;
+  }
+
+  // ---- budget exhausted: final true-residual check
+  if (threadIdx.x == 0)
+    sh.flag = 0;
+  __syncthreads();
+  for (int p = threadIdx.x; p < P.l; p += TB)
+  {
+    int need = 0;
+    for (int c = 0; c < m; ++c)
+      need |= sh.state[p * m + c] == kRun;
+    sh.pmask[p] = need;
+    if (need)
+      atomicOr(&sh.flag, 1);
+  }
+  __syncthreads();
+  if (sh.flag)
+  {
+    band_phase_a<TB, MT, RPT, true>(P, sh, smem_dyn, nullptr, nullptr);
+    grid.sync();
+    reduce_blocks<TB>(P, sh, m);
+    for (int s = threadIdx.x; s < S; s += TB)
+    {
+      if (sh.state[s] != kRun)
+        continue;
+      const double tt = sh.tot[(s / m) * 2 * kMaxM + s % m];
+      sh.state[s] = sqrt(tt) <= sh.target[s] ? kPendingConv : kMaxed;
+      sh.sit[s] = it;
+    }
+    __syncthreads();
+    band_finish_copy<TB>(P, sh);
+    for (int s = threadIdx.x; s < S; s += TB)
+      if (sh.state[s] == kPendingConv)
+        sh.state[s] = kConverged;
+    __syncthreads();
+  }
+  // ---- recurrence residual block, zero-rhs outputs, per-column scalars
+  for (int p = threadIdx.x; p < P.l; p += TB)
+    sh.pmask[p] = 1;
+  __syncthreads();
+  for_segments(P, sh, [&](int p, int64_t rs, int64_t re) {
+    const int64_t base = static_cast<int64_t>(p) * P.n * m;
+    for (int64_t i = rs + threadIdx.x; i < re; i += TB)
+      for (int c = 0; c < m; ++c)
+      {
+        const int s = p * m + c;
+        const int64_t o = static_cast<int64_t>(s) * P.n + i;
+        if (sh.state[s] == kZeroRhs)
+        {
+          if (P.X)
+            P.X[o] = 0.0;
+          if (P.TR)
+            P.TR[o] = 0.0;
+          if (P.REC)
+            P.REC[o] = 0.0;
+        }
+        else if (sh.state[s] != kBreakdown && P.REC)
+          P.REC[o] = __ldcg(P.r + base + i * m + c);
+      }
+  });
+  if (blockIdx.x == 0)
+  {
+    for (int s = threadIdx.x; s < S; s += TB)
+    {
+      const int st = sh.state[s];
+      P.iters[s] = sh.sit[s];
+      P.conv[s] = (st == kConverged || st == kZeroRhs) ? 1 : 0;
+      P.status[s] = st == kBreakdown ? MGPU_ERR_BREAKDOWN : MGPU_OK;
+      P.bd_iter[s] = st == kBreakdown ? sh.sit[s] : -1;
+    }
+    if (threadIdx.x == 0)
+      *P.loop_iters = it;
+  }
+}
+
 // B [p][c][row] (column-major per point; ldb between points) -> interleaved
 // b, r = b, d = b, x~ = 0.
 __global__ void cg_init(int l, int m, int64_t n, const double *__restrict__ B, int64_t ldb, double *__restrict__ b,
@@ -721,6 +1372,70 @@ void launch_cg(mgpu_ctx *ctx, const CgParams &P)
   check_launch(ctx, "cg_persistent");
 }
 
+template <int TB, int MT, int RPT>
+void launch_banded_cfg(mgpu_ctx *ctx, const BandParams &P)
+{
+  const size_t dyn = sizeof(double) * 2 * static_cast<size_t>(TB * RPT + 2 * P.hmax) * P.m;
+  MG_CUDA(cudaFuncSetAttribute(cg_banded<TB, MT, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(dyn)));
+  int per_sm = 0;
+  MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cg_banded<TB, MT, RPT>, TB, dyn));
+  if (per_sm < 1)
+    throw Error(MGPU_ERR_CUDA, "cg_banded: kernel does not fit on an SM");
+  BandParams local = P;
+  void *args[] = {&local};
+  MG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void *>(cg_banded<TB, MT, RPT>),
+                                      dim3(static_cast<unsigned>(ctx->num_sms)), dim3(TB), args, dyn, ctx->stream));
+  check_launch(ctx, "cg_banded");
+}
+
+// Rows per thread: enough that one chunk covers a block's range when the
+// problem is small; capped for register pressure.
+template <int TB, int MT>
+void launch_banded_rpt(mgpu_ctx *ctx, BandParams &P)
+{
+  const int64_t per_point = P.l <= ctx->num_sms ? (ctx->num_sms / P.l) : 1;
+  const int64_t rows_per_block =
+      P.l <= ctx->num_sms ? (P.npad + per_point - 1) / per_point : P.npad * ((P.l + ctx->num_sms - 1) / ctx->num_sms);
+  int rpt = static_cast<int>((rows_per_block + TB - 1) / TB);
+  rpt = rpt < 1 ? 1 : (rpt > kMaxRpt ? kMaxRpt : rpt);
+  if (rpt == 3)
+    rpt = 4;
+  P.rpt = rpt;
+  if (rpt == 1)
+    launch_banded_cfg<TB, MT, 1>(ctx, P);
+  else if (rpt == 2)
+    launch_banded_cfg<TB, MT, 2>(ctx, P);
+  else
+    launch_banded_cfg<TB, MT, 4>(ctx, P);
+}
+
+// Halo plan of the banded path; false when an operator is too wide for it.
+bool band_plan(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_csr *const *chains, int m,
+               int *halo, int *hmax)
+{
+  if (z > kMaxZ || static_cast<int64_t>(l) * m > kMaxSys || l > kMaxPoints)
+    return false;
+  int64_t bwA = 0;
+  std::vector<int64_t> bwF(static_cast<size_t>(z > 0 ? z : 1), 0);
+  for (int p = 0; p < l; ++p)
+  {
+    bwA = std::max(bwA, csr_bandwidth(ctx, const_cast<mgpu_csr *>(A[p])));
+    for (int f = 0; f < z; ++f)
+      bwF[f] = std::max(bwF[f], csr_bandwidth(ctx, const_cast<mgpu_csr *>(chains[static_cast<size_t>(p) * z + f])));
+  }
+  // stage st applies chains[z-1-st]; halo[st] = halo[st+1] + bw of that factor
+  int64_t h = bwA;
+  halo[z] = static_cast<int>(std::min<int64_t>(h, INT32_MAX));
+  for (int st = z - 1; st >= 0; --st)
+  {
+    h += bwF[z - 1 - st];
+    halo[st] = static_cast<int>(std::min<int64_t>(h, INT32_MAX));
+  }
+  *hmax = halo[0];
+  return h <= kMaxHalo;
+}
+
 // One sub-batch: l points (all columns m <= kMaxM).
 void cg_batch(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_csr *const *chains, int64_t n,
               int m, const double *B_dev, int64_t ldb, double rtol, int64_t maxit, double *X_dev, double *REC_dev,
@@ -728,21 +1443,17 @@ void cg_batch(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_
               double *ms_out, int64_t *loop_out)
 {
   cudaStream_t s = ctx->stream;
+  int halo[kMaxZ + 1] = {0};
+  int hmax = 0;
+  const bool banded = !ctx->force_general_cg && band_plan(ctx, l, A, z, chains, m, halo, &hmax);
   const int64_t vec = static_cast<int64_t>(l) * n * m;
   const int64_t vbytes = sizeof(double) * (vec > 0 ? vec : 1);
   DBuf b(vbytes, s), xt(vbytes, s), r(vbytes, s), d(vbytes, s), w(vbytes, s);
-  DBuf t0(z >= 1 ? vbytes : 8, s), t1(z >= 2 ? vbytes : 8, s);
-  // tile geometry depends on n only -> reduction order independent of the GPU
-  int rpt = static_cast<int>((n + static_cast<int64_t>(kCgThreads) * kMaxTiles - 1) /
-                             (static_cast<int64_t>(kCgThreads) * kMaxTiles));
-  if (rpt < 1)
-    rpt = 1;
-  const int64_t rows_per_tile = static_cast<int64_t>(rpt) * kCgThreads;
-  const int tiles = static_cast<int>((n + rows_per_tile - 1) / rows_per_tile);
-  DBuf partial(sizeof(double) * static_cast<size_t>(l) * 2 * kMaxM * tiles, s);
-  DBuf totals(sizeof(double) * 2 * static_cast<size_t>(l) * 2 * kMaxM, s);
-  DBuf counter(sizeof(unsigned int) * l, s);
-  MG_CUDA(cudaMemsetAsync(counter.ptr, 0, sizeof(unsigned int) * l, s));
+  DBuf t0(banded || z >= 1 ? vbytes : 8, s), t1(banded || z >= 2 ? vbytes : 8, s);
+  const int S = l * m;
+  DBuf d_it(sizeof(int64_t) * S, s), d_conv(sizeof(int) * S, s), d_st(sizeof(int) * S, s), d_bd(sizeof(int64_t) * S, s);
+  DBuf d_loop(sizeof(int64_t), s);
+  DBuf d_hist(hist ? sizeof(double) * static_cast<size_t>(S) * hist_cap : 8, s);
   std::vector<DCsr> hA(static_cast<size_t>(l)), hF(static_cast<size_t>(l) * (z > 0 ? z : 1));
   for (int p = 0; p < l; ++p)
   {
@@ -753,58 +1464,157 @@ void cg_batch(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_
   DBuf dA(sizeof(DCsr) * hA.size(), s), dF(sizeof(DCsr) * hF.size(), s);
   MG_CUDA(cudaMemcpyAsync(dA.ptr, hA.data(), sizeof(DCsr) * hA.size(), cudaMemcpyHostToDevice, s));
   MG_CUDA(cudaMemcpyAsync(dF.ptr, hF.data(), sizeof(DCsr) * hF.size(), cudaMemcpyHostToDevice, s));
-  const int S = l * m;
-  DBuf d_it(sizeof(int64_t) * S, s), d_conv(sizeof(int) * S, s), d_st(sizeof(int) * S, s), d_bd(sizeof(int64_t) * S, s);
-  DBuf d_loop(sizeof(int64_t), s);
-  DBuf d_hist(hist ? sizeof(double) * static_cast<size_t>(S) * hist_cap : 8, s);
 
   cg_init<<<blocks_for(vec), kThreads, 0, s>>>(l, m, n, B_dev, ldb, b.as<double>(), r.as<double>(), d.as<double>(),
                                                  xt.as<double>());
   check_launch(ctx, "cg_init");
 
-  CgParams P{};
-  P.l = l;
-  P.m = m;
-  P.z = z;
-  P.tiles = tiles;
-  P.rpt = rpt;
-  P.n = n;
-  P.rows_per_tile = rows_per_tile;
-  P.A = dA.as<DCsr>();
-  P.F = dF.as<DCsr>();
-  P.rtol = rtol;
-  P.maxit = maxit;
-  P.b = b.as<double>();
-  P.xt = xt.as<double>();
-  P.r = r.as<double>();
-  P.d = d.as<double>();
-  P.w = w.as<double>();
-  P.t0 = t0.as<double>();
-  P.t1 = t1.as<double>();
-  P.partial = partial.as<double>();
-  P.totals = totals.as<double>();
-  P.counter = counter.as<unsigned int>();
-  P.X = X_dev;
-  P.REC = REC_dev;
-  P.TR = TR_dev;
-  P.iters = d_it.as<int64_t>();
-  P.conv = d_conv.as<int>();
-  P.status = d_st.as<int>();
-  P.bd_iter = d_bd.as<int64_t>();
-  P.hist = hist ? d_hist.as<double>() : nullptr;
-  P.hist_cap = hist_cap;
-  P.loop_iters = d_loop.as<int64_t>();
-
-  MG_CUDA(cudaEventRecord(ctx->ev0, s));
-  if (m == 1)
-    launch_cg<1>(ctx, P);
-  else if (m == 2)
-    launch_cg<2>(ctx, P);
-  else if (m <= 4)
-    launch_cg<4>(ctx, P);
+  DBuf partial, totals, counter, segs, pblk;
+  if (banded)
+  {
+    partial = DBuf(sizeof(double) * static_cast<size_t>(l) * 2 * kMaxM * ctx->num_sms, s);
+    // Segment plan: with l <= #SMs every point gets its own run of blocks (no
+    // block straddles two points, so no block runs two latency chains); else
+    // blocks take whole points.  Rows split in 32-row aligned pieces.
+    const int G = ctx->num_sms;
+    std::vector<Seg> hseg(static_cast<size_t>(G) * kMaxSeg, Seg{-1, 0, 0, 0});
+    std::vector<int2> hpb(static_cast<size_t>(l));
+    if (l <= G)
+    {
+      for (int p = 0; p < l; ++p)
+      {
+        const int b0 = static_cast<int>(static_cast<int64_t>(p) * G / l);
+        const int b1 = static_cast<int>(static_cast<int64_t>(p + 1) * G / l);
+        const int nb = b1 - b0;
+        const int64_t groups = (n + 31) / 32;
+        for (int k = 0; k < nb; ++k)
+        {
+          const int64_t g0 = groups * k / nb, g1 = groups * (k + 1) / nb;
+          hseg[static_cast<size_t>(b0 + k) * kMaxSeg] =
+              Seg{p, static_cast<int>(g0 * 32), static_cast<int>(std::min<int64_t>(n, g1 * 32)), 0};
+        }
+        hpb[p] = make_int2(b0, b1);
+      }
+    }
+    else
+    {
+      for (int b = 0; b < G; ++b)
+      {
+        const int p0 = static_cast<int>(static_cast<int64_t>(b) * l / G);
+        const int p1 = static_cast<int>(static_cast<int64_t>(b + 1) * l / G);
+        if (p1 - p0 > kMaxSeg)
+          throw Error(MGPU_ERR_UNSUPPORTED, "cg: too many shifts per SM for the banded kernel");
+        for (int p = p0; p < p1; ++p)
+        {
+          hseg[static_cast<size_t>(b) * kMaxSeg + (p - p0)] = Seg{p, 0, static_cast<int>(n), 0};
+          hpb[p] = make_int2(b, b + 1);
+        }
+      }
+    }
+    segs = DBuf(sizeof(Seg) * hseg.size(), s);
+    pblk = DBuf(sizeof(int2) * hpb.size(), s);
+    MG_CUDA(cudaMemcpyAsync(segs.ptr, hseg.data(), sizeof(Seg) * hseg.size(), cudaMemcpyHostToDevice, s));
+    MG_CUDA(cudaMemcpyAsync(pblk.ptr, hpb.data(), sizeof(int2) * hpb.size(), cudaMemcpyHostToDevice, s));
+    BandParams P{};
+    P.seg = segs.as<Seg>();
+    P.pblk = pblk.as<int2>();
+    P.l = l;
+    P.m = m;
+    P.z = z;
+    P.n = n;
+    P.npad = (n + 31) / 32 * 32;
+    for (int q = 0; q <= z; ++q)
+      P.halo[q] = halo[q];
+    P.hmax = hmax;
+    P.A = dA.as<DCsr>();
+    P.F = dF.as<DCsr>();
+    P.rtol = rtol;
+    P.maxit = maxit;
+    P.b = b.as<double>();
+    P.xt = xt.as<double>();
+    P.r = r.as<double>();
+    P.dbuf0 = d.as<double>();
+    P.dbuf1 = t0.as<double>();
+    P.w = w.as<double>();
+    P.sol = t1.as<double>();
+    P.partial = partial.as<double>();
+    P.X = X_dev;
+    P.REC = REC_dev;
+    P.TR = TR_dev;
+    P.iters = d_it.as<int64_t>();
+    P.conv = d_conv.as<int>();
+    P.status = d_st.as<int>();
+    P.bd_iter = d_bd.as<int64_t>();
+    P.hist = hist ? d_hist.as<double>() : nullptr;
+    P.hist_cap = hist_cap;
+    P.loop_iters = d_loop.as<int64_t>();
+    MG_CUDA(cudaEventRecord(ctx->ev0, s));
+    if (m == 1)
+      launch_banded_rpt<1024, 1>(ctx, P);
+    else if (m == 2)
+      launch_banded_rpt<1024, 2>(ctx, P);
+    else if (m <= 4)
+      launch_banded_rpt<512, 4>(ctx, P);
+    else
+      launch_banded_rpt<512, 8>(ctx, P);
+    MG_CUDA(cudaEventRecord(ctx->ev1, s));
+  }
   else
-    launch_cg<8>(ctx, P);
-  MG_CUDA(cudaEventRecord(ctx->ev1, s));
+  {
+    // tile geometry depends on n only -> reduction order independent of the GPU
+    int rpt = static_cast<int>((n + static_cast<int64_t>(kCgThreads) * kMaxTiles - 1) /
+                               (static_cast<int64_t>(kCgThreads) * kMaxTiles));
+    if (rpt < 1)
+      rpt = 1;
+    const int64_t rows_per_tile = static_cast<int64_t>(rpt) * kCgThreads;
+    const int tiles = static_cast<int>((n + rows_per_tile - 1) / rows_per_tile);
+    partial = DBuf(sizeof(double) * static_cast<size_t>(l) * 2 * kMaxM * tiles, s);
+    totals = DBuf(sizeof(double) * 2 * static_cast<size_t>(l) * 2 * kMaxM, s);
+    counter = DBuf(sizeof(unsigned int) * l, s);
+    MG_CUDA(cudaMemsetAsync(counter.ptr, 0, sizeof(unsigned int) * l, s));
+    CgParams P{};
+    P.l = l;
+    P.m = m;
+    P.z = z;
+    P.tiles = tiles;
+    P.rpt = rpt;
+    P.n = n;
+    P.rows_per_tile = rows_per_tile;
+    P.A = dA.as<DCsr>();
+    P.F = dF.as<DCsr>();
+    P.rtol = rtol;
+    P.maxit = maxit;
+    P.b = b.as<double>();
+    P.xt = xt.as<double>();
+    P.r = r.as<double>();
+    P.d = d.as<double>();
+    P.w = w.as<double>();
+    P.t0 = t0.as<double>();
+    P.t1 = t1.as<double>();
+    P.partial = partial.as<double>();
+    P.totals = totals.as<double>();
+    P.counter = counter.as<unsigned int>();
+    P.X = X_dev;
+    P.REC = REC_dev;
+    P.TR = TR_dev;
+    P.iters = d_it.as<int64_t>();
+    P.conv = d_conv.as<int>();
+    P.status = d_st.as<int>();
+    P.bd_iter = d_bd.as<int64_t>();
+    P.hist = hist ? d_hist.as<double>() : nullptr;
+    P.hist_cap = hist_cap;
+    P.loop_iters = d_loop.as<int64_t>();
+    MG_CUDA(cudaEventRecord(ctx->ev0, s));
+    if (m == 1)
+      launch_cg<1>(ctx, P);
+    else if (m == 2)
+      launch_cg<2>(ctx, P);
+    else if (m <= 4)
+      launch_cg<4>(ctx, P);
+    else
+      launch_cg<8>(ctx, P);
+    MG_CUDA(cudaEventRecord(ctx->ev1, s));
+  }
 
   MG_CUDA(cudaMemcpyAsync(iters, d_it.ptr, sizeof(int64_t) * S, cudaMemcpyDeviceToHost, s));
   MG_CUDA(cudaMemcpyAsync(conv, d_conv.ptr, sizeof(int) * S, cudaMemcpyDeviceToHost, s));
@@ -820,6 +1630,7 @@ void cg_batch(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_
   MG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
   *ms_out += ms;
   *loop_out += loop;
+  ctx->last_cg_banded = banded;
 }
 
 } // namespace

@@ -1,4 +1,5 @@
 // Context, error state, CSR residency and the deterministic reduction.
+#include <climits>
 #include <cstring>
 #include <vector>
 
@@ -86,6 +87,25 @@ __global__ void validate_csr(int64_t nrows, int64_t ncols, int64_t nnz, const in
   }
   if (bad)
     atomicOr(flag, 1);
+  else if (e > b)
+  {
+    const int64_t w = max(i - static_cast<int64_t>(ci[b]), static_cast<int64_t>(ci[e - 1]) - i);
+    atomicMax(flag + 1, static_cast<int>(w > INT32_MAX ? INT32_MAX : w));
+  }
+}
+
+__global__ void bandwidth_rows(int64_t nrows, const int64_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                               int *bw)
+{
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nrows)
+    return;
+  const int64_t b = rp[i], e = rp[i + 1];
+  if (e > b)
+  {
+    const int64_t w = max(i - static_cast<int64_t>(ci[b]), static_cast<int64_t>(ci[e - 1]) - i);
+    atomicMax(bw, static_cast<int>(w > INT32_MAX ? INT32_MAX : w));
+  }
 }
 
 void upload_common(mgpu_ctx *ctx, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t *row_ptr,
@@ -107,16 +127,17 @@ void upload_common(mgpu_ctx *ctx, int64_t nrows, int64_t ncols, int64_t nnz, con
     }
     if (nrows > 0)
     {
-      DBuf flag(sizeof(int), ctx->stream);
-      MG_CUDA(cudaMemsetAsync(flag.ptr, 0, sizeof(int), ctx->stream));
+      DBuf flag(2 * sizeof(int), ctx->stream);
+      MG_CUDA(cudaMemsetAsync(flag.ptr, 0, 2 * sizeof(int), ctx->stream));
       validate_csr<<<blocks_for(nrows), kThreads, 0, ctx->stream>>>(nrows, ncols, nnz, a->row_ptr, a->col_idx,
                                                                     flag.as<int>());
       check_launch(ctx, "validate_csr");
-      int h = 0;
-      MG_CUDA(cudaMemcpyAsync(&h, flag.ptr, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      int h[2] = {0, 0};
+      MG_CUDA(cudaMemcpyAsync(h, flag.ptr, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
       MG_CUDA(cudaStreamSynchronize(ctx->stream));
-      if (h != 0)
+      if (h[0] != 0)
         throw Error(MGPU_ERR_ARG, "SparseMatrix: inconsistent CSR arrays");
+      a->bw = h[1];
     }
   }
   catch (...)
@@ -140,6 +161,24 @@ __global__ void count_nonzero_rows(int64_t nrows, const int64_t *__restrict__ rp
 }
 
 } // namespace
+
+int64_t csr_bandwidth(mgpu_ctx *ctx, mgpu_csr *A)
+{
+  if (A->bw >= 0)
+    return A->bw;
+  int h = 0;
+  if (A->nrows > 0 && A->nnz > 0)
+  {
+    DBuf bw(sizeof(int), ctx->stream);
+    MG_CUDA(cudaMemsetAsync(bw.ptr, 0, sizeof(int), ctx->stream));
+    bandwidth_rows<<<blocks_for(A->nrows), kThreads, 0, ctx->stream>>>(A->nrows, A->row_ptr, A->col_idx, bw.as<int>());
+    check_launch(ctx, "bandwidth_rows");
+    MG_CUDA(cudaMemcpyAsync(&h, bw.ptr, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    MG_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  A->bw = h;
+  return h;
+}
 
 void det_sum(mgpu_ctx *ctx, const double *vals, int64_t count, double *out_dev)
 {
@@ -258,6 +297,16 @@ const char *mgpu_status_string(int status)
 }
 
 int64_t mgpu_launch_count(const mgpu_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+int mgpu_ctx_set_cg_path(mgpu_ctx *ctx, int path)
+{
+  if (ctx == nullptr || path < 0 || path > 1)
+    return MGPU_ERR_ARG;
+  ctx->force_general_cg = path == 1;
+  return MGPU_OK;
+}
+
+int mgpu_last_cg_path(const mgpu_ctx *ctx) { return ctx && ctx->last_cg_banded ? 0 : 1; }
 
 int mgpu_last_cg_timing(const mgpu_ctx *ctx, double *ms, int64_t *iterations)
 {

@@ -526,6 +526,10 @@ mgpu_csr *spai_ls_one(mgpu_ctx *ctx, const mgpu_csr *A, const mgpu_csr *K_old, i
   }
   mgpu_csr *P = transpose_csr(ctx, PT);
   P->may_hold_zeros = true;
+  {
+    const int64_t ba = csr_bandwidth(ctx, const_cast<mgpu_csr *>(A));
+    P->bw = pattern == MGPU_PATTERN_A2 ? 2 * ba : ba; // J pattern bound (A*A at most doubles it)
+  }
   mgpu_csr_free(PT);
   mgpu_csr_free(At);
   mgpu_csr_free(Kot);

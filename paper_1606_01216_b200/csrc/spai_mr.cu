@@ -75,6 +75,7 @@ struct MrArgs
   double alpha, tol_sq;
   int64_t max_iters;
   int bl, bu; // K's lower / upper bandwidth
+  int *bw;               // pass 1: bandwidth bound of the factor
   int64_t *count;        // pass 1: nonzeros of column j
   double *residual;      // pass 1: final ||r|| (or ||r|| at failure)
   int64_t *fail_iters;   // pass 1: iterations at failure
@@ -237,6 +238,7 @@ __global__ void __launch_bounds__(kMrWarps * 32) mr_columns(MrArgs a)
     {
       a.count[j] = cnt;
       a.residual[j] = sqrt(rnorm_sq);
+      atomicMax(a.bw, static_cast<int>(max(j - plo, phi - j)));
     }
     return;
   }
@@ -280,7 +282,8 @@ mgpu_csr *mr_build(mgpu_ctx *ctx, const mgpu_csr *K, const mgpu_csr *rhs_src, do
     MG_CUDA(cudaMemcpyAsync(hbw, bw.ptr, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
   }
   DBuf count(sizeof(int64_t) * (n + 1), s), resid(sizeof(double) * (n > 0 ? n : 1), s),
-      fit(sizeof(int64_t) * (n > 0 ? n : 1), s), err(sizeof(unsigned long long), s);
+      fit(sizeof(int64_t) * (n > 0 ? n : 1), s), err(sizeof(unsigned long long), s), pbw(sizeof(int), s);
+  MG_CUDA(cudaMemsetAsync(pbw.ptr, 0, sizeof(int), s));
   MG_CUDA(cudaMemsetAsync(err.ptr, 0xff, sizeof(unsigned long long), s));
   MG_CUDA(cudaMemsetAsync(count.ptr, 0, sizeof(int64_t) * (n + 1), s));
   MG_CUDA(cudaStreamSynchronize(s));
@@ -295,6 +298,7 @@ mgpu_csr *mr_build(mgpu_ctx *ctx, const mgpu_csr *K, const mgpu_csr *rhs_src, do
   a.bl = hbw[0];
   a.bu = hbw[1];
   a.count = count.as<int64_t>() + 1;
+  a.bw = pbw.as<int>();
   a.residual = resid.as<double>();
   a.fail_iters = fit.as<int64_t>();
   a.err = err.as<unsigned long long>();
@@ -357,9 +361,12 @@ mgpu_csr *mr_build(mgpu_ctx *ctx, const mgpu_csr *K, const mgpu_csr *rhs_src, do
       count_launch(ctx);
     }
     int64_t nnz = 0;
+    int hpbw = 0;
     MG_CUDA(cudaMemcpyAsync(&nnz, PT->row_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    MG_CUDA(cudaMemcpyAsync(&hpbw, pbw.ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
     MG_CUDA(cudaStreamSynchronize(s));
     PT->nnz = nnz;
+    PT->bw = hpbw;
     MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&PT->col_idx), sizeof(int32_t) * (nnz > 0 ? nnz : 1), s));
     MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&PT->values), sizeof(double) * (nnz > 0 ? nnz : 1), s));
     a.offset = PT->row_ptr;

@@ -23,7 +23,7 @@ namespace
 // the intermediate md row (sparse.cpp:209).  Emits when out_ci != nullptr.
 template <bool kThird>
 __device__ __forceinline__ int64_t merge_row(int64_t i, DCsr A, DCsr B, DCsr Cm, double a, double b, int32_t *out_ci,
-                                             double *out_v)
+                                             double *out_v, int32_t *lohi = nullptr)
 {
   int64_t ka = A.rp[i], ea = A.rp[i + 1];
   int64_t kb = B.rp[i], eb = B.rp[i + 1];
@@ -86,6 +86,11 @@ __device__ __forceinline__ int64_t merge_row(int64_t i, DCsr A, DCsr B, DCsr Cm,
     }
     if (emit)
     {
+      if (lohi)
+      {
+        lohi[0] = min(lohi[0], col);
+        lohi[1] = max(lohi[1], col);
+      }
       if (out_ci)
       {
         out_ci[cnt] = col;
@@ -99,6 +104,7 @@ __device__ __forceinline__ int64_t merge_row(int64_t i, DCsr A, DCsr B, DCsr Cm,
 
 struct ShiftArgs
 {
+  int *bw; // [64] bandwidth of each output (atomicMax in the count pass)
   double a[64];
   double b[64];
   int64_t *rp[64];
@@ -114,7 +120,11 @@ __global__ void add_count_kernel(int l, int64_t n, DCsr A, DCsr B, DCsr Cm, Shif
     return;
   const int p = static_cast<int>(g / n);
   const int64_t i = g - static_cast<int64_t>(p) * n;
-  args.rp[p][i + 1] = merge_row<kThird>(i, A, B, Cm, args.a[p], args.b[p], nullptr, nullptr);
+  int32_t lohi[2] = {INT_MAX, -1};
+  const int64_t cnt = merge_row<kThird>(i, A, B, Cm, args.a[p], args.b[p], nullptr, nullptr, lohi);
+  args.rp[p][i + 1] = cnt;
+  if (cnt > 0)
+    atomicMax(&args.bw[p], static_cast<int>(max(i - lohi[0], static_cast<int64_t>(lohi[1]) - i)));
   if (i == 0)
     args.rp[p][0] = 0;
 }
@@ -168,6 +178,9 @@ void batched_add(mgpu_ctx *ctx, const mgpu_csr *A, const mgpu_csr *B, const mgpu
     }
     const DCsr cv = kThird ? Cm->view() : DCsr{nullptr, nullptr, nullptr};
     const int64_t total = static_cast<int64_t>(cnt) * n;
+    DBuf bwbuf(sizeof(int) * 64, ctx->stream);
+    MG_CUDA(cudaMemsetAsync(bwbuf.ptr, 0, sizeof(int) * 64, ctx->stream));
+    args.bw = bwbuf.as<int>();
     if (n > 0)
     {
       add_count_kernel<kThird><<<blocks_for(total), kThreads, 0, ctx->stream>>>(cnt, n, A->view(), B->view(), cv, args);
@@ -179,12 +192,16 @@ void batched_add(mgpu_ctx *ctx, const mgpu_csr *A, const mgpu_csr *B, const mgpu
         MG_CUDA(cudaMemsetAsync(args.rp[p], 0, sizeof(int64_t), ctx->stream));
     }
     std::vector<int64_t> nnz(static_cast<size_t>(cnt), 0);
+    int hbw[64] = {0};
     for (int p = 0; p < cnt; ++p)
     {
       scan_row_ptr(ctx, args.rp[p], n);
       MG_CUDA(cudaMemcpyAsync(&nnz[p], args.rp[p] + n, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
     }
+    MG_CUDA(cudaMemcpyAsync(hbw, bwbuf.ptr, sizeof(int) * 64, cudaMemcpyDeviceToHost, ctx->stream));
     MG_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int p = 0; p < cnt; ++p)
+      made[p]->bw = hbw[p];
     for (int p = 0; p < cnt; ++p)
     {
       mgpu_csr *o = made[p];
@@ -279,6 +296,7 @@ mgpu_csr *transpose_csr(mgpu_ctx *ctx, const mgpu_csr *A)
 {
   mgpu_csr *T = new_csr(ctx, A->ncols, A->nrows, A->nnz);
   T->may_hold_zeros = A->may_hold_zeros;
+  T->bw = A->bw; // max |i - j| is transpose invariant
   MG_CUDA(cudaMemsetAsync(T->row_ptr, 0, sizeof(int64_t) * (A->ncols + 1), ctx->stream));
   if (A->nnz == 0)
     return T;

@@ -141,6 +141,8 @@ extern "C" int mgpu_spgemm(mgpu_ctx *ctx, const mgpu_csr *A, const mgpu_csr *B, 
       spgemm_fill<<<blocks_for(n), kThreads, 0, s>>>(n, A->view(), B->view(), out->row_ptr, out->col_idx, out->values);
       check_launch(ctx, "spgemm_fill");
     }
+    if (A->bw >= 0 && B->bw >= 0)
+      out->bw = A->bw + B->bw;
     *C = out;
   });
 }

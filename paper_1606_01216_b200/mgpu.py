@@ -26,7 +26,7 @@ PATTERN_A, PATTERN_A2 = 0, 1
 # Symbols include/mgpu.h declares; tests check the library exports all of them.
 EXPORTED = [
     "mgpu_ctx_create", "mgpu_ctx_destroy", "mgpu_ctx_synchronize", "mgpu_last_error", "mgpu_status_string",
-    "mgpu_launch_count", "mgpu_last_cg_timing", "mgpu_csr_upload", "mgpu_csr_upload_device", "mgpu_csr_info",
+    "mgpu_launch_count", "mgpu_last_cg_timing", "mgpu_ctx_set_cg_path", "mgpu_last_cg_path", "mgpu_csr_upload", "mgpu_csr_upload_device", "mgpu_csr_info",
     "mgpu_csr_download", "mgpu_csr_device_view", "mgpu_csr_free", "mgpu_sp_add_scaled", "mgpu_shifted_operators",
     "mgpu_transpose", "mgpu_trace", "mgpu_trace_inner", "mgpu_spmv", "mgpu_chain_apply", "mgpu_spai_build",
     "mgpu_spai_update", "mgpu_spai_ls", "mgpu_spai_ls_batched", "mgpu_spgemm", "mgpu_cg_solve",
@@ -112,6 +112,8 @@ def lib():
         L.mgpu_launch_count.argtypes = [vp]
         L.mgpu_launch_count.restype = i64
         L.mgpu_last_cg_timing.argtypes = [vp, C.POINTER(dbl), C.POINTER(i64)]
+        L.mgpu_ctx_set_cg_path.argtypes = [vp, C.c_int]
+        L.mgpu_last_cg_path.argtypes = [vp]
         L.mgpu_csr_upload.argtypes = [vp, i64, i64, i64, vp, vp, vp, C.POINTER(vp)]
         L.mgpu_csr_upload_device.argtypes = [vp, i64, i64, i64, vp, vp, vp, C.POINTER(vp)]
         L.mgpu_csr_info.argtypes = [vp, vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]
@@ -232,6 +234,14 @@ class Context:
     @property
     def launches(self) -> int:
         return int(lib().mgpu_launch_count(self.handle))
+
+    def set_cg_path(self, path: str):
+        """'auto' (fused banded kernel when bandwidths allow) or 'general'."""
+        self.check(lib().mgpu_ctx_set_cg_path(self.handle, 1 if path == "general" else 0))
+
+    @property
+    def last_cg_path(self) -> str:
+        return "banded" if lib().mgpu_last_cg_path(self.handle) == 0 else "general"
 
     def last_cg_timing(self):
         ms, it = C.c_double(), C.c_int64()

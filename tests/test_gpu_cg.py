@@ -13,6 +13,35 @@ from conftest import rel
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True, params=["auto", "general"])
+def cg_path(request, mg):
+    """Every parity case runs through the fused banded kernel AND the general kernel."""
+    ctx = mg.default_context()
+    ctx.set_cg_path(request.param)
+    yield request.param
+    ctx.set_cg_path("auto")
+
+
+def test_path_selection(mg, oracle, cg_path):
+    M, D, K = oracle.hermite_generate(300)
+    A = oracle.shifted_operator(M, D, K, 100.0)
+    P = oracle.spai_ls(A, None, 1)
+    mg.pcg_solve(A, [P], np.ones(600), maxit=5)
+    assert mg.default_context().last_cg_path == ("banded" if cg_path == "auto" else "general")
+    # a wide operator (bandwidth > 64) always takes the general kernel
+    from oracle import Csr
+    rng = np.random.default_rng(9)
+    W = np.eye(300) * 4.0
+    for _ in range(40):
+        i, j = rng.integers(0, 300, 2)
+        if abs(i - j) > 70:
+            W[i, j] = W[j, i] = 0.01
+    want = oracle.pcg_solve(Csr.from_dense(W), [], np.ones(300))
+    got = mg.pcg_solve(Csr.from_dense(W), [], np.ones(300))
+    assert mg.default_context().last_cg_path == "general"
+    assert rel(got["solution"], want["solution"]) < 1e-12
+
+
 def _check(got, want, b=None, tol=1e-8, it_tol=2):
     assert abs(got["iterations"] - want["iterations"]) <= it_tol, (got["iterations"], want["iterations"])
     assert got["converged"] == want["converged"]
