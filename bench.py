@@ -263,6 +263,7 @@ def run_mgpu(args, rank, world, local_rank):
         e3.record(stream)
         if record is not None:
             cg_ms, loops = ctx.last_cg_timing()
+            record_path = ctx.last_cg_path
             bytes_iter = sum(8 * o.stored_nnz + 8 * f.matrix.stored_nnz + 48 * n * m for o, f in zip(ops, facs))
             record.append(dict(ev=(e0, e1, e2, e3), cg_ms=cg_ms, loops=loops, bytes=bytes_iter * loops,
                                iters=int(it.max()), breakdowns=int((st != 0).sum())))
@@ -364,7 +365,7 @@ def run_mgpu(args, rank, world, local_rank):
             "step_ms_min_med_max": [min(step_ms), statistics.median(step_ms), max(step_ms)],
             "spai_build_ms": statistics.median(spai_ms), "assemble_ms": statistics.median(asm_ms),
             "cg_ms": statistics.median(cg_ms), "cg_us_per_iteration": 1e3 * statistics.median(cg_ms) / max(loops, 1),
-            "cg_iterations": loops, "breakdowns": recs[-1]["breakdowns"],
+            "cg_iterations": loops, "breakdowns": recs[-1]["breakdowns"], "cg_kernel": ctx.last_cg_path,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "peak_source": peak_kind, "kernel": "cg_persistent",
                          "bytes_model": "per iteration, per shift: 8 nnz(A) + 8 nnz(P) + 48 n m"},

@@ -78,11 +78,13 @@ int64_t mgpu_launch_count(const mgpu_ctx *ctx);
  * mgpu_cg_solve* kernel region and the number of CG iterations it ran. */
 int mgpu_last_cg_timing(const mgpu_ctx *ctx, double *ms, int64_t *iterations);
 
-/* CG kernel selection: 0 = automatic (the fused banded kernel, 2 grid
- * barriers per iteration, when every operator and factor has bandwidth
- * <= 64 and chains have <= 8 factors; otherwise the general CSR kernel),
- * 1 = always the general kernel.  mgpu_last_cg_path reports 0 (banded) or
- * 1 (general) for the last solve. */
+/* CG kernel selection.  0 = automatic: when every operator and factor has
+ * bandwidth <= 64 and chains have <= 8 factors, the cluster-resident kernel
+ * (one thread-block cluster per shifted system, operators in shared memory)
+ * if the systems fit on chip, else the fused banded grid kernel (2 grid
+ * barriers per iteration); otherwise the general CSR kernel.
+ * 1 = always the general kernel, 2 = the banded grid kernel (no cluster).
+ * mgpu_last_cg_path reports 2 (cluster), 0 (banded grid) or 1 (general). */
 int mgpu_ctx_set_cg_path(mgpu_ctx *ctx, int path);
 int mgpu_last_cg_path(const mgpu_ctx *ctx);
 

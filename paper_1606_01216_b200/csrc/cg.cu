@@ -27,6 +27,12 @@ namespace cgrp = cooperative_groups;
 
 namespace mgpu
 {
+bool cg_cluster_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_csr *const *chains,
+                      int64_t n, int m, const double *B_dev, int64_t ldb, const int *halo, double rtol,
+                      int64_t maxit, double *X, double *REC, double *TR, int64_t *d_it, int *d_conv, int *d_st,
+                      int64_t *d_bd, double *d_hist, int64_t hist_cap, unsigned long long *d_loop, const DCsr *dA,
+                      const DCsr *dF);
+
 namespace
 {
 
@@ -1445,7 +1451,7 @@ void cg_batch(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_
   cudaStream_t s = ctx->stream;
   int halo[kMaxZ + 1] = {0};
   int hmax = 0;
-  const bool banded = !ctx->force_general_cg && band_plan(ctx, l, A, z, chains, m, halo, &hmax);
+  const bool banded = ctx->cg_path != 1 && band_plan(ctx, l, A, z, chains, m, halo, &hmax);
   const int64_t vec = static_cast<int64_t>(l) * n * m;
   const int64_t vbytes = sizeof(double) * (vec > 0 ? vec : 1);
   DBuf b(vbytes, s), xt(vbytes, s), r(vbytes, s), d(vbytes, s), w(vbytes, s);
@@ -1465,12 +1471,30 @@ void cg_batch(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_
   MG_CUDA(cudaMemcpyAsync(dA.ptr, hA.data(), sizeof(DCsr) * hA.size(), cudaMemcpyHostToDevice, s));
   MG_CUDA(cudaMemcpyAsync(dF.ptr, hF.data(), sizeof(DCsr) * hF.size(), cudaMemcpyHostToDevice, s));
 
-  cg_init<<<blocks_for(vec), kThreads, 0, s>>>(l, m, n, B_dev, ldb, b.as<double>(), r.as<double>(), d.as<double>(),
-                                                 xt.as<double>());
-  check_launch(ctx, "cg_init");
-
   DBuf partial, totals, counter, segs, pblk;
-  if (banded)
+  bool clustered = false;
+  if (banded && ctx->cg_path != 2)
+  {
+    // systems small enough to live on chip: one cluster per point, no grid barrier
+    MG_CUDA(cudaMemsetAsync(d_loop.ptr, 0, sizeof(int64_t), s));
+    MG_CUDA(cudaEventRecord(ctx->ev0, s));
+    clustered = cg_cluster_solve(ctx, l, A, z, chains, n, m, B_dev, ldb, halo, rtol, maxit, X_dev, REC_dev, TR_dev,
+                                 d_it.as<int64_t>(), d_conv.as<int>(), d_st.as<int>(), d_bd.as<int64_t>(),
+                                 hist ? d_hist.as<double>() : nullptr, hist_cap,
+                                 reinterpret_cast<unsigned long long *>(d_loop.ptr), dA.as<DCsr>(), dF.as<DCsr>());
+    if (clustered)
+      MG_CUDA(cudaEventRecord(ctx->ev1, s));
+  }
+  if (!clustered)
+  {
+    cg_init<<<blocks_for(vec), kThreads, 0, s>>>(l, m, n, B_dev, ldb, b.as<double>(), r.as<double>(), d.as<double>(),
+                                                   xt.as<double>());
+    check_launch(ctx, "cg_init");
+  }
+  if (clustered)
+  {
+  }
+  else if (banded)
   {
     partial = DBuf(sizeof(double) * static_cast<size_t>(l) * 2 * kMaxM * ctx->num_sms, s);
     // Segment plan: with l <= #SMs every point gets its own run of blocks (no
@@ -1630,7 +1654,7 @@ void cg_batch(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_
   MG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
   *ms_out += ms;
   *loop_out += loop;
-  ctx->last_cg_banded = banded;
+  ctx->last_cg_path = clustered ? 2 : (banded ? 0 : 1);
 }
 
 } // namespace

@@ -162,6 +162,34 @@ __global__ void count_nonzero_rows(int64_t nrows, const int64_t *__restrict__ rp
 
 } // namespace
 
+namespace
+{
+__global__ void max_row_kernel(int64_t nrows, const int64_t *__restrict__ rp, int *out)
+{
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < nrows)
+    atomicMax(out, static_cast<int>(rp[i + 1] - rp[i]));
+}
+} // namespace
+
+int64_t csr_max_row(mgpu_ctx *ctx, mgpu_csr *A)
+{
+  if (A->maxrow >= 0)
+    return A->maxrow;
+  int h = 0;
+  if (A->nrows > 0)
+  {
+    DBuf mx(sizeof(int), ctx->stream);
+    MG_CUDA(cudaMemsetAsync(mx.ptr, 0, sizeof(int), ctx->stream));
+    max_row_kernel<<<blocks_for(A->nrows), kThreads, 0, ctx->stream>>>(A->nrows, A->row_ptr, mx.as<int>());
+    check_launch(ctx, "max_row_kernel");
+    MG_CUDA(cudaMemcpyAsync(&h, mx.ptr, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    MG_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  A->maxrow = h;
+  return h;
+}
+
 int64_t csr_bandwidth(mgpu_ctx *ctx, mgpu_csr *A)
 {
   if (A->bw >= 0)
@@ -300,13 +328,13 @@ int64_t mgpu_launch_count(const mgpu_ctx *ctx) { return ctx ? ctx->launches : 0;
 
 int mgpu_ctx_set_cg_path(mgpu_ctx *ctx, int path)
 {
-  if (ctx == nullptr || path < 0 || path > 1)
+  if (ctx == nullptr || path < 0 || path > 2)
     return MGPU_ERR_ARG;
-  ctx->force_general_cg = path == 1;
+  ctx->cg_path = path;
   return MGPU_OK;
 }
 
-int mgpu_last_cg_path(const mgpu_ctx *ctx) { return ctx && ctx->last_cg_banded ? 0 : 1; }
+int mgpu_last_cg_path(const mgpu_ctx *ctx) { return ctx ? ctx->last_cg_path : -1; }
 
 int mgpu_last_cg_timing(const mgpu_ctx *ctx, double *ms, int64_t *iterations)
 {

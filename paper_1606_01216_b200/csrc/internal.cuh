@@ -108,8 +108,8 @@ struct mgpu_ctx
   int64_t launches = 0;
   double last_cg_ms = 0.0;
   int64_t last_cg_iters = 0;
-  bool last_cg_banded = false;
-  bool force_general_cg = false; // test hook: route CG through the general (unfused) kernel
+  int last_cg_path = 1; // 0 banded (grid), 1 general, 2 cluster-resident
+  int cg_path = 0;      // 0 auto, 1 force general, 2 force banded grid kernel (no cluster)
   // last error
   int last_status = MGPU_OK;
   int64_t err_index = -1, err_col = -1, err_point = -1;
@@ -125,6 +125,7 @@ struct mgpu_csr
   double *values = nullptr;
   bool may_hold_zeros = false; // fixed-pattern factors (LS-SPAI) may store exact zeros
   int64_t bw = -1;              // upper bound of max |i - j| over stored entries (-1: unknown)
+  int64_t maxrow = -1;          // longest row (-1: unknown)
 
   mgpu::DCsr view() const { return {row_ptr, col_idx, values}; }
 };
@@ -146,6 +147,8 @@ inline void check_launch(mgpu_ctx *ctx, const char *name)
 mgpu_csr *new_csr(mgpu_ctx *ctx, int64_t nrows, int64_t ncols, int64_t nnz);
 // Bandwidth bound of A (computed once with a reduction kernel when unknown).
 int64_t csr_bandwidth(mgpu_ctx *ctx, mgpu_csr *A);
+// Longest row of A (cached).
+int64_t csr_max_row(mgpu_ctx *ctx, mgpu_csr *A);
 void set_error(mgpu_ctx *ctx, const Error &e);
 
 // Deterministic fixed-shape sum of `count` doubles on the device (two-level,

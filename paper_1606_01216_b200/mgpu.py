@@ -236,12 +236,12 @@ class Context:
         return int(lib().mgpu_launch_count(self.handle))
 
     def set_cg_path(self, path: str):
-        """'auto' (fused banded kernel when bandwidths allow) or 'general'."""
-        self.check(lib().mgpu_ctx_set_cg_path(self.handle, 1 if path == "general" else 0))
+        """'auto' (cluster / banded / general by shape), 'general' or 'banded' (grid kernel, no cluster)."""
+        self.check(lib().mgpu_ctx_set_cg_path(self.handle, {"auto": 0, "general": 1, "banded": 2}[path]))
 
     @property
     def last_cg_path(self) -> str:
-        return "banded" if lib().mgpu_last_cg_path(self.handle) == 0 else "general"
+        return {0: "banded", 1: "general", 2: "cluster"}.get(lib().mgpu_last_cg_path(self.handle), "?")
 
     def last_cg_timing(self):
         ms, it = C.c_double(), C.c_int64()

@@ -13,9 +13,10 @@ from conftest import rel
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True, params=["auto", "general"])
+@pytest.fixture(autouse=True, params=["auto", "banded", "general"])
 def cg_path(request, mg):
-    """Every parity case runs through the fused banded kernel AND the general kernel."""
+    """Every parity case runs through all three CG kernels: cluster-resident (auto on
+    these on-chip sizes), the banded grid kernel and the general CSR kernel."""
     ctx = mg.default_context()
     ctx.set_cg_path(request.param)
     yield request.param
@@ -27,7 +28,8 @@ def test_path_selection(mg, oracle, cg_path):
     A = oracle.shifted_operator(M, D, K, 100.0)
     P = oracle.spai_ls(A, None, 1)
     mg.pcg_solve(A, [P], np.ones(600), maxit=5)
-    assert mg.default_context().last_cg_path == ("banded" if cg_path == "auto" else "general")
+    assert mg.default_context().last_cg_path == {"auto": "cluster", "banded": "banded",
+                                                  "general": "general"}[cg_path]
     # a wide operator (bandwidth > 64) always takes the general kernel
     from oracle import Csr
     rng = np.random.default_rng(9)
