@@ -17,6 +17,7 @@
 // storage (dropped on download), so the pattern is reusable across shifts.
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <climits>
 #include <vector>
 
@@ -25,6 +26,8 @@
 namespace mgpu
 {
 mgpu_csr *transpose_csr(mgpu_ctx *ctx, const mgpu_csr *A);
+mgpu_csr *transpose_perm(mgpu_ctx *ctx, const mgpu_csr *A, DBuf &perm);
+void gather_dev(mgpu_ctx *ctx, int64_t nnz, const int64_t *perm, const double *src, double *dst);
 
 namespace
 {
@@ -144,8 +147,12 @@ __device__ __forceinline__ void report(unsigned long long *err, int64_t j, int s
   atomicMin(err, (static_cast<unsigned long long>(j) << 8) | static_cast<unsigned long long>(status));
 }
 
+// Batched over l operators sharing one pattern: column g = p * n + j reads
+// A_p through At (shared structure, values at At.v + p * at_stride), K_old_p
+// likewise, and writes P_p^T values at out_vals + p * out_stride.
 template <int G, int NI>
-__global__ void ls_columns(int64_t n, DCsr pat, DCsr At, DCsr Kot, bool update, double *__restrict__ out_vals,
+__global__ void ls_columns(int64_t n, int l, DCsr pat, DCsr At, int64_t at_stride, DCsr Kot, int64_t ko_stride,
+                           bool update, double *__restrict__ out_base, int64_t out_stride,
                            unsigned long long *__restrict__ err, int *__restrict__ overflow)
 {
   extern __shared__ __align__(16) unsigned char ls_raw[];
@@ -154,9 +161,15 @@ __global__ void ls_columns(int64_t n, DCsr pat, DCsr At, DCsr Kot, bool update, 
   const int grp = lane / G, c = lane % G;
   const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
   auto &sm = reinterpret_cast<LsGroupSmem<G, NI> *>(ls_raw)[warp * kGroups + grp];
-  const int64_t j = (static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + warp) * kGroups + grp;
-  if (j >= n)
+  const int64_t g = (static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + warp) * kGroups + grp;
+  if (g >= static_cast<int64_t>(l) * n)
     return;
+  const int p = static_cast<int>(g / n);
+  const int64_t j = g - static_cast<int64_t>(p) * n;
+  At.v += p * at_stride;
+  if (update)
+    Kot.v += p * ko_stride;
+  double *out_vals = out_base + p * out_stride;
   const int64_t jb = pat.rp[j];
   const int nj = static_cast<int>(pat.rp[j + 1] - jb);
   if (nj == 0)
@@ -208,7 +221,7 @@ __global__ void ls_columns(int64_t n, DCsr pat, DCsr At, DCsr Kot, bool update, 
   if (sm.fail == 1)
   {
     if (c == 0)
-      report(err, j, MGPU_ERR_NUMERICAL);
+      report(err, g, MGPU_ERR_NUMERICAL);
     return;
   }
   const int ni = sm.ni;
@@ -317,7 +330,7 @@ __global__ void ls_columns(int64_t n, DCsr pat, DCsr At, DCsr Kot, bool update, 
   if (deficient) // rank < |J|
   {
     if (c == 0)
-      report(err, j, MGPU_ERR_NUMERICAL);
+      report(err, g, MGPU_ERR_NUMERICAL);
     return;
   }
   // ---- Q = H_0 ... H_{nj-1} E, lane c forms column c
@@ -385,32 +398,105 @@ __global__ void ls_columns(int64_t n, DCsr pat, DCsr At, DCsr Kot, bool update, 
 }
 
 template <int G, int NI, int WARPS>
-void launch_ls(mgpu_ctx *ctx, int64_t n, DCsr pat, DCsr At, DCsr Kot, bool update, double *out,
-               unsigned long long *err, int *ovf)
+void launch_ls(mgpu_ctx *ctx, int64_t n, int l, DCsr pat, DCsr At, int64_t at_stride, DCsr Kot, int64_t ko_stride,
+               bool update, double *out, int64_t out_stride, unsigned long long *err, int *ovf)
 {
   constexpr int per_block = WARPS * (32 / G);
   constexpr size_t smem = sizeof(LsGroupSmem<G, NI>) * per_block;
   static_assert(smem <= 48 * 1024, "LS group shared memory");
-  const unsigned grid = static_cast<unsigned>((n + per_block - 1) / per_block);
-  ls_columns<G, NI><<<grid, WARPS * 32, smem, ctx->stream>>>(n, pat, At, Kot, update, out, err, ovf);
+  const int64_t cols = static_cast<int64_t>(l) * n;
+  const unsigned grid = static_cast<unsigned>((cols + per_block - 1) / per_block);
+  ls_columns<G, NI><<<grid, WARPS * 32, smem, ctx->stream>>>(n, l, pat, At, at_stride, Kot, ko_stride, update, out,
+                                                             out_stride, err, ovf);
   check_launch(ctx, "ls_columns");
 }
 
-void check_err(mgpu_ctx *ctx, unsigned long long *err_dev)
+// Runs the LS columns with the smallest lane-group envelope that holds every
+// column; throws the lowest failing (point, column) like the reference's
+// sequential column loop would.
+void run_ls(mgpu_ctx *ctx, int64_t n, int l, int maxrow, DCsr pat, DCsr At, int64_t at_stride, DCsr Kot,
+            int64_t ko_stride, bool update, double *out, int64_t out_stride)
 {
-  unsigned long long h = 0;
-  MG_CUDA(cudaMemcpyAsync(&h, err_dev, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
-  MG_CUDA(cudaStreamSynchronize(ctx->stream));
-  if (h == ULLONG_MAX)
+  if (n == 0 || l == 0)
     return;
-  const int64_t col = static_cast<int64_t>(h >> 8);
-  const int st = static_cast<int>(h & 0xff);
-  if (st == MGPU_ERR_NUMERICAL)
-    throw Error(st, "spai_ls: rank-deficient least-squares problem in column " + std::to_string(col), col);
-  throw Error(MGPU_ERR_UNSUPPORTED, "spai_ls: column " + std::to_string(col) + " outside the device envelope", col);
+  DBuf err(sizeof(unsigned long long), ctx->stream), ovf(sizeof(int), ctx->stream);
+  for (int cfg = 0; cfg < 3; ++cfg)
+  {
+    const int G = cfg == 0 ? 8 : (cfg == 1 ? 16 : 32);
+    if (maxrow > G)
+      continue;
+    MG_CUDA(cudaMemsetAsync(err.ptr, 0xff, sizeof(unsigned long long), ctx->stream));
+    MG_CUDA(cudaMemsetAsync(ovf.ptr, 0, sizeof(int), ctx->stream));
+    auto *ev = err.as<unsigned long long>();
+    if (cfg == 0)
+      launch_ls<8, 16, 4>(ctx, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev, ovf.as<int>());
+    else if (cfg == 1)
+      launch_ls<16, 32, 2>(ctx, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev, ovf.as<int>());
+    else
+      launch_ls<32, 64, 1>(ctx, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev, ovf.as<int>());
+    unsigned long long h = 0;
+    int h_ovf = 0;
+    MG_CUDA(cudaMemcpyAsync(&h_ovf, ovf.ptr, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    MG_CUDA(cudaMemcpyAsync(&h, err.ptr, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    MG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (h_ovf)
+      continue; // a column exceeded this envelope: rerun everything with the next one
+    if (h == ULLONG_MAX)
+      return;
+    const int64_t g = static_cast<int64_t>(h >> 8);
+    const int64_t col = g % n, pt = g / n;
+    throw Error(MGPU_ERR_NUMERICAL, "spai_ls: rank-deficient least-squares problem in column " + std::to_string(col),
+                col, -1, pt);
+  }
+  throw Error(MGPU_ERR_UNSUPPORTED,
+              "spai_ls: a column exceeds the device envelope (|J| <= 32 pattern entries, |I| <= 64 rows)");
+}
+
+struct PatternPtrs
+{
+  const int64_t *rp[64];
+  const int32_t *ci[64];
+};
+
+__global__ void pattern_diff(int l, int64_t n, int64_t nnz, PatternPtrs a, const int64_t *rp0, const int32_t *ci0,
+                             int *diff)
+{
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (int p = 0; p < l; ++p)
+  {
+    if (k <= n && a.rp[p][k] != rp0[k])
+      atomicOr(diff, 1);
+    if (k < nnz && a.ci[p][k] != ci0[k])
+      atomicOr(diff, 1);
+  }
 }
 
 } // namespace
+
+// True when every matrix in mats (up to 64) has exactly ref's CSR pattern.
+bool same_pattern(mgpu_ctx *ctx, int l, const mgpu_csr *const *mats, const mgpu_csr *ref)
+{
+  if (l > 64)
+    return false;
+  PatternPtrs pp{};
+  for (int p = 0; p < l; ++p)
+  {
+    if (mats[p]->nrows != ref->nrows || mats[p]->ncols != ref->ncols || mats[p]->nnz != ref->nnz)
+      return false;
+    pp.rp[p] = mats[p]->row_ptr;
+    pp.ci[p] = mats[p]->col_idx;
+  }
+  DBuf diff(sizeof(int), ctx->stream);
+  MG_CUDA(cudaMemsetAsync(diff.ptr, 0, sizeof(int), ctx->stream));
+  const int64_t span = std::max<int64_t>(ref->nrows + 1, ref->nnz);
+  pattern_diff<<<blocks_for(span), kThreads, 0, ctx->stream>>>(l, ref->nrows, ref->nnz, pp, ref->row_ptr, ref->col_idx,
+                                                               diff.as<int>());
+  check_launch(ctx, "pattern_diff");
+  int h = 0;
+  MG_CUDA(cudaMemcpyAsync(&h, diff.ptr, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  MG_CUDA(cudaStreamSynchronize(ctx->stream));
+  return h == 0;
+}
 
 // Symbolic pattern of A*A (values = 1.0 placeholders).
 mgpu_csr *pattern_square(mgpu_ctx *ctx, const mgpu_csr *A)
@@ -476,45 +562,11 @@ mgpu_csr *spai_ls_one(mgpu_ctx *ctx, const mgpu_csr *A, const mgpu_csr *K_old, i
                             ctx->stream));
     MG_CUDA(cudaMemsetAsync(PT->values, 0, sizeof(double) * pat->nnz, ctx->stream));
   }
-  DBuf err(sizeof(unsigned long long), ctx->stream), maxlen(sizeof(int), ctx->stream), ovf(sizeof(int), ctx->stream);
-  MG_CUDA(cudaMemsetAsync(maxlen.ptr, 0, sizeof(int), ctx->stream));
-  int h_max = 0;
-  if (n > 0)
-  {
-    max_row_len<<<blocks_for(n), kThreads, 0, ctx->stream>>>(n, pat->row_ptr, maxlen.as<int>());
-    check_launch(ctx, "max_row_len");
-    MG_CUDA(cudaMemcpyAsync(&h_max, maxlen.ptr, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    MG_CUDA(cudaStreamSynchronize(ctx->stream));
-  }
   try
   {
-    bool done = n == 0;
+    const int maxrow = static_cast<int>(csr_max_row(ctx, const_cast<mgpu_csr *>(pat)));
     const DCsr kv = Kot ? Kot->view() : DCsr{nullptr, nullptr, nullptr};
-    for (int cfg = 0; cfg < 3 && !done; ++cfg)
-    {
-      const int G = cfg == 0 ? 8 : (cfg == 1 ? 16 : 32);
-      if (h_max > G)
-        continue;
-      MG_CUDA(cudaMemsetAsync(err.ptr, 0xff, sizeof(unsigned long long), ctx->stream));
-      MG_CUDA(cudaMemsetAsync(ovf.ptr, 0, sizeof(int), ctx->stream));
-      auto *ev = err.as<unsigned long long>();
-      if (cfg == 0)
-        launch_ls<8, 16, 4>(ctx, n, pat->view(), At->view(), kv, Kot != nullptr, PT->values, ev, ovf.as<int>());
-      else if (cfg == 1)
-        launch_ls<16, 32, 2>(ctx, n, pat->view(), At->view(), kv, Kot != nullptr, PT->values, ev, ovf.as<int>());
-      else
-        launch_ls<32, 64, 1>(ctx, n, pat->view(), At->view(), kv, Kot != nullptr, PT->values, ev, ovf.as<int>());
-      int h_ovf = 0;
-      MG_CUDA(cudaMemcpyAsync(&h_ovf, ovf.ptr, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-      MG_CUDA(cudaStreamSynchronize(ctx->stream));
-      if (h_ovf)
-        continue; // a column exceeded this envelope: rerun everything with the next one
-      check_err(ctx, ev);
-      done = true;
-    }
-    if (!done)
-      throw Error(MGPU_ERR_UNSUPPORTED,
-                  "spai_ls: a column exceeds the device envelope (|J| <= 32 pattern entries, |I| <= 64 rows)");
+    run_ls(ctx, n, 1, maxrow, pat->view(), At->view(), 0, kv, 0, Kot != nullptr, PT->values, 0);
   }
   catch (...)
   {
@@ -537,6 +589,82 @@ mgpu_csr *spai_ls_one(mgpu_ctx *ctx, const mgpu_csr *A, const mgpu_csr *K_old, i
   return P;
 }
 
+// LS-SPAI for l operators that share one CSR pattern (the shifted operators
+// of one system do): the pattern work -- J pattern, A^T structure and the
+// value permutation, P^T -> P permutation -- is done once, the l * n column
+// problems run in ONE launch, and each factor is a gather of its values.
+std::vector<mgpu_csr *> spai_ls_shared(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, const mgpu_csr *const *K_old,
+                                       int pattern)
+{
+  const mgpu_csr *A0 = A[0];
+  const int64_t n = A0->nrows, nnzA = A0->nnz;
+  cudaStream_t s = ctx->stream;
+  mgpu_csr *sq = pattern == MGPU_PATTERN_A2 ? pattern_square(ctx, A0) : nullptr;
+  const mgpu_csr *pat = sq ? sq : A0;
+  const int64_t nnzJ = pat->nnz;
+  std::vector<mgpu_csr *> out;
+  DBuf perm_t, perm_p;
+  mgpu_csr *At0 = nullptr, *PT0 = nullptr, *P0 = nullptr;
+  try
+  {
+    At0 = transpose_perm(ctx, A0, perm_t);
+    DBuf at_vals(sizeof(double) * static_cast<size_t>(l) * (nnzA > 0 ? nnzA : 1), s);
+    DBuf ko_vals(K_old ? sizeof(double) * static_cast<size_t>(l) * (nnzA > 0 ? nnzA : 1) : 8, s);
+    for (int p = 0; p < l; ++p)
+    {
+      gather_dev(ctx, nnzA, perm_t.as<int64_t>(), A[p]->values, at_vals.as<double>() + p * nnzA);
+      if (K_old)
+        gather_dev(ctx, nnzA, perm_t.as<int64_t>(), K_old[p]->values, ko_vals.as<double>() + p * nnzA);
+    }
+    DBuf pt_vals(sizeof(double) * static_cast<size_t>(l) * (nnzJ > 0 ? nnzJ : 1), s);
+    MG_CUDA(cudaMemsetAsync(pt_vals.ptr, 0, sizeof(double) * static_cast<size_t>(l) * nnzJ, s));
+    const int maxrow = static_cast<int>(csr_max_row(ctx, const_cast<mgpu_csr *>(pat)));
+    DCsr atv{At0->row_ptr, At0->col_idx, at_vals.as<double>()};
+    DCsr kov{At0->row_ptr, At0->col_idx, ko_vals.as<double>()};
+    run_ls(ctx, n, l, maxrow, pat->view(), atv, nnzA, kov, nnzA, K_old != nullptr, pt_vals.as<double>(), nnzJ);
+    // P^T (J pattern) -> P: one permutation for every factor
+    PT0 = new_csr(ctx, n, n, nnzJ);
+    MG_CUDA(cudaMemcpyAsync(PT0->row_ptr, pat->row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToDevice, s));
+    if (nnzJ > 0)
+    {
+      MG_CUDA(cudaMemcpyAsync(PT0->col_idx, pat->col_idx, sizeof(int32_t) * nnzJ, cudaMemcpyDeviceToDevice, s));
+      MG_CUDA(cudaMemcpyAsync(PT0->values, pt_vals.ptr, sizeof(double) * nnzJ, cudaMemcpyDeviceToDevice, s));
+    }
+    P0 = transpose_perm(ctx, PT0, perm_p);
+    const int64_t ba = csr_bandwidth(ctx, const_cast<mgpu_csr *>(A0));
+    for (int p = 0; p < l; ++p)
+    {
+      mgpu_csr *P = p == 0 ? P0 : new_csr(ctx, n, n, nnzJ);
+      if (p > 0)
+      {
+        MG_CUDA(cudaMemcpyAsync(P->row_ptr, P0->row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToDevice, s));
+        if (nnzJ > 0)
+          MG_CUDA(cudaMemcpyAsync(P->col_idx, P0->col_idx, sizeof(int32_t) * nnzJ, cudaMemcpyDeviceToDevice, s));
+        gather_dev(ctx, nnzJ, perm_p.as<int64_t>(), pt_vals.as<double>() + p * nnzJ, P->values);
+      }
+      P->may_hold_zeros = true;
+      P->bw = pattern == MGPU_PATTERN_A2 ? 2 * ba : ba;
+      P->maxrow = -1;
+      out.push_back(P);
+    }
+    P0 = nullptr;
+  }
+  catch (...)
+  {
+    for (auto *m : out)
+      mgpu_csr_free(m);
+    mgpu_csr_free(P0);
+    mgpu_csr_free(PT0);
+    mgpu_csr_free(At0);
+    mgpu_csr_free(sq);
+    throw;
+  }
+  mgpu_csr_free(PT0);
+  mgpu_csr_free(At0);
+  mgpu_csr_free(sq);
+  return out;
+}
+
 } // namespace mgpu
 
 using namespace mgpu;
@@ -556,6 +684,18 @@ int mgpu_spai_ls_batched(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, const m
 {
   return guard(ctx, [&] {
     MG_ARG(l >= 0 && A && P, "spai_ls: null argument");
+    for (int i = 0; i < l; ++i)
+      MG_ARG(A[i] && A[i]->nrows == A[i]->ncols && (!K_old || (K_old[i] && K_old[i]->nrows == A[i]->nrows &&
+                                                                   K_old[i]->ncols == A[i]->ncols)),
+             "spai_ls: operands must be square with equal shape");
+    MG_ARG(pattern == MGPU_PATTERN_A || pattern == MGPU_PATTERN_A2, "spai_ls: unknown pattern");
+    if (l >= 2 && same_pattern(ctx, l, A, A[0]) && (!K_old || same_pattern(ctx, l, K_old, A[0])))
+    {
+      std::vector<mgpu_csr *> made = spai_ls_shared(ctx, l, A, K_old, pattern);
+      for (int i = 0; i < l; ++i)
+        P[i] = made[i];
+      return;
+    }
     std::vector<mgpu_csr *> made;
     try
     {

@@ -323,6 +323,70 @@ mgpu_csr *transpose_csr(mgpu_ctx *ctx, const mgpu_csr *A)
   return T;
 }
 
+namespace
+{
+__global__ void iota_i64(int64_t n, int64_t *out)
+{
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < n)
+    out[k] = k;
+}
+__global__ void gather_values(int64_t nnz, const int64_t *__restrict__ perm, const double *__restrict__ src,
+                              double *__restrict__ dst)
+{
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < nnz)
+    dst[k] = src[perm[k]];
+}
+} // namespace
+
+// Transpose that also returns perm (T.values[k] = A.values[perm[k]]), so the
+// same pattern can be re-transposed for new values with a gather.
+mgpu_csr *transpose_perm(mgpu_ctx *ctx, const mgpu_csr *A, DBuf &perm)
+{
+  mgpu_csr *T = new_csr(ctx, A->ncols, A->nrows, A->nnz);
+  T->may_hold_zeros = A->may_hold_zeros;
+  T->bw = A->bw;
+  MG_CUDA(cudaMemsetAsync(T->row_ptr, 0, sizeof(int64_t) * (A->ncols + 1), ctx->stream));
+  perm = DBuf(sizeof(int64_t) * (A->nnz > 0 ? A->nnz : 1), ctx->stream);
+  if (A->nnz == 0)
+    return T;
+  DBuf keys(sizeof(unsigned long long) * A->nnz, ctx->stream);
+  DBuf keys_out(sizeof(unsigned long long) * A->nnz, ctx->stream);
+  DBuf idx(sizeof(int64_t) * A->nnz, ctx->stream);
+  expand_rows<<<blocks_for(A->nrows), kThreads, 0, ctx->stream>>>(A->nrows, A->row_ptr, A->col_idx,
+                                                                  keys.as<unsigned long long>(), T->row_ptr);
+  check_launch(ctx, "expand_rows");
+  iota_i64<<<blocks_for(A->nnz), kThreads, 0, ctx->stream>>>(A->nnz, idx.as<int64_t>());
+  check_launch(ctx, "iota_i64");
+  int bits = 32;
+  while ((1ll << (bits - 32)) <= A->ncols && bits < 64)
+    ++bits;
+  size_t tmp = 0;
+  MG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys.as<unsigned long long>(),
+                                          keys_out.as<unsigned long long>(), idx.as<int64_t>(), perm.as<int64_t>(),
+                                          A->nnz, 0, bits, ctx->stream));
+  DBuf t(tmp, ctx->stream);
+  MG_CUDA(cub::DeviceRadixSort::SortPairs(t.ptr, tmp, keys.as<unsigned long long>(), keys_out.as<unsigned long long>(),
+                                          idx.as<int64_t>(), perm.as<int64_t>(), A->nnz, 0, bits, ctx->stream));
+  count_launch(ctx);
+  keys_to_cols<<<blocks_for(A->nnz), kThreads, 0, ctx->stream>>>(A->nnz, keys_out.as<unsigned long long>(),
+                                                                  T->col_idx);
+  check_launch(ctx, "keys_to_cols");
+  gather_values<<<blocks_for(A->nnz), kThreads, 0, ctx->stream>>>(A->nnz, perm.as<int64_t>(), A->values, T->values);
+  check_launch(ctx, "gather_values");
+  scan_row_ptr(ctx, T->row_ptr, A->ncols);
+  return T;
+}
+
+void gather_dev(mgpu_ctx *ctx, int64_t nnz, const int64_t *perm, const double *src, double *dst)
+{
+  if (nnz == 0)
+    return;
+  gather_values<<<blocks_for(nnz), kThreads, 0, ctx->stream>>>(nnz, perm, src, dst);
+  check_launch(ctx, "gather_values");
+}
+
 void trace_dev(mgpu_ctx *ctx, const mgpu_csr *A, double *out_dev)
 {
   const int64_t n = A->nrows < A->ncols ? A->nrows : A->ncols;

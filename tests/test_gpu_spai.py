@@ -18,6 +18,13 @@ def _csr_close(got, want, tol=1e-10):
     assert rel(got.values, want.values) <= tol
 
 
+def _csr_equal(got, want):
+    """LS-SPAI replays thin_qr's operation order: bitwise equal to the oracle."""
+    np.testing.assert_array_equal(got.row_ptr, want.row_ptr)
+    np.testing.assert_array_equal(got.col_idx, want.col_idx)
+    np.testing.assert_array_equal(got.values, want.values)
+
+
 # ------------------------------------------------------------------ MR-SPAI
 @pytest.mark.parametrize("kscale,s", [(0.01, 1.0), (1.0, 1.0), (1.0, 10.0), (1.0, 100.0), (100.0, 10.0)])
 def test_mr_build_t1(mg, oracle, kscale, s):
@@ -107,7 +114,7 @@ def test_ls_build_hermite(mg, oracle, pattern, s):
     A = oracle.shifted_operator(M, D, K, s)
     want = oracle.spai_ls(A, None, pattern)
     got = mg.spai_ls(A, None, pattern).matrix.download()
-    _csr_close(got, want)
+    _csr_equal(got, want)
 
 
 @pytest.mark.parametrize("pattern", [0, 1])
@@ -117,7 +124,7 @@ def test_ls_update_hermite(mg, oracle, pattern):
     A2 = oracle.shifted_operator(M, D, K, 150.0)
     want = oracle.spai_ls(A2, A1, pattern)
     got = mg.spai_ls(A2, A1, pattern).matrix.download()
-    _csr_close(got, want)
+    _csr_equal(got, want)
 
 
 def test_ls_chain_model_and_dense(mg, oracle):
@@ -141,13 +148,33 @@ def test_ls_rank_deficiency(mg, oracle):
     assert eg.value.index == eo.value.index == 0
 
 
-def test_ls_batched_equals_single(mg, oracle):
+@pytest.mark.parametrize("pattern", [0, 1])
+def test_ls_batched_shared_pattern(mg, oracle, pattern):
+    """8 shifted operators share one pattern: one launch, gathered factors, bitwise == oracle."""
     M, D, K = oracle.hermite_generate(500)
     shifts = [10.0 ** (1 + 3 * i / 7) for i in range(8)]
     ops = mg.shifted_operators(M, D, K, shifts)
-    facs = mg.spai_ls_batched(ops)
-    for s, f in zip(shifts, facs):
-        _csr_close(f.matrix.download(), oracle.spai_ls(oracle.shifted_operator(M, D, K, s), None, 0))
+    facs = mg.spai_ls_batched(ops, None, pattern)
+    host = [oracle.shifted_operator(M, D, K, s) for s in shifts]
+    for A, f in zip(host, facs):
+        _csr_equal(f.matrix.download(), oracle.spai_ls(A, None, pattern))
+    # batched update (K_old per point, same pattern) -- the AIRGA vertical update
+    shifts2 = [s * 1.25 for s in shifts]
+    ops2 = mg.shifted_operators(M, D, K, shifts2)
+    upd = mg.spai_ls_batched(ops2, ops, pattern)
+    for A_old, s2, f in zip(host, shifts2, upd):
+        _csr_equal(f.matrix.download(), oracle.spai_ls(oracle.shifted_operator(M, D, K, s2), A_old, pattern))
+
+
+def test_ls_batched_mixed_patterns(mg, oracle):
+    """Operators with different patterns take the per-operator path."""
+    Mh, Dh, Kh = oracle.hermite_generate(200)
+    Mc, Dc, Kc = oracle.chain_generate(400, consistent=True, stiffness_scale=1.0)
+    A1 = oracle.shifted_operator(Mh, Dh, Kh, 100.0)
+    A2 = oracle.shifted_operator(Mc, Dc, Kc, 2.0)
+    facs = mg.spai_ls_batched([A1, A2], None, 0)
+    _csr_equal(facs[0].matrix.download(), oracle.spai_ls(A1, None, 0))
+    _csr_equal(facs[1].matrix.download(), oracle.spai_ls(A2, None, 0))
 
 
 # ------------------------------------------------------------------ SpGEMM chain collapse
