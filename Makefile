@@ -16,7 +16,9 @@ CPP_SRCS := $(wildcard $(SRC)/*.cpp)
 CU_OBJS  := $(patsubst $(SRC)/%.cu,$(OBJDIR)/%.o,$(CU_SRCS))
 CPP_OBJS := $(patsubst $(SRC)/%.cpp,$(OBJDIR)/%.cpp.o,$(CPP_SRCS))
 
-.PHONY: all lib oracle ref clean
+REFINC  ?= /root/reference/proj/include
+
+.PHONY: all lib shim oracle ref parity clean
 
 all: lib oracle
 
@@ -33,6 +35,20 @@ $(OBJDIR)/%.cpp.o: $(SRC)/%.cpp include/mgpu.h | $(OBJDIR)
 
 $(LIBDIR)/libmgpu.so: $(CU_OBJS) $(CPP_OBJS) | $(LIBDIR)
 	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart
+
+# C++ drop-in backend: compiled against the reference's own headers (only
+# where /root/reference exists); the .so travels to the GPU box.
+shim: $(LIBDIR)/libmor_cuda.so
+
+$(LIBDIR)/libmor_cuda.so: $(PKG)/host/cuda_backend.cpp $(PKG)/host/cuda_backend.hpp $(LIBDIR)/libmgpu.so
+	$(CXX) -std=c++20 -O2 -fPIC -shared -Wall -Wextra -I$(REFINC) -Iinclude -I$(PKG)/host -o $@ $< \
+	  -L$(LIBDIR) -lmgpu -Wl,-rpath,'$$ORIGIN'
+
+# Parity driver: reference CgBackend vs CudaCgBackend (checker, lives in oracle/_ref)
+parity: shim ref
+	$(CXX) -std=c++20 -O2 -Wall -I$(REFINC) -Iinclude -I$(PKG)/host -include functional -o oracle/_ref/backend_parity \
+	  tests/cpp/backend_parity.cpp $(filter-out oracle/_ref/ref_shim.o,$(wildcard oracle/_ref/*.o)) \
+	  -L$(LIBDIR) -lmor_cuda -lmgpu -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)' -lpthread
 
 oracle:
 	$(MAKE) -C oracle oracle

@@ -321,6 +321,55 @@ class Reference(_Lib):
     def force_kernels(self, variant: str) -> bool:
         return bool(self.lib.ref_force_kernels(0 if variant == "scalar" else 1))
 
+    def backend(self, solver: str, M: Csr, D: Csr, K: Csr, spai_tol=0.01, spai_max_col_iters=50, spai_mode=1,
+                cg_rtol=1e-10, cg_maxit_factor=10, update_start_iteration=3):
+        """The reference CgBackend through make_backend (airga.cpp:358-365)."""
+        return _RefBackend(self, solver, M, D, K, spai_tol, spai_max_col_iters, spai_mode, cg_rtol, cg_maxit_factor,
+                           update_start_iteration)
+
+
+class _RefBackend:
+    def __init__(self, ref, solver, M, D, K, spai_tol, spai_max_col_iters, spai_mode, cg_rtol, cg_maxit_factor,
+                 update_start_iteration):
+        self.ref, self.lib = ref, ref.lib
+        self.lib.ref_backend_create.restype = C.c_void_p
+        code = {"cg_plain": 1, "cg_spai": 2, "cg_spai_update": 3}[solver]
+        self._keep = [ref._in(x) for x in (M, D, K)]
+        self.h = C.c_void_p(self.lib.ref_backend_create(
+            C.c_int(code), C.c_double(spai_tol), C.c_int64(spai_max_col_iters), C.c_int(spai_mode),
+            C.c_double(cg_rtol), C.c_int64(cg_maxit_factor), C.c_int64(update_start_iteration),
+            *[C.byref(c) for c in self._keep]))
+        self.n = M.nrows
+
+    def prepare(self, points, outer):
+        pts = np.ascontiguousarray(points, np.float64)
+        l = len(pts)
+        sec, kind, chain = np.zeros(l), np.zeros(l, np.int32), np.zeros(l, np.int64)
+        err = _CErr()
+        st = self.lib.ref_backend_prepare(self.h, C.c_int64(l), _dp(pts), C.c_int64(outer), _dp(sec),
+                                          kind.ctypes.data_as(C.POINTER(C.c_int)), _ip(chain), C.byref(err))
+        self.ref._check(st, err)
+        return [dict(kind="base" if k == 0 else "update", chain_length=int(c), seconds=float(t))
+                for k, c, t in zip(kind, chain, sec)]
+
+    def solve(self, i, B):
+        B = np.asfortranarray(np.atleast_2d(np.asarray(B, np.float64).T).T)
+        n, m = B.shape
+        X, rec, tr = (np.zeros((n, m), order="F") for _ in range(3))
+        it = np.zeros(m, np.int64)
+        allc = C.c_int()
+        err = _CErr()
+        st = self.lib.ref_backend_solve(self.h, C.c_int64(i), C.c_int64(n), C.c_int64(m), _dp(B), _dp(X), _dp(rec),
+                                        _dp(tr), _ip(it), C.byref(allc), C.byref(err))
+        self.ref._check(st, err)
+        return dict(X=X, recurrence_residuals=rec, true_residuals=tr, iterations=it, all_converged=bool(allc.value))
+
+    def __del__(self):
+        try:
+            self.lib.ref_backend_destroy(self.h)
+        except Exception:
+            pass
+
 
 def reference_available() -> bool:
     return os.path.exists(REF_SO)

@@ -1,0 +1,448 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Host side of the drop-in B200 solve backend (see cuda_backend.hpp).  Pure
+// marshalling between the reference's value types and the C-ABI; all
+// arithmetic runs in libmgpu.so.  There is no CPU fallback: a missing device
+// or an unsupported shape surfaces as an exception.
+#include "cuda_backend.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <stdexcept>
+#include <string>
+
+#include "mgpu.h"
+#include "mor/errors.hpp"
+
+namespace mor
+{
+namespace
+{
+
+using Clock = std::chrono::steady_clock;
+
+// mgpu status -> the reference's exception taxonomy (errors.hpp:13-59).
+[[noreturn]] void raise(mgpu_ctx *ctx, int st)
+{
+  int64_t idx = -1, col = -1, pt = -1;
+  char msg[1024] = {0};
+  mgpu_last_error(ctx, &idx, &col, &pt, msg, sizeof msg);
+  switch (st)
+  {
+  case MGPU_ERR_ARG: throw ArgumentError(msg);
+  case MGPU_ERR_STAGNATION: throw StagnationError(msg, idx);
+  case MGPU_ERR_BREAKDOWN: throw BreakdownError(msg, idx);
+  case MGPU_ERR_NUMERICAL: throw NumericalError(msg);
+  default: throw std::runtime_error(std::string("mgpu (") + mgpu_status_string(st) + "): " + msg);
+  }
+}
+
+void check(mgpu_ctx *ctx, int st)
+{
+  if (st != MGPU_OK)
+    raise(ctx, st);
+}
+
+mgpu_csr *upload(mgpu_ctx *ctx, const SparseMatrix &A)
+{
+  mgpu_csr *h = nullptr;
+  check(ctx, mgpu_csr_upload(ctx, A.nrows, A.ncols, A.nnz(), A.row_ptr.data(), A.col_idx.data(), A.values.data(),
+                             &h));
+  return h;
+}
+
+SparseMatrix download(mgpu_ctx *ctx, const mgpu_csr *m)
+{
+  SparseMatrix A;
+  int64_t nr = 0, nc = 0, nnz = 0;
+  check(ctx, mgpu_csr_info(ctx, m, &nr, &nc, &nnz));
+  A.nrows = nr;
+  A.ncols = nc;
+  A.row_ptr.assign(static_cast<std::size_t>(nr + 1), 0);
+  A.col_idx.assign(static_cast<std::size_t>(nnz), 0);
+  A.values.assign(static_cast<std::size_t>(nnz), 0.0);
+  check(ctx, mgpu_csr_download(ctx, m, A.row_ptr.data(), A.col_idx.data(), A.values.data()));
+  return A;
+}
+
+double seconds_since(Clock::time_point t0) { return std::chrono::duration<double>(Clock::now() - t0).count(); }
+
+// One batched mgpu_cg_solve for `l` points sharing chain length z.
+std::vector<BlockSolveResult> solve_points(mgpu_ctx *ctx, const std::vector<mgpu_csr *> &A,
+                                           const std::vector<mgpu_csr *> &chains_flat, int z, const DenseMatrix &B,
+                                           double rtol, std::int64_t maxit)
+{
+  const int l = static_cast<int>(A.size());
+  const int64_t n = B.nrows, m = B.ncols;
+  const std::size_t blk = static_cast<std::size_t>(n * m);
+  std::vector<double> X(blk * l), REC(blk * l), TR(blk * l);
+  std::vector<int64_t> it(static_cast<std::size_t>(l * m)), bd(static_cast<std::size_t>(l * m));
+  std::vector<int> conv(static_cast<std::size_t>(l * m)), status(static_cast<std::size_t>(l * m));
+  mgpu_cg_out out{};
+  out.X = X.data();
+  out.recurrence = REC.data();
+  out.true_res = TR.data();
+  out.iterations = it.data();
+  out.converged = conv.data();
+  out.status = status.data();
+  out.breakdown_iteration = bd.data();
+  check(ctx, mgpu_cg_solve(ctx, l, A.data(), z, chains_flat.empty() ? nullptr : chains_flat.data(), n, m,
+                           B.values.data(), 0, rtol, maxit, MGPU_HOST, &out));
+  std::vector<BlockSolveResult> res(static_cast<std::size_t>(l));
+  for (int p = 0; p < l; ++p)
+  {
+    BlockSolveResult &r = res[static_cast<std::size_t>(p)];
+    r.X = DenseMatrix(n, m);
+    r.recurrence_residuals = DenseMatrix(n, m);
+    r.true_residuals = DenseMatrix(n, m);
+    std::copy(X.begin() + p * blk, X.begin() + (p + 1) * blk, r.X.values.begin());
+    std::copy(REC.begin() + p * blk, REC.begin() + (p + 1) * blk, r.recurrence_residuals.values.begin());
+    std::copy(TR.begin() + p * blk, TR.begin() + (p + 1) * blk, r.true_residuals.values.begin());
+    r.iterations.assign(it.begin() + p * m, it.begin() + (p + 1) * m);
+    r.all_converged = std::all_of(conv.begin() + p * m, conv.begin() + (p + 1) * m, [](int c) { return c != 0; });
+  }
+  return res;
+}
+
+} // namespace
+
+// ------------------------------------------------------------------ cuda::
+namespace cuda
+{
+
+Device::Device(int device)
+{
+  if (mgpu_ctx_create(device, nullptr, &ctx_) != MGPU_OK)
+    throw std::runtime_error("mor::cuda: no usable sm_100 device " + std::to_string(device) + " (no CPU fallback)");
+}
+
+Device::~Device() { mgpu_ctx_destroy(ctx_); }
+
+DeviceMatrix::DeviceMatrix(Device &dev, const SparseMatrix &A) : dev_(&dev), m_(upload(dev.ctx(), A)) {}
+DeviceMatrix::DeviceMatrix(Device &dev, mgpu_csr *adopt) : dev_(&dev), m_(adopt) {}
+DeviceMatrix::~DeviceMatrix() { mgpu_csr_free(m_); }
+DeviceMatrix::DeviceMatrix(DeviceMatrix &&o) noexcept : dev_(o.dev_), m_(o.m_) { o.m_ = nullptr; }
+DeviceMatrix &DeviceMatrix::operator=(DeviceMatrix &&o) noexcept
+{
+  if (this != &o)
+  {
+    mgpu_csr_free(m_);
+    dev_ = o.dev_;
+    m_ = o.m_;
+    o.m_ = nullptr;
+  }
+  return *this;
+}
+SparseMatrix DeviceMatrix::download() const { return mor::download(dev_->ctx(), m_); }
+
+namespace
+{
+int mode_of(const SpaiOptions &opts)
+{
+  return opts.mode == SpaiOptions::Mode::frozen ? MGPU_SPAI_FROZEN : MGPU_SPAI_SEQUENTIAL;
+}
+
+SpaiFactor finish_factor(mgpu_ctx *ctx, mgpu_csr *P, std::vector<double> res, Clock::time_point t0,
+                         SpaiFactor::Kind kind)
+{
+  SpaiFactor f;
+  f.matrix = mor::download(ctx, P);
+  mgpu_csr_free(P);
+  f.target_frob_residual = std::move(res);
+  f.build_seconds = seconds_since(t0);
+  f.kind = kind;
+  return f;
+}
+
+std::vector<mgpu_csr *> upload_chain(Device &dev, const PreconditionerChain &chain,
+                                     std::vector<DeviceMatrix> &keep)
+{
+  std::vector<mgpu_csr *> h;
+  for (const SpaiFactor &f : chain.factors) // newest first, as stored (spai.hpp:63-75)
+  {
+    keep.emplace_back(dev, f.matrix);
+    h.push_back(keep.back().get());
+  }
+  return h;
+}
+} // namespace
+
+SpaiFactor spai_build(Device &dev, const SparseMatrix &K, const SpaiOptions &opts)
+{
+  const auto t0 = Clock::now();
+  DeviceMatrix dK(dev, K);
+  std::vector<double> res(static_cast<std::size_t>(K.nrows));
+  mgpu_csr *P = nullptr;
+  check(dev.ctx(), mgpu_spai_build(dev.ctx(), dK.get(), opts.tol, opts.max_col_iters, mode_of(opts), &P, res.data()));
+  return finish_factor(dev.ctx(), P, std::move(res), t0, SpaiFactor::Kind::base);
+}
+
+SpaiFactor spai_update(Device &dev, const SparseMatrix &K_old, const SparseMatrix &K_new, const SpaiOptions &opts)
+{
+  const auto t0 = Clock::now();
+  DeviceMatrix dO(dev, K_old), dN(dev, K_new);
+  std::vector<double> res(static_cast<std::size_t>(K_new.nrows));
+  mgpu_csr *Q = nullptr;
+  check(dev.ctx(), mgpu_spai_update(dev.ctx(), dO.get(), dN.get(), opts.tol, opts.max_col_iters, mode_of(opts), &Q,
+                                    res.data()));
+  return finish_factor(dev.ctx(), Q, std::move(res), t0, SpaiFactor::Kind::update);
+}
+
+SpaiFactor spai_ls(Device &dev, const SparseMatrix &A, const SparseMatrix *K_old, int pattern)
+{
+  const auto t0 = Clock::now();
+  DeviceMatrix dA(dev, A);
+  DeviceMatrix dO;
+  if (K_old)
+    dO = DeviceMatrix(dev, *K_old);
+  mgpu_csr *P = nullptr;
+  check(dev.ctx(), mgpu_spai_ls(dev.ctx(), dA.get(), K_old ? dO.get() : nullptr, pattern, &P));
+  return finish_factor(dev.ctx(), P, {}, t0, K_old ? SpaiFactor::Kind::update : SpaiFactor::Kind::base);
+}
+
+std::vector<double> chain_apply(Device &dev, const PreconditionerChain &chain, std::span<const double> v)
+{
+  if (chain.empty())
+    return std::vector<double>(v.begin(), v.end()); // spai.hpp:77-78
+  if (chain.dim() != static_cast<std::int64_t>(v.size()))
+    throw ArgumentError("chain_apply: dimension mismatch");
+  std::vector<DeviceMatrix> keep;
+  const std::vector<mgpu_csr *> h = upload_chain(dev, chain, keep);
+  std::vector<double> out(v.size());
+  check(dev.ctx(), mgpu_chain_apply(dev.ctx(), static_cast<int>(h.size()), h.data(), v.data(), out.data(), MGPU_HOST));
+  return out;
+}
+
+SolveReport pcg_solve(Device &dev, const SparseMatrix &A, const PreconditionerChain &P, std::span<const double> b,
+                      double rtol, std::int64_t maxit)
+{
+  const int64_t n = A.nrows;
+  if (A.nrows != A.ncols)
+    throw ArgumentError("LinearOperator::from_sparse: matrix must be square");
+  if ((!P.empty() && P.dim() != n) || static_cast<int64_t>(b.size()) != n)
+    throw ArgumentError("pcg_solve: dimension mismatch");
+  DeviceMatrix dA(dev, A);
+  std::vector<DeviceMatrix> keep;
+  const std::vector<mgpu_csr *> ch = upload_chain(dev, P, keep);
+  std::vector<double> x(n), tr(n), rec(n);
+  int64_t it = 0, bd = -1;
+  int conv = 0, status = 0;
+  const int64_t cap = std::min<int64_t>(maxit, int64_t(1) << 20);
+  std::vector<double> hist(static_cast<std::size_t>(std::max<int64_t>(cap, 1)));
+  mgpu_cg_out out{};
+  out.X = x.data();
+  out.recurrence = rec.data();
+  out.true_res = tr.data();
+  out.iterations = &it;
+  out.converged = &conv;
+  out.status = &status;
+  out.breakdown_iteration = &bd;
+  out.history = hist.data();
+  out.history_cap = cap;
+  mgpu_csr *a = dA.get();
+  const int st = mgpu_cg_solve(dev.ctx(), 1, &a, static_cast<int>(ch.size()), ch.empty() ? nullptr : ch.data(), n, 1,
+                               b.data(), 0, rtol, maxit, MGPU_HOST, &out);
+  if (st == MGPU_ERR_BREAKDOWN) // pcg_solve's own message (krylov.cpp:108-111)
+    throw BreakdownError("pcg_solve: direction curvature breakdown at iteration " + std::to_string(bd), bd);
+  check(dev.ctx(), st);
+  SolveReport rep;
+  rep.solution = std::move(x);
+  rep.residual = std::move(tr);
+  rep.recurrence_residual = std::move(rec);
+  rep.iterations = it;
+  rep.converged = conv != 0;
+  hist.resize(static_cast<std::size_t>(std::min(it, cap)));
+  rep.relres_history = std::move(hist);
+  return rep;
+}
+
+BlockSolveResult block_solve(Device &dev, const SparseMatrix &A, const PreconditionerChain &P, const DenseMatrix &B,
+                             double rtol, std::int64_t maxit)
+{
+  if (B.nrows != A.nrows)
+    throw ArgumentError("block_solve: right-hand-side rows do not match the operator dimension");
+  DeviceMatrix dA(dev, A);
+  std::vector<DeviceMatrix> keep;
+  const std::vector<mgpu_csr *> ch = upload_chain(dev, P, keep);
+  return solve_points(dev.ctx(), {dA.get()}, ch, static_cast<int>(ch.size()), B, rtol, maxit)[0];
+}
+
+} // namespace cuda
+
+// ------------------------------------------------------------------ backend
+struct CudaCgBackend::State
+{
+  AirgaConfig cfg;
+  CudaBackendOptions opt;
+  cuda::Device dev;
+  int64_t n = 0;
+  const SecondOrderSystem *sys = nullptr;
+  cuda::DeviceMatrix M, D, K;
+  std::vector<cuda::DeviceMatrix> prev_ops;            // operators of the prepared iteration
+  std::vector<std::vector<cuda::DeviceMatrix>> chains; // per point, newest first
+
+  State(const AirgaConfig &c, const CudaBackendOptions &o) : cfg(c), opt(o), dev(o.device) {}
+};
+
+CudaCgBackend::CudaCgBackend(const AirgaConfig &cfg, const CudaBackendOptions &opt)
+  : st_(std::make_unique<State>(cfg, opt))
+{
+}
+
+CudaCgBackend::~CudaCgBackend() = default;
+
+// airga.cpp:108-164
+void CudaCgBackend::prepare(const SecondOrderSystem &sys, const std::vector<double> &points, std::int64_t outer,
+                            std::vector<PrecondRecord> *records)
+{
+  State &s = *st_;
+  mgpu_ctx *ctx = s.dev.ctx();
+  s.n = sys.order();
+  if (s.sys != &sys || !s.M.get())
+  {
+    s.M = cuda::DeviceMatrix(s.dev, sys.M);
+    s.D = cuda::DeviceMatrix(s.dev, sys.D);
+    s.K = cuda::DeviceMatrix(s.dev, sys.K);
+    s.sys = &sys;
+  }
+  const int l = static_cast<int>(points.size());
+  std::vector<mgpu_csr *> raw(static_cast<std::size_t>(l), nullptr);
+  if (l > 0)
+    check(ctx, mgpu_shifted_operators(ctx, s.M.get(), s.D.get(), s.K.get(), l, points.data(), raw.data()));
+  std::vector<cuda::DeviceMatrix> fresh;
+  for (mgpu_csr *h : raw)
+    fresh.emplace_back(s.dev, h);
+
+  if (s.cfg.solver == AirgaConfig::Solver::cg_plain)
+  {
+    s.chains.clear();
+    s.chains.resize(static_cast<std::size_t>(l));
+  }
+  else
+  {
+    SpaiOptions opts;
+    opts.tol = s.cfg.spai_tol;
+    opts.max_col_iters = s.cfg.spai_max_col_iters;
+    opts.mode = s.cfg.spai_mode;
+    const bool update_mode = s.cfg.solver == AirgaConfig::Solver::cg_spai_update &&
+                             outer >= s.cfg.update_start_iteration &&
+                             s.prev_ops.size() == static_cast<std::size_t>(l) &&
+                             s.chains.size() == static_cast<std::size_t>(l);
+    if (!update_mode)
+    {
+      s.chains.clear();
+      s.chains.resize(static_cast<std::size_t>(l));
+    }
+    if (s.opt.algorithm == cuda::SpaiAlgorithm::ls)
+    {
+      // one batched launch for every point; the per-point record gets the average
+      const auto t0 = Clock::now();
+      std::vector<mgpu_csr *> olds, outs(static_cast<std::size_t>(l), nullptr);
+      for (const auto &o : s.prev_ops)
+        olds.push_back(o.get());
+      check(ctx, mgpu_spai_ls_batched(ctx, l, raw.data(), update_mode ? olds.data() : nullptr, s.opt.ls_pattern,
+                                      outs.data()));
+      const double each = seconds_since(t0) / std::max(l, 1);
+      for (int i = 0; i < l; ++i)
+      {
+        s.chains[static_cast<std::size_t>(i)].insert(s.chains[static_cast<std::size_t>(i)].begin(),
+                                                     cuda::DeviceMatrix(s.dev, outs[static_cast<std::size_t>(i)]));
+        if (records)
+        {
+          PrecondRecord rec;
+          rec.outer = outer;
+          rec.point_index = i;
+          rec.point = points[static_cast<std::size_t>(i)];
+          rec.seconds = each;
+          rec.kind = update_mode ? SpaiFactor::Kind::update : SpaiFactor::Kind::base;
+          rec.chain_length = static_cast<std::int64_t>(s.chains[static_cast<std::size_t>(i)].size());
+          records->push_back(rec);
+        }
+      }
+    }
+    else
+    {
+      const int mode = opts.mode == SpaiOptions::Mode::frozen ? MGPU_SPAI_FROZEN : MGPU_SPAI_SEQUENTIAL;
+      for (int i = 0; i < l; ++i)
+      {
+        PrecondRecord rec;
+        rec.outer = outer;
+        rec.point_index = i;
+        rec.point = points[static_cast<std::size_t>(i)];
+        const auto t0 = Clock::now();
+        mgpu_csr *f = nullptr;
+        if (update_mode)
+        {
+          check(ctx, mgpu_spai_update(ctx, s.prev_ops[static_cast<std::size_t>(i)].get(), raw[static_cast<std::size_t>(i)],
+                                      opts.tol, opts.max_col_iters, mode, &f, nullptr));
+          rec.kind = SpaiFactor::Kind::update;
+        }
+        else
+        {
+          check(ctx, mgpu_spai_build(ctx, raw[static_cast<std::size_t>(i)], opts.tol, opts.max_col_iters, mode, &f,
+                                     nullptr));
+          rec.kind = SpaiFactor::Kind::base;
+        }
+        mgpu_ctx_synchronize(ctx);
+        auto &chain = s.chains[static_cast<std::size_t>(i)];
+        chain.insert(chain.begin(), cuda::DeviceMatrix(s.dev, f)); // push_newest (spai.cpp:352-359)
+        rec.seconds = seconds_since(t0);
+        rec.chain_length = static_cast<std::int64_t>(chain.size());
+        if (records)
+          records->push_back(rec);
+      }
+    }
+  }
+  s.prev_ops = std::move(fresh);
+}
+
+// airga.cpp:166-181
+BlockSolveResult CudaCgBackend::solve(std::int64_t point_index, const DenseMatrix &rhs)
+{
+  State &s = *st_;
+  if (point_index < 0 || point_index >= static_cast<std::int64_t>(s.prev_ops.size()))
+    throw std::out_of_range("CudaCgBackend::solve: point index");
+  if (rhs.nrows != s.n)
+    throw ArgumentError("block_solve: right-hand-side rows do not match the operator dimension");
+  std::vector<mgpu_csr *> chain;
+  if (!s.chains.empty())
+    for (const auto &f : s.chains[static_cast<std::size_t>(point_index)])
+      chain.push_back(f.get());
+  return solve_points(s.dev.ctx(), {s.prev_ops[static_cast<std::size_t>(point_index)].get()}, chain,
+                      static_cast<int>(chain.size()), rhs, s.cfg.cg_rtol, s.cfg.cg_maxit_factor * s.n)[0];
+}
+
+std::vector<BlockSolveResult> CudaCgBackend::solve_all(const DenseMatrix &rhs)
+{
+  State &s = *st_;
+  const int l = static_cast<int>(s.prev_ops.size());
+  std::vector<mgpu_csr *> A, flat;
+  std::size_t z = s.chains.empty() ? 0 : s.chains[0].size();
+  bool uniform = true;
+  for (int i = 0; i < l; ++i)
+  {
+    A.push_back(s.prev_ops[static_cast<std::size_t>(i)].get());
+    const std::size_t zi = s.chains.empty() ? 0 : s.chains[static_cast<std::size_t>(i)].size();
+    uniform = uniform && zi == z;
+    if (!s.chains.empty())
+      for (const auto &f : s.chains[static_cast<std::size_t>(i)])
+        flat.push_back(f.get());
+  }
+  if (!uniform)
+  {
+    std::vector<BlockSolveResult> out;
+    for (int i = 0; i < l; ++i)
+      out.push_back(solve(i, rhs));
+    return out;
+  }
+  return solve_points(s.dev.ctx(), A, flat, static_cast<int>(z), rhs, s.cfg.cg_rtol, s.cfg.cg_maxit_factor * s.n);
+}
+
+std::unique_ptr<SolveBackend> make_cuda_backend(const AirgaConfig &cfg, const CudaBackendOptions &opt)
+{
+  if (cfg.solver == AirgaConfig::Solver::direct)
+    throw ArgumentError("make_cuda_backend: the direct solver has no device backend");
+  return std::make_unique<CudaCgBackend>(cfg, opt);
+}
+
+} // namespace mor

@@ -1,0 +1,129 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Drop-in B200 solve backend for the reference AIRGA library (namespace mor).
+//
+// Compiles against the reference's own headers (proj/include/mor/*.hpp) and
+// calls the sm_100a kernels through the C-ABI in include/mgpu.h.  Nothing here
+// re-implements host-side arithmetic: every flop of prepare() and solve()
+// runs on the device.  See INTEGRATION.md for the two-line change to
+// make_backend (airga.cpp:358-365) that selects it.
+//
+//   class CudaCgBackend : public mor::SolveBackend   (airga.hpp:133-145)
+//       replaces CgBackend (airga.cpp:103-190): same prepare / solve /
+//       provides_residuals contract, same PrecondRecord bookkeeping, same
+//       exception types and payloads; plus solve_all() (every point in one
+//       batched kernel) and an LS-SPAI option.
+//   namespace mor::cuda                               free-function drop-ins
+//       spai_build / spai_update      (spai.hpp:53-61)  -> MR-SPAI on the device
+//       spai_ls                       (north star LS-SPAI, not in the reference)
+//       chain_apply                   (spai.hpp:77-79)
+//       pcg_solve / block_solve       (krylov.hpp:41-56)
+//   The reference's pcg_solve takes LinearOperators wrapping std::function;
+//   arbitrary host callables cannot run on the device, so the drop-ins take
+//   the SparseMatrix and PreconditionerChain that CgBackend::solve wraps
+//   (airga.cpp:168-180) -- the only operators the solve path ever builds.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <span>
+#include <vector>
+
+#include "mor/airga.hpp"
+#include "mor/krylov.hpp"
+#include "mor/spai.hpp"
+
+struct mgpu_ctx;
+struct mgpu_csr;
+
+namespace mor
+{
+
+namespace cuda
+{
+
+/// Device context (one GPU, one stream); not shareable across host threads.
+class Device
+{
+public:
+  explicit Device(int device = 0);
+  ~Device();
+  Device(const Device &) = delete;
+  Device &operator=(const Device &) = delete;
+  mgpu_ctx *ctx() const { return ctx_; }
+
+private:
+  mgpu_ctx *ctx_ = nullptr;
+};
+
+/// Device-resident CSR (owns an mgpu_csr).
+class DeviceMatrix
+{
+public:
+  DeviceMatrix() = default;
+  DeviceMatrix(Device &dev, const SparseMatrix &A);
+  DeviceMatrix(Device &dev, mgpu_csr *adopt);
+  ~DeviceMatrix();
+  DeviceMatrix(DeviceMatrix &&o) noexcept;
+  DeviceMatrix &operator=(DeviceMatrix &&o) noexcept;
+  DeviceMatrix(const DeviceMatrix &) = delete;
+  DeviceMatrix &operator=(const DeviceMatrix &) = delete;
+  mgpu_csr *get() const { return m_; }
+  /// Reference-convention CSR (exact zeros dropped), D2H.
+  SparseMatrix download() const;
+
+private:
+  Device *dev_ = nullptr;
+  mgpu_csr *m_ = nullptr;
+};
+
+enum class SpaiAlgorithm
+{
+  mr, ///< the reference's minimal-residual SPAI (Alg. 2/4), frozen mode
+  ls, ///< static-pattern least-squares SPAI (north star subsystem 1)
+};
+
+SpaiFactor spai_build(Device &dev, const SparseMatrix &K, const SpaiOptions &opts = {});
+SpaiFactor spai_update(Device &dev, const SparseMatrix &K_old, const SparseMatrix &K_new,
+                       const SpaiOptions &opts = {});
+/// pattern 0: A's pattern, 1: symbolic A*A.  K_old == nullptr builds P.
+SpaiFactor spai_ls(Device &dev, const SparseMatrix &A, const SparseMatrix *K_old, int pattern = 0);
+std::vector<double> chain_apply(Device &dev, const PreconditionerChain &chain, std::span<const double> v);
+SolveReport pcg_solve(Device &dev, const SparseMatrix &A, const PreconditionerChain &P, std::span<const double> b,
+                      double rtol, std::int64_t maxit);
+BlockSolveResult block_solve(Device &dev, const SparseMatrix &A, const PreconditionerChain &P, const DenseMatrix &B,
+                             double rtol, std::int64_t maxit);
+
+} // namespace cuda
+
+/// GPU-only choices on top of AirgaConfig.
+struct CudaBackendOptions
+{
+  int device = 0;
+  cuda::SpaiAlgorithm algorithm = cuda::SpaiAlgorithm::mr;
+  int ls_pattern = 0;
+};
+
+class CudaCgBackend final : public SolveBackend
+{
+public:
+  CudaCgBackend(const AirgaConfig &cfg, const CudaBackendOptions &opt = {});
+  ~CudaCgBackend() override;
+
+  void prepare(const SecondOrderSystem &sys, const std::vector<double> &points, std::int64_t outer,
+               std::vector<PrecondRecord> *records) override;
+  BlockSolveResult solve(std::int64_t point_index, const DenseMatrix &rhs) override;
+  bool provides_residuals() const override { return true; }
+
+  /// Every prepared point against the same rhs block in one batched kernel
+  /// (the reference solves point by point, airga.cpp:374-405).
+  std::vector<BlockSolveResult> solve_all(const DenseMatrix &rhs);
+
+private:
+  struct State;
+  std::unique_ptr<State> st_;
+};
+
+std::unique_ptr<SolveBackend> make_cuda_backend(const AirgaConfig &cfg, const CudaBackendOptions &opt = {});
+
+} // namespace mor
