@@ -50,13 +50,15 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="mgpu", choices=["mgpu", "reference"])
     ap.add_argument("--budget", type=int, default=1000, help="CG iterations per solve (fixed budget)")
-    ap.add_argument("--workload", default="config1", choices=["config0", "config1", "config3"])
+    ap.add_argument("--workload", default="config1", choices=["config0", "config1", "config2", "config3"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
 
 def workload(name: str, world: int, rank: int):
-    """(ne, m, shifts for this rank, all shifts, pattern, description)."""
+    """(ne, m, shifts for this rank, all shifts, pattern).  pattern: 0 LS-SPAI on A's
+    pattern, 1 on A^2's, -1 no preconditioner (P = I): on the BASELINE beam every
+    reference SPAI fails at n >= 4e5 (MR stagnates, LS rank-flushes), DESIGN.md."""
     from paper_1606_01216_b200 import sharding
     if name == "config0":
         ne, m, per, pattern = 1000, 1, 1, 0
@@ -64,8 +66,11 @@ def workload(name: str, world: int, rank: int):
     elif name == "config1":
         ne, m, per, pattern = 10000, 1, 8, 0
         all_shifts = sharding.log_shifts(per * world)
+    elif name == "config2":
+        ne, m, per, pattern = 50000, 1, 8, 0
+        all_shifts = sharding.log_shifts(per * world)
     else:
-        ne, m, per, pattern = 500000, 4, 16, 1
+        ne, m, per, pattern = 500000, 4, 16, -1
         all_shifts = sharding.log_shifts(per * world)
     return ne, m, sharding.shard(all_shifts, rank, world), all_shifts, pattern
 
@@ -148,9 +153,9 @@ def cpu_step_fn(kind: str, M, D, K, shifts, B, pattern, budget):
 
     def one(s):
         A = lib.shifted_operator(M, D, K, s)
-        P = lib.spai_ls(A, None, pattern)
+        chain = [lib.spai_ls(A, None, pattern)] if pattern >= 0 else []
         for c in range(B.shape[1]):
-            lib.pcg_solve(A, [P], B[:, c], rtol=1e-10, maxit=budget, history_cap=1)
+            lib.pcg_solve(A, chain, B[:, c], rtol=1e-10, maxit=budget, history_cap=1)
 
     def step():
         with ThreadPoolExecutor(threads) as ex:
@@ -192,12 +197,14 @@ def run_reference(args, rank, world):
 
 
 def config_dict(args, ne, m, shifts, pattern, world):
-    return {"workload": f"BASELINE.json configs[{ {'config0': 0, 'config1': 1, 'config3': 3}[args.workload] }]: "
-                        f"Hermite cantilever ne={ne} (n={2 * ne}), {len(shifts)} shifts log-spaced in [10,1e4], "
-                        f"m={m}, LS-SPAI on the {'A' if pattern == 0 else 'A^2'} pattern, right-preconditioned CG, "
-                        f"rtol 1e-10, fixed budget {args.budget} iterations",
+    spai = {0: "LS-SPAI on the A pattern", 1: "LS-SPAI on the A^2 pattern",
+            -1: "no preconditioner (P = I; every reference SPAI fails at this n on this beam, DESIGN.md)"}[pattern]
+    return {"workload": f"BASELINE.json configs[{ {'config0': 0, 'config1': 1, 'config2': 2, 'config3': 3}[args.workload] }]"
+                        f" shape: Hermite cantilever ne={ne} (n={2 * ne}), {len(shifts)} shifts log-spaced in "
+                        f"[10,1e4], m={m}, {spai}, right-preconditioned CG, rtol 1e-10, fixed budget "
+                        f"{args.budget} iterations",
             "n": 2 * ne, "shifts_total": len(shifts), "rhs": m, "cg_budget": args.budget,
-            "spai": "ls-" + ("A" if pattern == 0 else "A2"), "parallelism": f"shift-sharded x{world}",
+            "spai": {0: "ls-A", 1: "ls-A2", -1: "none"}[pattern], "parallelism": f"shift-sharded x{world}",
             "l2": "flushed between timed steps (256 MiB write)"}
 
 
@@ -256,15 +263,16 @@ def run_mgpu(args, rank, world, local_rank):
         e0.record(stream)
         ops = mg.shifted_operators(dM, dD, dK, shifts, ctx=ctx)
         e1.record(stream)
-        facs = mg.spai_ls_batched(ops, None, pattern, ctx=ctx)
+        facs = mg.spai_ls_batched(ops, None, pattern, ctx=ctx) if pattern >= 0 else []
         e2.record(stream)
-        it, cv, st, bd = mg.cg_solve_device(ops, [[f.matrix] for f in facs], B_dev, X_dev, R_dev, T_dev, rtol=1e-10,
+        chains = [[f.matrix] for f in facs] if facs else [[] for _ in ops]
+        it, cv, st, bd = mg.cg_solve_device(ops, chains, B_dev, X_dev, R_dev, T_dev, rtol=1e-10,
                                             maxit=budget, ctx=ctx)
         e3.record(stream)
         if record is not None:
             cg_ms, loops = ctx.last_cg_timing()
             record_path = ctx.last_cg_path
-            bytes_iter = sum(8 * o.stored_nnz + 8 * f.matrix.stored_nnz + 48 * n * m for o, f in zip(ops, facs))
+            bytes_iter = sum(8 * o.stored_nnz + 48 * n * m for o in ops) + sum(8 * f.matrix.stored_nnz for f in facs)
             record.append(dict(ev=(e0, e1, e2, e3), cg_ms=cg_ms, loops=loops, bytes=bytes_iter * loops,
                                iters=int(it.max()), breakdowns=int((st != 0).sum())))
 
@@ -273,9 +281,10 @@ def run_mgpu(args, rank, world, local_rank):
         e0.record(stream)
         hM, hD, hK = (mg.DeviceCsr.upload(x, ctx) for x in host_sys)
         ops = mg.shifted_operators(hM, hD, hK, shifts, ctx=ctx)
-        facs = mg.spai_ls_batched(ops, None, pattern, ctx=ctx)
+        facs = mg.spai_ls_batched(ops, None, pattern, ctx=ctx) if pattern >= 0 else []
         flat = [f.matrix for f in facs]
-        status, it, cv, st, bd, _ = mg.cg_solve_raw(ctx, ops, flat, 1, n, m, B_host.data_ptr(), 0, 1e-10, budget,
+        status, it, cv, st, bd, _ = mg.cg_solve_raw(ctx, ops, flat, 1 if facs else 0, n, m, B_host.data_ptr(), 0,
+                                                    1e-10, budget,
                                                     mg.mgpu.MGPU_HOST, X_host.data_ptr(), R_host.data_ptr(),
                                                     T_host.data_ptr())
         e1.record(stream)
@@ -341,8 +350,9 @@ def run_mgpu(args, rank, world, local_rank):
             orc = Oracle()
             hM, hD, hK = orc.hermite_generate(ne)
             kind = "reference" if reference_available() else "port"
-            sample_shifts = shifts if args.workload != "config3" else shifts[:1]
-            sample_budget = budget if args.workload != "config3" else 5
+            big = args.workload in ("config2", "config3")
+            sample_shifts = shifts if not big else shifts[:2]
+            sample_budget = budget if not big else 20
             step, threads, kind = cpu_step_fn(kind, hM, hD, hK, sample_shifts, B, pattern, sample_budget)
             t = time.perf_counter()
             step()
@@ -367,7 +377,10 @@ def run_mgpu(args, rank, world, local_rank):
             "cg_ms": statistics.median(cg_ms), "cg_us_per_iteration": 1e3 * statistics.median(cg_ms) / max(loops, 1),
             "cg_iterations": loops, "breakdowns": recs[-1]["breakdowns"], "cg_kernel": ctx.last_cg_path,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "peak_source": peak_kind, "kernel": "cg_persistent",
+                         "traffic": traffic, "peak_source": peak_kind, "kernel": "cg_" + ctx.last_cg_path,
+                         "regime": ("working set on chip (shared memory / L2): latency- and barrier-bound; the HBM "
+                                    "fraction is reported for the contract" if args.workload in ("config0", "config1")
+                                    else "HBM streaming"),
                          "bytes_model": "per iteration, per shift: 8 nnz(A) + 8 nnz(P) + 48 n m"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d_bytes,
                     "d2h_bytes_per_step": d2h_bytes},
