@@ -83,8 +83,11 @@ int mgpu_last_cg_timing(const mgpu_ctx *ctx, double *ms, int64_t *iterations);
  * (one thread-block cluster per shifted system, operators in shared memory)
  * if the systems fit on chip, else the fused banded grid kernel (2 grid
  * barriers per iteration); otherwise the general CSR kernel.
- * 1 = always the general kernel, 2 = the banded grid kernel (no cluster).
- * mgpu_last_cg_path reports 2 (cluster), 0 (banded grid) or 1 (general). */
+ * 1 = always the general kernel, 2 = the banded grid kernel (no cluster),
+ * 3 = cluster kernel v1 only (vectors in shared memory; v2 keeps them in
+ * registers and is preferred for single right-hand sides).
+ * mgpu_last_cg_path reports 2 (cluster v2), 3 (cluster v1), 0 (banded grid)
+ * or 1 (general). */
 int mgpu_ctx_set_cg_path(mgpu_ctx *ctx, int path);
 int mgpu_last_cg_path(const mgpu_ctx *ctx);
 

@@ -27,7 +27,7 @@ namespace cgrp = cooperative_groups;
 
 namespace mgpu
 {
-bool cg_cluster_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_csr *const *chains,
+int cg_cluster_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_csr *const *chains,
                       int64_t n, int m, const double *B_dev, int64_t ldb, const int *halo, double rtol,
                       int64_t maxit, double *X, double *REC, double *TR, int64_t *d_it, int *d_conv, int *d_st,
                       int64_t *d_bd, double *d_hist, int64_t hist_cap, unsigned long long *d_loop, const DCsr *dA,
@@ -1472,7 +1472,7 @@ void cg_batch(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_
   MG_CUDA(cudaMemcpyAsync(dF.ptr, hF.data(), sizeof(DCsr) * hF.size(), cudaMemcpyHostToDevice, s));
 
   DBuf partial, totals, counter, segs, pblk;
-  bool clustered = false;
+  int clustered = 0;
   if (banded && ctx->cg_path != 2)
   {
     // systems small enough to live on chip: one cluster per point, no grid barrier
@@ -1654,7 +1654,7 @@ void cg_batch(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_
   MG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
   *ms_out += ms;
   *loop_out += loop;
-  ctx->last_cg_path = clustered ? 2 : (banded ? 0 : 1);
+  ctx->last_cg_path = clustered ? clustered : (banded ? 0 : 1);
 }
 
 } // namespace

@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cmath>
 #include <vector>
 
 #include "internal.cuh"
@@ -650,18 +651,519 @@ bool launch_cluster(mgpu_ctx *ctx, ClParams &P, size_t dyn)
   return true;
 }
 
+// =====================================================================
+// v2 (single right-hand side): vectors in REGISTERS, d in a halo-padded
+// shared buffer updated in place, neighbours exchange only boundary rows.
+// Footprint ~110 B/row (A and P in ELL + d + t), so a 2e4-row system fits a
+// 10-CTA cluster and 8 systems run in ONE wave (11 co-resident 10-CTA
+// clusters on B200 vs 7 of 16).
+//   exports (parity-double-buffered, read by the neighbours through DSMEM):
+//     ex_r[q][side]: boundary rows of r_k  (written in phase B of k-1)
+//     ex_d[q][side]: boundary rows of d_{k-1} (written in phase A of k-1)
+//     ex_x[side]   : boundary rows of x~ (written before a residual check)
+// =====================================================================
+constexpr int kV2TB = 512;
+
+struct V2Params
+{
+  int l, z, cs, rb, ea, H;
+  int ef[kCMaxZ];
+  int halo[kCMaxZ + 1];
+  int64_t n;
+  const DCsr *A, *F;
+  const double *B;
+  int64_t ldb;
+  double rtol;
+  int64_t maxit;
+  size_t off_d, off_t0, off_t1, off_part, off_ex, off_av, off_ao, off_fv[kCMaxZ], off_fo[kCMaxZ];
+  double *X, *REC, *TR;
+  int64_t *iters;
+  int *conv, *status;
+  int64_t *bd_iter;
+  double *hist;
+  int64_t hist_cap;
+  unsigned long long *loop_iters;
+};
+
+template <int RPT>
+__global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
+{
+  cgrp::cluster_group cl = cgrp::this_cluster();
+  extern __shared__ __align__(16) unsigned char raw[];
+  __shared__ ClShared sh;
+  const int cs = P.cs, H = P.H;
+  const int rank = static_cast<int>(cl.block_rank());
+  const int p = static_cast<int>(blockIdx.x / cs);
+  const int64_t c0 = static_cast<int64_t>(rank) * P.rb;
+  const int64_t c1 = min(P.n, c0 + P.rb);
+  const int R = c1 > c0 ? static_cast<int>(c1 - c0) : 0;
+  double *dpad = reinterpret_cast<double *>(raw + P.off_d); // rows [c0 - H, c1 + H)
+  double *tb[2] = {reinterpret_cast<double *>(raw + P.off_t0), reinterpret_cast<double *>(raw + P.off_t1)};
+  double *part = reinterpret_cast<double *>(raw + P.off_part);                // [2 phases][2 * kCMaxM]
+  double *ex = reinterpret_cast<double *>(raw + P.off_ex);                    // exports
+  auto ex_r = [&](double *base, int q, int side) { return base + ((0 * 2 + q) * 2 + side) * H; };
+  auto ex_d = [&](double *base, int q, int side) { return base + ((1 * 2 + q) * 2 + side) * H; };
+  auto ex_x = [&](double *base, int side) { return base + (4 * 2 + side) * H; };
+  double *left = rank > 0 ? cl.map_shared_rank(ex, rank - 1) : nullptr;       // neighbour exports
+  double *right = rank + 1 < cs ? cl.map_shared_rank(ex, rank + 1) : nullptr;
+
+  load_ell(P.A[p], c0, c0 + R, P.n, P.ea, reinterpret_cast<double *>(raw + P.off_av),
+           reinterpret_cast<signed char *>(raw + P.off_ao), kV2TB);
+  for (int st = 0; st < P.z; ++st)
+  {
+    const int hd = P.halo[st + 1];
+    load_ell(P.F[p * P.z + (P.z - 1 - st)], c0 - hd, c0 + R + hd, P.n, P.ef[st],
+             reinterpret_cast<double *>(raw + P.off_fv[st]), reinterpret_cast<signed char *>(raw + P.off_fo[st]),
+             kV2TB);
+  }
+  double r[RPT], x[RPT], w[RPT], bv[RPT];
+  double pk[2] = {0.0, 0.0};
+#pragma unroll
+  for (int j = 0; j < RPT; ++j)
+  {
+    const int lr = threadIdx.x + j * kV2TB;
+    bv[j] = lr < R ? P.B[static_cast<int64_t>(p) * P.ldb + c0 + lr] : 0.0;
+    r[j] = bv[j];
+    x[j] = 0.0;
+    w[j] = 0.0;
+    if (lr < R)
+    {
+      dpad[H + lr] = bv[j];
+      pk[0] = __dadd_rn(pk[0], __dmul_rn(bv[j], bv[j]));
+      if (lr < H)
+      {
+        ex_r(ex, 0, 0)[lr] = bv[j];
+        ex_d(ex, 0, 0)[lr] = bv[j];
+      }
+      if (lr >= R - H)
+      {
+        ex_r(ex, 0, 1)[lr - (R - H)] = bv[j];
+        ex_d(ex, 0, 1)[lr - (R - H)] = bv[j];
+      }
+    }
+  }
+  cta_sum<kV2TB, 2>(sh, pk, 1, part);
+  cl.sync();
+  cluster_total(cl, sh, part, 1, cs);
+  if (threadIdx.x == 0)
+  {
+    const double bb = sh.tot[0], bn = sqrt(bb);
+    sh.bnorm[0] = bn;
+    sh.rho[0] = bb;
+    sh.target[0] = P.rtol * bn;
+    sh.state[0] = bn == 0.0 ? cZeroRhs : cRun;
+    sh.fresh[0] = 1;
+    sh.beta[0] = 0.0;
+    sh.sit[0] = 0;
+  }
+  __syncthreads();
+
+  // chain on shared memory: stage 0 source = dpad (halo H = halo[0]); returns
+  // the buffer holding P(source) and its halo.
+  auto chain = [&](int &hs) -> const double * {
+    const double *in = dpad;
+    hs = P.halo[0];
+    for (int st = 0; st < P.z; ++st)
+    {
+      const int hd = P.halo[st + 1];
+      const int E = P.ef[st];
+      const double *fv = reinterpret_cast<const double *>(raw + P.off_fv[st]);
+      const signed char *fo = reinterpret_cast<const signed char *>(raw + P.off_fo[st]);
+      double *out = tb[st & 1];
+      const int span = R + 2 * hd;
+      for (int q = threadIdx.x; q < span; q += kV2TB)
+      {
+        const int64_t i = c0 - hd + q;
+        if (i < 0 || i >= P.n)
+          continue;
+        const int base_in = q + hs - hd;
+        double acc = 0.0;
+        for (int e = 0; e < E; ++e)
+          acc = __dadd_rn(acc, __dmul_rn(fv[q * E + e], in[base_in + fo[q * E + e]]));
+        out[q] = acc;
+      }
+      __syncthreads();
+      in = out;
+      hs = hd;
+    }
+    return in;
+  };
+  auto apply_a = [&](const double *in, int hs, double (&y)[RPT]) {
+    const double *av = reinterpret_cast<const double *>(raw + P.off_av);
+    const signed char *ao = reinterpret_cast<const signed char *>(raw + P.off_ao);
+    const int E = P.ea;
+#pragma unroll
+    for (int j = 0; j < RPT; ++j)
+    {
+      const int lr = threadIdx.x + j * kV2TB;
+      y[j] = 0.0;
+      if (lr >= R)
+        continue;
+      for (int e = 0; e < E; ++e)
+        y[j] = __dadd_rn(y[j], __dmul_rn(av[lr * E + e], in[lr + hs + ao[lr * E + e]]));
+    }
+  };
+  // halo rows of dpad from the neighbours' exports (mode 0: d_new = fresh ? r : r + beta d; 1: x~)
+  auto fill_halo = [&](int mode, int q) {
+    for (int t = threadIdx.x; t < 2 * H; t += kV2TB)
+    {
+      const int side = t / H, k = t % H; // side 0: rows c0 - H + k (left neighbour's right export)
+      const int64_t i = side == 0 ? c0 - H + k : c1 + k;
+      if (i < 0 || i >= P.n)
+        continue;
+      double *nb = side == 0 ? left : right;
+      const int nside = side == 0 ? 1 : 0;
+      double v;
+      if (mode == 1)
+        v = ex_x(nb, nside)[k];
+      else
+      {
+        const double rv = ex_r(nb, q, nside)[k];
+        v = sh.fresh[0] ? rv : __dadd_rn(rv, __dmul_rn(sh.beta[0], ex_d(nb, q, nside)[k]));
+      }
+      dpad[side == 0 ? k : H + R + k] = v;
+    }
+  };
+
+  // true-residual check (kind 0 confirm, krylov.cpp:77-103; kind 1 budget exhausted, :128-137)
+  auto check = [&](int kind, int64_t it) {
+#pragma unroll
+    for (int j = 0; j < RPT; ++j)
+    {
+      const int lr = threadIdx.x + j * kV2TB;
+      if (lr < R)
+      {
+        dpad[H + lr] = x[j]; // d_old is not needed afterwards: the single column finishes or restarts
+        if (lr < H)
+          ex_x(ex, 0)[lr] = x[j];
+        if (lr >= R - H)
+          ex_x(ex, 1)[lr - (R - H)] = x[j];
+      }
+    }
+    cl.sync();
+    fill_halo(1, 0);
+    __syncthreads();
+    int hs;
+    const double *t = chain(hs);
+    double y[RPT], sol[RPT];
+    apply_a(t, hs, y);
+    double q2[2] = {0.0, 0.0};
+#pragma unroll
+    for (int j = 0; j < RPT; ++j)
+    {
+      const int lr = threadIdx.x + j * kV2TB;
+      sol[j] = 0.0;
+      if (lr < R)
+      {
+        sol[j] = t[lr + hs];
+        y[j] = __dsub_rn(bv[j], y[j]);
+        q2[0] = __dadd_rn(q2[0], __dmul_rn(y[j], y[j]));
+      }
+    }
+    cta_sum<kV2TB, 2>(sh, q2, 1, part);
+    cl.sync();
+    cluster_total(cl, sh, part, 1, cs);
+    const double tt = sh.tot[0];
+    bool fin = kind == 1 || sqrt(tt) <= sh.target[0];
+    const bool rst = !fin;
+    if (kind == 0 && !fin && sqrt(tt) <= sh.target[0]) // krylov.cpp:98-102
+      fin = true;
+#pragma unroll
+    for (int j = 0; j < RPT; ++j)
+    {
+      const int lr = threadIdx.x + j * kV2TB;
+      if (lr >= R)
+        continue;
+      const int64_t o = static_cast<int64_t>(p) * P.n + c0 + lr;
+      if (fin)
+      {
+        if (P.X)
+          P.X[o] = sol[j];
+        if (P.TR)
+          P.TR[o] = y[j];
+      }
+      else
+      {
+        r[j] = y[j]; // restart from the true residual, d = r
+        if (lr < H)
+          ex_r(ex, static_cast<int>(it & 1), 0)[lr] = y[j];
+        if (lr >= R - H)
+          ex_r(ex, static_cast<int>(it & 1), 1)[lr - (R - H)] = y[j];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+    {
+      if (fin)
+      {
+        sh.state[0] = (kind == 1 && !(sqrt(tt) <= sh.target[0])) ? cMaxed : cConverged;
+        sh.sit[0] = it;
+      }
+      else if (rst)
+      {
+        sh.rho[0] = tt;
+        sh.fresh[0] = 1;
+      }
+    }
+    cl.sync();
+  };
+
+  int64_t it = 0;
+  for (;;)
+  {
+    if (it >= P.maxit)
+      break;
+    if (sh.state[0] == cRun && sqrt(sh.rho[0]) <= sh.target[0])
+      check(0, it);
+    if (sh.state[0] != cRun)
+      break;
+    const int q = static_cast<int>(it & 1);
+    // ---- phase A: d_new in place (own rows) + halo from exports, t = P d, w = A t
+    double pa[2] = {0.0, 0.0};
+    const double beta = sh.beta[0];
+    const int fresh = sh.fresh[0];
+#pragma unroll
+    for (int j = 0; j < RPT; ++j)
+    {
+      const int lr = threadIdx.x + j * kV2TB;
+      if (lr < R)
+      {
+        const double dn = fresh ? r[j] : __dadd_rn(r[j], __dmul_rn(beta, dpad[H + lr]));
+        dpad[H + lr] = dn;
+        if (lr < H)
+          ex_d(ex, q ^ 1, 0)[lr] = dn;
+        if (lr >= R - H)
+          ex_d(ex, q ^ 1, 1)[lr - (R - H)] = dn;
+      }
+    }
+    fill_halo(0, q);
+    __syncthreads();
+    int hs;
+    const double *t = chain(hs);
+    apply_a(t, hs, w);
+#pragma unroll
+    for (int j = 0; j < RPT; ++j)
+    {
+      const int lr = threadIdx.x + j * kV2TB;
+      if (lr < R)
+      {
+        const double dn = dpad[H + lr];
+        pa[0] = __dadd_rn(pa[0], __dmul_rn(dn, w[j]));
+        pa[1] = __dadd_rn(pa[1], __dmul_rn(dn, dn));
+      }
+    }
+    cta_sum<kV2TB, 2>(sh, pa, 2, part);
+    cl.sync();
+    cluster_total(cl, sh, part, 2, cs);
+    const double curv = sh.tot[0], dd = sh.tot[1];
+    if (!(curv > 1e-30 * dd)) // krylov.cpp:108
+    {
+      __syncthreads();
+      if (threadIdx.x == 0)
+      {
+        sh.state[0] = cBreakdown;
+        sh.sit[0] = it;
+      }
+      __syncthreads();
+      break;
+    }
+    const double alpha = sh.rho[0] / curv;
+    // ---- phase B: x~ += alpha d, r -= alpha w, (r, r); export boundary r_{k+1}
+    double pb[2] = {0.0, 0.0};
+#pragma unroll
+    for (int j = 0; j < RPT; ++j)
+    {
+      const int lr = threadIdx.x + j * kV2TB;
+      if (lr < R)
+      {
+        x[j] = __dadd_rn(x[j], __dmul_rn(alpha, dpad[H + lr]));
+        r[j] = __dadd_rn(r[j], __dmul_rn(-alpha, w[j]));
+        pb[0] = __dadd_rn(pb[0], __dmul_rn(r[j], r[j]));
+        if (lr < H)
+          ex_r(ex, q ^ 1, 0)[lr] = r[j];
+        if (lr >= R - H)
+          ex_r(ex, q ^ 1, 1)[lr - (R - H)] = r[j];
+      }
+    }
+    cta_sum<kV2TB, 2>(sh, pb, 1, part + 2 * kCMaxM);
+    cl.sync();
+    cluster_total(cl, sh, part + 2 * kCMaxM, 1, cs);
+    ++it;
+    if (threadIdx.x == 0)
+    {
+      const double rn = sh.tot[0];
+      if (P.hist && rank == 0 && it - 1 < P.hist_cap)
+        P.hist[static_cast<int64_t>(p) * P.hist_cap + (it - 1)] = sqrt(rn) / sh.bnorm[0];
+      sh.beta[0] = rn / sh.rho[0];
+      sh.rho[0] = rn;
+      sh.fresh[0] = 0;
+    }
+    __syncthreads();
+  }
+  if (sh.state[0] == cRun)
+    check(1, it);
+  for (int j = 0; j < RPT; ++j)
+  {
+    const int lr = threadIdx.x + j * kV2TB;
+    if (lr >= R)
+      continue;
+    const int64_t o = static_cast<int64_t>(p) * P.n + c0 + lr;
+    if (sh.state[0] == cZeroRhs)
+    {
+      if (P.X)
+        P.X[o] = 0.0;
+      if (P.TR)
+        P.TR[o] = 0.0;
+      if (P.REC)
+        P.REC[o] = 0.0;
+    }
+    else if (sh.state[0] != cBreakdown && P.REC)
+      P.REC[o] = r[j];
+  }
+  if (rank == 0 && threadIdx.x == 0)
+  {
+    const int st = sh.state[0];
+    P.iters[p] = sh.sit[0];
+    P.conv[p] = (st == cConverged || st == cZeroRhs) ? 1 : 0;
+    P.status[p] = st == cBreakdown ? MGPU_ERR_BREAKDOWN : MGPU_OK;
+    P.bd_iter[p] = st == cBreakdown ? sh.sit[0] : -1;
+    atomicMax(P.loop_iters, static_cast<unsigned long long>(it));
+  }
+  cl.sync();
+}
+
+template <int RPT>
+int v2_active_clusters(const V2Params &P, size_t dyn)
+{
+  auto kern = cg_cluster_v2<RPT>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)) != cudaSuccess ||
+      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+  {
+    cudaGetLastError();
+    return 0;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(P.cs));
+  cfg.blockDim = dim3(kV2TB);
+  cfg.dynamicSmemBytes = dyn;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(P.cs);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int clusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) != cudaSuccess)
+  {
+    cudaGetLastError();
+    return 0;
+  }
+  return clusters;
+}
+
+template <int RPT>
+void v2_launch(mgpu_ctx *ctx, const V2Params &P, size_t dyn)
+{
+  MG_CUDA(cudaFuncSetAttribute(cg_cluster_v2<RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
+  MG_CUDA(cudaFuncSetAttribute(cg_cluster_v2<RPT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(P.l * P.cs));
+  cfg.blockDim = dim3(kV2TB);
+  cfg.dynamicSmemBytes = dyn;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(P.cs);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  MG_CUDA(cudaLaunchKernelEx(&cfg, cg_cluster_v2<RPT>, P));
+  check_launch(ctx, "cg_cluster_v2");
+}
+
+// Plans and launches v2; false when no cluster size fits.  Picks the size that
+// minimises (waves x rows per CTA) given the co-residency the driver reports.
+bool v2_solve(mgpu_ctx *ctx, V2Params P, size_t budget)
+{
+  int best_cs = 0, best_rpt = 0;
+  size_t best_dyn = 0;
+  double best_cost = 1e300;
+  V2Params best{};
+  for (int cs = 1; cs <= kCMaxCS; ++cs)
+  {
+    const int64_t rb = (P.n + cs - 1) / cs;
+    if (rb > static_cast<int64_t>(kV2TB) * 4)
+      continue;
+    const int64_t last = P.n - static_cast<int64_t>(cs - 1) * rb;
+    if (cs > 1 && (rb < P.halo[0] || last < P.halo[0]))
+      continue;
+    V2Params Q = P;
+    Q.cs = cs;
+    Q.rb = static_cast<int>(rb);
+    Q.H = P.halo[0];
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+      const size_t o = off;
+      off += (bytes + 15) & ~static_cast<size_t>(15);
+      return o;
+    };
+    Q.off_d = take(sizeof(double) * static_cast<size_t>(rb + 2 * Q.H));
+    Q.off_t0 = take(Q.z >= 1 ? sizeof(double) * static_cast<size_t>(rb + 2 * Q.halo[1]) : 16);
+    Q.off_t1 = take(Q.z >= 2 ? sizeof(double) * static_cast<size_t>(rb + 2 * Q.halo[2]) : 16);
+    Q.off_part = take(sizeof(double) * 4 * kCMaxM);
+    Q.off_ex = take(sizeof(double) * 10 * static_cast<size_t>(std::max(Q.H, 1)));
+    Q.off_av = take(sizeof(double) * static_cast<size_t>(rb) * Q.ea);
+    Q.off_ao = take(static_cast<size_t>(rb) * Q.ea);
+    for (int st = 0; st < Q.z; ++st)
+    {
+      const size_t rows = static_cast<size_t>(rb + 2 * Q.halo[st + 1]);
+      Q.off_fv[st] = take(sizeof(double) * rows * Q.ef[st]);
+      Q.off_fo[st] = take(rows * Q.ef[st]);
+    }
+    if (off > budget)
+      continue;
+    const int rpt = static_cast<int>((rb + kV2TB - 1) / kV2TB);
+    const int r4 = rpt <= 1 ? 1 : (rpt == 2 ? 2 : 4);
+    const int act = r4 == 1 ? v2_active_clusters<1>(Q, off) : (r4 == 2 ? v2_active_clusters<2>(Q, off)
+                                                                        : v2_active_clusters<4>(Q, off));
+    if (act < 1)
+      continue;
+    const double waves = std::ceil(static_cast<double>(P.l) / act);
+    const double cost = waves * static_cast<double>(rb) * (1.0 + 0.02 * cs); // larger clusters: costlier barriers
+    if (cost < best_cost)
+    {
+      best_cost = cost;
+      best_cs = cs;
+      best_rpt = r4;
+      best_dyn = off;
+      best = Q;
+    }
+  }
+  if (best_cs == 0)
+    return false;
+  if (best_rpt == 1)
+    v2_launch<1>(ctx, best, best_dyn);
+  else if (best_rpt == 2)
+    v2_launch<2>(ctx, best, best_dyn);
+  else
+    v2_launch<4>(ctx, best, best_dyn);
+  return true;
+}
+
 } // namespace
 
 // Tries the cluster-resident solve; false when the systems do not fit on chip
 // (the caller then uses the grid-wide kernels).
-bool cg_cluster_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_csr *const *chains,
-                      int64_t n, int m, const double *B_dev, int64_t ldb, const int *halo, double rtol,
-                      int64_t maxit, double *X, double *REC, double *TR, int64_t *d_it, int *d_conv, int *d_st,
-                      int64_t *d_bd, double *d_hist, int64_t hist_cap, unsigned long long *d_loop, const DCsr *dA,
-                      const DCsr *dF)
+int cg_cluster_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_csr *const *chains,
+                     int64_t n, int m, const double *B_dev, int64_t ldb, const int *halo, double rtol,
+                     int64_t maxit, double *X, double *REC, double *TR, int64_t *d_it, int *d_conv, int *d_st,
+                     int64_t *d_bd, double *d_hist, int64_t hist_cap, unsigned long long *d_loop, const DCsr *dA,
+                     const DCsr *dF)
 {
   if (m > kCMaxM || z > kCMaxZ || n <= 0 || n > INT32_MAX)
-    return false;
+    return 0;
   int ea = 0;
   int ef[kCMaxZ] = {0};
   for (int p = 0; p < l; ++p)
@@ -670,6 +1172,38 @@ bool cg_cluster_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, con
     for (int st = 0; st < z; ++st)
       ef[st] = std::max<int>(ef[st], static_cast<int>(csr_max_row(ctx, const_cast<mgpu_csr *>(
                                                                        chains[static_cast<size_t>(p) * z + (z - 1 - st)]))));
+  }
+  int cdev0 = 0;
+  MG_CUDA(cudaDeviceGetAttribute(&cdev0, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+  if (m == 1 && ctx->cg_path != 3)
+  {
+    V2Params V{};
+    V.l = l;
+    V.z = z;
+    V.ea = ea;
+    for (int st = 0; st < z; ++st)
+      V.ef[st] = ef[st];
+    for (int q = 0; q <= z; ++q)
+      V.halo[q] = halo[q];
+    V.n = n;
+    V.A = dA;
+    V.F = dF;
+    V.B = B_dev;
+    V.ldb = ldb;
+    V.rtol = rtol;
+    V.maxit = maxit;
+    V.X = X;
+    V.REC = REC;
+    V.TR = TR;
+    V.iters = d_it;
+    V.conv = d_conv;
+    V.status = d_st;
+    V.bd_iter = d_bd;
+    V.hist = d_hist;
+    V.hist_cap = hist_cap;
+    V.loop_iters = d_loop;
+    if (v2_solve(ctx, V, static_cast<size_t>(cdev0) - sizeof(ClShared) - 1024))
+      return 2;
   }
   const int TB = m <= 2 ? 1024 : 512;
   const int rpt_max = 2;
@@ -748,9 +1282,9 @@ bool cg_cluster_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, con
     else
       ok = rpt == 1 ? launch_cluster<512, 4, 1>(ctx, P, off) : launch_cluster<512, 4, 2>(ctx, P, off);
     if (ok)
-      return true;
+      return 3;
   }
-  return false;
+  return 0;
 }
 
 } // namespace mgpu

@@ -108,8 +108,8 @@ struct mgpu_ctx
   int64_t launches = 0;
   double last_cg_ms = 0.0;
   int64_t last_cg_iters = 0;
-  int last_cg_path = 1; // 0 banded (grid), 1 general, 2 cluster-resident
-  int cg_path = 0;      // 0 auto, 1 force general, 2 force banded grid kernel (no cluster)
+  int last_cg_path = 1; // 0 banded (grid), 1 general, 2 cluster v2 (m = 1), 3 cluster v1
+  int cg_path = 0;      // 0 auto, 1 force general, 2 force banded grid kernel (no cluster), 3 cluster v1 only
   // last error
   int last_status = MGPU_OK;
   int64_t err_index = -1, err_col = -1, err_point = -1;

@@ -13,7 +13,7 @@ from conftest import rel
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True, params=["auto", "banded", "general"])
+@pytest.fixture(autouse=True, params=["auto", "cluster_v1", "banded", "general"])
 def cg_path(request, mg):
     """Every parity case runs through all three CG kernels: cluster-resident (auto on
     these on-chip sizes), the banded grid kernel and the general CSR kernel."""
@@ -28,8 +28,8 @@ def test_path_selection(mg, oracle, cg_path):
     A = oracle.shifted_operator(M, D, K, 100.0)
     P = oracle.spai_ls(A, None, 1)
     mg.pcg_solve(A, [P], np.ones(600), maxit=5)
-    assert mg.default_context().last_cg_path == {"auto": "cluster", "banded": "banded",
-                                                  "general": "general"}[cg_path]
+    assert mg.default_context().last_cg_path == {"auto": "cluster", "cluster_v1": "cluster_v1",
+                                                  "banded": "banded", "general": "general"}[cg_path]
     # a wide operator (bandwidth > 64) always takes the general kernel
     from oracle import Csr
     rng = np.random.default_rng(9)
