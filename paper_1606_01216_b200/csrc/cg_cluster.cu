@@ -112,6 +112,22 @@ __device__ __forceinline__ void cta_sum(ClShared &sh, double (&v)[NV], int nv, d
   }
 }
 
+// After cluster.sync(): every warp forms tot[k] (k < nv) itself from the cs
+// remote slots with a fixed butterfly, so no CTA barrier / broadcast is needed.
+__device__ __forceinline__ void warp_cluster_total(cgrp::cluster_group &cl, const double *slot, int nv, int cs,
+                                                   double *out)
+{
+  const int lane = threadIdx.x & 31;
+  for (int k = 0; k < nv; ++k)
+  {
+    double v = lane < cs ? cl.map_shared_rank(slot, lane)[k] : 0.0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1)
+      v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+    out[k] = v;
+  }
+}
+
 // After cluster.sync(): tot[k] = sum over ranks (fixed order) of slot[k].
 __device__ __forceinline__ void cluster_total(cgrp::cluster_group &cl, ClShared &sh, double *slot, int nv, int cs)
 {
@@ -744,19 +760,14 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
   }
   cta_sum<kV2TB, 2>(sh, pk, 1, part);
   cl.sync();
-  cluster_total(cl, sh, part, 1, cs);
-  if (threadIdx.x == 0)
-  {
-    const double bb = sh.tot[0], bn = sqrt(bb);
-    sh.bnorm[0] = bn;
-    sh.rho[0] = bb;
-    sh.target[0] = P.rtol * bn;
-    sh.state[0] = bn == 0.0 ? cZeroRhs : cRun;
-    sh.fresh[0] = 1;
-    sh.beta[0] = 0.0;
-    sh.sit[0] = 0;
-  }
-  __syncthreads();
+  // per-system scalars live in registers; every thread derives identical values
+  double tv[2];
+  warp_cluster_total(cl, part, 1, cs, tv);
+  const double bnorm = sqrt(tv[0]);
+  double rho = tv[0], beta = 0.0;
+  const double target = P.rtol * bnorm;
+  int state = bnorm == 0.0 ? cZeroRhs : cRun, fresh = 1;
+  int64_t sit = 0;
 
   // chain on shared memory: stage 0 source = dpad (halo H = halo[0]); returns
   // the buffer holding P(source) and its halo.
@@ -771,16 +782,40 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
       const signed char *fo = reinterpret_cast<const signed char *>(raw + P.off_fo[st]);
       double *out = tb[st & 1];
       const int span = R + 2 * hd;
-      for (int q = threadIdx.x; q < span; q += kV2TB)
+      // RPT + 1 rows per thread, entries outer / rows inner: independent
+      // accumulation chains in flight (ILP); per-row order is unchanged.
+      constexpr int K = RPT + 1;
+      int q[K];
+      bool ok[K];
+      double acc[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j)
       {
-        const int64_t i = c0 - hd + q;
+        q[j] = threadIdx.x + j * kV2TB;
+        const int64_t i = c0 - hd + q[j];
+        ok[j] = q[j] < span && i >= 0 && i < P.n;
+        acc[j] = 0.0;
+      }
+      for (int e = 0; e < E; ++e)
+      {
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+          if (ok[j])
+            acc[j] = __dadd_rn(acc[j], __dmul_rn(fv[q[j] * E + e], in[q[j] + hs - hd + fo[q[j] * E + e]]));
+      }
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+        if (ok[j])
+          out[q[j]] = acc[j];
+      for (int qq = threadIdx.x + K * kV2TB; qq < span; qq += kV2TB) // only if span > K * TB
+      {
+        const int64_t i = c0 - hd + qq;
         if (i < 0 || i >= P.n)
           continue;
-        const int base_in = q + hs - hd;
-        double acc = 0.0;
+        double a = 0.0;
         for (int e = 0; e < E; ++e)
-          acc = __dadd_rn(acc, __dmul_rn(fv[q * E + e], in[base_in + fo[q * E + e]]));
-        out[q] = acc;
+          a = __dadd_rn(a, __dmul_rn(fv[qq * E + e], in[qq + hs - hd + fo[qq * E + e]]));
+        out[qq] = a;
       }
       __syncthreads();
       in = out;
@@ -792,15 +827,22 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
     const double *av = reinterpret_cast<const double *>(raw + P.off_av);
     const signed char *ao = reinterpret_cast<const signed char *>(raw + P.off_ao);
     const int E = P.ea;
+    bool ok[RPT];
 #pragma unroll
     for (int j = 0; j < RPT; ++j)
     {
-      const int lr = threadIdx.x + j * kV2TB;
       y[j] = 0.0;
-      if (lr >= R)
-        continue;
-      for (int e = 0; e < E; ++e)
-        y[j] = __dadd_rn(y[j], __dmul_rn(av[lr * E + e], in[lr + hs + ao[lr * E + e]]));
+      ok[j] = threadIdx.x + j * kV2TB < R;
+    }
+    for (int e = 0; e < E; ++e)
+    {
+#pragma unroll
+      for (int j = 0; j < RPT; ++j)
+      {
+        const int lr = threadIdx.x + j * kV2TB;
+        if (ok[j])
+          y[j] = __dadd_rn(y[j], __dmul_rn(av[lr * E + e], in[lr + hs + ao[lr * E + e]]));
+      }
     }
   };
   // halo rows of dpad from the neighbours' exports (mode 0: d_new = fresh ? r : r + beta d; 1: x~)
@@ -819,7 +861,7 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
       else
       {
         const double rv = ex_r(nb, q, nside)[k];
-        v = sh.fresh[0] ? rv : __dadd_rn(rv, __dmul_rn(sh.beta[0], ex_d(nb, q, nside)[k]));
+        v = fresh ? rv : __dadd_rn(rv, __dmul_rn(beta, ex_d(nb, q, nside)[k]));
       }
       dpad[side == 0 ? k : H + R + k] = v;
     }
@@ -862,11 +904,12 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
     }
     cta_sum<kV2TB, 2>(sh, q2, 1, part);
     cl.sync();
-    cluster_total(cl, sh, part, 1, cs);
-    const double tt = sh.tot[0];
-    bool fin = kind == 1 || sqrt(tt) <= sh.target[0];
+    double cv[1];
+    warp_cluster_total(cl, part, 1, cs, cv);
+    const double tt = cv[0];
+    bool fin = kind == 1 || sqrt(tt) <= target;
     const bool rst = !fin;
-    if (kind == 0 && !fin && sqrt(tt) <= sh.target[0]) // krylov.cpp:98-102
+    if (kind == 0 && !fin && sqrt(tt) <= target) // krylov.cpp:98-102
       fin = true;
 #pragma unroll
     for (int j = 0; j < RPT; ++j)
@@ -891,21 +934,17 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
           ex_r(ex, static_cast<int>(it & 1), 1)[lr - (R - H)] = y[j];
       }
     }
-    __syncthreads();
-    if (threadIdx.x == 0)
+    if (fin)
     {
-      if (fin)
-      {
-        sh.state[0] = (kind == 1 && !(sqrt(tt) <= sh.target[0])) ? cMaxed : cConverged;
-        sh.sit[0] = it;
-      }
-      else if (rst)
-      {
-        sh.rho[0] = tt;
-        sh.fresh[0] = 1;
-      }
+      state = (kind == 1 && !(sqrt(tt) <= target)) ? cMaxed : cConverged;
+      sit = it;
     }
-    cl.sync();
+    else if (rst)
+    {
+      rho = tt;
+      fresh = 1;
+    }
+    cl.sync(); // restarted r exports visible; the slots are free again
   };
 
   int64_t it = 0;
@@ -913,15 +952,13 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
   {
     if (it >= P.maxit)
       break;
-    if (sh.state[0] == cRun && sqrt(sh.rho[0]) <= sh.target[0])
+    if (state == cRun && sqrt(rho) <= target)
       check(0, it);
-    if (sh.state[0] != cRun)
+    if (state != cRun)
       break;
     const int q = static_cast<int>(it & 1);
     // ---- phase A: d_new in place (own rows) + halo from exports, t = P d, w = A t
     double pa[2] = {0.0, 0.0};
-    const double beta = sh.beta[0];
-    const int fresh = sh.fresh[0];
 #pragma unroll
     for (int j = 0; j < RPT; ++j)
     {
@@ -954,20 +991,16 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
     }
     cta_sum<kV2TB, 2>(sh, pa, 2, part);
     cl.sync();
-    cluster_total(cl, sh, part, 2, cs);
-    const double curv = sh.tot[0], dd = sh.tot[1];
+    double ta[2];
+    warp_cluster_total(cl, part, 2, cs, ta);
+    const double curv = ta[0], dd = ta[1];
     if (!(curv > 1e-30 * dd)) // krylov.cpp:108
     {
-      __syncthreads();
-      if (threadIdx.x == 0)
-      {
-        sh.state[0] = cBreakdown;
-        sh.sit[0] = it;
-      }
-      __syncthreads();
+      state = cBreakdown;
+      sit = it;
       break;
     }
-    const double alpha = sh.rho[0] / curv;
+    const double alpha = rho / curv;
     // ---- phase B: x~ += alpha d, r -= alpha w, (r, r); export boundary r_{k+1}
     double pb[2] = {0.0, 0.0};
 #pragma unroll
@@ -987,20 +1020,17 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
     }
     cta_sum<kV2TB, 2>(sh, pb, 1, part + 2 * kCMaxM);
     cl.sync();
-    cluster_total(cl, sh, part + 2 * kCMaxM, 1, cs);
+    double tb2[1];
+    warp_cluster_total(cl, part + 2 * kCMaxM, 1, cs, tb2);
     ++it;
-    if (threadIdx.x == 0)
-    {
-      const double rn = sh.tot[0];
-      if (P.hist && rank == 0 && it - 1 < P.hist_cap)
-        P.hist[static_cast<int64_t>(p) * P.hist_cap + (it - 1)] = sqrt(rn) / sh.bnorm[0];
-      sh.beta[0] = rn / sh.rho[0];
-      sh.rho[0] = rn;
-      sh.fresh[0] = 0;
-    }
-    __syncthreads();
+    const double rn = tb2[0];
+    if (P.hist && rank == 0 && threadIdx.x == 0 && it - 1 < P.hist_cap)
+      P.hist[static_cast<int64_t>(p) * P.hist_cap + (it - 1)] = sqrt(rn) / bnorm;
+    beta = rn / rho; // krylov.cpp:118-119
+    rho = rn;
+    fresh = 0;
   }
-  if (sh.state[0] == cRun)
+  if (state == cRun)
     check(1, it);
   for (int j = 0; j < RPT; ++j)
   {
@@ -1008,7 +1038,7 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
     if (lr >= R)
       continue;
     const int64_t o = static_cast<int64_t>(p) * P.n + c0 + lr;
-    if (sh.state[0] == cZeroRhs)
+    if (state == cZeroRhs)
     {
       if (P.X)
         P.X[o] = 0.0;
@@ -1017,16 +1047,15 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
       if (P.REC)
         P.REC[o] = 0.0;
     }
-    else if (sh.state[0] != cBreakdown && P.REC)
+    else if (state != cBreakdown && P.REC)
       P.REC[o] = r[j];
   }
   if (rank == 0 && threadIdx.x == 0)
   {
-    const int st = sh.state[0];
-    P.iters[p] = sh.sit[0];
-    P.conv[p] = (st == cConverged || st == cZeroRhs) ? 1 : 0;
-    P.status[p] = st == cBreakdown ? MGPU_ERR_BREAKDOWN : MGPU_OK;
-    P.bd_iter[p] = st == cBreakdown ? sh.sit[0] : -1;
+    P.iters[p] = sit;
+    P.conv[p] = (state == cConverged || state == cZeroRhs) ? 1 : 0;
+    P.status[p] = state == cBreakdown ? MGPU_ERR_BREAKDOWN : MGPU_OK;
+    P.bd_iter[p] = state == cBreakdown ? sit : -1;
     atomicMax(P.loop_iters, static_cast<unsigned long long>(it));
   }
   cl.sync();
