@@ -310,6 +310,29 @@ __device__ void load_ell(DCsr M, int64_t r0, int64_t r1, int64_t n, int E, doubl
   }
 }
 
+// Entry-major ELL repack (v[t * rows + q]): consecutive rows -> consecutive
+// shared-memory words, so a warp's SpMV loads are bank-conflict free.
+__device__ void load_ell_em(DCsr M, int64_t r0, int64_t r1, int64_t n, int E, double *v, signed char *o, int TBn)
+{
+  const int64_t rows = r1 - r0;
+  for (int64_t q = threadIdx.x; q < rows; q += TBn)
+  {
+    const int64_t i = r0 + q;
+    int64_t k = 0, e = 0;
+    if (i >= 0 && i < n)
+    {
+      k = M.rp[i];
+      e = M.rp[i + 1];
+    }
+    for (int t = 0; t < E; ++t)
+    {
+      const bool has = k + t < e;
+      v[t * rows + q] = has ? M.v[k + t] : 0.0; // padding after the row's entries adds +0 last
+      o[t * rows + q] = has ? static_cast<signed char>(M.ci[k + t] - i) : 0;
+    }
+  }
+}
+
 template <int TB, int MT, int RPT>
 __global__ void __launch_bounds__(TB, 1) cg_cluster(ClParams P)
 {
@@ -723,14 +746,14 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
   double *left = rank > 0 ? cl.map_shared_rank(ex, rank - 1) : nullptr;       // neighbour exports
   double *right = rank + 1 < cs ? cl.map_shared_rank(ex, rank + 1) : nullptr;
 
-  load_ell(P.A[p], c0, c0 + R, P.n, P.ea, reinterpret_cast<double *>(raw + P.off_av),
-           reinterpret_cast<signed char *>(raw + P.off_ao), kV2TB);
+  load_ell_em(P.A[p], c0, c0 + R, P.n, P.ea, reinterpret_cast<double *>(raw + P.off_av),
+              reinterpret_cast<signed char *>(raw + P.off_ao), kV2TB);
   for (int st = 0; st < P.z; ++st)
   {
     const int hd = P.halo[st + 1];
-    load_ell(P.F[p * P.z + (P.z - 1 - st)], c0 - hd, c0 + R + hd, P.n, P.ef[st],
-             reinterpret_cast<double *>(raw + P.off_fv[st]), reinterpret_cast<signed char *>(raw + P.off_fo[st]),
-             kV2TB);
+    load_ell_em(P.F[p * P.z + (P.z - 1 - st)], c0 - hd, c0 + R + hd, P.n, P.ef[st],
+                reinterpret_cast<double *>(raw + P.off_fv[st]), reinterpret_cast<signed char *>(raw + P.off_fo[st]),
+                kV2TB);
   }
   double r[RPT], x[RPT], w[RPT], bv[RPT];
   double pk[2] = {0.0, 0.0};
@@ -801,7 +824,7 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
 #pragma unroll
         for (int j = 0; j < K; ++j)
           if (ok[j])
-            acc[j] = __dadd_rn(acc[j], __dmul_rn(fv[q[j] * E + e], in[q[j] + hs - hd + fo[q[j] * E + e]]));
+            acc[j] = __dadd_rn(acc[j], __dmul_rn(fv[e * span + q[j]], in[q[j] + hs - hd + fo[e * span + q[j]]]));
       }
 #pragma unroll
       for (int j = 0; j < K; ++j)
@@ -814,7 +837,7 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
           continue;
         double a = 0.0;
         for (int e = 0; e < E; ++e)
-          a = __dadd_rn(a, __dmul_rn(fv[qq * E + e], in[qq + hs - hd + fo[qq * E + e]]));
+          a = __dadd_rn(a, __dmul_rn(fv[e * span + qq], in[qq + hs - hd + fo[e * span + qq]]));
         out[qq] = a;
       }
       __syncthreads();
@@ -841,7 +864,7 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
       {
         const int lr = threadIdx.x + j * kV2TB;
         if (ok[j])
-          y[j] = __dadd_rn(y[j], __dmul_rn(av[lr * E + e], in[lr + hs + ao[lr * E + e]]));
+          y[j] = __dadd_rn(y[j], __dmul_rn(av[e * R + lr], in[lr + hs + ao[e * R + lr]]));
       }
     }
   };
