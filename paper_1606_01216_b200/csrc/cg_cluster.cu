@@ -112,6 +112,56 @@ __device__ __forceinline__ void cta_sum(ClShared &sh, double (&v)[NV], int nv, d
   }
 }
 
+// CTA sum of nv values, PUSHED into slot k * kCMaxCS + rank of every CTA's
+// `inbox` (one remote store per destination, issued before the barrier):
+// after the cluster barrier each CTA reduces its own, local inbox.
+template <int TB, int NV>
+__device__ __forceinline__ void cta_sum_push(ClShared &sh, double (&v)[NV], int nv, cgrp::cluster_group &cl,
+                                             double *inbox, int cs, int rank)
+{
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+  {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1)
+      v[k] = __dadd_rn(v[k], __shfl_xor_sync(0xffffffffu, v[k], off));
+  }
+  if (lane == 0)
+  {
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+      sh.red[warp][k] = v[k];
+  }
+  __syncthreads();
+  if (warp == 0)
+  {
+    for (int k = 0; k < nv; ++k)
+    {
+      double x = lane < TB / 32 ? sh.red[lane][k] : 0.0;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1)
+        x = __dadd_rn(x, __shfl_xor_sync(0xffffffffu, x, off));
+      if (lane < cs)
+        cl.map_shared_rank(inbox, lane)[k * kCMaxCS + rank] = x;
+    }
+  }
+}
+
+// After the barrier: tot[k] = sum over ranks (fixed butterfly) of the local inbox.
+__device__ __forceinline__ void warp_inbox_total(const double *inbox, int nv, int cs, double *out)
+{
+  const int lane = threadIdx.x & 31;
+  for (int k = 0; k < nv; ++k)
+  {
+    double v = lane < cs ? inbox[k * kCMaxCS + lane] : 0.0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1)
+      v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+    out[k] = v;
+  }
+}
+
 // After cluster.sync(): every warp forms tot[k] (k < nv) itself from the cs
 // remote slots with a fixed butterfly, so no CTA barrier / broadcast is needed.
 __device__ __forceinline__ void warp_cluster_total(cgrp::cluster_group &cl, const double *slot, int nv, int cs,
@@ -331,6 +381,40 @@ __device__ void load_ell_em(DCsr M, int64_t r0, int64_t r1, int64_t n, int E, do
       o[t * rows + q] = has ? static_cast<signed char>(M.ci[k + t] - i) : 0;
     }
   }
+}
+
+// Same, with the row's int8 column offsets packed into one 64-bit word (E <= 8):
+// one shared-memory load per row instead of E byte loads.
+__device__ void load_ell_em_packed(DCsr M, int64_t r0, int64_t r1, int64_t n, int E, double *v,
+                                   unsigned long long *o, int TBn)
+{
+  const int64_t rows = r1 - r0;
+  for (int64_t q = threadIdx.x; q < rows; q += TBn)
+  {
+    const int64_t i = r0 + q;
+    int64_t k = 0, e = 0;
+    if (i >= 0 && i < n)
+    {
+      k = M.rp[i];
+      e = M.rp[i + 1];
+    }
+    unsigned long long word = 0;
+    for (int t = 0; t < E; ++t)
+    {
+      const bool has = k + t < e;
+      v[t * rows + q] = has ? M.v[k + t] : 0.0;
+      const unsigned long long b =
+          has ? static_cast<unsigned long long>(static_cast<unsigned char>(static_cast<signed char>(M.ci[k + t] - i)))
+              : 0ull;
+      word |= b << (8 * t);
+    }
+    o[q] = word;
+  }
+}
+
+__device__ __forceinline__ int off8(unsigned long long w, int t)
+{
+  return static_cast<int>(static_cast<signed char>((w >> (8 * t)) & 0xffull));
 }
 
 template <int TB, int MT, int RPT>
@@ -722,6 +806,7 @@ struct V2Params
   double *hist;
   int64_t hist_cap;
   unsigned long long *loop_iters;
+  long long *prof; // optional [16] accumulated clock64 deltas per phase (cluster 0, rank 0, thread 0)
 };
 
 template <int RPT>
@@ -738,22 +823,35 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
   const int R = c1 > c0 ? static_cast<int>(c1 - c0) : 0;
   double *dpad = reinterpret_cast<double *>(raw + P.off_d); // rows [c0 - H, c1 + H)
   double *tb[2] = {reinterpret_cast<double *>(raw + P.off_t0), reinterpret_cast<double *>(raw + P.off_t1)};
-  double *part = reinterpret_cast<double *>(raw + P.off_part);                // [2 phases][2 * kCMaxM]
+  double *part = reinterpret_cast<double *>(raw + P.off_part); // inboxes [2 phases][2 * kCMaxM][kCMaxCS]
+  double *inboxA = part, *inboxB = part + 2 * kCMaxM * kCMaxCS;
   double *ex = reinterpret_cast<double *>(raw + P.off_ex);                    // exports
   auto ex_r = [&](double *base, int q, int side) { return base + ((0 * 2 + q) * 2 + side) * H; };
   auto ex_d = [&](double *base, int q, int side) { return base + ((1 * 2 + q) * 2 + side) * H; };
   auto ex_x = [&](double *base, int side) { return base + (4 * 2 + side) * H; };
-  double *left = rank > 0 ? cl.map_shared_rank(ex, rank - 1) : nullptr;       // neighbour exports
-  double *right = rank + 1 < cs ? cl.map_shared_rank(ex, rank + 1) : nullptr;
+  // boundary rows are PUSHED into the neighbours' import buffers (remote
+  // stores before the barrier), so halos are read from local shared memory.
+  double *left = rank > 0 ? cl.map_shared_rank(ex, rank - 1) : nullptr;       // left neighbour's imports
+  double *right = rank + 1 < cs ? cl.map_shared_rank(ex, rank + 1) : nullptr; // right neighbour's imports
+  // my row lr (boundary) -> the neighbour import slot that mirrors it
+  auto push = [&](auto sel, int q, int lr, double v) {
+    if (lr < H && left)
+      sel(left, q, 1)[lr] = v;
+    if (lr >= R - H && right)
+      sel(right, q, 0)[lr - (R - H)] = v;
+  };
+  auto sel_r = [&](double *b, int q, int side) { return ex_r(b, q, side); };
+  auto sel_d = [&](double *b, int q, int side) { return ex_d(b, q, side); };
+  auto sel_x = [&](double *b, int, int side) { return ex_x(b, side); };
 
-  load_ell_em(P.A[p], c0, c0 + R, P.n, P.ea, reinterpret_cast<double *>(raw + P.off_av),
-              reinterpret_cast<signed char *>(raw + P.off_ao), kV2TB);
+  load_ell_em_packed(P.A[p], c0, c0 + R, P.n, P.ea, reinterpret_cast<double *>(raw + P.off_av),
+                     reinterpret_cast<unsigned long long *>(raw + P.off_ao), kV2TB);
   for (int st = 0; st < P.z; ++st)
   {
     const int hd = P.halo[st + 1];
-    load_ell_em(P.F[p * P.z + (P.z - 1 - st)], c0 - hd, c0 + R + hd, P.n, P.ef[st],
-                reinterpret_cast<double *>(raw + P.off_fv[st]), reinterpret_cast<signed char *>(raw + P.off_fo[st]),
-                kV2TB);
+    load_ell_em_packed(P.F[p * P.z + (P.z - 1 - st)], c0 - hd, c0 + R + hd, P.n, P.ef[st],
+                       reinterpret_cast<double *>(raw + P.off_fv[st]),
+                       reinterpret_cast<unsigned long long *>(raw + P.off_fo[st]), kV2TB);
   }
   double r[RPT], x[RPT], w[RPT], bv[RPT];
   double pk[2] = {0.0, 0.0};
@@ -769,23 +867,15 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
     {
       dpad[H + lr] = bv[j];
       pk[0] = __dadd_rn(pk[0], __dmul_rn(bv[j], bv[j]));
-      if (lr < H)
-      {
-        ex_r(ex, 0, 0)[lr] = bv[j];
-        ex_d(ex, 0, 0)[lr] = bv[j];
-      }
-      if (lr >= R - H)
-      {
-        ex_r(ex, 0, 1)[lr - (R - H)] = bv[j];
-        ex_d(ex, 0, 1)[lr - (R - H)] = bv[j];
-      }
+      push(sel_r, 0, lr, bv[j]);
+      push(sel_d, 0, lr, bv[j]);
     }
   }
-  cta_sum<kV2TB, 2>(sh, pk, 1, part);
+  cta_sum_push<kV2TB, 2>(sh, pk, 1, cl, inboxA, cs, rank);
   cl.sync();
   // per-system scalars live in registers; every thread derives identical values
   double tv[2];
-  warp_cluster_total(cl, part, 1, cs, tv);
+  warp_inbox_total(inboxA, 1, cs, tv);
   const double bnorm = sqrt(tv[0]);
   double rho = tv[0], beta = 0.0;
   const double target = P.rtol * bnorm;
@@ -802,7 +892,7 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
       const int hd = P.halo[st + 1];
       const int E = P.ef[st];
       const double *fv = reinterpret_cast<const double *>(raw + P.off_fv[st]);
-      const signed char *fo = reinterpret_cast<const signed char *>(raw + P.off_fo[st]);
+      const unsigned long long *fo = reinterpret_cast<const unsigned long long *>(raw + P.off_fo[st]);
       double *out = tb[st & 1];
       const int span = R + 2 * hd;
       // RPT + 1 rows per thread, entries outer / rows inner: independent
@@ -811,6 +901,7 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
       int q[K];
       bool ok[K];
       double acc[K];
+      unsigned long long ow[K];
 #pragma unroll
       for (int j = 0; j < K; ++j)
       {
@@ -818,13 +909,14 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
         const int64_t i = c0 - hd + q[j];
         ok[j] = q[j] < span && i >= 0 && i < P.n;
         acc[j] = 0.0;
+        ow[j] = ok[j] ? fo[q[j]] : 0ull;
       }
       for (int e = 0; e < E; ++e)
       {
 #pragma unroll
         for (int j = 0; j < K; ++j)
           if (ok[j])
-            acc[j] = __dadd_rn(acc[j], __dmul_rn(fv[e * span + q[j]], in[q[j] + hs - hd + fo[e * span + q[j]]]));
+            acc[j] = __dadd_rn(acc[j], __dmul_rn(fv[e * span + q[j]], in[q[j] + hs - hd + off8(ow[j], e)]));
       }
 #pragma unroll
       for (int j = 0; j < K; ++j)
@@ -836,8 +928,9 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
         if (i < 0 || i >= P.n)
           continue;
         double a = 0.0;
+        const unsigned long long w1 = fo[qq];
         for (int e = 0; e < E; ++e)
-          a = __dadd_rn(a, __dmul_rn(fv[e * span + qq], in[qq + hs - hd + fo[e * span + qq]]));
+          a = __dadd_rn(a, __dmul_rn(fv[e * span + qq], in[qq + hs - hd + off8(w1, e)]));
         out[qq] = a;
       }
       __syncthreads();
@@ -848,14 +941,16 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
   };
   auto apply_a = [&](const double *in, int hs, double (&y)[RPT]) {
     const double *av = reinterpret_cast<const double *>(raw + P.off_av);
-    const signed char *ao = reinterpret_cast<const signed char *>(raw + P.off_ao);
+    const unsigned long long *ao = reinterpret_cast<const unsigned long long *>(raw + P.off_ao);
     const int E = P.ea;
     bool ok[RPT];
+    unsigned long long ow[RPT];
 #pragma unroll
     for (int j = 0; j < RPT; ++j)
     {
       y[j] = 0.0;
       ok[j] = threadIdx.x + j * kV2TB < R;
+      ow[j] = ok[j] ? ao[threadIdx.x + j * kV2TB] : 0ull;
     }
     for (int e = 0; e < E; ++e)
     {
@@ -864,7 +959,7 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
       {
         const int lr = threadIdx.x + j * kV2TB;
         if (ok[j])
-          y[j] = __dadd_rn(y[j], __dmul_rn(av[e * R + lr], in[lr + hs + ao[e * R + lr]]));
+          y[j] = __dadd_rn(y[j], __dmul_rn(av[e * R + lr], in[lr + hs + off8(ow[j], e)]));
       }
     }
   };
@@ -876,15 +971,13 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
       const int64_t i = side == 0 ? c0 - H + k : c1 + k;
       if (i < 0 || i >= P.n)
         continue;
-      double *nb = side == 0 ? left : right;
-      const int nside = side == 0 ? 1 : 0;
       double v;
       if (mode == 1)
-        v = ex_x(nb, nside)[k];
+        v = ex_x(ex, side)[k];
       else
       {
-        const double rv = ex_r(nb, q, nside)[k];
-        v = fresh ? rv : __dadd_rn(rv, __dmul_rn(beta, ex_d(nb, q, nside)[k]));
+        const double rv = ex_r(ex, q, side)[k];
+        v = fresh ? rv : __dadd_rn(rv, __dmul_rn(beta, ex_d(ex, q, side)[k]));
       }
       dpad[side == 0 ? k : H + R + k] = v;
     }
@@ -899,10 +992,7 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
       if (lr < R)
       {
         dpad[H + lr] = x[j]; // d_old is not needed afterwards: the single column finishes or restarts
-        if (lr < H)
-          ex_x(ex, 0)[lr] = x[j];
-        if (lr >= R - H)
-          ex_x(ex, 1)[lr - (R - H)] = x[j];
+        push(sel_x, 0, lr, x[j]);
       }
     }
     cl.sync();
@@ -925,10 +1015,10 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
         q2[0] = __dadd_rn(q2[0], __dmul_rn(y[j], y[j]));
       }
     }
-    cta_sum<kV2TB, 2>(sh, q2, 1, part);
+    cta_sum_push<kV2TB, 2>(sh, q2, 1, cl, inboxA, cs, rank);
     cl.sync();
     double cv[1];
-    warp_cluster_total(cl, part, 1, cs, cv);
+    warp_inbox_total(inboxA, 1, cs, cv);
     const double tt = cv[0];
     bool fin = kind == 1 || sqrt(tt) <= target;
     const bool rst = !fin;
@@ -951,10 +1041,7 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
       else
       {
         r[j] = y[j]; // restart from the true residual, d = r
-        if (lr < H)
-          ex_r(ex, static_cast<int>(it & 1), 0)[lr] = y[j];
-        if (lr >= R - H)
-          ex_r(ex, static_cast<int>(it & 1), 1)[lr - (R - H)] = y[j];
+        push(sel_r, static_cast<int>(it & 1), lr, y[j]);
       }
     }
     if (fin)
@@ -970,6 +1057,17 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
     cl.sync(); // restarted r exports visible; the slots are free again
   };
 
+  const bool prof = P.prof && blockIdx.x == 0 && threadIdx.x == 0;
+  long long pacc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long tmark = clock64();
+  auto mark = [&](int k) {
+    if (prof)
+    {
+      const long long now = clock64();
+      pacc[k] += now - tmark;
+      tmark = now;
+    }
+  };
   int64_t it = 0;
   for (;;)
   {
@@ -979,6 +1077,7 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
       check(0, it);
     if (state != cRun)
       break;
+    mark(0);
     const int q = static_cast<int>(it & 1);
     // ---- phase A: d_new in place (own rows) + halo from exports, t = P d, w = A t
     double pa[2] = {0.0, 0.0};
@@ -990,16 +1089,15 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
       {
         const double dn = fresh ? r[j] : __dadd_rn(r[j], __dmul_rn(beta, dpad[H + lr]));
         dpad[H + lr] = dn;
-        if (lr < H)
-          ex_d(ex, q ^ 1, 0)[lr] = dn;
-        if (lr >= R - H)
-          ex_d(ex, q ^ 1, 1)[lr - (R - H)] = dn;
+        push(sel_d, q ^ 1, lr, dn);
       }
     }
     fill_halo(0, q);
     __syncthreads();
+    mark(1);
     int hs;
     const double *t = chain(hs);
+    mark(2);
     apply_a(t, hs, w);
 #pragma unroll
     for (int j = 0; j < RPT; ++j)
@@ -1012,10 +1110,14 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
         pa[1] = __dadd_rn(pa[1], __dmul_rn(dn, dn));
       }
     }
-    cta_sum<kV2TB, 2>(sh, pa, 2, part);
+    mark(3);
+    cta_sum_push<kV2TB, 2>(sh, pa, 2, cl, inboxA, cs, rank);
+    mark(4);
     cl.sync();
+    mark(5);
     double ta[2];
-    warp_cluster_total(cl, part, 2, cs, ta);
+    warp_inbox_total(inboxA, 2, cs, ta);
+    mark(6);
     const double curv = ta[0], dd = ta[1];
     if (!(curv > 1e-30 * dd)) // krylov.cpp:108
     {
@@ -1035,16 +1137,16 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
         x[j] = __dadd_rn(x[j], __dmul_rn(alpha, dpad[H + lr]));
         r[j] = __dadd_rn(r[j], __dmul_rn(-alpha, w[j]));
         pb[0] = __dadd_rn(pb[0], __dmul_rn(r[j], r[j]));
-        if (lr < H)
-          ex_r(ex, q ^ 1, 0)[lr] = r[j];
-        if (lr >= R - H)
-          ex_r(ex, q ^ 1, 1)[lr - (R - H)] = r[j];
+        push(sel_r, q ^ 1, lr, r[j]);
       }
     }
-    cta_sum<kV2TB, 2>(sh, pb, 1, part + 2 * kCMaxM);
+    mark(7);
+    cta_sum_push<kV2TB, 2>(sh, pb, 1, cl, inboxB, cs, rank);
     cl.sync();
+    mark(8);
     double tb2[1];
-    warp_cluster_total(cl, part + 2 * kCMaxM, 1, cs, tb2);
+    warp_inbox_total(inboxB, 1, cs, tb2);
+    mark(9);
     ++it;
     const double rn = tb2[0];
     if (P.hist && rank == 0 && threadIdx.x == 0 && it - 1 < P.hist_cap)
@@ -1053,6 +1155,9 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
     rho = rn;
     fresh = 0;
   }
+  if (prof)
+    for (int k = 0; k < 10; ++k)
+      P.prof[k] = pacc[k];
   if (state == cRun)
     check(1, it);
   for (int j = 0; j < RPT; ++j)
@@ -1164,15 +1269,15 @@ bool v2_solve(mgpu_ctx *ctx, V2Params P, size_t budget)
     Q.off_d = take(sizeof(double) * static_cast<size_t>(rb + 2 * Q.H));
     Q.off_t0 = take(Q.z >= 1 ? sizeof(double) * static_cast<size_t>(rb + 2 * Q.halo[1]) : 16);
     Q.off_t1 = take(Q.z >= 2 ? sizeof(double) * static_cast<size_t>(rb + 2 * Q.halo[2]) : 16);
-    Q.off_part = take(sizeof(double) * 4 * kCMaxM);
+    Q.off_part = take(sizeof(double) * 4 * kCMaxM * kCMaxCS);
     Q.off_ex = take(sizeof(double) * 10 * static_cast<size_t>(std::max(Q.H, 1)));
     Q.off_av = take(sizeof(double) * static_cast<size_t>(rb) * Q.ea);
-    Q.off_ao = take(static_cast<size_t>(rb) * Q.ea);
+    Q.off_ao = take(sizeof(unsigned long long) * static_cast<size_t>(rb));
     for (int st = 0; st < Q.z; ++st)
     {
       const size_t rows = static_cast<size_t>(rb + 2 * Q.halo[st + 1]);
       Q.off_fv[st] = take(sizeof(double) * rows * Q.ef[st]);
-      Q.off_fo[st] = take(rows * Q.ef[st]);
+      Q.off_fo[st] = take(sizeof(unsigned long long) * rows);
     }
     if (off > budget)
       continue;
@@ -1227,7 +1332,10 @@ int cg_cluster_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, cons
   }
   int cdev0 = 0;
   MG_CUDA(cudaDeviceGetAttribute(&cdev0, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
-  if (m == 1 && ctx->cg_path != 3)
+  bool narrow = ea <= 8;
+  for (int st = 0; st < z; ++st)
+    narrow = narrow && ef[st] <= 8;
+  if (m == 1 && ctx->cg_path != 3 && narrow)
   {
     V2Params V{};
     V.l = l;
@@ -1254,6 +1362,7 @@ int cg_cluster_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, cons
     V.hist = d_hist;
     V.hist_cap = hist_cap;
     V.loop_iters = d_loop;
+    V.prof = ctx->prof_dev;
     if (v2_solve(ctx, V, static_cast<size_t>(cdev0) - sizeof(ClShared) - 1024))
       return 2;
   }

@@ -1,5 +1,6 @@
 // Context, error state, CSR residency and the deterministic reduction.
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -258,6 +259,11 @@ int mgpu_ctx_create(int device, void *stream, mgpu_ctx **out)
     }
     MG_CUDA(cudaEventCreate(&ctx->ev0));
     MG_CUDA(cudaEventCreate(&ctx->ev1));
+    if (std::getenv("MGPU_PROFILE_PHASES"))
+    {
+      MG_CUDA(cudaMalloc(reinterpret_cast<void **>(&ctx->prof_dev), 16 * sizeof(long long)));
+      MG_CUDA(cudaMemset(ctx->prof_dev, 0, 16 * sizeof(long long)));
+    }
   });
   if (st != MGPU_OK)
   {
@@ -281,6 +287,16 @@ int mgpu_ctx_destroy(mgpu_ctx *ctx)
     cudaEventDestroy(ctx->ev1);
   if (ctx->own_stream)
     cudaStreamDestroy(ctx->stream);
+  if (ctx->prof_dev)
+  {
+    long long h[16] = {0};
+    cudaMemcpy(h, ctx->prof_dev, sizeof h, cudaMemcpyDeviceToHost);
+    std::fprintf(stderr, "MGPU_PROFILE_PHASES cycles:");
+    for (int k = 0; k < 10; ++k)
+      std::fprintf(stderr, " %lld", h[k]);
+    std::fprintf(stderr, "\n");
+    cudaFree(ctx->prof_dev);
+  }
   delete ctx;
   return MGPU_OK;
 }

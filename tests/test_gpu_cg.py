@@ -28,8 +28,13 @@ def test_path_selection(mg, oracle, cg_path):
     A = oracle.shifted_operator(M, D, K, 100.0)
     P = oracle.spai_ls(A, None, 1)
     mg.pcg_solve(A, [P], np.ones(600), maxit=5)
-    assert mg.default_context().last_cg_path == {"auto": "cluster", "cluster_v1": "cluster_v1",
+    # A^2-pattern factor: 10 entries per row -> the shared-memory cluster kernel (v1); v2 packs <= 8
+    assert mg.default_context().last_cg_path == {"auto": "cluster_v1", "cluster_v1": "cluster_v1",
                                                   "banded": "banded", "general": "general"}[cg_path]
+    if cg_path == "auto":
+        P1 = oracle.spai_ls(A, None, 0)
+        mg.pcg_solve(A, [P1], np.ones(600), maxit=5)
+        assert mg.default_context().last_cg_path == "cluster"
     # a wide operator (bandwidth > 64) always takes the general kernel
     from oracle import Csr
     rng = np.random.default_rng(9)
