@@ -85,9 +85,11 @@ int mgpu_last_cg_timing(const mgpu_ctx *ctx, double *ms, int64_t *iterations);
  * barriers per iteration); otherwise the general CSR kernel.
  * 1 = always the general kernel, 2 = the banded grid kernel (no cluster),
  * 3 = cluster kernel v1 only (vectors in shared memory; v2 keeps them in
- * registers and is preferred for single right-hand sides).
- * mgpu_last_cg_path reports 2 (cluster v2), 3 (cluster v1), 0 (banded grid)
- * or 1 (general). */
+ * registers and is preferred for single right-hand sides), 4 = the streaming
+ * kernel (TMA bulk copies into double-buffered shared memory; the automatic
+ * choice for banded systems too large for the cluster kernels).
+ * mgpu_last_cg_path reports 2 (cluster v2), 3 (cluster v1), 4 (stream),
+ * 0 (banded grid) or 1 (general). */
 int mgpu_ctx_set_cg_path(mgpu_ctx *ctx, int path);
 int mgpu_last_cg_path(const mgpu_ctx *ctx);
 

@@ -758,8 +758,8 @@ struct BandShared
 };
 
 // Iterate this block's row segments [rs, re) of point p (host plan in shared memory).
-template <class S, class F>
-__device__ __forceinline__ void for_segments(const BandParams &, const S &sh, F &&fn)
+template <class PT, class S, class F>
+__device__ __forceinline__ void for_segments(const PT &, const S &sh, F &&fn)
 {
   for (int q = 0; q < sh.nseg; ++q)
   {
@@ -813,16 +813,22 @@ __device__ __forceinline__ void begin_point(BandShared<TB> &sh)
 }
 
 template <int TB>
-__device__ __forceinline__ void end_point(const BandParams &P, BandShared<TB> &sh, int p, int nv)
+__device__ __forceinline__ void end_point(double *partial, BandShared<TB> &sh, int p, int nv)
 {
   if (threadIdx.x < nv)
-    P.partial[(static_cast<int64_t>(p) * 2 * kMaxM + threadIdx.x) * gridDim.x + blockIdx.x] = sh.acc[threadIdx.x];
+    partial[(static_cast<int64_t>(p) * 2 * kMaxM + threadIdx.x) * gridDim.x + blockIdx.x] = sh.acc[threadIdx.x];
   __syncthreads();
 }
 
-// After a barrier: tot[p][k] = sum over blocks (fixed order) for live points.
 template <int TB>
-__device__ void reduce_blocks(const BandParams &P, BandShared<TB> &sh, int nk)
+__device__ __forceinline__ void end_point(const BandParams &P, BandShared<TB> &sh, int p, int nv)
+{
+  end_point(P.partial, sh, p, nv);
+}
+
+// After a barrier: tot[p][k] = sum over blocks (fixed order) for live points.
+template <int TB, class PT>
+__device__ void reduce_blocks(const PT &P, BandShared<TB> &sh, int nk)
 {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int npairs = P.l * nk;
@@ -1130,7 +1136,7 @@ __global__ void __launch_bounds__(TB, 1) cg_banded(BandParams P)
     end_point(P, sh, p, m);
   });
   grid.sync();
-  reduce_blocks<TB>(P, sh, m);
+  reduce_blocks<TB, BandParams>(P, sh, m);
   for (int s = threadIdx.x; s < S; s += TB)
   {
     const double bb = sh.tot[(s / m) * 2 * kMaxM + s % m];
@@ -1172,7 +1178,7 @@ __global__ void __launch_bounds__(TB, 1) cg_banded(BandParams P)
     {
       band_phase_a<TB, MT, RPT, true>(P, sh, smem_dyn, nullptr, nullptr);
       grid.sync();
-      reduce_blocks<TB>(P, sh, m);
+      reduce_blocks<TB, BandParams>(P, sh, m);
       for (int s = threadIdx.x; s < S; s += TB)
       {
         if (!(sh.state[s] == kRun && sqrt(sh.rho[s]) <= sh.target[s]))
@@ -1231,7 +1237,7 @@ __global__ void __launch_bounds__(TB, 1) cg_banded(BandParams P)
     // ---- phase A: d_new, w = A P d_new, (d, w), (d, d)
     band_phase_a<TB, MT, RPT, false>(P, sh, smem_dyn, d_old, d_new);
     grid.sync();
-    reduce_blocks<TB>(P, sh, 2 * m);
+    reduce_blocks<TB, BandParams>(P, sh, 2 * m);
     for (int s = threadIdx.x; s < S; s += TB)
     {
       if (sh.state[s] != kRun)
@@ -1251,7 +1257,7 @@ __global__ void __launch_bounds__(TB, 1) cg_banded(BandParams P)
     // ---- phase B
     band_phase_b<TB, MT, RPT>(P, sh, d_new);
     grid.sync();
-    reduce_blocks<TB>(P, sh, m);
+    reduce_blocks<TB, BandParams>(P, sh, m);
     ++it;
     for (int s = threadIdx.x; s < S; s += TB)
     {
@@ -1286,7 +1292,7 @@ __global__ void __launch_bounds__(TB, 1) cg_banded(BandParams P)
   {
     band_phase_a<TB, MT, RPT, true>(P, sh, smem_dyn, nullptr, nullptr);
     grid.sync();
-    reduce_blocks<TB>(P, sh, m);
+    reduce_blocks<TB, BandParams>(P, sh, m);
     for (int s = threadIdx.x; s < S; s += TB)
     {
       if (sh.state[s] != kRun)
@@ -1339,6 +1345,736 @@ __global__ void __launch_bounds__(TB, 1) cg_banded(BandParams P)
     if (threadIdx.x == 0)
       *P.loop_iters = it;
   }
+}
+
+// =====================================================================
+// Streaming kernel for HBM-resident banded systems (cg_stream).
+//   * operators in PADDED ROW-MAJOR ELL: values [row][Epad] (Epad even) and
+//     the row's int8 column offsets packed in one u64, PADR zero rows at both
+//     ends -> every chunk's operator rows are ONE contiguous, 16B-aligned range
+//     (no row_ptr, no column index stream: 8 Epad + 8 bytes per row);
+//   * vectors interleaved [point][PADR + row][rhs], PADR zero rows per side;
+//   * per phase, each CTA walks its rows in chunks of CH = 512 * RPT rows; the
+//     inputs of chunk i+1 are fetched with cp.async.bulk (TMA bulk copies,
+//     mbarrier transaction counts) into the other half of a double buffer
+//     while the CTA computes chunk i from shared memory -> the copy engine
+//     keeps HBM busy independent of warp occupancy.
+// Control flow, reductions and arithmetic are those of cg_banded.
+// =====================================================================
+constexpr int kPadR = 64;
+
+__device__ __forceinline__ uint32_t sm_addr(const void *p)
+{
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sm_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+  asm volatile("{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+               "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+               "@!p bra WAIT_%=;\n\t}" ::"r"(sm_addr(bar)),
+               "r"(parity)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   sm_addr(dst)),
+               "l"(src), "r"(bytes), "r"(sm_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_async_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+struct PEll
+{
+  const double *v;             // logical row 0 (PADR zero rows before / after)
+  const unsigned long long *o; // packed int8 offsets, `ow` words per row
+  int E;                       // values per row (even, <= 16)
+  int ow;                      // 1 (E <= 8) or 2 (E <= 16)
+};
+
+struct StreamParams
+{
+  int l, m, z, rpt, ch; // ch: rows per chunk (<= block size)
+  int64_t n, ldv; // ldv = (n + 2 PADR) * m: doubles per point block
+  int halo[kMaxZ + 1];
+  int hmax;
+  const PEll *A, *F; // [l], [l * z] newest first
+  double rtol;
+  int64_t maxit;
+  // vectors: logical (point p, row i, col c) at base + p * ldv + (PADR + i) * m + c
+  const double *b;
+  double *xt, *r, *dbuf0, *dbuf1, *w, *sol;
+  double *partial;
+  const Seg *seg;
+  const int2 *pblk;
+  double *X, *REC, *TR;
+  int64_t *iters;
+  int *conv, *status;
+  int64_t *bd_iter;
+  double *hist;
+  int64_t hist_cap;
+  int64_t *loop_iters;
+  // shared-memory carve-up (bytes): two input buffers (phase A layout and
+  // phase B layout alias) + stage buffers
+  size_t buf_bytes, off_stage0, off_stage1, off_stage2;
+  size_t a_vr, a_vd, a_fv[kMaxZ], a_fo[kMaxZ], a_av, a_ao; // phase A offsets inside a buffer
+  size_t b_x, b_d, b_r, b_w;                               // phase B offsets inside a buffer
+};
+
+__device__ __forceinline__ const double *vrow(const StreamParams &P, const double *base, int p, int64_t i)
+{
+  return base + static_cast<int64_t>(p) * P.ldv + (kPadR + i) * P.m;
+}
+
+// chunk iterator over the block's segments
+struct ChunkIt
+{
+  int seg;
+  int64_t c0;
+};
+
+template <int TB>
+__device__ __forceinline__ bool chunk_next(const BandShared<TB> &sh, int64_t CH, ChunkIt &it, int &p, int64_t &c0,
+                                           int64_t &c1)
+{
+  while (it.seg < sh.nseg)
+  {
+    const Seg g = sh.seg[it.seg];
+    if (!sh.pmask[g.p] || it.c0 >= g.re)
+    {
+      ++it.seg;
+      it.c0 = it.seg < sh.nseg ? sh.seg[it.seg].rs : 0;
+      continue;
+    }
+    p = g.p;
+    c0 = it.c0;
+    c1 = min(static_cast<int64_t>(g.re), c0 + CH);
+    it.c0 = c1;
+    return true;
+  }
+  return false;
+}
+
+__device__ __forceinline__ int64_t even_up(int64_t x) { return (x + 1) & ~static_cast<int64_t>(1); }
+
+// Producer: issue the bulk copies of one chunk's inputs into buffer `buf`.
+// kind 0: phase A step, 1: phase A check (x~ instead of r, no d), 2: phase B.
+template <int TB>
+__device__ void stream_issue(const StreamParams &P, unsigned char *buf, uint64_t *bar, int kind, int p, int64_t c0,
+                             int64_t c1, const double *dold, const double *dnew)
+{
+  const int m = P.m;
+  uint32_t bytes = 0;
+  if (kind == 2)
+  {
+    const int64_t rows = even_up(c1 - c0);
+    const uint32_t vb = static_cast<uint32_t>(rows * m * 8);
+    bytes = 4 * vb;
+    mbar_expect_tx(bar, bytes);
+    bulk_g2s(buf + P.b_x, vrow(P, P.xt, p, c0), vb, bar);
+    bulk_g2s(buf + P.b_d, vrow(P, dnew, p, c0), vb, bar);
+    bulk_g2s(buf + P.b_r, vrow(P, P.r, p, c0), vb, bar);
+    bulk_g2s(buf + P.b_w, vrow(P, P.w, p, c0), vb, bar);
+    return;
+  }
+  const int H0 = P.hmax;
+  const int64_t vrows = even_up(c1 - c0 + 2 * H0);
+  const uint32_t vb = static_cast<uint32_t>(vrows * m * 8);
+  uint32_t total = kind == 0 ? 2 * vb : vb;
+  for (int st = 0; st < P.z; ++st)
+  {
+    const int hd = P.halo[st + 1];
+    const PEll F = P.F[p * P.z + (P.z - 1 - st)];
+    const int64_t rows = even_up(c1 - c0 + 2 * hd);
+    total += static_cast<uint32_t>(rows * F.E * 8 + rows * F.ow * 8);
+  }
+  {
+    const PEll A = P.A[p];
+    const int64_t rows = even_up(c1 - c0);
+    total += static_cast<uint32_t>(rows * A.E * 8 + rows * A.ow * 8);
+  }
+  mbar_expect_tx(bar, total);
+  bulk_g2s(buf + P.a_vr, vrow(P, kind == 0 ? P.r : P.xt, p, c0 - H0), vb, bar);
+  if (kind == 0)
+    bulk_g2s(buf + P.a_vd, vrow(P, dold, p, c0 - H0), vb, bar);
+  for (int st = 0; st < P.z; ++st)
+  {
+    const int hd = P.halo[st + 1];
+    const PEll F = P.F[p * P.z + (P.z - 1 - st)];
+    const int64_t rows = even_up(c1 - c0 + 2 * hd);
+    bulk_g2s(buf + P.a_fv[st], F.v + (c0 - hd) * F.E, static_cast<uint32_t>(rows * F.E * 8), bar);
+    bulk_g2s(buf + P.a_fo[st], F.o + (c0 - hd) * F.ow, static_cast<uint32_t>(rows * F.ow * 8), bar);
+  }
+  const PEll A = P.A[p];
+  const int64_t rows = even_up(c1 - c0);
+  bulk_g2s(buf + P.a_av, A.v + c0 * A.E, static_cast<uint32_t>(rows * A.E * 8), bar);
+  bulk_g2s(buf + P.a_ao, A.o + c0 * A.ow, static_cast<uint32_t>(rows * A.ow * 8), bar);
+}
+
+__device__ __forceinline__ int off8s(unsigned long long w, int t)
+{
+  return static_cast<int>(static_cast<signed char>((w >> (8 * t)) & 0xffull));
+}
+__device__ __forceinline__ int off16(unsigned long long w0, unsigned long long w1, int t)
+{
+  return t < 8 ? off8s(w0, t) : off8s(w1, t - 8);
+}
+
+// One pipelined pass over the block's chunks.  kind: 0 phase A (step),
+// 1 phase A (true-residual check), 2 phase B.
+template <int TB, int MT, int RPT>
+__device__ void stream_pass(const StreamParams &P, BandShared<TB> &sh, unsigned char *smem, uint64_t *bars,
+                            uint32_t &phase_bits, int kind, const double *dold, double *dnew)
+{
+  const int64_t CH = P.ch;
+  const int m = P.m;
+  ChunkIt prod{0, sh.nseg > 0 ? static_cast<int64_t>(sh.seg[0].rs) : 0};
+  ChunkIt cons = prod;
+  int pp, cp;
+  int64_t pc0, pc1, cc0, cc1;
+  // prologue: chunk 0 -> buffer 0
+  __syncthreads();
+  bool have_next = chunk_next(sh, CH, prod, pp, pc0, pc1);
+  if (threadIdx.x == 0)
+    fence_async_global(); // generic stores of the previous phase -> async-proxy (bulk copy) reads
+  if (threadIdx.x == 0 && have_next)
+  {
+    fence_async_shared();
+    stream_issue<TB>(P, smem, &bars[0], kind, pp, pc0, pc1, dold, dnew);
+  }
+  int k = 0;
+  int cur_p = -1;
+  while (chunk_next(sh, CH, cons, cp, cc0, cc1))
+  {
+    const int bi = k & 1;
+    // prefetch chunk k + 1 into the other buffer (free: its last use ended at the
+    // __syncthreads closing chunk k - 1)
+    have_next = chunk_next(sh, CH, prod, pp, pc0, pc1);
+    if (threadIdx.x == 0 && have_next)
+    {
+      fence_async_shared();
+      stream_issue<TB>(P, smem + (bi ^ 1) * P.buf_bytes, &bars[bi ^ 1], kind, pp, pc0, pc1, dold, dnew);
+    }
+    mbar_wait(&bars[bi], (phase_bits >> bi) & 1u);
+    phase_bits ^= 1u << bi;
+    unsigned char *buf = smem + bi * P.buf_bytes;
+    if (cp != cur_p)
+    {
+      if (cur_p >= 0)
+        end_point(P.partial, sh, cur_p, kind == 2 ? m : (kind == 1 ? m : 2 * m));
+      begin_point(sh);
+      cur_p = cp;
+    }
+    const int64_t base_i = cc0;
+    const int R = static_cast<int>(cc1 - cc0);
+    if (kind == 2)
+    {
+      const double *xs = reinterpret_cast<const double *>(buf + P.b_x);
+      const double *ds = reinterpret_cast<const double *>(buf + P.b_d);
+      const double *rs = reinterpret_cast<const double *>(buf + P.b_r);
+      const double *ws = reinterpret_cast<const double *>(buf + P.b_w);
+      bool run[MT];
+      double al[MT];
+#pragma unroll
+      for (int c = 0; c < MT; ++c)
+      {
+        run[c] = c < m && sh.state[cp * m + c] == kRun;
+        al[c] = run[c] ? sh.alpha[cp * m + c] : 0.0;
+      }
+      double pk[MT];
+#pragma unroll
+      for (int c = 0; c < MT; ++c)
+        pk[c] = 0.0;
+#pragma unroll
+      for (int j = 0; j < RPT; ++j)
+      {
+        const int lr = threadIdx.x + j * TB;
+        if (lr >= R)
+          break;
+#pragma unroll
+        for (int c = 0; c < MT; ++c)
+          if (run[c])
+          {
+            const int q = lr * m + c;
+            const double xn = __dadd_rn(xs[q], __dmul_rn(al[c], ds[q]));
+            const double rn = __dadd_rn(rs[q], __dmul_rn(-al[c], ws[q]));
+            double *xg = const_cast<double *>(vrow(P, P.xt, cp, base_i + lr)) + c;
+            double *rg = const_cast<double *>(vrow(P, P.r, cp, base_i + lr)) + c;
+            __stcg(xg, xn);
+            __stcg(rg, rn);
+            pk[c] = __dadd_rn(pk[c], __dmul_rn(rn, rn));
+          }
+      }
+      chunk_sum<TB, MT>(sh, pk, m);
+    }
+    else
+    {
+      const int H0 = P.hmax;
+      const double *vr = reinterpret_cast<const double *>(buf + P.a_vr);
+      const double *vd = reinterpret_cast<const double *>(buf + P.a_vd);
+      double *s0 = reinterpret_cast<double *>(smem + P.off_stage0);
+      double *sA = reinterpret_cast<double *>(smem + P.off_stage1);
+      double *sB = reinterpret_cast<double *>(smem + P.off_stage2);
+      double be[MT];
+      bool fr[MT];
+#pragma unroll
+      for (int c = 0; c < MT; ++c)
+      {
+        const int s = cp * m + c;
+        fr[c] = c < m && sh.fresh[s];
+        be[c] = c < m ? sh.beta[s] : 0.0;
+      }
+      // stage 0 rows [c0 - H0, c1 + H0)
+      const int span0 = R + 2 * H0;
+      for (int q = threadIdx.x; q < span0; q += TB)
+      {
+        const int64_t i = base_i - H0 + q;
+#pragma unroll
+        for (int c = 0; c < MT; ++c)
+        {
+          if (c >= m)
+            break;
+          double v;
+          if (kind == 1)
+            v = vr[q * m + c];
+          else
+          {
+            v = fr[c] ? vr[q * m + c] : __dadd_rn(vr[q * m + c], __dmul_rn(be[c], vd[q * m + c]));
+            if (q >= H0 && q < H0 + R)
+              __stcg(const_cast<double *>(vrow(P, dnew, cp, i)) + c, v);
+          }
+          s0[q * m + c] = v;
+        }
+      }
+      __syncthreads();
+      const double *src = s0;
+      int hs = H0;
+      for (int st = 0; st < P.z; ++st)
+      {
+        const int hd = P.halo[st + 1];
+        const PEll F = P.F[cp * P.z + (P.z - 1 - st)];
+        const double *fv = reinterpret_cast<const double *>(buf + P.a_fv[st]);
+        const unsigned long long *fo = reinterpret_cast<const unsigned long long *>(buf + P.a_fo[st]);
+        double *dst = (st & 1) ? sB : sA;
+        const int span = R + 2 * hd;
+        for (int q = threadIdx.x; q < span; q += TB)
+        {
+          const int in0 = q + hs - hd; // row q in src coordinates
+          const unsigned long long ow = fo[q * F.ow];
+          const unsigned long long ow1 = F.ow > 1 ? fo[q * F.ow + 1] : 0ull;
+          double acc[MT];
+#pragma unroll
+          for (int c = 0; c < MT; ++c)
+            acc[c] = 0.0;
+          for (int e = 0; e < F.E; ++e)
+          {
+            const double fvv = fv[q * F.E + e];
+            const int loc = (in0 + off16(ow, ow1, e)) * m;
+#pragma unroll
+            for (int c = 0; c < MT; ++c)
+              if (c < m)
+                acc[c] = __dadd_rn(acc[c], __dmul_rn(fvv, src[loc + c]));
+          }
+#pragma unroll
+          for (int c = 0; c < MT; ++c)
+            if (c < m)
+              dst[q * m + c] = acc[c];
+        }
+        __syncthreads();
+        src = dst;
+        hs = hd;
+      }
+      const PEll A = P.A[cp];
+      const double *av = reinterpret_cast<const double *>(buf + P.a_av);
+      const unsigned long long *ao = reinterpret_cast<const unsigned long long *>(buf + P.a_ao);
+      double pk[2 * MT];
+#pragma unroll
+      for (int q = 0; q < 2 * MT; ++q)
+        pk[q] = 0.0;
+#pragma unroll
+      for (int j = 0; j < RPT; ++j)
+      {
+        const int lr = threadIdx.x + j * TB;
+        if (lr >= R)
+          break;
+        const unsigned long long ow = ao[lr * A.ow];
+        const unsigned long long ow1 = A.ow > 1 ? ao[lr * A.ow + 1] : 0ull;
+        double acc[MT];
+#pragma unroll
+        for (int c = 0; c < MT; ++c)
+          acc[c] = 0.0;
+        for (int e = 0; e < A.E; ++e)
+        {
+          const double a = av[lr * A.E + e];
+          const int loc = (lr + hs + off16(ow, ow1, e)) * m;
+#pragma unroll
+          for (int c = 0; c < MT; ++c)
+            if (c < m)
+              acc[c] = __dadd_rn(acc[c], __dmul_rn(a, src[loc + c]));
+        }
+        const int64_t i = base_i + lr;
+#pragma unroll
+        for (int c = 0; c < MT; ++c)
+        {
+          if (c >= m)
+            break;
+          if (kind == 1)
+          {
+            const double res = __dsub_rn(__ldg(vrow(P, P.b, cp, i) + c), acc[c]);
+            __stcg(const_cast<double *>(vrow(P, P.w, cp, i)) + c, res);
+            __stcg(const_cast<double *>(vrow(P, P.sol, cp, i)) + c, src[(lr + hs) * m + c]);
+            pk[c] = __dadd_rn(pk[c], __dmul_rn(res, res));
+          }
+          else
+          {
+            const double dn = s0[(H0 + lr) * m + c];
+            __stcg(const_cast<double *>(vrow(P, P.w, cp, i)) + c, acc[c]);
+            pk[c] = __dadd_rn(pk[c], __dmul_rn(dn, acc[c]));
+            pk[MT + c] = __dadd_rn(pk[MT + c], __dmul_rn(dn, dn));
+          }
+        }
+      }
+      double pv[2 * MT];
+#pragma unroll
+      for (int q = 0; q < 2 * MT; ++q)
+        pv[q] = 0.0;
+#pragma unroll
+      for (int c = 0; c < MT; ++c)
+        if (c < m)
+        {
+          pv[c] = pk[c];
+          pv[m + c] = pk[MT + c];
+        }
+      chunk_sum<TB, 2 * MT>(sh, pv, kind == 1 ? m : 2 * m); // its barriers also free `buf`
+    }
+    ++k;
+  }
+  if (cur_p >= 0)
+    end_point(P.partial, sh, cur_p, kind == 2 ? m : (kind == 1 ? m : 2 * m));
+  __syncthreads();
+}
+
+template <int TB, int MT>
+__global__ void __launch_bounds__(TB, 1) cg_stream(StreamParams P)
+{
+  cgrp::grid_group grid = cgrp::this_grid();
+  extern __shared__ __align__(128) unsigned char smem_s[];
+  __shared__ BandShared<TB> sh;
+  __shared__ __align__(8) uint64_t bars[2];
+  const int m = P.m;
+  const int S = P.l * m;
+  uint32_t phase_bits = 0;
+  if (threadIdx.x == 0)
+  {
+    int q = 0;
+    while (q < kMaxSeg && P.seg[blockIdx.x * kMaxSeg + q].p >= 0)
+    {
+      sh.seg[q] = P.seg[blockIdx.x * kMaxSeg + q];
+      ++q;
+    }
+    sh.nseg = q;
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int p = threadIdx.x; p < P.l; p += TB)
+    sh.pmask[p] = 1;
+  __syncthreads();
+  // ---- phase 0: ||b||^2 (one pass, plain loads)
+  for_segments(P, sh, [&](int p, int64_t rs, int64_t re) {
+    begin_point(sh);
+    for (int64_t c0 = rs; c0 < re; c0 += TB)
+    {
+      const int64_t i = c0 + threadIdx.x;
+      double pk[MT];
+#pragma unroll
+      for (int c = 0; c < MT; ++c)
+      {
+        pk[c] = 0.0;
+        if (c < m && i < re)
+        {
+          const double bv = __ldg(vrow(P, P.b, p, i) + c);
+          pk[c] = __dmul_rn(bv, bv);
+        }
+      }
+      chunk_sum<TB, MT>(sh, pk, m);
+    }
+    end_point(P.partial, sh, p, m);
+  });
+  grid.sync();
+  reduce_blocks<TB, StreamParams>(P, sh, m);
+  for (int s = threadIdx.x; s < S; s += TB)
+  {
+    const double bb = sh.tot[(s / m) * 2 * kMaxM + s % m];
+    const double bn = sqrt(bb);
+    sh.bnorm[s] = bn;
+    sh.rho[s] = bb;
+    sh.target[s] = P.rtol * bn;
+    sh.state[s] = bn == 0.0 ? kZeroRhs : kRun;
+    sh.fresh[s] = 1;
+    sh.beta[s] = 0.0;
+    sh.sit[s] = 0;
+  }
+  __syncthreads();
+
+  auto copy_finish = [&]() {
+    for_segments(P, sh, [&](int p, int64_t rs, int64_t re) {
+      for (int64_t i = rs + threadIdx.x; i < re; i += TB)
+        for (int c = 0; c < m; ++c)
+        {
+          const int s = p * m + c;
+          const int64_t o = static_cast<int64_t>(s) * P.n + i;
+          if (sh.state[s] == kPendingConv || sh.state[s] == kMaxed)
+          {
+            if (P.X)
+              P.X[o] = __ldcg(vrow(P, P.sol, p, i) + c);
+            if (P.TR)
+              P.TR[o] = __ldcg(vrow(P, P.w, p, i) + c);
+          }
+          else if (sh.state[s] == kPendingRestart)
+            __stcg(const_cast<double *>(vrow(P, P.r, p, i)) + c, __ldcg(vrow(P, P.w, p, i) + c));
+        }
+    });
+    fence_async_global();
+  };
+
+  int cur = 0;
+  int64_t it = 0;
+  for (;;)
+  {
+    if (it >= P.maxit)
+      break;
+    if (threadIdx.x == 0)
+      sh.flag = 0;
+    __syncthreads();
+    for (int p = threadIdx.x; p < P.l; p += TB)
+    {
+      int need = 0;
+      for (int c = 0; c < m; ++c)
+      {
+        const int s = p * m + c;
+        need |= sh.state[s] == kRun && sqrt(sh.rho[s]) <= sh.target[s];
+      }
+      sh.pmask[p] = need;
+      if (need)
+        atomicOr(&sh.flag, 1);
+    }
+    __syncthreads();
+    if (sh.flag)
+    {
+      stream_pass<TB, MT, 1>(P, sh, smem_s, bars, phase_bits, 1, nullptr, nullptr);
+      fence_async_global();
+      grid.sync();
+      reduce_blocks<TB, StreamParams>(P, sh, m);
+      for (int s = threadIdx.x; s < S; s += TB)
+      {
+        if (!(sh.state[s] == kRun && sqrt(sh.rho[s]) <= sh.target[s]))
+          continue;
+        const double tt = sh.tot[(s / m) * 2 * kMaxM + s % m];
+        if (sqrt(tt) <= sh.target[s])
+        {
+          sh.state[s] = kPendingConv;
+          sh.sit[s] = it;
+        }
+        else
+        {
+          sh.rho[s] = tt;
+          if (sqrt(tt) <= sh.target[s])
+          {
+            sh.state[s] = kPendingConv;
+            sh.sit[s] = it;
+          }
+          else
+          {
+            sh.state[s] = kPendingRestart;
+            sh.fresh[s] = 1;
+          }
+        }
+      }
+      __syncthreads();
+      copy_finish();
+      grid.sync();
+      for (int s = threadIdx.x; s < S; s += TB)
+      {
+        if (sh.state[s] == kPendingConv)
+          sh.state[s] = kConverged;
+        else if (sh.state[s] == kPendingRestart)
+          sh.state[s] = kRun;
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0)
+      sh.flag = 0;
+    __syncthreads();
+    for (int p = threadIdx.x; p < P.l; p += TB)
+    {
+      int live = 0;
+      for (int c = 0; c < m; ++c)
+        live |= sh.state[p * m + c] == kRun;
+      sh.pmask[p] = live;
+      if (live)
+        atomicOr(&sh.flag, 1);
+    }
+    __syncthreads();
+    if (!sh.flag)
+      break;
+    double *d_old = cur ? P.dbuf1 : P.dbuf0;
+    double *d_new = cur ? P.dbuf0 : P.dbuf1;
+    stream_pass<TB, MT, 1>(P, sh, smem_s, bars, phase_bits, 0, d_old, d_new);
+    fence_async_global();
+    grid.sync();
+    reduce_blocks<TB, StreamParams>(P, sh, 2 * m);
+    for (int s = threadIdx.x; s < S; s += TB)
+    {
+      if (sh.state[s] != kRun)
+        continue;
+      const int p = s / m, c = s % m;
+      const double curv = sh.tot[p * 2 * kMaxM + c];
+      const double dd = sh.tot[p * 2 * kMaxM + m + c];
+      if (!(curv > 1e-30 * dd))
+      {
+        sh.state[s] = kBreakdown;
+        sh.sit[s] = it;
+      }
+      else
+        sh.alpha[s] = sh.rho[s] / curv;
+    }
+    __syncthreads();
+    stream_pass<TB, MT, 1>(P, sh, smem_s, bars, phase_bits, 2, d_old, d_new);
+    fence_async_global();
+    grid.sync();
+    reduce_blocks<TB, StreamParams>(P, sh, m);
+    ++it;
+    for (int s = threadIdx.x; s < S; s += TB)
+    {
+      if (sh.state[s] != kRun)
+        continue;
+      const double rn = sh.tot[(s / m) * 2 * kMaxM + s % m];
+      if (P.hist && blockIdx.x == 0 && it - 1 < P.hist_cap)
+        P.hist[static_cast<int64_t>(s) * P.hist_cap + (it - 1)] = sqrt(rn) / sh.bnorm[s];
+      sh.beta[s] = rn / sh.rho[s];
+      sh.rho[s] = rn;
+      sh.fresh[s] = 0;
+    }
+    __syncthreads();
+    cur ^= 1;
+  }
+  // ---- budget exhausted: final true-residual check
+  if (threadIdx.x == 0)
+    sh.flag = 0;
+  __syncthreads();
+  for (int p = threadIdx.x; p < P.l; p += TB)
+  {
+    int need = 0;
+    for (int c = 0; c < m; ++c)
+      need |= sh.state[p * m + c] == kRun;
+    sh.pmask[p] = need;
+    if (need)
+      atomicOr(&sh.flag, 1);
+  }
+  __syncthreads();
+  if (sh.flag)
+  {
+    stream_pass<TB, MT, 1>(P, sh, smem_s, bars, phase_bits, 1, nullptr, nullptr);
+    fence_async_global();
+    grid.sync();
+    reduce_blocks<TB, StreamParams>(P, sh, m);
+    for (int s = threadIdx.x; s < S; s += TB)
+    {
+      if (sh.state[s] != kRun)
+        continue;
+      const double tt = sh.tot[(s / m) * 2 * kMaxM + s % m];
+      sh.state[s] = sqrt(tt) <= sh.target[s] ? kPendingConv : kMaxed;
+      sh.sit[s] = it;
+    }
+    __syncthreads();
+    copy_finish();
+    for (int s = threadIdx.x; s < S; s += TB)
+      if (sh.state[s] == kPendingConv)
+        sh.state[s] = kConverged;
+    __syncthreads();
+  }
+  for (int p = threadIdx.x; p < P.l; p += TB)
+    sh.pmask[p] = 1;
+  __syncthreads();
+  for_segments(P, sh, [&](int p, int64_t rs, int64_t re) {
+    for (int64_t i = rs + threadIdx.x; i < re; i += TB)
+      for (int c = 0; c < m; ++c)
+      {
+        const int s = p * m + c;
+        const int64_t o = static_cast<int64_t>(s) * P.n + i;
+        if (sh.state[s] == kZeroRhs)
+        {
+          if (P.X)
+            P.X[o] = 0.0;
+          if (P.TR)
+            P.TR[o] = 0.0;
+          if (P.REC)
+            P.REC[o] = 0.0;
+        }
+        else if (sh.state[s] != kBreakdown && P.REC)
+          P.REC[o] = __ldcg(vrow(P, P.r, p, i) + c);
+      }
+  });
+  if (blockIdx.x == 0)
+  {
+    for (int s = threadIdx.x; s < S; s += TB)
+    {
+      const int st = sh.state[s];
+      P.iters[s] = sh.sit[s];
+      P.conv[s] = (st == kConverged || st == kZeroRhs) ? 1 : 0;
+      P.status[s] = st == kBreakdown ? MGPU_ERR_BREAKDOWN : MGPU_OK;
+      P.bd_iter[s] = st == kBreakdown ? sh.sit[s] : -1;
+    }
+    if (threadIdx.x == 0)
+      *P.loop_iters = it;
+  }
+}
+
+// CSR -> padded row-major ELL (values [row][E], int8 offsets packed in ow u64 words)
+__global__ void csr_to_pell(int64_t n, DCsr M, int E, int ow, double *vals, unsigned long long *offs)
+{
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n)
+    return;
+  const int64_t k0 = M.rp[i], k1 = M.rp[i + 1];
+  unsigned long long w[2] = {0ull, 0ull};
+  for (int t = 0; t < E; ++t)
+  {
+    const bool has = k0 + t < k1;
+    vals[i * E + t] = has ? M.v[k0 + t] : 0.0; // padding adds +0 after the row's entries
+    if (has)
+      w[t >> 3] |=
+          static_cast<unsigned long long>(static_cast<unsigned char>(static_cast<signed char>(M.ci[k0 + t] - i)))
+          << (8 * (t & 7));
+  }
+  for (int q = 0; q < ow; ++q)
+    offs[i * ow + q] = w[q];
+}
+
+__global__ void stream_init(int l, int m, int64_t n, int64_t ldv, const double *__restrict__ B, int64_t ldb,
+                            double *b, double *r, double *d, double *xt)
+{
+  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t per = n * m;
+  if (g >= per * l)
+    return;
+  const int64_t p = g / per, rem = g - p * per, i = rem / m, c = rem - i * m;
+  const double v = B[p * ldb + c * n + i];
+  const int64_t o = p * ldv + (kPadR + i) * m + c;
+  b[o] = v;
+  r[o] = v;
+  d[o] = v;
+  xt[o] = 0.0;
 }
 
 // B [p][c][row] (column-major per point; ldb between points) -> interleaved
@@ -1442,6 +2178,224 @@ bool band_plan(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu
   return h <= kMaxHalo;
 }
 
+// Host side of cg_stream.  Returns false if the chunk buffers do not fit.
+bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_csr *const *chains, int64_t n,
+                  int m, const double *B_dev, int64_t ldb, const int *halo, int hmax, double rtol, int64_t maxit,
+                  double *X_dev, double *REC_dev, double *TR_dev, int64_t *d_it, int *d_conv, int *d_st, int64_t *d_bd,
+                  double *d_hist, int64_t hist_cap, int64_t *d_loop)
+{
+  constexpr int TB = 512;
+  cudaStream_t s = ctx->stream;
+  // even halos keep every bulk copy 16-byte aligned; rebuilt inside-out so that
+  // hal[st] >= hal[st + 1] + bw(factor of stage st) still holds
+  std::vector<int> hal(static_cast<size_t>(z + 1));
+  hal[z] = (halo[z] + 1) & ~1;
+  for (int st = z - 1; st >= 0; --st)
+    hal[st] = (hal[st + 1] + (halo[st] - halo[st + 1]) + 1) & ~1;
+  const int H0 = hal[0];
+  (void)hmax;
+  if (H0 > kPadR || l > kMaxPoints || static_cast<int64_t>(l) * m > kMaxSys || l > ctx->num_sms * kMaxSeg)
+    return false;
+  // ---- padded ELL operators
+  auto ell_of = [&](const mgpu_csr *M, std::vector<DBuf> &keep) {
+    const int E = static_cast<int>((csr_max_row(ctx, const_cast<mgpu_csr *>(M)) + 1) & ~1ll);
+    const int Ee = E < 2 ? 2 : E;
+    const int ow = Ee > 8 ? 2 : 1;
+    const int64_t rows = n + 2 * kPadR;
+    keep.emplace_back(sizeof(double) * rows * Ee, s);
+    DBuf &v = keep.back();
+    keep.emplace_back(sizeof(unsigned long long) * rows * ow, s);
+    DBuf &o = keep.back();
+    MG_CUDA(cudaMemsetAsync(v.ptr, 0, sizeof(double) * rows * Ee, s));
+    MG_CUDA(cudaMemsetAsync(o.ptr, 0, sizeof(unsigned long long) * rows * ow, s));
+    double *v0 = v.as<double>() + kPadR * Ee;
+    unsigned long long *o0 = o.as<unsigned long long>() + kPadR * ow;
+    csr_to_pell<<<blocks_for(n), kThreads, 0, s>>>(n, M->view(), Ee, ow, v0, o0);
+    check_launch(ctx, "csr_to_pell");
+    return PEll{v0, o0, Ee, ow};
+  };
+  std::vector<DBuf> keep;
+  keep.reserve(static_cast<size_t>(2 * l * (z + 1) + 16));
+  for (int p = 0; p < l; ++p)
+  {
+    if (csr_max_row(ctx, const_cast<mgpu_csr *>(A[p])) > 16)
+      return false;
+    for (int f = 0; f < z; ++f)
+      if (csr_max_row(ctx, const_cast<mgpu_csr *>(chains[static_cast<size_t>(p) * z + f])) > 16)
+        return false;
+  }
+  std::vector<PEll> hA(static_cast<size_t>(l)), hF(static_cast<size_t>(l) * (z > 0 ? z : 1));
+  int EA = 0;
+  std::vector<int> EF(static_cast<size_t>(z > 0 ? z : 1), 0);
+  for (int p = 0; p < l; ++p)
+  {
+    hA[p] = ell_of(A[p], keep);
+    EA = std::max(EA, hA[p].E);
+    for (int f = 0; f < z; ++f)
+    {
+      hF[static_cast<size_t>(p) * z + f] = ell_of(chains[static_cast<size_t>(p) * z + f], keep);
+      const int st = z - 1 - f;
+      EF[st] = std::max(EF[st], hF[static_cast<size_t>(p) * z + f].E);
+    }
+  }
+  // ---- shared-memory plan: the largest chunk height whose double buffer fits
+  StreamParams P{};
+  size_t dyn = 0;
+  int64_t CH = 0;
+  int optin = 0;
+  MG_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+  const size_t stat = sizeof(BandShared<TB>) + 64;
+  for (int64_t ch : {int64_t(TB), int64_t(TB / 2), int64_t(TB / 4)})
+  {
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+      const size_t o2 = off;
+      off += (bytes + 127) & ~static_cast<size_t>(127);
+      return o2;
+    };
+    const int64_t vrows = (ch + 2 * H0 + 1) & ~1ll;
+    P.a_vr = take(sizeof(double) * vrows * m);
+    P.a_vd = take(sizeof(double) * vrows * m);
+    for (int st = 0; st < z; ++st)
+    {
+      const int64_t rows = (ch + 2 * hal[st + 1] + 1) & ~1ll;
+      P.a_fv[st] = take(sizeof(double) * rows * EF[st]);
+      P.a_fo[st] = take(sizeof(unsigned long long) * rows * 2);
+    }
+    P.a_av = take(sizeof(double) * ch * EA);
+    P.a_ao = take(sizeof(unsigned long long) * ch * 2);
+    const size_t a_bytes = off;
+    off = 0;
+    P.b_x = take(sizeof(double) * ch * m);
+    P.b_d = take(sizeof(double) * ch * m);
+    P.b_r = take(sizeof(double) * ch * m);
+    P.b_w = take(sizeof(double) * ch * m);
+    const size_t b_bytes = off;
+    P.buf_bytes = (std::max(a_bytes, b_bytes) + 127) & ~static_cast<size_t>(127);
+    off = 2 * P.buf_bytes;
+    P.off_stage0 = take(sizeof(double) * (ch + 2 * H0) * m);
+    P.off_stage1 = take(sizeof(double) * (ch + 2 * (z >= 1 ? hal[1] : 0)) * m);
+    P.off_stage2 = take(sizeof(double) * (ch + 2 * (z >= 2 ? hal[2] : 0)) * m);
+    if (off + stat <= static_cast<size_t>(optin))
+    {
+      dyn = off;
+      CH = ch;
+      break;
+    }
+  }
+  if (CH == 0)
+    return false;
+  // ---- vectors (padded) and the per-point block plan
+  const int64_t ldv = (n + 2 * kPadR) * m;
+  const size_t vb = sizeof(double) * static_cast<size_t>(l) * ldv;
+  DBuf b(vb, s), xt(vb, s), r(vb, s), d0(vb, s), d1(vb, s), w(vb, s), sol(vb, s);
+  for (DBuf *q : {&b, &xt, &r, &d0, &d1, &w, &sol})
+    MG_CUDA(cudaMemsetAsync(q->ptr, 0, vb, s));
+  stream_init<<<blocks_for(static_cast<int64_t>(l) * n * m), kThreads, 0, s>>>(
+      l, m, n, ldv, B_dev, ldb, b.as<double>(), r.as<double>(), d0.as<double>(), xt.as<double>());
+  check_launch(ctx, "stream_init");
+  const int G = ctx->num_sms;
+  std::vector<Seg> hseg(static_cast<size_t>(G) * kMaxSeg, Seg{-1, 0, 0, 0});
+  std::vector<int2> hpb(static_cast<size_t>(l));
+  if (l <= G)
+  {
+    for (int p = 0; p < l; ++p)
+    {
+      const int b0 = static_cast<int>(static_cast<int64_t>(p) * G / l);
+      const int b1 = static_cast<int>(static_cast<int64_t>(p + 1) * G / l);
+      const int nb = b1 - b0;
+      const int64_t groups = (n + 31) / 32;
+      for (int k = 0; k < nb; ++k)
+      {
+        const int64_t g0 = groups * k / nb, g1 = groups * (k + 1) / nb;
+        hseg[static_cast<size_t>(b0 + k) * kMaxSeg] =
+            Seg{p, static_cast<int>(g0 * 32), static_cast<int>(std::min<int64_t>(n, g1 * 32)), 0};
+      }
+      hpb[p] = make_int2(b0, b1);
+    }
+  }
+  else
+  {
+    for (int bk = 0; bk < G; ++bk)
+    {
+      const int p0 = static_cast<int>(static_cast<int64_t>(bk) * l / G);
+      const int p1 = static_cast<int>(static_cast<int64_t>(bk + 1) * l / G);
+      for (int p = p0; p < p1; ++p)
+      {
+        hseg[static_cast<size_t>(bk) * kMaxSeg + (p - p0)] = Seg{p, 0, static_cast<int>(n), 0};
+        hpb[p] = make_int2(bk, bk + 1);
+      }
+    }
+  }
+  DBuf segs(sizeof(Seg) * hseg.size(), s), pblk(sizeof(int2) * hpb.size(), s);
+  DBuf dA(sizeof(PEll) * hA.size(), s), dF(sizeof(PEll) * hF.size(), s);
+  DBuf partial(sizeof(double) * static_cast<size_t>(l) * 2 * kMaxM * G, s);
+  MG_CUDA(cudaMemcpyAsync(segs.ptr, hseg.data(), sizeof(Seg) * hseg.size(), cudaMemcpyHostToDevice, s));
+  MG_CUDA(cudaMemcpyAsync(pblk.ptr, hpb.data(), sizeof(int2) * hpb.size(), cudaMemcpyHostToDevice, s));
+  MG_CUDA(cudaMemcpyAsync(dA.ptr, hA.data(), sizeof(PEll) * hA.size(), cudaMemcpyHostToDevice, s));
+  MG_CUDA(cudaMemcpyAsync(dF.ptr, hF.data(), sizeof(PEll) * hF.size(), cudaMemcpyHostToDevice, s));
+  P.l = l;
+  P.m = m;
+  P.z = z;
+  P.rpt = 1;
+  P.ch = static_cast<int>(CH);
+  P.n = n;
+  P.ldv = ldv;
+  for (int q = 0; q <= z; ++q)
+    P.halo[q] = hal[q];
+  P.hmax = H0;
+  P.A = dA.as<PEll>();
+  P.F = dF.as<PEll>();
+  P.rtol = rtol;
+  P.maxit = maxit;
+  P.b = b.as<double>();
+  P.xt = xt.as<double>();
+  P.r = r.as<double>();
+  P.dbuf0 = d0.as<double>();
+  P.dbuf1 = d1.as<double>();
+  P.w = w.as<double>();
+  P.sol = sol.as<double>();
+  P.partial = partial.as<double>();
+  P.seg = segs.as<Seg>();
+  P.pblk = pblk.as<int2>();
+  P.X = X_dev;
+  P.REC = REC_dev;
+  P.TR = TR_dev;
+  P.iters = d_it;
+  P.conv = d_conv;
+  P.status = d_st;
+  P.bd_iter = d_bd;
+  P.hist = d_hist;
+  P.hist_cap = hist_cap;
+  P.loop_iters = d_loop;
+  auto launch = [&](auto kern) {
+    MG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
+    int per_sm = 0;
+    MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TB, dyn));
+    if (per_sm < 1)
+      return false;
+    void *args[] = {&P};
+    MG_CUDA(cudaEventRecord(ctx->ev0, s));
+    MG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void *>(kern), dim3(static_cast<unsigned>(G)), dim3(TB), args,
+                                        dyn, s));
+    check_launch(ctx, "cg_stream");
+    MG_CUDA(cudaEventRecord(ctx->ev1, s));
+    return true;
+  };
+  bool ok;
+  if (m == 1)
+    ok = launch(cg_stream<TB, 1>);
+  else if (m == 2)
+    ok = launch(cg_stream<TB, 2>);
+  else if (m <= 4)
+    ok = launch(cg_stream<TB, 4>);
+  else
+    ok = launch(cg_stream<TB, 8>);
+  if (ok)
+    MG_CUDA(cudaStreamSynchronize(s)); // keep the padded buffers alive until the kernel is done
+  return ok;
+}
+
 // One sub-batch: l points (all columns m <= kMaxM).
 void cg_batch(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_csr *const *chains, int64_t n,
               int m, const double *B_dev, int64_t ldb, double rtol, int64_t maxit, double *X_dev, double *REC_dev,
@@ -1473,7 +2427,7 @@ void cg_batch(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_
 
   DBuf partial, totals, counter, segs, pblk;
   int clustered = 0;
-  if (banded && ctx->cg_path != 2)
+  if (banded && ctx->cg_path != 2 && ctx->cg_path != 4)
   {
     // systems small enough to live on chip: one cluster per point, no grid barrier
     MG_CUDA(cudaMemsetAsync(d_loop.ptr, 0, sizeof(int64_t), s));
@@ -1485,13 +2439,21 @@ void cg_batch(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_
     if (clustered)
       MG_CUDA(cudaEventRecord(ctx->ev1, s));
   }
-  if (!clustered)
+  bool streamed = false;
+  if (banded && !clustered && ctx->cg_path != 2)
+  {
+    MG_CUDA(cudaMemsetAsync(d_loop.ptr, 0, sizeof(int64_t), s));
+    streamed = stream_solve(ctx, l, A, z, chains, n, m, B_dev, ldb, halo, hmax, rtol, maxit, X_dev, REC_dev, TR_dev,
+                            d_it.as<int64_t>(), d_conv.as<int>(), d_st.as<int>(), d_bd.as<int64_t>(),
+                            hist ? d_hist.as<double>() : nullptr, hist_cap, d_loop.as<int64_t>());
+  }
+  if (!clustered && !streamed)
   {
     cg_init<<<blocks_for(vec), kThreads, 0, s>>>(l, m, n, B_dev, ldb, b.as<double>(), r.as<double>(), d.as<double>(),
                                                    xt.as<double>());
     check_launch(ctx, "cg_init");
   }
-  if (clustered)
+  if (clustered || streamed)
   {
   }
   else if (banded)
@@ -1654,7 +2616,7 @@ void cg_batch(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_
   MG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
   *ms_out += ms;
   *loop_out += loop;
-  ctx->last_cg_path = clustered ? clustered : (banded ? 0 : 1);
+  ctx->last_cg_path = clustered ? clustered : (streamed ? 4 : (banded ? 0 : 1));
 }
 
 } // namespace

@@ -344,7 +344,7 @@ int64_t mgpu_launch_count(const mgpu_ctx *ctx) { return ctx ? ctx->launches : 0;
 
 int mgpu_ctx_set_cg_path(mgpu_ctx *ctx, int path)
 {
-  if (ctx == nullptr || path < 0 || path > 3)
+  if (ctx == nullptr || path < 0 || path > 4)
     return MGPU_ERR_ARG;
   ctx->cg_path = path;
   return MGPU_OK;

@@ -109,7 +109,7 @@ struct mgpu_ctx
   double last_cg_ms = 0.0;
   int64_t last_cg_iters = 0;
   int last_cg_path = 1; // 0 banded (grid), 1 general, 2 cluster v2 (m = 1), 3 cluster v1
-  int cg_path = 0;      // 0 auto, 1 force general, 2 force banded grid kernel (no cluster), 3 cluster v1 only
+  int cg_path = 0;      // 0 auto, 1 force general, 2 force banded grid kernel, 3 cluster v1 only, 4 stream (no cluster)
   long long *prof_dev = nullptr; // diagnostics: per-phase clock64 totals of the cluster kernel (MGPU_PROFILE_PHASES)
   // last error
   int last_status = MGPU_OK;

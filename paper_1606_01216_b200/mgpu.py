@@ -238,12 +238,13 @@ class Context:
     def set_cg_path(self, path: str):
         """'auto' (cluster / banded / general by shape), 'general' or 'banded' (grid kernel, no cluster)."""
         self.check(lib().mgpu_ctx_set_cg_path(self.handle,
-                                              {"auto": 0, "general": 1, "banded": 2, "cluster_v1": 3}[path]))
+                                              {"auto": 0, "general": 1, "banded": 2, "cluster_v1": 3,
+                                               "stream": 4}[path]))
 
     @property
     def last_cg_path(self) -> str:
-        return {0: "banded", 1: "general", 2: "cluster", 3: "cluster_v1"}.get(lib().mgpu_last_cg_path(self.handle),
-                                                                             "?")
+        return {0: "banded", 1: "general", 2: "cluster", 3: "cluster_v1", 4: "stream"}.get(
+            lib().mgpu_last_cg_path(self.handle), "?")
 
     def last_cg_timing(self):
         ms, it = C.c_double(), C.c_int64()

@@ -13,7 +13,7 @@ from conftest import rel
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True, params=["auto", "cluster_v1", "banded", "general"])
+@pytest.fixture(autouse=True, params=["auto", "cluster_v1", "stream", "banded", "general"])
 def cg_path(request, mg):
     """Every parity case runs through all three CG kernels: cluster-resident (auto on
     these on-chip sizes), the banded grid kernel and the general CSR kernel."""
@@ -29,7 +29,7 @@ def test_path_selection(mg, oracle, cg_path):
     P = oracle.spai_ls(A, None, 1)
     mg.pcg_solve(A, [P], np.ones(600), maxit=5)
     # A^2-pattern factor: 10 entries per row -> the shared-memory cluster kernel (v1); v2 packs <= 8
-    assert mg.default_context().last_cg_path == {"auto": "cluster_v1", "cluster_v1": "cluster_v1",
+    assert mg.default_context().last_cg_path == {"auto": "cluster_v1", "cluster_v1": "cluster_v1", "stream": "stream",
                                                   "banded": "banded", "general": "general"}[cg_path]
     if cg_path == "auto":
         P1 = oracle.spai_ls(A, None, 0)
