@@ -1362,6 +1362,7 @@ __global__ void __launch_bounds__(TB, 1) cg_banded(BandParams P)
 // Control flow, reductions and arithmetic are those of cg_banded.
 // =====================================================================
 constexpr int kPadR = 64;
+constexpr int kStreamNB = 4; // bulk-copy ring depth
 
 __device__ __forceinline__ uint32_t sm_addr(const void *p)
 {
@@ -1389,6 +1390,10 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
                    sm_addr(dst)),
                "l"(src), "r"(bytes), "r"(sm_addr(bar))
                : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+{
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm_addr(bar)) : "memory");
 }
 __device__ __forceinline__ void fence_async_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
@@ -1423,6 +1428,7 @@ struct StreamParams
   double *hist;
   int64_t hist_cap;
   int64_t *loop_iters;
+  long long *prof; // optional [16] clock64 totals per phase (block 0, thread 0; MGPU_PROFILE_PHASES)
   // shared-memory carve-up (bytes): two input buffers (phase A layout and
   // phase B layout alias) + stage buffers
   size_t buf_bytes, off_stage0, off_stage1, off_stage2;
@@ -1469,8 +1475,8 @@ __device__ __forceinline__ int64_t even_up(int64_t x) { return (x + 1) & ~static
 // Producer: issue the bulk copies of one chunk's inputs into buffer `buf`.
 // kind 0: phase A step, 1: phase A check (x~ instead of r, no d), 2: phase B.
 template <int TB>
-__device__ void stream_issue(const StreamParams &P, unsigned char *buf, uint64_t *bar, int kind, int p, int64_t c0,
-                             int64_t c1, const double *dold, const double *dnew)
+__device__ void stream_issue(const StreamParams &P, const PEll *tab, unsigned char *buf, uint64_t *bar, int kind, int p,
+                             int64_t c0, int64_t c1, const double *dold, const double *dnew)
 {
   const int m = P.m;
   uint32_t bytes = 0;
@@ -1493,12 +1499,12 @@ __device__ void stream_issue(const StreamParams &P, unsigned char *buf, uint64_t
   for (int st = 0; st < P.z; ++st)
   {
     const int hd = P.halo[st + 1];
-    const PEll F = P.F[p * P.z + (P.z - 1 - st)];
+    const PEll F = tab[1 + st];
     const int64_t rows = even_up(c1 - c0 + 2 * hd);
     total += static_cast<uint32_t>(rows * F.E * 8 + rows * F.ow * 8);
   }
   {
-    const PEll A = P.A[p];
+    const PEll A = tab[0];
     const int64_t rows = even_up(c1 - c0);
     total += static_cast<uint32_t>(rows * A.E * 8 + rows * A.ow * 8);
   }
@@ -1509,12 +1515,12 @@ __device__ void stream_issue(const StreamParams &P, unsigned char *buf, uint64_t
   for (int st = 0; st < P.z; ++st)
   {
     const int hd = P.halo[st + 1];
-    const PEll F = P.F[p * P.z + (P.z - 1 - st)];
+    const PEll F = tab[1 + st];
     const int64_t rows = even_up(c1 - c0 + 2 * hd);
     bulk_g2s(buf + P.a_fv[st], F.v + (c0 - hd) * F.E, static_cast<uint32_t>(rows * F.E * 8), bar);
     bulk_g2s(buf + P.a_fo[st], F.o + (c0 - hd) * F.ow, static_cast<uint32_t>(rows * F.ow * 8), bar);
   }
-  const PEll A = P.A[p];
+  const PEll A = tab[0];
   const int64_t rows = even_up(c1 - c0);
   bulk_g2s(buf + P.a_av, A.v + c0 * A.E, static_cast<uint32_t>(rows * A.E * 8), bar);
   bulk_g2s(buf + P.a_ao, A.o + c0 * A.ow, static_cast<uint32_t>(rows * A.ow * 8), bar);
@@ -1529,92 +1535,275 @@ __device__ __forceinline__ int off16(unsigned long long w0, unsigned long long w
   return t < 8 ? off8s(w0, t) : off8s(w1, t - 8);
 }
 
-// One pipelined pass over the block's chunks.  kind: 0 phase A (step),
-// 1 phase A (true-residual check), 2 phase B.
-template <int TB, int MT, int RPT>
-__device__ void stream_pass(const StreamParams &P, BandShared<TB> &sh, unsigned char *smem, uint64_t *bars,
-                            uint32_t &phase_bits, int kind, const double *dold, double *dnew)
+// Column of element e of a row-interleaved block with m columns (MT: compile-time bound, a power of two).
+template <int MT>
+__device__ __forceinline__ int col_of(int e, int m)
+{
+  if constexpr (MT == 1)
+    return 0;
+  else
+    return m == MT ? (e & (MT - 1)) : e % m;
+}
+// acc[c] += v without dynamic register indexing.
+template <int MT>
+__device__ __forceinline__ void acc_add(double *acc, int c, double v)
+{
+#pragma unroll
+  for (int k = 0; k < MT; ++k)
+    if (k == c)
+      acc[k] = __dadd_rn(acc[k], v);
+}
+// m doubles of one row (shared memory); 16-byte vector loads when m == MT >= 2.
+template <int MT>
+__device__ __forceinline__ void ld_row(const double *x, double (&v)[MT], int m)
+{
+  if (MT >= 2 && m == MT)
+  {
+#pragma unroll
+    for (int h = 0; h < MT / 2; ++h)
+    {
+      const double2 t = reinterpret_cast<const double2 *>(x)[h];
+      v[2 * h] = t.x;
+      v[2 * h + 1] = t.y;
+    }
+  }
+  else
+  {
+#pragma unroll
+    for (int c = 0; c < MT; ++c)
+      v[c] = c < m ? x[c] : 0.0;
+  }
+}
+template <int MT>
+__device__ __forceinline__ void st_row(double *x, const double (&v)[MT], int m)
+{
+  if (MT >= 2 && m == MT)
+  {
+#pragma unroll
+    for (int h = 0; h < MT / 2; ++h)
+      reinterpret_cast<double2 *>(x)[h] = make_double2(v[2 * h], v[2 * h + 1]);
+  }
+  else
+  {
+#pragma unroll
+    for (int c = 0; c < MT; ++c)
+      if (c < m)
+        x[c] = v[c];
+  }
+}
+// Streaming (L2-only) global store of one row.
+template <int MT>
+__device__ __forceinline__ void stg_row(double *x, const double (&v)[MT], int m)
+{
+  if (MT >= 2 && m == MT)
+  {
+#pragma unroll
+    for (int h = 0; h < MT / 2; ++h)
+      __stcg(reinterpret_cast<double2 *>(x) + h, make_double2(v[2 * h], v[2 * h + 1]));
+  }
+  else
+  {
+#pragma unroll
+    for (int c = 0; c < MT; ++c)
+      if (c < m)
+        __stcg(x + c, v[c]);
+  }
+}
+// One padded-ELL row (E even, values 16-byte aligned) times a row-interleaved
+// shared-memory block: a2[c] = sum_e val_e * src[(in0 + off_e) * m + c], e ascending.
+template <int MT>
+__device__ __forceinline__ void ell_row(const double *vals, const unsigned long long *offs, int E, int ow,
+                                        const double *src, int in0, int m, double (&a2)[MT])
+{
+#pragma unroll
+  for (int c = 0; c < MT; ++c)
+    a2[c] = 0.0;
+  const unsigned long long w0 = offs[0];
+  const unsigned long long w1 = ow > 1 ? offs[1] : 0ull;
+  const double2 *v2 = reinterpret_cast<const double2 *>(vals);
+  auto term = [&](double a, int e) {
+    double x[MT];
+    ld_row<MT>(src + (in0 + off16(w0, w1, e)) * m, x, m);
+#pragma unroll
+    for (int c = 0; c < MT; ++c)
+      if (c < m)
+        a2[c] = __dadd_rn(a2[c], __dmul_rn(a, x[c]));
+  };
+  for (int h = 0; h < E / 2; ++h)
+  {
+    const double2 f = v2[h];
+    term(f.x, 2 * h);
+    term(f.y, 2 * h + 1);
+  }
+}
+
+struct PhaseClock
+{
+  bool on;
+  long long t, acc[16];
+  __device__ void mark(int k)
+  {
+    if (on)
+    {
+      const long long now = clock64();
+      acc[k] += now - t;
+      t = now;
+    }
+  }
+};
+
+// Barrier among the TB consumer threads only (the producer warp streams on).
+template <int TB>
+__device__ __forceinline__ void consumer_sync()
+{
+  asm volatile("bar.sync 1, %0;" ::"n"(TB) : "memory");
+}
+
+// Producer-side state of the bulk-copy ring (lane 0 of the producer warp).
+struct RingProducer
+{
+  uint32_t filled; // bit b: buffer b has been filled at least once
+  uint32_t epar;   // bit b: parity of the next empty-barrier phase to wait for
+};
+
+// One pass over the block's chunks.  kind: 0 phase A (step), 1 phase A
+// (true-residual check), 2 phase B.  Warp-specialised: lane 0 of warp TB/32
+// streams chunk inputs into an NB-deep ring of shared buffers (full barrier:
+// bulk-copy bytes; empty barrier: consumers done), the TB consumer threads
+// compute.  Dot-product partials accumulate per consumer thread over all
+// chunks of a point (row order) and are reduced once per point.
+template <int TB, int MT, int NB>
+__device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, const PEll *tab, unsigned char *smem,
+                            uint64_t *full, uint64_t *empty, uint32_t &phase_bits, RingProducer &rp, int kind,
+                            const double *dold, double *dnew, PhaseClock &pc)
 {
   const int64_t CH = P.ch;
   const int m = P.m;
-  ChunkIt prod{0, sh.nseg > 0 ? static_cast<int64_t>(sh.seg[0].rs) : 0};
-  ChunkIt cons = prod;
-  int pp, cp;
-  int64_t pc0, pc1, cc0, cc1;
-  // prologue: chunk 0 -> buffer 0
+  const int nv = kind == 0 ? 2 * m : m;
+  ChunkIt cons{0, sh.nseg > 0 ? static_cast<int64_t>(sh.seg[0].rs) : 0};
   __syncthreads();
-  bool have_next = chunk_next(sh, CH, prod, pp, pc0, pc1);
-  if (threadIdx.x == 0)
-    fence_async_global(); // generic stores of the previous phase -> async-proxy (bulk copy) reads
-  if (threadIdx.x == 0 && have_next)
+  if (threadIdx.x >= TB)
   {
-    fence_async_shared();
-    stream_issue<TB>(P, smem, &bars[0], kind, pp, pc0, pc1, dold, dnew);
+    // ---- producer
+    if (threadIdx.x == TB)
+    {
+      fence_async_global(); // generic stores of the previous phase -> async-proxy (bulk copy) reads
+      ChunkIt prod = cons;
+      int pp;
+      int64_t pc0, pc1;
+      int k = 0;
+      while (chunk_next(sh, CH, prod, pp, pc0, pc1))
+      {
+        const int b = k % NB;
+        if ((rp.filled >> b) & 1u)
+        {
+          mbar_wait(&empty[b], (rp.epar >> b) & 1u);
+          rp.epar ^= 1u << b;
+        }
+        rp.filled |= 1u << b;
+        stream_issue<TB>(P, tab + prod.seg * (kMaxZ + 1), smem + b * P.buf_bytes, &full[b], kind, pp, pc0, pc1, dold,
+                         dnew);
+        ++k;
+      }
+    }
+    __syncthreads();
+    return;
   }
+  // ---- consumers
+  int cp;
+  int64_t cc0, cc1;
+  pc.mark(0);
+  double acc[2 * MT];
+#pragma unroll
+  for (int q = 0; q < 2 * MT; ++q)
+    acc[q] = 0.0;
   int k = 0;
   int cur_p = -1;
+  auto flush = [&](int pnt) {
+    double pv[2 * MT];
+#pragma unroll
+    for (int q = 0; q < 2 * MT; ++q)
+      pv[q] = 0.0;
+#pragma unroll
+    for (int c = 0; c < MT; ++c)
+      if (c < m)
+      {
+        pv[c] = acc[c];
+        if (kind == 0)
+          pv[m + c] = acc[MT + c];
+      }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < 2 * MT; ++q)
+    {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1)
+        pv[q] = __dadd_rn(pv[q], __shfl_xor_sync(0xffffffffu, pv[q], off));
+    }
+    if (lane == 0)
+    {
+#pragma unroll
+      for (int q = 0; q < 2 * MT; ++q)
+        sh.wsum[warp][q] = pv[q];
+    }
+    consumer_sync<TB>();
+    if (warp == 0)
+    {
+      for (int q = 0; q < nv; ++q)
+      {
+        double x = lane < TB / 32 ? sh.wsum[lane][q] : 0.0;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1)
+          x = __dadd_rn(x, __shfl_xor_sync(0xffffffffu, x, off));
+        if (lane == 0)
+          P.partial[(static_cast<int64_t>(pnt) * 2 * kMaxM + q) * gridDim.x + blockIdx.x] = x;
+      }
+    }
+    consumer_sync<TB>();
+#pragma unroll
+    for (int q = 0; q < 2 * MT; ++q)
+      acc[q] = 0.0;
+  };
   while (chunk_next(sh, CH, cons, cp, cc0, cc1))
   {
-    const int bi = k & 1;
-    // prefetch chunk k + 1 into the other buffer (free: its last use ended at the
-    // __syncthreads closing chunk k - 1)
-    have_next = chunk_next(sh, CH, prod, pp, pc0, pc1);
-    if (threadIdx.x == 0 && have_next)
-    {
-      fence_async_shared();
-      stream_issue<TB>(P, smem + (bi ^ 1) * P.buf_bytes, &bars[bi ^ 1], kind, pp, pc0, pc1, dold, dnew);
-    }
-    mbar_wait(&bars[bi], (phase_bits >> bi) & 1u);
-    phase_bits ^= 1u << bi;
-    unsigned char *buf = smem + bi * P.buf_bytes;
+    const int bi = k % NB;
+    pc.mark(1);
     if (cp != cur_p)
     {
       if (cur_p >= 0)
-        end_point(P.partial, sh, cur_p, kind == 2 ? m : (kind == 1 ? m : 2 * m));
-      begin_point(sh);
+        flush(cur_p);
       cur_p = cp;
     }
+    pc.mark(2);
+    mbar_wait(&full[bi], (phase_bits >> bi) & 1u);
+    phase_bits ^= 1u << bi;
+    pc.mark(3);
+    unsigned char *buf = smem + bi * P.buf_bytes;
     const int64_t base_i = cc0;
     const int R = static_cast<int>(cc1 - cc0);
+    const int sb = cp * m; // first system of the point
     if (kind == 2)
     {
+      // x~ += alpha d, r -= alpha w, partial (r, r): one element (row, column) per thread
       const double *xs = reinterpret_cast<const double *>(buf + P.b_x);
       const double *ds = reinterpret_cast<const double *>(buf + P.b_d);
       const double *rs = reinterpret_cast<const double *>(buf + P.b_r);
       const double *ws = reinterpret_cast<const double *>(buf + P.b_w);
-      bool run[MT];
-      double al[MT];
-#pragma unroll
-      for (int c = 0; c < MT; ++c)
+      double *xg = const_cast<double *>(vrow(P, P.xt, cp, base_i));
+      double *rg = const_cast<double *>(vrow(P, P.r, cp, base_i));
+      const int ne = R * m;
+      for (int e = threadIdx.x; e < ne; e += TB)
       {
-        run[c] = c < m && sh.state[cp * m + c] == kRun;
-        al[c] = run[c] ? sh.alpha[cp * m + c] : 0.0;
+        const int c = col_of<MT>(e, m);
+        if (sh.state[sb + c] != kRun)
+          continue;
+        const double al = sh.alpha[sb + c];
+        const double xn = __dadd_rn(xs[e], __dmul_rn(al, ds[e]));
+        const double rn = __dadd_rn(rs[e], __dmul_rn(-al, ws[e]));
+        __stcg(xg + e, xn);
+        __stcg(rg + e, rn);
+        acc_add<MT>(acc, c, __dmul_rn(rn, rn));
       }
-      double pk[MT];
-#pragma unroll
-      for (int c = 0; c < MT; ++c)
-        pk[c] = 0.0;
-#pragma unroll
-      for (int j = 0; j < RPT; ++j)
-      {
-        const int lr = threadIdx.x + j * TB;
-        if (lr >= R)
-          break;
-#pragma unroll
-        for (int c = 0; c < MT; ++c)
-          if (run[c])
-          {
-            const int q = lr * m + c;
-            const double xn = __dadd_rn(xs[q], __dmul_rn(al[c], ds[q]));
-            const double rn = __dadd_rn(rs[q], __dmul_rn(-al[c], ws[q]));
-            double *xg = const_cast<double *>(vrow(P, P.xt, cp, base_i + lr)) + c;
-            double *rg = const_cast<double *>(vrow(P, P.r, cp, base_i + lr)) + c;
-            __stcg(xg, xn);
-            __stcg(rg, rn);
-            pk[c] = __dadd_rn(pk[c], __dmul_rn(rn, rn));
-          }
-      }
-      chunk_sum<TB, MT>(sh, pk, m);
     }
     else
     {
@@ -1624,155 +1813,111 @@ __device__ void stream_pass(const StreamParams &P, BandShared<TB> &sh, unsigned 
       double *s0 = reinterpret_cast<double *>(smem + P.off_stage0);
       double *sA = reinterpret_cast<double *>(smem + P.off_stage1);
       double *sB = reinterpret_cast<double *>(smem + P.off_stage2);
-      double be[MT];
-      bool fr[MT];
-#pragma unroll
-      for (int c = 0; c < MT; ++c)
+      // stage 0: d = fresh ? r : r + beta d_old over the halo-extended chunk (check: x~)
+      const int ne0 = (R + 2 * H0) * m;
+      const int lo = H0 * m, hi = (H0 + R) * m;
+      double *dg = kind == 0 ? const_cast<double *>(vrow(P, dnew, cp, base_i - H0)) : nullptr;
+      for (int e = threadIdx.x; e < ne0; e += TB)
       {
-        const int s = cp * m + c;
-        fr[c] = c < m && sh.fresh[s];
-        be[c] = c < m ? sh.beta[s] : 0.0;
-      }
-      // stage 0 rows [c0 - H0, c1 + H0)
-      const int span0 = R + 2 * H0;
-      for (int q = threadIdx.x; q < span0; q += TB)
-      {
-        const int64_t i = base_i - H0 + q;
-#pragma unroll
-        for (int c = 0; c < MT; ++c)
+        double v;
+        if (kind == 1)
+          v = vr[e];
+        else
         {
-          if (c >= m)
-            break;
-          double v;
-          if (kind == 1)
-            v = vr[q * m + c];
-          else
-          {
-            v = fr[c] ? vr[q * m + c] : __dadd_rn(vr[q * m + c], __dmul_rn(be[c], vd[q * m + c]));
-            if (q >= H0 && q < H0 + R)
-              __stcg(const_cast<double *>(vrow(P, dnew, cp, i)) + c, v);
-          }
-          s0[q * m + c] = v;
+          const int c = col_of<MT>(e, m);
+          v = sh.fresh[sb + c] ? vr[e] : __dadd_rn(vr[e], __dmul_rn(sh.beta[sb + c], vd[e]));
+          if (e >= lo && e < hi)
+            __stcg(dg + e, v);
         }
+        s0[e] = v;
       }
-      __syncthreads();
+      consumer_sync<TB>();
+      pc.mark(4);
       const double *src = s0;
       int hs = H0;
       for (int st = 0; st < P.z; ++st)
       {
         const int hd = P.halo[st + 1];
-        const PEll F = P.F[cp * P.z + (P.z - 1 - st)];
+        const PEll F = tab[cons.seg * (kMaxZ + 1) + 1 + st];
         const double *fv = reinterpret_cast<const double *>(buf + P.a_fv[st]);
         const unsigned long long *fo = reinterpret_cast<const unsigned long long *>(buf + P.a_fo[st]);
         double *dst = (st & 1) ? sB : sA;
         const int span = R + 2 * hd;
         for (int q = threadIdx.x; q < span; q += TB)
         {
-          const int in0 = q + hs - hd; // row q in src coordinates
-          const unsigned long long ow = fo[q * F.ow];
-          const unsigned long long ow1 = F.ow > 1 ? fo[q * F.ow + 1] : 0ull;
-          double acc[MT];
-#pragma unroll
-          for (int c = 0; c < MT; ++c)
-            acc[c] = 0.0;
-          for (int e = 0; e < F.E; ++e)
-          {
-            const double fvv = fv[q * F.E + e];
-            const int loc = (in0 + off16(ow, ow1, e)) * m;
-#pragma unroll
-            for (int c = 0; c < MT; ++c)
-              if (c < m)
-                acc[c] = __dadd_rn(acc[c], __dmul_rn(fvv, src[loc + c]));
-          }
-#pragma unroll
-          for (int c = 0; c < MT; ++c)
-            if (c < m)
-              dst[q * m + c] = acc[c];
+          double a2[MT];
+          ell_row<MT>(fv + q * F.E, fo + q * F.ow, F.E, F.ow, src, q + hs - hd, m, a2);
+          st_row<MT>(dst + q * m, a2, m);
         }
-        __syncthreads();
+        consumer_sync<TB>();
         src = dst;
         hs = hd;
       }
-      const PEll A = P.A[cp];
+      pc.mark(5);
+      const PEll A = tab[cons.seg * (kMaxZ + 1)];
       const double *av = reinterpret_cast<const double *>(buf + P.a_av);
       const unsigned long long *ao = reinterpret_cast<const unsigned long long *>(buf + P.a_ao);
-      double pk[2 * MT];
-#pragma unroll
-      for (int q = 0; q < 2 * MT; ++q)
-        pk[q] = 0.0;
-#pragma unroll
-      for (int j = 0; j < RPT; ++j)
+      double *wg = const_cast<double *>(vrow(P, P.w, cp, base_i));
+      for (int lr = threadIdx.x; lr < R; lr += TB)
       {
-        const int lr = threadIdx.x + j * TB;
-        if (lr >= R)
-          break;
-        const unsigned long long ow = ao[lr * A.ow];
-        const unsigned long long ow1 = A.ow > 1 ? ao[lr * A.ow + 1] : 0ull;
-        double acc[MT];
-#pragma unroll
-        for (int c = 0; c < MT; ++c)
-          acc[c] = 0.0;
-        for (int e = 0; e < A.E; ++e)
+        double a2[MT];
+        ell_row<MT>(av + lr * A.E, ao + lr * A.ow, A.E, A.ow, src, lr + hs, m, a2);
+        if (kind == 1)
         {
-          const double a = av[lr * A.E + e];
-          const int loc = (lr + hs + off16(ow, ow1, e)) * m;
+          const int64_t i = base_i + lr;
+#pragma unroll
+          for (int c = 0; c < MT; ++c)
+          {
+            if (c >= m)
+              break;
+            const double res = __dsub_rn(__ldg(vrow(P, P.b, cp, i) + c), a2[c]);
+            __stcg(wg + lr * m + c, res);
+            __stcg(const_cast<double *>(vrow(P, P.sol, cp, i)) + c, src[(lr + hs) * m + c]);
+            acc[c] = __dadd_rn(acc[c], __dmul_rn(res, res));
+          }
+        }
+        else
+        {
+          double dn[MT];
+          ld_row<MT>(s0 + (H0 + lr) * m, dn, m);
+          stg_row<MT>(wg + lr * m, a2, m);
 #pragma unroll
           for (int c = 0; c < MT; ++c)
             if (c < m)
-              acc[c] = __dadd_rn(acc[c], __dmul_rn(a, src[loc + c]));
-        }
-        const int64_t i = base_i + lr;
-#pragma unroll
-        for (int c = 0; c < MT; ++c)
-        {
-          if (c >= m)
-            break;
-          if (kind == 1)
-          {
-            const double res = __dsub_rn(__ldg(vrow(P, P.b, cp, i) + c), acc[c]);
-            __stcg(const_cast<double *>(vrow(P, P.w, cp, i)) + c, res);
-            __stcg(const_cast<double *>(vrow(P, P.sol, cp, i)) + c, src[(lr + hs) * m + c]);
-            pk[c] = __dadd_rn(pk[c], __dmul_rn(res, res));
-          }
-          else
-          {
-            const double dn = s0[(H0 + lr) * m + c];
-            __stcg(const_cast<double *>(vrow(P, P.w, cp, i)) + c, acc[c]);
-            pk[c] = __dadd_rn(pk[c], __dmul_rn(dn, acc[c]));
-            pk[MT + c] = __dadd_rn(pk[MT + c], __dmul_rn(dn, dn));
-          }
+            {
+              acc[c] = __dadd_rn(acc[c], __dmul_rn(dn[c], a2[c]));
+              acc[MT + c] = __dadd_rn(acc[MT + c], __dmul_rn(dn[c], dn[c]));
+            }
         }
       }
-      double pv[2 * MT];
-#pragma unroll
-      for (int q = 0; q < 2 * MT; ++q)
-        pv[q] = 0.0;
-#pragma unroll
-      for (int c = 0; c < MT; ++c)
-        if (c < m)
-        {
-          pv[c] = pk[c];
-          pv[m + c] = pk[MT + c];
-        }
-      chunk_sum<TB, 2 * MT>(sh, pv, kind == 1 ? m : 2 * m); // its barriers also free `buf`
     }
+    pc.mark(kind == 2 ? 7 : 6);
+    consumer_sync<TB>(); // buffer bi and the stage buffers are free again
+    if (threadIdx.x == 0)
+      mbar_arrive(&empty[bi]);
+    pc.mark(8);
     ++k;
   }
   if (cur_p >= 0)
-    end_point(P.partial, sh, cur_p, kind == 2 ? m : (kind == 1 ? m : 2 * m));
+    flush(cur_p);
   __syncthreads();
+  pc.mark(2);
 }
 
 template <int TB, int MT>
-__global__ void __launch_bounds__(TB, 1) cg_stream(StreamParams P)
+__global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
 {
+  constexpr int TBX = TB + 32; // TB consumer threads + one producer warp
   cgrp::grid_group grid = cgrp::this_grid();
   extern __shared__ __align__(128) unsigned char smem_s[];
-  __shared__ BandShared<TB> sh;
-  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ BandShared<TBX> sh;
+  __shared__ __align__(8) uint64_t bars[2 * kStreamNB]; // full[NB], empty[NB]
+  __shared__ PEll tab[kMaxSeg * (kMaxZ + 1)]; // operator descriptors per segment: A, then stage factors
   const int m = P.m;
   const int S = P.l * m;
   uint32_t phase_bits = 0;
+  RingProducer rp{0u, 0u};
+  PhaseClock pc{P.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0, clock64(), {}};
   if (threadIdx.x == 0)
   {
     int q = 0;
@@ -1782,17 +1927,24 @@ __global__ void __launch_bounds__(TB, 1) cg_stream(StreamParams P)
       ++q;
     }
     sh.nseg = q;
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (int g = 0; g < q; ++g)
+    {
+      const int p = sh.seg[g].p;
+      tab[g * (kMaxZ + 1)] = P.A[p];
+      for (int st = 0; st < P.z; ++st)
+        tab[g * (kMaxZ + 1) + 1 + st] = P.F[p * P.z + (P.z - 1 - st)];
+    }
+    for (int b = 0; b < 2 * kStreamNB; ++b)
+      mbar_init(&bars[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int p = threadIdx.x; p < P.l; p += TB)
+  for (int p = threadIdx.x; p < P.l; p += TBX)
     sh.pmask[p] = 1;
   __syncthreads();
   // ---- phase 0: ||b||^2 (one pass, plain loads)
   for_segments(P, sh, [&](int p, int64_t rs, int64_t re) {
     begin_point(sh);
-    for (int64_t c0 = rs; c0 < re; c0 += TB)
+    for (int64_t c0 = rs; c0 < re; c0 += TBX)
     {
       const int64_t i = c0 + threadIdx.x;
       double pk[MT];
@@ -1806,13 +1958,13 @@ __global__ void __launch_bounds__(TB, 1) cg_stream(StreamParams P)
           pk[c] = __dmul_rn(bv, bv);
         }
       }
-      chunk_sum<TB, MT>(sh, pk, m);
+      chunk_sum<TBX, MT>(sh, pk, m);
     }
     end_point(P.partial, sh, p, m);
   });
   grid.sync();
-  reduce_blocks<TB, StreamParams>(P, sh, m);
-  for (int s = threadIdx.x; s < S; s += TB)
+  reduce_blocks<TBX, StreamParams>(P, sh, m);
+  for (int s = threadIdx.x; s < S; s += TBX)
   {
     const double bb = sh.tot[(s / m) * 2 * kMaxM + s % m];
     const double bn = sqrt(bb);
@@ -1828,7 +1980,7 @@ __global__ void __launch_bounds__(TB, 1) cg_stream(StreamParams P)
 
   auto copy_finish = [&]() {
     for_segments(P, sh, [&](int p, int64_t rs, int64_t re) {
-      for (int64_t i = rs + threadIdx.x; i < re; i += TB)
+      for (int64_t i = rs + threadIdx.x; i < re; i += TBX)
         for (int c = 0; c < m; ++c)
         {
           const int s = p * m + c;
@@ -1856,7 +2008,7 @@ __global__ void __launch_bounds__(TB, 1) cg_stream(StreamParams P)
     if (threadIdx.x == 0)
       sh.flag = 0;
     __syncthreads();
-    for (int p = threadIdx.x; p < P.l; p += TB)
+    for (int p = threadIdx.x; p < P.l; p += TBX)
     {
       int need = 0;
       for (int c = 0; c < m; ++c)
@@ -1871,11 +2023,11 @@ __global__ void __launch_bounds__(TB, 1) cg_stream(StreamParams P)
     __syncthreads();
     if (sh.flag)
     {
-      stream_pass<TB, MT, 1>(P, sh, smem_s, bars, phase_bits, 1, nullptr, nullptr);
+      stream_pass<TB, MT, kStreamNB>(P, sh, tab, smem_s, bars, bars + kStreamNB, phase_bits, rp, 1, nullptr, nullptr, pc);
       fence_async_global();
       grid.sync();
-      reduce_blocks<TB, StreamParams>(P, sh, m);
-      for (int s = threadIdx.x; s < S; s += TB)
+      reduce_blocks<TBX, StreamParams>(P, sh, m);
+      for (int s = threadIdx.x; s < S; s += TBX)
       {
         if (!(sh.state[s] == kRun && sqrt(sh.rho[s]) <= sh.target[s]))
           continue;
@@ -1903,7 +2055,7 @@ __global__ void __launch_bounds__(TB, 1) cg_stream(StreamParams P)
       __syncthreads();
       copy_finish();
       grid.sync();
-      for (int s = threadIdx.x; s < S; s += TB)
+      for (int s = threadIdx.x; s < S; s += TBX)
       {
         if (sh.state[s] == kPendingConv)
           sh.state[s] = kConverged;
@@ -1915,7 +2067,7 @@ __global__ void __launch_bounds__(TB, 1) cg_stream(StreamParams P)
     if (threadIdx.x == 0)
       sh.flag = 0;
     __syncthreads();
-    for (int p = threadIdx.x; p < P.l; p += TB)
+    for (int p = threadIdx.x; p < P.l; p += TBX)
     {
       int live = 0;
       for (int c = 0; c < m; ++c)
@@ -1929,11 +2081,14 @@ __global__ void __launch_bounds__(TB, 1) cg_stream(StreamParams P)
       break;
     double *d_old = cur ? P.dbuf1 : P.dbuf0;
     double *d_new = cur ? P.dbuf0 : P.dbuf1;
-    stream_pass<TB, MT, 1>(P, sh, smem_s, bars, phase_bits, 0, d_old, d_new);
+    pc.mark(9);
+    stream_pass<TB, MT, kStreamNB>(P, sh, tab, smem_s, bars, bars + kStreamNB, phase_bits, rp, 0, d_old, d_new, pc);
     fence_async_global();
     grid.sync();
-    reduce_blocks<TB, StreamParams>(P, sh, 2 * m);
-    for (int s = threadIdx.x; s < S; s += TB)
+    pc.mark(10);
+    reduce_blocks<TBX, StreamParams>(P, sh, 2 * m);
+    pc.mark(11);
+    for (int s = threadIdx.x; s < S; s += TBX)
     {
       if (sh.state[s] != kRun)
         continue;
@@ -1949,12 +2104,15 @@ __global__ void __launch_bounds__(TB, 1) cg_stream(StreamParams P)
         sh.alpha[s] = sh.rho[s] / curv;
     }
     __syncthreads();
-    stream_pass<TB, MT, 1>(P, sh, smem_s, bars, phase_bits, 2, d_old, d_new);
+    pc.mark(9);
+    stream_pass<TB, MT, kStreamNB>(P, sh, tab, smem_s, bars, bars + kStreamNB, phase_bits, rp, 2, d_old, d_new, pc);
     fence_async_global();
     grid.sync();
-    reduce_blocks<TB, StreamParams>(P, sh, m);
+    pc.mark(10);
+    reduce_blocks<TBX, StreamParams>(P, sh, m);
+    pc.mark(11);
     ++it;
-    for (int s = threadIdx.x; s < S; s += TB)
+    for (int s = threadIdx.x; s < S; s += TBX)
     {
       if (sh.state[s] != kRun)
         continue;
@@ -1972,7 +2130,7 @@ __global__ void __launch_bounds__(TB, 1) cg_stream(StreamParams P)
   if (threadIdx.x == 0)
     sh.flag = 0;
   __syncthreads();
-  for (int p = threadIdx.x; p < P.l; p += TB)
+  for (int p = threadIdx.x; p < P.l; p += TBX)
   {
     int need = 0;
     for (int c = 0; c < m; ++c)
@@ -1984,11 +2142,11 @@ __global__ void __launch_bounds__(TB, 1) cg_stream(StreamParams P)
   __syncthreads();
   if (sh.flag)
   {
-    stream_pass<TB, MT, 1>(P, sh, smem_s, bars, phase_bits, 1, nullptr, nullptr);
+    stream_pass<TB, MT, kStreamNB>(P, sh, tab, smem_s, bars, bars + kStreamNB, phase_bits, rp, 1, nullptr, nullptr, pc);
     fence_async_global();
     grid.sync();
-    reduce_blocks<TB, StreamParams>(P, sh, m);
-    for (int s = threadIdx.x; s < S; s += TB)
+    reduce_blocks<TBX, StreamParams>(P, sh, m);
+    for (int s = threadIdx.x; s < S; s += TBX)
     {
       if (sh.state[s] != kRun)
         continue;
@@ -1998,16 +2156,16 @@ __global__ void __launch_bounds__(TB, 1) cg_stream(StreamParams P)
     }
     __syncthreads();
     copy_finish();
-    for (int s = threadIdx.x; s < S; s += TB)
+    for (int s = threadIdx.x; s < S; s += TBX)
       if (sh.state[s] == kPendingConv)
         sh.state[s] = kConverged;
     __syncthreads();
   }
-  for (int p = threadIdx.x; p < P.l; p += TB)
+  for (int p = threadIdx.x; p < P.l; p += TBX)
     sh.pmask[p] = 1;
   __syncthreads();
   for_segments(P, sh, [&](int p, int64_t rs, int64_t re) {
-    for (int64_t i = rs + threadIdx.x; i < re; i += TB)
+    for (int64_t i = rs + threadIdx.x; i < re; i += TBX)
       for (int c = 0; c < m; ++c)
       {
         const int s = p * m + c;
@@ -2025,9 +2183,12 @@ __global__ void __launch_bounds__(TB, 1) cg_stream(StreamParams P)
           P.REC[o] = __ldcg(vrow(P, P.r, p, i) + c);
       }
   });
+  if (pc.on)
+    for (int k = 0; k < 12; ++k)
+      P.prof[k] = pc.acc[k];
   if (blockIdx.x == 0)
   {
-    for (int s = threadIdx.x; s < S; s += TB)
+    for (int s = threadIdx.x; s < S; s += TBX)
     {
       const int st = sh.state[s];
       P.iters[s] = sh.sit[s];
@@ -2184,7 +2345,7 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
                   double *X_dev, double *REC_dev, double *TR_dev, int64_t *d_it, int *d_conv, int *d_st, int64_t *d_bd,
                   double *d_hist, int64_t hist_cap, int64_t *d_loop)
 {
-  constexpr int TB = 512;
+  constexpr int TB = 480; // consumer threads; + one producer warp = 512
   cudaStream_t s = ctx->stream;
   // even halos keep every bulk copy 16-byte aligned; rebuilt inside-out so that
   // hal[st] >= hal[st + 1] + bw(factor of stage st) still holds
@@ -2244,8 +2405,8 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
   int64_t CH = 0;
   int optin = 0;
   MG_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
-  const size_t stat = sizeof(BandShared<TB>) + 64;
-  for (int64_t ch : {int64_t(TB), int64_t(TB / 2), int64_t(TB / 4)})
+  const size_t stat = sizeof(BandShared<TB + 32>) + sizeof(PEll) * kMaxSeg * (kMaxZ + 1) + 128;
+  for (int64_t ch : {int64_t(512), int64_t(256), int64_t(128)})
   {
     size_t off = 0;
     auto take = [&](size_t bytes) {
@@ -2272,7 +2433,7 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
     P.b_w = take(sizeof(double) * ch * m);
     const size_t b_bytes = off;
     P.buf_bytes = (std::max(a_bytes, b_bytes) + 127) & ~static_cast<size_t>(127);
-    off = 2 * P.buf_bytes;
+    off = kStreamNB * P.buf_bytes;
     P.off_stage0 = take(sizeof(double) * (ch + 2 * H0) * m);
     P.off_stage1 = take(sizeof(double) * (ch + 2 * (z >= 1 ? hal[1] : 0)) * m);
     P.off_stage2 = take(sizeof(double) * (ch + 2 * (z >= 2 ? hal[2] : 0)) * m);
@@ -2368,15 +2529,16 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
   P.hist = d_hist;
   P.hist_cap = hist_cap;
   P.loop_iters = d_loop;
+  P.prof = ctx->prof_dev;
   auto launch = [&](auto kern) {
     MG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
     int per_sm = 0;
-    MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TB, dyn));
+    MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TB + 32, dyn));
     if (per_sm < 1)
       return false;
     void *args[] = {&P};
     MG_CUDA(cudaEventRecord(ctx->ev0, s));
-    MG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void *>(kern), dim3(static_cast<unsigned>(G)), dim3(TB), args,
+    MG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void *>(kern), dim3(static_cast<unsigned>(G)), dim3(TB + 32), args,
                                         dyn, s));
     check_launch(ctx, "cg_stream");
     MG_CUDA(cudaEventRecord(ctx->ev1, s));
@@ -2440,7 +2602,11 @@ void cg_batch(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_
       MG_CUDA(cudaEventRecord(ctx->ev1, s));
   }
   bool streamed = false;
-  if (banded && !clustered && ctx->cg_path != 2)
+  // streaming pays once a block's share of the batch (rows x columns) hides the
+  // per-pass pipeline fill; below that the grid-banded kernel is faster (measured
+  // crossover ~16K elements per SM on B200)
+  const bool stream_pays = static_cast<int64_t>(l) * n * m >= static_cast<int64_t>(16384) * ctx->num_sms;
+  if (banded && !clustered && (ctx->cg_path == 4 || (ctx->cg_path == 0 && stream_pays)))
   {
     MG_CUDA(cudaMemsetAsync(d_loop.ptr, 0, sizeof(int64_t), s));
     streamed = stream_solve(ctx, l, A, z, chains, n, m, B_dev, ldb, halo, hmax, rtol, maxit, X_dev, REC_dev, TR_dev,

@@ -292,7 +292,7 @@ int mgpu_ctx_destroy(mgpu_ctx *ctx)
     long long h[16] = {0};
     cudaMemcpy(h, ctx->prof_dev, sizeof h, cudaMemcpyDeviceToHost);
     std::fprintf(stderr, "MGPU_PROFILE_PHASES cycles:");
-    for (int k = 0; k < 10; ++k)
+    for (int k = 0; k < 12; ++k)
       std::fprintf(stderr, " %lld", h[k]);
     std::fprintf(stderr, "\n");
     cudaFree(ctx->prof_dev);
