@@ -18,6 +18,9 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
+#include <utility>
 #include <cmath>
 #include <vector>
 
@@ -38,8 +41,8 @@ namespace
 
 constexpr int kCgThreads = 256;
 constexpr int kWarps = kCgThreads / 32;
-constexpr int kMaxSys = 512;   // systems (points x columns) per launch
-constexpr int kMaxPoints = 512;
+constexpr int kMaxSys = 128;   // systems (points x columns) per launch (mgpu_cg_solve splits larger batches)
+constexpr int kMaxPoints = 128;
 constexpr int kMaxTiles = 1024; // tiles per point (reduction fan-in)
 constexpr int kMaxM = 8;        // rhs columns per launch
 
@@ -826,7 +829,8 @@ __device__ __forceinline__ void end_point(const BandParams &P, BandShared<TB> &s
   end_point(P.partial, sh, p, nv);
 }
 
-// After a barrier: tot[p][k] = sum over blocks (fixed order) for live points.
+// After a barrier: tot = sum over blocks (fixed order) for live points; quantity k < m of
+// system (p, c = k) at tot[p m + c], quantity k >= m at tot[l m + p m + (k - m)].
 template <int TB, class PT>
 __device__ void reduce_blocks(const PT &P, BandShared<TB> &sh, int nk)
 {
@@ -846,7 +850,7 @@ __device__ void reduce_blocks(const PT &P, BandShared<TB> &sh, int nk)
     for (int off = 16; off > 0; off >>= 1)
       a = __dadd_rn(a, __shfl_xor_sync(0xffffffffu, a, off));
     if (lane == 0)
-      sh.tot[p * 2 * kMaxM + k] = a;
+      sh.tot[k < P.m ? p * P.m + k : P.l * P.m + p * P.m + (k - P.m)] = a;
   }
   __syncthreads();
 }
@@ -1139,7 +1143,7 @@ __global__ void __launch_bounds__(TB, 1) cg_banded(BandParams P)
   reduce_blocks<TB, BandParams>(P, sh, m);
   for (int s = threadIdx.x; s < S; s += TB)
   {
-    const double bb = sh.tot[(s / m) * 2 * kMaxM + s % m];
+    const double bb = sh.tot[s];
     const double bn = sqrt(bb);
     sh.bnorm[s] = bn;
     sh.rho[s] = bb;
@@ -1183,7 +1187,7 @@ __global__ void __launch_bounds__(TB, 1) cg_banded(BandParams P)
       {
         if (!(sh.state[s] == kRun && sqrt(sh.rho[s]) <= sh.target[s]))
           continue;
-        const double tt = sh.tot[(s / m) * 2 * kMaxM + s % m];
+        const double tt = sh.tot[s];
         if (sqrt(tt) <= sh.target[s])
         {
           sh.state[s] = kPendingConv;
@@ -1243,8 +1247,8 @@ __global__ void __launch_bounds__(TB, 1) cg_banded(BandParams P)
       if (sh.state[s] != kRun)
         continue;
       const int p = s / m, c = s % m;
-      const double curv = sh.tot[p * 2 * kMaxM + c];
-      const double dd = sh.tot[p * 2 * kMaxM + m + c];
+      const double curv = sh.tot[p * m + c];
+      const double dd = sh.tot[S + p * m + c];
       if (!(curv > 1e-30 * dd))
       {
         sh.state[s] = kBreakdown;
@@ -1263,7 +1267,7 @@ __global__ void __launch_bounds__(TB, 1) cg_banded(BandParams P)
     {
       if (sh.state[s] != kRun)
         continue;
-      const double rn = sh.tot[(s / m) * 2 * kMaxM + s % m];
+      const double rn = sh.tot[s];
       if (P.hist && blockIdx.x == 0 && it - 1 < P.hist_cap)
         P.hist[static_cast<int64_t>(s) * P.hist_cap + (it - 1)] = sqrt(rn) / sh.bnorm[s];
       sh.beta[s] = rn / sh.rho[s];
@@ -1297,7 +1301,7 @@ __global__ void __launch_bounds__(TB, 1) cg_banded(BandParams P)
     {
       if (sh.state[s] != kRun)
         continue;
-      const double tt = sh.tot[(s / m) * 2 * kMaxM + s % m];
+      const double tt = sh.tot[s];
       sh.state[s] = sqrt(tt) <= sh.target[s] ? kPendingConv : kMaxed;
       sh.sit[s] = it;
     }
@@ -1362,7 +1366,7 @@ __global__ void __launch_bounds__(TB, 1) cg_banded(BandParams P)
 // Control flow, reductions and arithmetic are those of cg_banded.
 // =====================================================================
 constexpr int kPadR = 64;
-constexpr int kStreamNB = 4; // bulk-copy ring depth
+constexpr int kStreamNB = 4; // bulk-copy ring depth (maximum; StreamParams::nb is the one in use)
 
 __device__ __forceinline__ uint32_t sm_addr(const void *p)
 {
@@ -1408,7 +1412,8 @@ struct PEll
 
 struct StreamParams
 {
-  int l, m, z, rpt, ch; // ch: rows per chunk (<= block size)
+  int l, m, z, rpt, ch; // ch: rows per chunk
+  int nb;               // ring depth (2..kStreamNB)
   int64_t n, ldv; // ldv = (n + 2 PADR) * m: doubles per point block
   int halo[kMaxZ + 1];
   int hmax;
@@ -1694,7 +1699,7 @@ __device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, cons
       int k = 0;
       while (chunk_next(sh, CH, prod, pp, pc0, pc1))
       {
-        const int b = k % NB;
+        const int b = k % P.nb;
         if ((rp.filled >> b) & 1u)
         {
           mbar_wait(&empty[b], (rp.epar >> b) & 1u);
@@ -1766,7 +1771,7 @@ __device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, cons
   };
   while (chunk_next(sh, CH, cons, cp, cc0, cc1))
   {
-    const int bi = k % NB;
+    const int bi = k % P.nb;
     pc.mark(1);
     if (cp != cur_p)
     {
@@ -1966,7 +1971,7 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
   reduce_blocks<TBX, StreamParams>(P, sh, m);
   for (int s = threadIdx.x; s < S; s += TBX)
   {
-    const double bb = sh.tot[(s / m) * 2 * kMaxM + s % m];
+    const double bb = sh.tot[s];
     const double bn = sqrt(bb);
     sh.bnorm[s] = bn;
     sh.rho[s] = bb;
@@ -2031,7 +2036,7 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
       {
         if (!(sh.state[s] == kRun && sqrt(sh.rho[s]) <= sh.target[s]))
           continue;
-        const double tt = sh.tot[(s / m) * 2 * kMaxM + s % m];
+        const double tt = sh.tot[s];
         if (sqrt(tt) <= sh.target[s])
         {
           sh.state[s] = kPendingConv;
@@ -2093,8 +2098,8 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
       if (sh.state[s] != kRun)
         continue;
       const int p = s / m, c = s % m;
-      const double curv = sh.tot[p * 2 * kMaxM + c];
-      const double dd = sh.tot[p * 2 * kMaxM + m + c];
+      const double curv = sh.tot[p * m + c];
+      const double dd = sh.tot[S + p * m + c];
       if (!(curv > 1e-30 * dd))
       {
         sh.state[s] = kBreakdown;
@@ -2116,7 +2121,7 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
     {
       if (sh.state[s] != kRun)
         continue;
-      const double rn = sh.tot[(s / m) * 2 * kMaxM + s % m];
+      const double rn = sh.tot[s];
       if (P.hist && blockIdx.x == 0 && it - 1 < P.hist_cap)
         P.hist[static_cast<int64_t>(s) * P.hist_cap + (it - 1)] = sqrt(rn) / sh.bnorm[s];
       sh.beta[s] = rn / sh.rho[s];
@@ -2150,7 +2155,7 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
     {
       if (sh.state[s] != kRun)
         continue;
-      const double tt = sh.tot[(s / m) * 2 * kMaxM + s % m];
+      const double tt = sh.tot[s];
       sh.state[s] = sqrt(tt) <= sh.target[s] ? kPendingConv : kMaxed;
       sh.sit[s] = it;
     }
@@ -2406,8 +2411,25 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
   int optin = 0;
   MG_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
   const size_t stat = sizeof(BandShared<TB + 32>) + sizeof(PEll) * kMaxSeg * (kMaxZ + 1) + 128;
-  for (int64_t ch : {int64_t(512), int64_t(256), int64_t(128)})
+  // (chunk rows, ring depth) in order of preference; MGPU_STREAM_CFG="rows,depth" forces one (diagnostics)
+  // largest chunk first (per-chunk barriers and pipeline bookkeeping amortise over its rows), 3-deep ring
+  // before 2-deep at equal height
+  std::vector<std::pair<int64_t, int>> cands;
+  for (int64_t ch = 1024; ch >= 128; ch -= 64)
   {
+    cands.push_back({ch, 3});
+    cands.push_back({ch, 2});
+  }
+  if (const char *f = std::getenv("MGPU_STREAM_CFG"))
+  {
+    long fr = 0, fd = 0;
+    if (std::sscanf(f, "%ld,%ld", &fr, &fd) == 2 && fr > 0 && fd >= 2 && fd <= kStreamNB)
+      cands.insert(cands.begin(), {static_cast<int64_t>(fr), static_cast<int>(fd)});
+  }
+  for (const auto &cand : cands)
+  {
+    const int64_t ch = cand.first;
+    const int nb = cand.second;
     size_t off = 0;
     auto take = [&](size_t bytes) {
       const size_t o2 = off;
@@ -2433,14 +2455,15 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
     P.b_w = take(sizeof(double) * ch * m);
     const size_t b_bytes = off;
     P.buf_bytes = (std::max(a_bytes, b_bytes) + 127) & ~static_cast<size_t>(127);
-    off = kStreamNB * P.buf_bytes;
+    off = nb * P.buf_bytes;
     P.off_stage0 = take(sizeof(double) * (ch + 2 * H0) * m);
-    P.off_stage1 = take(sizeof(double) * (ch + 2 * (z >= 1 ? hal[1] : 0)) * m);
-    P.off_stage2 = take(sizeof(double) * (ch + 2 * (z >= 2 ? hal[2] : 0)) * m);
+    P.off_stage1 = z >= 1 ? take(sizeof(double) * (ch + 2 * hal[1]) * m) : 0; // stage buffers the chain uses
+    P.off_stage2 = z >= 2 ? take(sizeof(double) * (ch + 2 * hal[2]) * m) : 0;
     if (off + stat <= static_cast<size_t>(optin))
     {
       dyn = off;
       CH = ch;
+      P.nb = nb;
       break;
     }
   }
@@ -2603,9 +2626,9 @@ void cg_batch(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_
   }
   bool streamed = false;
   // streaming pays once a block's share of the batch (rows x columns) hides the
-  // per-pass pipeline fill; below that the grid-banded kernel is faster (measured
-  // crossover ~16K elements per SM on B200)
-  const bool stream_pays = static_cast<int64_t>(l) * n * m >= static_cast<int64_t>(16384) * ctx->num_sms;
+  // per-pass pipeline fill; below that the grid-banded kernel is as fast (measured
+  // break-even ~1K elements per SM on B200)
+  const bool stream_pays = static_cast<int64_t>(l) * n * m >= static_cast<int64_t>(2048) * ctx->num_sms;
   if (banded && !clustered && (ctx->cg_path == 4 || (ctx->cg_path == 0 && stream_pays)))
   {
     MG_CUDA(cudaMemsetAsync(d_loop.ptr, 0, sizeof(int64_t), s));

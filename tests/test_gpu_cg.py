@@ -123,6 +123,21 @@ def test_multi_shift_batch(mg, oracle):
         assert np.all(np.abs(r.iterations - want["iterations"]) <= 2)
 
 
+def test_many_shifts_split_launches(mg, oracle):
+    """150 shifts x 1 rhs (more than one launch's 128 systems, and more points than a
+    kernel's reduction table held before re-indexing) == per-shift oracle solves."""
+    M, D, K = oracle.chain_generate(200, consistent=True, stiffness_scale=1.0)
+    shifts = [10.0 ** (1 + 3 * i / 149) for i in range(150)]
+    ops = [oracle.shifted_operator(M, D, K, s) for s in shifts]
+    b = np.zeros(200)
+    b[7] = 1.0
+    res = mg.cg_solve_batched(ops, [[] for _ in ops], b, rtol=1e-10)
+    for A, r in zip(ops, res):
+        want = oracle.pcg_solve(A, [], b, rtol=1e-10)
+        assert rel(r.X[:, 0], want["solution"]) < 1e-8
+        assert abs(int(r.iterations[0]) - want["iterations"]) <= 2
+
+
 def test_t2_hermite_fixed_k_iterates(mg, oracle):
     """BASELINE config 1 shape: n=2000, s=100, LS-SPAI (A pattern), fixed budget."""
     M, D, K = oracle.hermite_generate(1000)
