@@ -28,6 +28,8 @@ namespace mgpu
 mgpu_csr *transpose_csr(mgpu_ctx *ctx, const mgpu_csr *A);
 mgpu_csr *transpose_perm(mgpu_ctx *ctx, const mgpu_csr *A, DBuf &perm);
 void gather_dev(mgpu_ctx *ctx, int64_t nnz, const int64_t *perm, const double *src, double *dst);
+void gather_batched(mgpu_ctx *ctx, int l, int64_t nnz, const int64_t *perm, const double *const *src,
+                    double *const *dst);
 
 namespace
 {
@@ -118,7 +120,9 @@ template <int G, int NI>
 struct LsGroupSmem
 {
   double W[G * (NI + 1)]; // S / Householder vectors, column-major, ld = NI + 1 (odd: bank spread)
-  double Q[G * (NI + 1)];
+  double Q[G * (NI + 1)]; // Q; before the QR: staged values of A^T row J_c (lane c)
+  int32_t rows[G * NI];    // staged column indices of A^T row J_c (lane c)
+  int cnt[G];
   double e[NI];
   double m[G];
   double diag[G];
@@ -180,17 +184,35 @@ __global__ void ls_columns(int64_t n, int l, DCsr pat, DCsr At, int64_t at_strid
       atomicOr(overflow, 1);
     return;
   }
-  // ---- I = sorted union of the rows of A(:, J)   (leader, insertion)
+  // ---- stage A^T row J_c (= column J_c of A) per lane: one dependent-load chain per lane
+  if (c < nj)
+  {
+    const int32_t k = pat.ci[jb + c];
+    const int64_t t0 = At.rp[k], t1 = At.rp[k + 1];
+    const int len = static_cast<int>(t1 - t0);
+    sm.cnt[c] = len;
+    for (int u = 0; u < len && u < NI; ++u)
+    {
+      sm.rows[c * NI + u] = At.ci[t0 + u];
+      sm.Q[c * (NI + 1) + u] = At.v[t0 + u];
+    }
+  }
+  __syncwarp(gmask);
+  // ---- I = sorted union of the rows of A(:, J)   (leader, insertion over the staged lists)
   if (c == 0)
   {
     int ni = 0;
     bool over = false;
     for (int q = 0; q < nj && !over; ++q)
     {
-      const int32_t k = pat.ci[jb + q];
-      for (int64_t t = At.rp[k]; t < At.rp[k + 1]; ++t)
+      if (sm.cnt[q] > NI)
       {
-        const int32_t row = At.ci[t];
+        over = true;
+        break;
+      }
+      for (int u = 0; u < sm.cnt[q]; ++u)
+      {
+        const int32_t row = sm.rows[q * NI + u];
         int pos = ni;
         while (pos > 0 && sm.I[pos - 1] > row)
           --pos;
@@ -201,8 +223,8 @@ __global__ void ls_columns(int64_t n, int l, DCsr pat, DCsr At, int64_t at_strid
           over = true;
           break;
         }
-        for (int u = ni; u > pos; --u)
-          sm.I[u] = sm.I[u - 1];
+        for (int u2 = ni; u2 > pos; --u2)
+          sm.I[u2] = sm.I[u2 - 1];
         sm.I[pos] = row;
         ++ni;
       }
@@ -226,16 +248,15 @@ __global__ void ls_columns(int64_t n, int l, DCsr pat, DCsr At, int64_t at_strid
   }
   const int ni = sm.ni;
   constexpr int LD = NI + 1;
-  // ---- S = A(I, J): lane c fills column c from A^T row J_c; e = rhs|_I
+  // ---- S = A(I, J): lane c fills column c from its staged row; e = rhs|_I
   if (c < nj)
   {
     double *col = sm.W + c * LD;
     for (int i = 0; i < ni; ++i)
       col[i] = 0.0;
-    const int32_t k = pat.ci[jb + c];
-    for (int64_t t = At.rp[k]; t < At.rp[k + 1]; ++t)
+    for (int u = 0; u < sm.cnt[c]; ++u)
     {
-      const int32_t row = At.ci[t];
+      const int32_t row = sm.rows[c * NI + u];
       int lo = 0, hi = ni;
       while (lo < hi)
       {
@@ -245,7 +266,7 @@ __global__ void ls_columns(int64_t n, int l, DCsr pat, DCsr At, int64_t at_strid
         else
           hi = mid;
       }
-      col[lo] = At.v[t];
+      col[lo] = sm.Q[c * LD + u];
     }
   }
   if (c == 0)
@@ -403,7 +424,8 @@ void launch_ls(mgpu_ctx *ctx, int64_t n, int l, DCsr pat, DCsr At, int64_t at_st
 {
   constexpr int per_block = WARPS * (32 / G);
   constexpr size_t smem = sizeof(LsGroupSmem<G, NI>) * per_block;
-  static_assert(smem <= 48 * 1024, "LS group shared memory");
+  static_assert(smem <= 100 * 1024, "LS group shared memory");
+  MG_CUDA(cudaFuncSetAttribute(ls_columns<G, NI>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const int64_t cols = static_cast<int64_t>(l) * n;
   const unsigned grid = static_cast<unsigned>((cols + per_block - 1) / per_block);
   ls_columns<G, NI><<<grid, WARPS * 32, smem, ctx->stream>>>(n, l, pat, At, at_stride, Kot, ko_stride, update, out,
@@ -610,11 +632,22 @@ std::vector<mgpu_csr *> spai_ls_shared(mgpu_ctx *ctx, int l, const mgpu_csr *con
     At0 = transpose_perm(ctx, A0, perm_t);
     DBuf at_vals(sizeof(double) * static_cast<size_t>(l) * (nnzA > 0 ? nnzA : 1), s);
     DBuf ko_vals(K_old ? sizeof(double) * static_cast<size_t>(l) * (nnzA > 0 ? nnzA : 1) : 8, s);
-    for (int p = 0; p < l; ++p)
     {
-      gather_dev(ctx, nnzA, perm_t.as<int64_t>(), A[p]->values, at_vals.as<double>() + p * nnzA);
+      std::vector<const double *> src(static_cast<size_t>(l)), srck(static_cast<size_t>(l));
+      std::vector<double *> dst(static_cast<size_t>(l)), dstk(static_cast<size_t>(l));
+      for (int p = 0; p < l; ++p)
+      {
+        src[p] = A[p]->values;
+        dst[p] = at_vals.as<double>() + p * nnzA;
+        if (K_old)
+        {
+          srck[p] = K_old[p]->values;
+          dstk[p] = ko_vals.as<double>() + p * nnzA;
+        }
+      }
+      gather_batched(ctx, l, nnzA, perm_t.as<int64_t>(), src.data(), dst.data());
       if (K_old)
-        gather_dev(ctx, nnzA, perm_t.as<int64_t>(), K_old[p]->values, ko_vals.as<double>() + p * nnzA);
+        gather_batched(ctx, l, nnzA, perm_t.as<int64_t>(), srck.data(), dstk.data());
     }
     DBuf pt_vals(sizeof(double) * static_cast<size_t>(l) * (nnzJ > 0 ? nnzJ : 1), s);
     MG_CUDA(cudaMemsetAsync(pt_vals.ptr, 0, sizeof(double) * static_cast<size_t>(l) * nnzJ, s));
@@ -632,6 +665,9 @@ std::vector<mgpu_csr *> spai_ls_shared(mgpu_ctx *ctx, int l, const mgpu_csr *con
     }
     P0 = transpose_perm(ctx, PT0, perm_p);
     const int64_t ba = csr_bandwidth(ctx, const_cast<mgpu_csr *>(A0));
+    const int64_t pmax = csr_max_row(ctx, P0); // every factor shares P0's stored pattern
+    std::vector<const double *> gsrc;
+    std::vector<double *> gdst;
     for (int p = 0; p < l; ++p)
     {
       mgpu_csr *P = p == 0 ? P0 : new_csr(ctx, n, n, nnzJ);
@@ -640,14 +676,16 @@ std::vector<mgpu_csr *> spai_ls_shared(mgpu_ctx *ctx, int l, const mgpu_csr *con
         MG_CUDA(cudaMemcpyAsync(P->row_ptr, P0->row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToDevice, s));
         if (nnzJ > 0)
           MG_CUDA(cudaMemcpyAsync(P->col_idx, P0->col_idx, sizeof(int32_t) * nnzJ, cudaMemcpyDeviceToDevice, s));
-        gather_dev(ctx, nnzJ, perm_p.as<int64_t>(), pt_vals.as<double>() + p * nnzJ, P->values);
+        gsrc.push_back(pt_vals.as<double>() + p * nnzJ);
+        gdst.push_back(P->values);
       }
       P->may_hold_zeros = true;
       P->bw = pattern == MGPU_PATTERN_A2 ? 2 * ba : ba;
-      P->maxrow = -1;
+      P->maxrow = pmax;
       out.push_back(P);
     }
     P0 = nullptr;
+    gather_batched(ctx, static_cast<int>(gsrc.size()), nnzJ, perm_p.as<int64_t>(), gsrc.data(), gdst.data());
   }
   catch (...)
   {

@@ -104,7 +104,7 @@ __device__ __forceinline__ int64_t merge_row(int64_t i, DCsr A, DCsr B, DCsr Cm,
 
 struct ShiftArgs
 {
-  int *bw; // [64] bandwidth of each output (atomicMax in the count pass)
+  int *bw; // [128]: bandwidth of each output, then its longest row (atomicMax in the count pass)
   double a[64];
   double b[64];
   int64_t *rp[64];
@@ -123,10 +123,19 @@ __global__ void add_count_kernel(int l, int64_t n, DCsr A, DCsr B, DCsr Cm, Shif
   int32_t lohi[2] = {INT_MAX, -1};
   const int64_t cnt = merge_row<kThird>(i, A, B, Cm, args.a[p], args.b[p], nullptr, nullptr, lohi);
   args.rp[p][i + 1] = cnt;
-  if (cnt > 0)
-    atomicMax(&args.bw[p], static_cast<int>(max(i - lohi[0], static_cast<int64_t>(lohi[1]) - i)));
   if (i == 0)
     args.rp[p][0] = 0;
+  // reduce over the lanes of the same point first: one atomic per warp and point
+  int bwv = cnt > 0 ? static_cast<int>(max(i - lohi[0], static_cast<int64_t>(lohi[1]) - i)) : 0;
+  int mr = static_cast<int>(cnt);
+  const unsigned grp = __match_any_sync(__activemask(), p);
+  bwv = __reduce_max_sync(grp, bwv);
+  mr = __reduce_max_sync(grp, mr);
+  if ((threadIdx.x & 31) == __ffs(grp) - 1)
+  {
+    atomicMax(&args.bw[p], bwv);
+    atomicMax(&args.bw[64 + p], mr);
+  }
 }
 
 template <bool kThird>
@@ -151,6 +160,53 @@ void scan_row_ptr(mgpu_ctx *ctx, int64_t *rp, int64_t n)
   DBuf t(tmp, ctx->stream);
   MG_CUDA(cub::DeviceScan::InclusiveSum(t.ptr, tmp, rp + 1, rp + 1, n, ctx->stream));
   count_launch(ctx);
+}
+
+struct RpBatch
+{
+  int64_t *rp[64];
+};
+
+// Inclusive scan of rp[1..n] for up to 64 row-pointer arrays, one block each
+// (kScanItems consecutive entries per thread), totals[p] = rp[p][n].
+constexpr int kScanTB = 512, kScanItems = 8;
+__global__ void __launch_bounds__(kScanTB) scan_rows_batched(int64_t n, RpBatch rb, int64_t *__restrict__ totals)
+{
+  using BS = cub::BlockScan<int64_t, kScanTB>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ int64_t carry;
+  int64_t *rp = rb.rp[blockIdx.x];
+  if (threadIdx.x == 0)
+    carry = 0;
+  __syncthreads();
+  for (int64_t base = 1; base <= n; base += static_cast<int64_t>(kScanTB) * kScanItems)
+  {
+    const int64_t i0 = base + static_cast<int64_t>(threadIdx.x) * kScanItems;
+    int64_t v[kScanItems];
+    int64_t sum = 0;
+#pragma unroll
+    for (int u = 0; u < kScanItems; ++u)
+    {
+      v[u] = i0 + u <= n ? rp[i0 + u] : 0;
+      sum += v[u];
+    }
+    int64_t excl, agg;
+    BS(tmp).ExclusiveSum(sum, excl, agg);
+    int64_t run = carry + excl;
+#pragma unroll
+    for (int u = 0; u < kScanItems; ++u)
+    {
+      run += v[u];
+      if (i0 + u <= n)
+        rp[i0 + u] = run;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      carry += agg;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    totals[blockIdx.x] = carry;
 }
 
 // Batched sp_add over up to 64 (a_i, b_i) pairs, optionally + C.
@@ -178,8 +234,8 @@ void batched_add(mgpu_ctx *ctx, const mgpu_csr *A, const mgpu_csr *B, const mgpu
     }
     const DCsr cv = kThird ? Cm->view() : DCsr{nullptr, nullptr, nullptr};
     const int64_t total = static_cast<int64_t>(cnt) * n;
-    DBuf bwbuf(sizeof(int) * 64, ctx->stream);
-    MG_CUDA(cudaMemsetAsync(bwbuf.ptr, 0, sizeof(int) * 64, ctx->stream));
+    DBuf bwbuf(sizeof(int) * 128, ctx->stream);
+    MG_CUDA(cudaMemsetAsync(bwbuf.ptr, 0, sizeof(int) * 128, ctx->stream));
     args.bw = bwbuf.as<int>();
     if (n > 0)
     {
@@ -192,16 +248,33 @@ void batched_add(mgpu_ctx *ctx, const mgpu_csr *A, const mgpu_csr *B, const mgpu
         MG_CUDA(cudaMemsetAsync(args.rp[p], 0, sizeof(int64_t), ctx->stream));
     }
     std::vector<int64_t> nnz(static_cast<size_t>(cnt), 0);
-    int hbw[64] = {0};
-    for (int p = 0; p < cnt; ++p)
+    int hbw[128] = {0};
+    if (n > 0 && n <= 262144)
     {
-      scan_row_ptr(ctx, args.rp[p], n);
-      MG_CUDA(cudaMemcpyAsync(&nnz[p], args.rp[p] + n, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+      // short operators: one launch scans every row pointer, one copy returns every nnz
+      RpBatch rb{};
+      for (int p = 0; p < cnt; ++p)
+        rb.rp[p] = args.rp[p];
+      DBuf tot(sizeof(int64_t) * 64, ctx->stream);
+      scan_rows_batched<<<cnt, kScanTB, 0, ctx->stream>>>(n, rb, tot.as<int64_t>());
+      check_launch(ctx, "scan_rows_batched");
+      MG_CUDA(cudaMemcpyAsync(nnz.data(), tot.ptr, sizeof(int64_t) * cnt, cudaMemcpyDeviceToHost, ctx->stream));
     }
-    MG_CUDA(cudaMemcpyAsync(hbw, bwbuf.ptr, sizeof(int) * 64, cudaMemcpyDeviceToHost, ctx->stream));
+    else
+    {
+      for (int p = 0; p < cnt; ++p)
+      {
+        scan_row_ptr(ctx, args.rp[p], n);
+        MG_CUDA(cudaMemcpyAsync(&nnz[p], args.rp[p] + n, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+      }
+    }
+    MG_CUDA(cudaMemcpyAsync(hbw, bwbuf.ptr, sizeof(int) * 128, cudaMemcpyDeviceToHost, ctx->stream));
     MG_CUDA(cudaStreamSynchronize(ctx->stream));
     for (int p = 0; p < cnt; ++p)
+    {
       made[p]->bw = hbw[p];
+      made[p]->maxrow = hbw[64 + p];
+    }
     for (int p = 0; p < cnt; ++p)
     {
       mgpu_csr *o = made[p];
@@ -267,70 +340,67 @@ __global__ void row_inner(int64_t n, DCsr A, DCsr B, double *__restrict__ out)
   out[i] = acc;
 }
 
-__global__ void expand_rows(int64_t n, const int64_t *__restrict__ rp, const int32_t *__restrict__ ci,
-                            unsigned long long *__restrict__ keys, int64_t *__restrict__ col_counts)
+__global__ void count_cols(int64_t n, const int64_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                           int64_t *__restrict__ col_counts)
+{
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n)
+    return;
+  for (int64_t k = rp[i]; k < rp[i + 1]; ++k)
+    atomicAdd(reinterpret_cast<unsigned long long *>(&col_counts[static_cast<int64_t>(ci[k]) + 1]), 1ull);
+}
+
+// Bucket every entry into its column (arbitrary order inside a column).
+__global__ void scatter_cols(int64_t n, const int64_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                             const int64_t *__restrict__ rpt, unsigned long long *__restrict__ cursor,
+                             int64_t *__restrict__ perm, int32_t *__restrict__ trow)
 {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n)
     return;
   for (int64_t k = rp[i]; k < rp[i + 1]; ++k)
   {
-    const unsigned long long c = static_cast<unsigned long long>(ci[k]);
-    keys[k] = (c << 32) | static_cast<unsigned long long>(i);
-    atomicAdd(reinterpret_cast<unsigned long long *>(&col_counts[c + 1]), 1ull);
+    const int64_t j = ci[k];
+    const int64_t pos = rpt[j] + static_cast<int64_t>(atomicAdd(&cursor[j], 1ull));
+    perm[pos] = k;
+    trow[pos] = static_cast<int32_t>(i);
   }
 }
 
-__global__ void keys_to_cols(int64_t nnz, const unsigned long long *__restrict__ keys, int32_t *__restrict__ ci)
+// Order each column by source position.  Source positions grow with the row
+// (row-major CSR), so this is ascending original-row order (sparse.cpp:238-247);
+// keys are unique, so the result does not depend on the bucketing order above.
+__global__ void sort_cols(int64_t ncols, const int64_t *__restrict__ rpt, int64_t *__restrict__ perm,
+                          int32_t *__restrict__ trow)
 {
-  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k < nnz)
-    ci[k] = static_cast<int32_t>(keys[k] & 0xffffffffull);
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= ncols)
+    return;
+  const int64_t b = rpt[j], len = rpt[j + 1] - b;
+  int64_t *pk = perm + b;
+  int32_t *pr = trow + b;
+  // shell sort (gaps 3h+1): insertion sort for the short columns of banded operators,
+  // bounded work for an occasional long one
+  int64_t h = 1;
+  while (h < len / 3)
+    h = 3 * h + 1;
+  for (; h >= 1; h /= 3)
+    for (int64_t u = h; u < len; ++u)
+    {
+      const int64_t kv = pk[u];
+      const int32_t rv = pr[u];
+      int64_t v = u;
+      while (v >= h && pk[v - h] > kv)
+      {
+        pk[v] = pk[v - h];
+        pr[v] = pr[v - h];
+        v -= h;
+      }
+      pk[v] = kv;
+      pr[v] = rv;
+    }
 }
 
-} // namespace
-
-// Device CSR transpose, deterministic: radix sort of (col, row) keys gives
-// each transposed row in ascending original-row order (sparse.cpp:238-247).
-mgpu_csr *transpose_csr(mgpu_ctx *ctx, const mgpu_csr *A)
-{
-  mgpu_csr *T = new_csr(ctx, A->ncols, A->nrows, A->nnz);
-  T->may_hold_zeros = A->may_hold_zeros;
-  T->bw = A->bw; // max |i - j| is transpose invariant
-  MG_CUDA(cudaMemsetAsync(T->row_ptr, 0, sizeof(int64_t) * (A->ncols + 1), ctx->stream));
-  if (A->nnz == 0)
-    return T;
-  DBuf keys(sizeof(unsigned long long) * A->nnz, ctx->stream);
-  DBuf keys_out(sizeof(unsigned long long) * A->nnz, ctx->stream);
-  expand_rows<<<blocks_for(A->nrows), kThreads, 0, ctx->stream>>>(A->nrows, A->row_ptr, A->col_idx,
-                                                                  keys.as<unsigned long long>(), T->row_ptr);
-  check_launch(ctx, "expand_rows");
-  int bits = 32;
-  while ((1ll << (bits - 32)) <= A->ncols && bits < 64)
-    ++bits;
-  size_t tmp = 0;
-  MG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys.as<unsigned long long>(),
-                                          keys_out.as<unsigned long long>(), A->values, T->values, A->nnz, 0, bits,
-                                          ctx->stream));
-  DBuf t(tmp, ctx->stream);
-  MG_CUDA(cub::DeviceRadixSort::SortPairs(t.ptr, tmp, keys.as<unsigned long long>(), keys_out.as<unsigned long long>(),
-                                          A->values, T->values, A->nnz, 0, bits, ctx->stream));
-  count_launch(ctx);
-  keys_to_cols<<<blocks_for(A->nnz), kThreads, 0, ctx->stream>>>(A->nnz, keys_out.as<unsigned long long>(),
-                                                                  T->col_idx);
-  check_launch(ctx, "keys_to_cols");
-  scan_row_ptr(ctx, T->row_ptr, A->ncols);
-  return T;
-}
-
-namespace
-{
-__global__ void iota_i64(int64_t n, int64_t *out)
-{
-  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k < n)
-    out[k] = k;
-}
 __global__ void gather_values(int64_t nnz, const int64_t *__restrict__ perm, const double *__restrict__ src,
                               double *__restrict__ dst)
 {
@@ -341,42 +411,76 @@ __global__ void gather_values(int64_t nnz, const int64_t *__restrict__ perm, con
 } // namespace
 
 // Transpose that also returns perm (T.values[k] = A.values[perm[k]]), so the
-// same pattern can be re-transposed for new values with a gather.
+// same pattern can be re-transposed for new values with a gather.  Sort-free:
+// column counts -> scan -> bucket -> per-column order by source position.
 mgpu_csr *transpose_perm(mgpu_ctx *ctx, const mgpu_csr *A, DBuf &perm)
 {
   mgpu_csr *T = new_csr(ctx, A->ncols, A->nrows, A->nnz);
   T->may_hold_zeros = A->may_hold_zeros;
-  T->bw = A->bw;
+  T->bw = A->bw; // max |i - j| is transpose invariant
   MG_CUDA(cudaMemsetAsync(T->row_ptr, 0, sizeof(int64_t) * (A->ncols + 1), ctx->stream));
   perm = DBuf(sizeof(int64_t) * (A->nnz > 0 ? A->nnz : 1), ctx->stream);
   if (A->nnz == 0)
     return T;
-  DBuf keys(sizeof(unsigned long long) * A->nnz, ctx->stream);
-  DBuf keys_out(sizeof(unsigned long long) * A->nnz, ctx->stream);
-  DBuf idx(sizeof(int64_t) * A->nnz, ctx->stream);
-  expand_rows<<<blocks_for(A->nrows), kThreads, 0, ctx->stream>>>(A->nrows, A->row_ptr, A->col_idx,
-                                                                  keys.as<unsigned long long>(), T->row_ptr);
-  check_launch(ctx, "expand_rows");
-  iota_i64<<<blocks_for(A->nnz), kThreads, 0, ctx->stream>>>(A->nnz, idx.as<int64_t>());
-  check_launch(ctx, "iota_i64");
-  int bits = 32;
-  while ((1ll << (bits - 32)) <= A->ncols && bits < 64)
-    ++bits;
-  size_t tmp = 0;
-  MG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys.as<unsigned long long>(),
-                                          keys_out.as<unsigned long long>(), idx.as<int64_t>(), perm.as<int64_t>(),
-                                          A->nnz, 0, bits, ctx->stream));
-  DBuf t(tmp, ctx->stream);
-  MG_CUDA(cub::DeviceRadixSort::SortPairs(t.ptr, tmp, keys.as<unsigned long long>(), keys_out.as<unsigned long long>(),
-                                          idx.as<int64_t>(), perm.as<int64_t>(), A->nnz, 0, bits, ctx->stream));
-  count_launch(ctx);
-  keys_to_cols<<<blocks_for(A->nnz), kThreads, 0, ctx->stream>>>(A->nnz, keys_out.as<unsigned long long>(),
-                                                                  T->col_idx);
-  check_launch(ctx, "keys_to_cols");
+  count_cols<<<blocks_for(A->nrows), kThreads, 0, ctx->stream>>>(A->nrows, A->row_ptr, A->col_idx, T->row_ptr);
+  check_launch(ctx, "count_cols");
+  scan_row_ptr(ctx, T->row_ptr, A->ncols);
+  DBuf cursor(sizeof(unsigned long long) * (A->ncols > 0 ? A->ncols : 1), ctx->stream);
+  MG_CUDA(cudaMemsetAsync(cursor.ptr, 0, sizeof(unsigned long long) * A->ncols, ctx->stream));
+  scatter_cols<<<blocks_for(A->nrows), kThreads, 0, ctx->stream>>>(
+      A->nrows, A->row_ptr, A->col_idx, T->row_ptr, cursor.as<unsigned long long>(), perm.as<int64_t>(), T->col_idx);
+  check_launch(ctx, "scatter_cols");
+  sort_cols<<<blocks_for(A->ncols), kThreads, 0, ctx->stream>>>(A->ncols, T->row_ptr, perm.as<int64_t>(), T->col_idx);
+  check_launch(ctx, "sort_cols");
   gather_values<<<blocks_for(A->nnz), kThreads, 0, ctx->stream>>>(A->nnz, perm.as<int64_t>(), A->values, T->values);
   check_launch(ctx, "gather_values");
-  scan_row_ptr(ctx, T->row_ptr, A->ncols);
   return T;
+}
+
+// Device CSR transpose, deterministic (each transposed row in ascending
+// original-row order, sparse.cpp:238-247).
+mgpu_csr *transpose_csr(mgpu_ctx *ctx, const mgpu_csr *A)
+{
+  DBuf perm;
+  return transpose_perm(ctx, A, perm);
+}
+
+namespace
+{
+struct GatherBatch
+{
+  const double *src[64];
+  double *dst[64];
+};
+__global__ void gather_batched_kernel(int l, int64_t nnz, const int64_t *__restrict__ perm, GatherBatch gb)
+{
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= static_cast<int64_t>(l) * nnz)
+    return;
+  const int p = static_cast<int>(t / nnz);
+  const int64_t k = t - static_cast<int64_t>(p) * nnz;
+  gb.dst[p][k] = gb.src[p][perm[k]];
+}
+} // namespace
+
+// dst[p][k] = src[p][perm[k]] for l value arrays sharing one permutation (one launch per 64).
+void gather_batched(mgpu_ctx *ctx, int l, int64_t nnz, const int64_t *perm, const double *const *src,
+                    double *const *dst)
+{
+  if (nnz == 0)
+    return;
+  for (int b = 0; b < l; b += 64)
+  {
+    const int c = l - b < 64 ? l - b : 64;
+    GatherBatch gb{};
+    for (int p = 0; p < c; ++p)
+    {
+      gb.src[p] = src[b + p];
+      gb.dst[p] = dst[b + p];
+    }
+    gather_batched_kernel<<<blocks_for(static_cast<int64_t>(c) * nnz), kThreads, 0, ctx->stream>>>(c, nnz, perm, gb);
+    check_launch(ctx, "gather_batched");
+  }
 }
 
 void gather_dev(mgpu_ctx *ctx, int64_t nnz, const int64_t *perm, const double *src, double *dst)
