@@ -138,7 +138,7 @@ int mgpu_chain_apply(mgpu_ctx *ctx, int z, const mgpu_csr *const *factors, const
 
 typedef enum mgpu_spai_mode
 {
-  MGPU_SPAI_SEQUENTIAL = 0, /* spai.hpp:38-42 (not available on the device: MGPU_ERR_UNSUPPORTED) */
+  MGPU_SPAI_SEQUENTIAL = 0, /* spai.hpp:38-42 (device: dense built factor, n <= 8192, else MGPU_ERR_UNSUPPORTED) */
   MGPU_SPAI_FROZEN = 1,
 } mgpu_spai_mode;
 

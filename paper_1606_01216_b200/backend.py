@@ -11,8 +11,9 @@ plus solve_all(rhs), which batches every point into one persistent CG kernel
 
 Config fields are AirgaConfig's (airga.hpp:40-69) plus the GPU-only choices
 spai_algorithm ("mr" = the reference's Alg. 2/4, "ls" = static-pattern
-least squares) and ls_pattern (A or A^2).  The reference's default
-spai_mode=sequential has no device implementation yet and is rejected loudly.
+least squares) and ls_pattern (A or A^2).  spai_mode is the reference's
+(sequential by default in AirgaConfig; the device sequential mode keeps the
+built factor dense and is bounded at n <= 8192, frozen mode has no bound).
 """
 from __future__ import annotations
 
@@ -30,7 +31,7 @@ class CudaCgConfig:
     solver: str = "cg_spai"  # cg_plain | cg_spai | cg_spai_update   (airga.hpp:42-48)
     spai_tol: float = 0.01
     spai_max_col_iters: int = 50
-    spai_mode: int = mgpu.FROZEN
+    spai_mode: int = mgpu.SEQUENTIAL  # AirgaConfig default (airga.hpp)
     cg_rtol: float = 1e-10
     cg_maxit_factor: int = 10
     update_start_iteration: int = 3
@@ -53,9 +54,6 @@ class CudaCgBackend:
     def __init__(self, cfg: CudaCgConfig, ctx: Optional[mgpu.Context] = None):
         if cfg.solver not in ("cg_plain", "cg_spai", "cg_spai_update"):
             raise mgpu.ArgumentError(f"CudaCgBackend: unsupported solver {cfg.solver}")
-        if cfg.spai_algorithm == "mr" and cfg.spai_mode != mgpu.FROZEN and cfg.solver != "cg_plain":
-            raise mgpu.UnsupportedError("CudaCgBackend: sequential MR-SPAI has no device implementation; "
-                                        "use spai_mode=FROZEN or spai_algorithm='ls'")
         self.cfg = cfg
         self.ctx = ctx or mgpu.default_context()
         self.n = 0

@@ -26,6 +26,8 @@
 namespace mgpu
 {
 mgpu_csr *transpose_csr(mgpu_ctx *ctx, const mgpu_csr *A);
+mgpu_csr *mr_build_sequential(mgpu_ctx *ctx, const mgpu_csr *K, const mgpu_csr *rhs_src, double alpha, double tol,
+                              int64_t max_iters, double *col_residual);
 void trace_dev(mgpu_ctx *ctx, const mgpu_csr *A, double *out_dev);
 void trace_inner_dev(mgpu_ctx *ctx, const mgpu_csr *A, const mgpu_csr *B, double *out_dev);
 
@@ -416,8 +418,7 @@ int mgpu_spai_build(mgpu_ctx *ctx, const mgpu_csr *K, double tol, int64_t max_co
     MG_ARG(K && P, "spai_build: null argument");
     MG_ARG(K->nrows == K->ncols, "spai_build: K must be square"); // spai.cpp:316-319
     MG_ARG(tol > 0.0, "spai_build: tol must be positive");
-    if (mode != MGPU_SPAI_FROZEN)
-      throw Error(MGPU_ERR_UNSUPPORTED, "spai_build: sequential mode has no device implementation (use frozen)");
+    MG_ARG(mode == MGPU_SPAI_FROZEN || mode == MGPU_SPAI_SEQUENTIAL, "spai_build: unknown mode");
     DBuf sc(2 * sizeof(double), ctx->stream);
     trace_inner_dev(ctx, K, K, sc.as<double>());
     trace_dev(ctx, K, sc.as<double>() + 1);
@@ -425,7 +426,8 @@ int mgpu_spai_build(mgpu_ctx *ctx, const mgpu_csr *K, double tol, int64_t max_co
     if (!(denom > 0.0))
       throw Error(MGPU_ERR_NUMERICAL, "spai_build: trace(K K^T) is not positive");
     const double alpha = fetch(ctx, sc.as<double>() + 1) / denom; // spai.cpp:329
-    *P = mr_build(ctx, K, nullptr, alpha, tol, max_col_iters, col_residual);
+    *P = mode == MGPU_SPAI_SEQUENTIAL ? mr_build_sequential(ctx, K, nullptr, alpha, tol, max_col_iters, col_residual)
+                                      : mr_build(ctx, K, nullptr, alpha, tol, max_col_iters, col_residual);
   });
 }
 
@@ -437,8 +439,7 @@ int mgpu_spai_update(mgpu_ctx *ctx, const mgpu_csr *K_old, const mgpu_csr *K_new
     MG_ARG(K_old->nrows == K_old->ncols && K_new->nrows == K_new->ncols && K_old->nrows == K_new->nrows,
            "spai_update: operands must be square with equal shape");
     MG_ARG(tol > 0.0, "spai_update: tol must be positive");
-    if (mode != MGPU_SPAI_FROZEN)
-      throw Error(MGPU_ERR_UNSUPPORTED, "spai_update: sequential mode has no device implementation (use frozen)");
+    MG_ARG(mode == MGPU_SPAI_FROZEN || mode == MGPU_SPAI_SEQUENTIAL, "spai_update: unknown mode");
     DBuf sc(3 * sizeof(double), ctx->stream);
     trace_inner_dev(ctx, K_new, K_new, sc.as<double>());
     trace_inner_dev(ctx, K_old, K_new, sc.as<double>() + 1);
@@ -447,7 +448,9 @@ int mgpu_spai_update(mgpu_ctx *ctx, const mgpu_csr *K_old, const mgpu_csr *K_new
     if (!(denom > 0.0))
       throw Error(MGPU_ERR_NUMERICAL, "spai_update: trace(K_new^T K_new) is not positive");
     const double alpha = 0.5 * (fetch(ctx, sc.as<double>() + 1) + fetch(ctx, sc.as<double>() + 2)) / denom;
-    *Q = mr_build(ctx, K_new, K_old, alpha, tol, max_col_iters, col_residual); // spai.cpp:348-349
+    *Q = mode == MGPU_SPAI_SEQUENTIAL // spai.cpp:348-349
+             ? mr_build_sequential(ctx, K_new, K_old, alpha, tol, max_col_iters, col_residual)
+             : mr_build(ctx, K_new, K_old, alpha, tol, max_col_iters, col_residual);
   });
 }
 

@@ -92,6 +92,18 @@ int main()
   compare_backends("cg_spai", sys, cfg, seq, cuda::SpaiAlgorithm::mr);
   cfg.solver = AirgaConfig::Solver::cg_plain;
   compare_backends("cg_plain", sys, cfg, {{1.0, 50.0}}, cuda::SpaiAlgorithm::mr);
+  // the reference default, spai_mode = sequential (d = P r over the built columns): heavy fill,
+  // so a smaller system keeps the reference side to seconds
+  ModelSpec small = spec;
+  small.n = 400;
+  const SecondOrderSystem sys_small = beam_generate(small);
+  AirgaConfig seq_cfg;
+  seq_cfg.spai_mode = SpaiOptions::Mode::sequential;
+  seq_cfg.update_start_iteration = 2;
+  seq_cfg.solver = AirgaConfig::Solver::cg_spai_update;
+  compare_backends("cg_spai_update/sequential", sys_small, seq_cfg, seq, cuda::SpaiAlgorithm::mr);
+  seq_cfg.solver = AirgaConfig::Solver::cg_spai;
+  compare_backends("cg_spai/sequential", sys_small, seq_cfg, seq, cuda::SpaiAlgorithm::mr);
 
   cuda::Device dev(0);
   // free-function drop-ins: spai_build / spai_update / chain_apply / pcg_solve / block_solve

@@ -29,13 +29,15 @@ def test_cpp_dropin_backend_parity():
     assert res["solves"] >= 20 and res["max_rel_x"] <= 1e-8 and res["max_iter_diff"] <= 2
 
 
-@pytest.mark.parametrize("solver", ["cg_spai_update", "cg_spai", "cg_plain"])
-def test_python_backend_sequence(mg, ref, solver):
+@pytest.mark.parametrize("solver,mode,n", [("cg_spai_update", 1, 1500), ("cg_spai", 1, 1500), ("cg_plain", 1, 1500),
+                                          ("cg_spai_update", 0, 400), ("cg_spai", 0, 400)])
+def test_python_backend_sequence(mg, ref, solver, mode, n):
+    """mode 1 = frozen, 0 = sequential (AirgaConfig's default)."""
     from paper_1606_01216_b200.backend import CudaCgBackend, CudaCgConfig
-    M, D, K = ref.chain_generate(1500, consistent=True, stiffness_scale=1.0)
-    rb = ref.backend(solver, M, D, K, spai_mode=1, update_start_iteration=2)
-    gb = CudaCgBackend(CudaCgConfig(solver=solver, update_start_iteration=2))
-    F = np.zeros((1500, 1))
+    M, D, K = ref.chain_generate(n, consistent=True, stiffness_scale=1.0)
+    rb = ref.backend(solver, M, D, K, spai_mode=mode, update_start_iteration=2)
+    gb = CudaCgBackend(CudaCgConfig(solver=solver, update_start_iteration=2, spai_mode=mode))
+    F = np.zeros((n, 1))
     F[0, 0] = 1.0
     seq = [[1.0, 10.0, 100.0], [2.0, 12.0, 90.0], [3.0, 15.0, 80.0]]
     for z, pts in enumerate(seq, start=1):

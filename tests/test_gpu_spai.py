@@ -1,4 +1,4 @@
-"""SPAI parity: device MR-SPAI (reference Alg. 2/4, frozen) and LS-SPAI against the oracle.
+"""SPAI parity: device MR-SPAI (reference Alg. 2/4, frozen and sequential) and LS-SPAI against the oracle.
 
 Bar: SPAI entries within 1e-10 relative (BASELINE.json north_star), identical
 sparsity pattern, per-column residuals within 1e-10, identical exception class
@@ -100,8 +100,55 @@ def test_mr_stagnation_column_and_message(mg, oracle):
     assert str(eg.value).split(" stalled")[0] == eo.value.msg.split(" stalled")[0]
 
 
-def test_mr_sequential_rejected_loudly(mg, oracle):
-    M, D, K = oracle.chain_generate(100)
+# --------------------------------------------- MR-SPAI, sequential mode (the reference default)
+@pytest.mark.parametrize("n,kscale,s", [(300, 0.01, 1.0), (300, 1.0, 10.0), (300, 100.0, 10.0), (500, 1.0, 10.0),
+                                        (2000, 1.0, 100.0)])
+def test_mr_sequential_build_t1(mg, oracle, n, kscale, s):
+    """d = P r over the columns built so far (spai.cpp:138-158): heavy fill (200-700 nnz/column)."""
+    M, D, K = oracle.chain_generate(n, consistent=True, stiffness_scale=kscale)
+    A = oracle.shifted_operator(M, D, K, s)
+    want, wres = oracle.spai_build(A, mode=0)
+    f = mg.spai_build(A, mode=mg.SEQUENTIAL)
+    _csr_close(f.matrix.download(), want)
+    assert rel(f.target_frob_residual, wres) < 1e-10
+
+
+def test_mr_sequential_update_t1(mg, oracle):
+    """s = 10 -> 10.5 at n = 100, sequential mode."""
+    M, D, K = oracle.chain_generate(100, consistent=True, stiffness_scale=1.0)
+    A1 = oracle.shifted_operator(M, D, K, 10.0)
+    A2 = oracle.shifted_operator(M, D, K, 10.5)
+    want, wres = oracle.spai_update(A1, A2, mode=0)
+    f = mg.spai_update(A1, A2, mode=mg.SEQUENTIAL)
+    _csr_close(f.matrix.download(), want)
+    assert rel(f.target_frob_residual, wres) < 1e-10
+    Q = mg.spai_update(A2, A2, mode=mg.SEQUENTIAL).matrix.download()  # K_new == K_old -> Q = I exactly
+    np.testing.assert_array_equal(Q.todense(), np.eye(100))
+
+
+def test_mr_sequential_kats(mg):
+    from oracle import Csr
+    P = mg.spai_build(Csr.from_dense(np.eye(5)), mode=mg.SEQUENTIAL).matrix.download()
+    np.testing.assert_array_equal(P.todense(), np.eye(5))
+    P = mg.spai_build(Csr.from_dense(np.diag([2.0, 4.0])), tol=1e-12, mode=mg.SEQUENTIAL).matrix.download()
+    assert rel(P.todense(), np.diag([0.5, 0.25])) < 1e-12
+
+
+def test_mr_sequential_stagnation(mg, oracle):
+    from oracle import OracleError
+    M, D, K = oracle.hermite_generate(1000)
+    A = oracle.shifted_operator(M, D, K, 100.0)
+    with pytest.raises(OracleError) as eo:
+        oracle.spai_build(A, mode=0)
+    with pytest.raises(mg.StagnationError) as eg:
+        mg.spai_build(A, mode=mg.SEQUENTIAL)
+    assert eg.value.column == eo.value.index
+    assert str(eg.value).split(" stalled")[0] == eo.value.msg.split(" stalled")[0]
+
+
+def test_mr_sequential_size_bound(mg, oracle):
+    """The device keeps the built factor dense: n > 8192 is refused before any work."""
+    M, D, K = oracle.chain_generate(9000)
     with pytest.raises(mg.UnsupportedError):
         mg.spai_build(K, mode=mg.SEQUENTIAL)
 
