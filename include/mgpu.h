@@ -134,6 +134,12 @@ int mgpu_spmv(mgpu_ctx *ctx, const mgpu_csr *A, const double *x, double *y);
 int mgpu_chain_apply(mgpu_ctx *ctx, int z, const mgpu_csr *const *factors, const double *x, double *y,
                      mgpu_memkind where);
 
+/* spai.cpp:375-409 chain_quality: sqrt((n / samples) sum_k ||(I - K P_chain) g_k||^2) over
+ * `samples` unit-norm Gaussian probes from std::mt19937_64(seed) + std::normal_distribution
+ * (the reference's stream; default seed 42, spai.hpp:84-85).  factors newest first (z may be 0). */
+int mgpu_chain_quality(mgpu_ctx *ctx, int z, const mgpu_csr *const *factors, const mgpu_csr *K, int64_t samples,
+                       uint64_t seed, double *out);
+
 /* ------------------------------------------------------------------ SPAI */
 
 typedef enum mgpu_spai_mode

@@ -247,6 +247,16 @@ class _Lib:
             assert st == OK
         return Q, R, rank.value
 
+    def chain_quality(self, factors, K, samples: int, seed: int = 42) -> float:
+        """spai.cpp:375-409 (reference only: its probes are libstdc++'s mt19937_64 / normal_distribution)."""
+        if self.prefix != "ref_":
+            raise NotImplementedError("chain_quality is checked against the reference itself")
+        z, arr, keep = self._chain(factors)
+        hK = self._in(K)
+        f = self._f("chain_quality")
+        f.restype = C.c_double
+        return f(C.c_int(z), arr, C.byref(hK), C.c_int64(samples), C.c_uint64(seed))
+
     def chain_apply(self, factors, v) -> np.ndarray:
         v = np.ascontiguousarray(v, np.float64)
         out = np.zeros_like(v)

@@ -213,6 +213,20 @@ std::vector<double> chain_apply(Device &dev, const PreconditionerChain &chain, s
   return out;
 }
 
+double chain_quality(Device &dev, const PreconditionerChain &chain, const SparseMatrix &K, std::int64_t samples,
+                     std::uint64_t seed)
+{
+  if (samples < 1)
+    throw ArgumentError("chain_quality: samples must be >= 1"); // spai.cpp:378-381
+  std::vector<DeviceMatrix> keep;
+  const std::vector<mgpu_csr *> h = chain.empty() ? std::vector<mgpu_csr *>{} : upload_chain(dev, chain, keep);
+  const DeviceMatrix dK(dev, K);
+  double out = 0.0;
+  check(dev.ctx(), mgpu_chain_quality(dev.ctx(), static_cast<int>(h.size()), h.empty() ? nullptr : h.data(), dK.get(),
+                                      samples, seed, &out));
+  return out;
+}
+
 SolveReport pcg_solve(Device &dev, const SparseMatrix &A, const PreconditionerChain &P, std::span<const double> b,
                       double rtol, std::int64_t maxit)
 {

@@ -17,6 +17,7 @@
 //       spai_build / spai_update      (spai.hpp:53-61)  -> MR-SPAI on the device
 //       spai_ls                       (north star LS-SPAI, not in the reference)
 //       chain_apply                   (spai.hpp:77-79)
+//       chain_quality                 (spai.hpp:81-85)
 //       pcg_solve / block_solve       (krylov.hpp:41-56)
 //   The reference's pcg_solve takes LinearOperators wrapping std::function;
 //   arbitrary host callables cannot run on the device, so the drop-ins take
@@ -89,6 +90,9 @@ SpaiFactor spai_update(Device &dev, const SparseMatrix &K_old, const SparseMatri
 /// pattern 0: A's pattern, 1: symbolic A*A.  K_old == nullptr builds P.
 SpaiFactor spai_ls(Device &dev, const SparseMatrix &A, const SparseMatrix *K_old, int pattern = 0);
 std::vector<double> chain_apply(Device &dev, const PreconditionerChain &chain, std::span<const double> v);
+/// Stochastic ||I - K P_chain||_F, the reference's probe stream (mt19937_64(seed)).
+double chain_quality(Device &dev, const PreconditionerChain &chain, const SparseMatrix &K, std::int64_t samples,
+                     std::uint64_t seed = 42);
 SolveReport pcg_solve(Device &dev, const SparseMatrix &A, const PreconditionerChain &P, std::span<const double> b,
                       double rtol, std::int64_t maxit);
 BlockSolveResult block_solve(Device &dev, const SparseMatrix &A, const PreconditionerChain &P, const DenseMatrix &B,

@@ -28,7 +28,7 @@ EXPORTED = [
     "mgpu_ctx_create", "mgpu_ctx_destroy", "mgpu_ctx_synchronize", "mgpu_last_error", "mgpu_status_string",
     "mgpu_launch_count", "mgpu_last_cg_timing", "mgpu_ctx_set_cg_path", "mgpu_last_cg_path", "mgpu_csr_upload", "mgpu_csr_upload_device", "mgpu_csr_info",
     "mgpu_csr_download", "mgpu_csr_device_view", "mgpu_csr_free", "mgpu_sp_add_scaled", "mgpu_shifted_operators",
-    "mgpu_transpose", "mgpu_trace", "mgpu_trace_inner", "mgpu_spmv", "mgpu_chain_apply", "mgpu_spai_build",
+    "mgpu_transpose", "mgpu_trace", "mgpu_trace_inner", "mgpu_spmv", "mgpu_chain_apply", "mgpu_chain_quality", "mgpu_spai_build",
     "mgpu_spai_update", "mgpu_spai_ls", "mgpu_spai_ls_batched", "mgpu_spgemm", "mgpu_cg_solve",
     "mgpu_model_chain", "mgpu_model_hermite", "mgpu_host_free",
 ]
@@ -127,6 +127,7 @@ def lib():
         L.mgpu_trace_inner.argtypes = [vp, vp, vp, C.POINTER(dbl)]
         L.mgpu_spmv.argtypes = [vp, vp, vp, vp]
         L.mgpu_chain_apply.argtypes = [vp, C.c_int, vp, vp, vp, C.c_int]
+        L.mgpu_chain_quality.argtypes = [vp, C.c_int, vp, vp, C.c_int64, C.c_uint64, C.POINTER(C.c_double)]
         L.mgpu_spai_build.argtypes = [vp, vp, dbl, i64, C.c_int, C.POINTER(vp), vp]
         L.mgpu_spai_update.argtypes = [vp, vp, vp, dbl, i64, C.c_int, C.POINTER(vp), vp]
         L.mgpu_spai_ls.argtypes = [vp, vp, vp, C.c_int, C.POINTER(vp)]
@@ -372,6 +373,18 @@ def chain_apply(chain: Sequence, v, ctx=None) -> np.ndarray:
     out = np.zeros_like(v)
     ctx.check(lib().mgpu_chain_apply(ctx.handle, len(dev), _handles(dev), _ptr(v), _ptr(out), MGPU_HOST))
     return out
+
+
+def chain_quality(chain: Sequence, K, samples: int, seed: int = 42, ctx=None) -> float:
+    """spai.cpp:375-409: sqrt((n / samples) sum_k ||(I - K P) g_k||^2), the reference's probe
+    stream (mt19937_64(seed), normal_distribution); chain newest first, may be empty."""
+    ctx = ctx or default_context()
+    dK = _dev(K, ctx)
+    dev = [_dev(_factor_mat(f), ctx) for f in chain]
+    out = C.c_double()
+    ctx.check(lib().mgpu_chain_quality(ctx.handle, len(dev), _handles(dev) if dev else None, dK.handle,
+                                       int(samples), int(seed), C.byref(out)))
+    return out.value
 
 
 # ---------------------------------------------------------------- SPAI

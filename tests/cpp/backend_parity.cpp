@@ -134,6 +134,11 @@ int main()
     dchain = std::max(dchain, std::fabs(ca[i] - cb[i]));
   if (dchain != 0.0) // same factors, in-order SpMV: bitwise
     ++failures;
+  // chain_quality: the reference's probe stream, device SpMM + deterministic sums
+  const double qr_ref = chain_quality(chr, A2, 8, 42), qr_gpu = cuda::chain_quality(dev, chr, A2, 8, 42);
+  const double dq = std::fabs(qr_ref - qr_gpu) / std::fabs(qr_ref);
+  if (!(dq <= 1e-12))
+    ++failures;
   const auto P = LinearOperator{[&chr](std::span<const double> x) { return chain_apply(chr, x); }, 2000};
   const SolveReport ra = pcg_solve(LinearOperator::from_sparse(A2), P, v, 1e-10, 20000);
   const SolveReport rb = cuda::pcg_solve(dev, A2, chr, v, 1e-10, 20000);
@@ -164,8 +169,8 @@ int main()
   if (stag_ref != stag_gpu || stag_ref < 0 || bd_ref != bd_gpu || bd_ref < 0)
     ++failures;
   std::printf("{\"solves\": %d, \"max_rel_x\": %.3e, \"max_iter_diff\": %ld, \"spai_rel\": %.3e, "
-              "\"chain_apply_abs\": %.3e, \"pcg_rel\": %.3e, \"stagnation_col\": [%ld, %ld], "
+              "\"chain_apply_abs\": %.3e, \"chain_quality_rel\": %.3e, \"pcg_rel\": %.3e, \"stagnation_col\": [%ld, %ld], "
               "\"breakdown_it\": [%ld, %ld], \"failures\": %d}\n",
-              solves, worst_x, worst_it, dspai, dchain, dpcg, stag_ref, stag_gpu, bd_ref, bd_gpu, failures);
+              solves, worst_x, worst_it, dspai, dchain, dq, dpcg, stag_ref, stag_gpu, bd_ref, bd_gpu, failures);
   return failures == 0 ? 0 : 1;
 }

@@ -236,3 +236,24 @@ def test_spgemm_collapse(mg, oracle):
     assert rel(QP.todense(), dense) < 1e-14
     v = np.random.default_rng(2).standard_normal(800)
     assert rel(mg.chain_apply([QP], v), oracle.chain_apply([Q, P], v)) < 1e-12
+
+
+# ------------------------------------------------------------------ chain_quality
+@pytest.mark.parametrize("z,samples,seed", [(0, 3, 42), (1, 8, 42), (2, 5, 7)])
+def test_chain_quality_matches_reference(mg, oracle, ref, z, samples, seed):
+    """spai.cpp:375-409: same probe stream (mt19937_64 + normal_distribution), device SpMM + sums."""
+    M, D, K = oracle.chain_generate(1500, consistent=True, stiffness_scale=1.0)
+    A1 = oracle.shifted_operator(M, D, K, 10.0)
+    A2 = oracle.shifted_operator(M, D, K, 11.0)
+    P, _ = oracle.spai_build(A1, mode=1)
+    Q, _ = oracle.spai_update(A1, A2, mode=1)
+    chain = [Q, P][2 - z:] if z else []
+    want = ref.chain_quality(chain, A2, samples, seed)
+    got = mg.chain_quality(chain, A2, samples, seed)
+    assert abs(got - want) <= 1e-12 * abs(want)
+
+
+def test_chain_quality_rejects_zero_samples(mg, oracle):
+    M, D, K = oracle.chain_generate(50)
+    with pytest.raises(mg.ArgumentError, match="samples must be >= 1"):
+        mg.chain_quality([], K, 0)
