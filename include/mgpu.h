@@ -234,6 +234,28 @@ int mgpu_model_hermite(int64_t ne, double E, double I, double rho, double area, 
                        mgpu_host_csr *M, mgpu_host_csr *D, mgpu_host_csr *K);
 void mgpu_host_free(mgpu_host_csr *a);
 
+
+/* ------------------------------------------------------------------ global Arnoldi + projection */
+
+/* dense.cpp:153-246 thin_qr: A (rows x cols, column-major) -> Q (rows x cols), R (cols x cols), rank
+ * (Householder; columns with sigma <= rank_tol ||A||_F are flushed to zero, R's diagonal made
+ * nonnegative).  rows >= cols (MGPU_ERR_ARG otherwise), cols <= 1024 on the device. */
+int mgpu_thin_qr(mgpu_ctx *ctx, int64_t rows, int64_t cols, const double *A, double rank_tol, double *Q, double *R,
+                 int64_t *rank, mgpu_memkind where);
+
+/* airga.cpp:485-500 project_reduce: V (n x r, column-major, orthonormal basis) ->
+ *   Mh, Dh, Kh (r x r) = V^T S V,  Fh (r x m) = V^T F,  Cph, Cvh (q x r) = Cp V, Cv V
+ * (Cp, Cv: q x n column-major; m = 0 skips F, q = 0 skips Cp / Cv).  All dense buffers in `where` memory. */
+int mgpu_project_reduce(mgpu_ctx *ctx, const mgpu_csr *M, const mgpu_csr *D, const mgpu_csr *K, int64_t r,
+                        const double *V, int64_t m, const double *F, int64_t q, const double *Cp, const double *Cv,
+                        double *Mh, double *Dh, double *Kh, double *Fh, double *Cph, double *Cvh, mgpu_memkind where);
+
+/* airga.cpp:456-473 arnoldi_deflate: two sweeps of X -= <B_t, X> B_t over the nblocks basis blocks
+ * (each `len` values, the same shape as X); gammas[t] = sum of both sweeps' coefficients.
+ * X and blocks in `where` memory, gammas on the host. */
+int mgpu_arnoldi_deflate(mgpu_ctx *ctx, int64_t len, double *X, int nblocks, const double *const *blocks,
+                         double *gammas, mgpu_memkind where);
+
 #ifdef __cplusplus
 }
 #endif

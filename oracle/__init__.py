@@ -247,6 +247,39 @@ class _Lib:
             assert st == OK
         return Q, R, rank.value
 
+    def project_reduce(self, M, D, K, V, F=None, Cp=None, Cv=None) -> dict:
+        """airga.cpp:485-500 (reference only)."""
+        V = np.asfortranarray(V, np.float64)
+        n, r = V.shape
+        Fm = np.asfortranarray(F, np.float64) if F is not None else np.zeros((n, 0), order="F")
+        m = Fm.shape[1]
+        q = 0 if Cp is None else np.asarray(Cp).shape[0]
+        Cpm = np.asfortranarray(Cp, np.float64) if q else np.zeros((0, n), order="F")
+        Cvm = np.asfortranarray(Cv, np.float64) if q else np.zeros((0, n), order="F")
+        out = {k: np.zeros(shape, order="F") for k, shape in
+               (("Mh", (r, r)), ("Dh", (r, r)), ("Kh", (r, r)), ("Fh", (r, m)), ("Cph", (q, r)), ("Cvh", (q, r)))}
+        hM, hD, hK = self._in(M), self._in(D), self._in(K)
+        err = _CErr()
+        st = self._f("project_reduce")(C.byref(hM), C.byref(hD), C.byref(hK), C.c_int64(r), _dp(V), C.c_int64(m),
+                                       _dp(Fm), C.c_int64(q), _dp(Cpm), _dp(Cvm), _dp(out["Mh"]), _dp(out["Dh"]),
+                                       _dp(out["Kh"]), _dp(out["Fh"]), _dp(out["Cph"]), _dp(out["Cvh"]),
+                                       C.byref(err))
+        self._check(st, err)
+        return out
+
+    def arnoldi_deflate(self, X, blocks):
+        """airga.cpp:456-473 (reference only): returns (deflated X, gammas)."""
+        X = np.asfortranarray(X, np.float64).copy(order="F")
+        rows, cols = X.shape if X.ndim == 2 else (X.shape[0], 1)
+        bl = [np.asfortranarray(b, np.float64) for b in blocks]
+        ptrs = (C.c_void_p * max(len(bl), 1))(*[b.ctypes.data for b in bl])
+        g = np.zeros(max(len(bl), 1))
+        err = _CErr()
+        st = self._f("arnoldi_deflate")(C.c_int64(rows), C.c_int64(cols), _dp(X), C.c_int(len(bl)), ptrs, _dp(g),
+                                        C.byref(err))
+        self._check(st, err)
+        return X, g[:len(bl)]
+
     def chain_quality(self, factors, K, samples: int, seed: int = 42) -> float:
         """spai.cpp:375-409 (reference only: its probes are libstdc++'s mt19937_64 / normal_distribution)."""
         if self.prefix != "ref_":

@@ -372,6 +372,64 @@ int ref_thin_qr(int64_t rows, int64_t cols, const double *A, double rank_tol, do
   });
 }
 
+// project_reduce (airga.cpp:485-500) on (M, D, K, F, Cp, Cv) and an assembled basis V (n x r).
+int ref_project_reduce(const ref_csr *M, const ref_csr *D, const ref_csr *K, int64_t r, const double *V, int64_t m,
+                       const double *F, int64_t q, const double *Cp, const double *Cv, double *Mh, double *Dh,
+                       double *Kh, double *Fh, double *Cph, double *Cvh, ref_err *err)
+{
+  return guarded(err, [&] {
+    mor::SecondOrderSystem sys;
+    sys.M = to_mor(M);
+    sys.D = to_mor(D);
+    sys.K = to_mor(K);
+    const int64_t n = sys.M.nrows;
+    sys.F = mor::DenseMatrix(n, m);
+    if (m > 0)
+      std::memcpy(sys.F.values.data(), F, sizeof(double) * n * m);
+    sys.Cp = mor::DenseMatrix(q, n);
+    sys.Cv = mor::DenseMatrix(q, n);
+    if (q > 0)
+    {
+      std::memcpy(sys.Cp.values.data(), Cp, sizeof(double) * q * n);
+      std::memcpy(sys.Cv.values.data(), Cv, sizeof(double) * q * n);
+    }
+    mor::OrthonormalBasis basis;
+    basis.assembled = mor::DenseMatrix(n, r);
+    std::memcpy(basis.assembled.values.data(), V, sizeof(double) * n * r);
+    const mor::ReducedSystem rs = mor::project_reduce(sys, basis);
+    std::memcpy(Mh, rs.Mh.values.data(), sizeof(double) * r * r);
+    std::memcpy(Dh, rs.Dh.values.data(), sizeof(double) * r * r);
+    std::memcpy(Kh, rs.Kh.values.data(), sizeof(double) * r * r);
+    if (m > 0)
+      std::memcpy(Fh, rs.Fh.values.data(), sizeof(double) * r * m);
+    if (q > 0)
+    {
+      std::memcpy(Cph, rs.Cph.values.data(), sizeof(double) * q * r);
+      std::memcpy(Cvh, rs.Cvh.values.data(), sizeof(double) * q * r);
+    }
+  });
+}
+
+// arnoldi_deflate (airga.cpp:456-473): X (rows x cols) against nblocks blocks of the same shape.
+int ref_arnoldi_deflate(int64_t rows, int64_t cols, double *X, int nblocks, const double *const *blocks,
+                        double *gammas, ref_err *err)
+{
+  return guarded(err, [&] {
+    mor::DenseMatrix x(rows, cols);
+    std::memcpy(x.values.data(), X, sizeof(double) * rows * cols);
+    std::vector<mor::DenseMatrix> bl;
+    for (int t = 0; t < nblocks; ++t)
+    {
+      bl.emplace_back(rows, cols);
+      std::memcpy(bl.back().values.data(), blocks[t], sizeof(double) * rows * cols);
+    }
+    const std::vector<double> g = mor::arnoldi_deflate(x, bl);
+    std::memcpy(X, x.values.data(), sizeof(double) * rows * cols);
+    for (int t = 0; t < nblocks; ++t)
+      gammas[t] = g[static_cast<std::size_t>(t)];
+  });
+}
+
 // ---- LS-SPAI from reference primitives (SURVEY.md 8(a') definition) ----
 //
 // The static-pattern least-squares SPAI is NOT in the reference (north star

@@ -4,6 +4,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cublas_v2.h>
+
 #include "internal.cuh"
 
 namespace mgpu
@@ -287,6 +289,8 @@ int mgpu_ctx_destroy(mgpu_ctx *ctx)
     cudaEventDestroy(ctx->ev1);
   if (ctx->own_stream)
     cudaStreamDestroy(ctx->stream);
+  if (ctx->blas)
+    cublasDestroy(static_cast<cublasHandle_t>(ctx->blas));
   if (ctx->prof_dev)
   {
     long long h[16] = {0};

@@ -111,6 +111,7 @@ struct mgpu_ctx
   int last_cg_path = 1; // 0 banded (grid), 1 general, 2 cluster v2 (m = 1), 3 cluster v1
   int cg_path = 0;      // 0 auto, 1 force general, 2 force banded grid kernel, 3 cluster v1 only, 4 stream (no cluster)
   long long *prof_dev = nullptr; // diagnostics: per-phase clock64 totals of the cluster kernel (MGPU_PROFILE_PHASES)
+  void *blas = nullptr;          // cublasHandle_t, created on first dense product (project.cu)
   // last error
   int last_status = MGPU_OK;
   int64_t err_index = -1, err_col = -1, err_point = -1;

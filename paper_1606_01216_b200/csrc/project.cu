@@ -1,0 +1,504 @@
+// Global Arnoldi + projection on the device:
+//
+//   thin_qr         dense.cpp:153-246   Householder QR of the n x k basis block
+//   project_reduce  airga.cpp:485-500   Mh, Dh, Kh = V^T S V, Fh = V^T F, Cph/Cvh = C V
+//   arnoldi_deflate airga.cpp:456-473   X -= <B_t, X> B_t over two sweeps
+//
+// thin_qr is one cooperative persistent kernel that follows the reference's
+// column loop: per column k a tail norm (sigma^2 = x_k^2 + sum_{i>k} x_i^2),
+// the Householder vector, the trailing dots tau <v, y_j> (warps split the
+// columns, lanes the rows of a block's fixed row slab) and the rank-1 update,
+// three grid barriers per column.  The rank test, the zeroed flushed columns,
+// Q = H_0 ... H_{n-1} E applied per column in descending k, the sign fix and
+// the rank count are the reference's; its serial dots become fixed-order
+// trees (deterministic, ~1e-16 relative).  Every scalar update is an
+// unfused multiply then add, like the scalar kernel table.
+//
+// project_reduce: S V as an SpMM in CSR row order (spmv_into's order), then
+// the dense products V^T W, V^T F, Cp V, Cv V are plain GEMMs (cuBLAS DGEMM).
+#include <cooperative_groups.h>
+#include <cublas_v2.h>
+
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace cgrp = cooperative_groups;
+
+namespace mgpu
+{
+namespace
+{
+
+constexpr int kQrTB = 256;
+constexpr int kQrMaxCols = 1024;
+
+__device__ __forceinline__ double qr_warp_sum(double v)
+{
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1)
+    v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+  return v;
+}
+
+__device__ double qr_block_sum(double v, double *red)
+{
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = qr_warp_sum(v);
+  if (lane == 0)
+    red[warp] = v;
+  __syncthreads();
+  double t = lane < kQrTB / 32 ? red[lane] : 0.0;
+  t = qr_warp_sum(t);
+  __syncthreads();
+  return t; // every thread
+}
+
+struct QrArgs
+{
+  int64_t m; // rows
+  int n;     // columns
+  double *W; // m x n column-major: A in, Householder vectors (rows >= k of column k) + R above out
+  double *Q; // m x n
+  double *diag, *tau;
+  double tol;
+  double *part; // [G][n + 1]
+};
+
+// Factorisation: dense.cpp:165-190.
+__global__ void __launch_bounds__(kQrTB) qr_factor(QrArgs a)
+{
+  cgrp::grid_group grid = cgrp::this_grid();
+  __shared__ double red[kQrTB / 32];
+  __shared__ double sj[kQrMaxCols];
+  const int64_t m = a.m;
+  const int n = a.n;
+  const int G = gridDim.x, b = blockIdx.x;
+  const int64_t r0 = m * b / G, r1 = m * (b + 1) / G; // this block's row slab
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double *part = a.part + static_cast<int64_t>(b) * (n + 1);
+  for (int k = 0; k < n; ++k)
+  {
+    double *x = a.W + static_cast<int64_t>(k) * m;
+    // ---- tail norm over rows > k
+    double t = 0.0;
+    for (int64_t i = max(r0, static_cast<int64_t>(k) + 1) + threadIdx.x; i < r1; i += kQrTB)
+    {
+      const double xi = x[i];
+      t = __dadd_rn(t, __dmul_rn(xi, xi));
+    }
+    t = qr_block_sum(t, red);
+    if (threadIdx.x == 0)
+      part[0] = t;
+    grid.sync();
+    double tail = 0.0;
+    for (int bb = 0; bb < G; ++bb) // fixed order, identical in every block
+      tail = __dadd_rn(tail, __ldcg(a.part + static_cast<int64_t>(bb) * (n + 1)));
+    const double x0 = __ldcg(x + k);
+    const double sigma = sqrt(__dadd_rn(__dmul_rn(x0, x0), tail));
+    if (sigma <= a.tol)
+    {
+      // rank-deficient direction (dense.cpp:168-174)
+      for (int64_t i = max(r0, static_cast<int64_t>(k)) + threadIdx.x; i < r1; i += kQrTB)
+        x[i] = 0.0;
+      if (b == 0 && threadIdx.x == 0)
+      {
+        a.diag[k] = 0.0;
+        a.tau[k] = 0.0;
+      }
+      grid.sync();
+      continue;
+    }
+    const double alpha = x0 >= 0.0 ? -sigma : sigma;
+    const double v0 = __dsub_rn(x0, alpha);
+    const double vtv = __dadd_rn(__dmul_rn(v0, v0), tail);
+    const double tk = vtv > 0.0 ? 2.0 / vtv : 0.0;
+    if (b == 0 && threadIdx.x == 0)
+    {
+      a.diag[k] = alpha;
+      a.tau[k] = tk;
+    }
+    // ---- dots <v, y_j> for j > k over this block's rows (v_k = v0)
+    for (int j = k + 1 + warp; j < n; j += kQrTB / 32)
+    {
+      const double *y = a.W + static_cast<int64_t>(j) * m;
+      double d = 0.0;
+      for (int64_t i = max(r0, static_cast<int64_t>(k)) + lane; i < r1; i += 32)
+      {
+        const double xi = i == k ? v0 : x[i];
+        d = __dadd_rn(d, __dmul_rn(xi, y[i]));
+      }
+      d = qr_warp_sum(d);
+      if (lane == 0)
+        part[1 + j] = d;
+    }
+    grid.sync();
+    for (int j = k + 1 + threadIdx.x; j < n; j += kQrTB)
+    {
+      double d = 0.0;
+      for (int bb = 0; bb < G; ++bb)
+        d = __dadd_rn(d, __ldcg(a.part + static_cast<int64_t>(bb) * (n + 1) + 1 + j));
+      sj[j] = __dmul_rn(tk, d); // s = tau * dot (dense.cpp:187)
+    }
+    __syncthreads();
+    // ---- y_j -= s_j v over this block's rows (dense.cpp:188)
+    const int64_t lo = max(r0, static_cast<int64_t>(k));
+    const int64_t rows = r1 > lo ? r1 - lo : 0;
+    const int64_t cnt = rows * (n - k - 1);
+    for (int64_t e = threadIdx.x; e < cnt; e += kQrTB)
+    {
+      const int j = k + 1 + static_cast<int>(e / rows);
+      const int64_t i = lo + e % rows;
+      const double xi = i == k ? v0 : x[i];
+      double *y = a.W + static_cast<int64_t>(j) * m;
+      y[i] = __dadd_rn(y[i], __dmul_rn(-sj[j], xi));
+    }
+    __syncthreads();
+    if (k >= r0 && k < r1 && threadIdx.x == 0)
+      x[k] = v0;
+    grid.sync();
+  }
+}
+
+// Q = H_0 ... H_{n-1} E_n (dense.cpp:205-224): column j gets H_j, ..., H_0 in
+// that order; a descending k over all columns j >= k is the same sequence per column.
+__global__ void __launch_bounds__(kQrTB) qr_form_q(QrArgs a)
+{
+  cgrp::grid_group grid = cgrp::this_grid();
+  __shared__ double sj[kQrMaxCols];
+  const int64_t m = a.m;
+  const int n = a.n;
+  const int G = gridDim.x, b = blockIdx.x;
+  const int64_t r0 = m * b / G, r1 = m * (b + 1) / G;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double *part = a.part + static_cast<int64_t>(b) * (n + 1);
+  // Q = E on the kept columns, zero elsewhere
+  for (int64_t e = threadIdx.x; e < (r1 - r0) * n; e += kQrTB)
+  {
+    const int j = static_cast<int>(e / (r1 - r0));
+    const int64_t i = r0 + e % (r1 - r0);
+    a.Q[static_cast<int64_t>(j) * m + i] = (i == j && a.diag[j] != 0.0) ? 1.0 : 0.0;
+  }
+  grid.sync();
+  for (int k = n - 1; k >= 0; --k)
+  {
+    const double tk = a.tau[k];
+    if (tk == 0.0)
+      continue;
+    const double *v = a.W + static_cast<int64_t>(k) * m;
+    const int64_t lo = max(r0, static_cast<int64_t>(k));
+    for (int j = k + warp; j < n; j += kQrTB / 32)
+    {
+      if (a.diag[j] == 0.0)
+        continue;
+      const double *q = a.Q + static_cast<int64_t>(j) * m;
+      double d = 0.0;
+      for (int64_t i = lo + lane; i < r1; i += 32)
+        d = __dadd_rn(d, __dmul_rn(v[i], q[i]));
+      d = qr_warp_sum(d);
+      if (lane == 0)
+        part[1 + j] = d;
+    }
+    grid.sync();
+    for (int j = k + threadIdx.x; j < n; j += kQrTB)
+    {
+      double d = 0.0;
+      if (a.diag[j] != 0.0)
+        for (int bb = 0; bb < G; ++bb)
+          d = __dadd_rn(d, __ldcg(a.part + static_cast<int64_t>(bb) * (n + 1) + 1 + j));
+      sj[j] = __dmul_rn(tk, d);
+    }
+    __syncthreads();
+    const int64_t rows = r1 > lo ? r1 - lo : 0;
+    const int64_t cnt = rows * (n - k);
+    for (int64_t e = threadIdx.x; e < cnt; e += kQrTB)
+    {
+      const int j = k + static_cast<int>(e / rows);
+      if (a.diag[j] == 0.0)
+        continue;
+      const int64_t i = lo + e % rows;
+      double *q = a.Q + static_cast<int64_t>(j) * m;
+      q[i] = __dadd_rn(q[i], __dmul_rn(-sj[j], v[i]));
+    }
+    grid.sync();
+  }
+}
+
+// R (n x n) from W and diag, with the sign fix of dense.cpp:227-239 (rows with a
+// negative diagonal flip, and so do the matching Q columns).
+__global__ void qr_form_r(int64_t m, int n, const double *__restrict__ W, const double *__restrict__ diag,
+                          double *__restrict__ R)
+{
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= static_cast<int64_t>(n) * n)
+    return;
+  const int k = static_cast<int>(e / n), i = static_cast<int>(e % n); // column k, row i
+  double v = i < k ? W[static_cast<int64_t>(k) * m + i] : (i == k ? diag[k] : 0.0);
+  if (i <= k && diag[i] < 0.0)
+    v = -v;
+  R[e] = v;
+}
+
+__global__ void qr_sign_q(int64_t m, int n, const double *__restrict__ diag, double *__restrict__ Q)
+{
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= static_cast<int64_t>(n) * m)
+    return;
+  if (diag[e / m] < 0.0)
+    Q[e] = __dmul_rn(-1.0, Q[e]);
+}
+
+__global__ void square_all(int64_t count, const double *__restrict__ x, double *__restrict__ out)
+{
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t < count)
+    out[t] = __dmul_rn(x[t], x[t]);
+}
+
+__global__ void product_all(int64_t count, const double *__restrict__ x, const double *__restrict__ y,
+                            double *__restrict__ out)
+{
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t < count)
+    out[t] = __dmul_rn(x[t], y[t]);
+}
+
+// X -= g B unless g == 0 (airga.cpp:464-467), g read from device memory.
+__global__ void deflate_axpy(int64_t count, const double *__restrict__ g, const double *__restrict__ B,
+                             double *__restrict__ X)
+{
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const double gv = *g;
+  if (t < count && gv != 0.0)
+    X[t] = __dadd_rn(X[t], __dmul_rn(-gv, B[t]));
+}
+
+// W[:, j] = S V[:, j] (column-major n x r blocks), each row in CSR order (spmv_into).
+__global__ void spmm_block(int64_t n, int64_t r, DCsr S, const double *__restrict__ V, double *__restrict__ W)
+{
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n * r)
+    return;
+  const int64_t j = t / n, i = t - j * n;
+  const double *vj = V + j * n;
+  double acc = 0.0;
+  for (int64_t q = S.rp[i]; q < S.rp[i + 1]; ++q)
+    acc = __dadd_rn(acc, __dmul_rn(S.v[q], vj[S.ci[q]]));
+  W[t] = acc;
+}
+
+cublasHandle_t blas(mgpu_ctx *ctx)
+{
+  if (!ctx->blas)
+  {
+    cublasHandle_t h = nullptr;
+    if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS)
+      throw Error(MGPU_ERR_CUDA, "cublasCreate failed");
+    ctx->blas = h;
+  }
+  cublasHandle_t h = static_cast<cublasHandle_t>(ctx->blas);
+  if (cublasSetStream(h, ctx->stream) != CUBLAS_STATUS_SUCCESS)
+    throw Error(MGPU_ERR_CUDA, "cublasSetStream failed");
+  return h;
+}
+
+void dgemm(mgpu_ctx *ctx, cublasOperation_t ta, cublasOperation_t tb, int64_t M, int64_t N, int64_t K,
+           const double *A, int64_t lda, const double *B, int64_t ldb, double *C, int64_t ldc)
+{
+  if (M == 0 || N == 0)
+    return;
+  const double one = 1.0, zero = 0.0;
+  if (cublasDgemm_64(blas(ctx), ta, tb, M, N, K, &one, A, lda, B, ldb, &zero, C, ldc) != CUBLAS_STATUS_SUCCESS)
+    throw Error(MGPU_ERR_CUDA, "cublasDgemm failed");
+  count_launch(ctx);
+}
+
+// Device staging of a `where` buffer: device pointers pass through, host ones are copied.
+struct Staged
+{
+  DBuf buf;
+  const double *ptr = nullptr;
+  Staged(mgpu_ctx *ctx, const double *src, int64_t count, mgpu_memkind where)
+  {
+    if (where == MGPU_DEVICE || count == 0)
+    {
+      ptr = src;
+      return;
+    }
+    buf = DBuf(sizeof(double) * static_cast<size_t>(count), ctx->stream);
+    MG_CUDA(cudaMemcpyAsync(buf.ptr, src, sizeof(double) * count, cudaMemcpyHostToDevice, ctx->stream));
+    ptr = buf.as<double>();
+  }
+};
+
+void deliver(mgpu_ctx *ctx, double *dst, const double *dev, int64_t count, mgpu_memkind where)
+{
+  if (count == 0)
+    return;
+  MG_CUDA(cudaMemcpyAsync(dst, dev, sizeof(double) * count,
+                          where == MGPU_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, ctx->stream));
+}
+
+} // namespace
+} // namespace mgpu
+
+using namespace mgpu;
+
+extern "C" {
+
+int mgpu_thin_qr(mgpu_ctx *ctx, int64_t rows, int64_t cols, const double *A, double rank_tol, double *Q, double *R,
+                 int64_t *rank, mgpu_memkind where)
+{
+  return guard(ctx, [&] {
+    MG_ARG(A && Q && R && rank && rows >= 0 && cols >= 0, "thin_qr: null argument");
+    MG_ARG(where == MGPU_HOST || where == MGPU_DEVICE, "thin_qr: bad memory kind");
+    MG_ARG(rows >= cols, "thin_qr: requires nrows >= ncols"); // dense.cpp:155-158
+    if (cols > kQrMaxCols)
+      throw Error(MGPU_ERR_UNSUPPORTED,
+                  "thin_qr: at most " + std::to_string(kQrMaxCols) + " columns on the device (got " +
+                      std::to_string(cols) + ")");
+    cudaStream_t s = ctx->stream;
+    const int64_t total = rows * cols;
+    const size_t bytes = sizeof(double) * static_cast<size_t>(total > 0 ? total : 1);
+    DBuf W(bytes, s), Qd(bytes, s), Rd(sizeof(double) * static_cast<size_t>(cols > 0 ? cols * cols : 1), s);
+    DBuf diag(sizeof(double) * (cols > 0 ? cols : 1), s), tau(sizeof(double) * (cols > 0 ? cols : 1), s);
+    MG_CUDA(cudaMemcpyAsync(W.ptr, A, sizeof(double) * total,
+                            where == MGPU_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
+    int64_t rk = 0;
+    if (cols > 0)
+    {
+      // tol = rank_tol * ||A||_F (dense.cpp:162-163)
+      DBuf sq(bytes, s), nrm(sizeof(double), s);
+      square_all<<<blocks_for(total), kThreads, 0, s>>>(total, W.as<double>(), sq.as<double>());
+      check_launch(ctx, "square_all");
+      det_sum(ctx, sq.as<double>(), total, nrm.as<double>());
+      double an2 = 0.0;
+      MG_CUDA(cudaMemcpyAsync(&an2, nrm.ptr, sizeof(double), cudaMemcpyDeviceToHost, s));
+      MG_CUDA(cudaStreamSynchronize(s));
+      const double anorm = std::sqrt(an2);
+      const int G = ctx->num_sms;
+      DBuf part(sizeof(double) * static_cast<size_t>(G) * (cols + 1), s);
+      QrArgs a{rows, static_cast<int>(cols), W.as<double>(), Qd.as<double>(), diag.as<double>(), tau.as<double>(),
+               rank_tol * (anorm > 0.0 ? anorm : 1.0), part.as<double>()};
+      void *args[] = {&a};
+      MG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void *>(qr_factor), dim3(static_cast<unsigned>(G)),
+                                          dim3(kQrTB), args, 0, s));
+      check_launch(ctx, "qr_factor");
+      MG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void *>(qr_form_q), dim3(static_cast<unsigned>(G)),
+                                          dim3(kQrTB), args, 0, s));
+      check_launch(ctx, "qr_form_q");
+      qr_form_r<<<blocks_for(cols * cols), kThreads, 0, s>>>(rows, static_cast<int>(cols), W.as<double>(),
+                                                             diag.as<double>(), Rd.as<double>());
+      check_launch(ctx, "qr_form_r");
+      qr_sign_q<<<blocks_for(total), kThreads, 0, s>>>(rows, static_cast<int>(cols), diag.as<double>(),
+                                                       Qd.as<double>());
+      check_launch(ctx, "qr_sign_q");
+      std::vector<double> hd(static_cast<size_t>(cols));
+      MG_CUDA(cudaMemcpyAsync(hd.data(), diag.ptr, sizeof(double) * cols, cudaMemcpyDeviceToHost, s));
+      MG_CUDA(cudaStreamSynchronize(s));
+      for (double d : hd)
+        rk += d != 0.0; // |R_kk| > 0 after the sign fix (dense.cpp:236-239)
+    }
+    deliver(ctx, Q, Qd.as<double>(), total, where);
+    deliver(ctx, R, Rd.as<double>(), cols * cols, where);
+    MG_CUDA(cudaStreamSynchronize(s));
+    *rank = rk;
+  });
+}
+
+int mgpu_project_reduce(mgpu_ctx *ctx, const mgpu_csr *M, const mgpu_csr *D, const mgpu_csr *K, int64_t r,
+                        const double *V, int64_t m, const double *F, int64_t q, const double *Cp, const double *Cv,
+                        double *Mh, double *Dh, double *Kh, double *Fh, double *Cph, double *Cvh, mgpu_memkind where)
+{
+  return guard(ctx, [&] {
+    MG_ARG(M && D && K && V && Mh && Dh && Kh && r >= 0 && m >= 0 && q >= 0, "project_reduce: null argument");
+    MG_ARG(where == MGPU_HOST || where == MGPU_DEVICE, "project_reduce: bad memory kind");
+    MG_ARG(m == 0 || (F && Fh), "project_reduce: F / Fh missing");
+    MG_ARG(q == 0 || (Cp && Cv && Cph && Cvh), "project_reduce: Cp / Cv missing");
+    const int64_t n = M->nrows;
+    for (const mgpu_csr *S : {M, D, K})
+      MG_ARG(S->nrows == n && S->ncols == n, "project_reduce: operator shape mismatch");
+    cudaStream_t s = ctx->stream;
+    Staged dV(ctx, V, n * r, where), dF(ctx, F, n * m, where), dCp(ctx, Cp, q * n, where), dCv(ctx, Cv, q * n, where);
+    DBuf W(sizeof(double) * static_cast<size_t>(n * r > 0 ? n * r : 1), s);
+    DBuf H(sizeof(double) * static_cast<size_t>(r * r > 0 ? r * r : 1), s);
+    double *outs[3] = {Mh, Dh, Kh};
+    const mgpu_csr *ops[3] = {M, D, K};
+    for (int o = 0; o < 3; ++o) // airga.cpp:489-491: matmul_tn(V, sparse_times_dense(S, V))
+    {
+      if (n * r > 0)
+      {
+        spmm_block<<<blocks_for(n * r), kThreads, 0, s>>>(n, r, ops[o]->view(), dV.ptr, W.as<double>());
+        check_launch(ctx, "spmm_block");
+      }
+      if (r > 0 && n == 0)
+        MG_CUDA(cudaMemsetAsync(H.ptr, 0, sizeof(double) * r * r, s));
+      else
+        dgemm(ctx, CUBLAS_OP_T, CUBLAS_OP_N, r, r, n, dV.ptr, n, W.as<double>(), n, H.as<double>(), r);
+      deliver(ctx, outs[o], H.as<double>(), r * r, where);
+      MG_CUDA(cudaStreamSynchronize(s)); // H and W are reused by the next operator
+    }
+    if (m > 0) // airga.cpp:492: matmul_tn(V, F)
+    {
+      DBuf T(sizeof(double) * static_cast<size_t>(r * m > 0 ? r * m : 1), s);
+      dgemm(ctx, CUBLAS_OP_T, CUBLAS_OP_N, r, m, n, dV.ptr, n, dF.ptr, n, T.as<double>(), r);
+      deliver(ctx, Fh, T.as<double>(), r * m, where);
+      MG_CUDA(cudaStreamSynchronize(s));
+    }
+    if (q > 0) // airga.cpp:493-494: matmul(Cp, V), matmul(Cv, V)
+    {
+      DBuf T(sizeof(double) * static_cast<size_t>(q * r > 0 ? q * r : 1), s);
+      dgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, q, r, n, dCp.ptr, q, dV.ptr, n, T.as<double>(), q);
+      deliver(ctx, Cph, T.as<double>(), q * r, where);
+      MG_CUDA(cudaStreamSynchronize(s));
+      dgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, q, r, n, dCv.ptr, q, dV.ptr, n, T.as<double>(), q);
+      deliver(ctx, Cvh, T.as<double>(), q * r, where);
+    }
+    MG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int mgpu_arnoldi_deflate(mgpu_ctx *ctx, int64_t len, double *X, int nblocks, const double *const *blocks,
+                         double *gammas, mgpu_memkind where)
+{
+  return guard(ctx, [&] {
+    MG_ARG(X && nblocks >= 0 && (nblocks == 0 || (blocks && gammas)) && len >= 0, "arnoldi_deflate: null argument");
+    MG_ARG(where == MGPU_HOST || where == MGPU_DEVICE, "arnoldi_deflate: bad memory kind");
+    cudaStream_t s = ctx->stream;
+    const size_t bytes = sizeof(double) * static_cast<size_t>(len > 0 ? len : 1);
+    DBuf Xd(bytes, s), prod(bytes, s), g(sizeof(double) * (2 * nblocks > 0 ? 2 * nblocks : 1), s);
+    MG_CUDA(cudaMemcpyAsync(Xd.ptr, X, sizeof(double) * len,
+                            where == MGPU_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
+    std::vector<Staged> B;
+    B.reserve(static_cast<size_t>(nblocks));
+    for (int t = 0; t < nblocks; ++t)
+      B.emplace_back(ctx, blocks[t], len, where);
+    for (int sweep = 0; sweep < 2; ++sweep) // airga.cpp:459-470
+      for (int t = 0; t < nblocks; ++t)
+      {
+        double *gd = g.as<double>() + sweep * nblocks + t;
+        if (len > 0)
+        {
+          product_all<<<blocks_for(len), kThreads, 0, s>>>(len, B[t].ptr, Xd.as<double>(), prod.as<double>());
+          check_launch(ctx, "product_all");
+          det_sum(ctx, prod.as<double>(), len, gd); // trace_inner(B_t, X)
+          deflate_axpy<<<blocks_for(len), kThreads, 0, s>>>(len, gd, B[t].ptr, Xd.as<double>());
+          check_launch(ctx, "deflate_axpy");
+        }
+        else
+          MG_CUDA(cudaMemsetAsync(gd, 0, sizeof(double), s));
+      }
+    std::vector<double> hg(static_cast<size_t>(2 * nblocks));
+    if (nblocks > 0)
+      MG_CUDA(cudaMemcpyAsync(hg.data(), g.ptr, sizeof(double) * 2 * nblocks, cudaMemcpyDeviceToHost, s));
+    MG_CUDA(cudaMemcpyAsync(X, Xd.ptr, sizeof(double) * len,
+                            where == MGPU_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
+    MG_CUDA(cudaStreamSynchronize(s));
+    for (int t = 0; t < nblocks; ++t)
+      gammas[t] = (0.0 + hg[static_cast<size_t>(t)]) + hg[static_cast<size_t>(nblocks + t)]; // gammas[t] += g
+  });
+}
+
+} // extern "C"

@@ -281,6 +281,63 @@ BlockSolveResult block_solve(Device &dev, const SparseMatrix &A, const Precondit
   return solve_points(dev.ctx(), {dA.get()}, ch, static_cast<int>(ch.size()), B, rtol, maxit)[0];
 }
 
+QrResult thin_qr(Device &dev, const DenseMatrix &A, double rank_tol)
+{
+  if (A.nrows < A.ncols)
+    throw ArgumentError("thin_qr: requires nrows >= ncols"); // dense.cpp:155-158
+  QrResult out;
+  out.Q = DenseMatrix(A.nrows, A.ncols);
+  out.R = DenseMatrix(A.ncols, A.ncols);
+  int64_t rank = 0;
+  check(dev.ctx(), mgpu_thin_qr(dev.ctx(), A.nrows, A.ncols, A.values.data(), rank_tol, out.Q.values.data(),
+                                out.R.values.data(), &rank, MGPU_HOST));
+  out.rank = rank;
+  return out;
+}
+
+ReducedSystem project_reduce(Device &dev, const SecondOrderSystem &sys, const OrthonormalBasis &basis)
+{
+  const DenseMatrix &V = basis.assembled;
+  const int64_t n = sys.M.nrows, r = V.ncols, m = sys.F.ncols, q = sys.Cp.nrows;
+  if (V.nrows != n)
+    throw ArgumentError("project_reduce: basis has the wrong row count");
+  const DeviceMatrix dM(dev, sys.M), dD(dev, sys.D), dK(dev, sys.K);
+  ReducedSystem rs;
+  rs.Mh = DenseMatrix(r, r);
+  rs.Dh = DenseMatrix(r, r);
+  rs.Kh = DenseMatrix(r, r);
+  rs.Fh = DenseMatrix(r, m);
+  rs.Cph = DenseMatrix(q, r);
+  rs.Cvh = DenseMatrix(q, r);
+  check(dev.ctx(), mgpu_project_reduce(dev.ctx(), dM.get(), dD.get(), dK.get(), r, V.values.data(), m,
+                                       m ? sys.F.values.data() : nullptr, q, q ? sys.Cp.values.data() : nullptr,
+                                       q ? sys.Cv.values.data() : nullptr, rs.Mh.values.data(), rs.Dh.values.data(),
+                                       rs.Kh.values.data(), m ? rs.Fh.values.data() : nullptr,
+                                       q ? rs.Cph.values.data() : nullptr, q ? rs.Cvh.values.data() : nullptr,
+                                       MGPU_HOST));
+  rs.basis = V; // airga.cpp:495-499
+  rs.r = r;
+  rs.alpha = sys.alpha;
+  rs.beta = sys.beta;
+  return rs;
+}
+
+std::vector<double> arnoldi_deflate(Device &dev, DenseMatrix &X, std::span<const DenseMatrix> basis_blocks)
+{
+  std::vector<const double *> ptrs;
+  for (const DenseMatrix &b : basis_blocks)
+  {
+    if (b.nrows != X.nrows || b.ncols != X.ncols)
+      throw ArgumentError("trace_inner(dense): shape mismatch"); // dense.cpp:40-43 via trace_inner
+    ptrs.push_back(b.values.data());
+  }
+  std::vector<double> gammas(basis_blocks.size(), 0.0);
+  check(dev.ctx(), mgpu_arnoldi_deflate(dev.ctx(), static_cast<int64_t>(X.values.size()), X.values.data(),
+                                        static_cast<int>(ptrs.size()), ptrs.empty() ? nullptr : ptrs.data(),
+                                        gammas.empty() ? nullptr : gammas.data(), MGPU_HOST));
+  return gammas;
+}
+
 } // namespace cuda
 
 // ------------------------------------------------------------------ backend

@@ -19,6 +19,7 @@
 //       chain_apply                   (spai.hpp:77-79)
 //       chain_quality                 (spai.hpp:81-85)
 //       pcg_solve / block_solve       (krylov.hpp:41-56)
+//       thin_qr / project_reduce / arnoldi_deflate   (dense.hpp:69, airga.hpp:176-183)
 //   The reference's pcg_solve takes LinearOperators wrapping std::function;
 //   arbitrary host callables cannot run on the device, so the drop-ins take
 //   the SparseMatrix and PreconditionerChain that CgBackend::solve wraps
@@ -97,6 +98,11 @@ SolveReport pcg_solve(Device &dev, const SparseMatrix &A, const PreconditionerCh
                       double rtol, std::int64_t maxit);
 BlockSolveResult block_solve(Device &dev, const SparseMatrix &A, const PreconditionerChain &P, const DenseMatrix &B,
                              double rtol, std::int64_t maxit);
+
+// Global Arnoldi + projection
+QrResult thin_qr(Device &dev, const DenseMatrix &A, double rank_tol = 1e-12);                 // dense.hpp:69
+ReducedSystem project_reduce(Device &dev, const SecondOrderSystem &sys, const OrthonormalBasis &basis); // airga.hpp:183
+std::vector<double> arnoldi_deflate(Device &dev, DenseMatrix &X, std::span<const DenseMatrix> basis_blocks); // airga.hpp:176
 
 } // namespace cuda
 

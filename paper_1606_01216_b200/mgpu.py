@@ -30,7 +30,8 @@ EXPORTED = [
     "mgpu_csr_download", "mgpu_csr_device_view", "mgpu_csr_free", "mgpu_sp_add_scaled", "mgpu_shifted_operators",
     "mgpu_transpose", "mgpu_trace", "mgpu_trace_inner", "mgpu_spmv", "mgpu_chain_apply", "mgpu_chain_quality", "mgpu_spai_build",
     "mgpu_spai_update", "mgpu_spai_ls", "mgpu_spai_ls_batched", "mgpu_spgemm", "mgpu_cg_solve",
-    "mgpu_model_chain", "mgpu_model_hermite", "mgpu_host_free",
+    "mgpu_model_chain", "mgpu_model_hermite", "mgpu_host_free", "mgpu_thin_qr", "mgpu_project_reduce",
+    "mgpu_arnoldi_deflate",
 ]
 
 
@@ -128,6 +129,9 @@ def lib():
         L.mgpu_spmv.argtypes = [vp, vp, vp, vp]
         L.mgpu_chain_apply.argtypes = [vp, C.c_int, vp, vp, vp, C.c_int]
         L.mgpu_chain_quality.argtypes = [vp, C.c_int, vp, vp, C.c_int64, C.c_uint64, C.POINTER(C.c_double)]
+        L.mgpu_thin_qr.argtypes = [vp, i64, i64, vp, dbl, vp, vp, C.POINTER(C.c_int64), C.c_int]
+        L.mgpu_project_reduce.argtypes = [vp, vp, vp, vp, i64, vp, i64, vp, i64, vp, vp] + [vp] * 6 + [C.c_int]
+        L.mgpu_arnoldi_deflate.argtypes = [vp, i64, vp, C.c_int, vp, vp, C.c_int]
         L.mgpu_spai_build.argtypes = [vp, vp, dbl, i64, C.c_int, C.POINTER(vp), vp]
         L.mgpu_spai_update.argtypes = [vp, vp, vp, dbl, i64, C.c_int, C.POINTER(vp), vp]
         L.mgpu_spai_ls.argtypes = [vp, vp, vp, C.c_int, C.POINTER(vp)]
@@ -385,6 +389,63 @@ def chain_quality(chain: Sequence, K, samples: int, seed: int = 42, ctx=None) ->
     ctx.check(lib().mgpu_chain_quality(ctx.handle, len(dev), _handles(dev) if dev else None, dK.handle,
                                        int(samples), int(seed), C.byref(out)))
     return out.value
+
+
+# ---------------------------------------------------------------- global Arnoldi + projection
+def _fortran(a, rows=None):
+    a = np.asfortranarray(np.asarray(a, np.float64))
+    if a.ndim == 1:
+        a = a.reshape(-1, 1, order="F")
+    return a
+
+
+def thin_qr(A, rank_tol: float = 1e-12, ctx=None):
+    """dense.cpp:153-246 on the device: returns (Q, R, rank) like the reference's QrResult."""
+    ctx = ctx or default_context()
+    A = _fortran(A)
+    rows, cols = A.shape
+    Q = np.zeros((rows, cols), order="F")
+    R = np.zeros((cols, cols), order="F")
+    rank = C.c_int64()
+    ctx.check(lib().mgpu_thin_qr(ctx.handle, rows, cols, _ptr(A), rank_tol, _ptr(Q), _ptr(R), C.byref(rank),
+                                 MGPU_HOST))
+    return Q, R, rank.value
+
+
+def project_reduce(M, D, K, V, F=None, Cp=None, Cv=None, ctx=None) -> dict:
+    """airga.cpp:485-500 on the device: Mh, Dh, Kh = V^T S V, Fh = V^T F, Cph / Cvh = C V."""
+    ctx = ctx or default_context()
+    dM, dD, dK = (_dev(x, ctx) for x in (M, D, K))
+    V = _fortran(V)
+    n, r = V.shape
+    Fm = _fortran(F) if F is not None else np.zeros((n, 0), order="F")
+    m = Fm.shape[1]
+    q = 0 if Cp is None else _fortran(Cp).shape[0]
+    Cpm = _fortran(Cp) if q else np.zeros((0, n), order="F")
+    Cvm = _fortran(Cv) if q else np.zeros((0, n), order="F")
+    out = {k: np.zeros(shape, order="F") for k, shape in
+           (("Mh", (r, r)), ("Dh", (r, r)), ("Kh", (r, r)), ("Fh", (r, m)), ("Cph", (q, r)), ("Cvh", (q, r)))}
+    ctx.check(lib().mgpu_project_reduce(ctx.handle, dM.handle, dD.handle, dK.handle, r, _ptr(V), m,
+                                        _ptr(Fm) if m else None, q, _ptr(Cpm) if q else None,
+                                        _ptr(Cvm) if q else None, _ptr(out["Mh"]), _ptr(out["Dh"]), _ptr(out["Kh"]),
+                                        _ptr(out["Fh"]) if m else None, _ptr(out["Cph"]) if q else None,
+                                        _ptr(out["Cvh"]) if q else None, MGPU_HOST))
+    return out
+
+
+def arnoldi_deflate(X, blocks: Sequence, ctx=None):
+    """airga.cpp:456-473 on the device: returns (deflated X, gammas)."""
+    ctx = ctx or default_context()
+    X = _fortran(X).copy(order="F")
+    bl = [_fortran(b) for b in blocks]
+    for b in bl:
+        if b.shape != X.shape:
+            raise ArgumentError("arnoldi_deflate: block shape mismatch")
+    ptrs = (C.c_void_p * max(len(bl), 1))(*[b.ctypes.data for b in bl])
+    g = np.zeros(len(bl))
+    ctx.check(lib().mgpu_arnoldi_deflate(ctx.handle, X.size, _ptr(X), len(bl), ptrs if bl else None,
+                                         _ptr(g) if bl else None, MGPU_HOST))
+    return X, g
 
 
 # ---------------------------------------------------------------- SPAI

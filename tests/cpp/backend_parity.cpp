@@ -153,6 +153,49 @@ int main()
       ra.converged != rb.converged || ra.relres_history.size() != static_cast<std::size_t>(ra.iterations) ||
       rb.relres_history.size() != static_cast<std::size_t>(rb.iterations))
     ++failures;
+  // global Arnoldi + projection: thin_qr / arnoldi_deflate / project_reduce on solve blocks
+  DenseMatrix Vt(2000, 6);
+  for (int c = 0; c < 6; ++c)
+  {
+    const SparseMatrix Ac = shifted_operator(sys, 5.0 + 20.0 * c);
+    std::vector<double> rhs(2000, 0.0);
+    rhs[static_cast<std::size_t>(c * 300)] = 1.0;
+    const SolveReport sr = pcg_solve(LinearOperator::from_sparse(Ac), LinearOperator::identity(2000), rhs, 1e-12, 20000);
+    std::copy(sr.solution.begin(), sr.solution.end(), Vt.col(c));
+  }
+  const QrResult qa = thin_qr(Vt), qb = cuda::thin_qr(dev, Vt);
+  auto rel_dense = [](const DenseMatrix &a, const DenseMatrix &b) {
+    double num = 0.0, den = 0.0;
+    for (std::size_t k = 0; k < a.values.size(); ++k)
+    {
+      num += (a.values[k] - b.values[k]) * (a.values[k] - b.values[k]);
+      den += b.values[k] * b.values[k];
+    }
+    return std::sqrt(num / (den > 0.0 ? den : 1.0));
+  };
+  double dproj = std::max(rel_dense(qb.Q, qa.Q), rel_dense(qb.R, qa.R));
+  if (qa.rank != qb.rank)
+    ++failures;
+  DenseMatrix Xd(2000, 6);
+  for (std::size_t k = 0; k < Xd.values.size(); ++k)
+    Xd.values[k] = std::sin(0.001 * static_cast<double>(k)) + 0.5 * std::cos(0.37 * static_cast<double>(k));
+  DenseMatrix Xg = Xd;
+  std::vector<DenseMatrix> blocks = {qa.Q};
+  const auto ga = arnoldi_deflate(Xd, blocks), gb = cuda::arnoldi_deflate(dev, Xg, blocks);
+  dproj = std::max({dproj, rel_dense(Xg, Xd), std::fabs(ga[0] - gb[0]) / std::fabs(ga[0])});
+  SecondOrderSystem sysp = sys;
+  sysp.F = DenseMatrix(2000, 1);
+  sysp.F.at(0, 0) = 1.0;
+  sysp.Cp = DenseMatrix(1, 2000);
+  sysp.Cv = DenseMatrix(1, 2000);
+  sysp.Cp.at(0, 1999) = 1.0;
+  OrthonormalBasis ob;
+  ob.assembled = qa.Q;
+  const ReducedSystem ra_ = project_reduce(sysp, ob), rb_ = cuda::project_reduce(dev, sysp, ob);
+  dproj = std::max({dproj, rel_dense(rb_.Mh, ra_.Mh), rel_dense(rb_.Dh, ra_.Dh), rel_dense(rb_.Kh, ra_.Kh),
+                    rel_dense(rb_.Fh, ra_.Fh), rel_dense(rb_.Cph, ra_.Cph)});
+  if (!(dproj <= 1e-12))
+    ++failures;
   // exception parity: MR-SPAI stagnation on the BASELINE Hermite-like stiff case, CG breakdown
   long stag_ref = -1, stag_gpu = -1, bd_ref = -1, bd_gpu = -1;
   ModelSpec stiff = spec;
@@ -169,8 +212,8 @@ int main()
   if (stag_ref != stag_gpu || stag_ref < 0 || bd_ref != bd_gpu || bd_ref < 0)
     ++failures;
   std::printf("{\"solves\": %d, \"max_rel_x\": %.3e, \"max_iter_diff\": %ld, \"spai_rel\": %.3e, "
-              "\"chain_apply_abs\": %.3e, \"chain_quality_rel\": %.3e, \"pcg_rel\": %.3e, \"stagnation_col\": [%ld, %ld], "
+              "\"chain_apply_abs\": %.3e, \"chain_quality_rel\": %.3e, \"projection_rel\": %.3e, \"pcg_rel\": %.3e, \"stagnation_col\": [%ld, %ld], "
               "\"breakdown_it\": [%ld, %ld], \"failures\": %d}\n",
-              solves, worst_x, worst_it, dspai, dchain, dq, dpcg, stag_ref, stag_gpu, bd_ref, bd_gpu, failures);
+              solves, worst_x, worst_it, dspai, dchain, dq, dproj, dpcg, stag_ref, stag_gpu, bd_ref, bd_gpu, failures);
   return failures == 0 ? 0 : 1;
 }
