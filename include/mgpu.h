@@ -250,6 +250,16 @@ int mgpu_project_reduce(mgpu_ctx *ctx, const mgpu_csr *M, const mgpu_csr *D, con
                         const double *V, int64_t m, const double *F, int64_t q, const double *Cp, const double *Cv,
                         double *Mh, double *Dh, double *Kh, double *Fh, double *Cph, double *Cvh, mgpu_memkind where);
 
+/* Row-slab form of mgpu_project_reduce for a row-distributed basis: M, D, K are the slab's
+ * p rows (global column indices), Vext holds global basis rows [ext0, ext0 + next) (the slab's rows
+ * [row0, row0 + p) plus a halo covering every column the slab touches), F the slab's p x m rows and
+ * Cp / Cv its q x p columns.  Outputs are this slab's partial sums (an all-reduce over slabs gives
+ * mgpu_project_reduce's result). */
+int mgpu_project_reduce_slab(mgpu_ctx *ctx, const mgpu_csr *M, const mgpu_csr *D, const mgpu_csr *K, int64_t row0,
+                             int64_t ext0, int64_t next, int64_t r, const double *Vext, int64_t m, const double *F,
+                             int64_t q, const double *Cp, const double *Cv, double *Mh, double *Dh, double *Kh,
+                             double *Fh, double *Cph, double *Cvh, mgpu_memkind where);
+
 /* airga.cpp:456-473 arnoldi_deflate: two sweeps of X -= <B_t, X> B_t over the nblocks basis blocks
  * (each `len` values, the same shape as X); gammas[t] = sum of both sweeps' coefficients.
  * X and blocks in `where` memory, gammas on the host. */

@@ -275,17 +275,20 @@ __global__ void deflate_axpy(int64_t count, const double *__restrict__ g, const 
     X[t] = __dadd_rn(X[t], __dmul_rn(-gv, B[t]));
 }
 
-// W[:, j] = S V[:, j] (column-major n x r blocks), each row in CSR order (spmv_into).
-__global__ void spmm_block(int64_t n, int64_t r, DCsr S, const double *__restrict__ V, double *__restrict__ W)
+// W[:, j] = S X[:, j] for a row slab S (p rows, global column indices) and X
+// holding global rows [x0, x0 + ldx): column-major p x r result, each row in
+// CSR order (spmv_into).
+__global__ void spmm_block(int64_t p, int64_t r, DCsr S, const double *__restrict__ X, int64_t x0, int64_t ldx,
+                           double *__restrict__ W)
 {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= n * r)
+  if (t >= p * r)
     return;
-  const int64_t j = t / n, i = t - j * n;
-  const double *vj = V + j * n;
+  const int64_t j = t / p, i = t - j * p;
+  const double *xj = X + j * ldx - x0;
   double acc = 0.0;
   for (int64_t q = S.rp[i]; q < S.rp[i + 1]; ++q)
-    acc = __dadd_rn(acc, __dmul_rn(S.v[q], vj[S.ci[q]]));
+    acc = __dadd_rn(acc, __dmul_rn(S.v[q], xj[S.ci[q]]));
   W[t] = acc;
 }
 
@@ -408,56 +411,84 @@ int mgpu_thin_qr(mgpu_ctx *ctx, int64_t rows, int64_t cols, const double *A, dou
   });
 }
 
-int mgpu_project_reduce(mgpu_ctx *ctx, const mgpu_csr *M, const mgpu_csr *D, const mgpu_csr *K, int64_t r,
-                        const double *V, int64_t m, const double *F, int64_t q, const double *Cp, const double *Cv,
-                        double *Mh, double *Dh, double *Kh, double *Fh, double *Cph, double *Cvh, mgpu_memkind where)
+int mgpu_project_reduce_slab(mgpu_ctx *ctx, const mgpu_csr *M, const mgpu_csr *D, const mgpu_csr *K, int64_t row0,
+                             int64_t ext0, int64_t next, int64_t r, const double *Vext, int64_t m, const double *F,
+                             int64_t q, const double *Cp, const double *Cv, double *Mh, double *Dh, double *Kh,
+                             double *Fh, double *Cph, double *Cvh, mgpu_memkind where)
 {
   return guard(ctx, [&] {
-    MG_ARG(M && D && K && V && Mh && Dh && Kh && r >= 0 && m >= 0 && q >= 0, "project_reduce: null argument");
+    MG_ARG(M && D && K && Vext && Mh && Dh && Kh && r >= 0 && m >= 0 && q >= 0 && next >= 0,
+           "project_reduce: null argument");
     MG_ARG(where == MGPU_HOST || where == MGPU_DEVICE, "project_reduce: bad memory kind");
     MG_ARG(m == 0 || (F && Fh), "project_reduce: F / Fh missing");
     MG_ARG(q == 0 || (Cp && Cv && Cph && Cvh), "project_reduce: Cp / Cv missing");
-    const int64_t n = M->nrows;
+    const int64_t p = M->nrows;
     for (const mgpu_csr *S : {M, D, K})
-      MG_ARG(S->nrows == n && S->ncols == n, "project_reduce: operator shape mismatch");
+      MG_ARG(S->nrows == p, "project_reduce: operator slab shape mismatch");
+    MG_ARG(row0 >= ext0 && row0 + p <= ext0 + next, "project_reduce: slab rows outside the extended basis");
+    // precondition (mgpu.h): every column the slab touches lies in [ext0, ext0 + next)
     cudaStream_t s = ctx->stream;
-    Staged dV(ctx, V, n * r, where), dF(ctx, F, n * m, where), dCp(ctx, Cp, q * n, where), dCv(ctx, Cv, q * n, where);
-    DBuf W(sizeof(double) * static_cast<size_t>(n * r > 0 ? n * r : 1), s);
+    Staged dV(ctx, Vext, next * r, where), dF(ctx, F, p * m, where), dCp(ctx, Cp, q * p, where),
+        dCv(ctx, Cv, q * p, where);
+    const double *Y = dV.ptr + (row0 - ext0); // this slab's own rows of the basis (ld = next)
+    DBuf W(sizeof(double) * static_cast<size_t>(p * r > 0 ? p * r : 1), s);
     DBuf H(sizeof(double) * static_cast<size_t>(r * r > 0 ? r * r : 1), s);
     double *outs[3] = {Mh, Dh, Kh};
     const mgpu_csr *ops[3] = {M, D, K};
     for (int o = 0; o < 3; ++o) // airga.cpp:489-491: matmul_tn(V, sparse_times_dense(S, V))
     {
-      if (n * r > 0)
+      if (p * r > 0)
       {
-        spmm_block<<<blocks_for(n * r), kThreads, 0, s>>>(n, r, ops[o]->view(), dV.ptr, W.as<double>());
+        spmm_block<<<blocks_for(p * r), kThreads, 0, s>>>(p, r, ops[o]->view(), dV.ptr, ext0, next, W.as<double>());
         check_launch(ctx, "spmm_block");
       }
-      if (r > 0 && n == 0)
+      if (r > 0 && p == 0)
         MG_CUDA(cudaMemsetAsync(H.ptr, 0, sizeof(double) * r * r, s));
       else
-        dgemm(ctx, CUBLAS_OP_T, CUBLAS_OP_N, r, r, n, dV.ptr, n, W.as<double>(), n, H.as<double>(), r);
+        dgemm(ctx, CUBLAS_OP_T, CUBLAS_OP_N, r, r, p, Y, next, W.as<double>(), p, H.as<double>(), r);
       deliver(ctx, outs[o], H.as<double>(), r * r, where);
       MG_CUDA(cudaStreamSynchronize(s)); // H and W are reused by the next operator
     }
     if (m > 0) // airga.cpp:492: matmul_tn(V, F)
     {
       DBuf T(sizeof(double) * static_cast<size_t>(r * m > 0 ? r * m : 1), s);
-      dgemm(ctx, CUBLAS_OP_T, CUBLAS_OP_N, r, m, n, dV.ptr, n, dF.ptr, n, T.as<double>(), r);
+      if (p == 0)
+        MG_CUDA(cudaMemsetAsync(T.ptr, 0, sizeof(double) * r * m, s));
+      else
+        dgemm(ctx, CUBLAS_OP_T, CUBLAS_OP_N, r, m, p, Y, next, dF.ptr, p, T.as<double>(), r);
       deliver(ctx, Fh, T.as<double>(), r * m, where);
       MG_CUDA(cudaStreamSynchronize(s));
     }
     if (q > 0) // airga.cpp:493-494: matmul(Cp, V), matmul(Cv, V)
     {
       DBuf T(sizeof(double) * static_cast<size_t>(q * r > 0 ? q * r : 1), s);
-      dgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, q, r, n, dCp.ptr, q, dV.ptr, n, T.as<double>(), q);
-      deliver(ctx, Cph, T.as<double>(), q * r, where);
-      MG_CUDA(cudaStreamSynchronize(s));
-      dgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, q, r, n, dCv.ptr, q, dV.ptr, n, T.as<double>(), q);
-      deliver(ctx, Cvh, T.as<double>(), q * r, where);
+      for (int o = 0; o < 2; ++o)
+      {
+        if (p == 0)
+          MG_CUDA(cudaMemsetAsync(T.ptr, 0, sizeof(double) * q * r, s));
+        else
+          dgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, q, r, p, o == 0 ? dCp.ptr : dCv.ptr, q, Y, next, T.as<double>(), q);
+        deliver(ctx, o == 0 ? Cph : Cvh, T.as<double>(), q * r, where);
+        MG_CUDA(cudaStreamSynchronize(s));
+      }
     }
     MG_CUDA(cudaStreamSynchronize(s));
   });
+}
+
+int mgpu_project_reduce(mgpu_ctx *ctx, const mgpu_csr *M, const mgpu_csr *D, const mgpu_csr *K, int64_t r,
+                        const double *V, int64_t m, const double *F, int64_t q, const double *Cp, const double *Cv,
+                        double *Mh, double *Dh, double *Kh, double *Fh, double *Cph, double *Cvh, mgpu_memkind where)
+{
+  if (M && D && K)
+  {
+    const int64_t n = M->nrows;
+    for (const mgpu_csr *S : {M, D, K})
+      if (S->nrows != n || S->ncols != n)
+        return guard(ctx, [&] { throw Error(MGPU_ERR_ARG, "project_reduce: operator shape mismatch"); });
+    return mgpu_project_reduce_slab(ctx, M, D, K, 0, 0, n, r, V, m, F, q, Cp, Cv, Mh, Dh, Kh, Fh, Cph, Cvh, where);
+  }
+  return guard(ctx, [&] { throw Error(MGPU_ERR_ARG, "project_reduce: null argument"); });
 }
 
 int mgpu_arnoldi_deflate(mgpu_ctx *ctx, int64_t len, double *X, int nblocks, const double *const *blocks,

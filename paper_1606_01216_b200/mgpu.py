@@ -30,7 +30,7 @@ EXPORTED = [
     "mgpu_csr_download", "mgpu_csr_device_view", "mgpu_csr_free", "mgpu_sp_add_scaled", "mgpu_shifted_operators",
     "mgpu_transpose", "mgpu_trace", "mgpu_trace_inner", "mgpu_spmv", "mgpu_chain_apply", "mgpu_chain_quality", "mgpu_spai_build",
     "mgpu_spai_update", "mgpu_spai_ls", "mgpu_spai_ls_batched", "mgpu_spgemm", "mgpu_cg_solve",
-    "mgpu_model_chain", "mgpu_model_hermite", "mgpu_host_free", "mgpu_thin_qr", "mgpu_project_reduce",
+    "mgpu_model_chain", "mgpu_model_hermite", "mgpu_host_free", "mgpu_thin_qr", "mgpu_project_reduce", "mgpu_project_reduce_slab",
     "mgpu_arnoldi_deflate",
 ]
 
@@ -131,6 +131,8 @@ def lib():
         L.mgpu_chain_quality.argtypes = [vp, C.c_int, vp, vp, C.c_int64, C.c_uint64, C.POINTER(C.c_double)]
         L.mgpu_thin_qr.argtypes = [vp, i64, i64, vp, dbl, vp, vp, C.POINTER(C.c_int64), C.c_int]
         L.mgpu_project_reduce.argtypes = [vp, vp, vp, vp, i64, vp, i64, vp, i64, vp, vp] + [vp] * 6 + [C.c_int]
+        L.mgpu_project_reduce_slab.argtypes = [vp, vp, vp, vp, i64, i64, i64, i64, vp, i64, vp, i64, vp, vp] + \
+            [vp] * 6 + [C.c_int]
         L.mgpu_arnoldi_deflate.argtypes = [vp, i64, vp, C.c_int, vp, vp, C.c_int]
         L.mgpu_spai_build.argtypes = [vp, vp, dbl, i64, C.c_int, C.POINTER(vp), vp]
         L.mgpu_spai_update.argtypes = [vp, vp, vp, dbl, i64, C.c_int, C.POINTER(vp), vp]
@@ -430,6 +432,30 @@ def project_reduce(M, D, K, V, F=None, Cp=None, Cv=None, ctx=None) -> dict:
                                         _ptr(Cvm) if q else None, _ptr(out["Mh"]), _ptr(out["Dh"]), _ptr(out["Kh"]),
                                         _ptr(out["Fh"]) if m else None, _ptr(out["Cph"]) if q else None,
                                         _ptr(out["Cvh"]) if q else None, MGPU_HOST))
+    return out
+
+
+def project_reduce_slab(M, D, K, row0: int, ext0: int, Vext, F=None, Cp=None, Cv=None, ctx=None) -> dict:
+    """Partial projections of one row slab (mgpu_project_reduce_slab): M, D, K are the slab's rows with
+    global column indices, Vext the basis rows [ext0, ext0 + len(Vext)), F / Cp / Cv the slab's parts."""
+    ctx = ctx or default_context()
+    dM, dD, dK = (_dev(x, ctx) for x in (M, D, K))
+    V = _fortran(Vext)
+    nx, r = V.shape
+    p = dM.nrows
+    Fm = _fortran(F) if F is not None else np.zeros((p, 0), order="F")
+    m = Fm.shape[1]
+    q = 0 if Cp is None else _fortran(Cp).shape[0]
+    Cpm = _fortran(Cp) if q else np.zeros((0, p), order="F")
+    Cvm = _fortran(Cv) if q else np.zeros((0, p), order="F")
+    out = {k: np.zeros(shape, order="F") for k, shape in
+           (("Mh", (r, r)), ("Dh", (r, r)), ("Kh", (r, r)), ("Fh", (r, m)), ("Cph", (q, r)), ("Cvh", (q, r)))}
+    ctx.check(lib().mgpu_project_reduce_slab(ctx.handle, dM.handle, dD.handle, dK.handle, row0, ext0, nx, r, _ptr(V),
+                                             m, _ptr(Fm) if m else None, q, _ptr(Cpm) if q else None,
+                                             _ptr(Cvm) if q else None, _ptr(out["Mh"]), _ptr(out["Dh"]),
+                                             _ptr(out["Kh"]), _ptr(out["Fh"]) if m else None,
+                                             _ptr(out["Cph"]) if q else None, _ptr(out["Cvh"]) if q else None,
+                                             MGPU_HOST))
     return out
 
 

@@ -50,3 +50,128 @@ def gather_blocks(local_blocks: Sequence, local_index: Sequence[int], total: int
         for i, b in part:
             out[i] = b
     return out
+
+
+# ---------------------------------------------------------------- distributed projection
+# After the shift-sharded solves the Arnoldi basis is redistributed by ROWS: rank r keeps
+# rows [r0, r1) of every basis column, computes its slab's partial V_slab^T (S V) with a
+# halo of bandwidth rows from its neighbours, and one all-reduce sums the r x r partials
+# (airga.cpp:485-500 split over row slabs).
+def row_range(n: int, rank: int, world: int):
+    """Balanced contiguous row slab [r0, r1) of rank."""
+    return n * rank // world, n * (rank + 1) // world
+
+
+def row_slab(A, r0: int, r1: int):
+    """Rows [r0, r1) of a host CSR, global column indices kept (same type as A)."""
+    import numpy as np
+    b, e = int(A.row_ptr[r0]), int(A.row_ptr[r1])
+    rp = (np.asarray(A.row_ptr[r0:r1 + 1], np.int64) - b).astype(np.int64)
+    return type(A)(r1 - r0, A.ncols, rp, np.asarray(A.col_idx[b:e], np.int32).copy(),
+                   np.asarray(A.values[b:e], np.float64).copy())
+
+
+def bandwidth(A) -> int:
+    """max |i - j| over stored entries of a host CSR."""
+    import numpy as np
+    if A.nnz == 0:
+        return 0
+    rows = np.repeat(np.arange(A.nrows), np.diff(A.row_ptr))
+    return int(np.max(np.abs(rows - A.col_idx.astype(np.int64))))
+
+
+def columns_to_rows(X_local, col_ids: Sequence[int], total_cols: int, n: int, dist=None):
+    """All-to-all: every rank holds full-length columns col_ids of the basis (n x c_local);
+    returns this rank's row slab of all total_cols columns, in global column order."""
+    import numpy as np
+    X_local = np.asarray(X_local, np.float64).reshape(n, -1)
+    world = 1 if dist is None or not dist.is_initialized() else dist.get_world_size()
+    rank = 0 if world == 1 else dist.get_rank()
+    r0, r1 = row_range(n, rank, world)
+    out = np.zeros((r1 - r0, total_cols), order="F")
+    if world == 1:
+        out[:, list(col_ids)] = X_local[r0:r1]
+        return out
+    # each destination d receives rows [r0_d, r1_d) of this rank's columns
+    sends = [(list(col_ids), X_local[slice(*row_range(n, d, world))]) for d in range(world)]
+    recv = [None] * world
+    if dist.get_backend() == "nccl":
+        import torch
+        dev = torch.device("cuda", torch.cuda.current_device())
+        counts = [None] * world
+        dist.all_gather_object(counts, len(col_ids))
+        ids = [None] * world
+        dist.all_gather_object(ids, list(col_ids))
+        inputs = [torch.as_tensor(np.ascontiguousarray(s[1]), device=dev) for s in sends]
+        outputs = [torch.empty((r1 - r0, counts[s]), dtype=torch.float64, device=dev) for s in range(world)]
+        dist.all_to_all(outputs, inputs)
+        recv = [(ids[s], outputs[s].cpu().numpy()) for s in range(world)]
+    else:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, sends)
+        recv = [gathered[s][rank] for s in range(world)]
+    for ids, block in recv:
+        if len(ids):
+            out[:, ids] = block
+    return out
+
+
+def halo_rows(V_slab, r0: int, n: int, h: int, dist=None):
+    """Extend this rank's basis rows [r0, r1) by h rows on each side (clipped to [0, n)) with the
+    neighbours' boundary rows; returns (Vext, ext0)."""
+    import numpy as np
+    V_slab = np.asarray(V_slab, np.float64)
+    r1 = r0 + V_slab.shape[0]
+    world = 1 if dist is None or not dist.is_initialized() else dist.get_world_size()
+    lo, hi = max(0, r0 - h), min(n, r1 + h)
+    if world == 1 or h == 0:
+        if (lo, hi) != (r0, r1):
+            raise ValueError("halo rows requested without neighbours")
+        return np.asfortranarray(V_slab), r0
+    k = min(h, V_slab.shape[0])
+    mine = (r0, r1, V_slab[:k], V_slab[V_slab.shape[0] - k:])
+    parts = [None] * world
+    dist.all_gather_object(parts, mine)
+    ext = np.zeros((hi - lo, V_slab.shape[1]), order="F")
+    ext[r0 - lo:r1 - lo] = V_slab
+    for (a0, a1, first, last) in parts:
+        for base, rows in ((a0, first), (a1 - len(last), last)):
+            for t in range(len(rows)):
+                g = base + t
+                if lo <= g < hi and not (r0 <= g < r1):
+                    ext[g - lo] = rows[t]
+    return ext, lo
+
+
+def project_reduce_distributed(M, D, K, V_slab, r0: int, F=None, Cp=None, Cv=None, dist=None, local=None,
+                               device=None) -> dict:
+    """airga.cpp:485-500 over a row-distributed basis: local slab partials (device:
+    mgpu.project_reduce_slab) + one all-reduce.  `local` may stand in for the device product
+    (CPU tests).  Returns replicated Mh, Dh, Kh, Fh, Cph, Cvh."""
+    import numpy as np
+    n = M.nrows
+    V_slab = np.asarray(V_slab, np.float64)
+    r1 = r0 + V_slab.shape[0]
+    h = max(bandwidth(M), bandwidth(D), bandwidth(K))
+    Vext, ext0 = halo_rows(V_slab, r0, n, h, dist)
+    if local is None:
+        from . import mgpu
+        local = mgpu.project_reduce_slab
+    part = local(row_slab(M, r0, r1), row_slab(D, r0, r1), row_slab(K, r0, r1), r0, ext0, Vext,
+                 None if F is None else np.asarray(F)[r0:r1], None if Cp is None else np.asarray(Cp)[:, r0:r1],
+                 None if Cv is None else np.asarray(Cv)[:, r0:r1])
+    keys = ("Mh", "Dh", "Kh", "Fh", "Cph", "Cvh")
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return part
+    import torch
+    flat = np.concatenate([np.asarray(part[k]).ravel(order="F") for k in keys])
+    t = torch.as_tensor(flat, device=device)
+    dist.all_reduce(t)
+    flat = t.cpu().numpy()
+    out, o = {}, 0
+    for k in keys:
+        shape = np.asarray(part[k]).shape
+        cnt = int(np.prod(shape))
+        out[k] = flat[o:o + cnt].reshape(shape, order="F")
+        o += cnt
+    return out
