@@ -751,6 +751,7 @@ struct BandShared
   double tot[kMaxSys * 2];
   int state[kMaxSys];
   int fresh[kMaxSys];
+  int pend[kMaxSys]; // cg_stream: x~ += alpha d_old still owed (deferred from phase B)
   int64_t sit[kMaxSys];
   int pmask[kMaxPoints];
   Seg seg[kMaxSeg];
@@ -1412,7 +1413,9 @@ struct PEll
 
 struct StreamParams
 {
-  int l, m, z, rpt, ch; // ch: rows per chunk
+  int l, m, z, rpt, ch; // ch: rows per chunk (phase A and the check pass)
+  int ch_b;             // rows per chunk in phase B (fewer vectors per row: taller chunks fill the same slot)
+  int fold;             // 1: x~ += alpha d deferred to the next phase A (m = 1), 0: applied in phase B
   int nb;               // ring depth (2..kStreamNB)
   int64_t n, ldv; // ldv = (n + 2 PADR) * m: doubles per point block
   int halo[kMaxZ + 1];
@@ -1437,8 +1440,8 @@ struct StreamParams
   // shared-memory carve-up (bytes): two input buffers (phase A layout and
   // phase B layout alias) + stage buffers
   size_t buf_bytes, off_stage0, off_stage1, off_stage2;
-  size_t a_vr, a_vd, a_fv[kMaxZ], a_fo[kMaxZ], a_av, a_ao; // phase A offsets inside a buffer
-  size_t b_x, b_d, b_r, b_w;                               // phase B offsets inside a buffer
+  size_t a_vr, a_vd, a_vx, a_fv[kMaxZ], a_fo[kMaxZ], a_av, a_ao; // phase A offsets inside a buffer
+  size_t b_r, b_w, b_x, b_d;                                      // phase B offsets inside a buffer
 };
 
 __device__ __forceinline__ const double *vrow(const StreamParams &P, const double *base, int p, int64_t i)
@@ -1478,7 +1481,8 @@ __device__ __forceinline__ bool chunk_next(const BandShared<TB> &sh, int64_t CH,
 __device__ __forceinline__ int64_t even_up(int64_t x) { return (x + 1) & ~static_cast<int64_t>(1); }
 
 // Producer: issue the bulk copies of one chunk's inputs into buffer `buf`.
-// kind 0: phase A step, 1: phase A check (x~ instead of r, no d), 2: phase B.
+// kind 0: phase A step (r, d_old over the halo; x~ on own rows for the deferred
+// update), 1: phase A check (x~ and d_old over the halo), 2: phase B (r, w).
 template <int TB>
 __device__ void stream_issue(const StreamParams &P, const PEll *tab, unsigned char *buf, uint64_t *bar, int kind, int p,
                              int64_t c0, int64_t c1, const double *dold, const double *dnew)
@@ -1489,18 +1493,23 @@ __device__ void stream_issue(const StreamParams &P, const PEll *tab, unsigned ch
   {
     const int64_t rows = even_up(c1 - c0);
     const uint32_t vb = static_cast<uint32_t>(rows * m * 8);
-    bytes = 4 * vb;
+    bytes = (P.fold ? 2 : 4) * vb;
     mbar_expect_tx(bar, bytes);
-    bulk_g2s(buf + P.b_x, vrow(P, P.xt, p, c0), vb, bar);
-    bulk_g2s(buf + P.b_d, vrow(P, dnew, p, c0), vb, bar);
     bulk_g2s(buf + P.b_r, vrow(P, P.r, p, c0), vb, bar);
     bulk_g2s(buf + P.b_w, vrow(P, P.w, p, c0), vb, bar);
+    if (!P.fold)
+    {
+      bulk_g2s(buf + P.b_x, vrow(P, P.xt, p, c0), vb, bar);
+      bulk_g2s(buf + P.b_d, vrow(P, dnew, p, c0), vb, bar);
+    }
     return;
   }
   const int H0 = P.hmax;
   const int64_t vrows = even_up(c1 - c0 + 2 * H0);
   const uint32_t vb = static_cast<uint32_t>(vrows * m * 8);
-  uint32_t total = kind == 0 ? 2 * vb : vb;
+  const uint32_t xb = static_cast<uint32_t>(even_up(c1 - c0) * m * 8);
+  const bool need_d = kind == 0 || P.fold; // the check pass reads d_old only for the deferred update
+  uint32_t total = (need_d ? 2 * vb : vb) + (kind == 0 && P.fold ? xb : 0u);
   for (int st = 0; st < P.z; ++st)
   {
     const int hd = P.halo[st + 1];
@@ -1515,8 +1524,10 @@ __device__ void stream_issue(const StreamParams &P, const PEll *tab, unsigned ch
   }
   mbar_expect_tx(bar, total);
   bulk_g2s(buf + P.a_vr, vrow(P, kind == 0 ? P.r : P.xt, p, c0 - H0), vb, bar);
-  if (kind == 0)
+  if (need_d)
     bulk_g2s(buf + P.a_vd, vrow(P, dold, p, c0 - H0), vb, bar);
+  if (kind == 0 && P.fold)
+    bulk_g2s(buf + P.a_vx, vrow(P, P.xt, p, c0), xb, bar);
   for (int st = 0; st < P.z; ++st)
   {
     const int hd = P.halo[st + 1];
@@ -1682,7 +1693,7 @@ __device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, cons
                             uint64_t *full, uint64_t *empty, uint32_t &phase_bits, RingProducer &rp, int kind,
                             const double *dold, double *dnew, PhaseClock &pc)
 {
-  const int64_t CH = P.ch;
+  const int64_t CH = kind == 2 ? P.ch_b : P.ch;
   const int m = P.m;
   const int nv = kind == 0 ? 2 * m : m;
   ChunkIt cons{0, sh.nseg > 0 ? static_cast<int64_t>(sh.seg[0].rs) : 0};
@@ -1789,13 +1800,14 @@ __device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, cons
     const int sb = cp * m; // first system of the point
     if (kind == 2)
     {
-      // x~ += alpha d, r -= alpha w, partial (r, r): one element (row, column) per thread
-      const double *xs = reinterpret_cast<const double *>(buf + P.b_x);
-      const double *ds = reinterpret_cast<const double *>(buf + P.b_d);
+      // r -= alpha w, partial (r, r): one element (row, column) per thread.  x~ += alpha d
+      // (krylov.cpp:113) is deferred to the next phase A, which streams d anyway.
       const double *rs = reinterpret_cast<const double *>(buf + P.b_r);
       const double *ws = reinterpret_cast<const double *>(buf + P.b_w);
-      double *xg = const_cast<double *>(vrow(P, P.xt, cp, base_i));
+      const double *xs = reinterpret_cast<const double *>(buf + P.b_x);
+      const double *ds = reinterpret_cast<const double *>(buf + P.b_d);
       double *rg = const_cast<double *>(vrow(P, P.r, cp, base_i));
+      double *xg = const_cast<double *>(vrow(P, P.xt, cp, base_i));
       const int ne = R * m;
       for (int e = threadIdx.x; e < ne; e += TB)
       {
@@ -1803,9 +1815,9 @@ __device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, cons
         if (sh.state[sb + c] != kRun)
           continue;
         const double al = sh.alpha[sb + c];
-        const double xn = __dadd_rn(xs[e], __dmul_rn(al, ds[e]));
+        if (!P.fold)
+          __stcg(xg + e, __dadd_rn(xs[e], __dmul_rn(al, ds[e])));
         const double rn = __dadd_rn(rs[e], __dmul_rn(-al, ws[e]));
-        __stcg(xg + e, xn);
         __stcg(rg + e, rn);
         acc_add<MT>(acc, c, __dmul_rn(rn, rn));
       }
@@ -1818,21 +1830,30 @@ __device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, cons
       double *s0 = reinterpret_cast<double *>(smem + P.off_stage0);
       double *sA = reinterpret_cast<double *>(smem + P.off_stage1);
       double *sB = reinterpret_cast<double *>(smem + P.off_stage2);
-      // stage 0: d = fresh ? r : r + beta d_old over the halo-extended chunk (check: x~)
+      // stage 0: d = fresh ? r : r + beta d_old over the halo-extended chunk; the deferred
+      // x~ += alpha_prev d_old on own rows.  Check pass: source x~ + alpha_prev d_old (not
+      // written back: neighbours read the same x~ rows as halo during this pass).
+      const double *vx = reinterpret_cast<const double *>(buf + P.a_vx);
       const int ne0 = (R + 2 * H0) * m;
       const int lo = H0 * m, hi = (H0 + R) * m;
       double *dg = kind == 0 ? const_cast<double *>(vrow(P, dnew, cp, base_i - H0)) : nullptr;
+      double *xg = kind == 0 ? const_cast<double *>(vrow(P, P.xt, cp, base_i - H0)) : nullptr;
       for (int e = threadIdx.x; e < ne0; e += TB)
       {
+        const int c = col_of<MT>(e, m);
+        const int sys = sb + c;
         double v;
         if (kind == 1)
-          v = vr[e];
+          v = sh.pend[sys] ? __dadd_rn(vr[e], __dmul_rn(sh.alpha[sys], vd[e])) : vr[e];
         else
         {
-          const int c = col_of<MT>(e, m);
-          v = sh.fresh[sb + c] ? vr[e] : __dadd_rn(vr[e], __dmul_rn(sh.beta[sb + c], vd[e]));
+          v = sh.fresh[sys] ? vr[e] : __dadd_rn(vr[e], __dmul_rn(sh.beta[sys], vd[e]));
           if (e >= lo && e < hi)
+          {
             __stcg(dg + e, v);
+            if (sh.pend[sys] && sh.state[sys] == kRun)
+              __stcg(xg + e, __dadd_rn(vx[e - lo], __dmul_rn(sh.alpha[sys], vd[e])));
+          }
         }
         s0[e] = v;
       }
@@ -1978,6 +1999,7 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
     sh.target[s] = P.rtol * bn;
     sh.state[s] = bn == 0.0 ? kZeroRhs : kRun;
     sh.fresh[s] = 1;
+    sh.pend[s] = 0;
     sh.beta[s] = 0.0;
     sh.sit[s] = 0;
   }
@@ -2028,7 +2050,7 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
     __syncthreads();
     if (sh.flag)
     {
-      stream_pass<TB, MT, kStreamNB>(P, sh, tab, smem_s, bars, bars + kStreamNB, phase_bits, rp, 1, nullptr, nullptr, pc);
+      stream_pass<TB, MT, kStreamNB>(P, sh, tab, smem_s, bars, bars + kStreamNB, phase_bits, rp, 1, cur ? P.dbuf1 : P.dbuf0, nullptr, pc);
       fence_async_global();
       grid.sync();
       reduce_blocks<TBX, StreamParams>(P, sh, m);
@@ -2095,6 +2117,8 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
     pc.mark(11);
     for (int s = threadIdx.x; s < S; s += TBX)
     {
+      if (sh.pmask[s / m])
+        sh.pend[s] = 0; // phase A applied the deferred x~ update
       if (sh.state[s] != kRun)
         continue;
       const int p = s / m, c = s % m;
@@ -2127,6 +2151,7 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
       sh.beta[s] = rn / sh.rho[s];
       sh.rho[s] = rn;
       sh.fresh[s] = 0;
+      sh.pend[s] = P.fold; // x~ += alpha d owed to the next phase A / check pass
     }
     __syncthreads();
     cur ^= 1;
@@ -2147,7 +2172,7 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
   __syncthreads();
   if (sh.flag)
   {
-    stream_pass<TB, MT, kStreamNB>(P, sh, tab, smem_s, bars, bars + kStreamNB, phase_bits, rp, 1, nullptr, nullptr, pc);
+    stream_pass<TB, MT, kStreamNB>(P, sh, tab, smem_s, bars, bars + kStreamNB, phase_bits, rp, 1, cur ? P.dbuf1 : P.dbuf0, nullptr, pc);
     fence_async_global();
     grid.sync();
     reduce_blocks<TBX, StreamParams>(P, sh, m);
@@ -2404,6 +2429,13 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
       EF[st] = std::max(EF[st], hF[static_cast<size_t>(p) * z + f].E);
     }
   }
+  // x~ update placement: deferred into phase A (one vector pass fewer) when phase A is light --
+  // no chain and m <= 2 (measured on B200: m=2 333 -> 298 us/iter, m=1 P=I 215 -> 198); with a
+  // chain or m = 4 the latency-bound phase A gets slower than phase B gains, so it stays in B.
+  // MGPU_STREAM_FOLD=0/1 overrides (diagnostics).
+  bool fold = m <= 2 && z == 0;
+  if (const char *f = std::getenv("MGPU_STREAM_FOLD"))
+    fold = f[0] == '1';
   // ---- shared-memory plan: the largest chunk height whose double buffer fits
   StreamParams P{};
   size_t dyn = 0;
@@ -2439,6 +2471,7 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
     const int64_t vrows = (ch + 2 * H0 + 1) & ~1ll;
     P.a_vr = take(sizeof(double) * vrows * m);
     P.a_vd = take(sizeof(double) * vrows * m);
+    P.a_vx = fold ? take(sizeof(double) * ch * m) : 0;
     for (int st = 0; st < z; ++st)
     {
       const int64_t rows = (ch + 2 * hal[st + 1] + 1) & ~1ll;
@@ -2449,11 +2482,7 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
     P.a_ao = take(sizeof(unsigned long long) * ch * 2);
     const size_t a_bytes = off;
     off = 0;
-    P.b_x = take(sizeof(double) * ch * m);
-    P.b_d = take(sizeof(double) * ch * m);
-    P.b_r = take(sizeof(double) * ch * m);
-    P.b_w = take(sizeof(double) * ch * m);
-    const size_t b_bytes = off;
+    const size_t b_bytes = sizeof(double) * ch * m * (fold ? 2 : 4);
     P.buf_bytes = (std::max(a_bytes, b_bytes) + 127) & ~static_cast<size_t>(127);
     off = nb * P.buf_bytes;
     P.off_stage0 = take(sizeof(double) * (ch + 2 * H0) * m);
@@ -2487,15 +2516,18 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
     {
       const int b0 = static_cast<int>(static_cast<int64_t>(p) * G / l);
       const int b1 = static_cast<int>(static_cast<int64_t>(p + 1) * G / l);
-      const int nb = b1 - b0;
       const int64_t groups = (n + 31) / 32;
+      // a point spans at most one block per 32-row group: every block in [b0, b0 + nb) owns
+      // rows, so every partial-sum slot the reduction reads is written (a block without rows
+      // would never flush its slot)
+      const int nb = static_cast<int>(std::min<int64_t>(b1 - b0, groups));
       for (int k = 0; k < nb; ++k)
       {
         const int64_t g0 = groups * k / nb, g1 = groups * (k + 1) / nb;
         hseg[static_cast<size_t>(b0 + k) * kMaxSeg] =
             Seg{p, static_cast<int>(g0 * 32), static_cast<int>(std::min<int64_t>(n, g1 * 32)), 0};
       }
-      hpb[p] = make_int2(b0, b1);
+      hpb[p] = make_int2(b0, b0 + nb);
     }
   }
   else
@@ -2523,6 +2555,21 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
   P.z = z;
   P.rpt = 1;
   P.ch = static_cast<int>(CH);
+  {
+    // phase B: r, w (+ x~, d unfolded) -> the tallest chunk (multiple of 64 rows, <= 8192) that fits one slot
+    const int nvec = fold ? 2 : 4;
+    int64_t chb = static_cast<int64_t>(P.buf_bytes / (nvec * sizeof(double) * static_cast<size_t>(m))) & ~63ll;
+    chb = std::min<int64_t>(std::max<int64_t>(chb, CH), 8192);
+    if (std::getenv("MGPU_STREAM_SAME_CHB")) // diagnostics: phase B on the phase A chunk height
+      chb = CH;
+    P.ch_b = static_cast<int>(chb);
+    const size_t vb = static_cast<size_t>(chb) * m * sizeof(double); // multiple of 512 B
+    P.b_r = 0;
+    P.b_w = vb;
+    P.b_x = 2 * vb;
+    P.b_d = 3 * vb;
+    P.fold = fold ? 1 : 0;
+  }
   P.n = n;
   P.ldv = ldv;
   for (int q = 0; q <= z; ++q)
@@ -2660,15 +2707,15 @@ void cg_batch(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_
       {
         const int b0 = static_cast<int>(static_cast<int64_t>(p) * G / l);
         const int b1 = static_cast<int>(static_cast<int64_t>(p + 1) * G / l);
-        const int nb = b1 - b0;
         const int64_t groups = (n + 31) / 32;
+        const int nb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(b1 - b0, groups))); // no row-less blocks
         for (int k = 0; k < nb; ++k)
         {
           const int64_t g0 = groups * k / nb, g1 = groups * (k + 1) / nb;
           hseg[static_cast<size_t>(b0 + k) * kMaxSeg] =
               Seg{p, static_cast<int>(g0 * 32), static_cast<int>(std::min<int64_t>(n, g1 * 32)), 0};
         }
-        hpb[p] = make_int2(b0, b1);
+        hpb[p] = make_int2(b0, b0 + nb);
       }
     }
     else
