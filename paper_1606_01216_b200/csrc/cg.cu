@@ -2640,8 +2640,7 @@ void cg_batch(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_
   const bool banded = ctx->cg_path != 1 && band_plan(ctx, l, A, z, chains, m, halo, &hmax);
   const int64_t vec = static_cast<int64_t>(l) * n * m;
   const int64_t vbytes = sizeof(double) * (vec > 0 ? vec : 1);
-  DBuf b(vbytes, s), xt(vbytes, s), r(vbytes, s), d(vbytes, s), w(vbytes, s);
-  DBuf t0(banded || z >= 1 ? vbytes : 8, s), t1(banded || z >= 2 ? vbytes : 8, s);
+  DBuf b, xt, r, d, w, t0, t1; // grid kernels' vectors, allocated only if those kernels run
   const int S = l * m;
   DBuf d_it(sizeof(int64_t) * S, s), d_conv(sizeof(int) * S, s), d_st(sizeof(int) * S, s), d_bd(sizeof(int64_t) * S, s);
   DBuf d_loop(sizeof(int64_t), s);
@@ -2685,6 +2684,13 @@ void cg_batch(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_
   }
   if (!clustered && !streamed)
   {
+    b = DBuf(vbytes, s);
+    xt = DBuf(vbytes, s);
+    r = DBuf(vbytes, s);
+    d = DBuf(vbytes, s);
+    w = DBuf(vbytes, s);
+    t0 = DBuf(banded || z >= 1 ? vbytes : 8, s);
+    t1 = DBuf(banded || z >= 2 ? vbytes : 8, s);
     cg_init<<<blocks_for(vec), kThreads, 0, s>>>(l, m, n, B_dev, ldb, b.as<double>(), r.as<double>(), d.as<double>(),
                                                    xt.as<double>());
     check_launch(ctx, "cg_init");
@@ -2935,6 +2941,35 @@ extern "C" int mgpu_cg_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int
         for (int p0 = 0; p0 < l; p0 += pts)
         {
           const int lp = l - p0 < pts ? l - p0 : pts;
+          if (mc == m)
+          {
+            // every column in one launch: the caller's [point][column][row] layout is the
+            // kernel's, so B is read in place (point stride ldb, 0 = shared) and the
+            // outputs are written in place
+            const int Ss = lp * mc;
+            std::vector<int64_t> sit(Ss), sbd(Ss);
+            std::vector<int> scv(Ss), sst(Ss);
+            std::vector<double> shist(hist.empty() ? 0 : static_cast<size_t>(Ss) * out->history_cap);
+            const int64_t o = static_cast<int64_t>(p0) * blk;
+            cg_batch(ctx, lp, A + p0, z, z > 0 ? chains + static_cast<size_t>(p0) * z : nullptr, n, mc,
+                     B_dev + (ldb == 0 ? 0 : static_cast<int64_t>(p0) * ldb), ldb, rtol, maxit,
+                     X_dev ? X_dev + o : nullptr, REC_dev ? REC_dev + o : nullptr, TR_dev ? TR_dev + o : nullptr,
+                     sit.data(), scv.data(), sst.data(), sbd.data(), shist.empty() ? nullptr : shist.data(),
+                     out->history_cap, &total_ms, &total_loop);
+            for (int q = 0; q < Ss; ++q)
+            {
+              const int64_t dst = static_cast<int64_t>(p0) * m + q;
+              it[dst] = sit[q];
+              cv[dst] = scv[q];
+              st[dst] = sst[q];
+              bd[dst] = sbd[q];
+              if (!hist.empty())
+                std::copy(shist.begin() + static_cast<int64_t>(q) * out->history_cap,
+                          shist.begin() + static_cast<int64_t>(q + 1) * out->history_cap,
+                          hist.begin() + dst * out->history_cap);
+            }
+            continue;
+          }
           // gather the column slice [c0, c0+mc) of every point into a compact block
           DBuf Bs(sizeof(double) * static_cast<size_t>(lp) * n * mc, s);
           for (int p = 0; p < lp; ++p)

@@ -21,6 +21,9 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "internal.cuh"
@@ -1189,8 +1192,28 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
   cl.sync();
 }
 
+// cudaOccupancyMaxActiveClusters costs tens of microseconds and v2_solve asks it for every
+// cluster size on every solve: the answer depends only on (device, kernel, cluster size,
+// dynamic shared memory), so it is memoised.
+int cached_active_clusters(int device, int kernel_id, int cs, size_t dyn, int (*query)(int, size_t))
+{
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int, size_t>, int> cache;
+  const auto key = std::make_tuple(device, kernel_id, cs, dyn);
+  {
+    std::lock_guard<std::mutex> g(mu);
+    const auto it = cache.find(key);
+    if (it != cache.end())
+      return it->second;
+  }
+  const int v = query(cs, dyn);
+  std::lock_guard<std::mutex> g(mu);
+  cache[key] = v;
+  return v;
+}
+
 template <int RPT>
-int v2_active_clusters(const V2Params &P, size_t dyn)
+int v2_active_clusters_query(int cs, size_t dyn)
 {
   auto kern = cg_cluster_v2<RPT>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)) != cudaSuccess ||
@@ -1200,12 +1223,12 @@ int v2_active_clusters(const V2Params &P, size_t dyn)
     return 0;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(static_cast<unsigned>(P.cs));
+  cfg.gridDim = dim3(static_cast<unsigned>(cs));
   cfg.blockDim = dim3(kV2TB);
   cfg.dynamicSmemBytes = dyn;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = static_cast<unsigned>(P.cs);
+  attr[0].val.clusterDim.x = static_cast<unsigned>(cs);
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -1217,6 +1240,12 @@ int v2_active_clusters(const V2Params &P, size_t dyn)
     return 0;
   }
   return clusters;
+}
+
+template <int RPT>
+int v2_active_clusters(mgpu_ctx *ctx, const V2Params &P, size_t dyn)
+{
+  return cached_active_clusters(ctx->device, 100 + RPT, P.cs, dyn, v2_active_clusters_query<RPT>);
 }
 
 template <int RPT>
@@ -1283,8 +1312,8 @@ bool v2_solve(mgpu_ctx *ctx, V2Params P, size_t budget)
       continue;
     const int rpt = static_cast<int>((rb + kV2TB - 1) / kV2TB);
     const int r4 = rpt <= 1 ? 1 : (rpt == 2 ? 2 : 4);
-    const int act = r4 == 1 ? v2_active_clusters<1>(Q, off) : (r4 == 2 ? v2_active_clusters<2>(Q, off)
-                                                                        : v2_active_clusters<4>(Q, off));
+    const int act = r4 == 1 ? v2_active_clusters<1>(ctx, Q, off)
+                            : (r4 == 2 ? v2_active_clusters<2>(ctx, Q, off) : v2_active_clusters<4>(ctx, Q, off));
     if (act < 1)
       continue;
     const double waves = std::ceil(static_cast<double>(P.l) / act);
