@@ -233,6 +233,10 @@ int mgpu_model_chain(int64_t n, double alpha, double beta, double stiffness_scal
 int mgpu_model_hermite(int64_t ne, double E, double I, double rho, double area, double L, double alpha, double beta,
                        mgpu_host_csr *M, mgpu_host_csr *D, mgpu_host_csr *K);
 void mgpu_host_free(mgpu_host_csr *a);
+/* Device-side generation of the same Hermite cantilever: M, D, K assembled in HBM,
+ * bitwise equal to mgpu_model_hermite (row-parallel element sums in element order, exact zeros dropped). */
+int mgpu_model_hermite_device(mgpu_ctx *ctx, int64_t ne, double E, double I, double rho, double area, double L,
+                              double alpha, double beta, mgpu_csr **M, mgpu_csr **D, mgpu_csr **K);
 
 
 /* ------------------------------------------------------------------ global Arnoldi + projection */

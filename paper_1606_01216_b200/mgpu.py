@@ -31,7 +31,7 @@ EXPORTED = [
     "mgpu_transpose", "mgpu_trace", "mgpu_trace_inner", "mgpu_spmv", "mgpu_chain_apply", "mgpu_chain_quality", "mgpu_spai_build",
     "mgpu_spai_update", "mgpu_spai_ls", "mgpu_spai_ls_batched", "mgpu_spgemm", "mgpu_cg_solve",
     "mgpu_model_chain", "mgpu_model_hermite", "mgpu_host_free", "mgpu_thin_qr", "mgpu_project_reduce", "mgpu_project_reduce_slab",
-    "mgpu_arnoldi_deflate",
+    "mgpu_arnoldi_deflate", "mgpu_model_hermite_device",
 ]
 
 
@@ -143,6 +143,7 @@ def lib():
                                     C.POINTER(_CgOut)]
         L.mgpu_model_chain.argtypes = [i64, dbl, dbl, dbl, dbl, C.c_int] + [C.POINTER(_HostCsr)] * 3
         L.mgpu_model_hermite.argtypes = [i64] + [dbl] * 7 + [C.POINTER(_HostCsr)] * 3
+        L.mgpu_model_hermite_device.argtypes = [vp, i64] + [dbl] * 7 + [C.POINTER(C.c_void_p)] * 3
         L.mgpu_host_free.argtypes = [C.POINTER(_HostCsr)]
         _lib = L
     return _lib
@@ -191,6 +192,16 @@ def model_hermite(ne: int, E=2.1e11, I=1e-8, rho=7800.0, area=1e-4, L=1.0, alpha
     if st != MGPU_OK:
         raise ArgumentError("hermite model: bad arguments")
     return _from_host_struct(M), _from_host_struct(D), _from_host_struct(K)
+
+
+def model_hermite_device(ne: int, E=2.1e11, I=1e-8, rho=7800.0, area=1e-4, L=1.0, alpha=0.1, beta=1e-5, ctx=None):
+    """The Hermite cantilever assembled on the device (same matrices as model_hermite, bit for bit):
+    returns (M, D, K) as DeviceCsr."""
+    ctx = ctx or default_context()
+    hs = [C.c_void_p(), C.c_void_p(), C.c_void_p()]
+    ctx.check(lib().mgpu_model_hermite_device(ctx.handle, ne, E, I, rho, area, L, alpha, beta,
+                                              C.byref(hs[0]), C.byref(hs[1]), C.byref(hs[2])))
+    return tuple(DeviceCsr(ctx, h, 2 * ne) for h in hs)
 
 
 def model_chain(n: int, alpha=0.05, beta=0.05, stiffness_scale=0.01, mass_scale=1.0, consistent=False):

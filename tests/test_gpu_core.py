@@ -83,3 +83,15 @@ def test_argument_errors(mg, oracle):
         mg.shifted_operators(M2, D, K, [1.0])
     with pytest.raises(mg.ArgumentError):
         mg.pcg_solve(K, [], np.ones(50), rtol=0.0)
+
+
+@pytest.mark.parametrize("ne", [1, 2, 3, 1000, 250000])
+def test_device_beam_generation_bitwise(mg, ne):
+    """the Hermite cantilever assembled on the device == the host generator, bit for bit."""
+    want = mg.model_hermite(ne)
+    got = mg.model_hermite_device(ne)
+    for g, w in zip(got, want):
+        d = g.download()
+        np.testing.assert_array_equal(d.row_ptr, w.row_ptr)
+        np.testing.assert_array_equal(d.col_idx, w.col_idx)
+        np.testing.assert_array_equal(d.values, w.values)
