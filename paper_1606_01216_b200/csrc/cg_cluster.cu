@@ -124,10 +124,10 @@ __device__ __forceinline__ void cta_sum_push(ClShared &sh, double (&v)[NV], int 
 {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int k = 0; k < NV; ++k)
+  for (int off = 16; off > 0; off >>= 1)
   {
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1)
+    for (int k = 0; k < NV; ++k) // quantities interleaved: independent shuffle chains in flight
       v[k] = __dadd_rn(v[k], __shfl_xor_sync(0xffffffffu, v[k], off));
   }
   if (lane == 0)
@@ -139,19 +139,31 @@ __device__ __forceinline__ void cta_sum_push(ClShared &sh, double (&v)[NV], int 
   __syncthreads();
   if (warp == 0)
   {
-    for (int k = 0; k < nv; ++k)
-    {
-      double x = lane < TB / 32 ? sh.red[lane][k] : 0.0;
+    double x[NV];
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1)
-        x = __dadd_rn(x, __shfl_xor_sync(0xffffffffu, x, off));
-      if (lane < cs)
-        cl.map_shared_rank(inbox, lane)[k * kCMaxCS + rank] = x;
+    for (int k = 0; k < NV; ++k)
+      x[k] = (k < nv && lane < TB / 32) ? sh.red[lane][k] : 0.0;
+    // lanes >= TB / 32 hold exact zeros: the first butterfly level would add 0 (x + 0 == x)
+#pragma unroll
+    for (int off = TB / 32 >= 32 ? 16 : TB / 64; off > 0; off >>= 1)
+    {
+#pragma unroll
+      for (int k = 0; k < NV; ++k)
+        x[k] = __dadd_rn(x[k], __shfl_xor_sync(0xffffffffu, x[k], off));
+    }
+    if (lane < cs)
+    {
+      double *dst = cl.map_shared_rank(inbox, lane);
+#pragma unroll
+      for (int k = 0; k < NV; ++k)
+        if (k < nv)
+          dst[k * kCMaxCS + rank] = x[k];
     }
   }
 }
 
-// After the barrier: tot[k] = sum over ranks (fixed butterfly) of the local inbox.
+// After the barrier: tot[k] = sum over ranks (fixed butterfly) of the local inbox
+// (every lane ends with the total: all five levels are needed).
 __device__ __forceinline__ void warp_inbox_total(const double *inbox, int nv, int cs, double *out)
 {
   const int lane = threadIdx.x & 31;
@@ -163,6 +175,26 @@ __device__ __forceinline__ void warp_inbox_total(const double *inbox, int nv, in
       v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
     out[k] = v;
   }
+}
+
+template <int NV>
+__device__ __forceinline__ void warp_inbox_total(const double *inbox, int nv, int cs, double (&out)[NV])
+{
+  const int lane = threadIdx.x & 31;
+  double v[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+    v[k] = (k < nv && lane < cs) ? inbox[k * kCMaxCS + lane] : 0.0;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1)
+  {
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+      v[k] = __dadd_rn(v[k], __shfl_xor_sync(0xffffffffu, v[k], off));
+  }
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+    out[k] = v[k];
 }
 
 // After cluster.sync(): every warp forms tot[k] (k < nv) itself from the cs
@@ -812,7 +844,9 @@ struct V2Params
   long long *prof; // optional [16] accumulated clock64 deltas per phase (cluster 0, rank 0, thread 0)
 };
 
-template <int RPT>
+// EC > 0: every operator row (A and each chain factor) holds exactly EC ELL entries, known at
+// compile time, so the entry loops unroll with constant offsets; EC = 0: runtime widths.
+template <int RPT, int EC = 0>
 __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
 {
   cgrp::cluster_group cl = cgrp::this_cluster();
@@ -878,7 +912,7 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
   cl.sync();
   // per-system scalars live in registers; every thread derives identical values
   double tv[2];
-  warp_inbox_total(inboxA, 1, cs, tv);
+  warp_inbox_total<2>(inboxA, 1, cs, tv);
   const double bnorm = sqrt(tv[0]);
   double rho = tv[0], beta = 0.0;
   const double target = P.rtol * bnorm;
@@ -893,7 +927,7 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
     for (int st = 0; st < P.z; ++st)
     {
       const int hd = P.halo[st + 1];
-      const int E = P.ef[st];
+      const int E = EC > 0 ? EC : P.ef[st];
       const double *fv = reinterpret_cast<const double *>(raw + P.off_fv[st]);
       const unsigned long long *fo = reinterpret_cast<const unsigned long long *>(raw + P.off_fo[st]);
       double *out = tb[st & 1];
@@ -914,7 +948,8 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
         acc[j] = 0.0;
         ow[j] = ok[j] ? fo[q[j]] : 0ull;
       }
-      for (int e = 0; e < E; ++e)
+#pragma unroll
+      for (int e = 0; e < (EC > 0 ? EC : E); ++e)
       {
 #pragma unroll
         for (int j = 0; j < K; ++j)
@@ -945,7 +980,7 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
   auto apply_a = [&](const double *in, int hs, double (&y)[RPT]) {
     const double *av = reinterpret_cast<const double *>(raw + P.off_av);
     const unsigned long long *ao = reinterpret_cast<const unsigned long long *>(raw + P.off_ao);
-    const int E = P.ea;
+    const int E = EC > 0 ? EC : P.ea;
     bool ok[RPT];
     unsigned long long ow[RPT];
 #pragma unroll
@@ -955,7 +990,8 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
       ok[j] = threadIdx.x + j * kV2TB < R;
       ow[j] = ok[j] ? ao[threadIdx.x + j * kV2TB] : 0ull;
     }
-    for (int e = 0; e < E; ++e)
+#pragma unroll
+    for (int e = 0; e < (EC > 0 ? EC : E); ++e)
     {
 #pragma unroll
       for (int j = 0; j < RPT; ++j)
@@ -1020,8 +1056,8 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
     }
     cta_sum_push<kV2TB, 2>(sh, q2, 1, cl, inboxA, cs, rank);
     cl.sync();
-    double cv[1];
-    warp_inbox_total(inboxA, 1, cs, cv);
+    double cv[2];
+    warp_inbox_total<2>(inboxA, 1, cs, cv);
     const double tt = cv[0];
     bool fin = kind == 1 || sqrt(tt) <= target;
     const bool rst = !fin;
@@ -1119,7 +1155,7 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
     cl.sync();
     mark(5);
     double ta[2];
-    warp_inbox_total(inboxA, 2, cs, ta);
+    warp_inbox_total<2>(inboxA, 2, cs, ta);
     mark(6);
     const double curv = ta[0], dd = ta[1];
     if (!(curv > 1e-30 * dd)) // krylov.cpp:108
@@ -1147,8 +1183,8 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
     cta_sum_push<kV2TB, 2>(sh, pb, 1, cl, inboxB, cs, rank);
     cl.sync();
     mark(8);
-    double tb2[1];
-    warp_inbox_total(inboxB, 1, cs, tb2);
+    double tb2[2];
+    warp_inbox_total<2>(inboxB, 1, cs, tb2);
     mark(9);
     ++it;
     const double rn = tb2[0];
@@ -1248,11 +1284,12 @@ int v2_active_clusters(mgpu_ctx *ctx, const V2Params &P, size_t dyn)
   return cached_active_clusters(ctx->device, 100 + RPT, P.cs, dyn, v2_active_clusters_query<RPT>);
 }
 
-template <int RPT>
-void v2_launch(mgpu_ctx *ctx, const V2Params &P, size_t dyn)
+template <int RPT, int EC>
+void v2_launch_ec(mgpu_ctx *ctx, const V2Params &P, size_t dyn)
 {
-  MG_CUDA(cudaFuncSetAttribute(cg_cluster_v2<RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
-  MG_CUDA(cudaFuncSetAttribute(cg_cluster_v2<RPT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  MG_CUDA(cudaFuncSetAttribute(cg_cluster_v2<RPT, EC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(dyn)));
+  MG_CUDA(cudaFuncSetAttribute(cg_cluster_v2<RPT, EC>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(P.l * P.cs));
   cfg.blockDim = dim3(kV2TB);
@@ -1265,8 +1302,26 @@ void v2_launch(mgpu_ctx *ctx, const V2Params &P, size_t dyn)
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  MG_CUDA(cudaLaunchKernelEx(&cfg, cg_cluster_v2<RPT>, P));
+  MG_CUDA(cudaLaunchKernelEx(&cfg, cg_cluster_v2<RPT, EC>, P));
   check_launch(ctx, "cg_cluster_v2");
+}
+
+template <int RPT>
+void v2_launch(mgpu_ctx *ctx, const V2Params &P, size_t dyn)
+{
+  // uniform 5-entry rows (the Hermite operators and their LS-SPAI factors on the A pattern)
+  bool uniform5 = RPT == 4 && P.ea == 5;
+  for (int st = 0; st < P.z; ++st)
+    uniform5 = uniform5 && P.ef[st] == 5;
+  if constexpr (RPT == 4)
+  {
+    if (uniform5)
+    {
+      v2_launch_ec<4, 5>(ctx, P, dyn);
+      return;
+    }
+  }
+  v2_launch_ec<RPT, 0>(ctx, P, dyn);
 }
 
 // Plans and launches v2; false when no cluster size fits.  Picks the size that
