@@ -314,9 +314,11 @@ class DeviceCsr:
 
     def __del__(self):
         try:
-            if self.handle:
+            # a matrix outliving an explicitly closed context is left to process teardown
+            # (its stream-ordered free would use the destroyed context)
+            if self.handle and self.ctx.handle:
                 lib().mgpu_csr_free(self.handle)
-                self.handle = C.c_void_p()
+            self.handle = C.c_void_p()
         except Exception:
             pass
 

@@ -11,4 +11,5 @@ facs = mg.spai_ls_batched(ops, None, 0, ctx=ctx)
 b = np.zeros(M.nrows); b[-2] = 1
 mg.cg_solve_batched(ops, [[f.matrix] for f in facs], b, maxit=1000, ctx=ctx)
 print("cg ms", ctx.last_cg_timing(), ctx.last_cg_path)
+del ops, facs
 ctx.close()
