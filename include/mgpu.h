@@ -107,6 +107,11 @@ int mgpu_csr_upload_device(mgpu_ctx *ctx, int64_t nrows, int64_t ncols, int64_t 
  * (the LS-SPAI kernels keep the pattern fixed) are dropped on download. */
 int mgpu_csr_info(mgpu_ctx *ctx, const mgpu_csr *a, int64_t *nrows, int64_t *ncols, int64_t *nnz);
 int mgpu_csr_download(mgpu_ctx *ctx, const mgpu_csr *a, int64_t *row_ptr, int32_t *col_idx, double *values);
+/* Binary CSR sidecar (the reference interchanges Matrix Market text, model_io.cpp:154-351):
+ * "MGCSR\0\0\1", int64 nrows, ncols, nnz, row_ptr, col_idx (int32), values (f64), little-endian.
+ * write stores the download view; read validates like mgpu_csr_upload. */
+int mgpu_csr_write(mgpu_ctx *ctx, const mgpu_csr *a, const char *path);
+int mgpu_csr_read(mgpu_ctx *ctx, const char *path, mgpu_csr **out);
 /* Raw device view (no zero dropping) for callers that stay on the device. */
 int mgpu_csr_device_view(const mgpu_csr *a, int64_t *nrows, int64_t *nnz, const int64_t **row_ptr,
                          const int32_t **col_idx, const double **values);

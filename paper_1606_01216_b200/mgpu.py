@@ -31,7 +31,7 @@ EXPORTED = [
     "mgpu_transpose", "mgpu_trace", "mgpu_trace_inner", "mgpu_spmv", "mgpu_chain_apply", "mgpu_chain_quality", "mgpu_spai_build",
     "mgpu_spai_update", "mgpu_spai_ls", "mgpu_spai_ls_batched", "mgpu_spgemm", "mgpu_cg_solve",
     "mgpu_model_chain", "mgpu_model_hermite", "mgpu_host_free", "mgpu_thin_qr", "mgpu_project_reduce", "mgpu_project_reduce_slab",
-    "mgpu_arnoldi_deflate", "mgpu_model_hermite_device",
+    "mgpu_arnoldi_deflate", "mgpu_model_hermite_device", "mgpu_csr_write", "mgpu_csr_read",
 ]
 
 
@@ -143,6 +143,8 @@ def lib():
                                     C.POINTER(_CgOut)]
         L.mgpu_model_chain.argtypes = [i64, dbl, dbl, dbl, dbl, C.c_int] + [C.POINTER(_HostCsr)] * 3
         L.mgpu_model_hermite.argtypes = [i64] + [dbl] * 7 + [C.POINTER(_HostCsr)] * 3
+        L.mgpu_csr_write.argtypes = [vp, vp, C.c_char_p]
+        L.mgpu_csr_read.argtypes = [vp, C.c_char_p, C.POINTER(C.c_void_p)]
         L.mgpu_model_hermite_device.argtypes = [vp, i64] + [dbl] * 7 + [C.POINTER(C.c_void_p)] * 3
         L.mgpu_host_free.argtypes = [C.POINTER(_HostCsr)]
         _lib = L
@@ -311,6 +313,20 @@ class DeviceCsr:
         v = np.zeros(max(nnz.value, 1))
         self.ctx.check(lib().mgpu_csr_download(self.ctx.handle, self.handle, _ptr(rp), _ptr(ci), _ptr(v)))
         return SparseMatrix(n.value, nc.value, rp, ci[:nnz.value], v[:nnz.value])
+
+    def save(self, path: str) -> None:
+        """Binary CSR sidecar (mgpu_csr_write)."""
+        self.ctx.check(lib().mgpu_csr_write(self.ctx.handle, self.handle, os.fsencode(path)))
+
+    @staticmethod
+    def load(path: str, ctx: Optional[Context] = None) -> "DeviceCsr":
+        """Binary CSR sidecar straight into device memory (mgpu_csr_read)."""
+        ctx = ctx or default_context()
+        h = C.c_void_p()
+        ctx.check(lib().mgpu_csr_read(ctx.handle, os.fsencode(path), C.byref(h)))
+        n = C.c_int64()
+        lib().mgpu_csr_device_view(h, C.byref(n), None, None, None, None)
+        return DeviceCsr(ctx, h, n.value)
 
     def __del__(self):
         try:

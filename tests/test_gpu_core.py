@@ -95,3 +95,27 @@ def test_device_beam_generation_bitwise(mg, ne):
         np.testing.assert_array_equal(d.row_ptr, w.row_ptr)
         np.testing.assert_array_equal(d.col_idx, w.col_idx)
         np.testing.assert_array_equal(d.values, w.values)
+
+
+def test_binary_csr_sidecar_roundtrip(mg, tmp_path):
+    """binary CSR written from / read into device memory, exact round trip."""
+    M, D, K = mg.model_hermite(5000)
+    dK = mg.DeviceCsr.upload(K)
+    path = str(tmp_path / "K.mgcsr")
+    dK.save(path)
+    back = mg.DeviceCsr.load(path).download()
+    np.testing.assert_array_equal(back.row_ptr, K.row_ptr)
+    np.testing.assert_array_equal(back.col_idx, K.col_idx)
+    np.testing.assert_array_equal(back.values, K.values)
+    # a factor storing exact zeros is written in its download (reference) form
+    P = mg.spai_ls(mg.shifted_operator(M, D, K, 100.0), None, 0)
+    P.matrix.save(path)
+    np.testing.assert_array_equal(mg.DeviceCsr.load(path).download().values, P.matrix.download().values)
+    with open(path, "r+b") as f:
+        f.truncate(40)
+    with pytest.raises(mg.ArgumentError, match="truncated"):
+        mg.DeviceCsr.load(path)
+    bad = tmp_path / "bad.bin"
+    bad.write_bytes(b"not a csr file at all")
+    with pytest.raises(mg.ArgumentError, match="not a binary CSR"):
+        mg.DeviceCsr.load(str(bad))
