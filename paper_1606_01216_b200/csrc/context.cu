@@ -468,8 +468,11 @@ int mgpu_csr_free(mgpu_csr *a)
   if (a == nullptr)
     return MGPU_OK;
   cudaStream_t s = a->ctx ? a->ctx->stream : nullptr;
-  cudaFreeAsync(a->row_ptr, s);
-  cudaFreeAsync(a->col_idx, s);
+  if (!a->shared_structure) // shared structures are released by their last owner
+  {
+    cudaFreeAsync(a->row_ptr, s);
+    cudaFreeAsync(a->col_idx, s);
+  }
   cudaFreeAsync(a->values, s);
   delete a;
   return MGPU_OK;

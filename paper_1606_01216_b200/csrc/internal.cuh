@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <stdexcept>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -128,6 +129,9 @@ struct mgpu_csr
   bool may_hold_zeros = false; // fixed-pattern factors (LS-SPAI) may store exact zeros
   int64_t bw = -1;              // upper bound of max |i - j| over stored entries (-1: unknown)
   int64_t maxrow = -1;          // longest row (-1: unknown)
+  // set when row_ptr / col_idx belong to a structure shared by several matrices (the
+  // factors of one batched LS-SPAI build): the last owner frees it (stream-ordered)
+  std::shared_ptr<void> shared_structure;
 
   mgpu::DCsr view() const { return {row_ptr, col_idx, values}; }
 };

@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <memory>
 #include <vector>
 
 #include "internal.cuh"
@@ -655,37 +656,54 @@ std::vector<mgpu_csr *> spai_ls_shared(mgpu_ctx *ctx, int l, const mgpu_csr *con
     DCsr atv{At0->row_ptr, At0->col_idx, at_vals.as<double>()};
     DCsr kov{At0->row_ptr, At0->col_idx, ko_vals.as<double>()};
     run_ls(ctx, n, l, maxrow, pat->view(), atv, nnzA, kov, nnzA, K_old != nullptr, pt_vals.as<double>(), nnzJ);
-    // P^T (J pattern) -> P: one permutation for every factor
-    PT0 = new_csr(ctx, n, n, nnzJ);
-    MG_CUDA(cudaMemcpyAsync(PT0->row_ptr, pat->row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToDevice, s));
-    if (nnzJ > 0)
+    // P^T (J pattern) -> P: one structure and one permutation for every factor.  On A's
+    // pattern P^T has A0's CSR structure, so P has At0's and the values follow perm_t;
+    // on A^2's the J pattern is transposed once.
+    mgpu_csr *S = At0;
+    const int64_t *permP = perm_t.as<int64_t>();
+    if (sq)
     {
-      MG_CUDA(cudaMemcpyAsync(PT0->col_idx, pat->col_idx, sizeof(int32_t) * nnzJ, cudaMemcpyDeviceToDevice, s));
-      MG_CUDA(cudaMemcpyAsync(PT0->values, pt_vals.ptr, sizeof(double) * nnzJ, cudaMemcpyDeviceToDevice, s));
+      PT0 = new_csr(ctx, n, n, nnzJ);
+      MG_CUDA(cudaMemcpyAsync(PT0->row_ptr, pat->row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToDevice, s));
+      if (nnzJ > 0)
+        MG_CUDA(cudaMemcpyAsync(PT0->col_idx, pat->col_idx, sizeof(int32_t) * nnzJ, cudaMemcpyDeviceToDevice, s));
+      P0 = transpose_perm(ctx, PT0, perm_p);
+      S = P0;
+      permP = perm_p.as<int64_t>();
     }
-    P0 = transpose_perm(ctx, PT0, perm_p);
     const int64_t ba = csr_bandwidth(ctx, const_cast<mgpu_csr *>(A0));
-    const int64_t pmax = csr_max_row(ctx, P0); // every factor shares P0's stored pattern
+    const int64_t pmax = csr_max_row(ctx, S); // every factor has S's stored pattern
+    // hand S's structure to the factors (shared, freed by the last one)
+    int64_t *srp = S->row_ptr;
+    int32_t *sci = S->col_idx;
+    mgpu_ctx *owner_ctx = ctx;
+    std::shared_ptr<void> structure(srp, [owner_ctx, sci](void *rp) {
+      cudaFreeAsync(rp, owner_ctx->stream);
+      cudaFreeAsync(sci, owner_ctx->stream);
+    });
+    S->row_ptr = nullptr;
+    S->col_idx = nullptr;
     std::vector<const double *> gsrc;
     std::vector<double *> gdst;
     for (int p = 0; p < l; ++p)
     {
-      mgpu_csr *P = p == 0 ? P0 : new_csr(ctx, n, n, nnzJ);
-      if (p > 0)
-      {
-        MG_CUDA(cudaMemcpyAsync(P->row_ptr, P0->row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToDevice, s));
-        if (nnzJ > 0)
-          MG_CUDA(cudaMemcpyAsync(P->col_idx, P0->col_idx, sizeof(int32_t) * nnzJ, cudaMemcpyDeviceToDevice, s));
-        gsrc.push_back(pt_vals.as<double>() + p * nnzJ);
-        gdst.push_back(P->values);
-      }
+      auto *P = new mgpu_csr;
+      P->ctx = ctx;
+      P->nrows = n;
+      P->ncols = n;
+      P->nnz = nnzJ;
+      P->row_ptr = srp;
+      P->col_idx = sci;
+      P->shared_structure = structure;
+      out.push_back(P);
+      MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&P->values), sizeof(double) * (nnzJ > 0 ? nnzJ : 1), s));
       P->may_hold_zeros = true;
       P->bw = pattern == MGPU_PATTERN_A2 ? 2 * ba : ba;
       P->maxrow = pmax;
-      out.push_back(P);
+      gsrc.push_back(pt_vals.as<double>() + p * nnzJ);
+      gdst.push_back(P->values);
     }
-    P0 = nullptr;
-    gather_batched(ctx, static_cast<int>(gsrc.size()), nnzJ, perm_p.as<int64_t>(), gsrc.data(), gdst.data());
+    gather_batched(ctx, l, nnzJ, permP, gsrc.data(), gdst.data());
   }
   catch (...)
   {
@@ -697,6 +715,7 @@ std::vector<mgpu_csr *> spai_ls_shared(mgpu_ctx *ctx, int l, const mgpu_csr *con
     mgpu_csr_free(sq);
     throw;
   }
+  mgpu_csr_free(P0); // its structure now belongs to the factors
   mgpu_csr_free(PT0);
   mgpu_csr_free(At0);
   mgpu_csr_free(sq);
