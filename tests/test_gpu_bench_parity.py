@@ -1,0 +1,61 @@
+"""Parity at the benchmark's own workload (bench.py default = BASELINE configs[1] shape):
+Hermite beam ne = 10^4 (n = 2e4), 8 shifts log-spaced in [10, 1e4], LS-SPAI on A's pattern,
+the fixed 1000-iteration CG budget.  SURVEY.md 8(c) T2: fixed-k iterate parity (the
+device's fixed reduction trees vs the reference's serial sums, measured noise ~1e-13 at
+k = 1000), identical iteration counts / converged flags, no breakdown.  Every CG kernel
+the bench can select is checked against the same oracle solves.
+"""
+import functools
+
+import numpy as np
+import pytest
+
+from conftest import rel
+
+pytestmark = pytest.mark.gpu
+
+NE, BUDGET = 10000, 1000
+SHIFTS = [10.0 ** (1 + 3 * i / 7) for i in range(8)]
+
+
+@functools.lru_cache(maxsize=1)
+def _oracle_case():
+    from oracle import Oracle
+    orc = Oracle()
+    M, D, K = orc.hermite_generate(NE)
+    n = M.nrows
+    b = np.zeros(n)
+    b[n - 2] = 1.0
+    ops, facs, sols = [], [], []
+    for s in SHIFTS:
+        A = orc.shifted_operator(M, D, K, s)
+        P = orc.spai_ls(A, None, 0)
+        r = orc.pcg_solve(A, [P], b, rtol=1e-10, maxit=BUDGET)
+        ops.append(A)
+        facs.append(P)
+        sols.append(r)
+    return (M, D, K), ops, facs, b, sols
+
+
+@pytest.mark.parametrize("path", ["auto", "stream", "banded"])
+def test_bench_workload_iterate_parity(mg, path):
+    (M, D, K), ops, facs, b, want = _oracle_case()
+    ctx = mg.default_context()
+    ctx.set_cg_path(path)
+    try:
+        # the bench's device pipeline: assembly + batched LS-SPAI + one batched solve
+        dops = mg.shifted_operators(M, D, K, SHIFTS, ctx=ctx)
+        dfac = mg.spai_ls_batched(dops, None, mg.PATTERN_A, ctx=ctx)
+        for d, a in zip(dops, ops):
+            np.testing.assert_array_equal(d.download().values, a.values)  # bitwise assembly
+        for f, p in zip(dfac, facs):
+            np.testing.assert_array_equal(f.matrix.download().values, p.values)  # bitwise LS-SPAI
+        res = mg.cg_solve_batched(dops, [[f.matrix] for f in dfac], b, rtol=1e-10, maxit=BUDGET, ctx=ctx)
+        if path == "auto":
+            assert ctx.last_cg_path == "cluster"
+        for r, w in zip(res, want):
+            assert int(r.iterations[0]) == w["iterations"] == BUDGET
+            assert bool(r.converged[0]) == w["converged"]
+            assert rel(r.X[:, 0], w["solution"]) < 1e-8
+    finally:
+        ctx.set_cg_path("auto")
