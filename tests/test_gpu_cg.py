@@ -191,3 +191,18 @@ def test_zero_rhs(mg, oracle):
     got = mg.pcg_solve(K, [], np.zeros(100))
     assert got["iterations"] == 0 and got["converged"]
     np.testing.assert_array_equal(got["solution"], 0.0)
+
+
+@pytest.mark.parametrize("m", [2, 4])
+def test_multi_rhs_restart_plain(mg, oracle, m):
+    """P = I with m right-hand sides at an rtol near the FP64 floor: the true-residual confirm /
+    restart branch per column (krylov.cpp:77-103).  On the stream kernel m = 2 runs the deferred
+    x~ update (folded into phase A, the check pass adds the pending alpha d), m = 4 does not."""
+    M, D, K = oracle.chain_generate(1200, consistent=True, stiffness_scale=1.0)
+    A = oracle.shifted_operator(M, D, K, 0.5)
+    B = np.random.default_rng(m).standard_normal((1200, m))
+    want = oracle.block_solve(A, [], B, rtol=1e-15, maxit=400)
+    got = mg.block_solve(A, [], B, rtol=1e-15, maxit=400)
+    assert got.all_converged == want["all_converged"]
+    assert rel(got.X, want["X"]) < 1e-8
+    assert np.all(np.abs(np.asarray(got.iterations) - np.asarray(want["iterations"])) <= 2)
