@@ -197,22 +197,6 @@ __device__ __forceinline__ void warp_inbox_total(const double *inbox, int nv, in
     out[k] = v[k];
 }
 
-// After cluster.sync(): every warp forms tot[k] (k < nv) itself from the cs
-// remote slots with a fixed butterfly, so no CTA barrier / broadcast is needed.
-__device__ __forceinline__ void warp_cluster_total(cgrp::cluster_group &cl, const double *slot, int nv, int cs,
-                                                   double *out)
-{
-  const int lane = threadIdx.x & 31;
-  for (int k = 0; k < nv; ++k)
-  {
-    double v = lane < cs ? cl.map_shared_rank(slot, lane)[k] : 0.0;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1)
-      v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
-    out[k] = v;
-  }
-}
-
 // After cluster.sync(): tot[k] = sum over ranks (fixed order) of slot[k].
 __device__ __forceinline__ void cluster_total(cgrp::cluster_group &cl, ClShared &sh, double *slot, int nv, int cs)
 {
