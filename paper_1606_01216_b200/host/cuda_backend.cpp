@@ -281,6 +281,75 @@ BlockSolveResult block_solve(Device &dev, const SparseMatrix &A, const Precondit
   return solve_points(dev.ctx(), {dA.get()}, ch, static_cast<int>(ch.size()), B, rtol, maxit)[0];
 }
 
+std::vector<double> SparseApply::operator()(std::span<const double> v) const { return spmv(*A, v); }
+std::vector<double> ChainApply::operator()(std::span<const double> v) const { return mor::chain_apply(*chain, v); }
+
+LinearOperator sparse_operator(const SparseMatrix &A)
+{
+  if (A.nrows != A.ncols)
+    throw ArgumentError("LinearOperator::from_sparse: matrix must be square");
+  return {SparseApply{&A}, A.nrows};
+}
+
+LinearOperator chain_operator(const PreconditionerChain &chain, std::int64_t n)
+{
+  if (chain.empty())
+    return identity_operator(n);
+  return {ChainApply{&chain}, n};
+}
+
+LinearOperator identity_operator(std::int64_t n) { return {IdentityApply{}, n}; }
+
+namespace
+{
+// The operator pair as device inputs: A must be a matrix; P a matrix, chain or identity.
+struct DeviceOperands
+{
+  const SparseMatrix *A = nullptr;
+  PreconditionerChain chain; // copy of the factors (or the single matrix P)
+};
+
+DeviceOperands resolve(const LinearOperator &A, const LinearOperator &P, const char *who)
+{
+  DeviceOperands d;
+  if (const auto *sa = A.apply.target<SparseApply>())
+    d.A = sa->A;
+  else
+    throw ArgumentError(std::string(who) + ": operator not device-resident (build A with mor::cuda::sparse_operator)");
+  if (P.apply.target<IdentityApply>())
+    return d;
+  if (const auto *ca = P.apply.target<ChainApply>())
+    d.chain = *ca->chain;
+  else if (const auto *sp = P.apply.target<SparseApply>())
+  {
+    SpaiFactor f;
+    f.matrix = *sp->A;
+    d.chain.push_newest(std::move(f));
+  }
+  else
+    throw ArgumentError(std::string(who) +
+                        ": preconditioner not device-resident (use mor::cuda::chain_operator / sparse_operator / "
+                        "identity_operator)");
+  if (P.dim != A.dim)
+    throw ArgumentError(std::string(who) + ": dimension mismatch");
+  return d;
+}
+} // namespace
+
+SolveReport pcg_solve(Device &dev, const LinearOperator &A, const LinearOperator &P, std::span<const double> b,
+                      double rtol, std::int64_t maxit)
+{
+  const DeviceOperands d = resolve(A, P, "pcg_solve");
+  return pcg_solve(dev, *d.A, d.chain, b, rtol, maxit);
+}
+
+BlockSolveResult block_solve(Device &dev, const LinearOperator &A, const LinearOperator &P, const DenseMatrix &B,
+                             double rtol, std::int64_t maxit)
+{
+  const DeviceOperands d = resolve(A, P, "block_solve");
+  return block_solve(dev, *d.A, d.chain, B, rtol, maxit);
+}
+
 QrResult thin_qr(Device &dev, const DenseMatrix &A, double rank_tol)
 {
   if (A.nrows < A.ncols)

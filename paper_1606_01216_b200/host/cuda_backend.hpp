@@ -99,6 +99,33 @@ SolveReport pcg_solve(Device &dev, const SparseMatrix &A, const PreconditionerCh
 BlockSolveResult block_solve(Device &dev, const SparseMatrix &A, const PreconditionerChain &P, const DenseMatrix &B,
                              double rtol, std::int64_t maxit);
 
+// ---- LinearOperator overloads (krylov.hpp:41-56 signatures).  The reference's own
+// factories return unnamed lambdas a device cannot see into, so operators for the device
+// are built with these factories instead: ordinary LinearOperators (they run unchanged in
+// the reference's pcg_solve) whose callables are the named types below, recovered here
+// with std::function::target<T>().  Any other callable -> ArgumentError.
+struct SparseApply
+{
+  const SparseMatrix *A;
+  std::vector<double> operator()(std::span<const double> v) const;
+};
+struct ChainApply
+{
+  const PreconditionerChain *chain;
+  std::vector<double> operator()(std::span<const double> v) const;
+};
+struct IdentityApply
+{
+  std::vector<double> operator()(std::span<const double> v) const { return {v.begin(), v.end()}; }
+};
+LinearOperator sparse_operator(const SparseMatrix &A);                             // from_sparse (krylov.cpp:19-26)
+LinearOperator chain_operator(const PreconditionerChain &chain, std::int64_t n);  // airga.cpp:176-177
+LinearOperator identity_operator(std::int64_t n);                                  // identity (krylov.cpp:14-17)
+SolveReport pcg_solve(Device &dev, const LinearOperator &A, const LinearOperator &P, std::span<const double> b,
+                      double rtol, std::int64_t maxit);
+BlockSolveResult block_solve(Device &dev, const LinearOperator &A, const LinearOperator &P, const DenseMatrix &B,
+                             double rtol, std::int64_t maxit);
+
 // Global Arnoldi + projection
 QrResult thin_qr(Device &dev, const DenseMatrix &A, double rank_tol = 1e-12);                 // dense.hpp:69
 ReducedSystem project_reduce(Device &dev, const SecondOrderSystem &sys, const OrthonormalBasis &basis); // airga.hpp:183

@@ -134,6 +134,26 @@ int main()
     dchain = std::max(dchain, std::fabs(ca[i] - cb[i]));
   if (dchain != 0.0) // same factors, in-order SpMV: bitwise
     ++failures;
+  // LinearOperator overloads: the same named-functor operators through the reference's
+  // pcg_solve (CPU) and the device; foreign callables are refused
+  {
+    const LinearOperator Aop = cuda::sparse_operator(A2), Pop = cuda::chain_operator(chr, 2000);
+    const SolveReport lr = pcg_solve(Aop, Pop, v, 1e-10, 20000);
+    const SolveReport lg = cuda::pcg_solve(dev, Aop, Pop, v, 1e-10, 20000);
+    double dl = 0.0, nl = 0.0;
+    for (std::size_t i = 0; i < lr.solution.size(); ++i)
+    {
+      dl = std::max(dl, std::fabs(lr.solution[i] - lg.solution[i]));
+      nl = std::max(nl, std::fabs(lr.solution[i]));
+    }
+    if (!(dl <= 1e-8 * nl) || lr.converged != lg.converged)
+      ++failures;
+    bool refused = false;
+    try { (void)cuda::pcg_solve(dev, LinearOperator::from_sparse(A2), Pop, v, 1e-10, 100); }
+    catch (const ArgumentError &) { refused = true; }
+    if (!refused)
+      ++failures;
+  }
   // chain_quality: the reference's probe stream, device SpMM + deterministic sums
   const double qr_ref = chain_quality(chr, A2, 8, 42), qr_gpu = cuda::chain_quality(dev, chr, A2, 8, 42);
   const double dq = std::fabs(qr_ref - qr_gpu) / std::fabs(qr_ref);
