@@ -145,15 +145,15 @@ __global__ void __launch_bounds__(kQrTB) qr_factor(QrArgs a)
     __syncthreads();
     // ---- y_j -= s_j v over this block's rows (dense.cpp:188)
     const int64_t lo = max(r0, static_cast<int64_t>(k));
-    const int64_t rows = r1 > lo ? r1 - lo : 0;
-    const int64_t cnt = rows * (n - k - 1);
-    for (int64_t e = threadIdx.x; e < cnt; e += kQrTB)
+    for (int j = k + 1; j < n; ++j) // column-outer: no per-element index division
     {
-      const int j = k + 1 + static_cast<int>(e / rows);
-      const int64_t i = lo + e % rows;
-      const double xi = i == k ? v0 : x[i];
       double *y = a.W + static_cast<int64_t>(j) * m;
-      y[i] = __dadd_rn(y[i], __dmul_rn(-sj[j], xi));
+      const double ns = -sj[j];
+      for (int64_t i = lo + threadIdx.x; i < r1; i += kQrTB)
+      {
+        const double xi = i == k ? v0 : x[i];
+        y[i] = __dadd_rn(y[i], __dmul_rn(ns, xi));
+      }
     }
     __syncthreads();
     if (k >= r0 && k < r1 && threadIdx.x == 0)
@@ -175,11 +175,11 @@ __global__ void __launch_bounds__(kQrTB) qr_form_q(QrArgs a)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double *part = a.part + static_cast<int64_t>(b) * (n + 1);
   // Q = E on the kept columns, zero elsewhere
-  for (int64_t e = threadIdx.x; e < (r1 - r0) * n; e += kQrTB)
+  for (int j = 0; j < n; ++j)
   {
-    const int j = static_cast<int>(e / (r1 - r0));
-    const int64_t i = r0 + e % (r1 - r0);
-    a.Q[static_cast<int64_t>(j) * m + i] = (i == j && a.diag[j] != 0.0) ? 1.0 : 0.0;
+    const bool keep = a.diag[j] != 0.0;
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += kQrTB)
+      a.Q[static_cast<int64_t>(j) * m + i] = (i == j && keep) ? 1.0 : 0.0;
   }
   grid.sync();
   for (int k = n - 1; k >= 0; --k)
@@ -211,16 +211,14 @@ __global__ void __launch_bounds__(kQrTB) qr_form_q(QrArgs a)
       sj[j] = __dmul_rn(tk, d);
     }
     __syncthreads();
-    const int64_t rows = r1 > lo ? r1 - lo : 0;
-    const int64_t cnt = rows * (n - k);
-    for (int64_t e = threadIdx.x; e < cnt; e += kQrTB)
+    for (int j = k; j < n; ++j)
     {
-      const int j = k + static_cast<int>(e / rows);
       if (a.diag[j] == 0.0)
         continue;
-      const int64_t i = lo + e % rows;
       double *q = a.Q + static_cast<int64_t>(j) * m;
-      q[i] = __dadd_rn(q[i], __dmul_rn(-sj[j], v[i]));
+      const double ns = -sj[j];
+      for (int64_t i = lo + threadIdx.x; i < r1; i += kQrTB)
+        q[i] = __dadd_rn(q[i], __dmul_rn(ns, v[i]));
     }
     grid.sync();
   }
