@@ -19,7 +19,9 @@
 #include <cooperative_groups.h>
 #include <cublas_v2.h>
 
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -65,6 +67,7 @@ struct QrArgs
   double *diag, *tau;
   double tol;
   double *part; // [G][n + 1]
+  int k0, k1;   // qr_factor: the panel [k0, k1); reflectors update columns < k1 only
 };
 
 // Factorisation: dense.cpp:165-190.
@@ -79,7 +82,7 @@ __global__ void __launch_bounds__(kQrTB) qr_factor(QrArgs a)
   const int64_t r0 = m * b / G, r1 = m * (b + 1) / G; // this block's row slab
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double *part = a.part + static_cast<int64_t>(b) * (n + 1);
-  for (int k = 0; k < n; ++k)
+  for (int k = a.k0; k < a.k1; ++k)
   {
     double *x = a.W + static_cast<int64_t>(k) * m;
     // ---- tail norm over rows > k
@@ -121,7 +124,7 @@ __global__ void __launch_bounds__(kQrTB) qr_factor(QrArgs a)
       a.tau[k] = tk;
     }
     // ---- dots <v, y_j> for j > k over this block's rows (v_k = v0)
-    for (int j = k + 1 + warp; j < n; j += kQrTB / 32)
+    for (int j = k + 1 + warp; j < a.k1; j += kQrTB / 32)
     {
       const double *y = a.W + static_cast<int64_t>(j) * m;
       double d = 0.0;
@@ -135,7 +138,7 @@ __global__ void __launch_bounds__(kQrTB) qr_factor(QrArgs a)
         part[1 + j] = d;
     }
     grid.sync();
-    for (int j = k + 1 + threadIdx.x; j < n; j += kQrTB)
+    for (int j = k + 1 + threadIdx.x; j < a.k1; j += kQrTB)
     {
       double d = 0.0;
       for (int bb = 0; bb < G; ++bb)
@@ -145,7 +148,7 @@ __global__ void __launch_bounds__(kQrTB) qr_factor(QrArgs a)
     __syncthreads();
     // ---- y_j -= s_j v over this block's rows (dense.cpp:188)
     const int64_t lo = max(r0, static_cast<int64_t>(k));
-    for (int j = k + 1; j < n; ++j) // column-outer: no per-element index division
+    for (int j = k + 1; j < a.k1; ++j) // column-outer: no per-element index division
     {
       double *y = a.W + static_cast<int64_t>(j) * m;
       const double ns = -sj[j];
@@ -248,6 +251,53 @@ __global__ void qr_sign_q(int64_t m, int n, const double *__restrict__ diag, dou
     Q[e] = __dmul_rn(-1.0, Q[e]);
 }
 
+// Panel p = columns [j0, j0 + jb): V (rows j0..m-1, jb columns, ld mv = m - j0) with the
+// Householder vectors as qr_factor leaves them (v_k(k) = v0 stored, rows above k zeroed).
+__global__ void qr_panel_v(int64_t m, int64_t j0, int jb, const double *__restrict__ W, double *__restrict__ V)
+{
+  const int64_t mv = m - j0;
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= mv * jb)
+    return;
+  const int c = static_cast<int>(t / mv);
+  const int64_t i = t - static_cast<int64_t>(c) * mv; // row j0 + i
+  V[t] = i < c ? 0.0 : W[(j0 + c) * m + j0 + i];
+}
+
+// Compact WY (forward, columnwise): H_0 ... H_{jb-1} = I - V T V^T with T upper triangular,
+// T_kk = tau_k, T(0:k, k) = -tau_k T(0:k, 0:k) G(0:k, k), G = V^T V.  One warp.
+__global__ void qr_panel_t(int jb, const double *__restrict__ G, const double *__restrict__ tau, double *__restrict__ T)
+{
+  const int i = threadIdx.x;
+  for (int e = i; e < jb * jb; e += 32)
+    T[e] = 0.0;
+  __syncwarp();
+  for (int k = 0; k < jb; ++k)
+  {
+    const double tk = tau[k];
+    if (i < k)
+    {
+      double acc = 0.0;
+      for (int l = i; l < k; ++l)
+        acc = __dadd_rn(acc, __dmul_rn(T[l * jb + i], G[k * jb + l]));
+      T[k * jb + i] = __dmul_rn(-tk, acc);
+    }
+    if (i == 0)
+      T[k * jb + k] = tk;
+    __syncwarp();
+  }
+}
+
+// Q = E on the kept columns (diag != 0), zero elsewhere (dense.cpp:207-212).
+__global__ void qr_init_q(int64_t m, int n, const double *__restrict__ diag, double *__restrict__ Q)
+{
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= m * n)
+    return;
+  const int64_t j = t / m, i = t - j * m;
+  Q[t] = (i == j && diag[j] != 0.0) ? 1.0 : 0.0;
+}
+
 __global__ void square_all(int64_t count, const double *__restrict__ x, double *__restrict__ out)
 {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -305,15 +355,21 @@ cublasHandle_t blas(mgpu_ctx *ctx)
   return h;
 }
 
-void dgemm(mgpu_ctx *ctx, cublasOperation_t ta, cublasOperation_t tb, int64_t M, int64_t N, int64_t K,
-           const double *A, int64_t lda, const double *B, int64_t ldb, double *C, int64_t ldc)
+void dgemm_ab(mgpu_ctx *ctx, cublasOperation_t ta, cublasOperation_t tb, int64_t M, int64_t N, int64_t K,
+              double alpha, const double *A, int64_t lda, const double *B, int64_t ldb, double beta, double *C,
+              int64_t ldc)
 {
   if (M == 0 || N == 0)
     return;
-  const double one = 1.0, zero = 0.0;
-  if (cublasDgemm_64(blas(ctx), ta, tb, M, N, K, &one, A, lda, B, ldb, &zero, C, ldc) != CUBLAS_STATUS_SUCCESS)
+  if (cublasDgemm_64(blas(ctx), ta, tb, M, N, K, &alpha, A, lda, B, ldb, &beta, C, ldc) != CUBLAS_STATUS_SUCCESS)
     throw Error(MGPU_ERR_CUDA, "cublasDgemm failed");
   count_launch(ctx);
+}
+
+void dgemm(mgpu_ctx *ctx, cublasOperation_t ta, cublasOperation_t tb, int64_t M, int64_t N, int64_t K,
+           const double *A, int64_t lda, const double *B, int64_t ldb, double *C, int64_t ldc)
+{
+  dgemm_ab(ctx, ta, tb, M, N, K, 1.0, A, lda, B, ldb, 0.0, C, ldc);
 }
 
 // Device staging of a `where` buffer: device pointers pass through, host ones are copied.
@@ -382,14 +438,87 @@ int mgpu_thin_qr(mgpu_ctx *ctx, int64_t rows, int64_t cols, const double *A, dou
       const int G = ctx->num_sms;
       DBuf part(sizeof(double) * static_cast<size_t>(G) * (cols + 1), s);
       QrArgs a{rows, static_cast<int>(cols), W.as<double>(), Qd.as<double>(), diag.as<double>(), tau.as<double>(),
-               rank_tol * (anorm > 0.0 ? anorm : 1.0), part.as<double>()};
+               rank_tol * (anorm > 0.0 ? anorm : 1.0), part.as<double>(), 0, static_cast<int>(cols)};
       void *args[] = {&a};
-      MG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void *>(qr_factor), dim3(static_cast<unsigned>(G)),
-                                          dim3(kQrTB), args, 0, s));
-      check_launch(ctx, "qr_factor");
-      MG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void *>(qr_form_q), dim3(static_cast<unsigned>(G)),
-                                          dim3(kQrTB), args, 0, s));
-      check_launch(ctx, "qr_form_q");
+      if (std::getenv("MGPU_QR_UNBLOCKED")) // diagnostics: the column-by-column reference schedule
+      {
+        MG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void *>(qr_factor), dim3(static_cast<unsigned>(G)),
+                                            dim3(kQrTB), args, 0, s));
+        check_launch(ctx, "qr_factor");
+        MG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void *>(qr_form_q), dim3(static_cast<unsigned>(G)),
+                                            dim3(kQrTB), args, 0, s));
+        check_launch(ctx, "qr_form_q");
+      }
+      else
+      {
+        // Blocked (compact WY): the panel [j0, j0 + jb) is factored column by column (same
+        // rank test and reflectors as the reference), then the trailing block gets all jb
+        // reflectors at once, C -= V (T^T (V^T C)); Q applies I - V T V^T panel by panel in
+        // reverse.  Same H_k, applied as GEMMs: rounding differs from the reference's
+        // reflector-at-a-time order at the 1e-15 level.
+        constexpr int kPanel = 32;
+        const int ncol = static_cast<int>(cols);
+        const int npan = (ncol + kPanel - 1) / kPanel;
+        DBuf Tall(sizeof(double) * static_cast<size_t>(npan) * kPanel * kPanel, s);
+        DBuf Vp(sizeof(double) * static_cast<size_t>(rows) * kPanel, s);
+        DBuf Gm(sizeof(double) * kPanel * kPanel, s);
+        DBuf Wt(sizeof(double) * static_cast<size_t>(kPanel) * ncol, s), Wt2(sizeof(double) * static_cast<size_t>(kPanel) * ncol, s);
+        double *Wm = W.as<double>();
+        auto panel_vt = [&](int pi, bool build_t) {
+          const int64_t j0 = static_cast<int64_t>(pi) * kPanel;
+          const int jb = static_cast<int>(std::min<int64_t>(kPanel, cols - j0));
+          const int64_t mv = rows - j0;
+          qr_panel_v<<<blocks_for(mv * jb), kThreads, 0, s>>>(rows, j0, jb, Wm, Vp.as<double>());
+          check_launch(ctx, "qr_panel_v");
+          if (build_t)
+          {
+            dgemm(ctx, CUBLAS_OP_T, CUBLAS_OP_N, jb, jb, mv, Vp.as<double>(), mv, Vp.as<double>(), mv, Gm.as<double>(),
+                  jb);
+            qr_panel_t<<<1, 32, 0, s>>>(jb, Gm.as<double>(), tau.as<double>() + j0,
+                                        Tall.as<double>() + static_cast<size_t>(pi) * kPanel * kPanel);
+            check_launch(ctx, "qr_panel_t");
+          }
+        };
+        for (int pi = 0; pi < npan; ++pi)
+        {
+          const int64_t j0 = static_cast<int64_t>(pi) * kPanel;
+          const int jb = static_cast<int>(std::min<int64_t>(kPanel, cols - j0));
+          a.k0 = static_cast<int>(j0);
+          a.k1 = static_cast<int>(j0 + jb);
+          MG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void *>(qr_factor), dim3(static_cast<unsigned>(G)),
+                                              dim3(kQrTB), args, 0, s));
+          check_launch(ctx, "qr_factor");
+          const int64_t nc = cols - j0 - jb;
+          if (nc <= 0)
+            continue;
+          panel_vt(pi, true);
+          const int64_t mv = rows - j0;
+          const double *T = Tall.as<double>() + static_cast<size_t>(pi) * kPanel * kPanel;
+          double *C = Wm + (j0 + jb) * rows + j0;
+          dgemm(ctx, CUBLAS_OP_T, CUBLAS_OP_N, jb, nc, mv, Vp.as<double>(), mv, C, rows, Wt.as<double>(), jb);
+          dgemm(ctx, CUBLAS_OP_T, CUBLAS_OP_N, jb, nc, jb, T, jb, Wt.as<double>(), jb, Wt2.as<double>(), jb);
+          dgemm_ab(ctx, CUBLAS_OP_N, CUBLAS_OP_N, mv, nc, jb, -1.0, Vp.as<double>(), mv, Wt2.as<double>(), jb, 1.0, C,
+                   rows);
+        }
+        // T of the last panel (not needed for a trailing update, needed for Q)
+        panel_vt(npan - 1, true);
+        qr_init_q<<<blocks_for(total), kThreads, 0, s>>>(rows, ncol, diag.as<double>(), Qd.as<double>());
+        check_launch(ctx, "qr_init_q");
+        for (int pi = npan - 1; pi >= 0; --pi)
+        {
+          const int64_t j0 = static_cast<int64_t>(pi) * kPanel;
+          const int jb = static_cast<int>(std::min<int64_t>(kPanel, cols - j0));
+          const int64_t mv = rows - j0, nq = cols - j0;
+          if (pi != npan - 1)
+            panel_vt(pi, false);
+          const double *T = Tall.as<double>() + static_cast<size_t>(pi) * kPanel * kPanel;
+          double *Cq = Qd.as<double>() + j0 * rows + j0;
+          dgemm(ctx, CUBLAS_OP_T, CUBLAS_OP_N, jb, nq, mv, Vp.as<double>(), mv, Cq, rows, Wt.as<double>(), jb);
+          dgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, jb, nq, jb, T, jb, Wt.as<double>(), jb, Wt2.as<double>(), jb);
+          dgemm_ab(ctx, CUBLAS_OP_N, CUBLAS_OP_N, mv, nq, jb, -1.0, Vp.as<double>(), mv, Wt2.as<double>(), jb, 1.0, Cq,
+                   rows);
+        }
+      }
       qr_form_r<<<blocks_for(cols * cols), kThreads, 0, s>>>(rows, static_cast<int>(cols), W.as<double>(),
                                                              diag.as<double>(), Rd.as<double>());
       check_launch(ctx, "qr_form_r");
