@@ -162,21 +162,6 @@ __device__ __forceinline__ void cta_sum_push(ClShared &sh, double (&v)[NV], int 
   }
 }
 
-// After the barrier: tot[k] = sum over ranks (fixed butterfly) of the local inbox
-// (every lane ends with the total: all five levels are needed).
-__device__ __forceinline__ void warp_inbox_total(const double *inbox, int nv, int cs, double *out)
-{
-  const int lane = threadIdx.x & 31;
-  for (int k = 0; k < nv; ++k)
-  {
-    double v = lane < cs ? inbox[k * kCMaxCS + lane] : 0.0;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1)
-      v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
-    out[k] = v;
-  }
-}
-
 template <int NV>
 __device__ __forceinline__ void warp_inbox_total(const double *inbox, int nv, int cs, double (&out)[NV])
 {
@@ -379,31 +364,9 @@ __device__ void load_ell(DCsr M, int64_t r0, int64_t r1, int64_t n, int E, doubl
   }
 }
 
-// Entry-major ELL repack (v[t * rows + q]): consecutive rows -> consecutive
-// shared-memory words, so a warp's SpMV loads are bank-conflict free.
-__device__ void load_ell_em(DCsr M, int64_t r0, int64_t r1, int64_t n, int E, double *v, signed char *o, int TBn)
-{
-  const int64_t rows = r1 - r0;
-  for (int64_t q = threadIdx.x; q < rows; q += TBn)
-  {
-    const int64_t i = r0 + q;
-    int64_t k = 0, e = 0;
-    if (i >= 0 && i < n)
-    {
-      k = M.rp[i];
-      e = M.rp[i + 1];
-    }
-    for (int t = 0; t < E; ++t)
-    {
-      const bool has = k + t < e;
-      v[t * rows + q] = has ? M.v[k + t] : 0.0; // padding after the row's entries adds +0 last
-      o[t * rows + q] = has ? static_cast<signed char>(M.ci[k + t] - i) : 0;
-    }
-  }
-}
-
-// Same, with the row's int8 column offsets packed into one 64-bit word (E <= 8):
-// one shared-memory load per row instead of E byte loads.
+// Entry-major ELL repack (v[t * rows + q]): consecutive rows -> consecutive shared-memory
+// words, so a warp's SpMV loads are bank-conflict free; the row's int8 column offsets are
+// packed into one 64-bit word (E <= 8): one offset load per row instead of E byte loads.
 __device__ void load_ell_em_packed(DCsr M, int64_t r0, int64_t r1, int64_t n, int E, double *v,
                                    unsigned long long *o, int TBn)
 {

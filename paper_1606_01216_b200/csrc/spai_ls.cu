@@ -98,13 +98,6 @@ __global__ void square_fill(int64_t n, DCsr A, const int64_t *rp, int32_t *ci)
     ci[rp[i] + u] = buf[u];
 }
 
-__global__ void max_row_len(int64_t n, const int64_t *rp, int *out)
-{
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n)
-    atomicMax(out, static_cast<int>(rp[i + 1] - rp[i]));
-}
-
 // ---------------------------------------------------------------- LS columns
 //
 // One GROUP of G lanes per column j (G = 8, 16 or 32 = the |J| envelope, so a
