@@ -27,9 +27,9 @@ mgpu_csr *new_csr(mgpu_ctx *ctx, int64_t nrows, int64_t ncols, int64_t nnz)
   a->nrows = nrows;
   a->ncols = ncols;
   a->nnz = nnz;
-  MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&a->row_ptr), sizeof(int64_t) * (nrows + 1), ctx->stream));
-  MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&a->col_idx), sizeof(int32_t) * (nnz > 0 ? nnz : 1), ctx->stream));
-  MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&a->values), sizeof(double) * (nnz > 0 ? nnz : 1), ctx->stream));
+  MG_CUDA(mg_malloc(reinterpret_cast<void **>(&a->row_ptr), sizeof(int64_t) * (nrows + 1), ctx->stream));
+  MG_CUDA(mg_malloc(reinterpret_cast<void **>(&a->col_idx), sizeof(int32_t) * (nnz > 0 ? nnz : 1), ctx->stream));
+  MG_CUDA(mg_malloc(reinterpret_cast<void **>(&a->values), sizeof(double) * (nnz > 0 ? nnz : 1), ctx->stream));
   return a;
 }
 

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstdio>
 #include <stdexcept>
 #include <memory>
@@ -52,6 +53,24 @@ struct Error : std::runtime_error
   } while (0)
 
 // Device buffer owned by RAII (cudaMallocAsync on the context stream).
+// Every device allocation of the library.  MGPU_POISON=1 (diagnostics) fills fresh memory
+// with 0xFF bytes (a NaN pattern) so a read of never-written memory cannot pass silently.
+inline bool mg_poison_enabled()
+{
+  static const bool on = [] {
+    const char *e = std::getenv("MGPU_POISON");
+    return e != nullptr && e[0] == '1';
+  }();
+  return on;
+}
+inline cudaError_t mg_malloc(void **p, size_t bytes, cudaStream_t s)
+{
+  const cudaError_t e = cudaMallocAsync(p, bytes, s);
+  if (e == cudaSuccess && bytes > 0 && mg_poison_enabled())
+    return cudaMemsetAsync(*p, 0xff, bytes, s);
+  return e;
+}
+
 struct DBuf
 {
   void *ptr = nullptr;
@@ -61,7 +80,7 @@ struct DBuf
   DBuf(size_t n, cudaStream_t s) : bytes(n), stream(s)
   {
     if (n > 0)
-      MG_CUDA(cudaMallocAsync(&ptr, n, s));
+      MG_CUDA(mg_malloc(&ptr, n, s));
   }
   DBuf(const DBuf &) = delete;
   DBuf &operator=(const DBuf &) = delete;

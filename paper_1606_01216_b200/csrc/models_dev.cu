@@ -102,7 +102,7 @@ mgpu_csr *beam_matrix(mgpu_ctx *ctx, int64_t ne, int which, const BeamCoef &c)
   A->ncols = n;
   try
   {
-    MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&A->row_ptr), sizeof(int64_t) * (n + 1), s));
+    MG_CUDA(mg_malloc(reinterpret_cast<void **>(&A->row_ptr), sizeof(int64_t) * (n + 1), s));
     beam_rows<false><<<blocks_for(n), kThreads, 0, s>>>(ne, which, c, A->row_ptr, nullptr, nullptr);
     check_launch(ctx, "beam_rows<count>");
     size_t tmp = 0;
@@ -114,8 +114,8 @@ mgpu_csr *beam_matrix(mgpu_ctx *ctx, int64_t ne, int which, const BeamCoef &c)
     MG_CUDA(cudaMemcpyAsync(&nnz, A->row_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     MG_CUDA(cudaStreamSynchronize(s));
     A->nnz = nnz;
-    MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&A->col_idx), sizeof(int32_t) * (nnz > 0 ? nnz : 1), s));
-    MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&A->values), sizeof(double) * (nnz > 0 ? nnz : 1), s));
+    MG_CUDA(mg_malloc(reinterpret_cast<void **>(&A->col_idx), sizeof(int32_t) * (nnz > 0 ? nnz : 1), s));
+    MG_CUDA(mg_malloc(reinterpret_cast<void **>(&A->values), sizeof(double) * (nnz > 0 ? nnz : 1), s));
     beam_rows<true><<<blocks_for(n), kThreads, 0, s>>>(ne, which, c, A->row_ptr, A->col_idx, A->values);
     check_launch(ctx, "beam_rows<fill>");
     A->bw = 3;     // |i - j| <= 3 by construction

@@ -522,7 +522,7 @@ mgpu_csr *pattern_square(mgpu_ctx *ctx, const mgpu_csr *A)
   S->ctx = ctx;
   S->nrows = n;
   S->ncols = A->ncols;
-  MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&S->row_ptr), sizeof(int64_t) * (n + 1), ctx->stream));
+  MG_CUDA(mg_malloc(reinterpret_cast<void **>(&S->row_ptr), sizeof(int64_t) * (n + 1), ctx->stream));
   DBuf ovf(sizeof(int), ctx->stream);
   MG_CUDA(cudaMemsetAsync(ovf.ptr, 0, sizeof(int), ctx->stream));
   MG_CUDA(cudaMemsetAsync(S->row_ptr, 0, sizeof(int64_t), ctx->stream));
@@ -547,8 +547,8 @@ mgpu_csr *pattern_square(mgpu_ctx *ctx, const mgpu_csr *A)
     throw Error(MGPU_ERR_UNSUPPORTED, "spai_ls: A*A pattern row longer than 128 entries");
   }
   S->nnz = nnz;
-  MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&S->col_idx), sizeof(int32_t) * (nnz > 0 ? nnz : 1), ctx->stream));
-  MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&S->values), sizeof(double) * (nnz > 0 ? nnz : 1), ctx->stream));
+  MG_CUDA(mg_malloc(reinterpret_cast<void **>(&S->col_idx), sizeof(int32_t) * (nnz > 0 ? nnz : 1), ctx->stream));
+  MG_CUDA(mg_malloc(reinterpret_cast<void **>(&S->values), sizeof(double) * (nnz > 0 ? nnz : 1), ctx->stream));
   if (n > 0)
   {
     square_fill<<<blocks_for(n), kThreads, 0, ctx->stream>>>(n, A->view(), S->row_ptr, S->col_idx);
@@ -689,7 +689,7 @@ std::vector<mgpu_csr *> spai_ls_shared(mgpu_ctx *ctx, int l, const mgpu_csr *con
       P->col_idx = sci;
       P->shared_structure = structure;
       out.push_back(P);
-      MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&P->values), sizeof(double) * (nnzJ > 0 ? nnzJ : 1), s));
+      MG_CUDA(mg_malloc(reinterpret_cast<void **>(&P->values), sizeof(double) * (nnzJ > 0 ? nnzJ : 1), s));
       P->may_hold_zeros = true;
       P->bw = pattern == MGPU_PATTERN_A2 ? 2 * ba : ba;
       P->maxrow = pmax;

@@ -352,7 +352,7 @@ mgpu_csr *mr_build(mgpu_ctx *ctx, const mgpu_csr *K, const mgpu_csr *rhs_src, do
     PT->ctx = ctx;
     PT->nrows = n;
     PT->ncols = n;
-    MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&PT->row_ptr), sizeof(int64_t) * (n + 1), s));
+    MG_CUDA(mg_malloc(reinterpret_cast<void **>(&PT->row_ptr), sizeof(int64_t) * (n + 1), s));
     MG_CUDA(cudaMemcpyAsync(PT->row_ptr, count.ptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToDevice, s));
     if (n > 0)
     {
@@ -369,8 +369,8 @@ mgpu_csr *mr_build(mgpu_ctx *ctx, const mgpu_csr *K, const mgpu_csr *rhs_src, do
     MG_CUDA(cudaStreamSynchronize(s));
     PT->nnz = nnz;
     PT->bw = hpbw;
-    MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&PT->col_idx), sizeof(int32_t) * (nnz > 0 ? nnz : 1), s));
-    MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&PT->values), sizeof(double) * (nnz > 0 ? nnz : 1), s));
+    MG_CUDA(mg_malloc(reinterpret_cast<void **>(&PT->col_idx), sizeof(int32_t) * (nnz > 0 ? nnz : 1), s));
+    MG_CUDA(mg_malloc(reinterpret_cast<void **>(&PT->values), sizeof(double) * (nnz > 0 ? nnz : 1), s));
     a.offset = PT->row_ptr;
     a.out_rows = PT->col_idx;
     a.out_vals = PT->values;

@@ -380,7 +380,7 @@ mgpu_csr *mr_build_sequential(mgpu_ctx *ctx, const mgpu_csr *K, const mgpu_csr *
     P->ctx = ctx;
     P->nrows = n;
     P->ncols = n;
-    MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&P->row_ptr), sizeof(int64_t) * (n + 1), s));
+    MG_CUDA(mg_malloc(reinterpret_cast<void **>(&P->row_ptr), sizeof(int64_t) * (n + 1), s));
     MG_CUDA(cudaMemsetAsync(P->row_ptr, 0, sizeof(int64_t) * (n + 1), s));
     const unsigned rows_grid = static_cast<unsigned>((n * 32 + kThreads - 1) / kThreads);
     if (n > 0)
@@ -397,8 +397,8 @@ mgpu_csr *mr_build_sequential(mgpu_ctx *ctx, const mgpu_csr *K, const mgpu_csr *
     MG_CUDA(cudaMemcpyAsync(&nnz, P->row_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     MG_CUDA(cudaStreamSynchronize(s));
     P->nnz = nnz;
-    MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&P->col_idx), sizeof(int32_t) * (nnz > 0 ? nnz : 1), s));
-    MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&P->values), sizeof(double) * (nnz > 0 ? nnz : 1), s));
+    MG_CUDA(mg_malloc(reinterpret_cast<void **>(&P->col_idx), sizeof(int32_t) * (nnz > 0 ? nnz : 1), s));
+    MG_CUDA(mg_malloc(reinterpret_cast<void **>(&P->values), sizeof(double) * (nnz > 0 ? nnz : 1), s));
     if (n > 0)
     {
       dense_row_fill<<<rows_grid, kThreads, 0, s>>>(n, dense.as<double>(), P->row_ptr, P->col_idx, P->values);

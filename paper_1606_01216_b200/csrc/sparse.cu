@@ -228,7 +228,7 @@ void batched_add(mgpu_ctx *ctx, const mgpu_csr *A, const mgpu_csr *B, const mgpu
       o->ctx = ctx;
       o->nrows = n;
       o->ncols = A->ncols;
-      MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&o->row_ptr), sizeof(int64_t) * (n + 1), ctx->stream));
+      MG_CUDA(mg_malloc(reinterpret_cast<void **>(&o->row_ptr), sizeof(int64_t) * (n + 1), ctx->stream));
       made.push_back(o);
       args.rp[p] = o->row_ptr;
     }
@@ -279,9 +279,9 @@ void batched_add(mgpu_ctx *ctx, const mgpu_csr *A, const mgpu_csr *B, const mgpu
     {
       mgpu_csr *o = made[p];
       o->nnz = nnz[p];
-      MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&o->col_idx), sizeof(int32_t) * (nnz[p] > 0 ? nnz[p] : 1),
+      MG_CUDA(mg_malloc(reinterpret_cast<void **>(&o->col_idx), sizeof(int32_t) * (nnz[p] > 0 ? nnz[p] : 1),
                               ctx->stream));
-      MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&o->values), sizeof(double) * (nnz[p] > 0 ? nnz[p] : 1),
+      MG_CUDA(mg_malloc(reinterpret_cast<void **>(&o->values), sizeof(double) * (nnz[p] > 0 ? nnz[p] : 1),
                               ctx->stream));
       args.ci[p] = o->col_idx;
       args.v[p] = o->values;

@@ -109,7 +109,7 @@ extern "C" int mgpu_spgemm(mgpu_ctx *ctx, const mgpu_csr *A, const mgpu_csr *B, 
     out->ctx = ctx;
     out->nrows = n;
     out->ncols = B->ncols;
-    MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&out->row_ptr), sizeof(int64_t) * (n + 1), s));
+    MG_CUDA(mg_malloc(reinterpret_cast<void **>(&out->row_ptr), sizeof(int64_t) * (n + 1), s));
     MG_CUDA(cudaMemsetAsync(out->row_ptr, 0, sizeof(int64_t), s));
     DBuf ovf(sizeof(int), s);
     MG_CUDA(cudaMemsetAsync(ovf.ptr, 0, sizeof(int), s));
@@ -134,8 +134,8 @@ extern "C" int mgpu_spgemm(mgpu_ctx *ctx, const mgpu_csr *A, const mgpu_csr *B, 
       throw Error(MGPU_ERR_UNSUPPORTED, "spgemm: a product row has more than 96 entries");
     }
     out->nnz = nnz;
-    MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&out->col_idx), sizeof(int32_t) * (nnz > 0 ? nnz : 1), s));
-    MG_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&out->values), sizeof(double) * (nnz > 0 ? nnz : 1), s));
+    MG_CUDA(mg_malloc(reinterpret_cast<void **>(&out->col_idx), sizeof(int32_t) * (nnz > 0 ? nnz : 1), s));
+    MG_CUDA(mg_malloc(reinterpret_cast<void **>(&out->values), sizeof(double) * (nnz > 0 ? nnz : 1), s));
     if (n > 0)
     {
       spgemm_fill<<<blocks_for(n), kThreads, 0, s>>>(n, A->view(), B->view(), out->row_ptr, out->col_idx, out->values);
