@@ -1368,6 +1368,8 @@ __global__ void __launch_bounds__(TB, 1) cg_banded(BandParams P)
 // =====================================================================
 constexpr int kPadR = 64;
 constexpr int kStreamNB = 4; // bulk-copy ring depth (maximum; StreamParams::nb is the one in use)
+constexpr int kTabSlots = 16; // operator-descriptor slots: segments per block, or points (serial schedule)
+static_assert(kTabSlots >= kMaxSeg, "descriptor table must cover every segment");
 
 __device__ __forceinline__ uint32_t sm_addr(const void *p)
 {
@@ -1396,6 +1398,30 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
                "l"(src), "r"(bytes), "r"(sm_addr(bar))
                : "memory");
 }
+// Same copy with an L2 eviction-priority policy (createpolicy) attached to its reads.
+__device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t pol)
+{
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+               "%4;" ::"r"(sm_addr(dst)),
+               "l"(src), "r"(bytes), "r"(sm_addr(bar)), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first()
+{
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// L2-only store with an eviction-priority policy (data not re-read soon).
+__device__ __forceinline__ void stg_hint(double *p, double v, uint64_t pol)
+{
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+// Drops a 128-byte L2 line without writing it back (its contents become undefined).
+__device__ __forceinline__ void discard_l2(const void *p)
+{
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar)
 {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm_addr(bar)) : "memory");
@@ -1416,6 +1442,7 @@ struct StreamParams
   int ch_b;             // rows per chunk in phase B (fewer vectors per row: taller chunks fill the same slot)
   int fold;             // 1: x~ += alpha d deferred to the next phase A (m = 1), 0: applied in phase B
   int nb;               // ring depth (2..kStreamNB)
+  int serial;           // 1: points one after another (all blocks on one point's rows; L2 hand-off A -> B)
   int64_t n, ldv; // ldv = (n + 2 PADR) * m: doubles per point block
   int halo[kMaxZ + 1];
   int hmax;
@@ -1482,24 +1509,36 @@ __device__ __forceinline__ int64_t even_up(int64_t x) { return (x + 1) & ~static
 // Producer: issue the bulk copies of one chunk's inputs into buffer `buf`.
 // kind 0: phase A step (r, d_old over the halo; x~ on own rows for the deferred
 // update), 1: phase A check (x~ and d_old over the halo), 2: phase B (r, w).
+//
+// Serial schedule (P.serial): every read that is the last one before the data's next use
+// two or more passes later is tagged L2 evict_first (operators, d_old, x~, everything phase B
+// reads), so the lines phase B re-reads (r, d_new, w of the same point, written or read by
+// phase A just before) are the ones that stay in L2.
 template <int TB>
 __device__ void stream_issue(const StreamParams &P, const PEll *tab, unsigned char *buf, uint64_t *bar, int kind, int p,
                              int64_t c0, int64_t c1, const double *dold, const double *dnew)
 {
   const int m = P.m;
   uint32_t bytes = 0;
+  const uint64_t pol = policy_evict_first();
+  auto cp = [&](void *dst, const void *src, uint32_t nbytes, bool last_use) {
+    if (P.serial && last_use)
+      bulk_g2s_hint(dst, src, nbytes, bar, pol);
+    else
+      bulk_g2s(dst, src, nbytes, bar);
+  };
   if (kind == 2)
   {
     const int64_t rows = even_up(c1 - c0);
     const uint32_t vb = static_cast<uint32_t>(rows * m * 8);
     bytes = (P.fold ? 2 : 4) * vb;
     mbar_expect_tx(bar, bytes);
-    bulk_g2s(buf + P.b_r, vrow(P, P.r, p, c0), vb, bar);
-    bulk_g2s(buf + P.b_w, vrow(P, P.w, p, c0), vb, bar);
+    cp(buf + P.b_r, vrow(P, P.r, p, c0), vb, true);
+    cp(buf + P.b_w, vrow(P, P.w, p, c0), vb, true);
     if (!P.fold)
     {
-      bulk_g2s(buf + P.b_x, vrow(P, P.xt, p, c0), vb, bar);
-      bulk_g2s(buf + P.b_d, vrow(P, dnew, p, c0), vb, bar);
+      cp(buf + P.b_x, vrow(P, P.xt, p, c0), vb, true);
+      cp(buf + P.b_d, vrow(P, dnew, p, c0), vb, true);
     }
     return;
   }
@@ -1522,23 +1561,23 @@ __device__ void stream_issue(const StreamParams &P, const PEll *tab, unsigned ch
     total += static_cast<uint32_t>(rows * A.E * 8 + rows * A.ow * 8);
   }
   mbar_expect_tx(bar, total);
-  bulk_g2s(buf + P.a_vr, vrow(P, kind == 0 ? P.r : P.xt, p, c0 - H0), vb, bar);
+  cp(buf + P.a_vr, vrow(P, kind == 0 ? P.r : P.xt, p, c0 - H0), vb, kind != 0); // phase B re-reads r
   if (need_d)
-    bulk_g2s(buf + P.a_vd, vrow(P, dold, p, c0 - H0), vb, bar);
+    cp(buf + P.a_vd, vrow(P, dold, p, c0 - H0), vb, true);
   if (kind == 0 && P.fold)
-    bulk_g2s(buf + P.a_vx, vrow(P, P.xt, p, c0), xb, bar);
+    cp(buf + P.a_vx, vrow(P, P.xt, p, c0), xb, true);
   for (int st = 0; st < P.z; ++st)
   {
     const int hd = P.halo[st + 1];
     const PEll F = tab[1 + st];
     const int64_t rows = even_up(c1 - c0 + 2 * hd);
-    bulk_g2s(buf + P.a_fv[st], F.v + (c0 - hd) * F.E, static_cast<uint32_t>(rows * F.E * 8), bar);
-    bulk_g2s(buf + P.a_fo[st], F.o + (c0 - hd) * F.ow, static_cast<uint32_t>(rows * F.ow * 8), bar);
+    cp(buf + P.a_fv[st], F.v + (c0 - hd) * F.E, static_cast<uint32_t>(rows * F.E * 8), true);
+    cp(buf + P.a_fo[st], F.o + (c0 - hd) * F.ow, static_cast<uint32_t>(rows * F.ow * 8), true);
   }
   const PEll A = tab[0];
   const int64_t rows = even_up(c1 - c0);
-  bulk_g2s(buf + P.a_av, A.v + c0 * A.E, static_cast<uint32_t>(rows * A.E * 8), bar);
-  bulk_g2s(buf + P.a_ao, A.o + c0 * A.ow, static_cast<uint32_t>(rows * A.ow * 8), bar);
+  cp(buf + P.a_av, A.v + c0 * A.E, static_cast<uint32_t>(rows * A.E * 8), true);
+  cp(buf + P.a_ao, A.o + c0 * A.ow, static_cast<uint32_t>(rows * A.ow * 8), true);
 }
 
 __device__ __forceinline__ int off8s(unsigned long long w, int t)
@@ -1808,6 +1847,30 @@ __device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, cons
       double *rg = const_cast<double *>(vrow(P, P.r, cp, base_i));
       double *xg = const_cast<double *>(vrow(P, P.xt, cp, base_i));
       const int ne = R * m;
+      if (P.serial)
+      {
+        // w is dead once in shared memory: drop its L2 lines (no write-back to HBM), only
+        // lines that lie wholly inside this chunk's rows
+        const uintptr_t wa = reinterpret_cast<uintptr_t>(vrow(P, P.w, cp, base_i));
+        const uintptr_t l0 = (wa + 127) & ~static_cast<uintptr_t>(127);
+        const uintptr_t l1 = (wa + static_cast<uintptr_t>(ne) * 8) & ~static_cast<uintptr_t>(127);
+        for (uintptr_t a = l0 + static_cast<uintptr_t>(threadIdx.x) * 128; a < l1; a += static_cast<uintptr_t>(TB) * 128)
+          discard_l2(reinterpret_cast<const void *>(a));
+        const uint64_t pol = policy_evict_first();
+        for (int e = threadIdx.x; e < ne; e += TB)
+        {
+          const int c = col_of<MT>(e, m);
+          if (sh.state[sb + c] != kRun)
+            continue;
+          const double al = sh.alpha[sb + c];
+          if (!P.fold)
+            stg_hint(xg + e, __dadd_rn(xs[e], __dmul_rn(al, ds[e])), pol);
+          const double rn = __dadd_rn(rs[e], __dmul_rn(-al, ws[e]));
+          stg_hint(rg + e, rn, pol);
+          acc_add<MT>(acc, c, __dmul_rn(rn, rn));
+        }
+      }
+      else
       for (int e = threadIdx.x; e < ne; e += TB)
       {
         const int c = col_of<MT>(e, m);
@@ -1937,7 +2000,9 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
   extern __shared__ __align__(128) unsigned char smem_s[];
   __shared__ BandShared<TBX> sh;
   __shared__ __align__(8) uint64_t bars[2 * kStreamNB]; // full[NB], empty[NB]
-  __shared__ PEll tab[kMaxSeg * (kMaxZ + 1)]; // operator descriptors per segment: A, then stage factors
+  // operator descriptors per segment (serial schedule: per point): A, then stage factors
+  __shared__ PEll tab[kTabSlots * (kMaxZ + 1)];
+  __shared__ int64_t ser_rows[2]; // serial schedule: this block's row slab, the same for every point
   const int m = P.m;
   const int S = P.l * m;
   uint32_t phase_bits = 0;
@@ -1952,9 +2017,12 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
       ++q;
     }
     sh.nseg = q;
-    for (int g = 0; g < q; ++g)
+    ser_rows[0] = q > 0 ? sh.seg[0].rs : 0;
+    ser_rows[1] = q > 0 ? sh.seg[0].re : 0;
+    const int ntab = P.serial ? P.l : q;
+    for (int g = 0; g < ntab; ++g)
     {
-      const int p = sh.seg[g].p;
+      const int p = P.serial ? g : sh.seg[g].p;
       tab[g * (kMaxZ + 1)] = P.A[p];
       for (int st = 0; st < P.z; ++st)
         tab[g * (kMaxZ + 1) + 1 + st] = P.F[p * P.z + (P.z - 1 - st)];
@@ -1966,8 +2034,37 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
   for (int p = threadIdx.x; p < P.l; p += TBX)
     sh.pmask[p] = 1;
   __syncthreads();
+  // rows of every masked point this block owns (serial schedule: the block's slab of each point)
+  auto for_rows = [&](auto &&fn) {
+    if (P.serial)
+    {
+      for (int p = 0; p < P.l; ++p)
+        if (sh.pmask[p])
+          fn(p, ser_rows[0], ser_rows[1]);
+    }
+    else
+      for_segments(P, sh, fn);
+  };
+  // serial schedule: make point p the block's only segment (and the only masked point)
+  auto pick_point = [&](int p) {
+    __syncthreads();
+    for (int q = threadIdx.x; q < P.l; q += TBX)
+      sh.pmask[q] = q == p;
+    if (threadIdx.x == 0)
+    {
+      sh.seg[0] = Seg{p, static_cast<int>(ser_rows[0]), static_cast<int>(ser_rows[1]), 0};
+      sh.nseg = 1;
+    }
+    __syncthreads();
+  };
+  auto point_live = [&](int p) {
+    bool live = false;
+    for (int c = 0; c < m; ++c)
+      live |= sh.state[p * m + c] == kRun;
+    return live;
+  };
   // ---- phase 0: ||b||^2 (one pass, plain loads)
-  for_segments(P, sh, [&](int p, int64_t rs, int64_t re) {
+  for_rows([&](int p, int64_t rs, int64_t re) {
     begin_point(sh);
     for (int64_t c0 = rs; c0 < re; c0 += TBX)
     {
@@ -2005,7 +2102,7 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
   __syncthreads();
 
   auto copy_finish = [&]() {
-    for_segments(P, sh, [&](int p, int64_t rs, int64_t re) {
+    for_rows([&](int p, int64_t rs, int64_t re) {
       for (int64_t i = rs + threadIdx.x; i < re; i += TBX)
         for (int c = 0; c < m; ++c)
         {
@@ -2023,6 +2120,69 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
         }
     });
     fence_async_global();
+  };
+
+  // true-residual check pass over the masked points (serial schedule: one point at a time,
+  // no barrier in between -- the passes are independent); leaves pmask as it found it
+  auto check_pass = [&](const double *dcur) {
+    if (!P.serial)
+    {
+      stream_pass<TB, MT, kStreamNB>(P, sh, tab, smem_s, bars, bars + kStreamNB, phase_bits, rp, 1, dcur, nullptr, pc);
+      return;
+    }
+    uint32_t msk = 0;
+    for (int p = 0; p < P.l; ++p)
+      msk |= sh.pmask[p] ? 1u << p : 0u;
+    for (int p = 0; p < P.l; ++p)
+      if ((msk >> p) & 1u)
+      {
+        pick_point(p);
+        stream_pass<TB, MT, kStreamNB>(P, sh, tab + p * (kMaxZ + 1), smem_s, bars, bars + kStreamNB, phase_bits, rp, 1,
+                                       dcur, nullptr, pc);
+      }
+    __syncthreads();
+    for (int p = threadIdx.x; p < P.l; p += TBX)
+      sh.pmask[p] = (msk >> p) & 1u;
+    __syncthreads();
+  };
+  // after phase A's reduction: alpha or breakdown for the running systems of masked points
+  auto after_a = [&](int64_t itn) {
+    for (int s = threadIdx.x; s < S; s += TBX)
+    {
+      if (!sh.pmask[s / m])
+        continue;
+      sh.pend[s] = 0; // phase A applied the deferred x~ update
+      if (sh.state[s] != kRun)
+        continue;
+      const int p = s / m, c = s % m;
+      const double curv = sh.tot[p * m + c];
+      const double dd = sh.tot[S + p * m + c];
+      if (!(curv > 1e-30 * dd))
+      {
+        sh.state[s] = kBreakdown;
+        sh.sit[s] = itn;
+      }
+      else
+        sh.alpha[s] = sh.rho[s] / curv;
+    }
+    __syncthreads();
+  };
+  // after phase B's reduction: beta, rho for the running systems of masked points (itn: the
+  // iteration just completed, 0-based)
+  auto after_b = [&](int64_t itn) {
+    for (int s = threadIdx.x; s < S; s += TBX)
+    {
+      if (!sh.pmask[s / m] || sh.state[s] != kRun)
+        continue;
+      const double rn = sh.tot[s];
+      if (P.hist && blockIdx.x == 0 && itn < P.hist_cap)
+        P.hist[static_cast<int64_t>(s) * P.hist_cap + itn] = sqrt(rn) / sh.bnorm[s];
+      sh.beta[s] = rn / sh.rho[s];
+      sh.rho[s] = rn;
+      sh.fresh[s] = 0;
+      sh.pend[s] = P.fold; // x~ += alpha d owed to the next phase A / check pass
+    }
+    __syncthreads();
   };
 
   int cur = 0;
@@ -2049,7 +2209,7 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
     __syncthreads();
     if (sh.flag)
     {
-      stream_pass<TB, MT, kStreamNB>(P, sh, tab, smem_s, bars, bars + kStreamNB, phase_bits, rp, 1, cur ? P.dbuf1 : P.dbuf0, nullptr, pc);
+      check_pass(cur ? P.dbuf1 : P.dbuf0);
       fence_async_global();
       grid.sync();
       reduce_blocks<TBX, StreamParams>(P, sh, m);
@@ -2107,6 +2267,39 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
       break;
     double *d_old = cur ? P.dbuf1 : P.dbuf0;
     double *d_new = cur ? P.dbuf0 : P.dbuf1;
+    if (P.serial)
+    {
+      // one point at a time on every block: phase A writes d_new and w and phase B re-reads
+      // them (and r) straight from L2, two grid barriers per point
+      uint32_t live = 0;
+      for (int p = 0; p < P.l; ++p)
+        live |= sh.pmask[p] ? 1u << p : 0u;
+      for (int p = 0; p < P.l; ++p)
+      {
+        if (!((live >> p) & 1u))
+          continue;
+        pick_point(p);
+        const PEll *tp = tab + p * (kMaxZ + 1);
+        pc.mark(9);
+        stream_pass<TB, MT, kStreamNB>(P, sh, tp, smem_s, bars, bars + kStreamNB, phase_bits, rp, 0, d_old, d_new, pc);
+        fence_async_global();
+        grid.sync();
+        pc.mark(10);
+        reduce_blocks<TBX, StreamParams>(P, sh, 2 * m);
+        after_a(it);
+        pc.mark(11);
+        stream_pass<TB, MT, kStreamNB>(P, sh, tp, smem_s, bars, bars + kStreamNB, phase_bits, rp, 2, d_old, d_new, pc);
+        fence_async_global();
+        grid.sync();
+        pc.mark(10);
+        reduce_blocks<TBX, StreamParams>(P, sh, m);
+        after_b(it);
+        pc.mark(11);
+      }
+      ++it;
+      cur ^= 1;
+      continue;
+    }
     pc.mark(9);
     stream_pass<TB, MT, kStreamNB>(P, sh, tab, smem_s, bars, bars + kStreamNB, phase_bits, rp, 0, d_old, d_new, pc);
     fence_async_global();
@@ -2114,24 +2307,7 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
     pc.mark(10);
     reduce_blocks<TBX, StreamParams>(P, sh, 2 * m);
     pc.mark(11);
-    for (int s = threadIdx.x; s < S; s += TBX)
-    {
-      if (sh.pmask[s / m])
-        sh.pend[s] = 0; // phase A applied the deferred x~ update
-      if (sh.state[s] != kRun)
-        continue;
-      const int p = s / m, c = s % m;
-      const double curv = sh.tot[p * m + c];
-      const double dd = sh.tot[S + p * m + c];
-      if (!(curv > 1e-30 * dd))
-      {
-        sh.state[s] = kBreakdown;
-        sh.sit[s] = it;
-      }
-      else
-        sh.alpha[s] = sh.rho[s] / curv;
-    }
-    __syncthreads();
+    after_a(it);
     pc.mark(9);
     stream_pass<TB, MT, kStreamNB>(P, sh, tab, smem_s, bars, bars + kStreamNB, phase_bits, rp, 2, d_old, d_new, pc);
     fence_async_global();
@@ -2139,20 +2315,8 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
     pc.mark(10);
     reduce_blocks<TBX, StreamParams>(P, sh, m);
     pc.mark(11);
+    after_b(it);
     ++it;
-    for (int s = threadIdx.x; s < S; s += TBX)
-    {
-      if (sh.state[s] != kRun)
-        continue;
-      const double rn = sh.tot[s];
-      if (P.hist && blockIdx.x == 0 && it - 1 < P.hist_cap)
-        P.hist[static_cast<int64_t>(s) * P.hist_cap + (it - 1)] = sqrt(rn) / sh.bnorm[s];
-      sh.beta[s] = rn / sh.rho[s];
-      sh.rho[s] = rn;
-      sh.fresh[s] = 0;
-      sh.pend[s] = P.fold; // x~ += alpha d owed to the next phase A / check pass
-    }
-    __syncthreads();
     cur ^= 1;
   }
   // ---- budget exhausted: final true-residual check
@@ -2171,7 +2335,7 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
   __syncthreads();
   if (sh.flag)
   {
-    stream_pass<TB, MT, kStreamNB>(P, sh, tab, smem_s, bars, bars + kStreamNB, phase_bits, rp, 1, cur ? P.dbuf1 : P.dbuf0, nullptr, pc);
+    check_pass(cur ? P.dbuf1 : P.dbuf0);
     fence_async_global();
     grid.sync();
     reduce_blocks<TBX, StreamParams>(P, sh, m);
@@ -2193,7 +2357,7 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
   for (int p = threadIdx.x; p < P.l; p += TBX)
     sh.pmask[p] = 1;
   __syncthreads();
-  for_segments(P, sh, [&](int p, int64_t rs, int64_t re) {
+  for_rows([&](int p, int64_t rs, int64_t re) {
     for (int64_t i = rs + threadIdx.x; i < re; i += TBX)
       for (int c = 0; c < m; ++c)
       {
@@ -2441,7 +2605,7 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
   int64_t CH = 0;
   int optin = 0;
   MG_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
-  const size_t stat = sizeof(BandShared<TB + 32>) + sizeof(PEll) * kMaxSeg * (kMaxZ + 1) + 128;
+  const size_t stat = sizeof(BandShared<TB + 32>) + sizeof(PEll) * kTabSlots * (kMaxZ + 1) + 128;
   // (chunk rows, ring depth) in order of preference; MGPU_STREAM_CFG="rows,depth" forces one (diagnostics)
   // largest chunk first (per-chunk barriers and pipeline bookkeeping amortise over its rows), 3-deep ring
   // before 2-deep at equal height
@@ -2507,9 +2671,34 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
       l, m, n, ldv, B_dev, ldb, b.as<double>(), r.as<double>(), d0.as<double>(), xt.as<double>());
   check_launch(ctx, "stream_init");
   const int G = ctx->num_sms;
+  // Serial schedule (opt-in, MGPU_STREAM_SERIAL=1): the points run one after another on every
+  // block, so phase B re-reads phase A's outputs (r, d_new, w: 24 n m bytes) from L2 and w never
+  // reaches HBM (its lines are discarded once read).  Measured on configs[3] (n = 1e6, m = 4,
+  // 16 points): DRAM traffic 6.15 -> 4.70 GB per batched iteration, but 1072 -> 1415 us per
+  // iteration -- two grid barriers, two block reductions, two flushes and two pipeline fills
+  // per point (~10 us per pass, 32 passes) cost more than the bytes saved.  Off by default.
+  bool serial = false;
+  if (const char *f = std::getenv("MGPU_STREAM_SERIAL"))
+    serial = f[0] == '1';
+  serial = serial && l <= kTabSlots;
   std::vector<Seg> hseg(static_cast<size_t>(G) * kMaxSeg, Seg{-1, 0, 0, 0});
   std::vector<int2> hpb(static_cast<size_t>(l));
-  if (l <= G)
+  if (serial)
+  {
+    // every block: the same row slab of every point (32-row groups, no row-less block inside
+    // the reduction range)
+    const int64_t groups = (n + 31) / 32;
+    const int nb = static_cast<int>(std::min<int64_t>(G, groups));
+    for (int bk = 0; bk < G; ++bk)
+    {
+      const int64_t g0 = bk < nb ? groups * bk / nb : 0, g1 = bk < nb ? groups * (bk + 1) / nb : 0;
+      hseg[static_cast<size_t>(bk) * kMaxSeg] =
+          Seg{0, static_cast<int>(g0 * 32), static_cast<int>(std::min<int64_t>(n, g1 * 32)), 0};
+    }
+    for (int p = 0; p < l; ++p)
+      hpb[p] = make_int2(0, nb);
+  }
+  else if (l <= G)
   {
     for (int p = 0; p < l; ++p)
     {
@@ -2553,6 +2742,7 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
   P.m = m;
   P.z = z;
   P.rpt = 1;
+  P.serial = serial ? 1 : 0;
   P.ch = static_cast<int>(CH);
   {
     // phase B: r, w (+ x~, d unfolded) -> the tallest chunk (multiple of 64 rows, <= 8192) that fits one slot

@@ -37,11 +37,13 @@ def _oracle_case():
     return (M, D, K), ops, facs, b, sols
 
 
-@pytest.mark.parametrize("path", ["auto", "stream", "banded"])
-def test_bench_workload_iterate_parity(mg, path):
+@pytest.mark.parametrize("path", ["auto", "stream", "stream_serial", "banded"])
+def test_bench_workload_iterate_parity(mg, path, monkeypatch):
     (M, D, K), ops, facs, b, want = _oracle_case()
     ctx = mg.default_context()
-    ctx.set_cg_path(path)
+    if path == "stream_serial":
+        monkeypatch.setenv("MGPU_STREAM_SERIAL", "1")
+    ctx.set_cg_path("stream" if path == "stream_serial" else path)
     try:
         # the bench's device pipeline: assembly + batched LS-SPAI + one batched solve
         dops = mg.shifted_operators(M, D, K, SHIFTS, ctx=ctx)
@@ -59,3 +61,31 @@ def test_bench_workload_iterate_parity(mg, path):
             assert rel(r.X[:, 0], w["solution"]) < 1e-8
     finally:
         ctx.set_cg_path("auto")
+
+
+def test_config3_serial_schedule_matches_batched(mg, monkeypatch):
+    """BASELINE configs[3] shape (n = 1e6, m = 4, 16 shifts, P = I) through the streaming
+    kernel: the point-serial schedule (L2 hand-off between the phases, w discarded from L2)
+    against the batched schedule after 40 iterations.  Same arithmetic per element; only the
+    dot-product trees differ (block slabs), so the iterates agree to rounding noise."""
+    ne, m, k = 500000, 4, 40
+    shifts = [10.0 ** (1 + 3 * i / 15) for i in range(16)]
+    ctx = mg.default_context()
+    M, D, K = mg.model_hermite_device(ne, ctx=ctx)
+    n = 2 * ne
+    B = np.zeros((n, m))
+    for c in range(m):
+        B[2 * ((c + 1) * ne // m) - 2, c] = 1.0
+    ops = mg.shifted_operators(M, D, K, shifts, ctx=ctx)
+    ctx.set_cg_path("stream")
+    try:
+        monkeypatch.setenv("MGPU_STREAM_SERIAL", "0")
+        ref = mg.cg_solve_batched(ops, [[] for _ in ops], B, rtol=1e-10, maxit=k, ctx=ctx)
+        monkeypatch.setenv("MGPU_STREAM_SERIAL", "1")
+        got = mg.cg_solve_batched(ops, [[] for _ in ops], B, rtol=1e-10, maxit=k, ctx=ctx)
+    finally:
+        ctx.set_cg_path("auto")
+    for g, r in zip(got, ref):
+        np.testing.assert_array_equal(g.iterations, r.iterations)
+        assert rel(g.X, r.X) < 1e-10
+        assert np.all(np.isfinite(g.X)) and np.max(np.abs(g.X)) > 0

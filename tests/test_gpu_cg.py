@@ -13,12 +13,17 @@ from conftest import rel
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True, params=["auto", "cluster_v1", "stream", "banded", "general"])
-def cg_path(request, mg):
-    """Every parity case runs through all three CG kernels: cluster-resident (auto on
-    these on-chip sizes), the banded grid kernel and the general CSR kernel."""
+@pytest.fixture(autouse=True, params=["auto", "cluster_v1", "stream", "stream_serial", "banded", "general"])
+def cg_path(request, mg, monkeypatch):
+    """Every parity case runs through every CG kernel: cluster-resident (auto on these
+    on-chip sizes), the streaming kernel (batched and point-serial schedules), the banded
+    grid kernel and the general CSR kernel."""
     ctx = mg.default_context()
-    ctx.set_cg_path(request.param)
+    if request.param == "stream_serial":
+        monkeypatch.setenv("MGPU_STREAM_SERIAL", "1")
+        ctx.set_cg_path("stream")
+    else:
+        ctx.set_cg_path(request.param)
     yield request.param
     ctx.set_cg_path("auto")
 
@@ -30,7 +35,8 @@ def test_path_selection(mg, oracle, cg_path):
     mg.pcg_solve(A, [P], np.ones(600), maxit=5)
     # A^2-pattern factor: 10 entries per row -> the shared-memory cluster kernel (v1); v2 packs <= 8
     assert mg.default_context().last_cg_path == {"auto": "cluster_v1", "cluster_v1": "cluster_v1", "stream": "stream",
-                                                  "banded": "banded", "general": "general"}[cg_path]
+                                                  "stream_serial": "stream", "banded": "banded",
+                                                  "general": "general"}[cg_path]
     if cg_path == "auto":
         P1 = oracle.spai_ls(A, None, 0)
         mg.pcg_solve(A, [P1], np.ones(600), maxit=5)
