@@ -95,6 +95,20 @@ class CudaCgBackend:
                            and len(self.prev_ops) == len(points) and len(self.chains) == len(points))
             if not update_mode:
                 self.chains = [[] for _ in points]
+            if c.spai_algorithm == "ls":
+                # every point's factor in one batched device call (the operators share one
+                # pattern); each record carries an equal share of the batch time
+                t0 = time.perf_counter()
+                qs = mgpu.spai_ls_batched(fresh, self.prev_ops if update_mode else None, c.ls_pattern, ctx=self.ctx)
+                self.ctx.synchronize()
+                share = (time.perf_counter() - t0) / max(len(points), 1)
+                for i, s in enumerate(points):
+                    self.chains[i].insert(0, qs[i])  # push_newest (spai.cpp:352-359)
+                    if records is not None:
+                        records.append(PrecondRecord(outer, i, float(s), share, "update" if update_mode else "base",
+                                                     len(self.chains[i])))
+                self.prev_ops = fresh
+                return
             for i, s in enumerate(points):
                 t0 = time.perf_counter()
                 if update_mode:

@@ -711,7 +711,7 @@ __global__ void __launch_bounds__(kCgThreads) cg_persistent(CgParams P)
 // after the barrier every block sums the per-block partials in block order.
 // Deterministic for a given grid (one block per SM), no atomics.
 // =====================================================================
-constexpr int kMaxZ = 8;
+constexpr int kMaxZ = 12; // chain factors (the AIRGA update chain grows by one per outer iteration)
 constexpr int kMaxHalo = 64;
 constexpr int kMaxRpt = 4;
 constexpr int kMaxSeg = 8; // row segments per block
@@ -866,7 +866,9 @@ __device__ void band_phase_a(const BandParams &P, BandShared<TB> &sh, double *sm
   const int H0 = P.hmax;
   constexpr int CH = TB * RPT;
   const int stride = (CH + 2 * H0) * m;
-  double *buf0 = smem, *buf1 = smem + stride;
+  // buf0 keeps stage 0 (d_new) for the dot products; the chain stages ping-pong between
+  // buf1 and buf2 (allocated when z >= 2)
+  double *buf0 = smem, *buf1 = smem + stride, *buf2 = smem + 2 * stride;
   for_segments(P, sh, [&](int p, int64_t rs, int64_t re) {
     begin_point(sh);
     const int64_t base = static_cast<int64_t>(p) * P.n * m;
@@ -912,6 +914,7 @@ __device__ void band_phase_a(const BandParams &P, BandShared<TB> &sh, double *sm
       __syncthreads();
       // ---- chain stages (oldest factor first), shrinking halos
       double *src = buf0, *dst = buf1;
+      double *other = buf2;
       int hs = H0;
       for (int st = 0; st < P.z; ++st)
       {
@@ -944,7 +947,8 @@ __device__ void band_phase_a(const BandParams &P, BandShared<TB> &sh, double *sm
               dst[q * m + c] = acc[c];
         }
         __syncthreads();
-        double *tmp = src;
+        // next stage writes the buffer that is neither its source nor buf0
+        double *tmp = src == buf0 ? other : src;
         src = dst;
         dst = tmp;
         hs = hd;
@@ -2471,7 +2475,8 @@ void launch_cg(mgpu_ctx *ctx, const CgParams &P)
 template <int TB, int MT, int RPT>
 void launch_banded_cfg(mgpu_ctx *ctx, const BandParams &P)
 {
-  const size_t dyn = sizeof(double) * 2 * static_cast<size_t>(TB * RPT + 2 * P.hmax) * P.m;
+  // stage-0 buffer (d_new, read again by the dot products) + the chain's ping-pong pair
+  const size_t dyn = sizeof(double) * (P.z >= 2 ? 3 : 2) * static_cast<size_t>(TB * RPT + 2 * P.hmax) * P.m;
   MG_CUDA(cudaFuncSetAttribute(cg_banded<TB, MT, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(dyn)));
   int per_sm = 0;
@@ -2497,6 +2502,14 @@ void launch_banded_rpt(mgpu_ctx *ctx, BandParams &P)
   rpt = rpt < 1 ? 1 : (rpt > kMaxRpt ? kMaxRpt : rpt);
   if (rpt == 3)
     rpt = 4;
+  // shorter chunks when the stage buffers (2, or 3 with a chain of >= 2 factors) would not fit
+  int optin = 0;
+  MG_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+  const auto dyn_of = [&](int r) {
+    return sizeof(double) * (P.z >= 2 ? 3 : 2) * static_cast<size_t>(TB * r + 2 * P.hmax) * P.m + 4096;
+  };
+  while (rpt > 1 && dyn_of(rpt) + sizeof(BandShared<TB>) > static_cast<size_t>(optin))
+    rpt /= 2;
   P.rpt = rpt;
   if (rpt == 1)
     launch_banded_cfg<TB, MT, 1>(ctx, P);

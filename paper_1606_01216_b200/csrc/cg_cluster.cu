@@ -37,7 +37,7 @@ int64_t csr_max_row(mgpu_ctx *ctx, mgpu_csr *A);
 namespace
 {
 
-constexpr int kCMaxZ = 8;
+constexpr int kCMaxZ = 12; // chain factors (the AIRGA update chain grows by one per outer iteration)
 constexpr int kCMaxM = 4;
 constexpr int kCMaxCS = 16;
 

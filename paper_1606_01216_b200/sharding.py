@@ -15,6 +15,53 @@ def log_shifts(count: int, lo: float = 10.0, hi: float = 1e4) -> List[float]:
     return [10.0 ** (a + (b - a) * i / (count - 1)) for i in range(count)]
 
 
+class Mt19937_64:
+    """std::mt19937_64 (the C++ standard's 64-bit Mersenne twister; seeding per
+    [rand.eng.mers]), so host-drawn shifts match a C++ driver seeded the same way."""
+
+    _N, _M = 312, 156
+    _MASK = (1 << 64) - 1
+
+    def __init__(self, seed: int = 5489):
+        mt = [0] * self._N
+        mt[0] = seed & self._MASK
+        for i in range(1, self._N):
+            mt[i] = (6364136223846793005 * (mt[i - 1] ^ (mt[i - 1] >> 62)) + i) & self._MASK
+        self.mt, self.i = mt, self._N
+
+    def __call__(self) -> int:
+        mt, N, M = self.mt, self._N, self._M
+        if self.i >= N:
+            upper, lower = 0xFFFFFFFF80000000, 0x7FFFFFFF
+            for k in range(N):
+                x = (mt[k] & upper) | (mt[(k + 1) % N] & lower)
+                xa = x >> 1
+                if x & 1:
+                    xa ^= 0xB5026F5AA96619E9
+                mt[k] = mt[(k + M) % N] ^ xa
+            self.i = 0
+        y = mt[self.i]
+        self.i += 1
+        y ^= (y >> 29) & 0x5555555555555555
+        y ^= (y << 17) & 0x71D67FFFEDA60000
+        y ^= (y << 37) & 0xFFF7EEE000000000
+        y ^= y >> 43
+        return y & self._MASK
+
+
+def airga_shift_draws(outer: int, count: int, seed: int = 42, lo_exp: float = 1.0, span: float = 3.0) -> List[List[float]]:
+    """BASELINE configs[2]: per outer iteration, `count` shifts
+    s = 10^(lo_exp + span u), u = (mt19937_64(seed)() >> 11) * 2^-53, one generator across
+    the whole sequence, each draw sorted ascending (update partners pair by index,
+    airga.cpp:145)."""
+    g = Mt19937_64(seed)
+    out = []
+    for _ in range(outer):
+        draw = [10.0 ** (lo_exp + span * ((g() >> 11) * 2.0 ** -53)) for _ in range(count)]
+        out.append(sorted(draw))
+    return out
+
+
 def shard(items: Sequence, rank: int, world: int) -> list:
     """Round-robin shard of items for rank (disjoint, covering, balanced to +-1)."""
     if not (0 <= rank < world):
