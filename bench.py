@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="mgpu", choices=["mgpu", "reference"])
     ap.add_argument("--budget", type=int, default=1000, help="CG iterations per solve (fixed budget)")
-    ap.add_argument("--workload", default="config1", choices=["config0", "config1", "config2", "config3"])
+    ap.add_argument("--workload", default="config1", choices=["config0", "config1", "config2", "config3", "config4"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -69,8 +69,12 @@ def workload(name: str, world: int, rank: int):
     elif name == "config2":
         ne, m, per, pattern = 50000, 1, 8, 0
         all_shifts = sharding.log_shifts(per * world)
-    else:
+    elif name == "config3":
         ne, m, per, pattern = 500000, 4, 16, -1
+        all_shifts = sharding.log_shifts(per * world)
+    else:
+        # configs[4]: n = 1e7, m = 4, 64 shifts over 8 GPUs -> the per-GPU share, 8 shifts per rank
+        ne, m, per, pattern = 5000000, 4, 8, -1
         all_shifts = sharding.log_shifts(per * world)
     return ne, m, sharding.shard(all_shifts, rank, world), all_shifts, pattern
 
@@ -199,7 +203,7 @@ def run_reference(args, rank, world):
 def config_dict(args, ne, m, shifts, pattern, world):
     spai = {0: "LS-SPAI on the A pattern", 1: "LS-SPAI on the A^2 pattern",
             -1: "no preconditioner (P = I; every reference SPAI fails at this n on this beam, DESIGN.md)"}[pattern]
-    return {"workload": f"BASELINE.json configs[{ {'config0': 0, 'config1': 1, 'config2': 2, 'config3': 3}[args.workload] }]"
+    return {"workload": f"BASELINE.json configs[{ {'config0': 0, 'config1': 1, 'config2': 2, 'config3': 3, 'config4': 4}[args.workload] }]"
                         f" shape: Hermite cantilever ne={ne} (n={2 * ne}), {len(shifts)} shifts log-spaced in "
                         f"[10,1e4], m={m}, {spai}, right-preconditioned CG, rtol 1e-10, fixed budget "
                         f"{args.budget} iterations",
@@ -350,9 +354,9 @@ def run_mgpu(args, rank, world, local_rank):
             orc = Oracle()
             hM, hD, hK = orc.hermite_generate(ne)
             kind = "reference" if reference_available() else "port"
-            big = args.workload in ("config2", "config3")
+            big = args.workload in ("config2", "config3", "config4")
             sample_shifts = shifts if not big else shifts[:2]
-            sample_budget = budget if not big else 20
+            sample_budget = budget if not big else (5 if args.workload == "config4" else 20)
             step, threads, kind = cpu_step_fn(kind, hM, hD, hK, sample_shifts, B, pattern, sample_budget)
             t = time.perf_counter()
             step()

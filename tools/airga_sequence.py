@@ -110,9 +110,12 @@ def main():
     ap.add_argument("--ref-budget", type=int, default=0, help="CG iterations per shift in the reference arm (0: skip)")
     ap.add_argument("--ref-outers", default="1,2,5,10")
     ap.add_argument("--out", default="")
+    ap.add_argument("--cg-path", default="auto", help="auto | stream | banded | general (diagnostics)")
+    ap.add_argument("--arms", default="update,rebuild")
     a = ap.parse_args()
     draws = airga_shift_draws(a.outer, a.shifts)
     ctx = mg.Context(0)
+    ctx.set_cg_path(a.cg_path)
     M, D, K = mg.model_hermite_device(a.ne, ctx=ctx)
     n = 2 * a.ne
     b = np.zeros(n)
@@ -121,8 +124,9 @@ def main():
     result = {"workload": f"BASELINE configs[2]: Hermite ne={a.ne} (n={n}), {a.outer} outer iterations x "
                           f"{a.shifts} shifts log-uniform in [10,1e4] (mt19937_64 seed 42, sorted), LS-SPAI on the "
                           f"A pattern, update from z=2 vs rebuild, CG budget {a.budget}",
-              "update": device_arm(True, (M, D, K), draws, b, a.budget, ctx),
-              "rebuild": device_arm(False, (M, D, K), draws, b, a.budget, ctx)}
+              "cg_path": a.cg_path}
+    for arm in a.arms.split(","):
+        result[arm] = device_arm(arm == "update", (M, D, K), draws, b, a.budget, ctx)
     if a.ref_budget > 0:
         outers = {int(x) for x in a.ref_outers.split(",")}
         result["reference_update"] = reference_arm(True, a.ne, draws, b, a.ref_budget, a.budget, outers)
