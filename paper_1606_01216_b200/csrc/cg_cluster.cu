@@ -24,6 +24,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <type_traits>
 #include <vector>
 
 #include "internal.cuh"
@@ -180,6 +181,96 @@ __device__ __forceinline__ void warp_inbox_total(const double *inbox, int nv, in
 #pragma unroll
   for (int k = 0; k < NV; ++k)
     out[k] = v[k];
+}
+
+// ---- asynchronous cluster exchange (v2 main loop): remote stores that complete an
+// mbarrier transaction on the receiving CTA, so a reduction waits only for its own data
+// instead of a cluster-wide barrier (no release fence over every prior store, no L1 flush).
+__device__ __forceinline__ uint32_t cl_map(const void *local, int rank)
+{
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+               : "=r"(r)
+               : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(local))), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async_f64(uint32_t raddr, double v, uint32_t rbar)
+{
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(raddr), "d"(v),
+               "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void cl_mbar_init(uint64_t *bar)
+{
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+               : "memory");
+}
+__device__ __forceinline__ void cl_mbar_arm(uint64_t *bar, uint32_t bytes)
+{
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cl_mbar_wait(uint64_t *bar, uint32_t parity)
+{
+  asm volatile("{\n\t.reg .pred p;\n\tW_%=:\n\t"
+               "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+               "@!p bra W_%=;\n\t}" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+               "r"(parity)
+               : "memory");
+}
+
+// cta_sum_push over the asynchronous exchange: the CTA total of nv values goes to slot
+// k * kCMaxCS + rank of every CTA's inbox, completing `bar` (same offset) there.
+template <int TB, int NV>
+__device__ __forceinline__ void cta_sum_push_async(ClShared &sh, double (&v)[NV], int nv, double *inbox,
+                                                   uint64_t *bar, int cs, int rank)
+{
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1)
+  {
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+      v[k] = __dadd_rn(v[k], __shfl_xor_sync(0xffffffffu, v[k], off));
+  }
+  if (lane == 0)
+  {
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+      sh.red[warp][k] = v[k];
+  }
+  __syncthreads();
+  if (warp == 0)
+  {
+    // every sending lane sums the TB/32 warp totals itself (broadcast reads, pairwise tree):
+    // no shuffle round trips on the critical path
+    static_assert((TB / 32 & (TB / 32 - 1)) == 0, "warp count must be a power of two");
+    double x[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+    {
+      double t[TB / 32];
+#pragma unroll
+      for (int w = 0; w < TB / 32; ++w)
+        t[w] = k < nv ? sh.red[w][k] : 0.0;
+#pragma unroll
+      for (int h = TB / 64; h > 0; h >>= 1)
+#pragma unroll
+        for (int w = 0; w < h; ++w)
+          t[w] = __dadd_rn(t[2 * w], t[2 * w + 1]);
+      x[k] = t[0];
+    }
+    if (lane < cs)
+    {
+      const uint32_t rb = cl_map(bar, lane);
+#pragma unroll
+      for (int k = 0; k < NV; ++k)
+        if (k < nv)
+          st_async_f64(cl_map(inbox + k * kCMaxCS + rank, lane), x[k], rb);
+    }
+  }
 }
 
 // After cluster.sync(): tot[k] = sum over ranks (fixed order) of slot[k].
@@ -789,6 +880,7 @@ struct V2Params
   int64_t hist_cap;
   unsigned long long *loop_iters;
   long long *prof; // optional [16] accumulated clock64 deltas per phase (cluster 0, rank 0, thread 0)
+  int async_x;     // 1: main-loop reductions and halos over st.async + mbarriers, 0: cluster barriers
 };
 
 // EC > 0: every operator row (A and each chain factor) holds exactly EC ELL entries, known at
@@ -827,6 +919,45 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
   auto sel_r = [&](double *b, int q, int side) { return ex_r(b, q, side); };
   auto sel_d = [&](double *b, int q, int side) { return ex_d(b, q, side); };
   auto sel_x = [&](double *b, int, int side) { return ex_x(b, side); };
+  // asynchronous exchange (P.async_x): xbar[0] completes when phase A's partials (every CTA)
+  // and d boundary rows (neighbours) have landed, xbar[1] likewise for phase B and r
+  __shared__ __align__(8) uint64_t xbar[2];
+  const int nbrs = (rank > 0 ? 1 : 0) + (rank + 1 < cs ? 1 : 0);
+  const uint32_t bytesA = static_cast<uint32_t>(8 * (2 * cs + H * nbrs));
+  const uint32_t bytesB = static_cast<uint32_t>(8 * (cs + H * nbrs));
+  uint32_t exL = 0, exR = 0, barL[2] = {0, 0}, barR[2] = {0, 0};
+  if (P.async_x)
+  {
+    if (threadIdx.x == 0)
+    {
+      cl_mbar_init(&xbar[0]);
+      cl_mbar_init(&xbar[1]);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      cl_mbar_arm(&xbar[0], bytesA);
+      cl_mbar_arm(&xbar[1], bytesB);
+    }
+    if (rank > 0)
+    {
+      exL = cl_map(ex, rank - 1);
+      barL[0] = cl_map(&xbar[0], rank - 1);
+      barL[1] = cl_map(&xbar[1], rank - 1);
+    }
+    if (rank + 1 < cs)
+    {
+      exR = cl_map(ex, rank + 1);
+      barR[0] = cl_map(&xbar[0], rank + 1);
+      barR[1] = cl_map(&xbar[1], rank + 1);
+    }
+  }
+  // boundary row lr of r (which 0) or d (which 1), parity slot q -> the neighbours' imports,
+  // completing their phase-B (r) or phase-A (d) barrier
+  auto push_async = [&](int which, int q, int lr, double v) {
+    if (lr < H && exL)
+      st_async_f64(exL + 8u * static_cast<uint32_t>(((which * 2 + q) * 2 + 1) * H + lr), v, barL[which ^ 1]);
+    if (lr >= R - H && exR)
+      st_async_f64(exR + 8u * static_cast<uint32_t>(((which * 2 + q) * 2 + 0) * H + (lr - (R - H))), v,
+                   barR[which ^ 1]);
+  };
 
   load_ell_em_packed(P.A[p], c0, c0 + R, P.n, P.ea, reinterpret_cast<double *>(raw + P.off_av),
                      reinterpret_cast<unsigned long long *>(raw + P.off_ao), kV2TB);
@@ -879,34 +1010,42 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
       const unsigned long long *fo = reinterpret_cast<const unsigned long long *>(raw + P.off_fo[st]);
       double *out = tb[st & 1];
       const int span = R + 2 * hd;
-      // RPT + 1 rows per thread, entries outer / rows inner: independent
-      // accumulation chains in flight (ILP); per-row order is unchanged.
-      constexpr int K = RPT + 1;
-      int q[K];
-      bool ok[K];
-      double acc[K];
-      unsigned long long ow[K];
+      // K rows per thread, entries outer / rows inner: independent accumulation chains in
+      // flight (ILP); per-row order is unchanged.  K = RPT when the halo-extended span still
+      // fits RPT slots (no dead, predicated-off slot in the unrolled body), else RPT + 1.
+      auto rows_k = [&](auto kc) {
+        constexpr int K = decltype(kc)::value;
+        int q[K];
+        bool ok[K];
+        double acc[K];
+        unsigned long long ow[K];
 #pragma unroll
-      for (int j = 0; j < K; ++j)
-      {
-        q[j] = threadIdx.x + j * kV2TB;
-        const int64_t i = c0 - hd + q[j];
-        ok[j] = q[j] < span && i >= 0 && i < P.n;
-        acc[j] = 0.0;
-        ow[j] = ok[j] ? fo[q[j]] : 0ull;
-      }
+        for (int j = 0; j < K; ++j)
+        {
+          q[j] = threadIdx.x + j * kV2TB;
+          const int64_t i = c0 - hd + q[j];
+          ok[j] = q[j] < span && i >= 0 && i < P.n;
+          acc[j] = 0.0;
+          ow[j] = ok[j] ? fo[q[j]] : 0ull;
+        }
 #pragma unroll
-      for (int e = 0; e < (EC > 0 ? EC : E); ++e)
-      {
+        for (int e = 0; e < (EC > 0 ? EC : E); ++e)
+        {
+#pragma unroll
+          for (int j = 0; j < K; ++j)
+            if (ok[j])
+              acc[j] = __dadd_rn(acc[j], __dmul_rn(fv[e * span + q[j]], in[q[j] + hs - hd + off8(ow[j], e)]));
+        }
 #pragma unroll
         for (int j = 0; j < K; ++j)
           if (ok[j])
-            acc[j] = __dadd_rn(acc[j], __dmul_rn(fv[e * span + q[j]], in[q[j] + hs - hd + off8(ow[j], e)]));
-      }
-#pragma unroll
-      for (int j = 0; j < K; ++j)
-        if (ok[j])
-          out[q[j]] = acc[j];
+            out[q[j]] = acc[j];
+      };
+      constexpr int K = RPT + 1;
+      if (span <= RPT * kV2TB)
+        rows_k(std::integral_constant<int, RPT>{});
+      else
+        rows_k(std::integral_constant<int, RPT + 1>{});
       for (int qq = threadIdx.x + K * kV2TB; qq < span; qq += kV2TB) // only if span > K * TB
       {
         const int64_t i = c0 - hd + qq;
@@ -1075,7 +1214,10 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
       {
         const double dn = fresh ? r[j] : __dadd_rn(r[j], __dmul_rn(beta, dpad[H + lr]));
         dpad[H + lr] = dn;
-        push(sel_d, q ^ 1, lr, dn);
+        if (P.async_x)
+          push_async(1, q ^ 1, lr, dn);
+        else
+          push(sel_d, q ^ 1, lr, dn);
       }
     }
     fill_halo(0, q);
@@ -1097,9 +1239,20 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
       }
     }
     mark(3);
-    cta_sum_push<kV2TB, 2>(sh, pa, 2, cl, inboxA, cs, rank);
-    mark(4);
-    cl.sync();
+    if (P.async_x)
+    {
+      cta_sum_push_async<kV2TB, 2>(sh, pa, 2, inboxA, &xbar[0], cs, rank);
+      mark(4);
+      cl_mbar_wait(&xbar[0], static_cast<uint32_t>(q));
+      if (threadIdx.x == 0)
+        cl_mbar_arm(&xbar[0], bytesA); // next phase; peers send into it only after our phase-B partial
+    }
+    else
+    {
+      cta_sum_push<kV2TB, 2>(sh, pa, 2, cl, inboxA, cs, rank);
+      mark(4);
+      cl.sync();
+    }
     mark(5);
     double ta[2];
     warp_inbox_total<2>(inboxA, 2, cs, ta);
@@ -1123,12 +1276,25 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
         x[j] = __dadd_rn(x[j], __dmul_rn(alpha, dpad[H + lr]));
         r[j] = __dadd_rn(r[j], __dmul_rn(-alpha, w[j]));
         pb[0] = __dadd_rn(pb[0], __dmul_rn(r[j], r[j]));
-        push(sel_r, q ^ 1, lr, r[j]);
+        if (P.async_x)
+          push_async(0, q ^ 1, lr, r[j]);
+        else
+          push(sel_r, q ^ 1, lr, r[j]);
       }
     }
     mark(7);
-    cta_sum_push<kV2TB, 2>(sh, pb, 1, cl, inboxB, cs, rank);
-    cl.sync();
+    if (P.async_x)
+    {
+      cta_sum_push_async<kV2TB, 2>(sh, pb, 1, inboxB, &xbar[1], cs, rank);
+      cl_mbar_wait(&xbar[1], static_cast<uint32_t>(q));
+      if (threadIdx.x == 0)
+        cl_mbar_arm(&xbar[1], bytesB);
+    }
+    else
+    {
+      cta_sum_push<kV2TB, 2>(sh, pb, 1, cl, inboxB, cs, rank);
+      cl.sync();
+    }
     mark(8);
     double tb2[2];
     warp_inbox_total<2>(inboxB, 1, cs, tb2);
@@ -1394,6 +1560,9 @@ int cg_cluster_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, cons
     V.hist_cap = hist_cap;
     V.loop_iters = d_loop;
     V.prof = ctx->prof_dev;
+    V.async_x = 1;
+    if (const char *f = std::getenv("MGPU_CLUSTER_ASYNC")) // 0: cluster-barrier exchange (diagnostics)
+      V.async_x = f[0] != '0';
     if (v2_solve(ctx, V, static_cast<size_t>(cdev0) - sizeof(ClShared) - 1024))
       return 2;
   }
