@@ -885,7 +885,8 @@ struct V2Params
 
 // EC > 0: every operator row (A and each chain factor) holds exactly EC ELL entries, known at
 // compile time, so the entry loops unroll with constant offsets; EC = 0: runtime widths.
-template <int RPT, int EC = 0>
+// AX: asynchronous exchange (else cluster barriers); PR: per-phase clock64 profile (MGPU_PROFILE_PHASES)
+template <int RPT, int EC = 0, bool AX = true, bool PR = false>
 __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
 {
   cgrp::cluster_group cl = cgrp::this_cluster();
@@ -926,7 +927,7 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
   const uint32_t bytesA = static_cast<uint32_t>(8 * (2 * cs + H * nbrs));
   const uint32_t bytesB = static_cast<uint32_t>(8 * (cs + H * nbrs));
   uint32_t exL = 0, exR = 0, barL[2] = {0, 0}, barR[2] = {0, 0};
-  if (P.async_x)
+  if constexpr (AX)
   {
     if (threadIdx.x == 0)
     {
@@ -1182,7 +1183,7 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
     cl.sync(); // restarted r exports visible; the slots are free again
   };
 
-  const bool prof = P.prof && blockIdx.x == 0 && threadIdx.x == 0;
+  const bool prof = PR && P.prof && blockIdx.x == 0 && threadIdx.x == 0;
   long long pacc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long tmark = clock64();
   auto mark = [&](int k) {
@@ -1214,7 +1215,7 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
       {
         const double dn = fresh ? r[j] : __dadd_rn(r[j], __dmul_rn(beta, dpad[H + lr]));
         dpad[H + lr] = dn;
-        if (P.async_x)
+        if constexpr (AX)
           push_async(1, q ^ 1, lr, dn);
         else
           push(sel_d, q ^ 1, lr, dn);
@@ -1239,7 +1240,7 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
       }
     }
     mark(3);
-    if (P.async_x)
+    if constexpr (AX)
     {
       cta_sum_push_async<kV2TB, 2>(sh, pa, 2, inboxA, &xbar[0], cs, rank);
       mark(4);
@@ -1276,14 +1277,14 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
         x[j] = __dadd_rn(x[j], __dmul_rn(alpha, dpad[H + lr]));
         r[j] = __dadd_rn(r[j], __dmul_rn(-alpha, w[j]));
         pb[0] = __dadd_rn(pb[0], __dmul_rn(r[j], r[j]));
-        if (P.async_x)
+        if constexpr (AX)
           push_async(0, q ^ 1, lr, r[j]);
         else
           push(sel_r, q ^ 1, lr, r[j]);
       }
     }
     mark(7);
-    if (P.async_x)
+    if constexpr (AX)
     {
       cta_sum_push_async<kV2TB, 2>(sh, pb, 1, inboxB, &xbar[1], cs, rank);
       cl_mbar_wait(&xbar[1], static_cast<uint32_t>(q));
@@ -1400,9 +1401,10 @@ int v2_active_clusters(mgpu_ctx *ctx, const V2Params &P, size_t dyn)
 template <int RPT, int EC>
 void v2_launch_ec(mgpu_ctx *ctx, const V2Params &P, size_t dyn)
 {
-  MG_CUDA(cudaFuncSetAttribute(cg_cluster_v2<RPT, EC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(dyn)));
-  MG_CUDA(cudaFuncSetAttribute(cg_cluster_v2<RPT, EC>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  auto kern = !P.async_x ? cg_cluster_v2<RPT, EC, false>
+                         : (P.prof ? cg_cluster_v2<RPT, EC, true, true> : cg_cluster_v2<RPT, EC, true, false>);
+  MG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
+  MG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(P.l * P.cs));
   cfg.blockDim = dim3(kV2TB);
@@ -1415,7 +1417,7 @@ void v2_launch_ec(mgpu_ctx *ctx, const V2Params &P, size_t dyn)
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  MG_CUDA(cudaLaunchKernelEx(&cfg, cg_cluster_v2<RPT, EC>, P));
+  MG_CUDA(cudaLaunchKernelEx(&cfg, kern, P));
   check_launch(ctx, "cg_cluster_v2");
 }
 
