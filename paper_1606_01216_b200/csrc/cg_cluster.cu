@@ -969,7 +969,10 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
                        reinterpret_cast<double *>(raw + P.off_fv[st]),
                        reinterpret_cast<unsigned long long *>(raw + P.off_fo[st]), kV2TB);
   }
-  double r[RPT], x[RPT], w[RPT], bv[RPT];
+  double r[RPT], x[RPT], w[RPT];
+  // b is re-read from global memory by the (rare) true-residual checks: not register-resident
+  auto b_at = [&](int lr) { return P.B[static_cast<int64_t>(p) * P.ldb + c0 + lr]; };
+  double bv[RPT];
   double pk[2] = {0.0, 0.0};
 #pragma unroll
   for (int j = 0; j < RPT; ++j)
@@ -1137,7 +1140,7 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
       if (lr < R)
       {
         sol[j] = t[lr + hs];
-        y[j] = __dsub_rn(bv[j], y[j]);
+        y[j] = __dsub_rn(b_at(lr), y[j]);
         q2[0] = __dadd_rn(q2[0], __dmul_rn(y[j], y[j]));
       }
     }
