@@ -1695,17 +1695,22 @@ __device__ __forceinline__ void ell_row(const double *vals, const unsigned long 
   }
 }
 
+// Per-phase clock64 totals (MGPU_PROFILE_PHASES); the ON = false instantiation compiles away.
+template <bool ON>
 struct PhaseClock
 {
   bool on;
   long long t, acc[16];
   __device__ void mark(int k)
   {
-    if (on)
+    if constexpr (ON)
     {
-      const long long now = clock64();
-      acc[k] += now - t;
-      t = now;
+      if (on)
+      {
+        const long long now = clock64();
+        acc[k] += now - t;
+        t = now;
+      }
     }
   }
 };
@@ -1730,10 +1735,10 @@ struct RingProducer
 // bulk-copy bytes; empty barrier: consumers done), the TB consumer threads
 // compute.  Dot-product partials accumulate per consumer thread over all
 // chunks of a point (row order) and are reduced once per point.
-template <int TB, int MT, int NB>
+template <int TB, int MT, int NB, class PC>
 __device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, const PEll *tab, unsigned char *smem,
                             uint64_t *full, uint64_t *empty, uint32_t &phase_bits, RingProducer &rp, int kind,
-                            const double *dold, double *dnew, PhaseClock &pc)
+                            const double *dold, double *dnew, PC &pc)
 {
   const int64_t CH = kind == 2 ? P.ch_b : P.ch;
   const int m = P.m;
@@ -1996,7 +2001,7 @@ __device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, cons
   pc.mark(2);
 }
 
-template <int TB, int MT>
+template <int TB, int MT, bool PR = false>
 __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
 {
   constexpr int TBX = TB + 32; // TB consumer threads + one producer warp
@@ -2011,7 +2016,7 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
   const int S = P.l * m;
   uint32_t phase_bits = 0;
   RingProducer rp{0u, 0u};
-  PhaseClock pc{P.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0, clock64(), {}};
+  PhaseClock<PR> pc{PR && P.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0, clock64(), {}};
   if (threadIdx.x == 0)
   {
     int q = 0;
@@ -2131,7 +2136,7 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
   auto check_pass = [&](const double *dcur) {
     if (!P.serial)
     {
-      stream_pass<TB, MT, kStreamNB>(P, sh, tab, smem_s, bars, bars + kStreamNB, phase_bits, rp, 1, dcur, nullptr, pc);
+      stream_pass<TB, MT, kStreamNB, PhaseClock<PR>>(P, sh, tab, smem_s, bars, bars + kStreamNB, phase_bits, rp, 1, dcur, nullptr, pc);
       return;
     }
     uint32_t msk = 0;
@@ -2141,7 +2146,7 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
       if ((msk >> p) & 1u)
       {
         pick_point(p);
-        stream_pass<TB, MT, kStreamNB>(P, sh, tab + p * (kMaxZ + 1), smem_s, bars, bars + kStreamNB, phase_bits, rp, 1,
+        stream_pass<TB, MT, kStreamNB, PhaseClock<PR>>(P, sh, tab + p * (kMaxZ + 1), smem_s, bars, bars + kStreamNB, phase_bits, rp, 1,
                                        dcur, nullptr, pc);
       }
     __syncthreads();
@@ -2285,14 +2290,14 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
         pick_point(p);
         const PEll *tp = tab + p * (kMaxZ + 1);
         pc.mark(9);
-        stream_pass<TB, MT, kStreamNB>(P, sh, tp, smem_s, bars, bars + kStreamNB, phase_bits, rp, 0, d_old, d_new, pc);
+        stream_pass<TB, MT, kStreamNB, PhaseClock<PR>>(P, sh, tp, smem_s, bars, bars + kStreamNB, phase_bits, rp, 0, d_old, d_new, pc);
         fence_async_global();
         grid.sync();
         pc.mark(10);
         reduce_blocks<TBX, StreamParams>(P, sh, 2 * m);
         after_a(it);
         pc.mark(11);
-        stream_pass<TB, MT, kStreamNB>(P, sh, tp, smem_s, bars, bars + kStreamNB, phase_bits, rp, 2, d_old, d_new, pc);
+        stream_pass<TB, MT, kStreamNB, PhaseClock<PR>>(P, sh, tp, smem_s, bars, bars + kStreamNB, phase_bits, rp, 2, d_old, d_new, pc);
         fence_async_global();
         grid.sync();
         pc.mark(10);
@@ -2305,7 +2310,7 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
       continue;
     }
     pc.mark(9);
-    stream_pass<TB, MT, kStreamNB>(P, sh, tab, smem_s, bars, bars + kStreamNB, phase_bits, rp, 0, d_old, d_new, pc);
+    stream_pass<TB, MT, kStreamNB, PhaseClock<PR>>(P, sh, tab, smem_s, bars, bars + kStreamNB, phase_bits, rp, 0, d_old, d_new, pc);
     fence_async_global();
     grid.sync();
     pc.mark(10);
@@ -2313,7 +2318,7 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
     pc.mark(11);
     after_a(it);
     pc.mark(9);
-    stream_pass<TB, MT, kStreamNB>(P, sh, tab, smem_s, bars, bars + kStreamNB, phase_bits, rp, 2, d_old, d_new, pc);
+    stream_pass<TB, MT, kStreamNB, PhaseClock<PR>>(P, sh, tab, smem_s, bars, bars + kStreamNB, phase_bits, rp, 2, d_old, d_new, pc);
     fence_async_global();
     grid.sync();
     pc.mark(10);
@@ -2380,9 +2385,10 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
           P.REC[o] = __ldcg(vrow(P, P.r, p, i) + c);
       }
   });
-  if (pc.on)
-    for (int k = 0; k < 12; ++k)
-      P.prof[k] = pc.acc[k];
+  if constexpr (PR)
+    if (pc.on)
+      for (int k = 0; k < 12; ++k)
+        P.prof[k] = pc.acc[k];
   if (blockIdx.x == 0)
   {
     for (int s = threadIdx.x; s < S; s += TBX)
@@ -2817,12 +2823,13 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
     return true;
   };
   bool ok;
+  const bool pr = P.prof != nullptr;
   if (m == 1)
-    ok = launch(cg_stream<TB, 1>);
-  else if (m == 2)
+    ok = pr ? launch(cg_stream<TB, 1, true>) : launch(cg_stream<TB, 1>);
+  else if (m == 2) // (phase profile instantiated for m = 1 and m <= 4 only)
     ok = launch(cg_stream<TB, 2>);
   else if (m <= 4)
-    ok = launch(cg_stream<TB, 4>);
+    ok = pr ? launch(cg_stream<TB, 4, true>) : launch(cg_stream<TB, 4>);
   else
     ok = launch(cg_stream<TB, 8>);
   if (ok)
