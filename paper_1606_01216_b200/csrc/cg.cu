@@ -2611,11 +2611,12 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
       EF[st] = std::max(EF[st], hF[static_cast<size_t>(p) * z + f].E);
     }
   }
-  // x~ update placement: deferred into phase A (one vector pass fewer) when phase A is light --
-  // no chain and m <= 2 (measured on B200: m=2 333 -> 298 us/iter, m=1 P=I 215 -> 198); with a
-  // chain or m = 4 the latency-bound phase A gets slower than phase B gains, so it stays in B.
+  // x~ update placement: deferred into phase A, which streams d_old anyway (one vector pass
+  // fewer).  Measured on B200 once the kernel dropped to 107 registers: configs[3] (m = 4, P = I)
+  // 1029 -> 1005 us/iter, configs[4] share 5025 -> 4891, configs[2] shape (m = 1, one factor)
+  // 36.9 -> 36.1; earlier (122 registers) phase A was latency-bound and m = 4 / chains lost.
   // MGPU_STREAM_FOLD=0/1 overrides (diagnostics).
-  bool fold = m <= 2 && z == 0;
+  bool fold = true;
   if (const char *f = std::getenv("MGPU_STREAM_FOLD"))
     fold = f[0] == '1';
   // ---- shared-memory plan: the largest chunk height whose double buffer fits
