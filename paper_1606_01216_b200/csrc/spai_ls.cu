@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <memory>
 #include <vector>
 
@@ -412,6 +413,229 @@ __global__ void ls_columns(int64_t n, int l, DCsr pat, DCsr At, int64_t at_strid
     out_vals[jb + c] = sm.m[c];
 }
 
+// ---------------------------------------------------------------- LS columns, one LANE per column
+//
+// The same column problem as ls_columns, solved start to finish by one thread: 32 columns per
+// warp with every lane busy (the group kernel runs the leader-only steps -- union of I, the
+// Householder scalars, back-substitution -- on one lane in eight).  Per-lane scratch lives in
+// shared memory at an odd stride in 8-byte words, so the 32 lanes' same-offset accesses fall
+// in distinct banks.  Q is never stored whole: column c of Q is rebuilt in one NI-vector
+// (H_0 .. H_c applied to e_c, the same reflector loop as thin_qr's Q formation), sign-fixed
+// and dotted with e, which gives y_c with exactly the operations of the group kernel and the
+// oracle (bitwise equal).  Envelope: |J| <= NJ, |I| <= NI; a larger column sets `overflow` and
+// the host reruns the batch on the group kernels.
+template <int NJ, int NI>
+struct LaneLayout
+{
+  static constexpr int kW = 0;                // W[c * NI + i]: S, then Householder vectors / R
+  static constexpr int kQ = kW + NJ * NI;     // one column of Q
+  static constexpr int kE = kQ + NI;          // right-hand side restricted to I
+  static constexpr int kDiag = kE + NI;       // R diagonal (alpha)
+  static constexpr int kTau = kDiag + NJ;     // reflector scales, then |R_cc|
+  static constexpr int kM = kTau + NJ;        // y, then the solution
+  static constexpr int kI = kM + NJ;          // I (int32, NI of them = NI / 2 words)
+  static constexpr int kWords0 = kI + (NI + 1) / 2;
+  static constexpr int kWords = kWords0 | 1; // odd stride: conflict-free same-offset accesses
+};
+
+template <int NJ, int NI>
+__global__ void __launch_bounds__(64) ls_columns_lane(int64_t n, int l, DCsr pat, DCsr At, int64_t at_stride,
+                                                       DCsr Kot, int64_t ko_stride, bool update,
+                                                       double *__restrict__ out_base, int64_t out_stride,
+                                                       unsigned long long *__restrict__ err, int *__restrict__ overflow)
+{
+  using L = LaneLayout<NJ, NI>;
+  extern __shared__ __align__(16) double lane_raw[];
+  double *base = lane_raw + static_cast<size_t>(threadIdx.x) * L::kWords;
+  double *W = base + L::kW, *q = base + L::kQ, *e = base + L::kE;
+  double *diag = base + L::kDiag, *tau = base + L::kTau, *mv = base + L::kM;
+  int32_t *I = reinterpret_cast<int32_t *>(base + L::kI);
+  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g >= static_cast<int64_t>(l) * n)
+    return;
+  const int p = static_cast<int>(g / n);
+  const int64_t j = g - static_cast<int64_t>(p) * n;
+  const double *atv = At.v + p * at_stride;
+  const double *kov = update ? Kot.v + p * ko_stride : nullptr;
+  double *out_vals = out_base + p * out_stride;
+  const int64_t jb = pat.rp[j];
+  const int nj = static_cast<int>(pat.rp[j + 1] - jb);
+  if (nj == 0)
+    return;
+  if (nj > NJ)
+  {
+    atomicOr(overflow, 1);
+    return;
+  }
+  // ---- I = sorted union of the rows of A(:, J) (insertion, duplicates skipped)
+  int ni = 0;
+  for (int c = 0; c < nj; ++c)
+  {
+    const int32_t k = pat.ci[jb + c];
+    const int64_t t1 = At.rp[k + 1];
+    for (int64_t t = At.rp[k]; t < t1; ++t)
+    {
+      const int32_t row = At.ci[t];
+      int pos = ni;
+      while (pos > 0 && I[pos - 1] > row)
+        --pos;
+      if (pos > 0 && I[pos - 1] == row)
+        continue;
+      if (ni == NI)
+      {
+        atomicOr(overflow, 1);
+        return;
+      }
+      for (int u = ni; u > pos; --u)
+        I[u] = I[u - 1];
+      I[pos] = row;
+      ++ni;
+    }
+  }
+  if (ni < nj)
+  {
+    report(err, g, MGPU_ERR_NUMERICAL);
+    return;
+  }
+  auto find = [&](int32_t row) {
+    int lo = 0, hi = ni;
+    while (lo < hi)
+    {
+      const int mid = (lo + hi) >> 1;
+      if (I[mid] < row)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    return lo;
+  };
+  // ---- S = A(I, J), column-major
+  for (int c = 0; c < nj; ++c)
+  {
+    double *col = W + c * NI;
+    for (int i = 0; i < ni; ++i)
+      col[i] = 0.0;
+    const int32_t k = pat.ci[jb + c];
+    const int64_t t1 = At.rp[k + 1];
+    for (int64_t t = At.rp[k]; t < t1; ++t)
+      col[find(At.ci[t])] = atv[t];
+  }
+  // ---- e = rhs restricted to I
+  for (int i = 0; i < ni; ++i)
+    e[i] = 0.0;
+  if (update)
+  {
+    for (int64_t t = Kot.rp[j]; t < Kot.rp[j + 1]; ++t)
+    {
+      const int32_t row = Kot.ci[t];
+      const int lo = find(row);
+      if (lo < ni && I[lo] == row)
+        e[lo] = kov[t];
+    }
+  }
+  else
+  {
+    for (int i = 0; i < ni; ++i)
+      if (I[i] == j)
+        e[i] = 1.0;
+  }
+  // ---- thin_qr (dense.cpp:153-246): frob_norm tolerance in column-major order
+  double acc = 0.0;
+  for (int c = 0; c < nj; ++c)
+    for (int i = 0; i < ni; ++i)
+      acc = __dadd_rn(acc, __dmul_rn(W[c * NI + i], W[c * NI + i]));
+  const double anorm = sqrt(acc);
+  const double tol = 1e-12 * (anorm > 0.0 ? anorm : 1.0);
+  bool deficient = false;
+  for (int k = 0; k < nj; ++k)
+  {
+    const int len = ni - k;
+    double *x = W + k * NI + k;
+    const double sigma = sqrt(dot_serial(x, x, len));
+    if (sigma <= tol)
+    {
+      diag[k] = 0.0;
+      tau[k] = 0.0;
+      for (int i = 0; i < len; ++i)
+        x[i] = 0.0;
+      deficient = true;
+      continue;
+    }
+    const double alpha = x[0] >= 0.0 ? -sigma : sigma;
+    x[0] = __dsub_rn(x[0], alpha);
+    const double vtv = dot_serial(x, x, len);
+    const double tk = vtv > 0.0 ? 2.0 / vtv : 0.0;
+    tau[k] = tk;
+    diag[k] = alpha;
+    if (tk != 0.0)
+      for (int c = k + 1; c < nj; ++c)
+      {
+        double *y = W + c * NI + k;
+        const double sc = __dmul_rn(tk, dot_serial(x, y, len));
+        axpy_serial(len, -sc, x, y);
+      }
+  }
+  if (deficient) // rank < |J|
+  {
+    report(err, g, MGPU_ERR_NUMERICAL);
+    return;
+  }
+  // ---- y_c = (sign-fixed column c of Q = H_0 ... H_{nj-1} e_c)^T e
+  for (int c = 0; c < nj; ++c)
+  {
+    for (int i = 0; i < ni; ++i)
+      q[i] = 0.0;
+    q[c] = 1.0;
+    for (int k = c < nj - 1 ? c : nj - 1; k >= 0; --k)
+    {
+      if (tau[k] == 0.0)
+        continue;
+      const double *v = W + k * NI + k;
+      const int len = ni - k;
+      const double sc = __dmul_rn(tau[k], dot_serial(v, q + k, len));
+      axpy_serial(len, -sc, v, q + k);
+    }
+    if (diag[c] < 0.0)
+      for (int i = 0; i < ni; ++i)
+        q[i] = __dmul_rn(q[i], -1.0);
+    mv[c] = dot_serial(q, e, ni);
+  }
+  // ---- sign fix of R's off-diagonal rows (R(k, c) = W[c][k], c > k), |R_cc|
+  for (int c = 0; c < nj; ++c)
+  {
+    for (int k = 0; k < c; ++k)
+      if (diag[k] < 0.0)
+        W[c * NI + k] = -W[c * NI + k];
+    tau[c] = diag[c] < 0.0 ? -diag[c] : diag[c];
+  }
+  // ---- back-substitution R m = y (acc = y_k; acc -= R_kq m_q, q ascending)
+  for (int k = nj - 1; k >= 0; --k)
+  {
+    double a = mv[k];
+    for (int c = k + 1; c < nj; ++c)
+      a = __dsub_rn(a, __dmul_rn(W[c * NI + k], mv[c]));
+    mv[k] = a / tau[k];
+  }
+  for (int c = 0; c < nj; ++c)
+    out_vals[jb + c] = mv[c];
+}
+
+template <int NJ, int NI>
+void launch_ls_lane(mgpu_ctx *ctx, int64_t n, int l, DCsr pat, DCsr At, int64_t at_stride, DCsr Kot, int64_t ko_stride,
+                    bool update, double *out, int64_t out_stride, unsigned long long *err, int *ovf)
+{
+  constexpr int kThreadsPerBlock = 64;
+  constexpr size_t smem = sizeof(double) * LaneLayout<NJ, NI>::kWords * kThreadsPerBlock;
+  static_assert(smem <= 200 * 1024, "LS lane shared memory");
+  MG_CUDA(cudaFuncSetAttribute(ls_columns_lane<NJ, NI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem)));
+  const int64_t cols = static_cast<int64_t>(l) * n;
+  const unsigned grid = static_cast<unsigned>((cols + kThreadsPerBlock - 1) / kThreadsPerBlock);
+  ls_columns_lane<NJ, NI><<<grid, kThreadsPerBlock, smem, ctx->stream>>>(n, l, pat, At, at_stride, Kot, ko_stride,
+                                                                         update, out, out_stride, err, ovf);
+  check_launch(ctx, "ls_columns_lane");
+}
+
 template <int G, int NI, int WARPS>
 void launch_ls(mgpu_ctx *ctx, int64_t n, int l, DCsr pat, DCsr At, int64_t at_stride, DCsr Kot, int64_t ko_stride,
                bool update, double *out, int64_t out_stride, unsigned long long *err, int *ovf)
@@ -436,15 +660,22 @@ void run_ls(mgpu_ctx *ctx, int64_t n, int l, int maxrow, DCsr pat, DCsr At, int6
   if (n == 0 || l == 0)
     return;
   DBuf err(sizeof(unsigned long long), ctx->stream), ovf(sizeof(int), ctx->stream);
-  for (int cfg = 0; cfg < 3; ++cfg)
+  // lane-per-column envelopes first (|J| <= 6 / 8 pattern entries, |I| <= 14 / 16 rows), then
+  // the lane-group kernels; MGPU_LS_GROUP=1 skips the lane kernels (diagnostics)
+  const bool lanes = !std::getenv("MGPU_LS_GROUP");
+  for (int cfg = -2; cfg < 3; ++cfg)
   {
-    const int G = cfg == 0 ? 8 : (cfg == 1 ? 16 : 32);
-    if (maxrow > G)
+    const int G = cfg == -2 ? 6 : (cfg == -1 ? 8 : (cfg == 0 ? 8 : (cfg == 1 ? 16 : 32)));
+    if (maxrow > G || (cfg < 0 && !lanes))
       continue;
     MG_CUDA(cudaMemsetAsync(err.ptr, 0xff, sizeof(unsigned long long), ctx->stream));
     MG_CUDA(cudaMemsetAsync(ovf.ptr, 0, sizeof(int), ctx->stream));
     auto *ev = err.as<unsigned long long>();
-    if (cfg == 0)
+    if (cfg == -2)
+      launch_ls_lane<6, 14>(ctx, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev, ovf.as<int>());
+    else if (cfg == -1)
+      launch_ls_lane<8, 16>(ctx, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev, ovf.as<int>());
+    else if (cfg == 0)
       launch_ls<8, 16, 4>(ctx, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev, ovf.as<int>());
     else if (cfg == 1)
       launch_ls<16, 32, 2>(ctx, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev, ovf.as<int>());
