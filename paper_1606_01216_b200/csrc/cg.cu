@@ -22,6 +22,8 @@
 #include <cstdlib>
 #include <utility>
 #include <cmath>
+#include <cstring>
+#include <chrono>
 #include <vector>
 
 #include "internal.cuh"
@@ -2845,15 +2847,25 @@ void cg_batch(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_
               double *ms_out, int64_t *loop_out)
 {
   cudaStream_t s = ctx->stream;
+  host_mark("cg_batch enter");
   int halo[kMaxZ + 1] = {0};
   int hmax = 0;
   const bool banded = ctx->cg_path != 1 && band_plan(ctx, l, A, z, chains, m, halo, &hmax);
+  host_mark("band_plan done");
   const int64_t vec = static_cast<int64_t>(l) * n * m;
   const int64_t vbytes = sizeof(double) * (vec > 0 ? vec : 1);
   DBuf b, xt, r, d, w, t0, t1; // grid kernels' vectors, allocated only if those kernels run
   const int S = l * m;
-  DBuf d_it(sizeof(int64_t) * S, s), d_conv(sizeof(int) * S, s), d_st(sizeof(int) * S, s), d_bd(sizeof(int64_t) * S, s);
-  DBuf d_loop(sizeof(int64_t), s);
+  // per-system results in ONE device block (iterations, breakdown iteration, loop count,
+  // converged, status), read back with one copy into the context's pinned staging buffer
+  const size_t o_bd = sizeof(int64_t) * S, o_loop = 2 * sizeof(int64_t) * S, o_conv = o_loop + sizeof(int64_t),
+               o_st = o_conv + sizeof(int) * S, res_bytes = o_st + sizeof(int) * S;
+  DBuf res(res_bytes, s);
+  auto *p_it = res.as<int64_t>();
+  auto *p_bd = reinterpret_cast<int64_t *>(res.as<char>() + o_bd);
+  auto *p_loop = reinterpret_cast<int64_t *>(res.as<char>() + o_loop);
+  auto *p_conv = reinterpret_cast<int *>(res.as<char>() + o_conv);
+  auto *p_st = reinterpret_cast<int *>(res.as<char>() + o_st);
   DBuf d_hist(hist ? sizeof(double) * static_cast<size_t>(S) * hist_cap : 8, s);
   std::vector<DCsr> hA(static_cast<size_t>(l)), hF(static_cast<size_t>(l) * (z > 0 ? z : 1));
   for (int p = 0; p < l; ++p)
@@ -2866,19 +2878,21 @@ void cg_batch(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_
   MG_CUDA(cudaMemcpyAsync(dA.ptr, hA.data(), sizeof(DCsr) * hA.size(), cudaMemcpyHostToDevice, s));
   MG_CUDA(cudaMemcpyAsync(dF.ptr, hF.data(), sizeof(DCsr) * hF.size(), cudaMemcpyHostToDevice, s));
 
+  host_mark("descriptors staged");
   DBuf partial, totals, counter, segs, pblk;
   int clustered = 0;
   if (banded && ctx->cg_path != 2 && ctx->cg_path != 4)
   {
     // systems small enough to live on chip: one cluster per point, no grid barrier
-    MG_CUDA(cudaMemsetAsync(d_loop.ptr, 0, sizeof(int64_t), s));
+    MG_CUDA(cudaMemsetAsync(p_loop, 0, sizeof(int64_t), s));
     MG_CUDA(cudaEventRecord(ctx->ev0, s));
     clustered = cg_cluster_solve(ctx, l, A, z, chains, n, m, B_dev, ldb, halo, rtol, maxit, X_dev, REC_dev, TR_dev,
-                                 d_it.as<int64_t>(), d_conv.as<int>(), d_st.as<int>(), d_bd.as<int64_t>(),
+                                 p_it, p_conv, p_st, p_bd,
                                  hist ? d_hist.as<double>() : nullptr, hist_cap,
-                                 reinterpret_cast<unsigned long long *>(d_loop.ptr), dA.as<DCsr>(), dF.as<DCsr>());
+                                 reinterpret_cast<unsigned long long *>(p_loop), dA.as<DCsr>(), dF.as<DCsr>());
     if (clustered)
       MG_CUDA(cudaEventRecord(ctx->ev1, s));
+    host_mark("cluster launched");
   }
   bool streamed = false;
   // streaming pays once a block's share of the batch (rows x columns) hides the
@@ -2891,10 +2905,10 @@ void cg_batch(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_
   const bool stream_pays = static_cast<int64_t>(l) * n * m >= static_cast<int64_t>(2048) * ctx->num_sms && z <= 3;
   if (banded && !clustered && (ctx->cg_path == 4 || (ctx->cg_path == 0 && stream_pays)))
   {
-    MG_CUDA(cudaMemsetAsync(d_loop.ptr, 0, sizeof(int64_t), s));
+    MG_CUDA(cudaMemsetAsync(p_loop, 0, sizeof(int64_t), s));
     streamed = stream_solve(ctx, l, A, z, chains, n, m, B_dev, ldb, halo, hmax, rtol, maxit, X_dev, REC_dev, TR_dev,
-                            d_it.as<int64_t>(), d_conv.as<int>(), d_st.as<int>(), d_bd.as<int64_t>(),
-                            hist ? d_hist.as<double>() : nullptr, hist_cap, d_loop.as<int64_t>());
+                            p_it, p_conv, p_st, p_bd,
+                            hist ? d_hist.as<double>() : nullptr, hist_cap, p_loop);
   }
   if (!clustered && !streamed)
   {
@@ -2983,13 +2997,13 @@ void cg_batch(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_
     P.X = X_dev;
     P.REC = REC_dev;
     P.TR = TR_dev;
-    P.iters = d_it.as<int64_t>();
-    P.conv = d_conv.as<int>();
-    P.status = d_st.as<int>();
-    P.bd_iter = d_bd.as<int64_t>();
+    P.iters = p_it;
+    P.conv = p_conv;
+    P.status = p_st;
+    P.bd_iter = p_bd;
     P.hist = hist ? d_hist.as<double>() : nullptr;
     P.hist_cap = hist_cap;
-    P.loop_iters = d_loop.as<int64_t>();
+    P.loop_iters = p_loop;
     MG_CUDA(cudaEventRecord(ctx->ev0, s));
     if (m == 1)
       launch_banded_rpt<1024, 1>(ctx, P);
@@ -3039,13 +3053,13 @@ void cg_batch(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_
     P.X = X_dev;
     P.REC = REC_dev;
     P.TR = TR_dev;
-    P.iters = d_it.as<int64_t>();
-    P.conv = d_conv.as<int>();
-    P.status = d_st.as<int>();
-    P.bd_iter = d_bd.as<int64_t>();
+    P.iters = p_it;
+    P.conv = p_conv;
+    P.status = p_st;
+    P.bd_iter = p_bd;
     P.hist = hist ? d_hist.as<double>() : nullptr;
     P.hist_cap = hist_cap;
-    P.loop_iters = d_loop.as<int64_t>();
+    P.loop_iters = p_loop;
     MG_CUDA(cudaEventRecord(ctx->ev0, s));
     if (m == 1)
       launch_cg<1>(ctx, P);
@@ -3058,16 +3072,20 @@ void cg_batch(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_
     MG_CUDA(cudaEventRecord(ctx->ev1, s));
   }
 
-  MG_CUDA(cudaMemcpyAsync(iters, d_it.ptr, sizeof(int64_t) * S, cudaMemcpyDeviceToHost, s));
-  MG_CUDA(cudaMemcpyAsync(conv, d_conv.ptr, sizeof(int) * S, cudaMemcpyDeviceToHost, s));
-  MG_CUDA(cudaMemcpyAsync(status, d_st.ptr, sizeof(int) * S, cudaMemcpyDeviceToHost, s));
-  MG_CUDA(cudaMemcpyAsync(bd, d_bd.ptr, sizeof(int64_t) * S, cudaMemcpyDeviceToHost, s));
+  host_mark("results requested");
+  char *hres = static_cast<char *>(pinned_scratch(ctx, res_bytes));
+  MG_CUDA(cudaMemcpyAsync(hres, res.ptr, res_bytes, cudaMemcpyDeviceToHost, s));
   if (hist)
     MG_CUDA(cudaMemcpyAsync(hist, d_hist.ptr, sizeof(double) * static_cast<size_t>(S) * hist_cap,
                             cudaMemcpyDeviceToHost, s));
-  int64_t loop = 0;
-  MG_CUDA(cudaMemcpyAsync(&loop, d_loop.ptr, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   MG_CUDA(cudaStreamSynchronize(s));
+  std::memcpy(iters, hres, sizeof(int64_t) * S);
+  std::memcpy(bd, hres + o_bd, sizeof(int64_t) * S);
+  std::memcpy(conv, hres + o_conv, sizeof(int) * S);
+  std::memcpy(status, hres + o_st, sizeof(int) * S);
+  int64_t loop = 0;
+  std::memcpy(&loop, hres + o_loop, sizeof(int64_t));
+  host_mark("results read");
   float ms = 0.f;
   MG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
   *ms_out += ms;
@@ -3085,6 +3103,7 @@ extern "C" int mgpu_cg_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int
                              mgpu_memkind where, mgpu_cg_out *out)
 {
   return guard(ctx, [&] {
+    host_mark("mgpu_cg_solve enter");
     MG_ARG(l >= 1 && A != nullptr && B != nullptr && out != nullptr, "pcg_solve: null argument");
     MG_ARG(z >= 0 && (z == 0 || chains != nullptr), "pcg_solve: bad preconditioner chain");
     MG_ARG(m >= 1 && n >= 0, "block_solve: right-hand-side rows do not match the operator dimension");

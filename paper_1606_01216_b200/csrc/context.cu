@@ -1,4 +1,5 @@
 // Context, error state, CSR residency and the deterministic reduction.
+#include <chrono>
 #include <climits>
 #include <cstdlib>
 #include <cstring>
@@ -10,6 +11,32 @@
 
 namespace mgpu
 {
+
+// MGPU_HOST_TRACE=1: host timestamps (steady clock, microseconds) on stderr (diagnostics).
+void host_mark(const char *what)
+{
+  static const bool on = std::getenv("MGPU_HOST_TRACE") != nullptr;
+  if (!on)
+    return;
+  const double us =
+      std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  std::fprintf(stderr, "[host %10.1f us] %s\n", us, what);
+}
+
+void *pinned_scratch(mgpu_ctx *ctx, size_t bytes)
+{
+  if (bytes > ctx->pin_bytes)
+  {
+    if (ctx->pin)
+      MG_CUDA(cudaFreeHost(ctx->pin));
+    ctx->pin = nullptr;
+    ctx->pin_bytes = 0;
+    const size_t want = bytes < 4096 ? 4096 : bytes;
+    MG_CUDA(cudaMallocHost(&ctx->pin, want));
+    ctx->pin_bytes = want;
+  }
+  return ctx->pin;
+}
 
 void set_error(mgpu_ctx *ctx, const Error &e)
 {
@@ -291,6 +318,8 @@ int mgpu_ctx_destroy(mgpu_ctx *ctx)
     cudaStreamDestroy(ctx->stream);
   if (ctx->blas)
     cublasDestroy(static_cast<cublasHandle_t>(ctx->blas));
+  if (ctx->pin)
+    cudaFreeHost(ctx->pin);
   if (ctx->prof_dev)
   {
     long long h[16] = {0};
@@ -473,7 +502,8 @@ int mgpu_csr_free(mgpu_csr *a)
     cudaFreeAsync(a->row_ptr, s);
     cudaFreeAsync(a->col_idx, s);
   }
-  cudaFreeAsync(a->values, s);
+  if (!a->shared_values)
+    cudaFreeAsync(a->values, s);
   delete a;
   return MGPU_OK;
 }

@@ -19,6 +19,11 @@
 
 namespace mgpu
 {
+// The context's pinned host staging buffer, at least `bytes` long.  Every user copies into it,
+// synchronises the stream and unpacks before returning, so one buffer per context suffices.
+void *pinned_scratch(mgpu_ctx *ctx, size_t bytes);
+// MGPU_HOST_TRACE=1: prints a steady-clock host timestamp and `what` on stderr (diagnostics)
+void host_mark(const char *what);
 
 // A C++ exception carrying an mgpu_status; converted at the C boundary.
 struct Error : std::runtime_error
@@ -132,6 +137,8 @@ struct mgpu_ctx
   int cg_path = 0;      // 0 auto, 1 force general, 2 force banded grid kernel, 3 cluster v1 only, 4 stream (no cluster)
   long long *prof_dev = nullptr; // diagnostics: per-phase clock64 totals of the cluster kernel (MGPU_PROFILE_PHASES)
   void *blas = nullptr;          // cublasHandle_t, created on first dense product (project.cu)
+  void *pin = nullptr;           // pinned host staging for small device -> host reads (grown on demand)
+  size_t pin_bytes = 0;
   // last error
   int last_status = MGPU_OK;
   int64_t err_index = -1, err_col = -1, err_point = -1;
@@ -151,6 +158,8 @@ struct mgpu_csr
   // set when row_ptr / col_idx belong to a structure shared by several matrices (the
   // factors of one batched LS-SPAI build): the last owner frees it (stream-ordered)
   std::shared_ptr<void> shared_structure;
+  // set when `values` is a slice of one allocation shared by a batch of factors
+  std::shared_ptr<void> shared_values;
 
   mgpu::DCsr view() const { return {row_ptr, col_idx, values}; }
 };

@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
+#include <cstring>
 #include <memory>
 #include <vector>
 
@@ -413,6 +414,17 @@ __global__ void ls_columns(int64_t n, int l, DCsr pat, DCsr At, int64_t at_strid
     out_vals[jb + c] = sm.m[c];
 }
 
+// Longest row of a CSR structure (warp max, one atomic per warp).
+__global__ void ls_max_row(int64_t nrows, const int64_t *__restrict__ rp, int *out)
+{
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  int len = i < nrows ? static_cast<int>(rp[i + 1] - rp[i]) : 0;
+  for (int off = 16; off > 0; off >>= 1)
+    len = max(len, __shfl_xor_sync(0xffffffffu, len, off));
+  if ((threadIdx.x & 31) == 0 && len > 0)
+    atomicMax(out, len);
+}
+
 // ---------------------------------------------------------------- LS columns, one LANE per column
 //
 // The same column problem as ls_columns, solved start to finish by one thread: 32 columns per
@@ -655,7 +667,8 @@ void launch_ls(mgpu_ctx *ctx, int64_t n, int l, DCsr pat, DCsr At, int64_t at_st
 // column; throws the lowest failing (point, column) like the reference's
 // sequential column loop would.
 void run_ls(mgpu_ctx *ctx, int64_t n, int l, int maxrow, DCsr pat, DCsr At, int64_t at_stride, DCsr Kot,
-            int64_t ko_stride, bool update, double *out, int64_t out_stride)
+            int64_t ko_stride, bool update, double *out, int64_t out_stride, const int *extra_dev = nullptr,
+            int *extra_host = nullptr)
 {
   if (n == 0 || l == 0)
     return;
@@ -681,11 +694,18 @@ void run_ls(mgpu_ctx *ctx, int64_t n, int l, int maxrow, DCsr pat, DCsr At, int6
       launch_ls<16, 32, 2>(ctx, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev, ovf.as<int>());
     else
       launch_ls<32, 64, 1>(ctx, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev, ovf.as<int>());
-    unsigned long long h = 0;
-    int h_ovf = 0;
-    MG_CUDA(cudaMemcpyAsync(&h_ovf, ovf.ptr, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    MG_CUDA(cudaMemcpyAsync(&h, err.ptr, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    // one synchronisation returns the error key, the overflow flag and the caller's extra value
+    auto *hp = static_cast<unsigned long long *>(pinned_scratch(ctx, 3 * sizeof(unsigned long long)));
+    MG_CUDA(cudaMemcpyAsync(hp, err.ptr, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+    MG_CUDA(cudaMemcpyAsync(hp + 1, ovf.ptr, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    if (extra_dev)
+      MG_CUDA(cudaMemcpyAsync(hp + 2, extra_dev, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     MG_CUDA(cudaStreamSynchronize(ctx->stream));
+    const unsigned long long h = hp[0];
+    int h_ovf = 0;
+    std::memcpy(&h_ovf, hp + 1, sizeof(int));
+    if (extra_dev)
+      std::memcpy(extra_host, hp + 2, sizeof(int));
     if (h_ovf)
       continue; // a column exceeded this envelope: rerun everything with the next one
     if (h == ULLONG_MAX)
@@ -879,7 +899,21 @@ std::vector<mgpu_csr *> spai_ls_shared(mgpu_ctx *ctx, int l, const mgpu_csr *con
     const int maxrow = static_cast<int>(csr_max_row(ctx, const_cast<mgpu_csr *>(pat)));
     DCsr atv{At0->row_ptr, At0->col_idx, at_vals.as<double>()};
     DCsr kov{At0->row_ptr, At0->col_idx, ko_vals.as<double>()};
-    run_ls(ctx, n, l, maxrow, pat->view(), atv, nnzA, kov, nnzA, K_old != nullptr, pt_vals.as<double>(), nnzJ);
+    // On A's pattern the factors take At0's structure: its longest row rides along with the
+    // LS kernel's status read instead of costing a synchronisation of its own
+    DBuf mx(sizeof(int), s);
+    int at_maxrow = -1;
+    if (!sq && At0->maxrow < 0 && n > 0)
+    {
+      MG_CUDA(cudaMemsetAsync(mx.ptr, 0, sizeof(int), s));
+      ls_max_row<<<blocks_for(n), kThreads, 0, s>>>(n, At0->row_ptr, mx.as<int>());
+      check_launch(ctx, "ls_max_row");
+    }
+    const bool fetch = !sq && At0->maxrow < 0 && n > 0;
+    run_ls(ctx, n, l, maxrow, pat->view(), atv, nnzA, kov, nnzA, K_old != nullptr, pt_vals.as<double>(), nnzJ,
+           fetch ? mx.as<int>() : nullptr, fetch ? &at_maxrow : nullptr);
+    if (fetch)
+      At0->maxrow = at_maxrow;
     // P^T (J pattern) -> P: one structure and one permutation for every factor.  On A's
     // pattern P^T has A0's CSR structure, so P has At0's and the values follow perm_t;
     // on A^2's the J pattern is transposed once.
@@ -909,6 +943,11 @@ std::vector<mgpu_csr *> spai_ls_shared(mgpu_ctx *ctx, int l, const mgpu_csr *con
     S->col_idx = nullptr;
     std::vector<const double *> gsrc;
     std::vector<double *> gdst;
+    // every factor's values in one allocation (slices), released with the last factor
+    double *vblock = nullptr;
+    MG_CUDA(mg_malloc(reinterpret_cast<void **>(&vblock),
+                      sizeof(double) * static_cast<size_t>(l) * (nnzJ > 0 ? nnzJ : 1), s));
+    std::shared_ptr<void> values(vblock, [owner_ctx](void *v) { cudaFreeAsync(v, owner_ctx->stream); });
     for (int p = 0; p < l; ++p)
     {
       auto *P = new mgpu_csr;
@@ -920,7 +959,8 @@ std::vector<mgpu_csr *> spai_ls_shared(mgpu_ctx *ctx, int l, const mgpu_csr *con
       P->col_idx = sci;
       P->shared_structure = structure;
       out.push_back(P);
-      MG_CUDA(mg_malloc(reinterpret_cast<void **>(&P->values), sizeof(double) * (nnzJ > 0 ? nnzJ : 1), s));
+      P->values = vblock + static_cast<size_t>(p) * (nnzJ > 0 ? nnzJ : 1);
+      P->shared_values = values;
       P->may_hold_zeros = true;
       P->bw = pattern == MGPU_PATTERN_A2 ? 2 * ba : ba;
       P->maxrow = pmax;
@@ -928,6 +968,7 @@ std::vector<mgpu_csr *> spai_ls_shared(mgpu_ctx *ctx, int l, const mgpu_csr *con
       gdst.push_back(P->values);
     }
     gather_batched(ctx, l, nnzJ, permP, gsrc.data(), gdst.data());
+    host_mark("spai_ls_shared: last gather queued");
   }
   catch (...)
   {
@@ -943,6 +984,7 @@ std::vector<mgpu_csr *> spai_ls_shared(mgpu_ctx *ctx, int l, const mgpu_csr *con
   mgpu_csr_free(PT0);
   mgpu_csr_free(At0);
   mgpu_csr_free(sq);
+  host_mark("spai_ls_shared: return");
   return out;
 }
 

@@ -8,6 +8,7 @@
 #include <cub/cub.cuh>
 
 #include <climits>
+#include <cstring>
 #include <vector>
 
 #include "internal.cuh"
@@ -249,6 +250,7 @@ void batched_add(mgpu_ctx *ctx, const mgpu_csr *A, const mgpu_csr *B, const mgpu
     }
     std::vector<int64_t> nnz(static_cast<size_t>(cnt), 0);
     int hbw[128] = {0};
+    auto *hpin = static_cast<int64_t *>(pinned_scratch(ctx, sizeof(int64_t) * 64 + sizeof(int) * 128));
     if (n > 0 && n <= 262144)
     {
       // short operators: one launch scans every row pointer, one copy returns every nnz
@@ -258,18 +260,21 @@ void batched_add(mgpu_ctx *ctx, const mgpu_csr *A, const mgpu_csr *B, const mgpu
       DBuf tot(sizeof(int64_t) * 64, ctx->stream);
       scan_rows_batched<<<cnt, kScanTB, 0, ctx->stream>>>(n, rb, tot.as<int64_t>());
       check_launch(ctx, "scan_rows_batched");
-      MG_CUDA(cudaMemcpyAsync(nnz.data(), tot.ptr, sizeof(int64_t) * cnt, cudaMemcpyDeviceToHost, ctx->stream));
+      MG_CUDA(cudaMemcpyAsync(hpin, tot.ptr, sizeof(int64_t) * cnt, cudaMemcpyDeviceToHost, ctx->stream));
     }
     else
     {
       for (int p = 0; p < cnt; ++p)
       {
         scan_row_ptr(ctx, args.rp[p], n);
-        MG_CUDA(cudaMemcpyAsync(&nnz[p], args.rp[p] + n, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+        MG_CUDA(cudaMemcpyAsync(hpin + p, args.rp[p] + n, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
       }
     }
-    MG_CUDA(cudaMemcpyAsync(hbw, bwbuf.ptr, sizeof(int) * 128, cudaMemcpyDeviceToHost, ctx->stream));
+    // pinned staging: the copies stay asynchronous, one synchronisation for all of them
+    MG_CUDA(cudaMemcpyAsync(hpin + 64, bwbuf.ptr, sizeof(int) * 128, cudaMemcpyDeviceToHost, ctx->stream));
     MG_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::memcpy(nnz.data(), hpin, sizeof(int64_t) * cnt);
+    std::memcpy(hbw, hpin + 64, sizeof(int) * 128);
     for (int p = 0; p < cnt; ++p)
     {
       made[p]->bw = hbw[p];
