@@ -1784,7 +1784,20 @@ __device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, cons
     acc[q] = 0.0;
   int k = 0;
   int cur_p = -1;
+  // TB % m == 0 (every m <= 8 but 7): a consumer thread's elements e = tid + k TB all belong to
+  // column c = tid % m, so the element loops hoist the system's scalars, and phase B keeps its
+  // (r, r) partial in one register (the other columns' partials of this thread stay zero).
+  const bool cfix = (TB % m) == 0;
+  const int cth = threadIdx.x % m;
+  double accb = 0.0;
   auto flush = [&](int pnt) {
+    if (kind == 2 && cfix && !P.serial)
+    {
+#pragma unroll
+      for (int q = 0; q < MT; ++q)
+        acc[q] = q == cth ? accb : 0.0;
+      accb = 0.0;
+    }
     double pv[2 * MT];
 #pragma unroll
     for (int q = 0; q < 2 * MT; ++q)
@@ -1881,6 +1894,21 @@ __device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, cons
           acc_add<MT>(acc, c, __dmul_rn(rn, rn));
         }
       }
+      else if (cfix)
+      {
+        if (sh.state[sb + cth] == kRun)
+        {
+          const double al = sh.alpha[sb + cth];
+          for (int e = threadIdx.x; e < ne; e += TB)
+          {
+            if (!P.fold)
+              __stcg(xg + e, __dadd_rn(xs[e], __dmul_rn(al, ds[e])));
+            const double rn = __dadd_rn(rs[e], __dmul_rn(-al, ws[e]));
+            __stcg(rg + e, rn);
+            accb = __dadd_rn(accb, __dmul_rn(rn, rn));
+          }
+        }
+      }
       else
       for (int e = threadIdx.x; e < ne; e += TB)
       {
@@ -1911,6 +1939,28 @@ __device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, cons
       const int lo = H0 * m, hi = (H0 + R) * m;
       double *dg = kind == 0 ? const_cast<double *>(vrow(P, dnew, cp, base_i - H0)) : nullptr;
       double *xg = kind == 0 ? const_cast<double *>(vrow(P, P.xt, cp, base_i - H0)) : nullptr;
+      if (cfix)
+      {
+        const int sys = sb + cth;
+        const bool fr = sh.fresh[sys] != 0, pd = sh.pend[sys] != 0, run = sh.state[sys] == kRun;
+        const double be = sh.beta[sys], al = sh.alpha[sys];
+        if (kind == 1)
+          for (int e = threadIdx.x; e < ne0; e += TB)
+            s0[e] = pd ? __dadd_rn(vr[e], __dmul_rn(al, vd[e])) : vr[e];
+        else
+          for (int e = threadIdx.x; e < ne0; e += TB)
+          {
+            const double v = fr ? vr[e] : __dadd_rn(vr[e], __dmul_rn(be, vd[e]));
+            if (e >= lo && e < hi)
+            {
+              __stcg(dg + e, v);
+              if (pd && run)
+                __stcg(xg + e, __dadd_rn(vx[e - lo], __dmul_rn(al, vd[e])));
+            }
+            s0[e] = v;
+          }
+      }
+      else
       for (int e = threadIdx.x; e < ne0; e += TB)
       {
         const int c = col_of<MT>(e, m);
