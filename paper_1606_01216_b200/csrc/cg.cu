@@ -1442,6 +1442,22 @@ struct PEll
   int ow;                      // 1 (E <= 8) or 2 (E <= 16)
 };
 
+// eq[p] = 1 iff operator p has point 0's CSR structure (then its ELL offsets equal point 0's,
+// and the kernel streams point 0's copy for every such point: one DRAM read, L2 hits for the
+// rest, since the points advance through the rows together).  eq must be preset to 1.
+__global__ void pattern_eq_kernel(int64_t n, int64_t nnz, const int64_t *__restrict__ rp0,
+                                  const int32_t *__restrict__ ci0, const int64_t *__restrict__ rp,
+                                  const int32_t *__restrict__ ci, int *eq)
+{
+  bool same = true;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i <= n; i += gridDim.x * blockDim.x)
+    same = same && rp[i] == rp0[i];
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < nnz; k += gridDim.x * blockDim.x)
+    same = same && ci[k] == ci0[k];
+  if (!__all_sync(0xffffffffu, same) && (threadIdx.x & 31) == 0)
+    *eq = 0;
+}
+
 struct StreamParams
 {
   int l, m, z, rpt, ch; // ch: rows per chunk (phase A and the check pass)
@@ -1453,6 +1469,8 @@ struct StreamParams
   int halo[kMaxZ + 1];
   int hmax;
   const PEll *A, *F; // [l], [l * z] newest first
+  const int *eqA;     // [l]: operator p shares point 0's structure (use A[0]'s offsets)
+  const int *eqF;     // [l * z]: factor (p, f) shares factor (0, f)'s structure
   double rtol;
   int64_t maxit;
   // vectors: logical (point p, row i, col c) at base + p * ldv + (PADR + i) * m + c
@@ -1689,6 +1707,12 @@ __device__ __forceinline__ void ell_row(const double *vals, const unsigned long 
       if (c < m)
         a2[c] = __dadd_rn(a2[c], __dmul_rn(a, x[c]));
   };
+  if (E & 1) // odd width (no padding entry): rows are 8-byte aligned only
+  {
+    for (int e = 0; e < E; ++e)
+      term(vals[e], e);
+    return;
+  }
   for (int h = 0; h < E / 2; ++h)
   {
     const double2 f = v2[h];
@@ -2084,9 +2108,18 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
     for (int g = 0; g < ntab; ++g)
     {
       const int p = P.serial ? g : sh.seg[g].p;
-      tab[g * (kMaxZ + 1)] = P.A[p];
+      PEll a = P.A[p];
+      if (P.eqA[p])
+        a.o = P.A[0].o;
+      tab[g * (kMaxZ + 1)] = a;
       for (int st = 0; st < P.z; ++st)
-        tab[g * (kMaxZ + 1) + 1 + st] = P.F[p * P.z + (P.z - 1 - st)];
+      {
+        const int f = P.z - 1 - st;
+        PEll fe = P.F[p * P.z + f];
+        if (P.eqF[p * P.z + f])
+          fe.o = P.F[f].o;
+        tab[g * (kMaxZ + 1) + 1 + st] = fe;
+      }
     }
     for (int b = 0; b < 2 * kStreamNB; ++b)
       mbar_init(&bars[b], 1);
@@ -2623,8 +2656,10 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
     return false;
   // ---- padded ELL operators
   auto ell_of = [&](const mgpu_csr *M, std::vector<DBuf> &keep) {
-    const int E = static_cast<int>((csr_max_row(ctx, const_cast<mgpu_csr *>(M)) + 1) & ~1ll);
-    const int Ee = E < 2 ? 2 : E;
+    // exact row width (odd widths allowed: a 5-entry row streams 40 bytes, not 48); bulk
+    // copies stay 16-byte multiples because chunk row counts are even
+    const int E = static_cast<int>(csr_max_row(ctx, const_cast<mgpu_csr *>(M)));
+    const int Ee = E < 1 ? 1 : E;
     const int ow = Ee > 8 ? 2 : 1;
     const int64_t rows = n + 2 * kPadR;
     keep.emplace_back(sizeof(double) * rows * Ee, s);
@@ -2805,6 +2840,31 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
   }
   DBuf segs(sizeof(Seg) * hseg.size(), s), pblk(sizeof(int2) * hpb.size(), s);
   DBuf dA(sizeof(PEll) * hA.size(), s), dF(sizeof(PEll) * hF.size(), s);
+  // structure-equality flags against point 0 (no host round trip: the kernel reads them)
+  DBuf eqA(sizeof(int) * static_cast<size_t>(l), s), eqF(sizeof(int) * static_cast<size_t>(l) * (z > 0 ? z : 1), s);
+  {
+    std::vector<int> ones(static_cast<size_t>(l) * (z > 0 ? z : 1), 1);
+    MG_CUDA(cudaMemcpyAsync(eqA.ptr, ones.data(), sizeof(int) * l, cudaMemcpyHostToDevice, s));
+    MG_CUDA(cudaMemcpyAsync(eqF.ptr, ones.data(), sizeof(int) * ones.size(), cudaMemcpyHostToDevice, s));
+    auto compare = [&](const mgpu_csr *X, const mgpu_csr *X0, int *flag) {
+      if (X == X0 || (X->row_ptr == X0->row_ptr && X->col_idx == X0->col_idx))
+        return; // stays 1
+      if (X->nnz != X0->nnz)
+      {
+        MG_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
+        return;
+      }
+      pattern_eq_kernel<<<std::max(1, std::min(ctx->num_sms * 4, static_cast<int>((n + 255) / 256))), 256, 0, s>>>(
+          n, X->nnz, X0->row_ptr, X0->col_idx, X->row_ptr, X->col_idx, flag);
+      check_launch(ctx, "pattern_eq_kernel");
+    };
+    for (int p = 1; p < l; ++p)
+    {
+      compare(A[p], A[0], eqA.as<int>() + p);
+      for (int f = 0; f < z; ++f)
+        compare(chains[static_cast<size_t>(p) * z + f], chains[f], eqF.as<int>() + static_cast<size_t>(p) * z + f);
+    }
+  }
   DBuf partial(sizeof(double) * static_cast<size_t>(l) * 2 * kMaxM * G, s);
   MG_CUDA(cudaMemcpyAsync(segs.ptr, hseg.data(), sizeof(Seg) * hseg.size(), cudaMemcpyHostToDevice, s));
   MG_CUDA(cudaMemcpyAsync(pblk.ptr, hpb.data(), sizeof(int2) * hpb.size(), cudaMemcpyHostToDevice, s));
@@ -2838,6 +2898,8 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
   P.hmax = H0;
   P.A = dA.as<PEll>();
   P.F = dF.as<PEll>();
+  P.eqA = eqA.as<int>();
+  P.eqF = eqF.as<int>();
   P.rtol = rtol;
   P.maxit = maxit;
   P.b = b.as<double>();
