@@ -11,6 +11,8 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O
 timeout 600 python bench.py > $O/bench_c1.log 2>&1
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref.log 2>&1
 timeout 600 python bench.py --workload config3 --steps 5 --warmup 3 > $O/bench_c3.log 2>&1
+timeout 600 python bench.py --workload config2 --steps 10 --warmup 3 > $O/bench_c2.log 2>&1
+timeout 900 python bench.py --workload config4 --steps 2 --warmup 3 > $O/bench_c4.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c1.csv \
   python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $O/ncu_launches.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:cg_cluster_v2 -c 1 -f -o $O/cluster_c1 \
