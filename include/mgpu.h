@@ -220,6 +220,15 @@ int mgpu_cg_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
                   int64_t m, const double *B, int64_t ldb_point, double rtol, int64_t maxit, mgpu_memkind where,
                   mgpu_cg_out *out);
 
+/* The path in one call (CgBackend::prepare + a solve of every point, airga.cpp:108-181):
+ * out[i] = shifted_operator(M, D, K, shifts[i]) (system.cpp:64-68), its LS-SPAI factor on
+ * `pattern` (MGPU_PATTERN_A / MGPU_PATTERN_A2, or -1 for P = I), then mgpu_cg_solve over the
+ * l points with B / ldb_point / out as there.  Operators and factors are temporaries.
+ * phase_ms (optional, 3 doubles): device time of assembly, SPAI, and the solve call. */
+int mgpu_shifted_solve(mgpu_ctx *ctx, const mgpu_csr *M, const mgpu_csr *D, const mgpu_csr *K, int l,
+                       const double *shifts, int pattern, const double *B, int64_t m, int64_t ldb_point, double rtol,
+                       int64_t maxit, mgpu_memkind where, mgpu_cg_out *out, double *phase_ms);
+
 /* ------------------------------------------------------------ model input */
 
 /* Host-side model generators for benchmarks and tests (not on the hot path).

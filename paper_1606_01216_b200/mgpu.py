@@ -31,7 +31,7 @@ EXPORTED = [
     "mgpu_transpose", "mgpu_trace", "mgpu_trace_inner", "mgpu_spmv", "mgpu_chain_apply", "mgpu_chain_quality", "mgpu_spai_build",
     "mgpu_spai_update", "mgpu_spai_ls", "mgpu_spai_ls_batched", "mgpu_spgemm", "mgpu_cg_solve",
     "mgpu_model_chain", "mgpu_model_hermite", "mgpu_host_free", "mgpu_thin_qr", "mgpu_project_reduce", "mgpu_project_reduce_slab",
-    "mgpu_arnoldi_deflate", "mgpu_model_hermite_device", "mgpu_csr_write", "mgpu_csr_read",
+    "mgpu_arnoldi_deflate", "mgpu_model_hermite_device", "mgpu_csr_write", "mgpu_csr_read", "mgpu_shifted_solve",
 ]
 
 
@@ -141,6 +141,8 @@ def lib():
         L.mgpu_spgemm.argtypes = [vp, vp, vp, C.POINTER(vp)]
         L.mgpu_cg_solve.argtypes = [vp, C.c_int, vp, C.c_int, vp, i64, i64, vp, i64, dbl, i64, C.c_int,
                                     C.POINTER(_CgOut)]
+        L.mgpu_shifted_solve.argtypes = [vp, vp, vp, vp, C.c_int, vp, C.c_int, vp, i64, i64, dbl, i64, C.c_int,
+                                         C.POINTER(_CgOut), vp]
         L.mgpu_model_chain.argtypes = [i64, dbl, dbl, dbl, dbl, C.c_int] + [C.POINTER(_HostCsr)] * 3
         L.mgpu_model_hermite.argtypes = [i64] + [dbl] * 7 + [C.POINTER(_HostCsr)] * 3
         L.mgpu_csr_write.argtypes = [vp, vp, C.c_char_p]
@@ -602,6 +604,46 @@ def cg_solve_raw(ctx: Context, dA: Sequence[DeviceCsr], flat_chain: Sequence[Dev
     status = lib().mgpu_cg_solve(ctx.handle, l, _handles(dA), z, _handles(flat_chain), n, m, C.c_void_p(B_ptr), ldb,
                                  rtol, maxit, where, C.byref(out))
     return status, it, cv, st, bd, (hist.reshape(l, m, history_cap) if history_cap > 0 else None)
+
+
+def shifted_solve_raw(ctx: Context, M, D, K, shifts: Sequence[float], pattern: int, m: int, B_ptr: int, ldb: int,
+                      rtol: float, maxit: int, where: int, X_ptr: int, REC_ptr: int, TR_ptr: int):
+    """mgpu_shifted_solve: assembly of every shifted operator, LS-SPAI on `pattern` (-1: P = I)
+    and the batched solve in one library call (CgBackend::prepare + solve of every point,
+    airga.cpp:108-181).  Returns (status, iterations, converged, status_per_column,
+    breakdown_iteration, phase_ms[assembly, spai, solve])."""
+    dM, dD, dK = (_dev(x, ctx) for x in (M, D, K))
+    sh = np.ascontiguousarray(shifts, np.float64)
+    l = len(sh)
+    it = np.zeros(l * m, np.int64)
+    cv = np.zeros(l * m, np.int32)
+    st = np.zeros(l * m, np.int32)
+    bd = np.zeros(l * m, np.int64)
+    ph = np.zeros(3)
+    out = _CgOut(X_ptr, REC_ptr, TR_ptr, it.ctypes.data_as(C.POINTER(C.c_int64)),
+                 cv.ctypes.data_as(C.POINTER(C.c_int)), st.ctypes.data_as(C.POINTER(C.c_int)),
+                 bd.ctypes.data_as(C.POINTER(C.c_int64)), None, 0)
+    status = lib().mgpu_shifted_solve(ctx.handle, dM.handle, dD.handle, dK.handle, l, _ptr(sh), pattern,
+                                      C.c_void_p(B_ptr), m, ldb, rtol, maxit, where, C.byref(out), _ptr(ph))
+    return status, it, cv, st, bd, ph
+
+
+def shifted_solve_device(M, D, K, shifts: Sequence[float], pattern: int, B_dev, X_dev, REC_dev=None, TR_dev=None,
+                         rtol: float = 1e-10, maxit: Optional[int] = None, ctx=None):
+    """Device-resident shifted_solve: B_dev one (m, n) block shared by every point, X_dev /
+    REC_dev / TR_dev torch CUDA float64 tensors [point][column][row].  Raises on every status
+    but BREAKDOWN (reported per column).  Returns (iterations, converged, status, breakdown,
+    phase_ms)."""
+    ctx = ctx or default_context()
+    n = _dev(M, ctx).nrows
+    m = int(B_dev.shape[-2]) if B_dev.dim() >= 2 else 1
+    maxit = 10 * n if maxit is None else maxit
+    ptr = lambda t: t.data_ptr() if t is not None else 0
+    status, it, cv, st, bd, ph = shifted_solve_raw(ctx, M, D, K, shifts, pattern, m, B_dev.data_ptr(), 0, rtol, maxit,
+                                                   MGPU_DEVICE, ptr(X_dev), ptr(REC_dev), ptr(TR_dev))
+    if status != MGPU_OK and status != MGPU_ERR_BREAKDOWN:
+        ctx.check(status)
+    return it, cv, st, bd, ph
 
 
 def cg_solve_batched(As: Sequence, chains: Sequence[Sequence], B, rtol: float = 1e-10, maxit: Optional[int] = None,

@@ -89,3 +89,41 @@ def test_config3_serial_schedule_matches_batched(mg, monkeypatch):
         np.testing.assert_array_equal(g.iterations, r.iterations)
         assert rel(g.X, r.X) < 1e-10
         assert np.all(np.isfinite(g.X)) and np.max(np.abs(g.X)) > 0
+
+
+@pytest.mark.parametrize("where", ["device", "host"])
+def test_shifted_solve_one_call_matches_oracle(mg, where):
+    """mgpu_shifted_solve (the bench's step: assembly + LS-SPAI + batched solve in one library
+    call) on the configs[1] workload against the oracle's separate reference calls."""
+    import torch
+    (M, D, K), ops, facs, b, want = _oracle_case()
+    ctx = mg.default_context()
+    n, l = M.nrows, len(SHIFTS)
+    if where == "device":
+        dev = torch.device("cuda", 0)
+        B_dev = torch.tensor(b[None, :], dtype=torch.float64, device=dev)
+        X_dev = torch.empty((l, 1, n), dtype=torch.float64, device=dev)
+        it, cv, st, bd, ph = mg.shifted_solve_device(M, D, K, SHIFTS, mg.PATTERN_A, B_dev, X_dev, rtol=1e-10,
+                                                     maxit=BUDGET, ctx=ctx)
+        X = X_dev.cpu().numpy()
+        assert ph.shape == (3,) and np.all(ph >= 0)
+    else:
+        X = np.zeros((l, 1, n))
+        status, it, cv, st, bd, ph = mg.shifted_solve_raw(ctx, M, D, K, SHIFTS, mg.PATTERN_A, 1, b.ctypes.data, 0,
+                                                          1e-10, BUDGET, mg.mgpu.MGPU_HOST, X.ctypes.data, 0, 0)
+        assert status == mg.mgpu.MGPU_OK
+    assert np.all(st == 0)
+    for p, w in enumerate(want):
+        assert int(it[p]) == w["iterations"] == BUDGET
+        assert bool(cv[p]) == w["converged"]
+        assert rel(X[p, 0], w["solution"]) < 1e-8
+
+
+def test_shifted_solve_reports_argument_errors(mg):
+    M, D, K = mg.model_hermite(50)
+    ctx = mg.default_context()
+    X = np.zeros((1, 1, 100))
+    b = np.ones(100)
+    status, *_ = mg.shifted_solve_raw(ctx, M, D, K, [10.0], 7, 1, b.ctypes.data, 0, 1e-10, 10, mg.mgpu.MGPU_HOST,
+                                      X.ctypes.data, 0, 0)
+    assert status == mg.mgpu.MGPU_ERR_ARG
