@@ -212,3 +212,21 @@ def test_multi_rhs_restart_plain(mg, oracle, m):
     assert got.all_converged == want["all_converged"]
     assert rel(got.X, want["X"]) < 1e-8
     assert np.all(np.abs(np.asarray(got.iterations) - np.asarray(want["iterations"])) <= 2)
+
+
+def test_mixed_structures_in_one_batch(mg, oracle):
+    """Operators of different CSR structure in one batch (Hermite beam and chain model, same n):
+    the streaming kernel shares ELL offsets only between structurally equal points (device
+    pattern-equality flags), so every point must still match its own oracle solve."""
+    Mh, Dh, Kh = oracle.hermite_generate(1000)
+    Mc, Dc, Kc = oracle.chain_generate(2000, consistent=True, stiffness_scale=1.0)
+    ops = [oracle.shifted_operator(Mh, Dh, Kh, 100.0), oracle.shifted_operator(Mc, Dc, Kc, 10.0),
+           oracle.shifted_operator(Mh, Dh, Kh, 300.0), oracle.shifted_operator(Mc, Dc, Kc, 30.0)]
+    Ps = [oracle.spai_ls(A, None, 0) for A in ops]
+    b = np.zeros(2000)
+    b[1998] = 1.0
+    res = mg.cg_solve_batched(ops, [[P] for P in Ps], b, rtol=1e-10, maxit=120)
+    for A, P, r in zip(ops, Ps, res):
+        want = oracle.pcg_solve(A, [P], b, rtol=1e-10, maxit=120)
+        assert int(r.iterations[0]) == want["iterations"]
+        assert rel(r.X[:, 0], want["solution"]) < 1e-8

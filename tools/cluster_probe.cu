@@ -10,7 +10,7 @@ int main()
     for (int sm : smems)
     {
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-      for (int cs = 9; cs <= 16; ++cs)
+      for (int cs = 1; cs <= 16; ++cs)
       {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(cs * 8);
