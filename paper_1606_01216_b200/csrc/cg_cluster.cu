@@ -166,13 +166,16 @@ __device__ __forceinline__ void cta_sum_push(ClShared &sh, double (&v)[NV], int 
 template <int NV>
 __device__ __forceinline__ void warp_inbox_total(const double *inbox, int nv, int cs, double (&out)[NV])
 {
-  const int lane = threadIdx.x & 31;
+  // cs <= kCMaxCS = 16 slots: both half-warps load the same slots and reduce over 4 levels.
+  // Bitwise what a 5-level butterfly over 16 values + 16 zeros gives (x + 0 == x).
+  static_assert(kCMaxCS == 16, "half-warp inbox reduction");
+  const int slot = threadIdx.x & (kCMaxCS - 1);
   double v[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k)
-    v[k] = (k < nv && lane < cs) ? inbox[k * kCMaxCS + lane] : 0.0;
+    v[k] = (k < nv && slot < cs) ? inbox[k * kCMaxCS + slot] : 0.0;
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1)
+  for (int off = kCMaxCS / 2; off > 0; off >>= 1)
   {
 #pragma unroll
     for (int k = 0; k < NV; ++k)
