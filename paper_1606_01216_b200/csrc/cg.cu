@@ -2687,6 +2687,8 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
   std::vector<PEll> hA(static_cast<size_t>(l)), hF(static_cast<size_t>(l) * (z > 0 ? z : 1));
   int EA = 0;
   std::vector<int> EF(static_cast<size_t>(z > 0 ? z : 1), 0);
+  std::vector<int> OWF(static_cast<size_t>(z > 0 ? z : 1), 1); // offset words per row (1: <= 8 entries)
+  int OWA = 1;
   for (int p = 0; p < l; ++p)
   {
     hA[p] = ell_of(A[p], keep);
@@ -2696,7 +2698,9 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
       hF[static_cast<size_t>(p) * z + f] = ell_of(chains[static_cast<size_t>(p) * z + f], keep);
       const int st = z - 1 - f;
       EF[st] = std::max(EF[st], hF[static_cast<size_t>(p) * z + f].E);
+      OWF[st] = std::max(OWF[st], hF[static_cast<size_t>(p) * z + f].ow);
     }
+    OWA = std::max(OWA, hA[p].ow);
   }
   // x~ update placement: deferred into phase A, which streams d_old anyway (one vector pass
   // fewer).  Measured on B200 once the kernel dropped to 107 registers: configs[3] (m = 4, P = I)
@@ -2715,13 +2719,20 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
   const size_t stat = sizeof(BandShared<TB + 32>) + sizeof(PEll) * kTabSlots * (kMaxZ + 1) + 128;
   // (chunk rows, ring depth) in order of preference; MGPU_STREAM_CFG="rows,depth" forces one (diagnostics)
   // largest chunk first (per-chunk barriers and pipeline bookkeeping amortise over its rows), 3-deep ring
-  // before 2-deep at equal height
+  // before 2-deep at equal height.  With m >= 4, heights that are multiples of 128 rows are skipped:
+  // with every block striding through HBM in lock step they measured 3-4% slower on configs[3]
+  // (512 / 640 rows: 872 / 876 us per iteration against 843 / 836 for 576 / 448 rows); m = 1
+  // (configs[2] shape) measured best on its largest chunk.
   std::vector<std::pair<int64_t, int>> cands;
   for (int64_t ch = 1024; ch >= 128; ch -= 64)
   {
+    if (m >= 4 && ch % 128 == 0)
+      continue;
     cands.push_back({ch, 3});
     cands.push_back({ch, 2});
   }
+  cands.push_back({128, 3});
+  cands.push_back({128, 2});
   if (const char *f = std::getenv("MGPU_STREAM_CFG"))
   {
     long fr = 0, fd = 0;
@@ -2746,10 +2757,10 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
     {
       const int64_t rows = (ch + 2 * hal[st + 1] + 1) & ~1ll;
       P.a_fv[st] = take(sizeof(double) * rows * EF[st]);
-      P.a_fo[st] = take(sizeof(unsigned long long) * rows * 2);
+      P.a_fo[st] = take(sizeof(unsigned long long) * rows * OWF[st]);
     }
     P.a_av = take(sizeof(double) * ch * EA);
-    P.a_ao = take(sizeof(unsigned long long) * ch * 2);
+    P.a_ao = take(sizeof(unsigned long long) * ch * OWA);
     const size_t a_bytes = off;
     off = 0;
     const size_t b_bytes = sizeof(double) * ch * m * (fold ? 2 : 4);
@@ -2768,6 +2779,13 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
   }
   if (CH == 0)
     return false;
+  if (std::getenv("MGPU_HOST_TRACE"))
+  {
+    char msg[128];
+    std::snprintf(msg, sizeof msg, "cg_stream plan: %lld-row chunks, %d-deep ring, %zu B per slot",
+                  static_cast<long long>(CH), P.nb, P.buf_bytes);
+    host_mark(msg);
+  }
   // ---- vectors (padded) and the per-point block plan
   const int64_t ldv = (n + 2 * kPadR) * m;
   const size_t vb = sizeof(double) * static_cast<size_t>(l) * ldv;

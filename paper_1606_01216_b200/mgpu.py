@@ -16,6 +16,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libmgpu.so")
+# diagnostics: A/B timing of an alternative build of the same library (never a fallback)
+LIB_PATH = os.environ.get("MGPU_LIB", LIB_PATH)
 
 MGPU_OK, MGPU_ERR_ARG, MGPU_ERR_STAGNATION, MGPU_ERR_BREAKDOWN = 0, 1, 2, 3
 MGPU_ERR_NUMERICAL, MGPU_ERR_UNSUPPORTED, MGPU_ERR_CUDA, MGPU_ERR_NCCL = 4, 5, 6, 7
