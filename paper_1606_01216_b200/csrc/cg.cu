@@ -3030,10 +3030,10 @@ void cg_batch(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_
   // break-even ~1K elements per SM on B200)
   // and the chain is short: every chain stage adds factor buffers to each ring slot, so the
   // chunks shrink and the per-chunk cost wins -- measured on configs[2] (n = 1e5, 8 points,
-  // LS update chain, 1000 iterations): stream 31 / 47 / 54 / 68 / 87 / 119 / 185 / 203 ms at
-  // z = 1..8 against banded 45 / 56 / 67 / 77 / 89 / 99 / 110 / 121 ms, so z >= 6 goes to the
+  // LS update chain, 1000 iterations): stream 31 / 44 / 50 / 68 / 88 / 97 / 132 / 145 ms at
+  // z = 1..8 against banded 45 / 56 / 67 / 77 / 89 / 99 / 110 / 121 ms, so z >= 7 goes to the
   // banded kernel
-  const bool stream_pays = static_cast<int64_t>(l) * n * m >= static_cast<int64_t>(2048) * ctx->num_sms && z <= 5;
+  const bool stream_pays = static_cast<int64_t>(l) * n * m >= static_cast<int64_t>(2048) * ctx->num_sms && z <= 6;
   if (banded && !clustered && (ctx->cg_path == 4 || (ctx->cg_path == 0 && stream_pays)))
   {
     MG_CUDA(cudaMemsetAsync(p_loop, 0, sizeof(int64_t), s));
