@@ -21,7 +21,6 @@ import time
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
 
-import numpy as np
 
 from . import mgpu
 

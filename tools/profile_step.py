@@ -1,7 +1,7 @@
 """Host/device time per API call of one bench step (diagnostics; run on the GPU box)."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np, torch
+import torch
 import paper_1606_01216_b200 as mg
 
 dev = torch.device("cuda", 0)

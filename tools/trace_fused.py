@@ -1,7 +1,7 @@
 """Host trace of one fused configs[1] step (MGPU_HOST_TRACE=1 python tools/trace_fused.py)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np, torch
+import torch
 import paper_1606_01216_b200 as mg
 from paper_1606_01216_b200 import sharding
 dev = torch.device("cuda", 0); stream = torch.cuda.Stream(device=dev)
