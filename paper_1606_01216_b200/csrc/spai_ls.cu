@@ -632,11 +632,12 @@ __global__ void __launch_bounds__(64) ls_columns_lane(int64_t n, int l, DCsr pat
     out_vals[jb + c] = mv[c];
 }
 
-template <int NJ, int NI>
+// TPB: threads per block (32 packs the per-lane scratch more tightly for small envelopes)
+template <int NJ, int NI, int TPB = 64>
 void launch_ls_lane(mgpu_ctx *ctx, int64_t n, int l, DCsr pat, DCsr At, int64_t at_stride, DCsr Kot, int64_t ko_stride,
                     bool update, double *out, int64_t out_stride, unsigned long long *err, int *ovf)
 {
-  constexpr int kThreadsPerBlock = 64;
+  constexpr int kThreadsPerBlock = TPB;
   constexpr size_t smem = sizeof(double) * LaneLayout<NJ, NI>::kWords * kThreadsPerBlock;
   static_assert(smem <= 200 * 1024, "LS lane shared memory");
   MG_CUDA(cudaFuncSetAttribute(ls_columns_lane<NJ, NI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -668,23 +669,30 @@ void launch_ls(mgpu_ctx *ctx, int64_t n, int l, DCsr pat, DCsr At, int64_t at_st
 // sequential column loop would.
 void run_ls(mgpu_ctx *ctx, int64_t n, int l, int maxrow, DCsr pat, DCsr At, int64_t at_stride, DCsr Kot,
             int64_t ko_stride, bool update, double *out, int64_t out_stride, const int *extra_dev = nullptr,
-            int *extra_host = nullptr)
+            int *extra_host = nullptr, int64_t pat_bw = -1)
 {
   if (n == 0 || l == 0)
     return;
   DBuf err(sizeof(unsigned long long), ctx->stream), ovf(sizeof(int), ctx->stream);
-  // lane-per-column envelopes first (|J| <= 6 / 8 pattern entries, |I| <= 14 / 16 rows), then
-  // the lane-group kernels; MGPU_LS_GROUP=1 skips the lane kernels (diagnostics)
+  // lane-per-column envelopes first (|J| <= 5 / 6 / 8 pattern entries, |I| <= 13 / 14 / 16 rows),
+  // then the lane-group kernels; MGPU_LS_GROUP=1 skips the lane kernels (diagnostics).  The
+  // <5, 13> envelope is taken only when it cannot overflow: a J pattern of bandwidth b gives
+  // |I| <= 4 b + 1 (b = 3 on the Hermite beam: 13 rows).
   const bool lanes = !std::getenv("MGPU_LS_GROUP");
-  for (int cfg = -2; cfg < 3; ++cfg)
+  for (int cfg = -3; cfg < 3; ++cfg)
   {
-    const int G = cfg == -2 ? 6 : (cfg == -1 ? 8 : (cfg == 0 ? 8 : (cfg == 1 ? 16 : 32)));
+    const int G = cfg == -3 ? 5 : (cfg == -2 ? 6 : (cfg == -1 ? 8 : (cfg == 0 ? 8 : (cfg == 1 ? 16 : 32))));
     if (maxrow > G || (cfg < 0 && !lanes))
+      continue;
+    if (cfg == -3 && !(pat_bw >= 0 && 4 * pat_bw + 1 <= 13))
       continue;
     MG_CUDA(cudaMemsetAsync(err.ptr, 0xff, sizeof(unsigned long long), ctx->stream));
     MG_CUDA(cudaMemsetAsync(ovf.ptr, 0, sizeof(int), ctx->stream));
     auto *ev = err.as<unsigned long long>();
-    if (cfg == -2)
+    if (cfg == -3)
+      launch_ls_lane<5, 13, 32>(ctx, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev,
+                                ovf.as<int>());
+    else if (cfg == -2)
       launch_ls_lane<6, 14>(ctx, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev, ovf.as<int>());
     else if (cfg == -1)
       launch_ls_lane<8, 16>(ctx, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev, ovf.as<int>());
@@ -910,8 +918,10 @@ std::vector<mgpu_csr *> spai_ls_shared(mgpu_ctx *ctx, int l, const mgpu_csr *con
       check_launch(ctx, "ls_max_row");
     }
     const bool fetch = !sq && At0->maxrow < 0 && n > 0;
+    // J pattern bandwidth: A's, doubled for the symbolic A^2
+    const int64_t bwA = csr_bandwidth(ctx, const_cast<mgpu_csr *>(A0));
     run_ls(ctx, n, l, maxrow, pat->view(), atv, nnzA, kov, nnzA, K_old != nullptr, pt_vals.as<double>(), nnzJ,
-           fetch ? mx.as<int>() : nullptr, fetch ? &at_maxrow : nullptr);
+           fetch ? mx.as<int>() : nullptr, fetch ? &at_maxrow : nullptr, sq ? 2 * bwA : bwA);
     if (fetch)
       At0->maxrow = at_maxrow;
     // P^T (J pattern) -> P: one structure and one permutation for every factor.  On A's
