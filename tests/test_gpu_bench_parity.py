@@ -127,3 +127,24 @@ def test_shifted_solve_reports_argument_errors(mg):
     status, *_ = mg.shifted_solve_raw(ctx, M, D, K, [10.0], 7, 1, b.ctypes.data, 0, 1e-10, 10, mg.mgpu.MGPU_HOST,
                                       X.ctypes.data, 0, 0)
     assert status == mg.mgpu.MGPU_ERR_ARG
+
+
+@pytest.mark.parametrize("ne,m,nshift,k", [(500000, 4, 2, 30), (5000000, 1, 1, 8)])
+def test_full_size_iterates_match_oracle(mg, oracle, ne, m, nshift, k):
+    """BASELINE configs[3] / configs[4] sizes (n = 1e6 with m = 4, n = 1e7) through the
+    streaming kernel (P = I, as the bench runs them) against the oracle's block_solve after k
+    iterations: same iteration count, iterates within 1e-8."""
+    M, D, K = oracle.hermite_generate(ne)
+    n = M.nrows
+    B = np.zeros((n, m))
+    for c in range(m):
+        B[2 * ((c + 1) * ne // m) - 2, c] = 1.0
+    shifts = [10.0 ** (1 + 3 * i / 15) for i in range(16)][:nshift]
+    ctx = mg.default_context()
+    res = mg.cg_solve_batched([oracle.shifted_operator(M, D, K, s) for s in shifts], [[] for _ in shifts], B,
+                              rtol=1e-10, maxit=k, ctx=ctx)
+    assert ctx.last_cg_path == "stream"
+    for s, r in zip(shifts, res):
+        want = oracle.block_solve(oracle.shifted_operator(M, D, K, s), [], B, rtol=1e-10, maxit=k)
+        np.testing.assert_array_equal(r.iterations, want["iterations"])
+        assert rel(r.X, want["X"]) < 1e-8
