@@ -434,15 +434,15 @@ __global__ void ls_max_row(int64_t nrows, const int64_t *__restrict__ rp, int *o
 // in distinct banks.  Q is never stored whole: column c of Q is rebuilt in one NI-vector
 // (H_0 .. H_c applied to e_c, the same reflector loop as thin_qr's Q formation), sign-fixed
 // and dotted with e, which gives y_c with exactly the operations of the group kernel and the
-// oracle (bitwise equal).  Envelope: |J| <= NJ, |I| <= NI; a larger column sets `overflow` and
+// oracle (bitwise equal).  That column and e live in registers (loops unrolled to the NJ x NI
+// envelope, so every index is a compile-time constant): only W, the reflector scalars and I
+// take shared memory, which sets the occupancy.  Envelope: |J| <= NJ, |I| <= NI; a larger column sets `overflow` and
 // the host reruns the batch on the group kernels.
 template <int NJ, int NI>
 struct LaneLayout
 {
   static constexpr int kW = 0;                // W[c * NI + i]: S, then Householder vectors / R
-  static constexpr int kQ = kW + NJ * NI;     // one column of Q
-  static constexpr int kE = kQ + NI;          // right-hand side restricted to I
-  static constexpr int kDiag = kE + NI;       // R diagonal (alpha)
+  static constexpr int kDiag = kW + NJ * NI;  // R diagonal (alpha)
   static constexpr int kTau = kDiag + NJ;     // reflector scales, then |R_cc|
   static constexpr int kM = kTau + NJ;        // y, then the solution
   static constexpr int kI = kM + NJ;          // I (int32, NI of them = NI / 2 words)
@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(64) ls_columns_lane(int64_t n, int l, DCsr pat
   using L = LaneLayout<NJ, NI>;
   extern __shared__ __align__(16) double lane_raw[];
   double *base = lane_raw + static_cast<size_t>(threadIdx.x) * L::kWords;
-  double *W = base + L::kW, *q = base + L::kQ, *e = base + L::kE;
+  double *W = base + L::kW;
   double *diag = base + L::kDiag, *tau = base + L::kTau, *mv = base + L::kM;
   int32_t *I = reinterpret_cast<int32_t *>(base + L::kI);
   const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -532,8 +532,10 @@ __global__ void __launch_bounds__(64) ls_columns_lane(int64_t n, int l, DCsr pat
     for (int64_t t = At.rp[k]; t < t1; ++t)
       col[find(At.ci[t])] = atv[t];
   }
-  // ---- e = rhs restricted to I
-  for (int i = 0; i < ni; ++i)
+  // ---- e = rhs restricted to I (registers)
+  double e[NI];
+#pragma unroll
+  for (int i = 0; i < NI; ++i)
     e[i] = 0.0;
   if (update)
   {
@@ -542,13 +544,20 @@ __global__ void __launch_bounds__(64) ls_columns_lane(int64_t n, int l, DCsr pat
       const int32_t row = Kot.ci[t];
       const int lo = find(row);
       if (lo < ni && I[lo] == row)
-        e[lo] = kov[t];
+      {
+        const double v = kov[t];
+#pragma unroll
+        for (int i = 0; i < NI; ++i)
+          if (i == lo)
+            e[i] = v;
+      }
     }
   }
   else
   {
-    for (int i = 0; i < ni; ++i)
-      if (I[i] == j)
+#pragma unroll
+    for (int i = 0; i < NI; ++i)
+      if (i < ni && I[i] == j)
         e[i] = 1.0;
   }
   // ---- thin_qr (dense.cpp:153-246): frob_norm tolerance in column-major order
@@ -592,25 +601,43 @@ __global__ void __launch_bounds__(64) ls_columns_lane(int64_t n, int l, DCsr pat
     report(err, g, MGPU_ERR_NUMERICAL);
     return;
   }
-  // ---- y_c = (sign-fixed column c of Q = H_0 ... H_{nj-1} e_c)^T e
+  // ---- y_c = (sign-fixed column c of Q = H_0 ... H_{nj-1} e_c)^T e, column in registers
   for (int c = 0; c < nj; ++c)
   {
-    for (int i = 0; i < ni; ++i)
-      q[i] = 0.0;
-    q[c] = 1.0;
-    for (int k = c < nj - 1 ? c : nj - 1; k >= 0; --k)
+    double q[NI];
+#pragma unroll
+    for (int i = 0; i < NI; ++i)
+      q[i] = i == c ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = NJ - 1; k >= 0; --k) // k = min(c, nj - 1) .. 0 (c < nj)
     {
-      if (tau[k] == 0.0)
+      if (k > c || tau[k] == 0.0)
         continue;
       const double *v = W + k * NI + k;
       const int len = ni - k;
-      const double sc = __dmul_rn(tau[k], dot_serial(v, q + k, len));
-      axpy_serial(len, -sc, v, q + k);
+      double acc = 0.0;
+#pragma unroll
+      for (int i = 0; i + k < NI; ++i)
+        if (i < len)
+          acc = __dadd_rn(acc, __dmul_rn(v[i], q[k + i]));
+      const double sc = __dmul_rn(tau[k], acc);
+#pragma unroll
+      for (int i = 0; i + k < NI; ++i)
+        if (i < len)
+          q[k + i] = __dadd_rn(q[k + i], __dmul_rn(-sc, v[i]));
     }
     if (diag[c] < 0.0)
-      for (int i = 0; i < ni; ++i)
+    {
+#pragma unroll
+      for (int i = 0; i < NI; ++i)
         q[i] = __dmul_rn(q[i], -1.0);
-    mv[c] = dot_serial(q, e, ni);
+    }
+    double y = 0.0;
+#pragma unroll
+    for (int i = 0; i < NI; ++i)
+      if (i < ni)
+        y = __dadd_rn(y, __dmul_rn(q[i], e[i]));
+    mv[c] = y;
   }
   // ---- sign fix of R's off-diagonal rows (R(k, c) = W[c][k], c > k), |R_cc|
   for (int c = 0; c < nj; ++c)
