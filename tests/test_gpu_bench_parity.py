@@ -148,3 +148,24 @@ def test_full_size_iterates_match_oracle(mg, oracle, ne, m, nshift, k):
         want = oracle.block_solve(oracle.shifted_operator(M, D, K, s), [], B, rtol=1e-10, maxit=k)
         np.testing.assert_array_equal(r.iterations, want["iterations"])
         assert rel(r.X, want["X"]) < 1e-8
+
+
+def test_shifted_solve_raises_the_spai_error(mg):
+    """On the BASELINE beam at n = 5e5 the LS problems on A's pattern are rank-deficient
+    (DESIGN.md 4): the one-call path raises the same NumericalError as spai_ls_batched and
+    leaves the context usable."""
+    import torch
+    ctx = mg.default_context()
+    M, D, K = mg.model_hermite_device(250000, ctx=ctx)
+    n = 500000
+    dev = torch.device("cuda", 0)
+    B_dev = torch.zeros((1, n), dtype=torch.float64, device=dev)
+    B_dev[0, n - 2] = 1.0
+    X_dev = torch.empty((2, 1, n), dtype=torch.float64, device=dev)
+    with pytest.raises(mg.NumericalError):
+        mg.shifted_solve_device(M, D, K, [100.0, 1000.0], mg.PATTERN_A, B_dev, X_dev, maxit=5, ctx=ctx)
+    ops = mg.shifted_operators(M, D, K, [100.0, 1000.0], ctx=ctx)
+    with pytest.raises(mg.NumericalError):
+        mg.spai_ls_batched(ops, None, mg.PATTERN_A, ctx=ctx)
+    it, cv, st, bd, ph = mg.shifted_solve_device(M, D, K, [100.0], -1, B_dev, X_dev[:1], maxit=5, ctx=ctx)
+    assert int(it[0]) == 5
