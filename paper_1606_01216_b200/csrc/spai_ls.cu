@@ -868,7 +868,9 @@ mgpu_csr *spai_ls_one(mgpu_ctx *ctx, const mgpu_csr *A, const mgpu_csr *K_old, i
   {
     const int maxrow = static_cast<int>(csr_max_row(ctx, const_cast<mgpu_csr *>(pat)));
     const DCsr kv = Kot ? Kot->view() : DCsr{nullptr, nullptr, nullptr};
-    run_ls(ctx, n, 1, maxrow, pat->view(), At->view(), 0, kv, 0, Kot != nullptr, PT->values, 0);
+    const int64_t bwA = csr_bandwidth(ctx, const_cast<mgpu_csr *>(A));
+    run_ls(ctx, n, 1, maxrow, pat->view(), At->view(), 0, kv, 0, Kot != nullptr, PT->values, 0, nullptr, nullptr,
+           sq ? 2 * bwA : bwA);
   }
   catch (...)
   {
