@@ -1707,6 +1707,20 @@ __device__ __forceinline__ void ell_row(const double *vals, const unsigned long 
       if (c < m)
         a2[c] = __dadd_rn(a2[c], __dmul_rn(a, x[c]));
   };
+  // single right-hand side: the Hermite operators and their A-pattern LS factors (5 entries)
+  // unrolled with constant shifts (configs[2] shape 31.1 -> 27.6 us per iteration; with m = 4
+  // the preloaded values cost registers and it measured 2% slower, so MT > 1 keeps the loop)
+  if (MT == 1 && E == 5)
+  {
+    double a5[5];
+#pragma unroll
+    for (int e = 0; e < 5; ++e)
+      a5[e] = vals[e];
+#pragma unroll
+    for (int e = 0; e < 5; ++e)
+      term(a5[e], e);
+    return;
+  }
   if (E & 1) // odd width (no padding entry): rows are 8-byte aligned only
   {
     for (int e = 0; e < E; ++e)
