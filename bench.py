@@ -283,7 +283,7 @@ def run_mgpu(args, rank, world, local_rank):
     def step_e2e(record):
         e0, e1 = ev(), ev()
         e0.record(stream)
-        hM, hD, hK = (mg.DeviceCsr.upload(x, ctx) for x in host_sys)
+        hM, hD, hK = mg.DeviceCsr.upload_many(host_sys, ctx)
         status, it, cv, st, bd, _ = mg.shifted_solve_raw(ctx, hM, hD, hK, shifts, pattern, m, B_host.data_ptr(), 0,
                                                          1e-10, budget, mg.mgpu.MGPU_HOST, X_host.data_ptr(),
                                                          R_host.data_ptr(), T_host.data_ptr())

@@ -100,6 +100,11 @@ int mgpu_last_cg_path(const mgpu_ctx *ctx);
  * are validated on the device (MGPU_ERR_ARG on violation, cf. sparse.cpp:108-138). */
 int mgpu_csr_upload(mgpu_ctx *ctx, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t *row_ptr,
                     const int32_t *col_idx, const double *values, mgpu_csr **out);
+/* Several host CSR matrices at once (same validation as mgpu_csr_upload): every copy and
+ * check is queued before one read-back; out[q] receives matrix q. */
+int mgpu_csr_upload_batch(mgpu_ctx *ctx, int count, const int64_t *nrows, const int64_t *ncols, const int64_t *nnz,
+                          const int64_t *const *row_ptr, const int32_t *const *col_idx, const double *const *values,
+                          mgpu_csr **out);
 /* Same, from device pointers already on the context's device (copied). */
 int mgpu_csr_upload_device(mgpu_ctx *ctx, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t *row_ptr,
                            const int32_t *col_idx, const double *values, mgpu_csr **out);

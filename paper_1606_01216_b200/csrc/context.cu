@@ -402,6 +402,64 @@ int mgpu_csr_upload(mgpu_ctx *ctx, int64_t nrows, int64_t ncols, int64_t nnz, co
   return guard(ctx, [&] { upload_common(ctx, nrows, ncols, nnz, row_ptr, col_idx, values, cudaMemcpyHostToDevice, out); });
 }
 
+int mgpu_csr_upload_batch(mgpu_ctx *ctx, int count, const int64_t *nrows, const int64_t *ncols, const int64_t *nnz,
+                          const int64_t *const *row_ptr, const int32_t *const *col_idx, const double *const *values,
+                          mgpu_csr **out)
+{
+  return guard(ctx, [&] {
+    MG_ARG(count >= 0 && (count == 0 || (nrows && ncols && nnz && row_ptr && col_idx && values && out)),
+           "mgpu_csr_upload: null argument");
+    std::vector<mgpu_csr *> made;
+    try
+    {
+      // every copy and validation queued first, one read-back of all the flags
+      DBuf flags(sizeof(int) * 2 * static_cast<size_t>(count > 0 ? count : 1), ctx->stream);
+      MG_CUDA(cudaMemsetAsync(flags.ptr, 0, sizeof(int) * 2 * count, ctx->stream));
+      for (int q = 0; q < count; ++q)
+      {
+        MG_ARG(nrows[q] >= 0 && ncols[q] >= 0 && nnz[q] >= 0, "SparseMatrix: negative dimension");
+        MG_ARG(row_ptr[q] != nullptr && (nnz[q] == 0 || (col_idx[q] != nullptr && values[q] != nullptr)),
+               "SparseMatrix: null CSR array");
+        MG_ARG(nrows[q] <= INT32_MAX && ncols[q] <= INT32_MAX, "SparseMatrix: dimension exceeds int32 column indices");
+        mgpu_csr *a = new_csr(ctx, nrows[q], ncols[q], nnz[q]);
+        made.push_back(a);
+        MG_CUDA(cudaMemcpyAsync(a->row_ptr, row_ptr[q], sizeof(int64_t) * (nrows[q] + 1), cudaMemcpyHostToDevice,
+                                ctx->stream));
+        if (nnz[q] > 0)
+        {
+          MG_CUDA(cudaMemcpyAsync(a->col_idx, col_idx[q], sizeof(int32_t) * nnz[q], cudaMemcpyHostToDevice,
+                                  ctx->stream));
+          MG_CUDA(cudaMemcpyAsync(a->values, values[q], sizeof(double) * nnz[q], cudaMemcpyHostToDevice, ctx->stream));
+        }
+        if (nrows[q] > 0)
+        {
+          validate_csr<<<blocks_for(nrows[q]), kThreads, 0, ctx->stream>>>(nrows[q], ncols[q], nnz[q], a->row_ptr,
+                                                                           a->col_idx, flags.as<int>() + 2 * q);
+          check_launch(ctx, "validate_csr");
+        }
+      }
+      int *h = static_cast<int *>(pinned_scratch(ctx, sizeof(int) * 2 * static_cast<size_t>(count > 0 ? count : 1)));
+      MG_CUDA(cudaMemcpyAsync(h, flags.ptr, sizeof(int) * 2 * count, cudaMemcpyDeviceToHost, ctx->stream));
+      MG_CUDA(cudaStreamSynchronize(ctx->stream));
+      for (int q = 0; q < count; ++q)
+      {
+        if (h[2 * q] != 0)
+          throw Error(MGPU_ERR_ARG, "SparseMatrix: inconsistent CSR arrays");
+        if (nrows[q] > 0)
+          made[q]->bw = h[2 * q + 1];
+      }
+    }
+    catch (...)
+    {
+      for (auto *a : made)
+        mgpu_csr_free(a);
+      throw;
+    }
+    for (int q = 0; q < count; ++q)
+      out[q] = made[q];
+  });
+}
+
 int mgpu_csr_upload_device(mgpu_ctx *ctx, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t *row_ptr,
                            const int32_t *col_idx, const double *values, mgpu_csr **out)
 {

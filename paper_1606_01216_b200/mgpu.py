@@ -34,6 +34,7 @@ EXPORTED = [
     "mgpu_spai_update", "mgpu_spai_ls", "mgpu_spai_ls_batched", "mgpu_spgemm", "mgpu_cg_solve",
     "mgpu_model_chain", "mgpu_model_hermite", "mgpu_host_free", "mgpu_thin_qr", "mgpu_project_reduce", "mgpu_project_reduce_slab",
     "mgpu_arnoldi_deflate", "mgpu_model_hermite_device", "mgpu_csr_write", "mgpu_csr_read", "mgpu_shifted_solve",
+    "mgpu_csr_upload_batch",
 ]
 
 
@@ -119,6 +120,7 @@ def lib():
         L.mgpu_last_cg_path.argtypes = [vp]
         L.mgpu_csr_upload.argtypes = [vp, i64, i64, i64, vp, vp, vp, C.POINTER(vp)]
         L.mgpu_csr_upload_device.argtypes = [vp, i64, i64, i64, vp, vp, vp, C.POINTER(vp)]
+        L.mgpu_csr_upload_batch.argtypes = [vp, C.c_int, vp, vp, vp, vp, vp, vp, vp]
         L.mgpu_csr_info.argtypes = [vp, vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]
         L.mgpu_csr_download.argtypes = [vp, vp, vp, vp, vp]
         L.mgpu_csr_free.argtypes = [vp]
@@ -301,6 +303,23 @@ class DeviceCsr:
         ctx.check(lib().mgpu_csr_upload(ctx.handle, A.nrows, A.ncols, v.shape[0], _ptr(rp), _ptr(ci), _ptr(v),
                                         C.byref(h)))
         return DeviceCsr(ctx, h, A.nrows)
+
+    @staticmethod
+    def upload_many(mats: Sequence[SparseMatrix], ctx: Optional[Context] = None) -> list:
+        """Several host CSR matrices in one call (mgpu_csr_upload_batch): the same validation as
+        upload, one read-back for all of them."""
+        ctx = ctx or default_context()
+        arrs = [(np.ascontiguousarray(A.row_ptr, np.int64), np.ascontiguousarray(A.col_idx, np.int32),
+                 np.ascontiguousarray(A.values, np.float64)) for A in mats]
+        k = len(mats)
+        nr = np.array([A.nrows for A in mats], np.int64)
+        nc = np.array([A.ncols for A in mats], np.int64)
+        nz = np.array([a[2].shape[0] for a in arrs], np.int64)
+        ptrs = [(C.c_void_p * max(k, 1))(*[a[q].ctypes.data for a in arrs]) for q in range(3)]
+        out = (C.c_void_p * max(k, 1))()
+        ctx.check(lib().mgpu_csr_upload_batch(ctx.handle, k, _ptr(nr), _ptr(nc), _ptr(nz), ptrs[0], ptrs[1], ptrs[2],
+                                              out))
+        return [DeviceCsr(ctx, C.c_void_p(out[q]), mats[q].nrows) for q in range(k)]
 
     @property
     def stored_nnz(self) -> int:

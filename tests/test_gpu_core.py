@@ -119,3 +119,20 @@ def test_binary_csr_sidecar_roundtrip(mg, tmp_path):
     bad.write_bytes(b"not a csr file at all")
     with pytest.raises(mg.ArgumentError, match="not a binary CSR"):
         mg.DeviceCsr.load(str(bad))
+
+
+def test_upload_many_round_trip_and_validation(mg):
+    """DeviceCsr.upload_many (mgpu_csr_upload_batch): the same arrays back bit for bit, and an
+    inconsistent CSR among the batch raises ArgumentError like a single upload."""
+    import numpy as np
+    M, D, K = mg.model_hermite(300)
+    got = mg.DeviceCsr.upload_many([M, D, K])
+    for g, w in zip(got, (M, D, K)):
+        h = g.download()
+        np.testing.assert_array_equal(h.row_ptr, w.row_ptr)
+        np.testing.assert_array_equal(h.col_idx, w.col_idx)
+        np.testing.assert_array_equal(h.values, w.values)
+    bad = mg.SparseMatrix(M.nrows, M.ncols, M.row_ptr.copy(), M.col_idx.copy(), M.values.copy())
+    bad.col_idx[5] = M.ncols + 3  # column out of range
+    with pytest.raises(mg.ArgumentError):
+        mg.DeviceCsr.upload_many([M, bad, K])
