@@ -1453,8 +1453,13 @@ bool v2_solve(mgpu_ctx *ctx, V2Params P, size_t budget)
   size_t best_dyn = 0;
   double best_cost = 1e300;
   V2Params best{};
+  int only_cs = 0; // MGPU_CLUSTER_CS=k: consider cluster size k only (diagnostics)
+  if (const char *f = std::getenv("MGPU_CLUSTER_CS"))
+    only_cs = std::atoi(f);
   for (int cs = 1; cs <= kCMaxCS; ++cs)
   {
+    if (only_cs > 0 && cs != only_cs)
+      continue;
     const int64_t rb = (P.n + cs - 1) / cs;
     if (rb > static_cast<int64_t>(kV2TB) * 4)
       continue;
