@@ -694,12 +694,14 @@ void launch_ls(mgpu_ctx *ctx, int64_t n, int l, DCsr pat, DCsr At, int64_t at_st
 // Runs the LS columns with the smallest lane-group envelope that holds every
 // column; throws the lowest failing (point, column) like the reference's
 // sequential column loop would.
-void run_ls(mgpu_ctx *ctx, int64_t n, int l, int maxrow, DCsr pat, DCsr At, int64_t at_stride, DCsr Kot,
+// abort_dev (optional): a device flag read with the status; nonzero means the batch's shared-
+// pattern assumption was wrong, and run_ls returns false without interpreting the results.
+bool run_ls(mgpu_ctx *ctx, int64_t n, int l, int maxrow, DCsr pat, DCsr At, int64_t at_stride, DCsr Kot,
             int64_t ko_stride, bool update, double *out, int64_t out_stride, const int *extra_dev = nullptr,
-            int *extra_host = nullptr, int64_t pat_bw = -1)
+            int *extra_host = nullptr, int64_t pat_bw = -1, const int *abort_dev = nullptr)
 {
   if (n == 0 || l == 0)
-    return;
+    return true;
   DBuf err(sizeof(unsigned long long), ctx->stream), ovf(sizeof(int), ctx->stream);
   // lane-per-column envelopes first (|J| <= 5 / 6 / 8 pattern entries, |I| <= 13 / 14 / 16 rows),
   // then the lane-group kernels; MGPU_LS_GROUP=1 skips the lane kernels (diagnostics).  The
@@ -730,21 +732,27 @@ void run_ls(mgpu_ctx *ctx, int64_t n, int l, int maxrow, DCsr pat, DCsr At, int6
     else
       launch_ls<32, 64, 1>(ctx, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev, ovf.as<int>());
     // one synchronisation returns the error key, the overflow flag and the caller's extra value
-    auto *hp = static_cast<unsigned long long *>(pinned_scratch(ctx, 3 * sizeof(unsigned long long)));
+    auto *hp = static_cast<unsigned long long *>(pinned_scratch(ctx, 4 * sizeof(unsigned long long)));
     MG_CUDA(cudaMemcpyAsync(hp, err.ptr, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
     MG_CUDA(cudaMemcpyAsync(hp + 1, ovf.ptr, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     if (extra_dev)
       MG_CUDA(cudaMemcpyAsync(hp + 2, extra_dev, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    if (abort_dev)
+      MG_CUDA(cudaMemcpyAsync(hp + 3, abort_dev, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     MG_CUDA(cudaStreamSynchronize(ctx->stream));
     const unsigned long long h = hp[0];
-    int h_ovf = 0;
+    int h_ovf = 0, h_abort = 0;
     std::memcpy(&h_ovf, hp + 1, sizeof(int));
     if (extra_dev)
       std::memcpy(extra_host, hp + 2, sizeof(int));
+    if (abort_dev)
+      std::memcpy(&h_abort, hp + 3, sizeof(int));
+    if (h_abort)
+      return false;
     if (h_ovf)
       continue; // a column exceeded this envelope: rerun everything with the next one
     if (h == ULLONG_MAX)
-      return;
+      return true;
     const int64_t g = static_cast<int64_t>(h >> 8);
     const int64_t col = g % n, pt = g / n;
     throw Error(MGPU_ERR_NUMERICAL, "spai_ls: rank-deficient least-squares problem in column " + std::to_string(col),
@@ -798,6 +806,27 @@ bool same_pattern(mgpu_ctx *ctx, int l, const mgpu_csr *const *mats, const mgpu_
   MG_CUDA(cudaMemcpyAsync(&h, diff.ptr, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   MG_CUDA(cudaStreamSynchronize(ctx->stream));
   return h == 0;
+}
+
+// Queues the structure comparison of mats[] against ref, OR-ing a mismatch into *diff_dev; false
+// when the host-side sizes already differ (nothing queued: the patterns differ).
+bool queue_pattern_diff(mgpu_ctx *ctx, int l, const mgpu_csr *const *mats, const mgpu_csr *ref, int *diff_dev)
+{
+  if (l > 64)
+    return false;
+  PatternPtrs pp{};
+  for (int p = 0; p < l; ++p)
+  {
+    if (mats[p]->nrows != ref->nrows || mats[p]->ncols != ref->ncols || mats[p]->nnz != ref->nnz)
+      return false;
+    pp.rp[p] = mats[p]->row_ptr;
+    pp.ci[p] = mats[p]->col_idx;
+  }
+  const int64_t span = std::max<int64_t>(ref->nrows + 1, ref->nnz);
+  pattern_diff<<<blocks_for(span), kThreads, 0, ctx->stream>>>(l, ref->nrows, ref->nnz, pp, ref->row_ptr, ref->col_idx,
+                                                               diff_dev);
+  check_launch(ctx, "pattern_diff");
+  return true;
 }
 
 // Symbolic pattern of A*A (values = 1.0 placeholders).
@@ -897,8 +926,10 @@ mgpu_csr *spai_ls_one(mgpu_ctx *ctx, const mgpu_csr *A, const mgpu_csr *K_old, i
 // of one system do): the pattern work -- J pattern, A^T structure and the
 // value permutation, P^T -> P permutation -- is done once, the l * n column
 // problems run in ONE launch, and each factor is a gather of its values.
+// diff_dev (optional): the speculative shared-pattern flag (queue_pattern_diff); when it turns out
+// set, everything is released and an empty vector returned (the caller takes the per-operator path).
 std::vector<mgpu_csr *> spai_ls_shared(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, const mgpu_csr *const *K_old,
-                                       int pattern)
+                                       int pattern, const int *diff_dev = nullptr)
 {
   const mgpu_csr *A0 = A[0];
   const int64_t n = A0->nrows, nnzA = A0->nnz;
@@ -949,8 +980,13 @@ std::vector<mgpu_csr *> spai_ls_shared(mgpu_ctx *ctx, int l, const mgpu_csr *con
     const bool fetch = !sq && At0->maxrow < 0 && n > 0;
     // J pattern bandwidth: A's, doubled for the symbolic A^2
     const int64_t bwA = csr_bandwidth(ctx, const_cast<mgpu_csr *>(A0));
-    run_ls(ctx, n, l, maxrow, pat->view(), atv, nnzA, kov, nnzA, K_old != nullptr, pt_vals.as<double>(), nnzJ,
-           fetch ? mx.as<int>() : nullptr, fetch ? &at_maxrow : nullptr, sq ? 2 * bwA : bwA);
+    if (!run_ls(ctx, n, l, maxrow, pat->view(), atv, nnzA, kov, nnzA, K_old != nullptr, pt_vals.as<double>(), nnzJ,
+                fetch ? mx.as<int>() : nullptr, fetch ? &at_maxrow : nullptr, sq ? 2 * bwA : bwA, diff_dev))
+    {
+      mgpu_csr_free(At0);
+      mgpu_csr_free(sq);
+      return {};
+    }
     if (fetch)
       At0->maxrow = at_maxrow;
     // P^T (J pattern) -> P: one structure and one permutation for every factor.  On A's
@@ -1051,12 +1087,20 @@ int mgpu_spai_ls_batched(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, const m
                                                                    K_old[i]->ncols == A[i]->ncols)),
              "spai_ls: operands must be square with equal shape");
     MG_ARG(pattern == MGPU_PATTERN_A || pattern == MGPU_PATTERN_A2, "spai_ls: unknown pattern");
-    if (l >= 2 && same_pattern(ctx, l, A, A[0]) && (!K_old || same_pattern(ctx, l, K_old, A[0])))
+    // shared-pattern path, speculatively: the structure comparison is queued, not awaited; its
+    // flag comes back with the LS status, and on a mismatch the batch reruns per operator
+    DBuf diff(sizeof(int), ctx->stream);
+    MG_CUDA(cudaMemsetAsync(diff.ptr, 0, sizeof(int), ctx->stream));
+    if (l >= 2 && queue_pattern_diff(ctx, l, A, A[0], diff.as<int>()) &&
+        (!K_old || queue_pattern_diff(ctx, l, K_old, A[0], diff.as<int>())))
     {
-      std::vector<mgpu_csr *> made = spai_ls_shared(ctx, l, A, K_old, pattern);
-      for (int i = 0; i < l; ++i)
-        P[i] = made[i];
-      return;
+      std::vector<mgpu_csr *> made = spai_ls_shared(ctx, l, A, K_old, pattern, diff.as<int>());
+      if (!made.empty())
+      {
+        for (int i = 0; i < l; ++i)
+          P[i] = made[i];
+        return;
+      }
     }
     std::vector<mgpu_csr *> made;
     try

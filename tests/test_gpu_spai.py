@@ -224,6 +224,29 @@ def test_ls_batched_mixed_patterns(mg, oracle):
     _csr_equal(facs[1].matrix.download(), oracle.spai_ls(A2, None, 0))
 
 
+def test_ls_batched_same_nnz_different_structure(mg, oracle):
+    """Equal sizes and nnz but different column positions: the speculative shared-pattern path
+    must detect the mismatch (device flag read with the LS status) and rerun per operator."""
+    import numpy as np
+    from oracle import Csr
+    n = 300
+    rng = np.random.default_rng(5)
+    base = np.diag(np.full(n, 4.0)) + np.diag(np.full(n - 1, -1.0), 1) + np.diag(np.full(n - 1, -1.0), -1)
+    a1 = base.copy()
+    a2 = base.copy()
+    # move one off-diagonal pair in a2 (same nnz, different structure), keep it symmetric
+    a2[10, 11] = a2[11, 10] = 0.0
+    a2[10, 12] = a2[12, 10] = -1.0
+    a1 += np.diag(rng.uniform(0.0, 0.5, n))
+    a2 += np.diag(rng.uniform(0.0, 0.5, n))
+    A1, A2 = Csr.from_dense(a1), Csr.from_dense(a2)
+    assert A1.nnz == A2.nnz
+    facs = mg.spai_ls_batched([A1, A2, A1], None, 0)
+    _csr_equal(facs[0].matrix.download(), oracle.spai_ls(A1, None, 0))
+    _csr_equal(facs[1].matrix.download(), oracle.spai_ls(A2, None, 0))
+    _csr_equal(facs[2].matrix.download(), oracle.spai_ls(A1, None, 0))
+
+
 # ------------------------------------------------------------------ SpGEMM chain collapse
 def test_spgemm_collapse(mg, oracle):
     M, D, K = oracle.hermite_generate(400)
