@@ -21,6 +21,7 @@
 #include <climits>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <vector>
 
@@ -698,7 +699,8 @@ void launch_ls(mgpu_ctx *ctx, int64_t n, int l, DCsr pat, DCsr At, int64_t at_st
 // pattern assumption was wrong, and run_ls returns false without interpreting the results.
 bool run_ls(mgpu_ctx *ctx, int64_t n, int l, int maxrow, DCsr pat, DCsr At, int64_t at_stride, DCsr Kot,
             int64_t ko_stride, bool update, double *out, int64_t out_stride, const int *extra_dev = nullptr,
-            int *extra_host = nullptr, int64_t pat_bw = -1, const int *abort_dev = nullptr)
+            int *extra_host = nullptr, int64_t pat_bw = -1, const int *abort_dev = nullptr,
+            const std::function<void()> &after_launch = {})
 {
   if (n == 0 || l == 0)
     return true;
@@ -731,6 +733,8 @@ bool run_ls(mgpu_ctx *ctx, int64_t n, int l, int maxrow, DCsr pat, DCsr At, int6
       launch_ls<16, 32, 2>(ctx, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev, ovf.as<int>());
     else
       launch_ls<32, 64, 1>(ctx, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev, ovf.as<int>());
+    if (after_launch) // caller's dependent work, queued behind the LS kernel before the read-back
+      after_launch();
     // one synchronisation returns the error key, the overflow flag and the caller's extra value
     auto *hp = static_cast<unsigned long long *>(pinned_scratch(ctx, 4 * sizeof(unsigned long long)));
     MG_CUDA(cudaMemcpyAsync(hp, err.ptr, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
@@ -980,20 +984,71 @@ std::vector<mgpu_csr *> spai_ls_shared(mgpu_ctx *ctx, int l, const mgpu_csr *con
     const bool fetch = !sq && At0->maxrow < 0 && n > 0;
     // J pattern bandwidth: A's, doubled for the symbolic A^2
     const int64_t bwA = csr_bandwidth(ctx, const_cast<mgpu_csr *>(A0));
-    if (!run_ls(ctx, n, l, maxrow, pat->view(), atv, nnzA, kov, nnzA, K_old != nullptr, pt_vals.as<double>(), nnzJ,
-                fetch ? mx.as<int>() : nullptr, fetch ? &at_maxrow : nullptr, sq ? 2 * bwA : bwA, diff_dev))
+    // P^T (J pattern) -> P: one structure and one permutation for every factor.  On A's
+    // pattern P^T has A0's CSR structure, so P has At0's and the values follow perm_t: the
+    // factors are made and their value gather queued behind the LS kernel, before its status
+    // read-back.  On A^2's the J pattern is transposed once, after the LS solve.
+    const int64_t ba = csr_bandwidth(ctx, const_cast<mgpu_csr *>(A0));
+    std::vector<const double *> gsrc;
+    std::vector<double *> gdst;
+    mgpu_ctx *owner_ctx = ctx;
+    auto make_factors = [&](mgpu_csr *S, int64_t pmax) {
+      // hand S's structure to the factors (shared, freed by the last one)
+      int64_t *srp = S->row_ptr;
+      int32_t *sci = S->col_idx;
+      std::shared_ptr<void> structure(srp, [owner_ctx, sci](void *rp) {
+        cudaFreeAsync(rp, owner_ctx->stream);
+        cudaFreeAsync(sci, owner_ctx->stream);
+      });
+      S->row_ptr = nullptr;
+      S->col_idx = nullptr;
+      // every factor's values in one allocation (slices), released with the last factor
+      double *vblock = nullptr;
+      MG_CUDA(mg_malloc(reinterpret_cast<void **>(&vblock),
+                        sizeof(double) * static_cast<size_t>(l) * (nnzJ > 0 ? nnzJ : 1), s));
+      std::shared_ptr<void> values(vblock, [owner_ctx](void *v) { cudaFreeAsync(v, owner_ctx->stream); });
+      for (int p = 0; p < l; ++p)
+      {
+        auto *P = new mgpu_csr;
+        P->ctx = ctx;
+        P->nrows = n;
+        P->ncols = n;
+        P->nnz = nnzJ;
+        P->row_ptr = srp;
+        P->col_idx = sci;
+        P->shared_structure = structure;
+        out.push_back(P);
+        P->values = vblock + static_cast<size_t>(p) * (nnzJ > 0 ? nnzJ : 1);
+        P->shared_values = values;
+        P->may_hold_zeros = true;
+        P->bw = pattern == MGPU_PATTERN_A2 ? 2 * ba : ba;
+        P->maxrow = pmax;
+        gsrc.push_back(pt_vals.as<double>() + p * nnzJ);
+        gdst.push_back(P->values);
+      }
+    };
+    std::function<void()> gather_early;
+    if (!sq)
     {
+      make_factors(At0, At0->maxrow); // maxrow set below once fetched
+      gather_early = [&]() { gather_batched(ctx, l, nnzJ, perm_t.as<int64_t>(), gsrc.data(), gdst.data()); };
+    }
+    if (!run_ls(ctx, n, l, maxrow, pat->view(), atv, nnzA, kov, nnzA, K_old != nullptr, pt_vals.as<double>(), nnzJ,
+                fetch ? mx.as<int>() : nullptr, fetch ? &at_maxrow : nullptr, sq ? 2 * bwA : bwA, diff_dev,
+                gather_early))
+    {
+      for (auto *m : out)
+        mgpu_csr_free(m);
       mgpu_csr_free(At0);
       mgpu_csr_free(sq);
       return {};
     }
     if (fetch)
+    {
       At0->maxrow = at_maxrow;
-    // P^T (J pattern) -> P: one structure and one permutation for every factor.  On A's
-    // pattern P^T has A0's CSR structure, so P has At0's and the values follow perm_t;
-    // on A^2's the J pattern is transposed once.
-    mgpu_csr *S = At0;
-    const int64_t *permP = perm_t.as<int64_t>();
+      for (auto *P : out)
+        P->maxrow = at_maxrow;
+    }
     if (sq)
     {
       PT0 = new_csr(ctx, n, n, nnzJ);
@@ -1001,49 +1056,10 @@ std::vector<mgpu_csr *> spai_ls_shared(mgpu_ctx *ctx, int l, const mgpu_csr *con
       if (nnzJ > 0)
         MG_CUDA(cudaMemcpyAsync(PT0->col_idx, pat->col_idx, sizeof(int32_t) * nnzJ, cudaMemcpyDeviceToDevice, s));
       P0 = transpose_perm(ctx, PT0, perm_p);
-      S = P0;
-      permP = perm_p.as<int64_t>();
+      make_factors(P0, csr_max_row(ctx, P0)); // every factor has P0's stored pattern
+      gather_batched(ctx, l, nnzJ, perm_p.as<int64_t>(), gsrc.data(), gdst.data());
     }
-    const int64_t ba = csr_bandwidth(ctx, const_cast<mgpu_csr *>(A0));
-    const int64_t pmax = csr_max_row(ctx, S); // every factor has S's stored pattern
-    // hand S's structure to the factors (shared, freed by the last one)
-    int64_t *srp = S->row_ptr;
-    int32_t *sci = S->col_idx;
-    mgpu_ctx *owner_ctx = ctx;
-    std::shared_ptr<void> structure(srp, [owner_ctx, sci](void *rp) {
-      cudaFreeAsync(rp, owner_ctx->stream);
-      cudaFreeAsync(sci, owner_ctx->stream);
-    });
-    S->row_ptr = nullptr;
-    S->col_idx = nullptr;
-    std::vector<const double *> gsrc;
-    std::vector<double *> gdst;
-    // every factor's values in one allocation (slices), released with the last factor
-    double *vblock = nullptr;
-    MG_CUDA(mg_malloc(reinterpret_cast<void **>(&vblock),
-                      sizeof(double) * static_cast<size_t>(l) * (nnzJ > 0 ? nnzJ : 1), s));
-    std::shared_ptr<void> values(vblock, [owner_ctx](void *v) { cudaFreeAsync(v, owner_ctx->stream); });
-    for (int p = 0; p < l; ++p)
-    {
-      auto *P = new mgpu_csr;
-      P->ctx = ctx;
-      P->nrows = n;
-      P->ncols = n;
-      P->nnz = nnzJ;
-      P->row_ptr = srp;
-      P->col_idx = sci;
-      P->shared_structure = structure;
-      out.push_back(P);
-      P->values = vblock + static_cast<size_t>(p) * (nnzJ > 0 ? nnzJ : 1);
-      P->shared_values = values;
-      P->may_hold_zeros = true;
-      P->bw = pattern == MGPU_PATTERN_A2 ? 2 * ba : ba;
-      P->maxrow = pmax;
-      gsrc.push_back(pt_vals.as<double>() + p * nnzJ);
-      gdst.push_back(P->values);
-    }
-    gather_batched(ctx, l, nnzJ, permP, gsrc.data(), gdst.data());
-    host_mark("spai_ls_shared: last gather queued");
+    host_mark("spai_ls_shared: factors made");
   }
   catch (...)
   {
