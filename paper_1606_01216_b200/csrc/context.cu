@@ -320,6 +320,9 @@ int mgpu_ctx_destroy(mgpu_ctx *ctx)
     cublasDestroy(static_cast<cublasHandle_t>(ctx->blas));
   if (ctx->pin)
     cudaFreeHost(ctx->pin);
+  for (auto &e : ctx->phase_ev)
+    if (e)
+      cudaEventDestroy(e);
   if (ctx->prof_dev)
   {
     long long h[16] = {0};

@@ -137,6 +137,7 @@ struct mgpu_ctx
   int cg_path = 0;      // 0 auto, 1 force general, 2 force banded grid kernel, 3 cluster v1 only, 4 stream (no cluster)
   long long *prof_dev = nullptr; // diagnostics: per-phase clock64 totals of the cluster kernel (MGPU_PROFILE_PHASES)
   void *blas = nullptr;          // cublasHandle_t, created on first dense product (project.cu)
+  cudaEvent_t phase_ev[4] = {nullptr, nullptr, nullptr, nullptr}; // mgpu_shifted_solve phase timing (lazy)
   void *pin = nullptr;           // pinned host staging for small device -> host reads (grown on demand)
   size_t pin_bytes = 0;
   // last error

@@ -21,10 +21,10 @@ int mgpu_shifted_solve(mgpu_ctx *ctx, const mgpu_csr *M, const mgpu_csr *D, cons
       (pattern != -1 && pattern != MGPU_PATTERN_A && pattern != MGPU_PATTERN_A2))
     return guard(ctx, [&] { MG_ARG(false, "shifted_solve: bad argument"); });
   cudaStream_t s = ctx->stream;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t *ev = ctx->phase_ev; // created once per context
   if (phase_ms)
-    for (auto &e : ev)
-      if (cudaEventCreate(&e) != cudaSuccess)
+    for (int k = 0; k < 4; ++k)
+      if (!ev[k] && cudaEventCreate(&ev[k]) != cudaSuccess)
         return guard(ctx, [&] { MG_CUDA(cudaGetLastError()); });
   auto rec = [&](int k) {
     if (phase_ms)
@@ -60,11 +60,7 @@ int mgpu_shifted_solve(mgpu_ctx *ctx, const mgpu_csr *M, const mgpu_csr *D, cons
     cudaEventSynchronize(ev[3]);
     float t = 0.f;
     for (int k = 0; k < 3; ++k)
-    {
       phase_ms[k] = cudaEventElapsedTime(&t, ev[k], ev[k + 1]) == cudaSuccess ? t : -1.0;
-    }
-    for (auto &e : ev)
-      cudaEventDestroy(e);
   }
   release();
   return st;
