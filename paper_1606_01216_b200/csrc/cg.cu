@@ -2733,16 +2733,18 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
   const size_t stat = sizeof(BandShared<TB + 32>) + sizeof(PEll) * kTabSlots * (kMaxZ + 1) + 128;
   // (chunk rows, ring depth) in order of preference; MGPU_STREAM_CFG="rows,depth" forces one (diagnostics)
   // largest chunk first (per-chunk barriers and pipeline bookkeeping amortise over its rows), 3-deep ring
-  // before 2-deep at equal height.  With m >= 4, heights that are multiples of 128 rows are skipped:
-  // with every block striding through HBM in lock step they measured 3-4% slower on configs[3]
-  // (512 / 640 rows: 872 / 876 us per iteration against 843 / 836 for 576 / 448 rows); m = 1
+  // before 2-deep at equal height.  With m >= 4 the height is capped at 448 rows and multiples of
+  // 128 rows are skipped: with every block striding through HBM in lock step, 512 / 640 rows
+  // measured 872 / 876 us per iteration on configs[3] against 843 / 836 for 576 / 448, and 448
+  // (2-deep) against the 576 default gave configs[3] 847 -> 837, configs[4] 4152 -> 4085.  m = 1
   // (configs[2] shape) measured best on its largest chunk.
   std::vector<std::pair<int64_t, int>> cands;
   for (int64_t ch = 1024; ch >= 128; ch -= 64)
   {
-    if (m >= 4 && ch % 128 == 0)
+    if (m >= 4 && (ch % 128 == 0 || ch > 448))
       continue;
-    cands.push_back({ch, 3});
+    if (m < 4) // m >= 4: 2-deep only (448 rows 3-deep measured 924 us against 837 2-deep)
+      cands.push_back({ch, 3});
     cands.push_back({ch, 2});
   }
   cands.push_back({128, 3});
