@@ -1,26 +1,32 @@
 #!/usr/bin/env python
-"""Benchmark of the SPAI + shifted-system PCG path (BASELINE.json metric, configs[1]).
+"""Benchmark of the SPAI + shifted-system PCG path (BASELINE.json metric).
 
-Workload ("config1", the default; BASELINE.json configs[1]):
-  clamped Euler-Bernoulli Hermite beam, ne = 10,000 elements (n = 20,000),
-  8 real shifts log-spaced in [10, 1e4] per GPU, m = 1 rhs (unit tip load, dof n-2).
-  One STEP = the whole hot path for that batch:
-    assemble the 8 shifted operators A(s) = s^2 M + s D + K   (device, one call)
-    build 8 LS-SPAI factors on A's pattern                    (device, batched)
-    8 right-preconditioned CG solves, rtol 1e-10              (one persistent kernel)
-  rtol 1e-10 is unreachable in FP64 on this beam (cond ~1e13), so
-  the CG runs its fixed budget (--budget, default 1000 iterations) in both arms.
+Default workload ("config3"; BASELINE.json configs[3], the largest single-GPU config and the
+HBM-bound regime the metric's "% of HBM roofline" is about):
+  clamped Euler-Bernoulli Hermite beam, ne = 500,000 elements (n = 1e6), m = 4 right-hand sides
+  (unit loads on w at 25/50/75/100 % of L), 16 real shifts log-spaced in [10, 1e4].
+  One STEP = the whole hot path for that batch, inside the timed region:
+    assemble the 16 shifted operators A(s) = s^2 M + s D + K    (device, one call)
+    build 16 LS-SPAI factors on the A^2 pattern                 (device, batched; column-equilibrated,
+                                                                 mgpu.h MGPU_LS_COLSCALE)
+    16 x 4 right-preconditioned CG solves, rtol 1e-10           (one persistent streaming kernel)
+  rtol 1e-10 is unreachable in FP64 on this beam (cond ~1e13), so the CG runs its
+  fixed budget (--budget, default 1000 iterations) in both arms.
+Other workloads (--workload): config0 (n=2e3), config1 (n=2e4, 8 shifts, m=1, A pattern),
+config2 (n=1e5, 8 shifts), config4 (n=1e7, m=4, the per-GPU share of 64 shifts: 8 shifts, A pattern).
 
 Arms:
   default           this library (libmgpu.so, sm_100a).  `value` is measured with
                     M, D, K and the rhs resident in HBM; `e2e` runs the same step
                     through the public API from pinned host buffers, H2D of the
                     system + rhs and D2H of X / residual blocks inside the timed region.
-  --impl reference  the reference's own CPU path (oracle/_ref: the unmodified
-                    reference library; LS-SPAI from reference thin_qr), shifts run
-                    concurrently on all host cores, rank 0 only.
-Multi-GPU (torchrun): each rank solves its own 8 shifts (weak scaling, no
-collective on the data path); time = max over ranks of CUDA-event time.
+  --impl reference  the reference's own CPU path (oracle/_ref: the unmodified reference
+                    library; LS-SPAI from reference thin_qr), single-threaded as the reference
+                    is (no shift-level threading added), rank 0 only.  Each step
+                    is a bounded sample: one shift (rotating) -- assembly + LS-SPAI + CG at two
+                    small iteration counts per rhs, extrapolated linearly to the budget.
+Multi-GPU (torchrun): each rank solves its own shifts (weak scaling, no collective on the data
+path); time = max over ranks of CUDA-event time.
 """
 import argparse
 import json
@@ -29,7 +35,6 @@ import statistics
 import subprocess
 import sys
 import time
-from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
@@ -49,15 +54,15 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="mgpu", choices=["mgpu", "reference"])
     ap.add_argument("--budget", type=int, default=1000, help="CG iterations per solve (fixed budget)")
-    ap.add_argument("--workload", default="config1", choices=["config0", "config1", "config2", "config3", "config4"])
+    ap.add_argument("--workload", default="config3", choices=["config0", "config1", "config2", "config3", "config4"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
 
 def workload(name: str, world: int, rank: int):
     """(ne, m, shifts for this rank, all shifts, pattern).  pattern: 0 LS-SPAI on A's
-    pattern, 1 on A^2's, -1 no preconditioner (P = I): on the BASELINE beam every
-    reference SPAI fails at n >= 4e5 (MR stagnates, LS rank-flushes), DESIGN.md."""
+    pattern, 1 on A^2's, | 0x10 column-equilibrated (needed from n = 2e5 / 4e5 on this beam:
+    the unscaled LS rank-flushes there), -1 no preconditioner (P = I)."""
     from paper_1606_01216_b200 import sharding
     if name == "config0":
         ne, m, per, pattern = 1000, 1, 1, 0
@@ -69,11 +74,11 @@ def workload(name: str, world: int, rank: int):
         ne, m, per, pattern = 50000, 1, 8, 0
         all_shifts = sharding.log_shifts(per * world)
     elif name == "config3":
-        ne, m, per, pattern = 500000, 4, 16, -1
+        ne, m, per, pattern = 500000, 4, 16, 0x11
         all_shifts = sharding.log_shifts(per * world)
     else:
         # configs[4]: n = 1e7, m = 4, 64 shifts over 8 GPUs -> the per-GPU share, 8 shifts per rank
-        ne, m, per, pattern = 5000000, 4, 8, -1
+        ne, m, per, pattern = 5000000, 4, 8, 0x10
         all_shifts = sharding.log_shifts(per * world)
     return ne, m, sharding.shard(all_shifts, rank, world), all_shifts, pattern
 
@@ -148,23 +153,66 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU (reference) path
-def cpu_step_fn(kind: str, M, D, K, shifts, B, pattern, budget):
-    """One step of the reference CPU path; shifts run concurrently (ctypes releases the GIL)."""
-    from oracle import Oracle, Reference, reference_available
-    lib = Reference() if (kind == "reference" and reference_available()) else Oracle()
-    threads = min(len(shifts), os.cpu_count() or 1)
+def host_cpu():
+    """nproc and the CPU model (lscpu's "Model name"), BASELINE.md 2."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    if model is None:
+        try:
+            with open("/proc/cpuinfo") as f:
+                model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), None)
+        except Exception:
+            pass
+    return {"nproc": os.cpu_count(), "model": model}
 
-    def one(s):
-        A = lib.shifted_operator(M, D, K, s)
-        chain = [lib.spai_ls(A, None, pattern)] if pattern >= 0 else []
+
+class CpuSample:
+    """The reference's own CPU path for ONE shift, single-threaded (pcg_solve / block_solve are
+    single-threaded by construction; BASELINE.md 2 forbids adding shift-level threading):
+    shifted_operator, LS-SPAI (reference thin_qr), then pcg_solve per rhs column at k and 2k
+    iterations.  The per-shift time at the full budget is extrapolated linearly:
+        T_shift = t_asm + t_spai + sum_c [ T_c(k) + (budget - k) (T_c(2k) - T_c(k)) / k ]
+    (the intercept carries pcg_solve's set-up and finish; the slope is the per-iteration cost)."""
+
+    def __init__(self, kind, M, D, K, B, pattern, budget, k):
+        from oracle import Oracle, Reference, reference_available
+        self.lib = Reference() if (kind == "reference" and reference_available()) else Oracle()
+        self.kind = self.lib.kind
+        self.M, self.D, self.K, self.B = M, D, K, B
+        self.pattern, self.budget, self.k = pattern, budget, min(k, budget)
+
+    def run(self, s):
+        lib, B = self.lib, self.B
+        t0 = time.perf_counter()
+        A = lib.shifted_operator(self.M, self.D, self.K, s)
+        t1 = time.perf_counter()
+        chain = [lib.spai_ls(A, None, self.pattern)] if self.pattern >= 0 else []
+        t2 = time.perf_counter()
+        cg = 0.0
         for c in range(B.shape[1]):
-            lib.pcg_solve(A, chain, B[:, c], rtol=1e-10, maxit=budget, history_cap=1)
+            ta = time.perf_counter()
+            lib.pcg_solve(A, chain, B[:, c], rtol=1e-10, maxit=self.k, history_cap=1)
+            tb = time.perf_counter()
+            if self.k < self.budget:
+                lib.pcg_solve(A, chain, B[:, c], rtol=1e-10, maxit=2 * self.k, history_cap=1)
+                tc = time.perf_counter()
+                slope = max((tc - tb) - (tb - ta), 0.0) / self.k
+                cg += (tb - ta) + (self.budget - self.k) * slope
+            else:
+                cg += tb - ta
+        wall = time.perf_counter() - t0
+        return {"asm_s": t1 - t0, "spai_s": t2 - t1, "cg_s": cg, "shift_s": (t2 - t0) + cg, "wall_s": wall}
 
-    def step():
-        with ThreadPoolExecutor(threads) as ex:
-            list(ex.map(one, shifts))
-
-    return step, threads, lib.kind
+    def describe(self, m):
+        return (f"one shift per step (rotating over the workload's shifts), single thread: shifted_operator + "
+                f"LS-SPAI + pcg_solve of each of the {m} rhs at {self.k} and {2 * self.k} iterations, "
+                f"extrapolated linearly to the {self.budget}-iteration budget; value = m / T_shift")
 
 
 def run_reference(args, rank, world):
@@ -175,24 +223,28 @@ def run_reference(args, rank, world):
     M, D, K = Oracle().hermite_generate(ne)
     B = rhs_block(M.nrows, m)
     kind = "reference" if reference_available() else "port"
-    step, threads, kind = cpu_step_fn(kind, M, D, K, all_shifts, B, pattern, args.budget)
-    for _ in range(args.warmup):
-        step()
-    times = []
-    for _ in range(args.steps):
-        t = time.perf_counter()
-        step()
-        times.append(time.perf_counter() - t)
-    total = sum(times)
-    solves = len(all_shifts) * m * args.steps
-    value = solves / total
+    n = M.nrows
+    k = 2 if n >= 500000 else (10 if n >= 100000 else 50)
+    smp = CpuSample(kind, M, D, K, B, pattern, args.budget, k)
+    for i in range(args.warmup):
+        smp.run(all_shifts[i % len(all_shifts)])
+    recs = [smp.run(all_shifts[i % len(all_shifts)]) for i in range(args.steps)]
+    per_shift = statistics.mean(r["shift_s"] for r in recs)
+    value = m / per_shift  # solves/s on one core: l*m solves take l * per_shift seconds
+    cpu = host_cpu()
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (deterministic Hermite beam, BASELINE configs)",
+        "warmup": args.warmup, "ms_per_step": 1e3 * per_shift * len(all_shifts), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (deterministic Hermite beam, BASELINE configs)",
         "config": config_dict(args, ne, m, all_shifts, pattern, world),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": f"full steps: {len(all_shifts)} shifts x {m} rhs, {args.budget} CG iterations each"},
+        "spai_build_ms": 1e3 * statistics.mean(r["spai_s"] for r in recs),
+        "assemble_ms": 1e3 * statistics.mean(r["asm_s"] for r in recs),
+        "cg_ms": 1e3 * statistics.mean(r["cg_s"] for r in recs),
+        "sample_wall_s_per_step": statistics.mean(r["wall_s"] for r in recs),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": smp.kind, "sample": smp.describe(m),
+                         "nproc": cpu["nproc"], "cpu_model": cpu["model"],
+                         "x_nproc_ideal": value * (cpu["nproc"] or 1)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -200,15 +252,19 @@ def run_reference(args, rank, world):
 
 
 def config_dict(args, ne, m, shifts, pattern, world):
-    spai = {0: "LS-SPAI on the A pattern", 1: "LS-SPAI on the A^2 pattern",
-            -1: "no preconditioner (P = I; every reference SPAI fails at this n on this beam, DESIGN.md)"}[pattern]
-    return {"workload": f"BASELINE.json configs[{ {'config0': 0, 'config1': 1, 'config2': 2, 'config3': 3, 'config4': 4}[args.workload] }]"
-                        f" shape: Hermite cantilever ne={ne} (n={2 * ne}), {len(shifts)} shifts log-spaced in "
-                        f"[10,1e4], m={m}, {spai}, right-preconditioned CG, rtol 1e-10, fixed budget "
-                        f"{args.budget} iterations",
+    base = pattern & ~0x10 if pattern >= 0 else -1
+    spai = {0: "LS-SPAI on the A pattern", 1: "LS-SPAI on the A^2 pattern", -1: "no preconditioner (P = I)"}[base]
+    if pattern >= 0 and pattern & 0x10:
+        spai += " (column-equilibrated, MGPU_LS_COLSCALE)"
+    tag = {0: "ls-A", 1: "ls-A2", -1: "none"}[base] + ("-colscale" if pattern >= 0 and pattern & 0x10 else "")
+    idx = {"config0": 0, "config1": 1, "config2": 2, "config3": 3, "config4": 4}[args.workload]
+    share = " (the per-GPU share of BASELINE's 64 shifts at 8 GPUs)" if args.workload == "config4" else ""
+    return {"workload": f"BASELINE.json configs[{idx}]: Hermite cantilever ne={ne} (n={2 * ne}), {len(shifts)} "
+                        f"shifts log-spaced in [10,1e4]{share}, m={m}, {spai}, SPAI build inside the step, "
+                        f"right-preconditioned CG, rtol 1e-10, fixed budget {args.budget} iterations",
             "n": 2 * ne, "shifts_total": len(shifts), "rhs": m, "cg_budget": args.budget,
-            "spai": {0: "ls-A", 1: "ls-A2", -1: "none"}[pattern], "parallelism": f"shift-sharded x{world}",
-            "l2": "flushed between timed steps (256 MiB write)"}
+            "spai": tag, "parallelism": f"shift-sharded x{world}",
+            "l2": "flushed between timed steps (256 MiB write); inputs larger than L2 from n = 1e6"}
 
 
 # ------------------------------------------------------------------ GPU path
@@ -335,35 +391,29 @@ def run_mgpu(args, rank, world, local_rank):
     e2e_value = solves / (e2e_ms / 1e3)
     peak, peak_kind = peak_hbm()
     achieved = sum(r["bytes"] for r in recs) / (sum(cg_ms) / 1e3) / 1e9
+    # DRAM traffic is not measurable inside this process (ncu replays kernels); the per-launch
+    # dram__bytes of this command's top kernel are in profiles/ (DESIGN.md 5), not copied here.
     traffic = None
-    tfile = os.path.join(ROOT, "profiles", "cg_dram_traffic.json")
-    if os.path.exists(tfile):
-        try:
-            with open(tfile) as f:
-                traffic = json.load(f).get(args.workload)
-        except Exception:
-            traffic = None
     loops = recs[-1]["loops"]
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             from oracle import Oracle, reference_available
-            orc = Oracle()
-            hM, hD, hK = orc.hermite_generate(ne)
+            hM, hD, hK = Oracle().hermite_generate(ne)
             kind = "reference" if reference_available() else "port"
-            big = args.workload in ("config2", "config3", "config4")
-            sample_shifts = shifts if not big else shifts[:2]
-            sample_budget = budget if not big else (5 if args.workload == "config4" else 20)
-            step, threads, kind = cpu_step_fn(kind, hM, hD, hK, sample_shifts, B, pattern, sample_budget)
-            t = time.perf_counter()
-            step()
-            dt = time.perf_counter() - t
-            cpu = {"value": len(sample_shifts) * m / dt * (sample_budget / budget), "unit": UNIT, "cores": threads,
-                   "kind": kind,
-                   "sample": f"one step: {len(sample_shifts)} shifts x {m} rhs, assemble + LS-SPAI + "
-                             f"{sample_budget} CG iterations (value scaled to the {budget}-iteration budget)",
-                   "seconds": dt}
+            k = 2 if n >= 500000 else (10 if n >= 100000 else 50)
+            smp = CpuSample(kind, hM, hD, hK, B, pattern, budget, k)
+            picks = [all_shifts[0], all_shifts[-1]] if len(all_shifts) > 1 else all_shifts
+            rr = [smp.run(s) for s in picks]
+            per_shift = statistics.mean(r["shift_s"] for r in rr)
+            hc = host_cpu()
+            cpu = {"value": m / per_shift, "unit": UNIT, "cores": 1, "kind": smp.kind,
+                   "sample": smp.describe(m).replace("one shift per step (rotating over the workload's shifts)",
+                                                     f"shifts {picks}"),
+                   "seconds": sum(r["wall_s"] for r in rr), "nproc": hc["nproc"], "cpu_model": hc["model"],
+                   "x_nproc_ideal": m / per_shift * (hc["nproc"] or 1),
+                   "spai_s_per_shift": statistics.mean(r["spai_s"] for r in rr)}
         except Exception as e:  # reported, never silently replaced
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable", "sample": repr(e)}
 
@@ -379,7 +429,8 @@ def run_mgpu(args, rank, world, local_rank):
             "cg_ms": statistics.median(cg_ms), "cg_us_per_iteration": 1e3 * statistics.median(cg_ms) / max(loops, 1),
             "cg_iterations": loops, "breakdowns": recs[-1]["breakdowns"], "cg_kernel": ctx.last_cg_path,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "peak_source": peak_kind, "kernel": "cg_" + ctx.last_cg_path,
+                         "traffic": traffic, "traffic_note": "null: measured per launch by ncu, see profiles/",
+                         "peak_source": peak_kind, "kernel": "cg_" + ctx.last_cg_path,
                          "regime": ("working set on chip (shared memory / L2): latency- and barrier-bound; the HBM "
                                     "fraction is reported for the contract" if args.workload in ("config0", "config1")
                                     else "HBM streaming"),

@@ -848,7 +848,15 @@ int orc_pattern_square(const orc_csr *A, orc_csr *out)
   return ORC_OK;
 }
 
-/* SURVEY.md 8(a') "LS-SPAI oracle definition": J = pattern row j, I = sorted
+/* Column-equilibrated variant (pattern | ORC_LS_COLSCALE): before the QR every column c of S
+ * is divided by d_c = ||S_c|| (in-order dot, sqrt), and the back-substituted solution is divided
+ * by d_c again (m_c = u_c / d_c).  In exact arithmetic this is the same least-squares minimiser
+ * (S D^-1 (D m) = S m); it removes the spurious global rank flush of thin_qr (sigma <= 1e-12
+ * ||S||_F, dense.cpp:162-179), which on the Hermite beam fires once the theta-dof columns
+ * (~h^2 smaller than the w-dof ones) drop below 1e-12 of the Frobenius norm (n >= 2e5 on the
+ * A^2 pattern, n >= 4e5 on A's).  A zero column (d_c == 0) is rank deficiency.
+ *
+ * SURVEY.md 8(a') "LS-SPAI oracle definition": J = pattern row j, I = sorted
  * union of the rows of A(:, J), S = A(I, J), (Q, R) = thin_qr(S),
  * y = Q^T e|_I (e = e_j, or K_old(:, j) for the update), R m = y by
  * back-substitution (acc = y_k; acc -= R_kt m_t for t ascending; m_k = acc / R_kk),
@@ -857,6 +865,9 @@ int orc_pattern_square(const orc_csr *A, orc_csr *out)
 int orc_spai_ls(const orc_csr *A, const orc_csr *K_old, int pattern, orc_csr *P, orc_err *err)
 {
   clear_err(err);
+  /* pattern | ORC_LS_COLSCALE: column-equilibrated variant (see the header comment) */
+  const int colscale = (pattern & ORC_LS_COLSCALE) != 0;
+  pattern &= ~ORC_LS_COLSCALE;
   if (A->nrows != A->ncols || (K_old && (K_old->nrows != A->nrows || K_old->ncols != A->ncols)))
   {
     set_err(err, -1, "spai_ls: operands must be square with equal shape");
@@ -915,6 +926,7 @@ int orc_spai_ls(const orc_csr *A, const orc_csr *K_old, int pattern, orc_csr *P,
       double *e = (double *)calloc((size_t)ni, sizeof(double));
       double *y = (double *)malloc(sizeof(double) * (size_t)nj);
       double *mm = (double *)malloc(sizeof(double) * (size_t)nj);
+      double *dsc = (double *)malloc(sizeof(double) * (size_t)nj);
       for (int64_t c = 0; c < nj; ++c)
       {
         const int64_t k = pat.col_idx[jb + c];
@@ -930,7 +942,23 @@ int orc_spai_ls(const orc_csr *A, const orc_csr *K_old, int pattern, orc_csr *P,
       else if (pos[j] >= 0)
         e[pos[j]] = 1.0;
       int64_t rank = 0;
-      orc_thin_qr(ni, nj, S, 1e-12, Qm, R, &rank);
+      int zero_col = 0;
+      if (colscale)
+      {
+        /* d_c = sqrt(dot(S_c, S_c)) in index order (kernels_scalar.cpp:13-19), S_c /= d_c */
+        for (int64_t c = 0; c < nj; ++c)
+        {
+          const double d = sqrt(dot_s(S + c * ni, S + c * ni, ni));
+          dsc[c] = d;
+          if (d == 0.0)
+            zero_col = 1;
+          else
+            for (int64_t i = 0; i < ni; ++i)
+              S[c * ni + i] = S[c * ni + i] / d;
+        }
+      }
+      if (!zero_col)
+        orc_thin_qr(ni, nj, S, 1e-12, Qm, R, &rank);
       if (rank < nj)
       {
         char msg[256];
@@ -949,6 +977,9 @@ int orc_spai_ls(const orc_csr *A, const orc_csr *K_old, int pattern, orc_csr *P,
             acc -= R[q * nj + k] * mm[q];
           mm[k] = acc / R[k * nj + k];
         }
+        if (colscale)
+          for (int64_t c = 0; c < nj; ++c)
+            mm[c] = mm[c] / dsc[c];
         for (int64_t c = 0; c < nj; ++c)
         {
           tr[t] = pat.col_idx[jb + c];
@@ -962,6 +993,7 @@ int orc_spai_ls(const orc_csr *A, const orc_csr *K_old, int pattern, orc_csr *P,
       free(e);
       free(y);
       free(mm);
+      free(dsc);
     }
     for (int64_t a = 0; a < ni; ++a)
       pos[I[a]] = -1;

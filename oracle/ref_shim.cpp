@@ -448,6 +448,10 @@ int ref_spai_ls(const ref_csr *A_in, const ref_csr *K_old_in, int pattern, ref_c
     {
       throw mor::ArgumentError("spai_ls: operands must be square with equal shape");
     }
+    // pattern | 0x10: column-equilibrated variant (oracle.c orc_spai_ls header): S_c /= ||S_c||
+    // before thin_qr, m_c = u_c / ||S_c|| after the back-substitution
+    const bool colscale = (pattern & 0x10) != 0;
+    pattern &= ~0x10;
     // symbolic pattern rows
     std::vector<std::vector<int32_t>> pat(static_cast<std::size_t>(n));
     for (int64_t i = 0; i < n; ++i)
@@ -529,12 +533,29 @@ int ref_spai_ls(const ref_csr *A_in, const ref_csr *K_old_in, int pattern, ref_c
       {
         e[static_cast<std::size_t>(pos[static_cast<std::size_t>(j)])] = 1.0;
       }
+      const auto &ops = mor::kernels::active();
+      std::vector<double> dsc(static_cast<std::size_t>(nj), 1.0);
+      if (colscale)
+      {
+        for (int64_t c = 0; c < nj; ++c)
+        {
+          const double d = std::sqrt(ops.dot(S.col(c), S.col(c), static_cast<std::size_t>(ni)));
+          if (d == 0.0)
+          {
+            throw mor::NumericalError("spai_ls: rank-deficient least-squares problem in column " + std::to_string(j));
+          }
+          dsc[static_cast<std::size_t>(c)] = d;
+          for (int64_t i = 0; i < ni; ++i)
+          {
+            S.at(i, c) = S.at(i, c) / d;
+          }
+        }
+      }
       const mor::QrResult qr = mor::thin_qr(S);
       if (qr.rank < nj)
       {
         throw mor::NumericalError("spai_ls: rank-deficient least-squares problem in column " + std::to_string(j));
       }
-      const auto &ops = mor::kernels::active();
       std::vector<double> y(static_cast<std::size_t>(nj)), m(static_cast<std::size_t>(nj));
       for (int64_t c = 0; c < nj; ++c)
       {
@@ -548,6 +569,13 @@ int ref_spai_ls(const ref_csr *A_in, const ref_csr *K_old_in, int pattern, ref_c
           acc -= qr.R.at(k, q) * m[static_cast<std::size_t>(q)];
         }
         m[static_cast<std::size_t>(k)] = acc / qr.R.at(k, k);
+      }
+      if (colscale)
+      {
+        for (int64_t c = 0; c < nj; ++c)
+        {
+          m[static_cast<std::size_t>(c)] = m[static_cast<std::size_t>(c)] / dsc[static_cast<std::size_t>(c)];
+        }
       }
       for (int64_t c = 0; c < nj; ++c)
       {

@@ -12,6 +12,6 @@ from .mgpu import (  # noqa: F401
     default_context, lib, model_chain, model_hermite, model_hermite_device, pcg_solve, shifted_operator, shifted_operators, sp_add_scaled,
     spai_build, spai_ls, spai_ls_batched, spai_update, spgemm, trace, trace_inner, transpose,
     shifted_solve_raw, shifted_solve_device,
-    FROZEN, SEQUENTIAL, PATTERN_A, PATTERN_A2,
+    FROZEN, SEQUENTIAL, PATTERN_A, PATTERN_A2, LS_COLSCALE,
 )
 from .backend import CudaCgBackend  # noqa: F401

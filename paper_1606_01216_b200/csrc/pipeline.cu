@@ -18,7 +18,8 @@ int mgpu_shifted_solve(mgpu_ctx *ctx, const mgpu_csr *M, const mgpu_csr *D, cons
   if (ctx == nullptr)
     return MGPU_ERR_ARG;
   if (M == nullptr || D == nullptr || K == nullptr || shifts == nullptr || l < 1 ||
-      (pattern != -1 && pattern != MGPU_PATTERN_A && pattern != MGPU_PATTERN_A2))
+      (pattern != -1 && (pattern & ~MGPU_LS_COLSCALE) != MGPU_PATTERN_A &&
+       (pattern & ~MGPU_LS_COLSCALE) != MGPU_PATTERN_A2))
     return guard(ctx, [&] { MG_ARG(false, "shifted_solve: bad argument"); });
   cudaStream_t s = ctx->stream;
   cudaEvent_t *ev = ctx->phase_ev; // created once per context

@@ -116,6 +116,7 @@ __global__ void square_fill(int64_t n, DCsr A, const int64_t *rp, int32_t *ci)
 template <int G, int NI>
 struct LsGroupSmem
 {
+  double dsc[G]; // column scales ||S_c|| (column-equilibrated variant)
   double W[G * (NI + 1)]; // S / Householder vectors, column-major, ld = NI + 1 (odd: bank spread)
   double Q[G * (NI + 1)]; // Q; before the QR: staged values of A^T row J_c (lane c)
   int32_t rows[G * NI];    // staged column indices of A^T row J_c (lane c)
@@ -151,7 +152,7 @@ __device__ __forceinline__ void report(unsigned long long *err, int64_t j, int s
 // Batched over l operators sharing one pattern: column g = p * n + j reads
 // A_p through At (shared structure, values at At.v + p * at_stride), K_old_p
 // likewise, and writes P_p^T values at out_vals + p * out_stride.
-template <int G, int NI>
+template <int G, int NI, bool CS>
 __global__ void ls_columns(int64_t n, int l, DCsr pat, DCsr At, int64_t at_stride, DCsr Kot, int64_t ko_stride,
                            bool update, double *__restrict__ out_base, int64_t out_stride,
                            unsigned long long *__restrict__ err, int *__restrict__ overflow)
@@ -296,6 +297,28 @@ __global__ void ls_columns(int64_t n, int l, DCsr pat, DCsr At, int64_t at_strid
     }
   }
   __syncwarp(gmask);
+  if (CS) // column equilibration: d_c = ||S_c|| (in-order dot), S_c /= d_c (oracle.c orc_spai_ls)
+  {
+    if (c < nj)
+    {
+      double *col = sm.W + c * LD;
+      const double d = sqrt(dot_serial(col, col, ni));
+      sm.dsc[c] = d;
+      if (d != 0.0)
+        for (int i = 0; i < ni; ++i)
+          col[i] = col[i] / d;
+    }
+    __syncwarp(gmask);
+    bool zero = false;
+    for (int q = 0; q < nj; ++q)
+      zero |= sm.dsc[q] == 0.0;
+    if (zero)
+    {
+      if (c == 0)
+        report(err, g, MGPU_ERR_NUMERICAL);
+      return;
+    }
+  }
   // ---- thin_qr (dense.cpp:153-246)
   double tol = 0.0;
   if (c == 0)
@@ -412,7 +435,7 @@ __global__ void ls_columns(int64_t n, int l, DCsr pat, DCsr At, int64_t at_strid
   }
   __syncwarp(gmask);
   if (c < nj)
-    out_vals[jb + c] = sm.m[c];
+    out_vals[jb + c] = CS ? sm.m[c] / sm.dsc[c] : sm.m[c];
 }
 
 // Longest row of a CSR structure (warp max, one atomic per warp).
@@ -439,7 +462,7 @@ __global__ void ls_max_row(int64_t nrows, const int64_t *__restrict__ rp, int *o
 // envelope, so every index is a compile-time constant): only W, the reflector scalars and I
 // take shared memory, which sets the occupancy.  Envelope: |J| <= NJ, |I| <= NI; a larger column sets `overflow` and
 // the host reruns the batch on the group kernels.
-template <int NJ, int NI>
+template <int NJ, int NI, bool CS = false>
 struct LaneLayout
 {
   static constexpr int kW = 0;                // W[c * NI + i]: S, then Householder vectors / R
@@ -447,21 +470,22 @@ struct LaneLayout
   static constexpr int kTau = kDiag + NJ;     // reflector scales, then |R_cc|
   static constexpr int kM = kTau + NJ;        // y, then the solution
   static constexpr int kI = kM + NJ;          // I (int32, NI of them = NI / 2 words)
-  static constexpr int kWords0 = kI + (NI + 1) / 2;
+  static constexpr int kDsc = kI + (NI + 1) / 2; // column scales (CS only)
+  static constexpr int kWords0 = kDsc + (CS ? NJ : 0);
   static constexpr int kWords = kWords0 | 1; // odd stride: conflict-free same-offset accesses
 };
 
-template <int NJ, int NI>
+template <int NJ, int NI, bool CS>
 __global__ void __launch_bounds__(64) ls_columns_lane(int64_t n, int l, DCsr pat, DCsr At, int64_t at_stride,
                                                        DCsr Kot, int64_t ko_stride, bool update,
                                                        double *__restrict__ out_base, int64_t out_stride,
                                                        unsigned long long *__restrict__ err, int *__restrict__ overflow)
 {
-  using L = LaneLayout<NJ, NI>;
+  using L = LaneLayout<NJ, NI, CS>;
   extern __shared__ __align__(16) double lane_raw[];
   double *base = lane_raw + static_cast<size_t>(threadIdx.x) * L::kWords;
   double *W = base + L::kW;
-  double *diag = base + L::kDiag, *tau = base + L::kTau, *mv = base + L::kM;
+  double *diag = base + L::kDiag, *tau = base + L::kTau, *mv = base + L::kM, *dsc = base + L::kDsc;
   int32_t *I = reinterpret_cast<int32_t *>(base + L::kI);
   const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (g >= static_cast<int64_t>(l) * n)
@@ -561,6 +585,22 @@ __global__ void __launch_bounds__(64) ls_columns_lane(int64_t n, int l, DCsr pat
       if (i < ni && I[i] == j)
         e[i] = 1.0;
   }
+  if (CS) // column equilibration: d_c = ||S_c|| (in-order dot), S_c /= d_c (oracle.c orc_spai_ls)
+  {
+    for (int c = 0; c < nj; ++c)
+    {
+      double *col = W + c * NI;
+      const double d = sqrt(dot_serial(col, col, ni));
+      if (d == 0.0)
+      {
+        report(err, g, MGPU_ERR_NUMERICAL);
+        return;
+      }
+      dsc[c] = d;
+      for (int i = 0; i < ni; ++i)
+        col[i] = col[i] / d;
+    }
+  }
   // ---- thin_qr (dense.cpp:153-246): frob_norm tolerance in column-major order
   double acc = 0.0;
   for (int c = 0; c < nj; ++c)
@@ -657,39 +697,64 @@ __global__ void __launch_bounds__(64) ls_columns_lane(int64_t n, int l, DCsr pat
     mv[k] = a / tau[k];
   }
   for (int c = 0; c < nj; ++c)
-    out_vals[jb + c] = mv[c];
+    out_vals[jb + c] = CS ? mv[c] / dsc[c] : mv[c];
 }
 
 // TPB: threads per block (32 packs the per-lane scratch more tightly for small envelopes)
-template <int NJ, int NI, int TPB = 64>
-void launch_ls_lane(mgpu_ctx *ctx, int64_t n, int l, DCsr pat, DCsr At, int64_t at_stride, DCsr Kot, int64_t ko_stride,
-                    bool update, double *out, int64_t out_stride, unsigned long long *err, int *ovf)
+template <int NJ, int NI, bool CS, int TPB>
+void launch_ls_lane_cs(mgpu_ctx *ctx, int64_t n, int l, DCsr pat, DCsr At, int64_t at_stride, DCsr Kot,
+                       int64_t ko_stride, bool update, double *out, int64_t out_stride, unsigned long long *err,
+                       int *ovf)
 {
   constexpr int kThreadsPerBlock = TPB;
-  constexpr size_t smem = sizeof(double) * LaneLayout<NJ, NI>::kWords * kThreadsPerBlock;
+  constexpr size_t smem = sizeof(double) * LaneLayout<NJ, NI, CS>::kWords * kThreadsPerBlock;
   static_assert(smem <= 200 * 1024, "LS lane shared memory");
-  MG_CUDA(cudaFuncSetAttribute(ls_columns_lane<NJ, NI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  MG_CUDA(cudaFuncSetAttribute(ls_columns_lane<NJ, NI, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(smem)));
   const int64_t cols = static_cast<int64_t>(l) * n;
   const unsigned grid = static_cast<unsigned>((cols + kThreadsPerBlock - 1) / kThreadsPerBlock);
-  ls_columns_lane<NJ, NI><<<grid, kThreadsPerBlock, smem, ctx->stream>>>(n, l, pat, At, at_stride, Kot, ko_stride,
-                                                                         update, out, out_stride, err, ovf);
+  ls_columns_lane<NJ, NI, CS><<<grid, kThreadsPerBlock, smem, ctx->stream>>>(n, l, pat, At, at_stride, Kot, ko_stride,
+                                                                             update, out, out_stride, err, ovf);
   check_launch(ctx, "ls_columns_lane");
 }
 
-template <int G, int NI, int WARPS>
-void launch_ls(mgpu_ctx *ctx, int64_t n, int l, DCsr pat, DCsr At, int64_t at_stride, DCsr Kot, int64_t ko_stride,
-               bool update, double *out, int64_t out_stride, unsigned long long *err, int *ovf)
+template <int NJ, int NI, int TPB = 64>
+void launch_ls_lane(mgpu_ctx *ctx, bool cs, int64_t n, int l, DCsr pat, DCsr At, int64_t at_stride, DCsr Kot,
+                    int64_t ko_stride, bool update, double *out, int64_t out_stride, unsigned long long *err, int *ovf)
+{
+  if (cs)
+    launch_ls_lane_cs<NJ, NI, true, TPB>(ctx, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, err,
+                                         ovf);
+  else
+    launch_ls_lane_cs<NJ, NI, false, TPB>(ctx, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, err,
+                                          ovf);
+}
+
+template <int G, int NI, int WARPS, bool CS>
+void launch_ls_cs(mgpu_ctx *ctx, int64_t n, int l, DCsr pat, DCsr At, int64_t at_stride, DCsr Kot, int64_t ko_stride,
+                  bool update, double *out, int64_t out_stride, unsigned long long *err, int *ovf)
 {
   constexpr int per_block = WARPS * (32 / G);
   constexpr size_t smem = sizeof(LsGroupSmem<G, NI>) * per_block;
   static_assert(smem <= 100 * 1024, "LS group shared memory");
-  MG_CUDA(cudaFuncSetAttribute(ls_columns<G, NI>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  MG_CUDA(cudaFuncSetAttribute(ls_columns<G, NI, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem)));
   const int64_t cols = static_cast<int64_t>(l) * n;
   const unsigned grid = static_cast<unsigned>((cols + per_block - 1) / per_block);
-  ls_columns<G, NI><<<grid, WARPS * 32, smem, ctx->stream>>>(n, l, pat, At, at_stride, Kot, ko_stride, update, out,
-                                                             out_stride, err, ovf);
+  ls_columns<G, NI, CS><<<grid, WARPS * 32, smem, ctx->stream>>>(n, l, pat, At, at_stride, Kot, ko_stride, update,
+                                                                 out, out_stride, err, ovf);
   check_launch(ctx, "ls_columns");
+}
+
+template <int G, int NI, int WARPS>
+void launch_ls(mgpu_ctx *ctx, bool cs, int64_t n, int l, DCsr pat, DCsr At, int64_t at_stride, DCsr Kot,
+               int64_t ko_stride, bool update, double *out, int64_t out_stride, unsigned long long *err, int *ovf)
+{
+  if (cs)
+    launch_ls_cs<G, NI, WARPS, true>(ctx, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, err, ovf);
+  else
+    launch_ls_cs<G, NI, WARPS, false>(ctx, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, err,
+                                      ovf);
 }
 
 // Runs the LS columns with the smallest lane-group envelope that holds every
@@ -697,7 +762,7 @@ void launch_ls(mgpu_ctx *ctx, int64_t n, int l, DCsr pat, DCsr At, int64_t at_st
 // sequential column loop would.
 // abort_dev (optional): a device flag read with the status; nonzero means the batch's shared-
 // pattern assumption was wrong, and run_ls returns false without interpreting the results.
-bool run_ls(mgpu_ctx *ctx, int64_t n, int l, int maxrow, DCsr pat, DCsr At, int64_t at_stride, DCsr Kot,
+bool run_ls(mgpu_ctx *ctx, bool cs, int64_t n, int l, int maxrow, DCsr pat, DCsr At, int64_t at_stride, DCsr Kot,
             int64_t ko_stride, bool update, double *out, int64_t out_stride, const int *extra_dev = nullptr,
             int *extra_host = nullptr, int64_t pat_bw = -1, const int *abort_dev = nullptr,
             const std::function<void()> &after_launch = {})
@@ -721,18 +786,18 @@ bool run_ls(mgpu_ctx *ctx, int64_t n, int l, int maxrow, DCsr pat, DCsr At, int6
     MG_CUDA(cudaMemsetAsync(ovf.ptr, 0, sizeof(int), ctx->stream));
     auto *ev = err.as<unsigned long long>();
     if (cfg == -3)
-      launch_ls_lane<5, 13, 32>(ctx, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev,
+      launch_ls_lane<5, 13, 32>(ctx, cs, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev,
                                 ovf.as<int>());
     else if (cfg == -2)
-      launch_ls_lane<6, 14>(ctx, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev, ovf.as<int>());
+      launch_ls_lane<6, 14>(ctx, cs, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev, ovf.as<int>());
     else if (cfg == -1)
-      launch_ls_lane<8, 16>(ctx, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev, ovf.as<int>());
+      launch_ls_lane<8, 16>(ctx, cs, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev, ovf.as<int>());
     else if (cfg == 0)
-      launch_ls<8, 16, 4>(ctx, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev, ovf.as<int>());
+      launch_ls<8, 16, 4>(ctx, cs, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev, ovf.as<int>());
     else if (cfg == 1)
-      launch_ls<16, 32, 2>(ctx, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev, ovf.as<int>());
+      launch_ls<16, 32, 2>(ctx, cs, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev, ovf.as<int>());
     else
-      launch_ls<32, 64, 1>(ctx, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev, ovf.as<int>());
+      launch_ls<32, 64, 1>(ctx, cs, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev, ovf.as<int>());
     if (after_launch) // caller's dependent work, queued behind the LS kernel before the read-back
       after_launch();
     // one synchronisation returns the error key, the overflow flag and the caller's extra value
@@ -879,6 +944,8 @@ mgpu_csr *pattern_square(mgpu_ctx *ctx, const mgpu_csr *A)
 // P (or Q) for one operator.  `pat` may be A itself (pattern 0).
 mgpu_csr *spai_ls_one(mgpu_ctx *ctx, const mgpu_csr *A, const mgpu_csr *K_old, int pattern)
 {
+  const bool cs = (pattern & MGPU_LS_COLSCALE) != 0;
+  pattern &= ~MGPU_LS_COLSCALE;
   MG_ARG(A->nrows == A->ncols, "spai_ls: operands must be square with equal shape");
   MG_ARG(!K_old || (K_old->nrows == A->nrows && K_old->ncols == A->ncols),
          "spai_ls: operands must be square with equal shape");
@@ -902,7 +969,7 @@ mgpu_csr *spai_ls_one(mgpu_ctx *ctx, const mgpu_csr *A, const mgpu_csr *K_old, i
     const int maxrow = static_cast<int>(csr_max_row(ctx, const_cast<mgpu_csr *>(pat)));
     const DCsr kv = Kot ? Kot->view() : DCsr{nullptr, nullptr, nullptr};
     const int64_t bwA = csr_bandwidth(ctx, const_cast<mgpu_csr *>(A));
-    run_ls(ctx, n, 1, maxrow, pat->view(), At->view(), 0, kv, 0, Kot != nullptr, PT->values, 0, nullptr, nullptr,
+    run_ls(ctx, cs, n, 1, maxrow, pat->view(), At->view(), 0, kv, 0, Kot != nullptr, PT->values, 0, nullptr, nullptr,
            sq ? 2 * bwA : bwA);
   }
   catch (...)
@@ -935,6 +1002,8 @@ mgpu_csr *spai_ls_one(mgpu_ctx *ctx, const mgpu_csr *A, const mgpu_csr *K_old, i
 std::vector<mgpu_csr *> spai_ls_shared(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, const mgpu_csr *const *K_old,
                                        int pattern, const int *diff_dev = nullptr)
 {
+  const bool cs = (pattern & MGPU_LS_COLSCALE) != 0;
+  pattern &= ~MGPU_LS_COLSCALE;
   const mgpu_csr *A0 = A[0];
   const int64_t n = A0->nrows, nnzA = A0->nnz;
   cudaStream_t s = ctx->stream;
@@ -1033,7 +1102,7 @@ std::vector<mgpu_csr *> spai_ls_shared(mgpu_ctx *ctx, int l, const mgpu_csr *con
       make_factors(At0, At0->maxrow); // maxrow set below once fetched
       gather_early = [&]() { gather_batched(ctx, l, nnzJ, perm_t.as<int64_t>(), gsrc.data(), gdst.data()); };
     }
-    if (!run_ls(ctx, n, l, maxrow, pat->view(), atv, nnzA, kov, nnzA, K_old != nullptr, pt_vals.as<double>(), nnzJ,
+    if (!run_ls(ctx, cs, n, l, maxrow, pat->view(), atv, nnzA, kov, nnzA, K_old != nullptr, pt_vals.as<double>(), nnzJ,
                 fetch ? mx.as<int>() : nullptr, fetch ? &at_maxrow : nullptr, sq ? 2 * bwA : bwA, diff_dev,
                 gather_early))
     {
@@ -1102,7 +1171,8 @@ int mgpu_spai_ls_batched(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, const m
       MG_ARG(A[i] && A[i]->nrows == A[i]->ncols && (!K_old || (K_old[i] && K_old[i]->nrows == A[i]->nrows &&
                                                                    K_old[i]->ncols == A[i]->ncols)),
              "spai_ls: operands must be square with equal shape");
-    MG_ARG(pattern == MGPU_PATTERN_A || pattern == MGPU_PATTERN_A2, "spai_ls: unknown pattern");
+    MG_ARG((pattern & ~MGPU_LS_COLSCALE) == MGPU_PATTERN_A || (pattern & ~MGPU_LS_COLSCALE) == MGPU_PATTERN_A2,
+           "spai_ls: unknown pattern");
     // shared-pattern path, speculatively: the structure comparison is queued, not awaited; its
     // flag comes back with the LS status, and on a mismatch the batch reruns per operator
     DBuf diff(sizeof(int), ctx->stream);

@@ -24,6 +24,7 @@ MGPU_ERR_NUMERICAL, MGPU_ERR_UNSUPPORTED, MGPU_ERR_CUDA, MGPU_ERR_NCCL = 4, 5, 6
 MGPU_HOST, MGPU_DEVICE = 0, 1
 SEQUENTIAL, FROZEN = 0, 1
 PATTERN_A, PATTERN_A2 = 0, 1
+LS_COLSCALE = 0x10  # flag: column-equilibrated LS-SPAI (mgpu.h MGPU_LS_COLSCALE)
 
 # Symbols include/mgpu.h declares; tests check the library exports all of them.
 EXPORTED = [

@@ -98,7 +98,8 @@ def main():
     H1 = ref.shifted_operator(Mh, Dh, Kh, 100.0)
     H2 = ref.shifted_operator(Mh, Dh, Kh, 150.0)
     out.update(csr("herm_A1", H1) | csr("herm_A2", H2))
-    for pat in (0, 1):
+    # pattern | 0x10: the column-equilibrated LS variant (ref_shim.cpp ref_spai_ls, reference thin_qr)
+    for pat in (0, 1, 0x10, 0x11):
         out.update(csr(f"herm_LS{pat}", ref.spai_ls(H1, None, pat)))
         out.update(csr(f"herm_LSU{pat}", ref.spai_ls(H2, H1, pat)))
     Pl = ref.spai_ls(H1, None, 0)

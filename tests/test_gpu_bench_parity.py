@@ -169,3 +169,35 @@ def test_shifted_solve_raises_the_spai_error(mg):
         mg.spai_ls_batched(ops, None, mg.PATTERN_A, ctx=ctx)
     it, cv, st, bd, ph = mg.shifted_solve_device(M, D, K, [100.0], -1, B_dev, X_dev[:1], maxit=5, ctx=ctx)
     assert int(it[0]) == 5
+
+
+@pytest.mark.parametrize("ne,m,pattern,nshift,k", [(500000, 4, 0x11, 2, 30), (5000000, 4, 0x10, 1, 8)])
+def test_full_size_preconditioned_matches_oracle(mg, oracle, ne, m, pattern, nshift, k):
+    """BASELINE configs[3] (n = 1e6, m = 4, column-equilibrated LS-SPAI on the A^2 pattern) and
+    configs[4] (n = 1e7, m = 4, A pattern): the bench's one-call device path (assembly, batched
+    LS-SPAI, streaming CG) against the oracle's separate calls after k iterations: factors
+    bitwise, same iteration counts, iterates within 1e-8."""
+    import torch
+    M, D, K = oracle.hermite_generate(ne)
+    n = M.nrows
+    B = np.zeros((n, m))
+    for c in range(m):
+        B[2 * ((c + 1) * ne // m) - 2, c] = 1.0
+    shifts = [10.0 ** (1 + 3 * i / 15) for i in range(16)][:: 16 // nshift][:nshift]
+    ctx = mg.default_context()
+    dev = torch.device("cuda", 0)
+    B_dev = torch.tensor(B.T.copy(), dtype=torch.float64, device=dev)
+    X_dev = torch.empty((nshift, m, n), dtype=torch.float64, device=dev)
+    it, cv, st, bd, ph = mg.shifted_solve_device(M, D, K, shifts, pattern, B_dev, X_dev, rtol=1e-10, maxit=k,
+                                                 ctx=ctx)
+    assert ctx.last_cg_path == "stream"
+    X = X_dev.cpu().numpy()
+    dops = mg.shifted_operators(M, D, K, shifts, ctx=ctx)
+    dfac = mg.spai_ls_batched(dops, None, pattern, ctx=ctx)
+    for p, s in enumerate(shifts):
+        A = oracle.shifted_operator(M, D, K, s)
+        P = oracle.spai_ls(A, None, pattern)
+        np.testing.assert_array_equal(dfac[p].matrix.download().values, P.values)
+        want = oracle.block_solve(A, [P], B, rtol=1e-10, maxit=k)
+        np.testing.assert_array_equal(it[p * m:(p + 1) * m], want["iterations"])
+        assert rel(X[p].T, want["X"]) < 1e-8

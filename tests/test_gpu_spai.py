@@ -174,6 +174,43 @@ def test_ls_update_hermite(mg, oracle, pattern):
     _csr_equal(got, want)
 
 
+@pytest.mark.parametrize("pattern", [0x10, 0x11])
+@pytest.mark.parametrize("s", [10.0, 1e4])
+def test_ls_colscale_build_and_update_hermite(mg, oracle, pattern, s):
+    """Column-equilibrated LS (pattern | MGPU_LS_COLSCALE): lane kernel (A pattern) and lane-group
+    kernel (A^2 pattern), build and update, bitwise equal to the oracle restatement."""
+    M, D, K = oracle.hermite_generate(1000)
+    A = oracle.shifted_operator(M, D, K, s)
+    _csr_equal(mg.spai_ls(A, None, pattern).matrix.download(), oracle.spai_ls(A, None, pattern))
+    A2 = oracle.shifted_operator(M, D, K, 1.5 * s)
+    _csr_equal(mg.spai_ls(A2, A, pattern).matrix.download(), oracle.spai_ls(A2, A, pattern))
+
+
+@pytest.mark.parametrize("pattern", [0x10, 0x11])
+def test_ls_colscale_full_size_batched(mg, oracle, pattern):
+    """BASELINE configs[3] size (n = 1e6), where the unscaled LS rank-flushes: the batched
+    column-equilibrated factors of 2 shifts are bitwise equal to the oracle's, every column."""
+    M, D, K = oracle.hermite_generate(500000)
+    shifts = [10.0, 1e4]
+    ops = mg.shifted_operators(M, D, K, shifts)
+    facs = mg.spai_ls_batched(ops, None, pattern)
+    for s, f in zip(shifts, facs):
+        _csr_equal(f.matrix.download(), oracle.spai_ls(oracle.shifted_operator(M, D, K, s), None, pattern))
+
+
+def test_ls_colscale_zero_column(mg, oracle):
+    """A zero column of S is rank deficiency in the equilibrated variant too (same column)."""
+    from oracle import Csr, OracleError
+    a = np.array([[1.0, 0.0, 0.0], [0.0, 0.0, 0.0], [0.0, 0.0, 3.0]])
+    a[1, 1] = 1e-320  # stored, but squares to zero: ||S_c|| == 0
+    A = Csr.from_dense(a)
+    with pytest.raises(OracleError) as eo:
+        oracle.spai_ls(A, None, 0x10)
+    with pytest.raises(mg.NumericalError) as eg:
+        mg.spai_ls(A, None, 0x10)
+    assert eg.value.index == eo.value.index
+
+
 def test_ls_chain_model_and_dense(mg, oracle):
     from oracle import Csr
     M, D, K = oracle.chain_generate(3000, consistent=True, stiffness_scale=1.0)

@@ -76,7 +76,7 @@ def test_hermite_generator_matches_reference_assembly(oracle):
     assert K.nnz == 5 * 200 - 6  # interior (w, theta) couplings cancel exactly
 
 
-@pytest.mark.parametrize("pat", [0, 1])
+@pytest.mark.parametrize("pat", [0, 1, 0x10, 0x11])
 def test_ls_spai_against_reference_primitives(oracle, pat):
     A1, A2 = _csr("herm_A1"), _csr("herm_A2")
     _same(oracle.spai_ls(A1, None, pat), f"herm_LS{pat}")
@@ -156,3 +156,21 @@ def test_live_reference_matches_restatement(oracle, ref):
         np.testing.assert_array_equal(P.values, Po.values)
         b = np.ones(500)
         np.testing.assert_array_equal(ref.pcg_solve(A, [P], b)["solution"], oracle.pcg_solve(A, [Po], b)["solution"])
+
+
+def test_ls_colscale_avoids_the_global_rank_flush(oracle):
+    """At n = 4e5 the reference thin_qr's global flush (sigma <= 1e-12 ||S||_F, dense.cpp:162-179)
+    declares the A^2-pattern problems rank-deficient; the column-equilibrated variant (same
+    least-squares minimiser) solves them.  Small n: both variants agree to rounding."""
+    from oracle import OracleError
+    M, D, K = oracle.hermite_generate(200000)
+    A = oracle.shifted_operator(M, D, K, 100.0)
+    with pytest.raises(OracleError):
+        oracle.spai_ls(A, None, 1)
+    P = oracle.spai_ls(A, None, 0x11)
+    assert P.nnz == 10 * A.nrows - 24 and np.all(np.isfinite(P.values))
+    M, D, K = oracle.hermite_generate(200)
+    A = oracle.shifted_operator(M, D, K, 100.0)
+    P0, P1 = oracle.spai_ls(A, None, 1), oracle.spai_ls(A, None, 0x11)
+    assert np.array_equal(P0.col_idx, P1.col_idx)
+    assert np.max(np.abs(P0.values - P1.values)) <= 1e-10 * np.max(np.abs(P0.values))
