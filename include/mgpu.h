@@ -93,6 +93,27 @@ int mgpu_last_cg_timing(const mgpu_ctx *ctx, double *ms, int64_t *iterations);
 int mgpu_ctx_set_cg_path(mgpu_ctx *ctx, int path);
 int mgpu_last_cg_path(const mgpu_ctx *ctx);
 
+/* Per-context tuning / diagnostic options (no environment variables are read by the library).
+ * Defaults are the measured best choices; the others exist for the A/B experiments in DESIGN.md. */
+typedef enum mgpu_option
+{
+  MGPU_OPT_STREAM_FOLD = 0,     /* cg_stream: x~ update deferred into the next phase A (default 1) */
+  MGPU_OPT_STREAM_SERIAL = 1,   /* cg_stream: point-serial schedule with the L2 hand-off (default 0) */
+  MGPU_OPT_STREAM_CHUNK = 2,    /* cg_stream: forced chunk rows (0 = planner, default) */
+  MGPU_OPT_STREAM_RING = 3,     /* cg_stream: forced ring depth with MGPU_OPT_STREAM_CHUNK (2..4) */
+  MGPU_OPT_STREAM_SAME_CHB = 4, /* cg_stream: phase B on phase A's chunk height (default 0) */
+  MGPU_OPT_CLUSTER_CS = 5,      /* cg_cluster_v2: forced cluster size (0 = planner, default) */
+  MGPU_OPT_CLUSTER_ASYNC = 6,   /* cg_cluster_v2: st.async + mbarrier exchange (default 1; 0 = cluster barriers) */
+  MGPU_OPT_PROFILE_PHASES = 7,  /* clock64 per-phase totals of the CG kernels (default 0; read with mgpu_phase_profile) */
+  MGPU_OPT_QR_UNBLOCKED = 8,    /* thin_qr: column-at-a-time schedule instead of compact WY (default 0) */
+  MGPU_OPT_LS_GROUP = 9,        /* LS-SPAI: skip the lane-per-column kernels (default 0) */
+  MGPU_OPT_COUNT = 10,
+} mgpu_option;
+int mgpu_ctx_set_option(mgpu_ctx *ctx, int option, int64_t value);
+int mgpu_ctx_get_option(const mgpu_ctx *ctx, int option, int64_t *value);
+/* Copies the 16 clock64 phase totals (MGPU_OPT_PROFILE_PHASES) and resets them. */
+int mgpu_phase_profile(mgpu_ctx *ctx, long long *out16);
+
 /* ------------------------------------------------------------------ CSR I/O */
 
 /* Replaces constructing a mor::SparseMatrix (sparse.hpp:16-46).  The host

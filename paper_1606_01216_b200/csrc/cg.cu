@@ -2666,7 +2666,8 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
     hal[st] = (hal[st + 1] + (halo[st] - halo[st + 1]) + 1) & ~1;
   const int H0 = hal[0];
   (void)hmax;
-  if (H0 > kPadR || l > kMaxPoints || static_cast<int64_t>(l) * m > kMaxSys || l > ctx->num_sms * kMaxSeg)
+  if (H0 >= kPadR || // even_up(c1 - c0 + 2 H0) may reach one row past the kPadR padding when H0 == kPadR
+       l > kMaxPoints || static_cast<int64_t>(l) * m > kMaxSys || l > ctx->num_sms * kMaxSeg)
     return false;
   // ---- padded ELL operators
   auto ell_of = [&](const mgpu_csr *M, std::vector<DBuf> &keep) {
@@ -2720,10 +2721,8 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
   // fewer).  Measured on B200 once the kernel dropped to 107 registers: configs[3] (m = 4, P = I)
   // 1029 -> 1005 us/iter, configs[4] share 5025 -> 4891, configs[2] shape (m = 1, one factor)
   // 36.9 -> 36.1; earlier (122 registers) phase A was latency-bound and m = 4 / chains lost.
-  // MGPU_STREAM_FOLD=0/1 overrides (diagnostics).
-  bool fold = true;
-  if (const char *f = std::getenv("MGPU_STREAM_FOLD"))
-    fold = f[0] == '1';
+  // MGPU_OPT_STREAM_FOLD = 0 overrides (diagnostics).
+  const bool fold = ctx->opt[MGPU_OPT_STREAM_FOLD] != 0;
   // ---- shared-memory plan: the largest chunk height whose double buffer fits
   StreamParams P{};
   size_t dyn = 0;
@@ -2749,11 +2748,10 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
   }
   cands.push_back({128, 3});
   cands.push_back({128, 2});
-  if (const char *f = std::getenv("MGPU_STREAM_CFG"))
+  if (ctx->opt[MGPU_OPT_STREAM_CHUNK] > 0) // forced plan (diagnostics)
   {
-    long fr = 0, fd = 0;
-    if (std::sscanf(f, "%ld,%ld", &fr, &fd) == 2 && fr > 0 && fd >= 2 && fd <= kStreamNB)
-      cands.insert(cands.begin(), {static_cast<int64_t>(fr), static_cast<int>(fd)});
+    const int fd = ctx->opt[MGPU_OPT_STREAM_RING] ? static_cast<int>(ctx->opt[MGPU_OPT_STREAM_RING]) : 2;
+    cands.insert(cands.begin(), {ctx->opt[MGPU_OPT_STREAM_CHUNK], fd});
   }
   for (const auto &cand : cands)
   {
@@ -2795,13 +2793,14 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
   }
   if (CH == 0)
     return false;
-  if (std::getenv("MGPU_HOST_TRACE"))
+#ifdef MGPU_HOST_TRACE
   {
     char msg[128];
     std::snprintf(msg, sizeof msg, "cg_stream plan: %lld-row chunks, %d-deep ring, %zu B per slot",
                   static_cast<long long>(CH), P.nb, P.buf_bytes);
     host_mark(msg);
   }
+#endif
   // ---- vectors (padded) and the per-point block plan
   const int64_t ldv = (n + 2 * kPadR) * m;
   const size_t vb = sizeof(double) * static_cast<size_t>(l) * ldv;
@@ -2818,10 +2817,7 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
   // 16 points): DRAM traffic 6.15 -> 4.70 GB per batched iteration, but 1072 -> 1415 us per
   // iteration -- two grid barriers, two block reductions, two flushes and two pipeline fills
   // per point (~10 us per pass, 32 passes) cost more than the bytes saved.  Off by default.
-  bool serial = false;
-  if (const char *f = std::getenv("MGPU_STREAM_SERIAL"))
-    serial = f[0] == '1';
-  serial = serial && l <= kTabSlots;
+  const bool serial = ctx->opt[MGPU_OPT_STREAM_SERIAL] != 0 && l <= kTabSlots;
   std::vector<Seg> hseg(static_cast<size_t>(G) * kMaxSeg, Seg{-1, 0, 0, 0});
   std::vector<int2> hpb(static_cast<size_t>(l));
   if (serial)
@@ -2915,7 +2911,7 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
     const int nvec = fold ? 2 : 4;
     int64_t chb = static_cast<int64_t>(P.buf_bytes / (nvec * sizeof(double) * static_cast<size_t>(m))) & ~63ll;
     chb = std::min<int64_t>(std::max<int64_t>(chb, CH), 8192);
-    if (std::getenv("MGPU_STREAM_SAME_CHB")) // diagnostics: phase B on the phase A chunk height
+    if (ctx->opt[MGPU_OPT_STREAM_SAME_CHB]) // diagnostics: phase B on the phase A chunk height
       chb = CH;
     P.ch_b = static_cast<int>(chb);
     const size_t vb = static_cast<size_t>(chb) * m * sizeof(double); // multiple of 512 B

@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -1351,10 +1352,10 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
 // cudaOccupancyMaxActiveClusters costs tens of microseconds and v2_solve asks it for every
 // cluster size on every solve: the answer depends only on (device, kernel, cluster size,
 // dynamic shared memory), so it is memoised.
-int cached_active_clusters(int device, int kernel_id, int cs, size_t dyn, int (*query)(int, size_t))
+int cached_active_clusters(int device, uintptr_t kernel_id, int cs, size_t dyn, const std::function<int(int, size_t)> &query)
 {
   static std::mutex mu;
-  static std::map<std::tuple<int, int, int, size_t>, int> cache;
+  static std::map<std::tuple<int, uintptr_t, int, size_t>, int> cache;
   const auto key = std::make_tuple(device, kernel_id, cs, dyn);
   {
     std::lock_guard<std::mutex> g(mu);
@@ -1368,10 +1369,33 @@ int cached_active_clusters(int device, int kernel_id, int cs, size_t dyn, int (*
   return v;
 }
 
-template <int RPT>
-int v2_active_clusters_query(int cs, size_t dyn)
+using V2Kernel = void (*)(V2Params);
+
+template <int RPT, int EC>
+V2Kernel v2_kernel_ec(const V2Params &P)
 {
-  auto kern = cg_cluster_v2<RPT>;
+  return !P.async_x ? cg_cluster_v2<RPT, EC, false>
+                    : (P.prof ? cg_cluster_v2<RPT, EC, true, true> : cg_cluster_v2<RPT, EC, true, false>);
+}
+
+// The exact instance v2_launch runs for these parameters (the uniform 5-entry-row variant for the
+// Hermite operators and their A-pattern factors at 4 rows per thread).
+template <int RPT>
+V2Kernel v2_kernel(const V2Params &P)
+{
+  if constexpr (RPT == 4)
+  {
+    bool uniform5 = P.ea == 5;
+    for (int st = 0; st < P.z; ++st)
+      uniform5 = uniform5 && P.ef[st] == 5;
+    if (uniform5)
+      return v2_kernel_ec<4, 5>(P);
+  }
+  return v2_kernel_ec<RPT, 0>(P);
+}
+
+int v2_active_clusters_query(V2Kernel kern, int cs, size_t dyn)
+{
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)) != cudaSuccess ||
       cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
   {
@@ -1398,17 +1422,19 @@ int v2_active_clusters_query(int cs, size_t dyn)
   return clusters;
 }
 
+// Co-resident clusters of the instance that will actually launch (memoised per instance).
 template <int RPT>
 int v2_active_clusters(mgpu_ctx *ctx, const V2Params &P, size_t dyn)
 {
-  return cached_active_clusters(ctx->device, 100 + RPT, P.cs, dyn, v2_active_clusters_query<RPT>);
+  const V2Kernel kern = v2_kernel<RPT>(P);
+  return cached_active_clusters(ctx->device, reinterpret_cast<uintptr_t>(kern), P.cs, dyn,
+                                [kern](int cs, size_t d) { return v2_active_clusters_query(kern, cs, d); });
 }
 
-template <int RPT, int EC>
-void v2_launch_ec(mgpu_ctx *ctx, const V2Params &P, size_t dyn)
+template <int RPT>
+void v2_launch(mgpu_ctx *ctx, const V2Params &P, size_t dyn)
 {
-  auto kern = !P.async_x ? cg_cluster_v2<RPT, EC, false>
-                         : (P.prof ? cg_cluster_v2<RPT, EC, true, true> : cg_cluster_v2<RPT, EC, true, false>);
+  const V2Kernel kern = v2_kernel<RPT>(P);
   MG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
   MG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg{};
@@ -1427,24 +1453,6 @@ void v2_launch_ec(mgpu_ctx *ctx, const V2Params &P, size_t dyn)
   check_launch(ctx, "cg_cluster_v2");
 }
 
-template <int RPT>
-void v2_launch(mgpu_ctx *ctx, const V2Params &P, size_t dyn)
-{
-  // uniform 5-entry rows (the Hermite operators and their LS-SPAI factors on the A pattern)
-  bool uniform5 = RPT == 4 && P.ea == 5;
-  for (int st = 0; st < P.z; ++st)
-    uniform5 = uniform5 && P.ef[st] == 5;
-  if constexpr (RPT == 4)
-  {
-    if (uniform5)
-    {
-      v2_launch_ec<4, 5>(ctx, P, dyn);
-      return;
-    }
-  }
-  v2_launch_ec<RPT, 0>(ctx, P, dyn);
-}
-
 // Plans and launches v2; false when no cluster size fits.  Picks the size that
 // minimises (waves x rows per CTA) given the co-residency the driver reports.
 bool v2_solve(mgpu_ctx *ctx, V2Params P, size_t budget)
@@ -1453,9 +1461,7 @@ bool v2_solve(mgpu_ctx *ctx, V2Params P, size_t budget)
   size_t best_dyn = 0;
   double best_cost = 1e300;
   V2Params best{};
-  int only_cs = 0; // MGPU_CLUSTER_CS=k: consider cluster size k only (diagnostics)
-  if (const char *f = std::getenv("MGPU_CLUSTER_CS"))
-    only_cs = std::atoi(f);
+  const int only_cs = static_cast<int>(ctx->opt[MGPU_OPT_CLUSTER_CS]); // k > 0: cluster size k only (diagnostics)
   for (int cs = 1; cs <= kCMaxCS; ++cs)
   {
     if (only_cs > 0 && cs != only_cs)
@@ -1573,9 +1579,7 @@ int cg_cluster_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, cons
     V.hist_cap = hist_cap;
     V.loop_iters = d_loop;
     V.prof = ctx->prof_dev;
-    V.async_x = 1;
-    if (const char *f = std::getenv("MGPU_CLUSTER_ASYNC")) // 0: cluster-barrier exchange (diagnostics)
-      V.async_x = f[0] != '0';
+    V.async_x = ctx->opt[MGPU_OPT_CLUSTER_ASYNC] != 0; // 0: cluster-barrier exchange (diagnostics)
     if (v2_solve(ctx, V, static_cast<size_t>(cdev0) - sizeof(ClShared) - 1024))
       return 2;
   }

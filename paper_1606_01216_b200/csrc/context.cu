@@ -12,12 +12,13 @@
 namespace mgpu
 {
 
-// MGPU_HOST_TRACE=1: host timestamps (steady clock, microseconds) on stderr (diagnostics).
+// -DMGPU_HOST_TRACE: host timestamps (steady clock, microseconds) on stderr (diagnostics).
 void host_mark(const char *what)
 {
-  static const bool on = std::getenv("MGPU_HOST_TRACE") != nullptr;
-  if (!on)
-    return;
+#ifndef MGPU_HOST_TRACE
+  (void)what;
+  return;
+#endif
   const double us =
       std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
   std::fprintf(stderr, "[host %10.1f us] %s\n", us, what);
@@ -288,11 +289,6 @@ int mgpu_ctx_create(int device, void *stream, mgpu_ctx **out)
     }
     MG_CUDA(cudaEventCreate(&ctx->ev0));
     MG_CUDA(cudaEventCreate(&ctx->ev1));
-    if (std::getenv("MGPU_PROFILE_PHASES"))
-    {
-      MG_CUDA(cudaMalloc(reinterpret_cast<void **>(&ctx->prof_dev), 16 * sizeof(long long)));
-      MG_CUDA(cudaMemset(ctx->prof_dev, 0, 16 * sizeof(long long)));
-    }
   });
   if (st != MGPU_OK)
   {
@@ -387,6 +383,49 @@ int mgpu_ctx_set_cg_path(mgpu_ctx *ctx, int path)
 }
 
 int mgpu_last_cg_path(const mgpu_ctx *ctx) { return ctx ? ctx->last_cg_path : -1; }
+
+int mgpu_ctx_set_option(mgpu_ctx *ctx, int option, int64_t value)
+{
+  if (ctx == nullptr)
+    return MGPU_ERR_ARG;
+  return guard(ctx, [&] {
+    MG_ARG(option >= 0 && option < MGPU_OPT_COUNT, "ctx_set_option: unknown option");
+    if (option == MGPU_OPT_STREAM_RING)
+      MG_ARG(value == 0 || (value >= 2 && value <= 4), "ctx_set_option: ring depth must be 2..4");
+    if (option == MGPU_OPT_PROFILE_PHASES && value && !ctx->prof_dev)
+    {
+      MG_CUDA(cudaMalloc(reinterpret_cast<void **>(&ctx->prof_dev), 16 * sizeof(long long)));
+      MG_CUDA(cudaMemset(ctx->prof_dev, 0, 16 * sizeof(long long)));
+    }
+    if (option == MGPU_OPT_PROFILE_PHASES && !value && ctx->prof_dev)
+    {
+      MG_CUDA(cudaDeviceSynchronize());
+      MG_CUDA(cudaFree(ctx->prof_dev));
+      ctx->prof_dev = nullptr;
+    }
+    ctx->opt[option] = value;
+  });
+}
+
+int mgpu_ctx_get_option(const mgpu_ctx *ctx, int option, int64_t *value)
+{
+  if (ctx == nullptr || value == nullptr || option < 0 || option >= MGPU_OPT_COUNT)
+    return MGPU_ERR_ARG;
+  *value = ctx->opt[option];
+  return MGPU_OK;
+}
+
+int mgpu_phase_profile(mgpu_ctx *ctx, long long *out16)
+{
+  if (ctx == nullptr || out16 == nullptr)
+    return MGPU_ERR_ARG;
+  return guard(ctx, [&] {
+    MG_ARG(ctx->prof_dev != nullptr, "phase_profile: MGPU_OPT_PROFILE_PHASES is off");
+    MG_CUDA(cudaStreamSynchronize(ctx->stream));
+    MG_CUDA(cudaMemcpy(out16, ctx->prof_dev, 16 * sizeof(long long), cudaMemcpyDeviceToHost));
+    MG_CUDA(cudaMemset(ctx->prof_dev, 0, 16 * sizeof(long long)));
+  });
+}
 
 int mgpu_last_cg_timing(const mgpu_ctx *ctx, double *ms, int64_t *iterations)
 {

@@ -22,7 +22,7 @@ namespace mgpu
 // The context's pinned host staging buffer, at least `bytes` long.  Every user copies into it,
 // synchronises the stream and unpacks before returning, so one buffer per context suffices.
 void *pinned_scratch(mgpu_ctx *ctx, size_t bytes);
-// MGPU_HOST_TRACE=1: prints a steady-clock host timestamp and `what` on stderr (diagnostics)
+// Built with -DMGPU_HOST_TRACE: prints a steady-clock host timestamp and `what` on stderr (diagnostics)
 void host_mark(const char *what);
 
 // A C++ exception carrying an mgpu_status; converted at the C boundary.
@@ -58,15 +58,15 @@ struct Error : std::runtime_error
   } while (0)
 
 // Device buffer owned by RAII (cudaMallocAsync on the context stream).
-// Every device allocation of the library.  MGPU_POISON=1 (diagnostics) fills fresh memory
-// with 0xFF bytes (a NaN pattern) so a read of never-written memory cannot pass silently.
-inline bool mg_poison_enabled()
+// Every device allocation of the library.  Built with -DMGPU_POISON (diagnostics), fresh memory
+// is filled with 0xFF bytes (a NaN pattern) so a read of never-written memory cannot pass silently.
+inline constexpr bool mg_poison_enabled()
 {
-  static const bool on = [] {
-    const char *e = std::getenv("MGPU_POISON");
-    return e != nullptr && e[0] == '1';
-  }();
-  return on;
+#ifdef MGPU_POISON
+  return true;
+#else
+  return false;
+#endif
 }
 inline cudaError_t mg_malloc(void **p, size_t bytes, cudaStream_t s)
 {
@@ -135,7 +135,8 @@ struct mgpu_ctx
   int64_t last_cg_iters = 0;
   int last_cg_path = 1; // 0 banded (grid), 1 general, 2 cluster v2 (m = 1), 3 cluster v1
   int cg_path = 0;      // 0 auto, 1 force general, 2 force banded grid kernel, 3 cluster v1 only, 4 stream (no cluster)
-  long long *prof_dev = nullptr; // diagnostics: per-phase clock64 totals of the cluster kernel (MGPU_PROFILE_PHASES)
+  long long *prof_dev = nullptr; // diagnostics: per-phase clock64 totals of the CG kernels (MGPU_OPT_PROFILE_PHASES)
+  int64_t opt[MGPU_OPT_COUNT] = {1, 0, 0, 0, 0, 0, 1, 0, 0, 0}; // mgpu_ctx_set_option
   void *blas = nullptr;          // cublasHandle_t, created on first dense product (project.cu)
   cudaEvent_t phase_ev[4] = {nullptr, nullptr, nullptr, nullptr}; // mgpu_shifted_solve phase timing (lazy)
   void *pin = nullptr;           // pinned host staging for small device -> host reads (grown on demand)

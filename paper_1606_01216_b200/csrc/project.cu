@@ -440,7 +440,7 @@ int mgpu_thin_qr(mgpu_ctx *ctx, int64_t rows, int64_t cols, const double *A, dou
       QrArgs a{rows, static_cast<int>(cols), W.as<double>(), Qd.as<double>(), diag.as<double>(), tau.as<double>(),
                rank_tol * (anorm > 0.0 ? anorm : 1.0), part.as<double>(), 0, static_cast<int>(cols)};
       void *args[] = {&a};
-      if (std::getenv("MGPU_QR_UNBLOCKED")) // diagnostics: the column-by-column reference schedule
+      if (ctx->opt[MGPU_OPT_QR_UNBLOCKED]) // diagnostics: the column-by-column reference schedule
       {
         MG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void *>(qr_factor), dim3(static_cast<unsigned>(G)),
                                             dim3(kQrTB), args, 0, s));

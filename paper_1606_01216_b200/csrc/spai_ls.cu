@@ -771,10 +771,10 @@ bool run_ls(mgpu_ctx *ctx, bool cs, int64_t n, int l, int maxrow, DCsr pat, DCsr
     return true;
   DBuf err(sizeof(unsigned long long), ctx->stream), ovf(sizeof(int), ctx->stream);
   // lane-per-column envelopes first (|J| <= 5 / 6 / 8 pattern entries, |I| <= 13 / 14 / 16 rows),
-  // then the lane-group kernels; MGPU_LS_GROUP=1 skips the lane kernels (diagnostics).  The
+  // then the lane-group kernels; MGPU_OPT_LS_GROUP skips the lane kernels (diagnostics).  The
   // <5, 13> envelope is taken only when it cannot overflow: a J pattern of bandwidth b gives
   // |I| <= 4 b + 1 (b = 3 on the Hermite beam: 13 rows).
-  const bool lanes = !std::getenv("MGPU_LS_GROUP");
+  const bool lanes = ctx->opt[MGPU_OPT_LS_GROUP] == 0;
   for (int cfg = -3; cfg < 3; ++cfg)
   {
     const int G = cfg == -3 ? 5 : (cfg == -2 ? 6 : (cfg == -1 ? 8 : (cfg == 0 ? 8 : (cfg == 1 ? 16 : 32))));

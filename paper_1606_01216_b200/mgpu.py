@@ -35,8 +35,12 @@ EXPORTED = [
     "mgpu_spai_update", "mgpu_spai_ls", "mgpu_spai_ls_batched", "mgpu_spgemm", "mgpu_cg_solve",
     "mgpu_model_chain", "mgpu_model_hermite", "mgpu_host_free", "mgpu_thin_qr", "mgpu_project_reduce", "mgpu_project_reduce_slab",
     "mgpu_arnoldi_deflate", "mgpu_model_hermite_device", "mgpu_csr_write", "mgpu_csr_read", "mgpu_shifted_solve",
-    "mgpu_csr_upload_batch",
+    "mgpu_csr_upload_batch", "mgpu_ctx_set_option", "mgpu_ctx_get_option", "mgpu_phase_profile",
 ]
+
+# mgpu.h mgpu_option
+OPTIONS = {"stream_fold": 0, "stream_serial": 1, "stream_chunk": 2, "stream_ring": 3, "stream_same_chb": 4,
+           "cluster_cs": 5, "cluster_async": 6, "profile_phases": 7, "qr_unblocked": 8, "ls_group": 9}
 
 
 # ---------------------------------------------------------------- errors
@@ -118,6 +122,9 @@ def lib():
         L.mgpu_launch_count.restype = i64
         L.mgpu_last_cg_timing.argtypes = [vp, C.POINTER(dbl), C.POINTER(i64)]
         L.mgpu_ctx_set_cg_path.argtypes = [vp, C.c_int]
+        L.mgpu_ctx_set_option.argtypes = [vp, C.c_int, i64]
+        L.mgpu_ctx_get_option.argtypes = [vp, C.c_int, C.POINTER(i64)]
+        L.mgpu_phase_profile.argtypes = [vp, C.POINTER(C.c_longlong)]
         L.mgpu_last_cg_path.argtypes = [vp]
         L.mgpu_csr_upload.argtypes = [vp, i64, i64, i64, vp, vp, vp, C.POINTER(vp)]
         L.mgpu_csr_upload_device.argtypes = [vp, i64, i64, i64, vp, vp, vp, C.POINTER(vp)]
@@ -267,6 +274,20 @@ class Context:
         self.check(lib().mgpu_ctx_set_cg_path(self.handle,
                                               {"auto": 0, "general": 1, "banded": 2, "cluster_v1": 3,
                                                "stream": 4}[path]))
+
+    def set_option(self, name: str, value: int):
+        """mgpu_ctx_set_option (tuning / diagnostic switches; the library reads no environment)."""
+        self.check(lib().mgpu_ctx_set_option(self.handle, OPTIONS[name], int(value)))
+
+    def get_option(self, name: str) -> int:
+        v = C.c_int64()
+        self.check(lib().mgpu_ctx_get_option(self.handle, OPTIONS[name], C.byref(v)))
+        return v.value
+
+    def phase_profile(self):
+        out = (C.c_longlong * 16)()
+        self.check(lib().mgpu_phase_profile(self.handle, out))
+        return list(out)
 
     @property
     def last_cg_path(self) -> str:

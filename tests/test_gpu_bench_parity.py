@@ -38,11 +38,10 @@ def _oracle_case():
 
 
 @pytest.mark.parametrize("path", ["auto", "stream", "stream_serial", "banded"])
-def test_bench_workload_iterate_parity(mg, path, monkeypatch):
+def test_bench_workload_iterate_parity(mg, path):
     (M, D, K), ops, facs, b, want = _oracle_case()
     ctx = mg.default_context()
-    if path == "stream_serial":
-        monkeypatch.setenv("MGPU_STREAM_SERIAL", "1")
+    ctx.set_option("stream_serial", 1 if path == "stream_serial" else 0)
     ctx.set_cg_path("stream" if path == "stream_serial" else path)
     try:
         # the bench's device pipeline: assembly + batched LS-SPAI + one batched solve
@@ -61,9 +60,10 @@ def test_bench_workload_iterate_parity(mg, path, monkeypatch):
             assert rel(r.X[:, 0], w["solution"]) < 1e-8
     finally:
         ctx.set_cg_path("auto")
+        ctx.set_option("stream_serial", 0)
 
 
-def test_config3_serial_schedule_matches_batched(mg, monkeypatch):
+def test_config3_serial_schedule_matches_batched(mg):
     """BASELINE configs[3] shape (n = 1e6, m = 4, 16 shifts, P = I) through the streaming
     kernel: the point-serial schedule (L2 hand-off between the phases, w discarded from L2)
     against the batched schedule after 40 iterations.  Same arithmetic per element; only the
@@ -79,12 +79,13 @@ def test_config3_serial_schedule_matches_batched(mg, monkeypatch):
     ops = mg.shifted_operators(M, D, K, shifts, ctx=ctx)
     ctx.set_cg_path("stream")
     try:
-        monkeypatch.setenv("MGPU_STREAM_SERIAL", "0")
+        ctx.set_option("stream_serial", 0)
         ref = mg.cg_solve_batched(ops, [[] for _ in ops], B, rtol=1e-10, maxit=k, ctx=ctx)
-        monkeypatch.setenv("MGPU_STREAM_SERIAL", "1")
+        ctx.set_option("stream_serial", 1)
         got = mg.cg_solve_batched(ops, [[] for _ in ops], B, rtol=1e-10, maxit=k, ctx=ctx)
     finally:
         ctx.set_cg_path("auto")
+        ctx.set_option("stream_serial", 0)
     for g, r in zip(got, ref):
         np.testing.assert_array_equal(g.iterations, r.iterations)
         assert rel(g.X, r.X) < 1e-10

@@ -14,18 +14,19 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.fixture(autouse=True, params=["auto", "cluster_v1", "stream", "stream_serial", "banded", "general"])
-def cg_path(request, mg, monkeypatch):
+def cg_path(request, mg):
     """Every parity case runs through every CG kernel: cluster-resident (auto on these
     on-chip sizes), the streaming kernel (batched and point-serial schedules), the banded
     grid kernel and the general CSR kernel."""
     ctx = mg.default_context()
     if request.param == "stream_serial":
-        monkeypatch.setenv("MGPU_STREAM_SERIAL", "1")
+        ctx.set_option("stream_serial", 1)
         ctx.set_cg_path("stream")
     else:
         ctx.set_cg_path(request.param)
     yield request.param
     ctx.set_cg_path("auto")
+    ctx.set_option("stream_serial", 0)
 
 
 def test_path_selection(mg, oracle, cg_path):

@@ -1,4 +1,4 @@
-"""Per-phase clock64 breakdown of the streaming CG kernel (MGPU_PROFILE_PHASES=1; block 0,
+"""Per-phase clock64 breakdown of the streaming CG kernel (context option profile_phases; block 0,
 thread 0).  Usage: python tools/stream_prof.py [iters] [ne] [m] [points] [ls]
 (defaults: BASELINE configs[3] shape, 50 iterations; ls=1 adds an LS-SPAI factor per point)."""
 import os, sys
@@ -8,6 +8,7 @@ import paper_1606_01216_b200 as mg
 a = [int(x) for x in sys.argv[1:]] + [None] * 5
 k, ne, m, l, ls = a[0] or 50, a[1] or 500000, a[2] or 4, a[3] or 16, a[4] or 0
 ctx = mg.Context(0)
+ctx.set_option("profile_phases", 1)
 M, D, K = mg.model_hermite_device(ne, ctx=ctx)
 shifts = [10.0 ** (1 + 3 * i / (l - 1)) for i in range(l)] if l > 1 else [100.0]
 ops = mg.shifted_operators(M, D, K, shifts, ctx=ctx)

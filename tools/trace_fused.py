@@ -1,4 +1,4 @@
-"""Host trace of one fused configs[1] step (MGPU_HOST_TRACE=1 python tools/trace_fused.py)."""
+"""Host trace of one fused configs[1] step (build libmgpu with -DMGPU_HOST_TRACE, then python tools/trace_fused.py)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
