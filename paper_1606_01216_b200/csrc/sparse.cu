@@ -221,6 +221,8 @@ void batched_add(mgpu_ctx *ctx, const mgpu_csr *A, const mgpu_csr *B, const mgpu
     const int cnt = l - base < 64 ? l - base : 64;
     ShiftArgs args{};
     std::vector<mgpu_csr *> made;
+    try
+    {
     for (int p = 0; p < cnt; ++p)
     {
       args.a[p] = as[base + p];
@@ -295,6 +297,19 @@ void batched_add(mgpu_ctx *ctx, const mgpu_csr *A, const mgpu_csr *B, const mgpu
     {
       add_fill_kernel<kThird><<<blocks_for(total), kThreads, 0, ctx->stream>>>(cnt, n, A->view(), B->view(), cv, args);
       check_launch(ctx, "add_fill_kernel");
+    }
+    }
+    catch (...)
+    {
+      // nothing is handed out on failure: this chunk's matrices and the earlier chunks' outputs
+      for (auto *o : made)
+        mgpu_csr_free(o);
+      for (int q = 0; q < base; ++q)
+      {
+        mgpu_csr_free(out[q]);
+        out[q] = nullptr;
+      }
+      throw;
     }
     for (int p = 0; p < cnt; ++p)
       out[base + p] = made[p];
