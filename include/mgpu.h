@@ -193,9 +193,9 @@ typedef enum mgpu_ls_pattern
 {
   MGPU_PATTERN_A = 0,  /* J_j = pattern of row j of A               */
   MGPU_PATTERN_A2 = 1, /* J_j = pattern of row j of the symbolic A*A */
-  /* flag, OR-ed into the pattern: column-equilibrated LS.  Every column c of S = A(I,J) is divided
-   * by d_c = ||S_c|| (in-order dot) before the QR and the solution by d_c after the
-   * back-substitution.  Same least-squares minimiser; it avoids thin_qr's global rank flush
+  /* flag, OR-ed into the pattern: column-equilibrated LS.  Every column c of S = A(I,J) is scaled
+   * by r_c = 1 / ||S_c|| (in-order dot, one division) before the QR and the solution by r_c after
+   * the back-substitution.  Same least-squares minimiser; it avoids thin_qr's global rank flush
    * (sigma <= 1e-12 ||S||_F, dense.cpp:162-179), which on the Hermite beam declares every column
    * rank-deficient from n = 2e5 (A^2 pattern) / 4e5 (A pattern) because the theta-dof columns
    * scale like h^2.  The oracle restates it in oracle.c orc_spai_ls / ref_shim.cpp ref_spai_ls. */

@@ -849,8 +849,8 @@ int orc_pattern_square(const orc_csr *A, orc_csr *out)
 }
 
 /* Column-equilibrated variant (pattern | ORC_LS_COLSCALE): before the QR every column c of S
- * is divided by d_c = ||S_c|| (in-order dot, sqrt), and the back-substituted solution is divided
- * by d_c again (m_c = u_c / d_c).  In exact arithmetic this is the same least-squares minimiser
+ * is scaled by r_c = 1 / ||S_c|| (in-order dot, sqrt, one division, S_ic * r_c), and the
+ * back-substituted solution by r_c again (m_c = u_c * r_c).  In exact arithmetic this is the same least-squares minimiser
  * (S D^-1 (D m) = S m); it removes the spurious global rank flush of thin_qr (sigma <= 1e-12
  * ||S||_F, dense.cpp:162-179), which on the Hermite beam fires once the theta-dof columns
  * (~h^2 smaller than the w-dof ones) drop below 1e-12 of the Frobenius norm (n >= 2e5 on the
@@ -945,16 +945,20 @@ int orc_spai_ls(const orc_csr *A, const orc_csr *K_old, int pattern, orc_csr *P,
       int zero_col = 0;
       if (colscale)
       {
-        /* d_c = sqrt(dot(S_c, S_c)) in index order (kernels_scalar.cpp:13-19), S_c /= d_c */
+        /* d_c = sqrt(dot(S_c, S_c)) in index order (kernels_scalar.cpp:13-19), r_c = 1 / d_c,
+         * S_c *= r_c */
         for (int64_t c = 0; c < nj; ++c)
         {
           const double d = sqrt(dot_s(S + c * ni, S + c * ni, ni));
-          dsc[c] = d;
           if (d == 0.0)
+          {
             zero_col = 1;
-          else
-            for (int64_t i = 0; i < ni; ++i)
-              S[c * ni + i] = S[c * ni + i] / d;
+            dsc[c] = 0.0;
+            continue;
+          }
+          dsc[c] = 1.0 / d;
+          for (int64_t i = 0; i < ni; ++i)
+            S[c * ni + i] = S[c * ni + i] * dsc[c];
         }
       }
       if (!zero_col)
@@ -979,7 +983,7 @@ int orc_spai_ls(const orc_csr *A, const orc_csr *K_old, int pattern, orc_csr *P,
         }
         if (colscale)
           for (int64_t c = 0; c < nj; ++c)
-            mm[c] = mm[c] / dsc[c];
+            mm[c] = mm[c] * dsc[c];
         for (int64_t c = 0; c < nj; ++c)
         {
           tr[t] = pat.col_idx[jb + c];

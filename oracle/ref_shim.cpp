@@ -448,8 +448,8 @@ int ref_spai_ls(const ref_csr *A_in, const ref_csr *K_old_in, int pattern, ref_c
     {
       throw mor::ArgumentError("spai_ls: operands must be square with equal shape");
     }
-    // pattern | 0x10: column-equilibrated variant (oracle.c orc_spai_ls header): S_c /= ||S_c||
-    // before thin_qr, m_c = u_c / ||S_c|| after the back-substitution
+    // pattern | 0x10: column-equilibrated variant (oracle.c orc_spai_ls header): r_c = 1 / ||S_c||,
+    // S_c *= r_c before thin_qr, m_c = u_c * r_c after the back-substitution
     const bool colscale = (pattern & 0x10) != 0;
     pattern &= ~0x10;
     // symbolic pattern rows
@@ -544,10 +544,11 @@ int ref_spai_ls(const ref_csr *A_in, const ref_csr *K_old_in, int pattern, ref_c
           {
             throw mor::NumericalError("spai_ls: rank-deficient least-squares problem in column " + std::to_string(j));
           }
-          dsc[static_cast<std::size_t>(c)] = d;
+          const double r = 1.0 / d;
+          dsc[static_cast<std::size_t>(c)] = r;
           for (int64_t i = 0; i < ni; ++i)
           {
-            S.at(i, c) = S.at(i, c) / d;
+            S.at(i, c) = S.at(i, c) * r;
           }
         }
       }
@@ -574,7 +575,7 @@ int ref_spai_ls(const ref_csr *A_in, const ref_csr *K_old_in, int pattern, ref_c
       {
         for (int64_t c = 0; c < nj; ++c)
         {
-          m[static_cast<std::size_t>(c)] = m[static_cast<std::size_t>(c)] / dsc[static_cast<std::size_t>(c)];
+          m[static_cast<std::size_t>(c)] = m[static_cast<std::size_t>(c)] * dsc[static_cast<std::size_t>(c)];
         }
       }
       for (int64_t c = 0; c < nj; ++c)

@@ -1465,6 +1465,11 @@ struct StreamParams
   int fold;             // 1: x~ += alpha d deferred to the next phase A (m = 1), 0: applied in phase B
   int nb;               // ring depth (2..kStreamNB)
   int serial;           // 1: points one after another (all blocks on one point's rows; L2 hand-off A -> B)
+  // stage-buffer layout: 0 = row-interleaved [row][c]; > 0 (m == 4) = two planes of double2,
+  // (c0, c1) and (c2, c3) per row, plane stride `pst` doubles.  A thread's row loads are then two
+  // 16-byte loads from consecutive 16-byte slots across the warp (no bank conflicts; the
+  // interleaved 32-byte rows cost two wavefronts per 16-byte load).
+  int pst;
   int64_t n, ldv; // ldv = (n + 2 PADR) * m: doubles per point block
   int halo[kMaxZ + 1];
   int hmax;
@@ -1735,6 +1740,137 @@ __device__ __forceinline__ void ell_row(const double *vals, const unsigned long 
   }
 }
 
+// The same row with the width EC and the column count MT known at compile time (m == MT): the
+// offsets are byte extracts at constant positions, the loads vectorised, no per-column guards.
+// Same terms in the same order as ell_row (bitwise equal).
+template <int MT, int EC, bool PL = false>
+__device__ __forceinline__ void ell_row_fixed(const double *vals, const unsigned long long *offs, const double *src,
+                                              int in0, double (&a2)[MT], int pst = 0)
+{
+#pragma unroll
+  for (int c = 0; c < MT; ++c)
+    a2[c] = 0.0;
+  const unsigned long long w0 = offs[0];
+  const unsigned long long w1 = EC > 8 ? offs[1] : 0ull;
+#pragma unroll
+  for (int e = 0; e < EC; ++e)
+  {
+    const double ae = vals[e];
+    const int off = e < 8 ? off8s(w0, e) : off8s(w1, e - 8);
+    double x[MT];
+    if constexpr (PL && MT == 4)
+    {
+      const double2 t0 = reinterpret_cast<const double2 *>(src)[in0 + off];
+      const double2 t1 = reinterpret_cast<const double2 *>(src + pst)[in0 + off];
+      x[0] = t0.x;
+      x[1] = t0.y;
+      x[2] = t1.x;
+      x[3] = t1.y;
+    }
+    else if constexpr (MT >= 2)
+    {
+#pragma unroll
+      for (int h = 0; h < MT / 2; ++h)
+      {
+        const double2 t = reinterpret_cast<const double2 *>(src + (in0 + off) * MT)[h];
+        x[2 * h] = t.x;
+        x[2 * h + 1] = t.y;
+      }
+    }
+    else
+      x[0] = src[in0 + off];
+#pragma unroll
+    for (int c = 0; c < MT; ++c)
+      a2[c] = __dadd_rn(a2[c], __dmul_rn(ae, x[c]));
+  }
+}
+
+// Planar (m == 4) row of any width: ell_row's terms in ell_row's order.
+__device__ __forceinline__ void ell_row_planar(const double *vals, const unsigned long long *offs, int E, int ow,
+                                               const double *src, int in0, int pst, double (&a2)[4])
+{
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    a2[c] = 0.0;
+  const unsigned long long w0 = offs[0];
+  const unsigned long long w1 = ow > 1 ? offs[1] : 0ull;
+  for (int e = 0; e < E; ++e)
+  {
+    const int r = in0 + off16(w0, w1, e);
+    const double a = vals[e];
+    const double2 t0 = reinterpret_cast<const double2 *>(src)[r];
+    const double2 t1 = reinterpret_cast<const double2 *>(src + pst)[r];
+    a2[0] = __dadd_rn(a2[0], __dmul_rn(a, t0.x));
+    a2[1] = __dadd_rn(a2[1], __dmul_rn(a, t0.y));
+    a2[2] = __dadd_rn(a2[2], __dmul_rn(a, t1.x));
+    a2[3] = __dadd_rn(a2[3], __dmul_rn(a, t1.y));
+  }
+}
+
+// Stage-buffer row access in the P.pst layout.
+template <int MT>
+__device__ __forceinline__ void ld_stage(const double *buf, int row, double (&v)[MT], int m, int pst)
+{
+  if constexpr (MT == 4)
+  {
+    if (pst > 0)
+    {
+      const double2 t0 = reinterpret_cast<const double2 *>(buf)[row];
+      const double2 t1 = reinterpret_cast<const double2 *>(buf + pst)[row];
+      v[0] = t0.x;
+      v[1] = t0.y;
+      v[2] = t1.x;
+      v[3] = t1.y;
+      return;
+    }
+  }
+  ld_row<MT>(buf + row * m, v, m);
+}
+template <int MT>
+__device__ __forceinline__ void st_stage(double *buf, int row, const double (&v)[MT], int m, int pst)
+{
+  if constexpr (MT == 4)
+  {
+    if (pst > 0)
+    {
+      reinterpret_cast<double2 *>(buf)[row] = make_double2(v[0], v[1]);
+      reinterpret_cast<double2 *>(buf + pst)[row] = make_double2(v[2], v[3]);
+      return;
+    }
+  }
+  st_row<MT>(buf + row * m, v, m);
+}
+// Index of element e (= row * m + c) of a stage buffer.
+__device__ __forceinline__ int stage_idx(int e, int m, int pst)
+{
+  if (pst > 0) // m == 4
+    return ((e & 2) ? pst : 0) + ((e >> 2) << 1) + (e & 1);
+  return e;
+}
+
+// ell_row with the common widths (the Hermite operators: 5; their A^2-pattern factors: 10) and
+// m == MT dispatched to ell_row_fixed.
+// EF: the width this call site expects (the A^2-pattern factors: 10; the Hermite operators: 5),
+// unrolled; any other width takes the loop.  One unrolled width per call site keeps the kernel
+// inside its 128 registers (two unrolled widths per site pushed the parameters to local memory).
+template <int MT, int EF>
+__device__ __forceinline__ void ell_row_any(const double *vals, const unsigned long long *offs, int E, int ow,
+                                            const double *src, int in0, int m, double (&a2)[MT], int pst)
+{
+  if constexpr (MT == 4)
+  {
+    if (pst > 0)
+    {
+      if (E == EF)
+        ell_row_fixed<4, EF, true>(vals, offs, src, in0, a2, pst);
+      else
+        ell_row_planar(vals, offs, E, ow, src, in0, pst, a2);
+      return;
+    }
+  }
+  ell_row<MT>(vals, offs, E, ow, src, in0, m, a2);
+}
+
 // Per-phase clock64 totals (MGPU_PROFILE_PHASES); the ON = false instantiation compiles away.
 template <bool ON>
 struct PhaseClock
@@ -1984,7 +2120,7 @@ __device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, cons
         const double be = sh.beta[sys], al = sh.alpha[sys];
         if (kind == 1)
           for (int e = threadIdx.x; e < ne0; e += TB)
-            s0[e] = pd ? __dadd_rn(vr[e], __dmul_rn(al, vd[e])) : vr[e];
+            s0[stage_idx(e, m, P.pst)] = pd ? __dadd_rn(vr[e], __dmul_rn(al, vd[e])) : vr[e];
         else
           for (int e = threadIdx.x; e < ne0; e += TB)
           {
@@ -1995,7 +2131,7 @@ __device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, cons
               if (pd && run)
                 __stcg(xg + e, __dadd_rn(vx[e - lo], __dmul_rn(al, vd[e])));
             }
-            s0[e] = v;
+            s0[stage_idx(e, m, P.pst)] = v;
           }
       }
       else
@@ -2016,7 +2152,7 @@ __device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, cons
               __stcg(xg + e, __dadd_rn(vx[e - lo], __dmul_rn(sh.alpha[sys], vd[e])));
           }
         }
-        s0[e] = v;
+        s0[stage_idx(e, m, P.pst)] = v;
       }
       consumer_sync<TB>();
       pc.mark(4);
@@ -2033,8 +2169,8 @@ __device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, cons
         for (int q = threadIdx.x; q < span; q += TB)
         {
           double a2[MT];
-          ell_row<MT>(fv + q * F.E, fo + q * F.ow, F.E, F.ow, src, q + hs - hd, m, a2);
-          st_row<MT>(dst + q * m, a2, m);
+          ell_row_any<MT, 10>(fv + q * F.E, fo + q * F.ow, F.E, F.ow, src, q + hs - hd, m, a2, P.pst);
+          st_stage<MT>(dst, q, a2, m, P.pst);
         }
         consumer_sync<TB>();
         src = dst;
@@ -2048,7 +2184,7 @@ __device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, cons
       for (int lr = threadIdx.x; lr < R; lr += TB)
       {
         double a2[MT];
-        ell_row<MT>(av + lr * A.E, ao + lr * A.ow, A.E, A.ow, src, lr + hs, m, a2);
+        ell_row_any<MT, 5>(av + lr * A.E, ao + lr * A.ow, A.E, A.ow, src, lr + hs, m, a2, P.pst);
         if (kind == 1)
         {
           const int64_t i = base_i + lr;
@@ -2059,14 +2195,14 @@ __device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, cons
               break;
             const double res = __dsub_rn(__ldg(vrow(P, P.b, cp, i) + c), a2[c]);
             __stcg(wg + lr * m + c, res);
-            __stcg(const_cast<double *>(vrow(P, P.sol, cp, i)) + c, src[(lr + hs) * m + c]);
+            __stcg(const_cast<double *>(vrow(P, P.sol, cp, i)) + c, src[stage_idx((lr + hs) * m + c, m, P.pst)]);
             acc[c] = __dadd_rn(acc[c], __dmul_rn(res, res));
           }
         }
         else
         {
           double dn[MT];
-          ld_row<MT>(s0 + (H0 + lr) * m, dn, m);
+          ld_stage<MT>(s0, H0 + lr, dn, m, P.pst);
           stg_row<MT>(wg + lr * m, a2, m);
 #pragma unroll
           for (int c = 0; c < MT; ++c)
@@ -2780,9 +2916,12 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
     const size_t b_bytes = sizeof(double) * ch * m * (fold ? 2 : 4);
     P.buf_bytes = (std::max(a_bytes, b_bytes) + 127) & ~static_cast<size_t>(127);
     off = nb * P.buf_bytes;
-    P.off_stage0 = take(sizeof(double) * (ch + 2 * H0) * m);
-    P.off_stage1 = z >= 1 ? take(sizeof(double) * (ch + 2 * hal[1]) * m) : 0; // stage buffers the chain uses
-    P.off_stage2 = z >= 2 ? take(sizeof(double) * (ch + 2 * hal[2]) * m) : 0;
+    // m == 4 with a chain: planar stage buffers, one plane stride (the widest buffer's rows) for all
+    const int64_t srows0 = ch + 2 * H0;
+    P.pst = (m == 4 && z >= 1) ? static_cast<int>(2 * srows0) : 0; // (P = I measured 842 -> 859 us planar)
+    P.off_stage0 = take(sizeof(double) * srows0 * m);
+    P.off_stage1 = z >= 1 ? take(sizeof(double) * (P.pst ? srows0 : ch + 2 * hal[1]) * m) : 0; // chain stages
+    P.off_stage2 = z >= 2 ? take(sizeof(double) * (P.pst ? srows0 : ch + 2 * hal[2]) * m) : 0;
     if (off + stat <= static_cast<size_t>(optin))
     {
       dyn = off;

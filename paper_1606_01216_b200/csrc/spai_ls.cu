@@ -116,7 +116,7 @@ __global__ void square_fill(int64_t n, DCsr A, const int64_t *rp, int32_t *ci)
 template <int G, int NI>
 struct LsGroupSmem
 {
-  double dsc[G]; // column scales ||S_c|| (column-equilibrated variant)
+  double dsc[G]; // column scales 1 / ||S_c|| (column-equilibrated variant)
   double W[G * (NI + 1)]; // S / Householder vectors, column-major, ld = NI + 1 (odd: bank spread)
   double Q[G * (NI + 1)]; // Q; before the QR: staged values of A^T row J_c (lane c)
   int32_t rows[G * NI];    // staged column indices of A^T row J_c (lane c)
@@ -297,16 +297,16 @@ __global__ void ls_columns(int64_t n, int l, DCsr pat, DCsr At, int64_t at_strid
     }
   }
   __syncwarp(gmask);
-  if (CS) // column equilibration: d_c = ||S_c|| (in-order dot), S_c /= d_c (oracle.c orc_spai_ls)
+  if (CS) // column equilibration: r_c = 1 / ||S_c|| (in-order dot), S_c *= r_c (oracle.c orc_spai_ls)
   {
     if (c < nj)
     {
       double *col = sm.W + c * LD;
       const double d = sqrt(dot_serial(col, col, ni));
-      sm.dsc[c] = d;
+      sm.dsc[c] = d == 0.0 ? 0.0 : 1.0 / d;
       if (d != 0.0)
         for (int i = 0; i < ni; ++i)
-          col[i] = col[i] / d;
+          col[i] = __dmul_rn(col[i], sm.dsc[c]);
     }
     __syncwarp(gmask);
     bool zero = false;
@@ -435,7 +435,7 @@ __global__ void ls_columns(int64_t n, int l, DCsr pat, DCsr At, int64_t at_strid
   }
   __syncwarp(gmask);
   if (c < nj)
-    out_vals[jb + c] = CS ? sm.m[c] / sm.dsc[c] : sm.m[c];
+    out_vals[jb + c] = CS ? __dmul_rn(sm.m[c], sm.dsc[c]) : sm.m[c];
 }
 
 // Longest row of a CSR structure (warp max, one atomic per warp).
@@ -585,7 +585,7 @@ __global__ void __launch_bounds__(64) ls_columns_lane(int64_t n, int l, DCsr pat
       if (i < ni && I[i] == j)
         e[i] = 1.0;
   }
-  if (CS) // column equilibration: d_c = ||S_c|| (in-order dot), S_c /= d_c (oracle.c orc_spai_ls)
+  if (CS) // column equilibration: r_c = 1 / ||S_c|| (in-order dot), S_c *= r_c (oracle.c orc_spai_ls)
   {
     for (int c = 0; c < nj; ++c)
     {
@@ -596,9 +596,10 @@ __global__ void __launch_bounds__(64) ls_columns_lane(int64_t n, int l, DCsr pat
         report(err, g, MGPU_ERR_NUMERICAL);
         return;
       }
-      dsc[c] = d;
+      const double r = 1.0 / d;
+      dsc[c] = r;
       for (int i = 0; i < ni; ++i)
-        col[i] = col[i] / d;
+        col[i] = __dmul_rn(col[i], r);
     }
   }
   // ---- thin_qr (dense.cpp:153-246): frob_norm tolerance in column-major order
@@ -608,77 +609,170 @@ __global__ void __launch_bounds__(64) ls_columns_lane(int64_t n, int l, DCsr pat
       acc = __dadd_rn(acc, __dmul_rn(W[c * NI + i], W[c * NI + i]));
   const double anorm = sqrt(acc);
   const double tol = 1e-12 * (anorm > 0.0 ? anorm : 1.0);
-  bool deficient = false;
+  // Householder steps.  The reflector x (column k below the diagonal) is held in registers for
+  // the whole trailing update, and the trailing columns are updated two at a time (two
+  // independent in-order dot chains, one shared-memory read of x per step): per column the
+  // operations and their order are exactly thin_qr's (dense.cpp:168-188).  A flushed column
+  // (sigma <= tol) makes the problem rank-deficient, which is an error whatever follows, so the
+  // lane stops there.
   for (int k = 0; k < nj; ++k)
   {
     const int len = ni - k;
-    double *x = W + k * NI + k;
-    const double sigma = sqrt(dot_serial(x, x, len));
+    double *xs = W + k * NI + k;
+    double x[NI];
+#pragma unroll
+    for (int i = 0; i < NI; ++i)
+      x[i] = i < len ? xs[i] : 0.0;
+    double acc2 = 0.0;
+#pragma unroll
+    for (int i = 0; i < NI; ++i)
+      if (i < len)
+        acc2 = __dadd_rn(acc2, __dmul_rn(x[i], x[i]));
+    const double sigma = sqrt(acc2);
     if (sigma <= tol)
     {
-      diag[k] = 0.0;
-      tau[k] = 0.0;
-      for (int i = 0; i < len; ++i)
-        x[i] = 0.0;
-      deficient = true;
-      continue;
+      report(err, g, MGPU_ERR_NUMERICAL); // rank < |J|
+      return;
     }
     const double alpha = x[0] >= 0.0 ? -sigma : sigma;
     x[0] = __dsub_rn(x[0], alpha);
-    const double vtv = dot_serial(x, x, len);
+    xs[0] = x[0];
+    double vtv = 0.0;
+#pragma unroll
+    for (int i = 0; i < NI; ++i)
+      if (i < len)
+        vtv = __dadd_rn(vtv, __dmul_rn(x[i], x[i]));
     const double tk = vtv > 0.0 ? 2.0 / vtv : 0.0;
     tau[k] = tk;
     diag[k] = alpha;
-    if (tk != 0.0)
-      for (int c = k + 1; c < nj; ++c)
-      {
-        double *y = W + c * NI + k;
-        const double sc = __dmul_rn(tk, dot_serial(x, y, len));
-        axpy_serial(len, -sc, x, y);
-      }
+    if (tk == 0.0)
+      continue;
+    int c = k + 1;
+    for (; c + 1 < nj; c += 2)
+    {
+      double *ya = W + c * NI + k, *yb = ya + NI;
+      double y0[NI], y1[NI];
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int i = 0; i < NI; ++i)
+        if (i < len)
+        {
+          y0[i] = ya[i];
+          y1[i] = yb[i];
+          a0 = __dadd_rn(a0, __dmul_rn(x[i], y0[i]));
+          a1 = __dadd_rn(a1, __dmul_rn(x[i], y1[i]));
+        }
+      const double s0 = -__dmul_rn(tk, a0), s1 = -__dmul_rn(tk, a1);
+#pragma unroll
+      for (int i = 0; i < NI; ++i)
+        if (i < len)
+        {
+          ya[i] = __dadd_rn(y0[i], __dmul_rn(s0, x[i]));
+          yb[i] = __dadd_rn(y1[i], __dmul_rn(s1, x[i]));
+        }
+    }
+    if (c < nj)
+    {
+      double *ya = W + c * NI + k;
+      double y0[NI];
+      double a0 = 0.0;
+#pragma unroll
+      for (int i = 0; i < NI; ++i)
+        if (i < len)
+        {
+          y0[i] = ya[i];
+          a0 = __dadd_rn(a0, __dmul_rn(x[i], y0[i]));
+        }
+      const double s0 = -__dmul_rn(tk, a0);
+#pragma unroll
+      for (int i = 0; i < NI; ++i)
+        if (i < len)
+          ya[i] = __dadd_rn(y0[i], __dmul_rn(s0, x[i]));
+    }
   }
-  if (deficient) // rank < |J|
+  // ---- y_c = (sign-fixed column c of Q = H_0 ... H_{nj-1} e_c)^T e.  Columns c and c + 1 are
+  // formed together in registers: q1 takes reflector c + 1 alone, then both take c .. 0, so each
+  // column sees thin_qr's reflector sequence (dense.cpp:200-218) and every reflector is read
+  // from shared memory once per pair.
+  for (int c = 0; c < nj; c += 2)
   {
-    report(err, g, MGPU_ERR_NUMERICAL);
-    return;
-  }
-  // ---- y_c = (sign-fixed column c of Q = H_0 ... H_{nj-1} e_c)^T e, column in registers
-  for (int c = 0; c < nj; ++c)
-  {
-    double q[NI];
+    const bool two = c + 1 < nj;
+    double q0[NI], q1[NI];
 #pragma unroll
     for (int i = 0; i < NI; ++i)
-      q[i] = i == c ? 1.0 : 0.0;
-#pragma unroll
-    for (int k = NJ - 1; k >= 0; --k) // k = min(c, nj - 1) .. 0 (c < nj)
     {
-      if (k > c || tau[k] == 0.0)
+      q0[i] = i == c ? 1.0 : 0.0;
+      q1[i] = i == c + 1 ? 1.0 : 0.0;
+    }
+#pragma unroll
+    for (int k = NJ - 1; k >= 0; --k)
+    {
+      if (k > c + 1 || (k == c + 1 && !two))
         continue;
-      const double *v = W + k * NI + k;
+      const double tk = tau[k];
+      if (tk == 0.0)
+        continue;
+      const double *vs = W + k * NI + k;
       const int len = ni - k;
-      double acc = 0.0;
+      double v[NI];
+#pragma unroll
+      for (int i = 0; i + k < NI; ++i)
+        v[i] = i < len ? vs[i] : 0.0;
+      if (k == c + 1) // q1 only
+      {
+        double a1 = 0.0;
+#pragma unroll
+        for (int i = 0; i + k < NI; ++i)
+          if (i < len)
+            a1 = __dadd_rn(a1, __dmul_rn(v[i], q1[k + i]));
+        const double s1 = -__dmul_rn(tk, a1);
+#pragma unroll
+        for (int i = 0; i + k < NI; ++i)
+          if (i < len)
+            q1[k + i] = __dadd_rn(q1[k + i], __dmul_rn(s1, v[i]));
+        continue;
+      }
+      double a0 = 0.0, a1 = 0.0;
 #pragma unroll
       for (int i = 0; i + k < NI; ++i)
         if (i < len)
-          acc = __dadd_rn(acc, __dmul_rn(v[i], q[k + i]));
-      const double sc = __dmul_rn(tau[k], acc);
+        {
+          a0 = __dadd_rn(a0, __dmul_rn(v[i], q0[k + i]));
+          a1 = __dadd_rn(a1, __dmul_rn(v[i], q1[k + i]));
+        }
+      const double s0 = -__dmul_rn(tk, a0), s1 = -__dmul_rn(tk, a1);
 #pragma unroll
       for (int i = 0; i + k < NI; ++i)
         if (i < len)
-          q[k + i] = __dadd_rn(q[k + i], __dmul_rn(-sc, v[i]));
+        {
+          q0[k + i] = __dadd_rn(q0[k + i], __dmul_rn(s0, v[i]));
+          if (two)
+            q1[k + i] = __dadd_rn(q1[k + i], __dmul_rn(s1, v[i]));
+        }
     }
     if (diag[c] < 0.0)
     {
 #pragma unroll
       for (int i = 0; i < NI; ++i)
-        q[i] = __dmul_rn(q[i], -1.0);
+        q0[i] = __dmul_rn(q0[i], -1.0);
     }
-    double y = 0.0;
+    if (two && diag[c + 1] < 0.0)
+    {
+#pragma unroll
+      for (int i = 0; i < NI; ++i)
+        q1[i] = __dmul_rn(q1[i], -1.0);
+    }
+    double y0 = 0.0, y1 = 0.0;
 #pragma unroll
     for (int i = 0; i < NI; ++i)
       if (i < ni)
-        y = __dadd_rn(y, __dmul_rn(q[i], e[i]));
-    mv[c] = y;
+      {
+        y0 = __dadd_rn(y0, __dmul_rn(q0[i], e[i]));
+        y1 = __dadd_rn(y1, __dmul_rn(q1[i], e[i]));
+      }
+    mv[c] = y0;
+    if (two)
+      mv[c + 1] = y1;
   }
   // ---- sign fix of R's off-diagonal rows (R(k, c) = W[c][k], c > k), |R_cc|
   for (int c = 0; c < nj; ++c)
@@ -697,7 +791,7 @@ __global__ void __launch_bounds__(64) ls_columns_lane(int64_t n, int l, DCsr pat
     mv[k] = a / tau[k];
   }
   for (int c = 0; c < nj; ++c)
-    out_vals[jb + c] = CS ? mv[c] / dsc[c] : mv[c];
+    out_vals[jb + c] = CS ? __dmul_rn(mv[c], dsc[c]) : mv[c];
 }
 
 // TPB: threads per block (32 packs the per-lane scratch more tightly for small envelopes)
@@ -775,29 +869,58 @@ bool run_ls(mgpu_ctx *ctx, bool cs, int64_t n, int l, int maxrow, DCsr pat, DCsr
   // <5, 13> envelope is taken only when it cannot overflow: a J pattern of bandwidth b gives
   // |I| <= 4 b + 1 (b = 3 on the Hermite beam: 13 rows).
   const bool lanes = ctx->opt[MGPU_OPT_LS_GROUP] == 0;
-  for (int cfg = -3; cfg < 3; ++cfg)
+  // envelopes, tried in order: lane kernels <NJ, NI> (cfg < 0), then lane groups of 8 / 16 / 32
+  struct Env
   {
-    const int G = cfg == -3 ? 5 : (cfg == -2 ? 6 : (cfg == -1 ? 8 : (cfg == 0 ? 8 : (cfg == 1 ? 16 : 32))));
-    if (maxrow > G || (cfg < 0 && !lanes))
+    int nj;
+    bool lane;
+  };
+  static constexpr Env kEnv[] = {{5, true}, {6, true}, {8, true}, {10, true}, {10, true}, {8, false}, {16, false},
+                                 {32, false}};
+  for (int cfg = 0; cfg < 8; ++cfg)
+  {
+    const int G = kEnv[cfg].nj;
+    if (maxrow > G || (kEnv[cfg].lane && !lanes))
       continue;
-    if (cfg == -3 && !(pat_bw >= 0 && 4 * pat_bw + 1 <= 13))
+    if (cfg == 0 && !(pat_bw >= 0 && 4 * pat_bw + 1 <= 13))
       continue;
     MG_CUDA(cudaMemsetAsync(err.ptr, 0xff, sizeof(unsigned long long), ctx->stream));
     MG_CUDA(cudaMemsetAsync(ovf.ptr, 0, sizeof(int), ctx->stream));
     auto *ev = err.as<unsigned long long>();
-    if (cfg == -3)
+    switch (cfg)
+    {
+    case 0:
       launch_ls_lane<5, 13, 32>(ctx, cs, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev,
                                 ovf.as<int>());
-    else if (cfg == -2)
-      launch_ls_lane<6, 14>(ctx, cs, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev, ovf.as<int>());
-    else if (cfg == -1)
-      launch_ls_lane<8, 16>(ctx, cs, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev, ovf.as<int>());
-    else if (cfg == 0)
-      launch_ls<8, 16, 4>(ctx, cs, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev, ovf.as<int>());
-    else if (cfg == 1)
-      launch_ls<16, 32, 2>(ctx, cs, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev, ovf.as<int>());
-    else
-      launch_ls<32, 64, 1>(ctx, cs, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev, ovf.as<int>());
+      break;
+    case 1:
+      launch_ls_lane<6, 14>(ctx, cs, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev,
+                            ovf.as<int>());
+      break;
+    case 2:
+      launch_ls_lane<8, 16>(ctx, cs, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev,
+                            ovf.as<int>());
+      break;
+    case 3: // the A^2 pattern of the Hermite beam: |J| = 10, |I| = 14
+      launch_ls_lane<10, 14, 32>(ctx, cs, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev,
+                                 ovf.as<int>());
+      break;
+    case 4:
+      launch_ls_lane<10, 18, 32>(ctx, cs, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev,
+                                 ovf.as<int>());
+      break;
+    case 5:
+      launch_ls<8, 16, 4>(ctx, cs, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev,
+                          ovf.as<int>());
+      break;
+    case 6:
+      launch_ls<16, 32, 2>(ctx, cs, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev,
+                           ovf.as<int>());
+      break;
+    default:
+      launch_ls<32, 64, 1>(ctx, cs, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev,
+                           ovf.as<int>());
+    }
     if (after_launch) // caller's dependent work, queued behind the LS kernel before the read-back
       after_launch();
     // one synchronisation returns the error key, the overflow flag and the caller's extra value

@@ -1,32 +1,37 @@
-"""Aggregate ncu warp-stall samples per CUDA source line (ncu --page source --csv --print-source cuda,sass)."""
+"""Warp-stall samples and executed instructions per CUDA source line of one ncu report.
+usage: ncu -i REP --page source --csv --print-source cuda,sass > /tmp/src.csv; python tools/ncu_lines.py /tmp/src.csv [top]"""
 import csv
 import sys
 from collections import defaultdict
 
-rows = list(csv.reader(open(sys.argv[1])))
-top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
-agg = defaultdict(float)
+
+def num(x):
+    try:
+        return float(x)
+    except ValueError:
+        return 0.0
+
+
+rows = list(csv.reader(open(sys.argv[1], errors="replace")))
+top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+hdr = None
+agg = defaultdict(lambda: [0.0, 0.0])
 src = {}
-fname = "?"
-line = None
 for r in rows:
-    if not r:
+    if len(r) > 2 and r[0] == "Line No":
+        hdr = r
         continue
-    if r[0] == "File Path":
-        fname = r[1].split("/")[-1]
+    if hdr is None or len(r) < 9 or not r[0]:
         continue
-    if r[0] == "Line No":
+    try:
+        ln = int(r[0])
+    except ValueError:
         continue
-    if len(r) > 4:
-        if r[0].strip():
-            line = (fname, int(r[0]))
-            src[line] = r[1].strip()
-        try:
-            v = float(r[4] or 0)
-        except ValueError:
-            continue
-        if line is not None:
-            agg[line] += v
-tot = sum(agg.values()) or 1
-for k, v in sorted(agg.items(), key=lambda kv: -kv[1])[:top]:
-    print(f"{100 * v / tot:5.1f}% {k[0]}:{k[1]:<5} {src.get(k, '')[:100]}")
+    src[ln] = r[1]
+    agg[ln][0] += num(r[4])
+    agg[ln][1] += num(r[7])
+tot = sum(v[0] for v in agg.values()) or 1
+toti = sum(v[1] for v in agg.values()) or 1
+print(f"samples {tot:.0f}, warp instructions {toti:.3e}")
+for ln, v in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
+    print(f"{100 * v[0] / tot:5.1f}% stall  {100 * v[1] / toti:5.1f}% inst  {ln:5d} {src[ln][:90]}")

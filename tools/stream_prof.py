@@ -1,6 +1,6 @@
 """Per-phase clock64 breakdown of the streaming CG kernel (context option profile_phases; block 0,
 thread 0).  Usage: python tools/stream_prof.py [iters] [ne] [m] [points] [ls]
-(defaults: BASELINE configs[3] shape, 50 iterations; ls=1 adds an LS-SPAI factor per point)."""
+(defaults: BASELINE configs[3] shape, 50 iterations; ls = pattern + 1 adds an LS-SPAI factor per point: 1 A, 2 A^2, 18 A^2 colscale)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -12,7 +12,7 @@ ctx.set_option("profile_phases", 1)
 M, D, K = mg.model_hermite_device(ne, ctx=ctx)
 shifts = [10.0 ** (1 + 3 * i / (l - 1)) for i in range(l)] if l > 1 else [100.0]
 ops = mg.shifted_operators(M, D, K, shifts, ctx=ctx)
-chains = [[f.matrix] for f in mg.spai_ls_batched(ops, None, 0, ctx=ctx)] if ls else [[] for _ in ops]
+chains = [[f.matrix] for f in mg.spai_ls_batched(ops, None, ls - 1, ctx=ctx)] if ls else [[] for _ in ops]
 B = np.zeros((2 * ne, m))
 for c in range(m):
     B[2 * ((c + 1) * ne // m) - 2, c] = 1.0
