@@ -40,9 +40,9 @@ $(LIBDIR)/libmgpu.so: $(CU_OBJS) $(CPP_OBJS) | $(LIBDIR)
 # where /root/reference exists); the .so travels to the GPU box.
 shim: $(LIBDIR)/libmor_cuda.so
 
-$(LIBDIR)/libmor_cuda.so: $(PKG)/host/cuda_backend.cpp $(PKG)/host/cuda_backend.hpp $(LIBDIR)/libmgpu.so
-	$(CXX) -std=c++20 -O2 -fPIC -shared -Wall -Wextra -I$(REFINC) -Iinclude -I$(PKG)/host -o $@ $< \
-	  -L$(LIBDIR) -lmgpu -Wl,-rpath,'$$ORIGIN'
+$(LIBDIR)/libmor_cuda.so: $(PKG)/host/cuda_backend.cpp $(PKG)/host/capi.cpp $(PKG)/host/cuda_backend.hpp include/mor_cuda.h $(LIBDIR)/libmgpu.so
+	$(CXX) -std=c++20 -O2 -fPIC -shared -Wall -Wextra -I$(REFINC) -Iinclude -I$(PKG)/host -o $@ \
+	  $(PKG)/host/cuda_backend.cpp $(PKG)/host/capi.cpp -L$(LIBDIR) -lmgpu -Wl,-rpath,'$$ORIGIN'
 
 # Parity driver: reference CgBackend vs CudaCgBackend (checker, lives in oracle/_ref)
 parity: shim ref

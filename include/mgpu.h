@@ -114,6 +114,14 @@ int mgpu_ctx_get_option(const mgpu_ctx *ctx, int option, int64_t *value);
 /* Copies the 16 clock64 phase totals (MGPU_OPT_PROFILE_PHASES) and resets them. */
 int mgpu_phase_profile(mgpu_ctx *ctx, long long *out16);
 
+/* Device scratch buffers for callers that keep results on the device between calls (the drop-in
+ * backend's batched solve, read back point by point).  Stream-ordered on the context stream;
+ * mgpu_memcpy synchronises the stream before returning (MGPU_HOST: dst is host memory). */
+int mgpu_buffer_alloc(mgpu_ctx *ctx, size_t bytes, void **out);
+int mgpu_buffer_free(mgpu_ctx *ctx, void *p);
+int mgpu_memcpy_d2h(mgpu_ctx *ctx, void *host_dst, const void *dev_src, size_t bytes);
+int mgpu_memcpy_h2d(mgpu_ctx *ctx, void *dev_dst, const void *host_src, size_t bytes);
+
 /* ------------------------------------------------------------------ CSR I/O */
 
 /* Replaces constructing a mor::SparseMatrix (sparse.hpp:16-46).  The host

@@ -333,6 +333,49 @@ int mgpu_ctx_destroy(mgpu_ctx *ctx)
   return MGPU_OK;
 }
 
+int mgpu_buffer_alloc(mgpu_ctx *ctx, size_t bytes, void **out)
+{
+  if (ctx == nullptr || out == nullptr)
+    return MGPU_ERR_ARG;
+  return guard(ctx, [&] {
+    *out = nullptr;
+    if (bytes > 0)
+      MG_CUDA(mg_malloc(out, bytes, ctx->stream));
+  });
+}
+
+int mgpu_buffer_free(mgpu_ctx *ctx, void *p)
+{
+  if (ctx == nullptr)
+    return MGPU_ERR_ARG;
+  return guard(ctx, [&] {
+    if (p)
+      MG_CUDA(cudaFreeAsync(p, ctx->stream));
+  });
+}
+
+int mgpu_memcpy_d2h(mgpu_ctx *ctx, void *host_dst, const void *dev_src, size_t bytes)
+{
+  if (ctx == nullptr || (bytes > 0 && (host_dst == nullptr || dev_src == nullptr)))
+    return MGPU_ERR_ARG;
+  return guard(ctx, [&] {
+    if (bytes > 0)
+      MG_CUDA(cudaMemcpyAsync(host_dst, dev_src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    MG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int mgpu_memcpy_h2d(mgpu_ctx *ctx, void *dev_dst, const void *host_src, size_t bytes)
+{
+  if (ctx == nullptr || (bytes > 0 && (host_src == nullptr || dev_dst == nullptr)))
+    return MGPU_ERR_ARG;
+  return guard(ctx, [&] {
+    if (bytes > 0)
+      MG_CUDA(cudaMemcpyAsync(dev_dst, host_src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    MG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
 int mgpu_ctx_synchronize(mgpu_ctx *ctx)
 {
   return guard(ctx, [&] { MG_CUDA(cudaStreamSynchronize(ctx->stream)); });

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstring>
 #include <stdexcept>
 #include <string>
 
@@ -68,9 +69,10 @@ SparseMatrix download(mgpu_ctx *ctx, const mgpu_csr *m)
 double seconds_since(Clock::time_point t0) { return std::chrono::duration<double>(Clock::now() - t0).count(); }
 
 // One batched mgpu_cg_solve for `l` points sharing chain length z.
+// status_out: per (point, column) status instead of raising the first breakdown.
 std::vector<BlockSolveResult> solve_points(mgpu_ctx *ctx, const std::vector<mgpu_csr *> &A,
                                            const std::vector<mgpu_csr *> &chains_flat, int z, const DenseMatrix &B,
-                                           double rtol, std::int64_t maxit)
+                                           double rtol, std::int64_t maxit, std::vector<int> *status_out = nullptr)
 {
   const int l = static_cast<int>(A.size());
   const int64_t n = B.nrows, m = B.ncols;
@@ -86,8 +88,12 @@ std::vector<BlockSolveResult> solve_points(mgpu_ctx *ctx, const std::vector<mgpu
   out.converged = conv.data();
   out.status = status.data();
   out.breakdown_iteration = bd.data();
-  check(ctx, mgpu_cg_solve(ctx, l, A.data(), z, chains_flat.empty() ? nullptr : chains_flat.data(), n, m,
-                           B.values.data(), 0, rtol, maxit, MGPU_HOST, &out));
+  const int st = mgpu_cg_solve(ctx, l, A.data(), z, chains_flat.empty() ? nullptr : chains_flat.data(), n, m,
+                               B.values.data(), 0, rtol, maxit, MGPU_HOST, &out);
+  if (!(status_out && st == MGPU_ERR_BREAKDOWN))
+    check(ctx, st);
+  if (status_out)
+    *status_out = status;
   std::vector<BlockSolveResult> res(static_cast<std::size_t>(l));
   for (int p = 0; p < l; ++p)
   {
@@ -412,19 +418,54 @@ std::vector<double> arnoldi_deflate(Device &dev, DenseMatrix &X, std::span<const
 // ------------------------------------------------------------------ backend
 struct CudaCgBackend::State
 {
-  AirgaConfig cfg;
+  CudaSolveSettings cfg;
   CudaBackendOptions opt;
   cuda::Device dev;
   int64_t n = 0;
-  const SecondOrderSystem *sys = nullptr;
   cuda::DeviceMatrix M, D, K;
   std::vector<cuda::DeviceMatrix> prev_ops;            // operators of the prepared iteration
   std::vector<std::vector<cuda::DeviceMatrix>> chains; // per point, newest first
+  // speculative batched solve of sys.F (CudaBackendOptions::speculative_solve): X, recurrence and
+  // true residuals of every point stay on the device ([array][point][column][row]) until
+  // solve(i, F) reads point i back
+  std::vector<double> spec_rhs; // the F it was solved for
+  int64_t spec_m = 0;
+  void *spec_dev = nullptr;
+  std::vector<int64_t> spec_it;
+  std::vector<int> spec_conv;
+  std::vector<char> spec_ready; // per point: results valid and not yet handed out
 
-  State(const AirgaConfig &c, const CudaBackendOptions &o) : cfg(c), opt(o), dev(o.device) {}
+  State(const CudaSolveSettings &c, const CudaBackendOptions &o) : cfg(c), opt(o), dev(o.device) {}
+  ~State() { drop_spec(); }
+  void drop_spec()
+  {
+    if (spec_dev)
+      mgpu_buffer_free(dev.ctx(), spec_dev);
+    spec_dev = nullptr;
+    spec_ready.clear();
+  }
+  int64_t maxit() const { return opt.maxit_override > 0 ? opt.maxit_override : cfg.cg_maxit_factor * n; }
 };
 
+CudaSolveSettings settings_of(const AirgaConfig &cfg)
+{
+  CudaSolveSettings s;
+  s.solver = cfg.solver;
+  s.spai_tol = cfg.spai_tol;
+  s.spai_max_col_iters = cfg.spai_max_col_iters;
+  s.spai_mode = cfg.spai_mode;
+  s.cg_rtol = cfg.cg_rtol;
+  s.cg_maxit_factor = cfg.cg_maxit_factor;
+  s.update_start_iteration = cfg.update_start_iteration;
+  return s;
+}
+
 CudaCgBackend::CudaCgBackend(const AirgaConfig &cfg, const CudaBackendOptions &opt)
+  : st_(std::make_unique<State>(settings_of(cfg), opt))
+{
+}
+
+CudaCgBackend::CudaCgBackend(const CudaSolveSettings &cfg, const CudaBackendOptions &opt)
   : st_(std::make_unique<State>(cfg, opt))
 {
 }
@@ -438,12 +479,29 @@ void CudaCgBackend::prepare(const SecondOrderSystem &sys, const std::vector<doub
   State &s = *st_;
   mgpu_ctx *ctx = s.dev.ctx();
   s.n = sys.order();
-  if (s.sys != &sys || !s.M.get())
+  s.drop_spec();
+  // M, D, K are uploaded on every prepare, as the reference rebuilds shifted_operator(sys, s) from
+  // sys on every prepare (airga.cpp:110-116): a caller may edit sys between outer iterations.
   {
-    s.M = cuda::DeviceMatrix(s.dev, sys.M);
-    s.D = cuda::DeviceMatrix(s.dev, sys.D);
-    s.K = cuda::DeviceMatrix(s.dev, sys.K);
-    s.sys = &sys;
+    const SparseMatrix *src[3] = {&sys.M, &sys.D, &sys.K};
+    int64_t nr[3], nc[3], nz[3];
+    const int64_t *rp[3];
+    const int32_t *ci[3];
+    const double *va[3];
+    for (int q = 0; q < 3; ++q)
+    {
+      nr[q] = src[q]->nrows;
+      nc[q] = src[q]->ncols;
+      nz[q] = src[q]->nnz();
+      rp[q] = src[q]->row_ptr.data();
+      ci[q] = src[q]->col_idx.data();
+      va[q] = src[q]->values.data();
+    }
+    mgpu_csr *h[3] = {nullptr, nullptr, nullptr};
+    check(ctx, mgpu_csr_upload_batch(ctx, 3, nr, nc, nz, rp, ci, va, h));
+    s.M = cuda::DeviceMatrix(s.dev, h[0]);
+    s.D = cuda::DeviceMatrix(s.dev, h[1]);
+    s.K = cuda::DeviceMatrix(s.dev, h[2]);
   }
   const int l = static_cast<int>(points.size());
   std::vector<mgpu_csr *> raw(static_cast<std::size_t>(l), nullptr);
@@ -534,6 +592,57 @@ void CudaCgBackend::prepare(const SecondOrderSystem &sys, const std::vector<doub
     }
   }
   s.prev_ops = std::move(fresh);
+  // speculative batched solve of sys.F for every point (one kernel; zeroth_moments asks for
+  // exactly these next).  A breakdown is left to the on-demand path, which raises it with the
+  // reference's payload; the other points keep their results.
+  const int64_t m = sys.F.ncols;
+  if (s.opt.speculative_solve && l > 0 && m > 0 && sys.F.nrows == s.n)
+  {
+    std::vector<mgpu_csr *> A, flat;
+    const std::size_t z = s.chains.empty() ? 0 : s.chains[0].size();
+    bool uniform = true;
+    for (int i = 0; i < l; ++i)
+    {
+      A.push_back(s.prev_ops[static_cast<std::size_t>(i)].get());
+      const std::size_t zi = s.chains.empty() ? 0 : s.chains[static_cast<std::size_t>(i)].size();
+      uniform = uniform && zi == z;
+      if (!s.chains.empty())
+        for (const auto &f : s.chains[static_cast<std::size_t>(i)])
+          flat.push_back(f.get());
+    }
+    if (uniform)
+    {
+      const std::size_t blk = static_cast<std::size_t>(s.n * m), cnt = static_cast<std::size_t>(l) * m;
+      check(ctx, mgpu_buffer_alloc(ctx, (3 * blk * l + blk) * sizeof(double), &s.spec_dev));
+      auto *base = static_cast<double *>(s.spec_dev);
+      double *Bd = base + 3 * blk * l; // the rhs block, uploaded once
+      check(ctx, mgpu_memcpy_h2d(ctx, Bd, sys.F.values.data(), blk * sizeof(double)));
+      std::vector<int> status(cnt);
+      std::vector<int64_t> bd(cnt);
+      s.spec_it.assign(cnt, 0);
+      s.spec_conv.assign(cnt, 0);
+      mgpu_cg_out out{};
+      out.X = base;
+      out.recurrence = base + blk * l;
+      out.true_res = base + 2 * blk * l;
+      out.iterations = s.spec_it.data();
+      out.converged = s.spec_conv.data();
+      out.status = status.data();
+      out.breakdown_iteration = bd.data();
+      // the results stay in spec_dev until solve(i, F) reads point i back
+      const int st = mgpu_cg_solve(ctx, l, A.data(), static_cast<int>(z), flat.empty() ? nullptr : flat.data(), s.n,
+                                   m, Bd, 0, s.cfg.cg_rtol, s.maxit(), MGPU_DEVICE, &out);
+      if (st != MGPU_OK && st != MGPU_ERR_BREAKDOWN)
+        check(ctx, st);
+      s.spec_ready.assign(static_cast<std::size_t>(l), 1);
+      for (int i = 0; i < l; ++i)
+        for (int64_t c = 0; c < m; ++c)
+          if (status[static_cast<std::size_t>(i * m + c)] != MGPU_OK)
+            s.spec_ready[static_cast<std::size_t>(i)] = 0; // the on-demand solve raises the breakdown
+      s.spec_rhs = sys.F.values;
+      s.spec_m = m;
+    }
+  }
 }
 
 // airga.cpp:166-181
@@ -544,12 +653,60 @@ BlockSolveResult CudaCgBackend::solve(std::int64_t point_index, const DenseMatri
     throw std::out_of_range("CudaCgBackend::solve: point index");
   if (rhs.nrows != s.n)
     throw ArgumentError("block_solve: right-hand-side rows do not match the operator dimension");
+  const std::size_t pi = static_cast<std::size_t>(point_index);
+  if (cached(point_index, rhs))
+  {
+    BlockSolveResult r;
+    r.X = DenseMatrix(s.n, rhs.ncols);
+    r.recurrence_residuals = DenseMatrix(s.n, rhs.ncols);
+    r.true_residuals = DenseMatrix(s.n, rhs.ncols);
+    r.iterations.assign(static_cast<std::size_t>(rhs.ncols), 0);
+    take_cached(point_index, r.X.values.data(), r.recurrence_residuals.values.data(), r.true_residuals.values.data(),
+                r.iterations.data(), &r.all_converged);
+    return r;
+  }
   std::vector<mgpu_csr *> chain;
   if (!s.chains.empty())
-    for (const auto &f : s.chains[static_cast<std::size_t>(point_index)])
+    for (const auto &f : s.chains[pi])
       chain.push_back(f.get());
-  return solve_points(s.dev.ctx(), {s.prev_ops[static_cast<std::size_t>(point_index)].get()}, chain,
-                      static_cast<int>(chain.size()), rhs, s.cfg.cg_rtol, s.cfg.cg_maxit_factor * s.n)[0];
+  return solve_points(s.dev.ctx(), {s.prev_ops[pi].get()}, chain, static_cast<int>(chain.size()), rhs, s.cfg.cg_rtol,
+                      s.maxit())[0];
+}
+
+bool CudaCgBackend::cached(std::int64_t point_index, const DenseMatrix &rhs) const
+{
+  return rhs.nrows == st_->n && cached(point_index, rhs.values.data(), rhs.ncols);
+}
+
+bool CudaCgBackend::cached(std::int64_t point_index, const double *rhs, std::int64_t m) const
+{
+  const State &s = *st_;
+  const std::size_t pi = static_cast<std::size_t>(point_index);
+  return point_index >= 0 && pi < s.spec_ready.size() && s.spec_ready[pi] && m == s.spec_m &&
+         std::memcmp(rhs, s.spec_rhs.data(), sizeof(double) * s.spec_rhs.size()) == 0;
+}
+
+void CudaCgBackend::take_cached(std::int64_t point_index, double *X, double *REC, double *TR, std::int64_t *iterations,
+                                bool *all_converged)
+{
+  State &s = *st_;
+  const std::size_t pi = static_cast<std::size_t>(point_index), l = s.spec_ready.size();
+  const std::size_t blk = static_cast<std::size_t>(s.n * s.spec_m);
+  const auto *base = static_cast<const double *>(s.spec_dev);
+  double *dst[3] = {X, REC, TR};
+  for (int q = 0; q < 3; ++q)
+    if (dst[q])
+      check(s.dev.ctx(), mgpu_memcpy_d2h(s.dev.ctx(), dst[q], base + (q * l + pi) * blk, blk * sizeof(double)));
+  bool conv = true;
+  for (int64_t c = 0; c < s.spec_m; ++c)
+  {
+    if (iterations)
+      iterations[c] = s.spec_it[pi * s.spec_m + c];
+    conv = conv && s.spec_conv[pi * s.spec_m + c] != 0;
+  }
+  if (all_converged)
+    *all_converged = conv;
+  s.spec_ready[pi] = 0; // handed out once; a repeated request solves again
 }
 
 std::vector<BlockSolveResult> CudaCgBackend::solve_all(const DenseMatrix &rhs)
@@ -575,7 +732,7 @@ std::vector<BlockSolveResult> CudaCgBackend::solve_all(const DenseMatrix &rhs)
       out.push_back(solve(i, rhs));
     return out;
   }
-  return solve_points(s.dev.ctx(), A, flat, static_cast<int>(z), rhs, s.cfg.cg_rtol, s.cfg.cg_maxit_factor * s.n);
+  return solve_points(s.dev.ctx(), A, flat, static_cast<int>(z), rhs, s.cfg.cg_rtol, s.maxit());
 }
 
 std::unique_ptr<SolveBackend> make_cuda_backend(const AirgaConfig &cfg, const CudaBackendOptions &opt)

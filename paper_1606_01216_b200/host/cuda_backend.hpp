@@ -138,13 +138,37 @@ struct CudaBackendOptions
 {
   int device = 0;
   cuda::SpaiAlgorithm algorithm = cuda::SpaiAlgorithm::mr;
-  int ls_pattern = 0;
+  int ls_pattern = 0; ///< MGPU_PATTERN_A / _A2, optionally | MGPU_LS_COLSCALE
+  /// prepare() also solves sys.F for every prepared point in ONE batched kernel and keeps the
+  /// results; solve(i, rhs) returns them when rhs is sys.F (bitwise), which is what
+  /// zeroth_moments asks for right after prepare (airga.cpp:374-381).  Any other rhs is solved
+  /// on demand, as before.
+  bool speculative_solve = true;
+  /// > 0: CG iteration budget in place of cg_maxit_factor * n (fixed-budget benchmarking; the
+  /// factor is an integer multiple of n in AirgaConfig).
+  std::int64_t maxit_override = 0;
 };
+
+/// The AirgaConfig fields the CG backend reads (airga.hpp:40-69).  Kept separately so that the
+/// backend can be built without an AirgaConfig, whose default initial_points call into the
+/// reference library (the C API in include/mor_cuda.h does this).
+struct CudaSolveSettings
+{
+  AirgaConfig::Solver solver = AirgaConfig::Solver::cg_spai;
+  double spai_tol = 0.01;
+  std::int64_t spai_max_col_iters = 50;
+  SpaiOptions::Mode spai_mode = SpaiOptions::Mode::sequential;
+  double cg_rtol = 1e-10;
+  std::int64_t cg_maxit_factor = 10;
+  std::int64_t update_start_iteration = 3;
+};
+CudaSolveSettings settings_of(const AirgaConfig &cfg);
 
 class CudaCgBackend final : public SolveBackend
 {
 public:
   CudaCgBackend(const AirgaConfig &cfg, const CudaBackendOptions &opt = {});
+  CudaCgBackend(const CudaSolveSettings &cfg, const CudaBackendOptions &opt = {});
   ~CudaCgBackend() override;
 
   void prepare(const SecondOrderSystem &sys, const std::vector<double> &points, std::int64_t outer,
@@ -155,6 +179,14 @@ public:
   /// Every prepared point against the same rhs block in one batched kernel
   /// (the reference solves point by point, airga.cpp:374-405).
   std::vector<BlockSolveResult> solve_all(const DenseMatrix &rhs);
+
+  /// True when solve(point_index, rhs) would be served from prepare's batched solve.
+  bool cached(std::int64_t point_index, const DenseMatrix &rhs) const;
+  bool cached(std::int64_t point_index, const double *rhs, std::int64_t m) const; ///< rhs: n x m column-major
+  /// Reads that result straight into caller buffers (each optional; n x m column-major) and
+  /// marks it handed out -- the C API's path, one device-to-host copy per array.
+  void take_cached(std::int64_t point_index, double *X, double *REC, double *TR, std::int64_t *iterations,
+                   bool *all_converged);
 
 private:
   struct State;

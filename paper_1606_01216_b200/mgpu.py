@@ -36,6 +36,7 @@ EXPORTED = [
     "mgpu_model_chain", "mgpu_model_hermite", "mgpu_host_free", "mgpu_thin_qr", "mgpu_project_reduce", "mgpu_project_reduce_slab",
     "mgpu_arnoldi_deflate", "mgpu_model_hermite_device", "mgpu_csr_write", "mgpu_csr_read", "mgpu_shifted_solve",
     "mgpu_csr_upload_batch", "mgpu_ctx_set_option", "mgpu_ctx_get_option", "mgpu_phase_profile",
+    "mgpu_buffer_alloc", "mgpu_buffer_free", "mgpu_memcpy_d2h", "mgpu_memcpy_h2d",
 ]
 
 # mgpu.h mgpu_option

@@ -11,10 +11,10 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _declared(header):
+def _declared(header, prefix="mgpu_"):
     src = open(os.path.join(ROOT, header)).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(mgpu_[a-z0-9_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(" + prefix + r"[a-z0-9_]+)\s*\(", src)))
 
 
 def _exported(so):
@@ -31,6 +31,20 @@ def test_libmgpu_exports_every_declared_symbol():
     assert not missing, missing
     assert sorted(mg.mgpu.EXPORTED) == declared
     lib = ctypes.CDLL(so)
+    for s in declared:
+        getattr(lib, s)
+
+
+def test_plugin_exports_every_declared_symbol():
+    """include/mor_cuda.h: the drop-in SolveBackend's C entry points (libmor_cuda.so)."""
+    from paper_1606_01216_b200 import plugin
+    if not os.path.exists(plugin.LIB_PATH):
+        pytest.skip("libmor_cuda.so needs the reference headers (make shim)")
+    declared = _declared("include/mor_cuda.h", "mor_cuda_")
+    missing = [s for s in declared if s not in _exported(plugin.LIB_PATH)]
+    assert not missing, missing
+    assert sorted(plugin.EXPORTED) == declared
+    lib = plugin.lib()
     for s in declared:
         getattr(lib, s)
 
