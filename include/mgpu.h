@@ -325,6 +325,35 @@ int mgpu_project_reduce_slab(mgpu_ctx *ctx, const mgpu_csr *M, const mgpu_csr *D
 int mgpu_arnoldi_deflate(mgpu_ctx *ctx, int64_t len, double *X, int nblocks, const double *const *blocks,
                          double *gammas, mgpu_memkind where);
 
+/* ------------------------------------------------------------------ NVLink / NCCL data plane */
+
+/* One NCCL rank per context (one process per GPU).  Rank 0 creates the id (128 bytes) and the
+ * caller distributes it (torch.distributed, MPI, a file); every rank then calls mgpu_comm_init. */
+int mgpu_comm_unique_id(void *id128);
+int mgpu_comm_init(mgpu_ctx *ctx, const void *id128, int nranks, int rank);
+int mgpu_comm_destroy(mgpu_ctx *ctx);
+/* In-place sum over ranks of a device buffer (synchronous). */
+int mgpu_comm_allreduce_sum(mgpu_ctx *ctx, double *buf, int64_t count);
+/* This rank's balanced row slab [row0, row0 + p) of an n-row basis and its halo-extended range
+ * [ext0, ext0 + next) (h rows each side, clipped). */
+int mgpu_comm_rows(mgpu_ctx *ctx, int64_t n, int64_t h, int64_t *row0, int64_t *p, int64_t *ext0, int64_t *next);
+/* Arnoldi-block redistribution after the shift-sharded solves: this rank holds the full-length
+ * columns col_ids[c_local] (host ids, global) of an n x R block in X_local (device, n x c_local
+ * column-major); Vext (device, next x R column-major) receives rows [ext0, ext0 + next) of all R
+ * columns.  Grouped ncclSend / ncclRecv, no host staging. */
+int mgpu_comm_columns_to_rows(mgpu_ctx *ctx, int64_t n, int64_t h, int64_t c_local, const int64_t *col_ids,
+                              const double *X_local, int64_t R, double *Vext);
+/* airga.cpp:485-500 project_reduce over the row-distributed basis: M, D, K are the full operators
+ * (replicated), Vext this rank's extended slab (h >= the operators' bandwidth), F (n x m) and Cp, Cv
+ * (q x n) the full input / output maps in `where` memory.  Slab partials on the device
+ * (mgpu_project_reduce_slab) + one ncclAllReduce; every rank receives the reduced matrices. */
+int mgpu_comm_project_reduce(mgpu_ctx *ctx, const mgpu_csr *M, const mgpu_csr *D, const mgpu_csr *K, int64_t h,
+                             int64_t r, const double *Vext, int64_t m, const double *F, int64_t q, const double *Cp,
+                             const double *Cv, double *Mh, double *Dh, double *Kh, double *Fh, double *Cph,
+                             double *Cvh, mgpu_memkind where);
+/* max |i - j| over the stored entries (the halo the projection needs). */
+int mgpu_csr_bandwidth(mgpu_ctx *ctx, const mgpu_csr *a, int64_t *bw);
+
 #ifdef __cplusplus
 }
 #endif

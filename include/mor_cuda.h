@@ -34,6 +34,12 @@ int mor_cuda_backend_create(int device, int solver, int algorithm, int ls_patter
                             int64_t spai_max_col_iters, int spai_mode, double cg_rtol, int64_t cg_maxit_factor,
                             int64_t maxit_override, int64_t update_start_iteration, int speculative,
                             mor_cuda_backend **out, char *msg, size_t cap);
+/* Shift sharding over several devices in one process (mor::MultiDeviceCgBackend): point i is
+ * prepared and solved on devices[i % ndev]; the devices prepare concurrently. */
+int mor_cuda_backend_create_multi(int ndev, const int *devices, int solver, int algorithm, int ls_pattern,
+                                  double spai_tol, int64_t spai_max_col_iters, int spai_mode, double cg_rtol,
+                                  int64_t cg_maxit_factor, int64_t maxit_override, int64_t update_start_iteration,
+                                  int speculative, mor_cuda_backend **out, char *msg, size_t cap);
 void mor_cuda_backend_destroy(mor_cuda_backend *b);
 
 /* The SecondOrderSystem the backend prepares (system.hpp:15-33): M, D, K as CSR (n x n), F as

@@ -306,6 +306,8 @@ int mgpu_ctx_destroy(mgpu_ctx *ctx)
     return MGPU_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  if (ctx->nccl)
+    mgpu_comm_destroy(ctx);
   if (ctx->ev0)
     cudaEventDestroy(ctx->ev0);
   if (ctx->ev1)

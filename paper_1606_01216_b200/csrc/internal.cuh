@@ -138,6 +138,8 @@ struct mgpu_ctx
   long long *prof_dev = nullptr; // diagnostics: per-phase clock64 totals of the CG kernels (MGPU_OPT_PROFILE_PHASES)
   int64_t opt[MGPU_OPT_COUNT] = {1, 0, 0, 0, 0, 0, 1, 0, 0, 0}; // mgpu_ctx_set_option
   void *blas = nullptr;          // cublasHandle_t, created on first dense product (project.cu)
+  void *nccl = nullptr;          // ncclComm_t (mgpu_comm_init), one rank per context
+  int nranks = 1, rank = 0;
   cudaEvent_t phase_ev[4] = {nullptr, nullptr, nullptr, nullptr}; // mgpu_shifted_solve phase timing (lazy)
   void *pin = nullptr;           // pinned host staging for small device -> host reads (grown on demand)
   size_t pin_bytes = 0;
@@ -197,6 +199,8 @@ int guard(mgpu_ctx *ctx, F &&body)
 {
   try
   {
+    if (ctx) // a context may be driven from any host thread (one per device in the multi-device backend)
+      MG_CUDA(cudaSetDevice(ctx->device));
     body();
     if (ctx)
     {

@@ -15,7 +15,9 @@
 
 struct mor_cuda_backend
 {
-  std::unique_ptr<mor::CudaCgBackend> impl;
+  std::unique_ptr<mor::CudaCgBackend> impl;         // one device
+  std::unique_ptr<mor::MultiDeviceCgBackend> multi; // or shift-sharded over several
+  mor::SolveBackend &backend() { return multi ? static_cast<mor::SolveBackend &>(*multi) : *impl; }
   mor::SecondOrderSystem sys;
   int64_t n = 0;
 };
@@ -83,32 +85,60 @@ mor::SparseMatrix csr(int64_t n, int64_t nnz, const int64_t *rp, const int32_t *
 
 extern "C" {
 
+namespace
+{
+void settings(int solver, int algorithm, int ls_pattern, double spai_tol, int64_t spai_max_col_iters, int spai_mode,
+              double cg_rtol, int64_t cg_maxit_factor, int64_t maxit_override, int64_t update_start_iteration,
+              int speculative, mor::CudaSolveSettings &s, mor::CudaBackendOptions &o)
+{
+  if (solver < 1 || solver > 3 || algorithm < 0 || algorithm > 1)
+    throw mor::ArgumentError("mor_cuda_backend_create: bad argument");
+  s.solver = solver == 1   ? mor::AirgaConfig::Solver::cg_plain
+             : solver == 2 ? mor::AirgaConfig::Solver::cg_spai
+                           : mor::AirgaConfig::Solver::cg_spai_update;
+  s.spai_tol = spai_tol;
+  s.spai_max_col_iters = spai_max_col_iters;
+  s.spai_mode = spai_mode == 0 ? mor::SpaiOptions::Mode::sequential : mor::SpaiOptions::Mode::frozen;
+  s.cg_rtol = cg_rtol;
+  s.cg_maxit_factor = cg_maxit_factor;
+  s.update_start_iteration = update_start_iteration;
+  o.algorithm = algorithm == 1 ? mor::cuda::SpaiAlgorithm::ls : mor::cuda::SpaiAlgorithm::mr;
+  o.ls_pattern = ls_pattern;
+  o.speculative_solve = speculative != 0;
+  o.maxit_override = maxit_override;
+}
+} // namespace
+
 int mor_cuda_backend_create(int device, int solver, int algorithm, int ls_pattern, double spai_tol,
                             int64_t spai_max_col_iters, int spai_mode, double cg_rtol, int64_t cg_maxit_factor,
                             int64_t maxit_override, int64_t update_start_iteration, int speculative,
                             mor_cuda_backend **out, char *msg, size_t cap)
 {
+  return mor_cuda_backend_create_multi(1, &device, solver, algorithm, ls_pattern, spai_tol, spai_max_col_iters,
+                                       spai_mode, cg_rtol, cg_maxit_factor, maxit_override, update_start_iteration,
+                                       speculative, out, msg, cap);
+}
+
+int mor_cuda_backend_create_multi(int ndev, const int *devices, int solver, int algorithm, int ls_pattern,
+                                  double spai_tol, int64_t spai_max_col_iters, int spai_mode, double cg_rtol,
+                                  int64_t cg_maxit_factor, int64_t maxit_override, int64_t update_start_iteration,
+                                  int speculative, mor_cuda_backend **out, char *msg, size_t cap)
+{
   return guarded(msg, cap, [&] {
-    if (!out || solver < 1 || solver > 3 || algorithm < 0 || algorithm > 1)
+    if (!out || ndev < 1 || !devices)
       throw mor::ArgumentError("mor_cuda_backend_create: bad argument");
     mor::CudaSolveSettings s;
-    s.solver = solver == 1   ? mor::AirgaConfig::Solver::cg_plain
-               : solver == 2 ? mor::AirgaConfig::Solver::cg_spai
-                             : mor::AirgaConfig::Solver::cg_spai_update;
-    s.spai_tol = spai_tol;
-    s.spai_max_col_iters = spai_max_col_iters;
-    s.spai_mode = spai_mode == 0 ? mor::SpaiOptions::Mode::sequential : mor::SpaiOptions::Mode::frozen;
-    s.cg_rtol = cg_rtol;
-    s.cg_maxit_factor = cg_maxit_factor;
-    s.update_start_iteration = update_start_iteration;
     mor::CudaBackendOptions o;
-    o.device = device;
-    o.algorithm = algorithm == 1 ? mor::cuda::SpaiAlgorithm::ls : mor::cuda::SpaiAlgorithm::mr;
-    o.ls_pattern = ls_pattern;
-    o.speculative_solve = speculative != 0;
-    o.maxit_override = maxit_override;
+    settings(solver, algorithm, ls_pattern, spai_tol, spai_max_col_iters, spai_mode, cg_rtol, cg_maxit_factor,
+             maxit_override, update_start_iteration, speculative, s, o);
     auto b = std::make_unique<mor_cuda_backend>();
-    b->impl = std::make_unique<mor::CudaCgBackend>(s, o);
+    if (ndev == 1)
+    {
+      o.device = devices[0];
+      b->impl = std::make_unique<mor::CudaCgBackend>(s, o);
+    }
+    else
+      b->multi = std::make_unique<mor::MultiDeviceCgBackend>(s, o, std::vector<int>(devices, devices + ndev));
     *out = b.release();
   });
 }
@@ -141,7 +171,7 @@ int mor_cuda_backend_prepare(mor_cuda_backend *b, int l, const double *points, i
     if (!b || l < 0 || (l > 0 && !points))
       throw mor::ArgumentError("mor_cuda_backend_prepare: bad argument");
     std::vector<mor::PrecondRecord> recs;
-    b->impl->prepare(b->sys, std::vector<double>(points, points + l), outer, &recs);
+    b->backend().prepare(b->sys, std::vector<double>(points, points + l), outer, &recs);
     if (record_seconds)
       for (const auto &r : recs)
         if (r.point_index >= 0 && r.point_index < l)
@@ -155,17 +185,25 @@ int mor_cuda_backend_solve(mor_cuda_backend *b, int64_t point_index, int64_t m, 
   return guarded(msg, cap, [&] {
     if (!b || !rhs || m < 0)
       throw mor::ArgumentError("mor_cuda_backend_solve: bad argument");
-    if (b->impl->cached(point_index, rhs, m)) // prepare's batched solve: one device -> host copy per array
+    mor::CudaCgBackend *part = b->impl.get();
+    int64_t local = point_index;
+    if (b->multi && point_index >= 0)
+    {
+      const auto own = b->multi->owner(point_index);
+      part = &b->multi->part(own.first);
+      local = own.second;
+    }
+    if (part->cached(local, rhs, m)) // prepare's batched solve: one device -> host copy per array
     {
       bool conv = false;
-      b->impl->take_cached(point_index, X, REC, TR, iterations, &conv);
+      part->take_cached(local, X, REC, TR, iterations, &conv);
       if (all_converged)
         *all_converged = conv ? 1 : 0;
       return;
     }
     mor::DenseMatrix B(b->n, m);
     std::memcpy(B.values.data(), rhs, sizeof(double) * static_cast<size_t>(b->n * m));
-    mor::BlockSolveResult r = b->impl->solve(point_index, B);
+    mor::BlockSolveResult r = b->backend().solve(point_index, B);
     const size_t bytes = sizeof(double) * static_cast<size_t>(b->n * m);
     if (X)
       std::memcpy(X, r.X.values.data(), bytes);

@@ -10,6 +10,7 @@
 #include <chrono>
 #include <cstring>
 #include <stdexcept>
+#include <thread>
 #include <string>
 
 #include "mgpu.h"
@@ -733,6 +734,84 @@ std::vector<BlockSolveResult> CudaCgBackend::solve_all(const DenseMatrix &rhs)
     return out;
   }
   return solve_points(s.dev.ctx(), A, flat, static_cast<int>(z), rhs, s.cfg.cg_rtol, s.maxit());
+}
+
+// ------------------------------------------------------------------ multi-device backend
+MultiDeviceCgBackend::MultiDeviceCgBackend(const CudaSolveSettings &cfg, const CudaBackendOptions &opt,
+                                           std::vector<int> devices)
+{
+  if (devices.empty())
+    throw ArgumentError("MultiDeviceCgBackend: no devices");
+  for (int d : devices)
+  {
+    CudaBackendOptions o = opt;
+    o.device = d;
+    parts_.push_back(std::make_unique<CudaCgBackend>(cfg, o));
+  }
+}
+
+MultiDeviceCgBackend::MultiDeviceCgBackend(const AirgaConfig &cfg, const CudaBackendOptions &opt,
+                                           std::vector<int> devices)
+  : MultiDeviceCgBackend(settings_of(cfg), opt, std::move(devices))
+{
+}
+
+MultiDeviceCgBackend::~MultiDeviceCgBackend() = default;
+
+std::pair<std::size_t, std::int64_t> MultiDeviceCgBackend::owner(std::int64_t point_index) const
+{
+  const auto N = static_cast<std::int64_t>(parts_.size());
+  return {static_cast<std::size_t>(point_index % N), point_index / N};
+}
+
+void MultiDeviceCgBackend::prepare(const SecondOrderSystem &sys, const std::vector<double> &points,
+                                   std::int64_t outer, std::vector<PrecondRecord> *records)
+{
+  const std::size_t N = parts_.size();
+  std::vector<std::vector<double>> mine(N);
+  for (std::size_t i = 0; i < points.size(); ++i)
+    mine[i % N].push_back(points[i]);
+  std::vector<std::vector<PrecondRecord>> recs(N);
+  std::vector<std::exception_ptr> err(N);
+  std::vector<std::thread> th;
+  for (std::size_t d = 0; d < N; ++d)
+    th.emplace_back([&, d] {
+      try
+      {
+        parts_[d]->prepare(sys, mine[d], outer, &recs[d]);
+      }
+      catch (...)
+      {
+        err[d] = std::current_exception();
+      }
+    });
+  for (auto &t : th)
+    t.join();
+  for (std::size_t d = 0; d < N; ++d) // the lowest device slot's error, as a serial loop would meet first
+    if (err[d])
+      std::rethrow_exception(err[d]);
+  if (records) // global point order, as CgBackend::prepare records them
+  {
+    std::vector<PrecondRecord> all;
+    for (std::size_t d = 0; d < N; ++d)
+      for (PrecondRecord r : recs[d])
+      {
+        r.point_index = r.point_index * static_cast<std::int64_t>(N) + static_cast<std::int64_t>(d);
+        all.push_back(r);
+      }
+    std::sort(all.begin(), all.end(), [](const PrecondRecord &a, const PrecondRecord &b) {
+      return a.point_index < b.point_index;
+    });
+    records->insert(records->end(), all.begin(), all.end());
+  }
+}
+
+BlockSolveResult MultiDeviceCgBackend::solve(std::int64_t point_index, const DenseMatrix &rhs)
+{
+  if (point_index < 0)
+    throw std::out_of_range("MultiDeviceCgBackend::solve: point index");
+  const auto [d, local] = owner(point_index);
+  return parts_[d]->solve(local, rhs);
 }
 
 std::unique_ptr<SolveBackend> make_cuda_backend(const AirgaConfig &cfg, const CudaBackendOptions &opt)

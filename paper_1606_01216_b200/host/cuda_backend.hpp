@@ -193,6 +193,31 @@ private:
   std::unique_ptr<State> st_;
 };
 
+/// Shift sharding inside one process: one CudaCgBackend -- one context -- per
+/// listed device; prepare deals the points out round-robin (point i to device i mod N) and prepares
+/// every device concurrently (one host thread each), solve(i, rhs) runs on point i's device.  The
+/// shifted systems are independent, so nothing crosses devices on the solve path.
+class MultiDeviceCgBackend final : public SolveBackend
+{
+public:
+  MultiDeviceCgBackend(const CudaSolveSettings &cfg, const CudaBackendOptions &opt, std::vector<int> devices);
+  MultiDeviceCgBackend(const AirgaConfig &cfg, const CudaBackendOptions &opt, std::vector<int> devices);
+  ~MultiDeviceCgBackend() override;
+
+  void prepare(const SecondOrderSystem &sys, const std::vector<double> &points, std::int64_t outer,
+               std::vector<PrecondRecord> *records) override;
+  BlockSolveResult solve(std::int64_t point_index, const DenseMatrix &rhs) override;
+  bool provides_residuals() const override { return true; }
+
+  std::size_t devices() const { return parts_.size(); }
+  CudaCgBackend &part(std::size_t d) { return *parts_[d]; }
+  /// (device slot, local point index) of a global point index
+  std::pair<std::size_t, std::int64_t> owner(std::int64_t point_index) const;
+
+private:
+  std::vector<std::unique_ptr<CudaCgBackend>> parts_;
+};
+
 std::unique_ptr<SolveBackend> make_cuda_backend(const AirgaConfig &cfg, const CudaBackendOptions &opt = {});
 
 } // namespace mor

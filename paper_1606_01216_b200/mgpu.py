@@ -37,6 +37,8 @@ EXPORTED = [
     "mgpu_arnoldi_deflate", "mgpu_model_hermite_device", "mgpu_csr_write", "mgpu_csr_read", "mgpu_shifted_solve",
     "mgpu_csr_upload_batch", "mgpu_ctx_set_option", "mgpu_ctx_get_option", "mgpu_phase_profile",
     "mgpu_buffer_alloc", "mgpu_buffer_free", "mgpu_memcpy_d2h", "mgpu_memcpy_h2d",
+    "mgpu_comm_unique_id", "mgpu_comm_init", "mgpu_comm_destroy", "mgpu_comm_allreduce_sum", "mgpu_comm_rows",
+    "mgpu_comm_columns_to_rows", "mgpu_comm_project_reduce", "mgpu_csr_bandwidth",
 ]
 
 # mgpu.h mgpu_option
@@ -162,6 +164,19 @@ def lib():
         L.mgpu_csr_read.argtypes = [vp, C.c_char_p, C.POINTER(C.c_void_p)]
         L.mgpu_model_hermite_device.argtypes = [vp, i64] + [dbl] * 7 + [C.POINTER(C.c_void_p)] * 3
         L.mgpu_host_free.argtypes = [C.POINTER(_HostCsr)]
+        L.mgpu_comm_unique_id.argtypes = [vp]
+        L.mgpu_comm_init.argtypes = [vp, vp, C.c_int, C.c_int]
+        L.mgpu_comm_destroy.argtypes = [vp]
+        L.mgpu_comm_allreduce_sum.argtypes = [vp, vp, i64]
+        L.mgpu_comm_rows.argtypes = [vp, i64, i64] + [C.POINTER(i64)] * 4
+        L.mgpu_comm_columns_to_rows.argtypes = [vp, i64, i64, i64, vp, vp, i64, vp]
+        L.mgpu_comm_project_reduce.argtypes = [vp, vp, vp, vp, i64, i64, vp, i64, vp, i64, vp, vp] + [vp] * 6 + \
+            [C.c_int]
+        L.mgpu_csr_bandwidth.argtypes = [vp, vp, C.POINTER(i64)]
+        L.mgpu_buffer_alloc.argtypes = [vp, C.c_size_t, C.POINTER(vp)]
+        L.mgpu_buffer_free.argtypes = [vp, vp]
+        L.mgpu_memcpy_d2h.argtypes = [vp, vp, vp, C.c_size_t]
+        L.mgpu_memcpy_h2d.argtypes = [vp, vp, vp, C.c_size_t]
         _lib = L
     return _lib
 
@@ -275,6 +290,27 @@ class Context:
         self.check(lib().mgpu_ctx_set_cg_path(self.handle,
                                               {"auto": 0, "general": 1, "banded": 2, "cluster_v1": 3,
                                                "stream": 4}[path]))
+
+    # ---- NCCL data plane (mgpu_comm_*; one rank per context)
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        st = lib().mgpu_comm_unique_id(buf)
+        if st != MGPU_OK:
+            raise MgpuError("ncclGetUniqueId failed", -1, -1, -1)
+        return buf.raw
+
+    def comm_init(self, uid: bytes, nranks: int, rank: int):
+        buf = C.create_string_buffer(bytes(uid), 128)
+        self.check(lib().mgpu_comm_init(self.handle, buf, nranks, rank))
+
+    def comm_destroy(self):
+        self.check(lib().mgpu_comm_destroy(self.handle))
+
+    def comm_rows(self, n: int, h: int):
+        v = [C.c_int64() for _ in range(4)]
+        self.check(lib().mgpu_comm_rows(self.handle, n, h, *[C.byref(x) for x in v]))
+        return tuple(x.value for x in v)  # row0, p, ext0, next
 
     def set_option(self, name: str, value: int):
         """mgpu_ctx_set_option (tuning / diagnostic switches; the library reads no environment)."""
@@ -771,3 +807,56 @@ def pcg_solve(A, chain: Sequence, b, rtol: float = 1e-10, maxit: Optional[int] =
         hist = r.relres_history[0][:min(int(r.iterations[0]), history_cap)]
     return dict(solution=r.X[:, 0], residual=r.true_residuals[:, 0], recurrence_residual=r.recurrence_residuals[:, 0],
                 iterations=int(r.iterations[0]), converged=bool(r.converged[0]), relres_history=hist)
+
+
+# ---------------------------------------------------------------- NCCL data plane
+def csr_bandwidth(A, ctx=None) -> int:
+    ctx = ctx or default_context()
+    v = C.c_int64()
+    ctx.check(lib().mgpu_csr_bandwidth(ctx.handle, _dev(A, ctx).handle, C.byref(v)))
+    return v.value
+
+
+def comm_allreduce_sum(t, ctx=None):
+    """In-place sum over the context's ranks of a CUDA float64 tensor."""
+    ctx = ctx or default_context()
+    ctx.check(lib().mgpu_comm_allreduce_sum(ctx.handle, t.data_ptr(), t.numel()))
+
+
+def comm_columns_to_rows(X_local, col_ids, R: int, h: int, ctx=None):
+    """Device redistribution (mgpu_comm_columns_to_rows).  X_local: CUDA float64 tensor of shape
+    (c_local, n) (= n x c_local column-major), col_ids its global column ids.  Returns
+    (Vext, ext0): Vext a CUDA tensor (R, next) = next x R column-major rows [ext0, ext0 + next)."""
+    import torch
+    ctx = ctx or default_context()
+    c_local, n = (int(X_local.shape[0]), int(X_local.shape[1])) if X_local.dim() == 2 else (0, 0)
+    row0, p, ext0, nx = ctx.comm_rows(n, h)
+    Vext = torch.empty((R, nx), dtype=torch.float64, device=X_local.device)
+    ids = np.ascontiguousarray(np.asarray(col_ids, np.int64))
+    ctx.check(lib().mgpu_comm_columns_to_rows(ctx.handle, n, h, c_local, _ptr(ids) if c_local else None,
+                                              X_local.data_ptr() if c_local else None, R, Vext.data_ptr()))
+    return Vext, ext0
+
+
+def comm_project_reduce(M, D, K, h: int, Vext, F=None, Cp=None, Cv=None, ctx=None) -> dict:
+    """mgpu_comm_project_reduce: replicated device operators, this rank's extended slab (CUDA tensor
+    (r, next)), host F (n x m) / Cp, Cv (q x n).  Every rank receives the reduced matrices."""
+    ctx = ctx or default_context()
+    dM, dD, dK = (_dev(x, ctx) for x in (M, D, K))
+    n = dM.nrows
+    r = int(Vext.shape[0])
+    Fm = _fortran(F) if F is not None else np.zeros((n, 0), order="F")
+    m = Fm.shape[1]
+    q = 0 if Cp is None else _fortran(Cp).shape[0]
+    Cpm = _fortran(Cp) if q else np.zeros((0, n), order="F")
+    Cvm = _fortran(Cv) if q else np.zeros((0, n), order="F")
+    out = {k: np.zeros(shape, order="F") for k, shape in
+           (("Mh", (r, r)), ("Dh", (r, r)), ("Kh", (r, r)), ("Fh", (r, m)), ("Cph", (q, r)), ("Cvh", (q, r)))}
+    ctx.check(lib().mgpu_comm_project_reduce(ctx.handle, dM.handle, dD.handle, dK.handle, h, r, Vext.data_ptr(), m,
+                                             _ptr(Fm) if m else None, q, _ptr(Cpm) if q else None,
+                                             _ptr(Cvm) if q else None, _ptr(out["Mh"]), _ptr(out["Dh"]),
+                                             _ptr(out["Kh"]), _ptr(out["Fh"]) if m else None,
+                                             _ptr(out["Cph"]) if q else None, _ptr(out["Cvh"]) if q else None,
+                                             MGPU_HOST))
+    return out
+

@@ -14,7 +14,7 @@ from . import mgpu as _mg
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(ROOT, "lib", "libmor_cuda.so")
-EXPORTED = ["mor_cuda_backend_create", "mor_cuda_backend_destroy", "mor_cuda_backend_set_system",
+EXPORTED = ["mor_cuda_backend_create", "mor_cuda_backend_create_multi", "mor_cuda_backend_destroy", "mor_cuda_backend_set_system",
             "mor_cuda_backend_prepare", "mor_cuda_backend_solve"]
 SOLVERS = {"cg_plain": 1, "cg_spai": 2, "cg_spai_update": 3}
 _lib = None
@@ -34,6 +34,9 @@ def lib():
         L.mor_cuda_backend_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, i64, C.c_int,
                                               C.c_double, i64, i64, i64, C.c_int, C.POINTER(vp), C.c_char_p,
                                               C.c_size_t]
+        L.mor_cuda_backend_create_multi.argtypes = [C.c_int, vp, C.c_int, C.c_int, C.c_int, C.c_double, i64,
+                                                    C.c_int, C.c_double, i64, i64, i64, C.c_int, C.POINTER(vp),
+                                                    C.c_char_p, C.c_size_t]
         L.mor_cuda_backend_destroy.argtypes = [vp]
         L.mor_cuda_backend_destroy.restype = None
         L.mor_cuda_backend_set_system.argtypes = [vp, i64] + [i64, vp, vp, vp] * 3 + [i64, vp, C.c_char_p,
@@ -58,13 +61,16 @@ class PluginBackend:
 
     def __init__(self, solver="cg_spai", algorithm="ls", ls_pattern=0, spai_tol=0.01, spai_max_col_iters=50,
                  spai_mode=1, cg_rtol=1e-10, cg_maxit_factor=10, maxit=0, update_start_iteration=3,
-                 speculative=True, device=0):
+                 speculative=True, device=0, devices=None):
+        """devices: several device ordinals -> mor::MultiDeviceCgBackend (point i on devices[i % N])."""
         self.h = C.c_void_p()
         buf = C.create_string_buffer(1024)
-        st = lib().mor_cuda_backend_create(device, SOLVERS[solver], 1 if algorithm == "ls" else 0, ls_pattern,
-                                           spai_tol, spai_max_col_iters, spai_mode, cg_rtol, cg_maxit_factor, maxit,
-                                           update_start_iteration, 1 if speculative else 0, C.byref(self.h), buf,
-                                           1024)
+        devs = np.asarray(devices if devices is not None else [device], np.int32)
+        st = lib().mor_cuda_backend_create_multi(len(devs), devs.ctypes.data, SOLVERS[solver],
+                                                 1 if algorithm == "ls" else 0, ls_pattern, spai_tol,
+                                                 spai_max_col_iters, spai_mode, cg_rtol, cg_maxit_factor, maxit,
+                                                 update_start_iteration, 1 if speculative else 0, C.byref(self.h),
+                                                 buf, 1024)
         _raise(st, buf)
         self.n = 0
 

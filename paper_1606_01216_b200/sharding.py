@@ -139,24 +139,14 @@ def columns_to_rows(X_local, col_ids: Sequence[int], total_cols: int, n: int, di
     if world == 1:
         out[:, list(col_ids)] = X_local[r0:r1]
         return out
+    if dist.get_backend() == "nccl":
+        raise ValueError("columns_to_rows is the host (gloo) restatement; on NCCL use project_reduce_nccl, "
+                         "which redistributes device buffers with mgpu_comm_columns_to_rows")
     # each destination d receives rows [r0_d, r1_d) of this rank's columns
     sends = [(list(col_ids), X_local[slice(*row_range(n, d, world))]) for d in range(world)]
-    recv = [None] * world
-    if dist.get_backend() == "nccl":
-        import torch
-        dev = torch.device("cuda", torch.cuda.current_device())
-        counts = [None] * world
-        dist.all_gather_object(counts, len(col_ids))
-        ids = [None] * world
-        dist.all_gather_object(ids, list(col_ids))
-        inputs = [torch.as_tensor(np.ascontiguousarray(s[1]), device=dev) for s in sends]
-        outputs = [torch.empty((r1 - r0, counts[s]), dtype=torch.float64, device=dev) for s in range(world)]
-        dist.all_to_all(outputs, inputs)
-        recv = [(ids[s], outputs[s].cpu().numpy()) for s in range(world)]
-    else:
-        gathered = [None] * world
-        dist.all_gather_object(gathered, sends)
-        recv = [gathered[s][rank] for s in range(world)]
+    gathered = [None] * world
+    dist.all_gather_object(gathered, sends)
+    recv = [gathered[s][rank] for s in range(world)]
     for ids, block in recv:
         if len(ids):
             out[:, ids] = block
@@ -222,3 +212,17 @@ def project_reduce_distributed(M, D, K, V_slab, r0: int, F=None, Cp=None, Cv=Non
         out[k] = flat[o:o + cnt].reshape(shape, order="F")
         o += cnt
     return out
+
+
+def project_reduce_nccl(ctx, M, D, K, X_local, col_ids, R: int, F=None, Cp=None, Cv=None) -> dict:
+    """airga.cpp:485-500 after the shift-sharded solves, entirely on the devices over NCCL: this rank's
+    solution columns X_local (CUDA float64 tensor (c_local, n), global ids col_ids) become its row slab
+    of the n x R block plus the operators' bandwidth halo (mgpu_comm_columns_to_rows: grouped
+    ncclSend / ncclRecv), the slab partials run on the device and one ncclAllReduce sums them
+    (mgpu_comm_project_reduce).  The context must hold a communicator (Context.comm_init).  M, D, K:
+    the replicated operators (host CSR or DeviceCsr).  Returns the replicated reduced matrices."""
+    from . import mgpu
+    h = max(mgpu.csr_bandwidth(x, ctx) for x in (M, D, K))
+    Vext, _ = mgpu.comm_columns_to_rows(X_local, col_ids, R, h, ctx)
+    return mgpu.comm_project_reduce(M, D, K, h, Vext, F, Cp, Cv, ctx)
+

@@ -110,7 +110,7 @@ def _projection_case(n=600, r=6):
     return M, D, K, np.asfortranarray(V), F, Cp, Cv
 
 
-def _proj_worker(rank, world, port, q):
+def _proj_worker(rank, world, port, q, device_slab=False):
     import torch.distributed as dist
 
     from paper_1606_01216_b200 import sharding
@@ -122,19 +122,23 @@ def _proj_worker(rank, world, port, q):
     V_slab = sharding.columns_to_rows(V[:, mine], mine, r, n, dist)
     r0, r1 = sharding.row_range(n, rank, world)
     assert np.array_equal(V_slab, V[r0:r1])
-    out = sharding.project_reduce_distributed(M, D, K, V_slab, r0, F, Cp, Cv, dist=dist, local=_numpy_slab)
+    # device_slab: each rank's partials from the sm_100a slab kernel (mgpu_project_reduce_slab on cuda:0,
+    # both ranks share the one GPU; the gloo all-reduce sums host partials, no kernel waits on another rank)
+    out = sharding.project_reduce_distributed(M, D, K, V_slab, r0, F, Cp, Cv, dist=dist,
+                                              local=None if device_slab else _numpy_slab)
     if rank == 0:
         q.put(out)
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_two_rank_distributed_projection():
+@pytest.mark.parametrize("device_slab", [False, pytest.param(True, marks=pytest.mark.gpu)])
+def test_two_rank_distributed_projection(device_slab):
     """Columns -> row slabs (all-to-all), halo rows, slab partials, all-reduce == global V^T S V."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_proj_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_proj_worker, args=(r, 2, port, q, device_slab)) for r in range(2)]
     for p in procs:
         p.start()
     out = q.get(timeout=120)
