@@ -29,17 +29,21 @@ typedef struct mor_cuda_backend mor_cuda_backend;
 /* solver: 1 cg_plain, 2 cg_spai, 3 cg_spai_update (AirgaConfig::Solver, airga.hpp:42-48);
  * algorithm: 0 MR-SPAI (reference spai_build / spai_update), 1 LS-SPAI with ls_pattern
  * (MGPU_PATTERN_A / MGPU_PATTERN_A2, | MGPU_LS_COLSCALE); spai_mode: 0 sequential, 1 frozen;
- * maxit_override > 0 replaces cg_maxit_factor * n; speculative: batch-solve sys.F in prepare. */
+ * maxit_override > 0 replaces cg_maxit_factor * n; flags: MOR_CUDA_SPECULATIVE (batch-solve sys.F in
+ * prepare, CudaBackendOptions::speculative_solve), MOR_CUDA_COLLAPSE (collapse the update chain into
+ * one factor with a device SpGEMM, CudaBackendOptions::collapse). */
+#define MOR_CUDA_SPECULATIVE 1
+#define MOR_CUDA_COLLAPSE 2
 int mor_cuda_backend_create(int device, int solver, int algorithm, int ls_pattern, double spai_tol,
                             int64_t spai_max_col_iters, int spai_mode, double cg_rtol, int64_t cg_maxit_factor,
-                            int64_t maxit_override, int64_t update_start_iteration, int speculative,
+                            int64_t maxit_override, int64_t update_start_iteration, int flags,
                             mor_cuda_backend **out, char *msg, size_t cap);
 /* Shift sharding over several devices in one process (mor::MultiDeviceCgBackend): point i is
  * prepared and solved on devices[i % ndev]; the devices prepare concurrently. */
 int mor_cuda_backend_create_multi(int ndev, const int *devices, int solver, int algorithm, int ls_pattern,
                                   double spai_tol, int64_t spai_max_col_iters, int spai_mode, double cg_rtol,
                                   int64_t cg_maxit_factor, int64_t maxit_override, int64_t update_start_iteration,
-                                  int speculative, mor_cuda_backend **out, char *msg, size_t cap);
+                                  int flags, mor_cuda_backend **out, char *msg, size_t cap);
 void mor_cuda_backend_destroy(mor_cuda_backend *b);
 
 /* The SecondOrderSystem the backend prepares (system.hpp:15-33): M, D, K as CSR (n x n), F as

@@ -37,6 +37,9 @@ class CudaCgConfig:
     spai_algorithm: str = "mr"  # "mr" | "ls"
     ls_pattern: int = mgpu.PATTERN_A
     maxit_override: Optional[int] = None  # fixed CG budget (benchmarks); None = factor * n
+    # north-star subsystem 2: in update mode, collapse the chain after each update into one factor,
+    # P <- Q P (device SpGEMM, the product chain_apply applies factor by factor, spai.cpp:361-373)
+    collapse: bool = False
 
 
 @dataclass
@@ -58,6 +61,7 @@ class CudaCgBackend:
         self.n = 0
         self.prev_ops: List[mgpu.DeviceCsr] = []
         self.chains: List[List[mgpu.SpaiFactor]] = []
+        self.zlog: List[int] = []  # logical chain length (factors composed), as the reference counts it
         self._dev_sys = None
 
     def provides_residuals(self) -> bool:
@@ -101,13 +105,17 @@ class CudaCgBackend:
                 qs = mgpu.spai_ls_batched(fresh, self.prev_ops if update_mode else None, c.ls_pattern, ctx=self.ctx)
                 self.ctx.synchronize()
                 share = (time.perf_counter() - t0) / max(len(points), 1)
+                if not update_mode:
+                    self.zlog = [0] * len(points)
                 for i, s in enumerate(points):
-                    self.chains[i].insert(0, qs[i])  # push_newest (spai.cpp:352-359)
+                    self._push(i, qs[i], update_mode)
                     if records is not None:
                         records.append(PrecondRecord(outer, i, float(s), share, "update" if update_mode else "base",
-                                                     len(self.chains[i])))
+                                                     self.zlog[i]))
                 self.prev_ops = fresh
                 return
+            if not update_mode:
+                self.zlog = [0] * len(points)
             for i, s in enumerate(points):
                 t0 = time.perf_counter()
                 if update_mode:
@@ -117,11 +125,20 @@ class CudaCgBackend:
                     q = self._build(fresh[i])
                     kind = "base"
                 self.ctx.synchronize()
-                self.chains[i].insert(0, q)  # push_newest (spai.cpp:352-359)
+                self._push(i, q, update_mode)
                 if records is not None:
                     records.append(PrecondRecord(outer, i, float(s), time.perf_counter() - t0, kind,
-                                                 len(self.chains[i])))
+                                                 self.zlog[i]))
         self.prev_ops = fresh
+
+    def _push(self, i: int, q, update_mode: bool):
+        """push_newest (spai.cpp:352-359), or with collapse the product Q P of the new factor and the
+        collapsed chain (one factor; the reference's chain_apply applies Q_z ... Q_2 P in that order)."""
+        if self.cfg.collapse and update_mode and self.chains[i]:
+            self.chains[i] = [mgpu.spgemm(q.matrix, mgpu._factor_mat(self.chains[i][0]), ctx=self.ctx)]
+        else:
+            self.chains[i].insert(0, q)
+        self.zlog[i] += 1
 
     def _maxit(self) -> int:
         c = self.cfg

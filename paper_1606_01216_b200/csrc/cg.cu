@@ -1373,6 +1373,7 @@ __global__ void __launch_bounds__(TB, 1) cg_banded(BandParams P)
 // Control flow, reductions and arithmetic are those of cg_banded.
 // =====================================================================
 constexpr int kPadR = 64;
+constexpr int kEllMax = 64; // widest ELL row the streaming kernel takes (int8 offsets: bandwidth < kPadR)
 constexpr int kStreamNB = 4; // bulk-copy ring depth (maximum; StreamParams::nb is the one in use)
 constexpr int kTabSlots = 16; // operator-descriptor slots: segments per block, or points (serial schedule)
 static_assert(kTabSlots >= kMaxSeg, "descriptor table must cover every segment");
@@ -1439,7 +1440,7 @@ struct PEll
   const double *v;             // logical row 0 (PADR zero rows before / after)
   const unsigned long long *o; // packed int8 offsets, `ow` words per row
   int E;                       // values per row (even, <= 16)
-  int ow;                      // 1 (E <= 8) or 2 (E <= 16)
+  int ow;                      // offset words per row: ceil(E / 8) (E <= kEllMax)
 };
 
 // eq[p] = 1 iff operator p has point 0's CSR structure (then its ELL offsets equal point 0's,
@@ -1617,6 +1618,12 @@ __device__ __forceinline__ int off16(unsigned long long w0, unsigned long long w
 {
   return t < 8 ? off8s(w0, t) : off8s(w1, t - 8);
 }
+// offset t of a row with ow words (the first two held in registers)
+__device__ __forceinline__ int off_any(const unsigned long long *offs, unsigned long long w0, unsigned long long w1,
+                                       int t)
+{
+  return t < 16 ? off16(w0, w1, t) : off8s(offs[t >> 3], t & 7);
+}
 
 // Column of element e of a row-interleaved block with m columns (MT: compile-time bound, a power of two).
 template <int MT>
@@ -1704,6 +1711,19 @@ __device__ __forceinline__ void ell_row(const double *vals, const unsigned long 
   const unsigned long long w0 = offs[0];
   const unsigned long long w1 = ow > 1 ? offs[1] : 0ull;
   const double2 *v2 = reinterpret_cast<const double2 *>(vals);
+  if (ow > 2) // wide rows (collapsed update chains): offsets beyond the first two words read per term
+  {
+    for (int e = 0; e < E; ++e)
+    {
+      double x[MT];
+      ld_row<MT>(src + (in0 + off_any(offs, w0, w1, e)) * m, x, m);
+#pragma unroll
+      for (int c = 0; c < MT; ++c)
+        if (c < m)
+          a2[c] = __dadd_rn(a2[c], __dmul_rn(vals[e], x[c]));
+    }
+    return;
+  }
   auto term = [&](double a, int e) {
     double x[MT];
     ld_row<MT>(src + (in0 + off16(w0, w1, e)) * m, x, m);
@@ -1796,7 +1816,7 @@ __device__ __forceinline__ void ell_row_planar(const double *vals, const unsigne
   const unsigned long long w1 = ow > 1 ? offs[1] : 0ull;
   for (int e = 0; e < E; ++e)
   {
-    const int r = in0 + off16(w0, w1, e);
+    const int r = in0 + off_any(offs, w0, w1, e);
     const double a = vals[e];
     const double2 t0 = reinterpret_cast<const double2 *>(src)[r];
     const double2 t1 = reinterpret_cast<const double2 *>(src + pst)[r];
@@ -2646,7 +2666,7 @@ __global__ void csr_to_pell(int64_t n, DCsr M, int E, int ow, double *vals, unsi
   if (i >= n)
     return;
   const int64_t k0 = M.rp[i], k1 = M.rp[i + 1];
-  unsigned long long w[2] = {0ull, 0ull};
+  unsigned long long w[kEllMax / 8] = {};
   for (int t = 0; t < E; ++t)
   {
     const bool has = k0 + t < k1;
@@ -2811,7 +2831,7 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
     // copies stay 16-byte multiples because chunk row counts are even
     const int E = static_cast<int>(csr_max_row(ctx, const_cast<mgpu_csr *>(M)));
     const int Ee = E < 1 ? 1 : E;
-    const int ow = Ee > 8 ? 2 : 1;
+    const int ow = (Ee + 7) / 8;
     const int64_t rows = n + 2 * kPadR;
     keep.emplace_back(sizeof(double) * rows * Ee, s);
     DBuf &v = keep.back();
@@ -2829,10 +2849,11 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
   keep.reserve(static_cast<size_t>(2 * l * (z + 1) + 16));
   for (int p = 0; p < l; ++p)
   {
-    if (csr_max_row(ctx, const_cast<mgpu_csr *>(A[p])) > 16)
+    // rows of up to kEllMax entries (collapsed update chains widen with every product)
+    if (csr_max_row(ctx, const_cast<mgpu_csr *>(A[p])) > kEllMax)
       return false;
     for (int f = 0; f < z; ++f)
-      if (csr_max_row(ctx, const_cast<mgpu_csr *>(chains[static_cast<size_t>(p) * z + f])) > 16)
+      if (csr_max_row(ctx, const_cast<mgpu_csr *>(chains[static_cast<size_t>(p) * z + f])) > kEllMax)
         return false;
   }
   std::vector<PEll> hA(static_cast<size_t>(l)), hF(static_cast<size_t>(l) * (z > 0 ? z : 1));

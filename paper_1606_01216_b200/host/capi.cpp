@@ -89,7 +89,7 @@ namespace
 {
 void settings(int solver, int algorithm, int ls_pattern, double spai_tol, int64_t spai_max_col_iters, int spai_mode,
               double cg_rtol, int64_t cg_maxit_factor, int64_t maxit_override, int64_t update_start_iteration,
-              int speculative, mor::CudaSolveSettings &s, mor::CudaBackendOptions &o)
+              int flags, mor::CudaSolveSettings &s, mor::CudaBackendOptions &o)
 {
   if (solver < 1 || solver > 3 || algorithm < 0 || algorithm > 1)
     throw mor::ArgumentError("mor_cuda_backend_create: bad argument");
@@ -104,25 +104,26 @@ void settings(int solver, int algorithm, int ls_pattern, double spai_tol, int64_
   s.update_start_iteration = update_start_iteration;
   o.algorithm = algorithm == 1 ? mor::cuda::SpaiAlgorithm::ls : mor::cuda::SpaiAlgorithm::mr;
   o.ls_pattern = ls_pattern;
-  o.speculative_solve = speculative != 0;
+  o.speculative_solve = (flags & MOR_CUDA_SPECULATIVE) != 0;
+  o.collapse = (flags & MOR_CUDA_COLLAPSE) != 0;
   o.maxit_override = maxit_override;
 }
 } // namespace
 
 int mor_cuda_backend_create(int device, int solver, int algorithm, int ls_pattern, double spai_tol,
                             int64_t spai_max_col_iters, int spai_mode, double cg_rtol, int64_t cg_maxit_factor,
-                            int64_t maxit_override, int64_t update_start_iteration, int speculative,
+                            int64_t maxit_override, int64_t update_start_iteration, int flags,
                             mor_cuda_backend **out, char *msg, size_t cap)
 {
   return mor_cuda_backend_create_multi(1, &device, solver, algorithm, ls_pattern, spai_tol, spai_max_col_iters,
                                        spai_mode, cg_rtol, cg_maxit_factor, maxit_override, update_start_iteration,
-                                       speculative, out, msg, cap);
+                                       flags, out, msg, cap);
 }
 
 int mor_cuda_backend_create_multi(int ndev, const int *devices, int solver, int algorithm, int ls_pattern,
                                   double spai_tol, int64_t spai_max_col_iters, int spai_mode, double cg_rtol,
                                   int64_t cg_maxit_factor, int64_t maxit_override, int64_t update_start_iteration,
-                                  int speculative, mor_cuda_backend **out, char *msg, size_t cap)
+                                  int flags, mor_cuda_backend **out, char *msg, size_t cap)
 {
   return guarded(msg, cap, [&] {
     if (!out || ndev < 1 || !devices)
@@ -130,7 +131,7 @@ int mor_cuda_backend_create_multi(int ndev, const int *devices, int solver, int 
     mor::CudaSolveSettings s;
     mor::CudaBackendOptions o;
     settings(solver, algorithm, ls_pattern, spai_tol, spai_max_col_iters, spai_mode, cg_rtol, cg_maxit_factor,
-             maxit_override, update_start_iteration, speculative, s, o);
+             maxit_override, update_start_iteration, flags, s, o);
     auto b = std::make_unique<mor_cuda_backend>();
     if (ndev == 1)
     {

@@ -426,6 +426,7 @@ struct CudaCgBackend::State
   cuda::DeviceMatrix M, D, K;
   std::vector<cuda::DeviceMatrix> prev_ops;            // operators of the prepared iteration
   std::vector<std::vector<cuda::DeviceMatrix>> chains; // per point, newest first
+  std::vector<std::int64_t> zlog;                      // logical chain length per point (collapse)
   // speculative batched solve of sys.F (CudaBackendOptions::speculative_solve): X, recurrence and
   // true residuals of every point stay on the device ([array][point][column][row]) until
   // solve(i, F) reads point i back
@@ -531,7 +532,22 @@ void CudaCgBackend::prepare(const SecondOrderSystem &sys, const std::vector<doub
     {
       s.chains.clear();
       s.chains.resize(static_cast<std::size_t>(l));
+      s.zlog.assign(static_cast<std::size_t>(l), 0);
     }
+    // push_newest (spai.cpp:352-359), or with collapse the product Q P with the collapsed chain
+    auto push = [&](int i, mgpu_csr *f) {
+      auto &chain = s.chains[static_cast<std::size_t>(i)];
+      if (s.opt.collapse && update_mode && !chain.empty())
+      {
+        cuda::DeviceMatrix q(s.dev, f);
+        mgpu_csr *qp = nullptr;
+        check(ctx, mgpu_spgemm(ctx, q.get(), chain.front().get(), &qp));
+        chain.front() = cuda::DeviceMatrix(s.dev, qp);
+      }
+      else
+        chain.insert(chain.begin(), cuda::DeviceMatrix(s.dev, f));
+      return ++s.zlog[static_cast<std::size_t>(i)];
+    };
     if (s.opt.algorithm == cuda::SpaiAlgorithm::ls)
     {
       // one batched launch for every point; the per-point record gets the average
@@ -544,8 +560,7 @@ void CudaCgBackend::prepare(const SecondOrderSystem &sys, const std::vector<doub
       const double each = seconds_since(t0) / std::max(l, 1);
       for (int i = 0; i < l; ++i)
       {
-        s.chains[static_cast<std::size_t>(i)].insert(s.chains[static_cast<std::size_t>(i)].begin(),
-                                                     cuda::DeviceMatrix(s.dev, outs[static_cast<std::size_t>(i)]));
+        const std::int64_t z = push(i, outs[static_cast<std::size_t>(i)]);
         if (records)
         {
           PrecondRecord rec;
@@ -554,7 +569,7 @@ void CudaCgBackend::prepare(const SecondOrderSystem &sys, const std::vector<doub
           rec.point = points[static_cast<std::size_t>(i)];
           rec.seconds = each;
           rec.kind = update_mode ? SpaiFactor::Kind::update : SpaiFactor::Kind::base;
-          rec.chain_length = static_cast<std::int64_t>(s.chains[static_cast<std::size_t>(i)].size());
+          rec.chain_length = z;
           records->push_back(rec);
         }
       }
@@ -583,10 +598,8 @@ void CudaCgBackend::prepare(const SecondOrderSystem &sys, const std::vector<doub
           rec.kind = SpaiFactor::Kind::base;
         }
         mgpu_ctx_synchronize(ctx);
-        auto &chain = s.chains[static_cast<std::size_t>(i)];
-        chain.insert(chain.begin(), cuda::DeviceMatrix(s.dev, f)); // push_newest (spai.cpp:352-359)
+        rec.chain_length = push(i, f);
         rec.seconds = seconds_since(t0);
-        rec.chain_length = static_cast<std::int64_t>(chain.size());
         if (records)
           records->push_back(rec);
       }

@@ -147,6 +147,10 @@ struct CudaBackendOptions
   /// > 0: CG iteration budget in place of cg_maxit_factor * n (fixed-budget benchmarking; the
   /// factor is an integer multiple of n in AirgaConfig).
   std::int64_t maxit_override = 0;
+  /// North-star subsystem 2: in update mode the chain is collapsed after every update into ONE
+  /// factor, P <- Q P (device SpGEMM, mgpu_spgemm), instead of growing [Q_z, ..., Q_2, P]
+  /// (spai.cpp:352-373).  Records still report the logical chain length.
+  bool collapse = false;
 };
 
 /// The AirgaConfig fields the CG backend reads (airga.hpp:40-69).  Kept separately so that the

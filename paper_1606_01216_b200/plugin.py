@@ -61,7 +61,7 @@ class PluginBackend:
 
     def __init__(self, solver="cg_spai", algorithm="ls", ls_pattern=0, spai_tol=0.01, spai_max_col_iters=50,
                  spai_mode=1, cg_rtol=1e-10, cg_maxit_factor=10, maxit=0, update_start_iteration=3,
-                 speculative=True, device=0, devices=None):
+                 speculative=True, device=0, devices=None, collapse=False):
         """devices: several device ordinals -> mor::MultiDeviceCgBackend (point i on devices[i % N])."""
         self.h = C.c_void_p()
         buf = C.create_string_buffer(1024)
@@ -69,7 +69,8 @@ class PluginBackend:
         st = lib().mor_cuda_backend_create_multi(len(devs), devs.ctypes.data, SOLVERS[solver],
                                                  1 if algorithm == "ls" else 0, ls_pattern, spai_tol,
                                                  spai_max_col_iters, spai_mode, cg_rtol, cg_maxit_factor, maxit,
-                                                 update_start_iteration, 1 if speculative else 0, C.byref(self.h),
+                                                 update_start_iteration,
+                                                 (1 if speculative else 0) | (2 if collapse else 0), C.byref(self.h),
                                                  buf, 1024)
         _raise(st, buf)
         self.n = 0

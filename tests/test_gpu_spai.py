@@ -298,6 +298,23 @@ def test_spgemm_collapse(mg, oracle):
     assert rel(mg.chain_apply([QP], v), oracle.chain_apply([Q, P], v)) < 1e-12
 
 
+def test_spgemm_long_rows(mg):
+    """No row-length cap: banded factors of bandwidth 40 give 161-entry product rows."""
+    from oracle import Csr
+    rng = np.random.default_rng(9)
+    n, bw = 400, 40
+    def banded():
+        a = np.zeros((n, n))
+        for i in range(n):
+            lo, hi = max(0, i - bw), min(n, i + bw + 1)
+            a[i, lo:hi] = rng.standard_normal(hi - lo)
+        return a
+    a, c = banded(), banded()
+    AB = mg.spgemm(Csr.from_dense(a), Csr.from_dense(c)).download()
+    assert np.max(np.diff(AB.row_ptr)) == 2 * 2 * bw + 1
+    assert rel(AB.todense(), a @ c) < 1e-14
+
+
 # ------------------------------------------------------------------ chain_quality
 @pytest.mark.parametrize("z,samples,seed", [(0, 3, 42), (1, 8, 42), (2, 5, 7)])
 def test_chain_quality_matches_reference(mg, oracle, ref, z, samples, seed):

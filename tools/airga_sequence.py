@@ -9,6 +9,8 @@ SolveBackend mirror (backend.CudaCgBackend, airga.cpp:103-190) with LS-SPAI on A
   update  -- solver cg_spai_update, update_start_iteration = 2: a fresh factor at z = 1,
              afterwards Q_z = LS update (K_new Q ~ K_old on A's pattern) pushed onto the
              chain, so the preconditioner at z is Q_z ... Q_2 P_1 (z factors);
+  collapse-- the same updates, the chain collapsed into one factor after each (P <- Q P, device
+             SpGEMM; north-star subsystem 2), so every CG iteration applies one wider factor;
   rebuild -- solver cg_spai: a fresh LS factor at every z (chain length 1).
 
 Per outer iteration and arm: prepare time (device assembly of the 8 operators + the batched
@@ -37,9 +39,9 @@ from paper_1606_01216_b200.backend import CudaCgBackend, CudaCgConfig
 from paper_1606_01216_b200.sharding import airga_shift_draws
 
 
-def device_arm(update: bool, sysm, draws, b, budget, ctx):
+def device_arm(update: bool, sysm, draws, b, budget, ctx, collapse=False):
     cfg = CudaCgConfig(solver="cg_spai_update" if update else "cg_spai", spai_algorithm="ls",
-                       ls_pattern=mg.PATTERN_A, update_start_iteration=2, maxit_override=budget)
+                       ls_pattern=mg.PATTERN_A, update_start_iteration=2, maxit_override=budget, collapse=collapse)
     be = CudaCgBackend(cfg, ctx=ctx)
     rows = []
     bn = np.linalg.norm(b)
@@ -54,12 +56,15 @@ def device_arm(update: bool, sysm, draws, b, budget, ctx):
         t2 = time.perf_counter()
         cg_ms, loop_it = ctx.last_cg_timing()
         relres = [float(np.linalg.norm(r.true_residuals[:, 0]) / bn) for r in res]
+        factor_nnz = sum(mg.mgpu._factor_mat(f).stored_nnz for f in be.chains[0]) if be.chains else 0
         rows.append({"outer": z, "shifts": pts, "kind": recs[0].kind, "chain_length": recs[0].chain_length,
+                     "factors_applied": len(be.chains[0]) if be.chains else 0, "factor_nnz_point0": factor_nnz,
                      "prepare_ms": 1e3 * (t1 - t0), "spai_ms": 1e3 * sum(r.seconds for r in recs),
                      "solve_ms": 1e3 * (t2 - t1), "cg_kernel_ms": cg_ms, "cg_iterations": int(loop_it),
                      "cg_kernel": ctx.last_cg_path, "breakdowns": int(sum(int(r.status[0] != 0) for r in res)),
                      "max_true_relres": max(relres), "median_true_relres": float(np.median(relres))})
-        print(json.dumps({"arm": "update" if update else "rebuild", **{k: v for k, v in rows[-1].items()
+        print(json.dumps({"arm": ("collapse" if collapse else "update") if update else "rebuild",
+                          **{k: v for k, v in rows[-1].items()
                                                                       if k != "shifts"}}), flush=True)
     return rows
 
@@ -111,7 +116,7 @@ def main():
     ap.add_argument("--ref-outers", default="1,2,5,10")
     ap.add_argument("--out", default="")
     ap.add_argument("--cg-path", default="auto", help="auto | stream | banded | general (diagnostics)")
-    ap.add_argument("--arms", default="update,rebuild")
+    ap.add_argument("--arms", default="update,collapse,rebuild")
     a = ap.parse_args()
     draws = airga_shift_draws(a.outer, a.shifts)
     ctx = mg.Context(0)
@@ -128,7 +133,8 @@ def main():
                           f"A pattern, update from z=2 vs rebuild, CG budget {a.budget}",
               "cg_path": a.cg_path}
     for arm in a.arms.split(","):
-        result[arm] = device_arm(arm == "update", (M, D, K), draws, b, a.budget, ctx)
+        result[arm] = device_arm(arm in ("update", "collapse"), (M, D, K), draws, b, a.budget, ctx,
+                                 collapse=arm == "collapse")
     if a.ref_budget > 0:
         outers = {int(x) for x in a.ref_outers.split(",")}
         result["reference_update"] = reference_arm(True, a.ne, draws, b, a.ref_budget, a.budget, outers)
