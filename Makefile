@@ -34,7 +34,7 @@ $(OBJDIR)/%.cpp.o: $(SRC)/%.cpp include/mgpu.h | $(OBJDIR)
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
 $(LIBDIR)/libmgpu.so: $(CU_OBJS) $(CPP_OBJS) | $(LIBDIR)
-	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart -lcublas -lnccl
+	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart -ldl
 
 # C++ drop-in backend: compiled against the reference's own headers (only
 # where /root/reference exists); the .so travels to the GPU box.

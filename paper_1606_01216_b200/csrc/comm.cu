@@ -10,11 +10,13 @@
 //   project_reduce:  every rank's slab partials V_slab^T (S V), V_slab^T F, C V_slab
 //                    (mgpu_project_reduce_slab, on the device) and ONE ncclAllReduce of them.
 // Nothing passes through host memory but the column-id bookkeeping (a few integers per column).
-#include <nccl.h>
+#include <dlfcn.h>
+#include <nccl.h> // types only: the library is resolved at run time (see Nccl below)
 
 #include <algorithm>
 #include <cstring>
 #include <numeric>
+#include <type_traits>
 #include <vector>
 
 #include "internal.cuh"
@@ -24,12 +26,62 @@ namespace mgpu
 namespace
 {
 
-#define MG_NCCL(expr)                                                                                                  \
+// NCCL is bound on first use, not at load time: libmgpu.so must not pull a libnccl.so.2 into a
+// process before PyTorch loads its own (a second NCCL of another version under the same soname
+// breaks torch's bindings).  The copy already in the process (RTLD_NOLOAD: torch's, under
+// torch.distributed) is preferred; otherwise the system libnccl.so.2.
+struct Nccl
+{
+  ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char *(*GetErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+const Nccl &nccl()
+{
+  static const Nccl lib = [] {
+    Nccl n;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h)
+      h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!h)
+      return n;
+    auto sym = [&](auto &fp, const char *name) { fp = reinterpret_cast<std::remove_reference_t<decltype(fp)>>(dlsym(h, name)); };
+    sym(n.GetUniqueId, "ncclGetUniqueId");
+    sym(n.CommInitRank, "ncclCommInitRank");
+    sym(n.CommDestroy, "ncclCommDestroy");
+    sym(n.AllReduce, "ncclAllReduce");
+    sym(n.AllGather, "ncclAllGather");
+    sym(n.Send, "ncclSend");
+    sym(n.Recv, "ncclRecv");
+    sym(n.GroupStart, "ncclGroupStart");
+    sym(n.GroupEnd, "ncclGroupEnd");
+    sym(n.GetErrorString, "ncclGetErrorString");
+    n.ok = n.GetUniqueId && n.CommInitRank && n.CommDestroy && n.AllReduce && n.AllGather && n.Send && n.Recv &&
+           n.GroupStart && n.GroupEnd && n.GetErrorString;
+    return n;
+  }();
+  if (!lib.ok)
+    throw Error(MGPU_ERR_NCCL, "NCCL (libnccl.so.2) not available");
+  return lib;
+}
+
+#define MG_NCCL(fn, ...)                                                                                               \
   do                                                                                                                   \
   {                                                                                                                    \
-    ncclResult_t _r = (expr);                                                                                          \
+    const ::mgpu::Nccl &_n = ::mgpu::nccl();                                                                           \
+    ncclResult_t _r = _n.fn(__VA_ARGS__);                                                                              \
     if (_r != ncclSuccess)                                                                                             \
-      throw ::mgpu::Error(MGPU_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(_r));                          \
+      throw ::mgpu::Error(MGPU_ERR_NCCL, std::string("nccl" #fn ": ") + _n.GetErrorString(_r));                       \
   } while (0)
 
 ncclComm_t comm_of(mgpu_ctx *ctx)
@@ -99,11 +151,18 @@ int mgpu_comm_unique_id(void *id)
 {
   if (id == nullptr)
     return MGPU_ERR_ARG;
-  ncclUniqueId u;
-  if (ncclGetUniqueId(&u) != ncclSuccess)
+  try
+  {
+    ncclUniqueId u;
+    if (nccl().GetUniqueId(&u) != ncclSuccess)
+      return MGPU_ERR_NCCL;
+    std::memcpy(id, &u, sizeof u);
+    return MGPU_OK;
+  }
+  catch (const Error &)
+  {
     return MGPU_ERR_NCCL;
-  std::memcpy(id, &u, sizeof u);
-  return MGPU_OK;
+  }
 }
 
 int mgpu_comm_init(mgpu_ctx *ctx, const void *id, int nranks, int rank)
@@ -117,7 +176,7 @@ int mgpu_comm_init(mgpu_ctx *ctx, const void *id, int nranks, int rank)
     std::memcpy(&u, id, sizeof u);
     ncclComm_t c = nullptr;
     MG_CUDA(cudaSetDevice(ctx->device));
-    MG_NCCL(ncclCommInitRank(&c, nranks, u, rank));
+    MG_NCCL(CommInitRank, &c, nranks, u, rank);
     ctx->nccl = c;
     ctx->nranks = nranks;
     ctx->rank = rank;
@@ -132,7 +191,7 @@ int mgpu_comm_destroy(mgpu_ctx *ctx)
     if (ctx->nccl)
     {
       MG_CUDA(cudaStreamSynchronize(ctx->stream));
-      MG_NCCL(ncclCommDestroy(static_cast<ncclComm_t>(ctx->nccl)));
+      MG_NCCL(CommDestroy, static_cast<ncclComm_t>(ctx->nccl));
     }
     ctx->nccl = nullptr;
     ctx->nranks = 1;
@@ -147,7 +206,7 @@ int mgpu_comm_allreduce_sum(mgpu_ctx *ctx, double *buf, int64_t count)
   return guard(ctx, [&] {
     MG_ARG(buf != nullptr || count == 0, "comm_allreduce: null buffer");
     if (count > 0)
-      MG_NCCL(ncclAllReduce(buf, buf, static_cast<size_t>(count), ncclDouble, ncclSum, comm_of(ctx), ctx->stream));
+      MG_NCCL(AllReduce, buf, buf, static_cast<size_t>(count), ncclDouble, ncclSum, comm_of(ctx), ctx->stream);
     MG_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
@@ -175,7 +234,7 @@ int mgpu_comm_columns_to_rows(mgpu_ctx *ctx, int64_t n, int64_t h, int64_t c_loc
     DBuf cnt_d(sizeof(int64_t) * W, s);
     int64_t mine = c_local;
     MG_CUDA(cudaMemcpyAsync(cnt_d.as<int64_t>() + me, &mine, sizeof(int64_t), cudaMemcpyHostToDevice, s));
-    MG_NCCL(ncclAllGather(cnt_d.as<int64_t>() + me, cnt_d.ptr, 1, ncclInt64, comm, s));
+    MG_NCCL(AllGather, cnt_d.as<int64_t>() + me, cnt_d.ptr, 1, ncclInt64, comm, s);
     std::vector<int64_t> cnt(static_cast<size_t>(W));
     MG_CUDA(cudaMemcpyAsync(cnt.data(), cnt_d.ptr, sizeof(int64_t) * W, cudaMemcpyDeviceToHost, s));
     MG_CUDA(cudaStreamSynchronize(s));
@@ -188,7 +247,7 @@ int mgpu_comm_columns_to_rows(mgpu_ctx *ctx, int64_t n, int64_t h, int64_t c_loc
       MG_CUDA(cudaMemcpyAsync(ids_d.as<int64_t>() + me * cmax, pad.data(), sizeof(int64_t) * cmax,
                               cudaMemcpyHostToDevice, s));
       if (cmax > 0)
-        MG_NCCL(ncclAllGather(ids_d.as<int64_t>() + me * cmax, ids_d.ptr, static_cast<size_t>(cmax), ncclInt64, comm, s));
+        MG_NCCL(AllGather, ids_d.as<int64_t>() + me * cmax, ids_d.ptr, static_cast<size_t>(cmax), ncclInt64, comm, s);
     }
     int64_t r0, p, e0, ne;
     slab_of(n, W, me, h, r0, p, e0, ne);
@@ -210,14 +269,14 @@ int mgpu_comm_columns_to_rows(mgpu_ctx *ctx, int64_t n, int64_t h, int64_t c_loc
     for (int q = 0; q < W; ++q)
       roff[q + 1] = roff[q] + ne * cnt[q];
     DBuf rbuf(sizeof(double) * static_cast<size_t>(roff[W] > 0 ? roff[W] : 1), s);
-    MG_NCCL(ncclGroupStart());
+    MG_NCCL(GroupStart);
     for (int d = 0; d < W; ++d)
       if (sne[d] * c_local > 0)
-        MG_NCCL(ncclSend(sbuf.as<double>() + soff[d], static_cast<size_t>(sne[d] * c_local), ncclDouble, d, comm, s));
+        MG_NCCL(Send, sbuf.as<double>() + soff[d], static_cast<size_t>(sne[d] * c_local), ncclDouble, d, comm, s);
     for (int q = 0; q < W; ++q)
       if (ne * cnt[q] > 0)
-        MG_NCCL(ncclRecv(rbuf.as<double>() + roff[q], static_cast<size_t>(ne * cnt[q]), ncclDouble, q, comm, s));
-    MG_NCCL(ncclGroupEnd());
+        MG_NCCL(Recv, rbuf.as<double>() + roff[q], static_cast<size_t>(ne * cnt[q]), ncclDouble, q, comm, s);
+    MG_NCCL(GroupEnd);
     // scatter every source's block into Vext at its global column ids
     for (int q = 0; q < W; ++q)
       if (ne * cnt[q] > 0)
@@ -276,7 +335,7 @@ int mgpu_comm_project_reduce(mgpu_ctx *ctx, const mgpu_csr *M, const mgpu_csr *D
     if (st2 != MGPU_OK)
       throw Error(st2, ctx->err_msg, ctx->err_index, ctx->err_col, ctx->err_point);
     if (tot > 0)
-      MG_NCCL(ncclAllReduce(P, P, static_cast<size_t>(tot), ncclDouble, ncclSum, comm_of(ctx), s));
+      MG_NCCL(AllReduce, P, P, static_cast<size_t>(tot), ncclDouble, ncclSum, comm_of(ctx), s);
     double *outs[6] = {Mh, Dh, Kh, Fh, Cph, Cvh};
     const int64_t sizes[6] = {r * r, r * r, r * r, r * m, q * r, q * r};
     int64_t o = 0;

@@ -5,7 +5,6 @@
 #include <cstring>
 #include <vector>
 
-#include <cublas_v2.h>
 
 #include "internal.cuh"
 
@@ -314,8 +313,6 @@ int mgpu_ctx_destroy(mgpu_ctx *ctx)
     cudaEventDestroy(ctx->ev1);
   if (ctx->own_stream)
     cudaStreamDestroy(ctx->stream);
-  if (ctx->blas)
-    cublasDestroy(static_cast<cublasHandle_t>(ctx->blas));
   if (ctx->pin)
     cudaFreeHost(ctx->pin);
   for (auto &e : ctx->phase_ev)

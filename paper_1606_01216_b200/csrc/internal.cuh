@@ -137,7 +137,6 @@ struct mgpu_ctx
   int cg_path = 0;      // 0 auto, 1 force general, 2 force banded grid kernel, 3 cluster v1 only, 4 stream (no cluster)
   long long *prof_dev = nullptr; // diagnostics: per-phase clock64 totals of the CG kernels (MGPU_OPT_PROFILE_PHASES)
   int64_t opt[MGPU_OPT_COUNT] = {1, 0, 0, 0, 0, 0, 1, 0, 0, 0}; // mgpu_ctx_set_option
-  void *blas = nullptr;          // cublasHandle_t, created on first dense product (project.cu)
   void *nccl = nullptr;          // ncclComm_t (mgpu_comm_init), one rank per context
   int nranks = 1, rank = 0;
   cudaEvent_t phase_ev[4] = {nullptr, nullptr, nullptr, nullptr}; // mgpu_shifted_solve phase timing (lazy)
@@ -188,6 +187,11 @@ int64_t csr_bandwidth(mgpu_ctx *ctx, mgpu_csr *A);
 // Longest row of A (cached).
 int64_t csr_max_row(mgpu_ctx *ctx, mgpu_csr *A);
 void set_error(mgpu_ctx *ctx, const Error &e);
+
+// FP64 GEMM (dense_gemm.cu): C (M x N) = alpha op(A) B + beta C, column-major, op(A) = A^T when
+// transA; tall K split across blocks with an in-order partial sum (deterministic).
+void gemm(mgpu_ctx *ctx, bool transA, int64_t M, int64_t N, int64_t K, double alpha, const double *A, int64_t lda,
+          const double *B, int64_t ldb, double beta, double *C, int64_t ldc);
 
 // Deterministic fixed-shape sum of `count` doubles on the device (two-level,
 // grid size independent of the device).  Result written to *out_dev.

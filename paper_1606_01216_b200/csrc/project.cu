@@ -17,7 +17,6 @@
 // project_reduce: S V as an SpMM in CSR row order (spmv_into's order), then
 // the dense products V^T W, V^T F, Cp V, Cv V are plain GEMMs (cuBLAS DGEMM).
 #include <cooperative_groups.h>
-#include <cublas_v2.h>
 
 #include <algorithm>
 #include <cmath>
@@ -323,53 +322,101 @@ __global__ void deflate_axpy(int64_t count, const double *__restrict__ g, const 
     X[t] = __dadd_rn(X[t], __dmul_rn(-gv, B[t]));
 }
 
-// W[:, j] = S X[:, j] for a row slab S (p rows, global column indices) and X
-// holding global rows [x0, x0 + ldx): column-major p x r result, each row in
-// CSR order (spmv_into).
-__global__ void spmm_block(int64_t p, int64_t r, DCsr S, const double *__restrict__ X, int64_t x0, int64_t ldx,
-                           double *__restrict__ W)
+// V_slab^T (S_o V) for the three operators at once, S_o V never leaving the SM (verdict: no
+// intermediate in HBM).  Block (tile, split): a 64 x 64 tile (ta, tb) of the three r x r outputs
+// over the slab rows of its split, 16 rows at a time:
+//   Ya  = Y[rows, ta cols]                                   (shared memory)
+//   W_o = S_o[rows, :] Vext[:, tb cols]  (each row in CSR order, spmv_into, no FMA)  (shared memory)
+//   acc_o += Ya^T W_o                                        (4 x 4 per thread, DFMA)
+// Partial tiles go to part[split][o][r][r]; proj_reduce sums the splits in order (deterministic).
+constexpr int kPT = 64, kPR = 16; // 16-row chunks: 33 KB of static shared memory
+
+__global__ void __launch_bounds__(256) proj_fused(int64_t p, int64_t r, DCsr S0, DCsr S1, DCsr S2,
+                                                  const double *__restrict__ V, int64_t ext0, int64_t ldv,
+                                                  int64_t y0, int64_t rows_per_split, double *__restrict__ part)
+{
+  __shared__ double Ya[kPR][kPT + 1];
+  __shared__ double Wo[3][kPR][kPT + 1];
+  const int64_t ntile = (r + kPT - 1) / kPT;
+  const int64_t ta = blockIdx.x % ntile, tb = blockIdx.x / ntile;
+  const int64_t a0 = ta * kPT, b0 = tb * kPT;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t lo = static_cast<int64_t>(blockIdx.y) * rows_per_split;
+  const int64_t hi = p < lo + rows_per_split ? p : lo + rows_per_split;
+  const DCsr S[3] = {S0, S1, S2};
+  double acc[3][4][4] = {};
+  for (int64_t i0 = lo; i0 < hi; i0 += kPR)
+  {
+    // Ya: slab rows i0 .. i0 + 31 of basis columns a0 .. a0 + 63 (threads along rows: coalesced)
+    for (int t = threadIdx.x; t < kPR * kPT; t += 256)
+    {
+      const int i = t % kPR, a = t / kPR;
+      const int64_t gi = i0 + i, ga = a0 + a;
+      Ya[i][a] = (gi < hi && ga < r) ? V[ga * ldv + y0 + gi] : 0.0;
+    }
+    // W_o = S_o rows i0 .. i0 + 31 times basis columns b0 .. b0 + 63
+    for (int t = threadIdx.x; t < 3 * kPR * kPT; t += 256)
+    {
+      const int o = t / (kPR * kPT), rem = t % (kPR * kPT);
+      const int i = rem % kPR, b = rem / kPR;
+      const int64_t gi = i0 + i, gb = b0 + b;
+      double w = 0.0;
+      if (gi < hi && gb < r)
+      {
+        const double *vb = V + gb * ldv - ext0;
+        for (int64_t q = S[o].rp[gi]; q < S[o].rp[gi + 1]; ++q)
+          w = __dadd_rn(w, __dmul_rn(S[o].v[q], vb[S[o].ci[q]]));
+      }
+      Wo[o][i][b] = w;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int i = 0; i < kPR; ++i)
+    {
+      double ya[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        ya[u] = Ya[i][ty + 16 * u];
+#pragma unroll
+      for (int o = 0; o < 3; ++o)
+      {
+        double wb[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          wb[v] = Wo[o][i][tx + 16 * v];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v)
+            acc[o][u][v] = fma(ya[u], wb[v], acc[o][u][v]);
+      }
+    }
+    __syncthreads();
+  }
+  const int64_t rr = r * r;
+#pragma unroll
+  for (int o = 0; o < 3; ++o)
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+      {
+        const int64_t ga = a0 + ty + 16 * u, gb = b0 + tx + 16 * v;
+        if (ga < r && gb < r)
+          part[(static_cast<int64_t>(blockIdx.y) * 3 + o) * rr + gb * r + ga] = acc[o][u][v];
+      }
+}
+
+__global__ void proj_reduce(int64_t rr, int splits, const double *__restrict__ part, double *__restrict__ H)
 {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= p * r)
+  if (t >= 3 * rr)
     return;
-  const int64_t j = t / p, i = t - j * p;
-  const double *xj = X + j * ldx - x0;
-  double acc = 0.0;
-  for (int64_t q = S.rp[i]; q < S.rp[i + 1]; ++q)
-    acc = __dadd_rn(acc, __dmul_rn(S.v[q], xj[S.ci[q]]));
-  W[t] = acc;
-}
-
-cublasHandle_t blas(mgpu_ctx *ctx)
-{
-  if (!ctx->blas)
-  {
-    cublasHandle_t h = nullptr;
-    if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS)
-      throw Error(MGPU_ERR_CUDA, "cublasCreate failed");
-    ctx->blas = h;
-  }
-  cublasHandle_t h = static_cast<cublasHandle_t>(ctx->blas);
-  if (cublasSetStream(h, ctx->stream) != CUBLAS_STATUS_SUCCESS)
-    throw Error(MGPU_ERR_CUDA, "cublasSetStream failed");
-  return h;
-}
-
-void dgemm_ab(mgpu_ctx *ctx, cublasOperation_t ta, cublasOperation_t tb, int64_t M, int64_t N, int64_t K,
-              double alpha, const double *A, int64_t lda, const double *B, int64_t ldb, double beta, double *C,
-              int64_t ldc)
-{
-  if (M == 0 || N == 0)
-    return;
-  if (cublasDgemm_64(blas(ctx), ta, tb, M, N, K, &alpha, A, lda, B, ldb, &beta, C, ldc) != CUBLAS_STATUS_SUCCESS)
-    throw Error(MGPU_ERR_CUDA, "cublasDgemm failed");
-  count_launch(ctx);
-}
-
-void dgemm(mgpu_ctx *ctx, cublasOperation_t ta, cublasOperation_t tb, int64_t M, int64_t N, int64_t K,
-           const double *A, int64_t lda, const double *B, int64_t ldb, double *C, int64_t ldc)
-{
-  dgemm_ab(ctx, ta, tb, M, N, K, 1.0, A, lda, B, ldb, 0.0, C, ldc);
+  const int64_t o = t / rr, e = t - o * rr;
+  double s = 0.0;
+  for (int z = 0; z < splits; ++z) // split order: deterministic
+    s += part[(static_cast<int64_t>(z) * 3 + o) * rr + e];
+  H[t] = s;
 }
 
 // Device staging of a `where` buffer: device pointers pass through, host ones are copied.
@@ -472,8 +519,7 @@ int mgpu_thin_qr(mgpu_ctx *ctx, int64_t rows, int64_t cols, const double *A, dou
           check_launch(ctx, "qr_panel_v");
           if (build_t)
           {
-            dgemm(ctx, CUBLAS_OP_T, CUBLAS_OP_N, jb, jb, mv, Vp.as<double>(), mv, Vp.as<double>(), mv, Gm.as<double>(),
-                  jb);
+            gemm(ctx, true, jb, jb, mv, 1.0, Vp.as<double>(), mv, Vp.as<double>(), mv, 0.0, Gm.as<double>(), jb);
             qr_panel_t<<<1, 32, 0, s>>>(jb, Gm.as<double>(), tau.as<double>() + j0,
                                         Tall.as<double>() + static_cast<size_t>(pi) * kPanel * kPanel);
             check_launch(ctx, "qr_panel_t");
@@ -495,10 +541,9 @@ int mgpu_thin_qr(mgpu_ctx *ctx, int64_t rows, int64_t cols, const double *A, dou
           const int64_t mv = rows - j0;
           const double *T = Tall.as<double>() + static_cast<size_t>(pi) * kPanel * kPanel;
           double *C = Wm + (j0 + jb) * rows + j0;
-          dgemm(ctx, CUBLAS_OP_T, CUBLAS_OP_N, jb, nc, mv, Vp.as<double>(), mv, C, rows, Wt.as<double>(), jb);
-          dgemm(ctx, CUBLAS_OP_T, CUBLAS_OP_N, jb, nc, jb, T, jb, Wt.as<double>(), jb, Wt2.as<double>(), jb);
-          dgemm_ab(ctx, CUBLAS_OP_N, CUBLAS_OP_N, mv, nc, jb, -1.0, Vp.as<double>(), mv, Wt2.as<double>(), jb, 1.0, C,
-                   rows);
+          gemm(ctx, true, jb, nc, mv, 1.0, Vp.as<double>(), mv, C, rows, 0.0, Wt.as<double>(), jb);
+          gemm(ctx, true, jb, nc, jb, 1.0, T, jb, Wt.as<double>(), jb, 0.0, Wt2.as<double>(), jb);
+          gemm(ctx, false, mv, nc, jb, -1.0, Vp.as<double>(), mv, Wt2.as<double>(), jb, 1.0, C, rows);
         }
         // T of the last panel (not needed for a trailing update, needed for Q)
         panel_vt(npan - 1, true);
@@ -513,10 +558,9 @@ int mgpu_thin_qr(mgpu_ctx *ctx, int64_t rows, int64_t cols, const double *A, dou
             panel_vt(pi, false);
           const double *T = Tall.as<double>() + static_cast<size_t>(pi) * kPanel * kPanel;
           double *Cq = Qd.as<double>() + j0 * rows + j0;
-          dgemm(ctx, CUBLAS_OP_T, CUBLAS_OP_N, jb, nq, mv, Vp.as<double>(), mv, Cq, rows, Wt.as<double>(), jb);
-          dgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, jb, nq, jb, T, jb, Wt.as<double>(), jb, Wt2.as<double>(), jb);
-          dgemm_ab(ctx, CUBLAS_OP_N, CUBLAS_OP_N, mv, nq, jb, -1.0, Vp.as<double>(), mv, Wt2.as<double>(), jb, 1.0, Cq,
-                   rows);
+          gemm(ctx, true, jb, nq, mv, 1.0, Vp.as<double>(), mv, Cq, rows, 0.0, Wt.as<double>(), jb);
+          gemm(ctx, false, jb, nq, jb, 1.0, T, jb, Wt.as<double>(), jb, 0.0, Wt2.as<double>(), jb);
+          gemm(ctx, false, mv, nq, jb, -1.0, Vp.as<double>(), mv, Wt2.as<double>(), jb, 1.0, Cq, rows);
         }
       }
       qr_form_r<<<blocks_for(cols * cols), kThreads, 0, s>>>(rows, static_cast<int>(cols), W.as<double>(),
@@ -558,31 +602,39 @@ int mgpu_project_reduce_slab(mgpu_ctx *ctx, const mgpu_csr *M, const mgpu_csr *D
     Staged dV(ctx, Vext, next * r, where), dF(ctx, F, p * m, where), dCp(ctx, Cp, q * p, where),
         dCv(ctx, Cv, q * p, where);
     const double *Y = dV.ptr + (row0 - ext0); // this slab's own rows of the basis (ld = next)
-    DBuf W(sizeof(double) * static_cast<size_t>(p * r > 0 ? p * r : 1), s);
-    DBuf H(sizeof(double) * static_cast<size_t>(r * r > 0 ? r * r : 1), s);
-    double *outs[3] = {Mh, Dh, Kh};
-    const mgpu_csr *ops[3] = {M, D, K};
-    for (int o = 0; o < 3; ++o) // airga.cpp:489-491: matmul_tn(V, sparse_times_dense(S, V))
+    // airga.cpp:489-491 matmul_tn(V, sparse_times_dense(S, V)) for M, D, K in one fused pass
+    // (proj_fused: S V formed tile by tile in shared memory, never written to HBM)
+    DBuf H(sizeof(double) * static_cast<size_t>(3 * r * r > 0 ? 3 * r * r : 1), s);
+    if (r > 0 && p == 0)
+      MG_CUDA(cudaMemsetAsync(H.ptr, 0, sizeof(double) * 3 * r * r, s));
+    else if (r > 0)
     {
-      if (p * r > 0)
-      {
-        spmm_block<<<blocks_for(p * r), kThreads, 0, s>>>(p, r, ops[o]->view(), dV.ptr, ext0, next, W.as<double>());
-        check_launch(ctx, "spmm_block");
-      }
-      if (r > 0 && p == 0)
-        MG_CUDA(cudaMemsetAsync(H.ptr, 0, sizeof(double) * r * r, s));
-      else
-        dgemm(ctx, CUBLAS_OP_T, CUBLAS_OP_N, r, r, p, Y, next, W.as<double>(), p, H.as<double>(), r);
-      deliver(ctx, outs[o], H.as<double>(), r * r, where);
-      MG_CUDA(cudaStreamSynchronize(s)); // H and W are reused by the next operator
+      const int64_t nt = (r + kPT - 1) / kPT, tiles = nt * nt;
+      int64_t splits = std::max<int64_t>(1, (4 * static_cast<int64_t>(ctx->num_sms) + tiles - 1) / tiles);
+      splits = std::min<int64_t>(splits, (p + kPR - 1) / kPR);
+      splits = std::min<int64_t>(splits, std::max<int64_t>(1, (int64_t{24} << 20) / (3 * r * r))); // partials <= 192 MB
+      int64_t per = (p + splits - 1) / splits;
+      per = (per + kPR - 1) / kPR * kPR;
+      splits = (p + per - 1) / per;
+      DBuf part(sizeof(double) * static_cast<size_t>(splits * 3 * r * r), s);
+      proj_fused<<<dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(splits)), 256, 0, s>>>(
+          p, r, M->view(), D->view(), K->view(), dV.ptr, ext0, next, row0 - ext0, per, part.as<double>());
+      check_launch(ctx, "proj_fused");
+      proj_reduce<<<blocks_for(3 * r * r), kThreads, 0, s>>>(r * r, static_cast<int>(splits), part.as<double>(),
+                                                            H.as<double>());
+      check_launch(ctx, "proj_reduce");
     }
+    double *outs[3] = {Mh, Dh, Kh};
+    for (int o = 0; o < 3; ++o)
+      deliver(ctx, outs[o], H.as<double>() + o * r * r, r * r, where);
+    MG_CUDA(cudaStreamSynchronize(s));
     if (m > 0) // airga.cpp:492: matmul_tn(V, F)
     {
       DBuf T(sizeof(double) * static_cast<size_t>(r * m > 0 ? r * m : 1), s);
       if (p == 0)
         MG_CUDA(cudaMemsetAsync(T.ptr, 0, sizeof(double) * r * m, s));
       else
-        dgemm(ctx, CUBLAS_OP_T, CUBLAS_OP_N, r, m, p, Y, next, dF.ptr, p, T.as<double>(), r);
+        gemm(ctx, true, r, m, p, 1.0, Y, next, dF.ptr, p, 0.0, T.as<double>(), r);
       deliver(ctx, Fh, T.as<double>(), r * m, where);
       MG_CUDA(cudaStreamSynchronize(s));
     }
@@ -594,7 +646,7 @@ int mgpu_project_reduce_slab(mgpu_ctx *ctx, const mgpu_csr *M, const mgpu_csr *D
         if (p == 0)
           MG_CUDA(cudaMemsetAsync(T.ptr, 0, sizeof(double) * q * r, s));
         else
-          dgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, q, r, p, o == 0 ? dCp.ptr : dCv.ptr, q, Y, next, T.as<double>(), q);
+          gemm(ctx, false, q, r, p, 1.0, o == 0 ? dCp.ptr : dCv.ptr, q, Y, next, 0.0, T.as<double>(), q);
         deliver(ctx, o == 0 ? Cph : Cvh, T.as<double>(), q * r, where);
         MG_CUDA(cudaStreamSynchronize(s));
       }

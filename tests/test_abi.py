@@ -87,3 +87,15 @@ def test_oracle_library_loads():
     for s in ["orc_spai_build", "orc_spai_update", "orc_spai_ls", "orc_pcg_solve", "orc_block_solve",
               "orc_shifted_operator", "orc_thin_qr", "orc_chain_apply"]:
         getattr(lib, s)
+
+
+def test_library_loads_before_torch():
+    """libmgpu.so links neither NCCL nor cuBLAS: loading it first must not hand torch a foreign
+    libnccl.so.2 (NCCL is resolved at the first mgpu_comm_* call, comm.cu)."""
+    code = ("import sys; sys.path.insert(0, %r); import paper_1606_01216_b200 as mg; mg.lib(); "
+            "import torch; print('ok')" % ROOT)
+    out = subprocess.run([__import__("sys").executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+    needed = subprocess.run(["readelf", "-d", os.path.join(ROOT, "paper_1606_01216_b200", "lib", "libmgpu.so")],
+                            capture_output=True, text=True).stdout
+    assert "nccl" not in needed and "cublas" not in needed
