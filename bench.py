@@ -96,6 +96,22 @@ def rhs_block(n: int, m: int) -> np.ndarray:
     return B
 
 
+def peak_fp64():
+    """Measured DFMA peak of this part (tools/fp64_peak.cu; profiles/fp64_peak.json), TFLOP/s."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as f:
+            return float(json.load(f)["dfma_tflops"]), "measured (profiles/fp64_peak.json)"
+    except Exception:
+        return None, "unavailable"
+
+
+def ls_flops_per_column(pattern):
+    """2|I||J|^2 - 2/3|J|^3 + 2|I||J| + |J|^2 for the interior Hermite problems
+    (A pattern 10 x 5, A^2 pattern 14 x 10)."""
+    ni, nj = (14, 10) if (pattern & 1) else (10, 5)
+    return 2 * ni * nj * nj - 2.0 / 3.0 * nj ** 3 + 2 * ni * nj + nj * nj
+
+
 def peak_hbm():
     try:
         with open(PEAKS) as f:
@@ -447,6 +463,18 @@ def run_mgpu(args, rank, world, local_rank):
         except Exception as e:  # reported, never silently replaced
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable", "sample": repr(e)}
 
+    spai_roof = None
+    if pattern >= 0:
+        fpk, fsrc = peak_fp64()
+        sp_ms = statistics.median(spai_ms)
+        alg = ls_flops_per_column(pattern) * n * l / (sp_ms * 1e-3) / 1e12
+        spai_roof = {"bound": "fp64", "achieved": alg, "peak": fpk, "unit": "TFLOP/s",
+                     "frac": alg / fpk if fpk else None, "peak_source": fsrc, "kernel": "ls_columns_lane",
+                     "flop_model": "algorithmic LS FLOPs per column (SURVEY 8d: 2|I||J|^2 - 2/3|J|^3 + 2|I||J| + |J|^2, "
+                                   "interior Hermite |I| x |J|) x columns / SPAI phase time; the kernel replays "
+                                   "thin_qr's explicit-Q schedule (about 2.3x these FLOPs) to stay bitwise with "
+                                   "the oracle"}
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -465,6 +493,7 @@ def run_mgpu(args, rank, world, local_rank):
                                     "fraction is reported for the contract" if args.workload in ("config0", "config1")
                                     else "HBM streaming"),
                          "bytes_model": "per iteration, per shift: 8 nnz(A) + 8 nnz(P) + 48 n m"},
+            "spai_roofline": spai_roof,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d_bytes,
                     "d2h_bytes_per_step": d2h_bytes,
                     "prepare_ms": 1e3 * statistics.median(p for p, _ in plug_split),

@@ -475,6 +475,233 @@ struct LaneLayout
   static constexpr int kWords = kWords0 | 1; // odd stride: conflict-free same-offset accesses
 };
 
+// The column's least-squares solve once S (= A(I, J), column-major at stride NI in W) and e are
+// staged: optional column equilibration, thin_qr, y = Q^T e, back-substitution; m written to out.
+// EX: the column fills the envelope exactly (|I| = NI, |J| = NJ -- every interior column of the
+// Hermite operators), so every loop has a compile-time trip count and unrolls without per-entry
+// guards; otherwise the same operations with run-time bounds.  False: rank deficiency.
+template <int NJ, int NI, bool CS, bool EX>
+__device__ __forceinline__ bool ls_lane_solve(double *W, double *diag, double *tau, double *mv, double *dsc,
+                                              const double (&e)[NI], int ni_rt, int nj_rt, double *out)
+{
+  const int ni = EX ? NI : ni_rt;
+  const int nj = EX ? NJ : nj_rt;
+  if (CS) // column equilibration: r_c = 1 / ||S_c|| (in-order dot), S_c *= r_c (oracle.c orc_spai_ls)
+  {
+    #pragma unroll(EX ? NJ : 1)
+    for (int c = 0; c < nj; ++c)
+    {
+      double *col = W + c * NI;
+      const double d = sqrt(dot_serial(col, col, ni));
+      if (d == 0.0)
+        return false;
+      const double r = 1.0 / d;
+      dsc[c] = r;
+      #pragma unroll(EX ? NI : 1)
+      for (int i = 0; i < ni; ++i)
+        col[i] = __dmul_rn(col[i], r);
+    }
+  }
+  // ---- thin_qr (dense.cpp:153-246): frob_norm tolerance in column-major order
+  double acc = 0.0;
+  #pragma unroll(EX ? NJ : 1)
+  for (int c = 0; c < nj; ++c)
+    #pragma unroll(EX ? NI : 1)
+    for (int i = 0; i < ni; ++i)
+      acc = __dadd_rn(acc, __dmul_rn(W[c * NI + i], W[c * NI + i]));
+  const double anorm = sqrt(acc);
+  const double tol = 1e-12 * (anorm > 0.0 ? anorm : 1.0);
+  // Householder steps.  The reflector x (column k below the diagonal) is held in registers for
+  // the whole trailing update, and the trailing columns are updated two at a time (two
+  // independent in-order dot chains, one shared-memory read of x per step): per column the
+  // operations and their order are exactly thin_qr's (dense.cpp:168-188).  A flushed column
+  // (sigma <= tol) makes the problem rank-deficient, which is an error whatever follows, so the
+  // lane stops there.
+  #pragma unroll(EX ? NJ : 1)
+  for (int k = 0; k < nj; ++k)
+  {
+    const int len = ni - k;
+    double *xs = W + k * NI + k;
+    double x[NI];
+#pragma unroll
+    for (int i = 0; i < NI; ++i)
+      x[i] = i < len ? xs[i] : 0.0;
+    double acc2 = 0.0;
+#pragma unroll
+    for (int i = 0; i < NI; ++i)
+      if (i < len)
+        acc2 = __dadd_rn(acc2, __dmul_rn(x[i], x[i]));
+    const double sigma = sqrt(acc2);
+    if (sigma <= tol)
+      return false; // rank < |J|
+    const double alpha = x[0] >= 0.0 ? -sigma : sigma;
+    x[0] = __dsub_rn(x[0], alpha);
+    xs[0] = x[0];
+    double vtv = 0.0;
+#pragma unroll
+    for (int i = 0; i < NI; ++i)
+      if (i < len)
+        vtv = __dadd_rn(vtv, __dmul_rn(x[i], x[i]));
+    const double tk = vtv > 0.0 ? 2.0 / vtv : 0.0;
+    tau[k] = tk;
+    diag[k] = alpha;
+    if (tk == 0.0)
+      continue;
+    int c = k + 1;
+    #pragma unroll(EX ? NJ : 1)
+    for (; c + 1 < nj; c += 2)
+    {
+      double *ya = W + c * NI + k, *yb = ya + NI;
+      double y0[NI], y1[NI];
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int i = 0; i < NI; ++i)
+        if (i < len)
+        {
+          y0[i] = ya[i];
+          y1[i] = yb[i];
+          a0 = __dadd_rn(a0, __dmul_rn(x[i], y0[i]));
+          a1 = __dadd_rn(a1, __dmul_rn(x[i], y1[i]));
+        }
+      const double s0 = -__dmul_rn(tk, a0), s1 = -__dmul_rn(tk, a1);
+#pragma unroll
+      for (int i = 0; i < NI; ++i)
+        if (i < len)
+        {
+          ya[i] = __dadd_rn(y0[i], __dmul_rn(s0, x[i]));
+          yb[i] = __dadd_rn(y1[i], __dmul_rn(s1, x[i]));
+        }
+    }
+    if (c < nj)
+    {
+      double *ya = W + c * NI + k;
+      double y0[NI];
+      double a0 = 0.0;
+#pragma unroll
+      for (int i = 0; i < NI; ++i)
+        if (i < len)
+        {
+          y0[i] = ya[i];
+          a0 = __dadd_rn(a0, __dmul_rn(x[i], y0[i]));
+        }
+      const double s0 = -__dmul_rn(tk, a0);
+#pragma unroll
+      for (int i = 0; i < NI; ++i)
+        if (i < len)
+          ya[i] = __dadd_rn(y0[i], __dmul_rn(s0, x[i]));
+    }
+  }
+  // ---- y_c = (sign-fixed column c of Q = H_0 ... H_{nj-1} e_c)^T e.  Columns c and c + 1 are
+  // formed together in registers: q1 takes reflector c + 1 alone, then both take c .. 0, so each
+  // column sees thin_qr's reflector sequence (dense.cpp:200-218) and every reflector is read
+  // from shared memory once per pair.
+  #pragma unroll(EX ? NJ : 1)
+  for (int c = 0; c < nj; c += 2)
+  {
+    const bool two = c + 1 < nj;
+    double q0[NI], q1[NI];
+#pragma unroll
+    for (int i = 0; i < NI; ++i)
+    {
+      q0[i] = i == c ? 1.0 : 0.0;
+      q1[i] = i == c + 1 ? 1.0 : 0.0;
+    }
+#pragma unroll
+    for (int k = NJ - 1; k >= 0; --k)
+    {
+      if (k > c + 1 || (k == c + 1 && !two))
+        continue;
+      const double tk = tau[k];
+      if (tk == 0.0)
+        continue;
+      const double *vs = W + k * NI + k;
+      const int len = ni - k;
+      double v[NI];
+#pragma unroll
+      for (int i = 0; i + k < NI; ++i)
+        v[i] = i < len ? vs[i] : 0.0;
+      if (k == c + 1) // q1 only
+      {
+        double a1 = 0.0;
+#pragma unroll
+        for (int i = 0; i + k < NI; ++i)
+          if (i < len)
+            a1 = __dadd_rn(a1, __dmul_rn(v[i], q1[k + i]));
+        const double s1 = -__dmul_rn(tk, a1);
+#pragma unroll
+        for (int i = 0; i + k < NI; ++i)
+          if (i < len)
+            q1[k + i] = __dadd_rn(q1[k + i], __dmul_rn(s1, v[i]));
+        continue;
+      }
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int i = 0; i + k < NI; ++i)
+        if (i < len)
+        {
+          a0 = __dadd_rn(a0, __dmul_rn(v[i], q0[k + i]));
+          a1 = __dadd_rn(a1, __dmul_rn(v[i], q1[k + i]));
+        }
+      const double s0 = -__dmul_rn(tk, a0), s1 = -__dmul_rn(tk, a1);
+#pragma unroll
+      for (int i = 0; i + k < NI; ++i)
+        if (i < len)
+        {
+          q0[k + i] = __dadd_rn(q0[k + i], __dmul_rn(s0, v[i]));
+          if (two)
+            q1[k + i] = __dadd_rn(q1[k + i], __dmul_rn(s1, v[i]));
+        }
+    }
+    if (diag[c] < 0.0)
+    {
+#pragma unroll
+      for (int i = 0; i < NI; ++i)
+        q0[i] = __dmul_rn(q0[i], -1.0);
+    }
+    if (two && diag[c + 1] < 0.0)
+    {
+#pragma unroll
+      for (int i = 0; i < NI; ++i)
+        q1[i] = __dmul_rn(q1[i], -1.0);
+    }
+    double y0 = 0.0, y1 = 0.0;
+#pragma unroll
+    for (int i = 0; i < NI; ++i)
+      if (i < ni)
+      {
+        y0 = __dadd_rn(y0, __dmul_rn(q0[i], e[i]));
+        y1 = __dadd_rn(y1, __dmul_rn(q1[i], e[i]));
+      }
+    mv[c] = y0;
+    if (two)
+      mv[c + 1] = y1;
+  }
+  // ---- sign fix of R's off-diagonal rows (R(k, c) = W[c][k], c > k), |R_cc|
+  #pragma unroll(EX ? NJ : 1)
+  for (int c = 0; c < nj; ++c)
+  {
+    for (int k = 0; k < c; ++k)
+      if (diag[k] < 0.0)
+        W[c * NI + k] = -W[c * NI + k];
+    tau[c] = diag[c] < 0.0 ? -diag[c] : diag[c];
+  }
+  // ---- back-substitution R m = y (acc = y_k; acc -= R_kq m_q, q ascending)
+  #pragma unroll(EX ? NJ : 1)
+  for (int k = nj - 1; k >= 0; --k)
+  {
+    double a = mv[k];
+    #pragma unroll(EX ? NJ : 1)
+    for (int c = k + 1; c < nj; ++c)
+      a = __dsub_rn(a, __dmul_rn(W[c * NI + k], mv[c]));
+    mv[k] = a / tau[k];
+  }
+#pragma unroll(EX ? NJ : 1)
+  #pragma unroll(EX ? NJ : 1)
+  for (int c = 0; c < nj; ++c)
+    out[c] = CS ? __dmul_rn(mv[c], dsc[c]) : mv[c];
+  return true;
+}
+
 template <int NJ, int NI, bool CS>
 __global__ void __launch_bounds__(64) ls_columns_lane(int64_t n, int l, DCsr pat, DCsr At, int64_t at_stride,
                                                        DCsr Kot, int64_t ko_stride, bool update,
@@ -585,213 +812,11 @@ __global__ void __launch_bounds__(64) ls_columns_lane(int64_t n, int l, DCsr pat
       if (i < ni && I[i] == j)
         e[i] = 1.0;
   }
-  if (CS) // column equilibration: r_c = 1 / ||S_c|| (in-order dot), S_c *= r_c (oracle.c orc_spai_ls)
-  {
-    for (int c = 0; c < nj; ++c)
-    {
-      double *col = W + c * NI;
-      const double d = sqrt(dot_serial(col, col, ni));
-      if (d == 0.0)
-      {
-        report(err, g, MGPU_ERR_NUMERICAL);
-        return;
-      }
-      const double r = 1.0 / d;
-      dsc[c] = r;
-      for (int i = 0; i < ni; ++i)
-        col[i] = __dmul_rn(col[i], r);
-    }
-  }
-  // ---- thin_qr (dense.cpp:153-246): frob_norm tolerance in column-major order
-  double acc = 0.0;
-  for (int c = 0; c < nj; ++c)
-    for (int i = 0; i < ni; ++i)
-      acc = __dadd_rn(acc, __dmul_rn(W[c * NI + i], W[c * NI + i]));
-  const double anorm = sqrt(acc);
-  const double tol = 1e-12 * (anorm > 0.0 ? anorm : 1.0);
-  // Householder steps.  The reflector x (column k below the diagonal) is held in registers for
-  // the whole trailing update, and the trailing columns are updated two at a time (two
-  // independent in-order dot chains, one shared-memory read of x per step): per column the
-  // operations and their order are exactly thin_qr's (dense.cpp:168-188).  A flushed column
-  // (sigma <= tol) makes the problem rank-deficient, which is an error whatever follows, so the
-  // lane stops there.
-  for (int k = 0; k < nj; ++k)
-  {
-    const int len = ni - k;
-    double *xs = W + k * NI + k;
-    double x[NI];
-#pragma unroll
-    for (int i = 0; i < NI; ++i)
-      x[i] = i < len ? xs[i] : 0.0;
-    double acc2 = 0.0;
-#pragma unroll
-    for (int i = 0; i < NI; ++i)
-      if (i < len)
-        acc2 = __dadd_rn(acc2, __dmul_rn(x[i], x[i]));
-    const double sigma = sqrt(acc2);
-    if (sigma <= tol)
-    {
-      report(err, g, MGPU_ERR_NUMERICAL); // rank < |J|
-      return;
-    }
-    const double alpha = x[0] >= 0.0 ? -sigma : sigma;
-    x[0] = __dsub_rn(x[0], alpha);
-    xs[0] = x[0];
-    double vtv = 0.0;
-#pragma unroll
-    for (int i = 0; i < NI; ++i)
-      if (i < len)
-        vtv = __dadd_rn(vtv, __dmul_rn(x[i], x[i]));
-    const double tk = vtv > 0.0 ? 2.0 / vtv : 0.0;
-    tau[k] = tk;
-    diag[k] = alpha;
-    if (tk == 0.0)
-      continue;
-    int c = k + 1;
-    for (; c + 1 < nj; c += 2)
-    {
-      double *ya = W + c * NI + k, *yb = ya + NI;
-      double y0[NI], y1[NI];
-      double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-      for (int i = 0; i < NI; ++i)
-        if (i < len)
-        {
-          y0[i] = ya[i];
-          y1[i] = yb[i];
-          a0 = __dadd_rn(a0, __dmul_rn(x[i], y0[i]));
-          a1 = __dadd_rn(a1, __dmul_rn(x[i], y1[i]));
-        }
-      const double s0 = -__dmul_rn(tk, a0), s1 = -__dmul_rn(tk, a1);
-#pragma unroll
-      for (int i = 0; i < NI; ++i)
-        if (i < len)
-        {
-          ya[i] = __dadd_rn(y0[i], __dmul_rn(s0, x[i]));
-          yb[i] = __dadd_rn(y1[i], __dmul_rn(s1, x[i]));
-        }
-    }
-    if (c < nj)
-    {
-      double *ya = W + c * NI + k;
-      double y0[NI];
-      double a0 = 0.0;
-#pragma unroll
-      for (int i = 0; i < NI; ++i)
-        if (i < len)
-        {
-          y0[i] = ya[i];
-          a0 = __dadd_rn(a0, __dmul_rn(x[i], y0[i]));
-        }
-      const double s0 = -__dmul_rn(tk, a0);
-#pragma unroll
-      for (int i = 0; i < NI; ++i)
-        if (i < len)
-          ya[i] = __dadd_rn(y0[i], __dmul_rn(s0, x[i]));
-    }
-  }
-  // ---- y_c = (sign-fixed column c of Q = H_0 ... H_{nj-1} e_c)^T e.  Columns c and c + 1 are
-  // formed together in registers: q1 takes reflector c + 1 alone, then both take c .. 0, so each
-  // column sees thin_qr's reflector sequence (dense.cpp:200-218) and every reflector is read
-  // from shared memory once per pair.
-  for (int c = 0; c < nj; c += 2)
-  {
-    const bool two = c + 1 < nj;
-    double q0[NI], q1[NI];
-#pragma unroll
-    for (int i = 0; i < NI; ++i)
-    {
-      q0[i] = i == c ? 1.0 : 0.0;
-      q1[i] = i == c + 1 ? 1.0 : 0.0;
-    }
-#pragma unroll
-    for (int k = NJ - 1; k >= 0; --k)
-    {
-      if (k > c + 1 || (k == c + 1 && !two))
-        continue;
-      const double tk = tau[k];
-      if (tk == 0.0)
-        continue;
-      const double *vs = W + k * NI + k;
-      const int len = ni - k;
-      double v[NI];
-#pragma unroll
-      for (int i = 0; i + k < NI; ++i)
-        v[i] = i < len ? vs[i] : 0.0;
-      if (k == c + 1) // q1 only
-      {
-        double a1 = 0.0;
-#pragma unroll
-        for (int i = 0; i + k < NI; ++i)
-          if (i < len)
-            a1 = __dadd_rn(a1, __dmul_rn(v[i], q1[k + i]));
-        const double s1 = -__dmul_rn(tk, a1);
-#pragma unroll
-        for (int i = 0; i + k < NI; ++i)
-          if (i < len)
-            q1[k + i] = __dadd_rn(q1[k + i], __dmul_rn(s1, v[i]));
-        continue;
-      }
-      double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-      for (int i = 0; i + k < NI; ++i)
-        if (i < len)
-        {
-          a0 = __dadd_rn(a0, __dmul_rn(v[i], q0[k + i]));
-          a1 = __dadd_rn(a1, __dmul_rn(v[i], q1[k + i]));
-        }
-      const double s0 = -__dmul_rn(tk, a0), s1 = -__dmul_rn(tk, a1);
-#pragma unroll
-      for (int i = 0; i + k < NI; ++i)
-        if (i < len)
-        {
-          q0[k + i] = __dadd_rn(q0[k + i], __dmul_rn(s0, v[i]));
-          if (two)
-            q1[k + i] = __dadd_rn(q1[k + i], __dmul_rn(s1, v[i]));
-        }
-    }
-    if (diag[c] < 0.0)
-    {
-#pragma unroll
-      for (int i = 0; i < NI; ++i)
-        q0[i] = __dmul_rn(q0[i], -1.0);
-    }
-    if (two && diag[c + 1] < 0.0)
-    {
-#pragma unroll
-      for (int i = 0; i < NI; ++i)
-        q1[i] = __dmul_rn(q1[i], -1.0);
-    }
-    double y0 = 0.0, y1 = 0.0;
-#pragma unroll
-    for (int i = 0; i < NI; ++i)
-      if (i < ni)
-      {
-        y0 = __dadd_rn(y0, __dmul_rn(q0[i], e[i]));
-        y1 = __dadd_rn(y1, __dmul_rn(q1[i], e[i]));
-      }
-    mv[c] = y0;
-    if (two)
-      mv[c + 1] = y1;
-  }
-  // ---- sign fix of R's off-diagonal rows (R(k, c) = W[c][k], c > k), |R_cc|
-  for (int c = 0; c < nj; ++c)
-  {
-    for (int k = 0; k < c; ++k)
-      if (diag[k] < 0.0)
-        W[c * NI + k] = -W[c * NI + k];
-    tau[c] = diag[c] < 0.0 ? -diag[c] : diag[c];
-  }
-  // ---- back-substitution R m = y (acc = y_k; acc -= R_kq m_q, q ascending)
-  for (int k = nj - 1; k >= 0; --k)
-  {
-    double a = mv[k];
-    for (int c = k + 1; c < nj; ++c)
-      a = __dsub_rn(a, __dmul_rn(W[c * NI + k], mv[c]));
-    mv[k] = a / tau[k];
-  }
-  for (int c = 0; c < nj; ++c)
-    out_vals[jb + c] = CS ? __dmul_rn(mv[c], dsc[c]) : mv[c];
+  const bool solved = (ni == NI && nj == NJ)
+                          ? ls_lane_solve<NJ, NI, CS, true>(W, diag, tau, mv, dsc, e, ni, nj, out_vals + jb)
+                          : ls_lane_solve<NJ, NI, CS, false>(W, diag, tau, mv, dsc, e, ni, nj, out_vals + jb);
+  if (!solved)
+    report(err, g, MGPU_ERR_NUMERICAL);
 }
 
 // TPB: threads per block (32 packs the per-lane scratch more tightly for small envelopes)
@@ -875,14 +900,17 @@ bool run_ls(mgpu_ctx *ctx, bool cs, int64_t n, int l, int maxrow, DCsr pat, DCsr
     int nj;
     bool lane;
   };
-  static constexpr Env kEnv[] = {{5, true}, {6, true}, {8, true}, {10, true}, {10, true}, {8, false}, {16, false},
-                                 {32, false}};
-  for (int cfg = 0; cfg < 8; ++cfg)
+  // <5, 10> is the exact Hermite A-pattern problem (every interior column: |I| = 10, |J| = 5), which
+  // takes ls_lane_solve's fully unrolled path; a column with more rows overflows it and the batch
+  // reruns on <5, 13>.  <10, 14> is the exact A^2-pattern problem.
+  static constexpr Env kEnv[] = {{5, true}, {5, true}, {6, true}, {8, true}, {10, true}, {10, true}, {8, false},
+                                 {16, false}, {32, false}};
+  for (int cfg = 0; cfg < 9; ++cfg)
   {
     const int G = kEnv[cfg].nj;
     if (maxrow > G || (kEnv[cfg].lane && !lanes))
       continue;
-    if (cfg == 0 && !(pat_bw >= 0 && 4 * pat_bw + 1 <= 13))
+    if (cfg == 1 && !(pat_bw >= 0 && 4 * pat_bw + 1 <= 13))
       continue;
     MG_CUDA(cudaMemsetAsync(err.ptr, 0xff, sizeof(unsigned long long), ctx->stream));
     MG_CUDA(cudaMemsetAsync(ovf.ptr, 0, sizeof(int), ctx->stream));
@@ -890,30 +918,34 @@ bool run_ls(mgpu_ctx *ctx, bool cs, int64_t n, int l, int maxrow, DCsr pat, DCsr
     switch (cfg)
     {
     case 0:
-      launch_ls_lane<5, 13, 32>(ctx, cs, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev,
+      launch_ls_lane<5, 10, 32>(ctx, cs, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev,
                                 ovf.as<int>());
       break;
     case 1:
+      launch_ls_lane<5, 13, 32>(ctx, cs, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev,
+                                ovf.as<int>());
+      break;
+    case 2:
       launch_ls_lane<6, 14>(ctx, cs, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev,
                             ovf.as<int>());
       break;
-    case 2:
+    case 3:
       launch_ls_lane<8, 16>(ctx, cs, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev,
                             ovf.as<int>());
       break;
-    case 3: // the A^2 pattern of the Hermite beam: |J| = 10, |I| = 14
+    case 4: // the A^2 pattern of the Hermite beam: |J| = 10, |I| = 14
       launch_ls_lane<10, 14, 32>(ctx, cs, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev,
                                  ovf.as<int>());
       break;
-    case 4:
+    case 5:
       launch_ls_lane<10, 18, 32>(ctx, cs, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev,
                                  ovf.as<int>());
       break;
-    case 5:
+    case 6:
       launch_ls<8, 16, 4>(ctx, cs, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev,
                           ovf.as<int>());
       break;
-    case 6:
+    case 7:
       launch_ls<16, 32, 2>(ctx, cs, n, l, pat, At, at_stride, Kot, ko_stride, update, out, out_stride, ev,
                            ovf.as<int>());
       break;

@@ -2,7 +2,7 @@
 workloads: c1 (n=2e4, 8 shifts, A), c3 (n=1e6, 16 shifts, A^2 colscale), c4 (n=1e7, 8 shifts, A colscale).
 Time = CUDA events around mgpu_spai_ls_batched on the context stream (median of 5 after 2 warm-ups).
 Algorithmic FLOPs per column: 2|I||J|^2 - 2/3|J|^3 + 2|I||J| + |J|^2 with the Hermite
-|I| x |J| = 10 x 5 (A pattern; 13 x 5 in the interior counting the I union) / 14 x 10 (A^2)."""
+|I| x |J| = 10 x 5 (A pattern) / 14 x 10 (A^2) of the interior columns."""
 import json, os, statistics, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -31,7 +31,7 @@ for name in (sys.argv[1:] or ["c1", "c3"]):
         del f
     ms = statistics.median(ts)
     n = 2 * ne
-    nj, ni = (10, 14) if pat & 1 else (5, 13)
+    nj, ni = (10, 14) if pat & 1 else (5, 10)  # interior Hermite columns
     flop = 2 * ni * nj * nj - 2 / 3 * nj ** 3 + 2 * ni * nj + nj * nj
     tf = flop * n * l / (ms * 1e-3) / 1e12
     print(json.dumps({"workload": name, "n": n, "shifts": l, "pattern": hex(pat), "ms": ms, "columns_per_s": n * l / (ms * 1e-3),
