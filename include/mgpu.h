@@ -183,7 +183,7 @@ int mgpu_chain_quality(mgpu_ctx *ctx, int z, const mgpu_csr *const *factors, con
 
 typedef enum mgpu_spai_mode
 {
-  MGPU_SPAI_SEQUENTIAL = 0, /* spai.hpp:38-42 (device: dense built factor, n <= 8192, else MGPU_ERR_UNSUPPORTED) */
+  MGPU_SPAI_SEQUENTIAL = 0, /* spai.hpp:38-42 (device: sparse row lists of the built columns, any n) */
   MGPU_SPAI_FROZEN = 1,
 } mgpu_spai_mode;
 

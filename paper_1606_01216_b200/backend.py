@@ -13,7 +13,7 @@ Config fields are AirgaConfig's (airga.hpp:40-69) plus the GPU-only choices
 spai_algorithm ("mr" = the reference's Alg. 2/4, "ls" = static-pattern
 least squares) and ls_pattern (A or A^2).  spai_mode is the reference's
 (sequential by default in AirgaConfig; the device sequential mode keeps the
-built factor dense and is bounded at n <= 8192, frozen mode has no bound).
+built columns as sparse row lists, frozen mode is column-parallel).
 """
 from __future__ import annotations
 

@@ -1,24 +1,24 @@
-// K-mr in SEQUENTIAL mode (spai.cpp:113-209 with SpaiOptions::Mode::sequential,
-// the reference default): column j's step d = P r applies the columns 0..j-1
-// that are already built (spai.cpp:138-158), so columns are processed in
-// order.  One cooperative persistent kernel walks the columns; every MR
-// iteration is three grid-wide phases:
+// K-mr in SEQUENTIAL mode (spai.cpp:113-209 with SpaiOptions::Mode::sequential, the reference
+// default): column j's step d = P r applies the columns 0..j-1 already built (spai.cpp:138-158),
+// so columns are processed in order and the build is a serial column chain.  One persistent
+// block walks the columns (the chain leaves nothing to spread over SMs but each step's rows);
+// the factor is kept SPARSE, so n is bounded only by memory:
 //
-//   d = P r      one warp per row: d_row = sum_{i < j} r_i P(row, i), then the
-//                unbuilt self term alpha r_row for row >= j (it follows the
-//                built columns in the reference's ascending-i order);
-//   w = K d      one thread per row, ascending column (spai.cpp:159-169),
-//                with the (w, w) and (w, r) block partials;
-//   p += a d, r += (-a) w, ||r||^2 partials (spai.cpp:185-195).
-//
-// The built part of P is a dense row-major n x n array (a warp reads one row
-// coalesced), so the device mode is bounded at n <= kSeqMaxN.  Sums the
-// reference takes serially over sorted supports (ww, rw, ||r||^2 and the
-// per-row d sum) are fixed-order trees here: deterministic, ~1e-16 relative
-// from the serial order.  A dense slot that is not in a Spa's support holds an
-// exact zero and contributes an exact zero, so the dense sums equal the sparse
-// ones up to that reordering.
-#include <cooperative_groups.h>
+//   built factor   row lists: row i holds (column, value) of the built columns with an entry in row
+//                  i, columns ascending (appended in build order), capacity `cap` per row;
+//   supports       every accumulator (p, r, d, w) is a dense n-vector that is zero outside an index
+//                  range [lo, hi] tracked per accumulator (the reference's Spa with a sorted
+//                  support, spai.cpp:22-68; an index inside the range but outside the support
+//                  holds an exact zero and contributes nothing);
+//   d = P r        one thread per row of d's range: the row's list entries with a column inside r's
+//                  range, ascending, each r_i P(row, i) with r_i != 0, then the unbuilt self term
+//                  alpha r_row for row >= j -- per row exactly the reference's ascending-i
+//                  accumulation (bitwise);
+//   w = K d        one thread per row, K's row in ascending column (spai.cpp:159-169, bitwise);
+//   ww, rw, ||r||^2  fixed-order block trees over the ranges (the reference sums serially over the
+//                  sorted support: ~1e-16 relative, deterministic);
+//   p += a d, r += (-a) w (spai.cpp:185-195), then the column's nonzeros are appended to the row
+//   lists and the accumulators cleared over their ranges.
 #include <cub/cub.cuh>
 
 #include <climits>
@@ -28,8 +28,6 @@
 
 #include "internal.cuh"
 
-namespace cgrp = cooperative_groups;
-
 namespace mgpu
 {
 mgpu_csr *transpose_csr(mgpu_ctx *ctx, const mgpu_csr *A);
@@ -37,16 +35,16 @@ mgpu_csr *transpose_csr(mgpu_ctx *ctx, const mgpu_csr *A);
 namespace
 {
 
-constexpr int kSeqTB = 256;
-constexpr int64_t kSeqMaxN = 8192;
+constexpr int kSeqTB = 1024;
 
 enum SeqFail : int
 {
   kSeqOk = 0,
-  kSeqStall = 1,       // spai.cpp:129-135
-  kSeqZeroCurv = 2,    // spai.cpp:178
-  kSeqNonFiniteW = 3,  // spai.cpp:174-177
-  kSeqNonFiniteA = 4,  // spai.cpp:181-184
+  kSeqStall = 1,      // spai.cpp:129-135
+  kSeqZeroCurv = 2,   // spai.cpp:178
+  kSeqNonFiniteW = 3, // spai.cpp:174-177
+  kSeqNonFiniteA = 4, // spai.cpp:181-184
+  kSeqCapacity = 5,   // a row list is full (host retries with a larger capacity)
 };
 
 struct SeqArgs
@@ -57,11 +55,15 @@ struct SeqArgs
   DCsr Rt; // columns of the rhs operator (update); rp == nullptr for the build
   double alpha, tol_sq;
   int64_t max_iters;
-  double *P; // dense row-major: P[row * n + i] = entry (row, i) of built column i
-  double *p, *r, *d, *w;
-  double *partial;  // [3][gridDim.x]
-  double *residual; // [n]
-  int *fail;        // [0] code, [1] spare
+  int64_t bwK;        // bandwidth of K (w's range around d's)
+  int64_t cap;        // row-list capacity
+  int32_t *rl_cnt;    // [n]
+  int32_t *rl_col;    // [n * cap]
+  double *rl_val;     // [n * cap]
+  int64_t *col_lo, *col_hi; // [n] row range of built column i (lo > hi: empty)
+  double *p, *r, *d, *w;    // dense, zero outside their ranges
+  double *residual;         // [n]
+  int *fail;
   int64_t *fail_col, *fail_iters;
   double *fail_rn;
 };
@@ -74,7 +76,7 @@ __device__ __forceinline__ double warp_sum(double v)
   return v;
 }
 
-// Block sum of v (fixed tree), result valid in thread 0.
+// Block sum (fixed tree), the same value in every thread.
 __device__ double block_sum(double v, double *red)
 {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -82,44 +84,40 @@ __device__ double block_sum(double v, double *red)
   if (lane == 0)
     red[warp] = v;
   __syncthreads();
-  double t = 0.0;
-  if (warp == 0)
-  {
-    t = lane < kSeqTB / 32 ? red[lane] : 0.0;
-    t = warp_sum(t);
-  }
+  double t = lane < kSeqTB / 32 ? red[lane] : 0.0;
+  t = warp_sum(t);
   __syncthreads();
   return t;
 }
 
-// Sum of partial[0..G) in a fixed order, the same value in every block.
-__device__ double grid_total(const double *partial, double *red)
+__device__ int64_t block_min(int64_t v, int64_t *red)
 {
-  double v = 0.0;
-  for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += kSeqTB)
-    v = __dadd_rn(v, __ldcg(partial + b));
-  v = block_sum(v, red);
-  if (threadIdx.x == 0)
-    red[kSeqTB / 32] = v;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1)
+    v = min(v, static_cast<int64_t>(__shfl_xor_sync(0xffffffffu, static_cast<long long>(v), off)));
+  if (lane == 0)
+    red[warp] = v;
   __syncthreads();
-  const double t = red[kSeqTB / 32];
+  int64_t t = lane < kSeqTB / 32 ? red[lane] : LLONG_MAX;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1)
+    t = min(t, static_cast<int64_t>(__shfl_xor_sync(0xffffffffu, static_cast<long long>(t), off)));
   __syncthreads();
   return t;
 }
 
-__global__ void __launch_bounds__(kSeqTB) mr_sequential(SeqArgs a)
+__device__ int64_t block_max(int64_t v, int64_t *red) { return -block_min(-v, red); }
+
+__global__ void __launch_bounds__(kSeqTB, 1) mr_sequential(SeqArgs a)
 {
-  cgrp::grid_group grid = cgrp::this_grid();
-  __shared__ double red[kSeqTB / 32 + 1];
+  __shared__ double red[kSeqTB / 32];
+  __shared__ int64_t ired[kSeqTB / 32];
   const int64_t n = a.n;
-  const int64_t G = gridDim.x;
-  const int64_t gt = static_cast<int64_t>(blockIdx.x) * kSeqTB + threadIdx.x;
-  const int64_t gs = G * kSeqTB;
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = gt >> 5, nw = gs >> 5;
-  double *ww_part = a.partial, *rw_part = a.partial + G, *rn_part = a.partial + 2 * G;
+  const int t = threadIdx.x;
+  double *p = a.p, *r = a.r, *d = a.d, *w = a.w;
   auto fail = [&](int code, int64_t j, double rn, int64_t it) {
-    if (gt == 0)
+    if (t == 0)
     {
       a.fail[0] = code;
       *a.fail_col = j;
@@ -127,42 +125,55 @@ __global__ void __launch_bounds__(kSeqTB) mr_sequential(SeqArgs a)
       *a.fail_rn = rn;
     }
   };
-  auto rnorm_sq = [&]() {
-    double v = 0.0;
-    for (int64_t i = gt; i < n; i += gs)
-    {
-      const double ri = __ldcg(a.r + i);
-      v = __dadd_rn(v, __dmul_rn(ri, ri));
-    }
-    v = block_sum(v, red);
-    if (threadIdx.x == 0)
-      rn_part[blockIdx.x] = v;
-    grid.sync();
-    return grid_total(rn_part, red);
-  };
   for (int64_t j = 0; j < n; ++j)
   {
     // ---- p = alpha e_j ; r = rhs - alpha K e_j   (spai.cpp:119-122)
-    for (int64_t i = gt; i < n; i += gs)
-    {
-      a.p[i] = i == j ? a.alpha : 0.0;
-      a.r[i] = 0.0;
-    }
-    grid.sync();
+    int64_t r_lo = j, r_hi = j;
+    if (t == 0)
+      p[j] = a.alpha;
     if (a.Rt.rp)
     {
-      for (int64_t q = a.Rt.rp[j] + gt; q < a.Rt.rp[j + 1]; q += gs)
-        a.r[a.Rt.ci[q]] = __dmul_rn(1.0, a.Rt.v[q]);
+      for (int64_t q = a.Rt.rp[j] + t; q < a.Rt.rp[j + 1]; q += kSeqTB)
+        r[a.Rt.ci[q]] = __dmul_rn(1.0, a.Rt.v[q]);
+      if (a.Rt.rp[j + 1] > a.Rt.rp[j])
+      {
+        r_lo = a.Rt.ci[a.Rt.rp[j]];
+        r_hi = a.Rt.ci[a.Rt.rp[j + 1] - 1];
+      }
+      else
+        r_lo = 0, r_hi = -1; // empty (lo > hi)
     }
-    else if (gt == 0)
-      a.r[j] = 1.0;
-    grid.sync();
-    for (int64_t q = a.Kt.rp[j] + gt; q < a.Kt.rp[j + 1]; q += gs)
+    else if (t == 0)
+      r[j] = 1.0;
+    __syncthreads();
+    for (int64_t q = a.Kt.rp[j] + t; q < a.Kt.rp[j + 1]; q += kSeqTB)
     {
       const int64_t i = a.Kt.ci[q];
-      a.r[i] = __dadd_rn(__ldcg(a.r + i), __dmul_rn(-a.alpha, a.Kt.v[q]));
+      r[i] = __dadd_rn(r[i], __dmul_rn(-a.alpha, a.Kt.v[q]));
     }
-    grid.sync();
+    // ranges: [lo, hi], empty when lo > hi; unite() is the union's hull
+    auto unite = [](int64_t &lo, int64_t &hi, int64_t lo2, int64_t hi2) {
+      if (lo2 > hi2)
+        return;
+      if (lo > hi)
+      {
+        lo = lo2;
+        hi = hi2;
+        return;
+      }
+      lo = min(lo, lo2);
+      hi = max(hi, hi2);
+    };
+    if (a.Kt.rp[j + 1] > a.Kt.rp[j])
+      unite(r_lo, r_hi, a.Kt.ci[a.Kt.rp[j]], a.Kt.ci[a.Kt.rp[j + 1] - 1]);
+    int64_t p_lo = j, p_hi = j, d_lo = 0, d_hi = -1, w_lo = 0, w_hi = -1;
+    __syncthreads();
+    auto rnorm_sq = [&]() {
+      double v = 0.0;
+      for (int64_t i = r_lo + t; i <= r_hi; i += kSeqTB)
+        v = __dadd_rn(v, __dmul_rn(r[i], r[i]));
+      return block_sum(v, red);
+    };
     double rn = rnorm_sq();
     int64_t iters = 0;
     while (rn > a.tol_sq)
@@ -172,51 +183,93 @@ __global__ void __launch_bounds__(kSeqTB) mr_sequential(SeqArgs a)
         fail(kSeqStall, j, sqrt(rn), iters);
         return;
       }
-      // ---- d = P r  (built columns i < j), + alpha r_row for the unbuilt column row >= j
-      for (int64_t row = gw; row < n; row += nw)
+      // ---- d's range: built columns i < j in r's support spread over [col_lo, col_hi]; unbuilt
+      // indices contribute to themselves
+      int64_t lo = LLONG_MAX, hi = -1;
+      for (int64_t i = r_lo + t; i <= r_hi; i += kSeqTB)
       {
-        const double *prow = a.P + row * n;
-        double acc = 0.0;
-        for (int64_t i = lane; i < j; i += 32)
-          acc = __dadd_rn(acc, __dmul_rn(__ldcg(a.r + i), __ldcg(prow + i)));
-        acc = warp_sum(acc);
-        if (lane == 0)
+        if (r[i] == 0.0)
+          continue;
+        if (i < j)
         {
-          if (row >= j)
+          if (a.col_lo[i] <= a.col_hi[i])
           {
-            const double rr = __ldcg(a.r + row);
-            if (rr != 0.0)
-              acc = __dadd_rn(acc, __dmul_rn(a.alpha, rr));
+            lo = min(lo, a.col_lo[i]);
+            hi = max(hi, a.col_hi[i]);
           }
-          a.d[row] = acc;
+        }
+        else
+        {
+          lo = min(lo, i);
+          hi = max(hi, i);
         }
       }
-      grid.sync();
-      // ---- w = K d, (w, w), (w, r)
+      int64_t nd_lo = block_min(lo, ired), nd_hi = block_max(hi, ired);
+      if (nd_lo > nd_hi)
+        nd_lo = 0, nd_hi = -1;
+      // clear the previous d range, then d = P r over the new one
+      for (int64_t i = d_lo + t; i <= d_hi; i += kSeqTB)
+        d[i] = 0.0;
+      __syncthreads();
+      d_lo = nd_lo;
+      d_hi = nd_hi;
+      const int64_t ib = min(r_hi, j - 1); // built columns inside r's range: [r_lo, ib]
+      for (int64_t row = d_lo + t; row <= d_hi; row += kSeqTB)
+      {
+        const int32_t cnt = a.rl_cnt[row];
+        const int32_t *cols = a.rl_col + row * a.cap;
+        const double *vals = a.rl_val + row * a.cap;
+        int lo2 = 0, hi2 = cnt; // first list entry with column >= r_lo
+        while (lo2 < hi2)
+        {
+          const int mid = (lo2 + hi2) >> 1;
+          if (cols[mid] < r_lo)
+            lo2 = mid + 1;
+          else
+            hi2 = mid;
+        }
+        double acc = 0.0;
+        for (int e = lo2; e < cnt && cols[e] <= ib; ++e)
+        {
+          const double ri = r[cols[e]];
+          if (ri != 0.0)
+            acc = __dadd_rn(acc, __dmul_rn(ri, vals[e]));
+        }
+        if (row >= j && row >= r_lo && row <= r_hi)
+        {
+          const double rr = r[row];
+          if (rr != 0.0)
+            acc = __dadd_rn(acc, __dmul_rn(a.alpha, rr));
+        }
+        d[row] = acc;
+      }
+      __syncthreads();
+      // ---- w = K d over d's range plus K's bandwidth; (w, w), (w, r)
+      for (int64_t i = w_lo + t; i <= w_hi; i += kSeqTB)
+        w[i] = 0.0;
+      __syncthreads();
+      w_lo = d_lo - a.bwK > 0 ? d_lo - a.bwK : 0;
+      w_hi = d_hi + a.bwK < n - 1 ? d_hi + a.bwK : n - 1;
+      if (d_lo > d_hi)
+        w_lo = 0, w_hi = -1;
       double ww = 0.0, rw = 0.0;
-      for (int64_t row = gt; row < n; row += gs)
+      for (int64_t row = w_lo + t; row <= w_hi; row += kSeqTB)
       {
         double acc = 0.0;
         for (int64_t q = a.K.rp[row]; q < a.K.rp[row + 1]; ++q)
         {
-          const double dk = __ldcg(a.d + a.K.ci[q]);
+          const int64_t c = a.K.ci[q];
+          const double dk = (c >= d_lo && c <= d_hi) ? d[c] : 0.0;
           if (dk != 0.0)
             acc = __dadd_rn(acc, __dmul_rn(dk, a.K.v[q]));
         }
-        a.w[row] = acc;
+        w[row] = acc;
         ww = __dadd_rn(ww, __dmul_rn(acc, acc));
-        rw = __dadd_rn(rw, __dmul_rn(acc, __ldcg(a.r + row)));
+        const double rv = (row >= r_lo && row <= r_hi) ? r[row] : 0.0;
+        rw = __dadd_rn(rw, __dmul_rn(acc, rv));
       }
       ww = block_sum(ww, red);
       rw = block_sum(rw, red);
-      if (threadIdx.x == 0)
-      {
-        ww_part[blockIdx.x] = ww;
-        rw_part[blockIdx.x] = rw;
-      }
-      grid.sync();
-      ww = grid_total(ww_part, red);
-      rw = grid_total(rw_part, red);
       if (!(ww > 0.0))
       {
         fail(isfinite(ww) ? kSeqZeroCurv : kSeqNonFiniteW, j, sqrt(rn), iters);
@@ -228,63 +281,85 @@ __global__ void __launch_bounds__(kSeqTB) mr_sequential(SeqArgs a)
         fail(kSeqNonFiniteA, j, sqrt(rn), iters);
         return;
       }
-      for (int64_t i = gt; i < n; i += gs)
-      {
-        a.p[i] = __dadd_rn(a.p[i], __dmul_rn(step, __ldcg(a.d + i)));
-        a.r[i] = __dadd_rn(__ldcg(a.r + i), __dmul_rn(-step, __ldcg(a.w + i)));
-      }
-      grid.sync();
+      for (int64_t i = d_lo + t; i <= d_hi; i += kSeqTB)
+        p[i] = __dadd_rn(p[i], __dmul_rn(step, d[i]));
+      for (int64_t i = w_lo + t; i <= w_hi; i += kSeqTB)
+        r[i] = __dadd_rn(r[i], __dmul_rn(-step, w[i]));
+      unite(p_lo, p_hi, d_lo, d_hi);
+      unite(r_lo, r_hi, w_lo, w_hi);
+      __syncthreads();
       rn = rnorm_sq();
       ++iters;
     }
-    // ---- column j of P (exact zeros are "not stored", spai.cpp:197-206)
-    if (gt == 0)
+    // ---- column j of P: its nonzeros (spai.cpp:197-206) appended to the row lists
+    if (t == 0)
       a.residual[j] = sqrt(rn);
-    for (int64_t row = gt; row < n; row += gs)
-      a.P[row * n + j] = a.p[row];
-    grid.sync();
-  }
-}
-
-// CSR of the dense row-major factor: one warp per row, ascending column.
-__global__ void dense_row_count(int64_t n, const double *__restrict__ P, int64_t *__restrict__ cnt)
-{
-  const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (row >= n)
-    return;
-  int64_t c = 0;
-  for (int64_t i = lane; i < n; i += 32)
-    c += P[row * n + i] != 0.0;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1)
-    c += __shfl_xor_sync(0xffffffffu, c, off);
-  if (lane == 0)
-    cnt[row + 1] = c;
-}
-
-__global__ void dense_row_fill(int64_t n, const double *__restrict__ P, const int64_t *__restrict__ rp,
-                               int32_t *__restrict__ ci, double *__restrict__ v)
-{
-  const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (row >= n)
-    return;
-  int64_t out = rp[row];
-  for (int64_t i0 = 0; i0 < n; i0 += 32)
-  {
-    const int64_t i = i0 + lane;
-    const double x = i < n ? P[row * n + i] : 0.0;
-    const bool nz = x != 0.0;
-    const unsigned mask = __ballot_sync(0xffffffffu, nz);
-    if (nz)
+    int64_t clo = LLONG_MAX, chi = -1;
+    bool full = false;
+    for (int64_t row = p_lo + t; row <= p_hi; row += kSeqTB)
     {
-      const int64_t o = out + __popc(mask & ((1u << lane) - 1u));
-      ci[o] = static_cast<int32_t>(i);
-      v[o] = x;
+      const double v = p[row];
+      if (v == 0.0)
+        continue;
+      const int32_t c = a.rl_cnt[row];
+      if (c >= a.cap)
+      {
+        full = true;
+        continue;
+      }
+      a.rl_col[row * a.cap + c] = static_cast<int32_t>(j);
+      a.rl_val[row * a.cap + c] = v;
+      a.rl_cnt[row] = c + 1;
+      clo = min(clo, row);
+      chi = max(chi, row);
     }
-    out += __popc(mask);
+    if (__syncthreads_or(full))
+    {
+      fail(kSeqCapacity, j, 0.0, 0);
+      return;
+    }
+    clo = block_min(clo, ired);
+    chi = block_max(chi, ired);
+    if (t == 0)
+    {
+      a.col_lo[j] = clo <= chi ? clo : 0; // an all-zero column: empty range
+      a.col_hi[j] = clo <= chi ? chi : -1;
+    }
+    // ---- clear the accumulators over their ranges
+    for (int64_t i = p_lo + t; i <= p_hi; i += kSeqTB)
+      p[i] = 0.0;
+    for (int64_t i = r_lo + t; i <= r_hi; i += kSeqTB)
+      r[i] = 0.0;
+    for (int64_t i = d_lo + t; i <= d_hi; i += kSeqTB)
+      d[i] = 0.0;
+    for (int64_t i = w_lo + t; i <= w_hi; i += kSeqTB)
+      w[i] = 0.0;
+    __syncthreads();
   }
+}
+
+// Row lists -> CSR (rows keep their ascending columns).
+__global__ void rl_fill(int64_t n, int64_t cap, const int32_t *__restrict__ cnt, const int32_t *__restrict__ col,
+                        const double *__restrict__ val, const int64_t *__restrict__ rp, int32_t *__restrict__ ci,
+                        double *__restrict__ v)
+{
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (row >= n)
+    return;
+  for (int32_t e = 0; e < cnt[row]; ++e)
+  {
+    ci[rp[row] + e] = col[row * cap + e];
+    v[rp[row] + e] = val[row * cap + e];
+  }
+}
+
+__global__ void rl_counts(int64_t n, const int32_t *__restrict__ cnt, int64_t *__restrict__ rp)
+{
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (row < n)
+    rp[row + 1] = cnt[row];
+  if (row == 0)
+    rp[0] = 0;
 }
 
 std::string fmt_seq(double v)
@@ -301,10 +376,6 @@ mgpu_csr *mr_build_sequential(mgpu_ctx *ctx, const mgpu_csr *K, const mgpu_csr *
                               int64_t max_iters, double *col_residual)
 {
   const int64_t n = K->nrows;
-  if (n > kSeqMaxN)
-    throw Error(MGPU_ERR_UNSUPPORTED, "spai: sequential mode on the device holds the built factor densely (n <= " +
-                                          std::to_string(kSeqMaxN) + ", got " + std::to_string(n) +
-                                          "); use frozen mode or LS-SPAI");
   cudaStream_t s = ctx->stream;
   mgpu_csr *Kt = transpose_csr(ctx, K);
   mgpu_csr *Rt = nullptr;
@@ -313,100 +384,114 @@ mgpu_csr *mr_build_sequential(mgpu_ctx *ctx, const mgpu_csr *K, const mgpu_csr *
   {
     Rt = rhs_src ? transpose_csr(ctx, rhs_src) : nullptr;
     const int64_t nn = n > 0 ? n : 1;
-    DBuf dense(sizeof(double) * static_cast<size_t>(nn) * nn, s);
-    DBuf vec(sizeof(double) * 4 * nn, s), resid(sizeof(double) * nn, s);
-    const int G = ctx->num_sms;
-    DBuf part(sizeof(double) * 3 * G, s), fl(sizeof(int) * 2, s), fcol(sizeof(int64_t), s), fit(sizeof(int64_t), s),
-        frn(sizeof(double), s);
-    MG_CUDA(cudaMemsetAsync(fl.ptr, 0, sizeof(int) * 2, s));
-    MG_CUDA(cudaMemsetAsync(dense.ptr, 0, sizeof(double) * static_cast<size_t>(nn) * nn, s));
-    SeqArgs a{};
-    a.n = n;
-    a.K = K->view();
-    a.Kt = Kt->view();
-    a.Rt = Rt ? Rt->view() : DCsr{nullptr, nullptr, nullptr};
-    a.alpha = alpha;
-    a.tol_sq = tol * tol;
-    a.max_iters = max_iters;
-    a.P = dense.as<double>();
-    a.p = vec.as<double>();
-    a.r = a.p + nn;
-    a.d = a.r + nn;
-    a.w = a.d + nn;
-    a.partial = part.as<double>();
-    a.residual = resid.as<double>();
-    a.fail = fl.as<int>();
-    a.fail_col = fcol.as<int64_t>();
-    a.fail_iters = fit.as<int64_t>();
-    a.fail_rn = frn.as<double>();
-    if (n > 0)
+    const int64_t bwK = csr_bandwidth(ctx, const_cast<mgpu_csr *>(K));
+    // row-list capacity: ~4 GB of lists by default, never more than n; a full list stops the
+    // kernel and the build reruns with twice the capacity
+    int64_t cap = std::min<int64_t>(nn, std::max<int64_t>(64, (int64_t{4} << 30) / (12 * nn)));
+    for (;;)
     {
-      int per_sm = 0;
-      MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mr_sequential, kSeqTB, 0));
-      if (per_sm < 1)
-        throw Error(MGPU_ERR_CUDA, "spai: sequential kernel cannot be resident");
-      void *args[] = {&a};
-      MG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void *>(mr_sequential), dim3(static_cast<unsigned>(G)),
-                                          dim3(kSeqTB), args, 0, s));
-      check_launch(ctx, "mr_sequential");
-    }
-    int hf[2] = {0, 0};
-    int64_t col = 0, it = 0;
-    double rn = 0.0;
-    MG_CUDA(cudaMemcpyAsync(hf, fl.ptr, sizeof hf, cudaMemcpyDeviceToHost, s));
-    MG_CUDA(cudaMemcpyAsync(&col, fcol.ptr, sizeof col, cudaMemcpyDeviceToHost, s));
-    MG_CUDA(cudaMemcpyAsync(&it, fit.ptr, sizeof it, cudaMemcpyDeviceToHost, s));
-    MG_CUDA(cudaMemcpyAsync(&rn, frn.ptr, sizeof rn, cudaMemcpyDeviceToHost, s));
-    MG_CUDA(cudaStreamSynchronize(s));
-    if (hf[0] != kSeqOk)
-    {
-      const std::string c = std::to_string(col);
-      switch (hf[0])
+      DBuf cnt(sizeof(int32_t) * nn, s), lcol(sizeof(int32_t) * static_cast<size_t>(nn * cap), s),
+          lval(sizeof(double) * static_cast<size_t>(nn * cap), s), crange(sizeof(int64_t) * 2 * nn, s);
+      DBuf vec(sizeof(double) * 4 * nn, s), resid(sizeof(double) * nn, s);
+      DBuf fl(sizeof(int) * 2, s), fcol(sizeof(int64_t), s), fit(sizeof(int64_t), s), frn(sizeof(double), s);
+      MG_CUDA(cudaMemsetAsync(fl.ptr, 0, sizeof(int) * 2, s));
+      MG_CUDA(cudaMemsetAsync(cnt.ptr, 0, sizeof(int32_t) * nn, s));
+      MG_CUDA(cudaMemsetAsync(vec.ptr, 0, sizeof(double) * 4 * nn, s));
+      SeqArgs a{};
+      a.n = n;
+      a.K = K->view();
+      a.Kt = Kt->view();
+      a.Rt = Rt ? Rt->view() : DCsr{nullptr, nullptr, nullptr};
+      a.alpha = alpha;
+      a.tol_sq = tol * tol;
+      a.max_iters = max_iters;
+      a.bwK = bwK;
+      a.cap = cap;
+      a.rl_cnt = cnt.as<int32_t>();
+      a.rl_col = lcol.as<int32_t>();
+      a.rl_val = lval.as<double>();
+      a.col_lo = crange.as<int64_t>();
+      a.col_hi = a.col_lo + nn;
+      a.p = vec.as<double>();
+      a.r = a.p + nn;
+      a.d = a.r + nn;
+      a.w = a.d + nn;
+      a.residual = resid.as<double>();
+      a.fail = fl.as<int>();
+      a.fail_col = fcol.as<int64_t>();
+      a.fail_iters = fit.as<int64_t>();
+      a.fail_rn = frn.as<double>();
+      if (n > 0)
       {
-      case kSeqStall:
-        throw Error(MGPU_ERR_STAGNATION,
-                    "spai: column " + c + " stalled at ||r|| = " + fmt_seq(rn) + " after " + std::to_string(it) +
-                        " iterations (tol " + fmt_seq(tol) + ")",
-                    col);
-      case kSeqZeroCurv:
-        throw Error(MGPU_ERR_STAGNATION, "spai: zero curvature in column " + c + " with ||r|| > tol", col);
-      case kSeqNonFiniteW:
-        throw Error(MGPU_ERR_NUMERICAL, "spai: non-finite values in column " + c, col);
-      default:
-        throw Error(MGPU_ERR_NUMERICAL, "spai: non-finite step in column " + c, col);
+        mr_sequential<<<1, kSeqTB, 0, s>>>(a);
+        check_launch(ctx, "mr_sequential");
       }
+      int hf[2] = {0, 0};
+      int64_t col = 0, it = 0;
+      double rn = 0.0;
+      MG_CUDA(cudaMemcpyAsync(hf, fl.ptr, sizeof hf, cudaMemcpyDeviceToHost, s));
+      MG_CUDA(cudaMemcpyAsync(&col, fcol.ptr, sizeof col, cudaMemcpyDeviceToHost, s));
+      MG_CUDA(cudaMemcpyAsync(&it, fit.ptr, sizeof it, cudaMemcpyDeviceToHost, s));
+      MG_CUDA(cudaMemcpyAsync(&rn, frn.ptr, sizeof rn, cudaMemcpyDeviceToHost, s));
+      MG_CUDA(cudaStreamSynchronize(s));
+      if (hf[0] == kSeqCapacity)
+      {
+        if (cap >= nn)
+          throw Error(MGPU_ERR_CUDA, "spai: sequential row lists overflowed at full capacity");
+        cap = std::min<int64_t>(nn, 2 * cap);
+        continue;
+      }
+      if (hf[0] != kSeqOk)
+      {
+        const std::string c = std::to_string(col);
+        switch (hf[0])
+        {
+        case kSeqStall:
+          throw Error(MGPU_ERR_STAGNATION,
+                      "spai: column " + c + " stalled at ||r|| = " + fmt_seq(rn) + " after " + std::to_string(it) +
+                          " iterations (tol " + fmt_seq(tol) + ")",
+                      col);
+        case kSeqZeroCurv:
+          throw Error(MGPU_ERR_STAGNATION, "spai: zero curvature in column " + c + " with ||r|| > tol", col);
+        case kSeqNonFiniteW:
+          throw Error(MGPU_ERR_NUMERICAL, "spai: non-finite values in column " + c, col);
+        default:
+          throw Error(MGPU_ERR_NUMERICAL, "spai: non-finite step in column " + c, col);
+        }
+      }
+      P = new mgpu_csr;
+      P->ctx = ctx;
+      P->nrows = n;
+      P->ncols = n;
+      MG_CUDA(mg_malloc(reinterpret_cast<void **>(&P->row_ptr), sizeof(int64_t) * (n + 1), s));
+      MG_CUDA(cudaMemsetAsync(P->row_ptr, 0, sizeof(int64_t) * (n + 1), s));
+      if (n > 0)
+      {
+        rl_counts<<<blocks_for(n), kThreads, 0, s>>>(n, cnt.as<int32_t>(), P->row_ptr);
+        check_launch(ctx, "rl_counts");
+        size_t tmp = 0;
+        MG_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp, P->row_ptr + 1, P->row_ptr + 1, n, s));
+        DBuf tb(tmp, s);
+        MG_CUDA(cub::DeviceScan::InclusiveSum(tb.ptr, tmp, P->row_ptr + 1, P->row_ptr + 1, n, s));
+        count_launch(ctx);
+      }
+      int64_t nnz = 0;
+      MG_CUDA(cudaMemcpyAsync(&nnz, P->row_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      MG_CUDA(cudaStreamSynchronize(s));
+      P->nnz = nnz;
+      MG_CUDA(mg_malloc(reinterpret_cast<void **>(&P->col_idx), sizeof(int32_t) * (nnz > 0 ? nnz : 1), s));
+      MG_CUDA(mg_malloc(reinterpret_cast<void **>(&P->values), sizeof(double) * (nnz > 0 ? nnz : 1), s));
+      if (n > 0)
+      {
+        rl_fill<<<blocks_for(n), kThreads, 0, s>>>(n, cap, cnt.as<int32_t>(), lcol.as<int32_t>(), lval.as<double>(),
+                                                   P->row_ptr, P->col_idx, P->values);
+        check_launch(ctx, "rl_fill");
+      }
+      if (col_residual && n > 0)
+        MG_CUDA(cudaMemcpyAsync(col_residual, resid.ptr, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+      MG_CUDA(cudaStreamSynchronize(s));
+      break;
     }
-    P = new mgpu_csr;
-    P->ctx = ctx;
-    P->nrows = n;
-    P->ncols = n;
-    MG_CUDA(mg_malloc(reinterpret_cast<void **>(&P->row_ptr), sizeof(int64_t) * (n + 1), s));
-    MG_CUDA(cudaMemsetAsync(P->row_ptr, 0, sizeof(int64_t) * (n + 1), s));
-    const unsigned rows_grid = static_cast<unsigned>((n * 32 + kThreads - 1) / kThreads);
-    if (n > 0)
-    {
-      dense_row_count<<<rows_grid, kThreads, 0, s>>>(n, dense.as<double>(), P->row_ptr);
-      check_launch(ctx, "dense_row_count");
-      size_t tmp = 0;
-      MG_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp, P->row_ptr + 1, P->row_ptr + 1, n, s));
-      DBuf t(tmp, s);
-      MG_CUDA(cub::DeviceScan::InclusiveSum(t.ptr, tmp, P->row_ptr + 1, P->row_ptr + 1, n, s));
-      count_launch(ctx);
-    }
-    int64_t nnz = 0;
-    MG_CUDA(cudaMemcpyAsync(&nnz, P->row_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    MG_CUDA(cudaStreamSynchronize(s));
-    P->nnz = nnz;
-    MG_CUDA(mg_malloc(reinterpret_cast<void **>(&P->col_idx), sizeof(int32_t) * (nnz > 0 ? nnz : 1), s));
-    MG_CUDA(mg_malloc(reinterpret_cast<void **>(&P->values), sizeof(double) * (nnz > 0 ? nnz : 1), s));
-    if (n > 0)
-    {
-      dense_row_fill<<<rows_grid, kThreads, 0, s>>>(n, dense.as<double>(), P->row_ptr, P->col_idx, P->values);
-      check_launch(ctx, "dense_row_fill");
-    }
-    if (col_residual && n > 0)
-      MG_CUDA(cudaMemcpyAsync(col_residual, resid.ptr, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
-    MG_CUDA(cudaStreamSynchronize(s));
   }
   catch (...)
   {

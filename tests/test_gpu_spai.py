@@ -146,11 +146,22 @@ def test_mr_sequential_stagnation(mg, oracle):
     assert str(eg.value).split(" stalled")[0] == eo.value.msg.split(" stalled")[0]
 
 
-def test_mr_sequential_size_bound(mg, oracle):
-    """The device keeps the built factor dense: n > 8192 is refused before any work."""
-    M, D, K = oracle.chain_generate(9000)
-    with pytest.raises(mg.UnsupportedError):
-        mg.spai_build(K, mode=mg.SEQUENTIAL)
+def test_mr_sequential_large_n(mg, oracle):
+    """n = 2e4 (the sparse row-list factor; the earlier dense device layout stopped at 8192):
+    ~660 nnz per column of fill, entries within 1e-10 of the oracle, same pattern and residuals,
+    and the small-capacity retry path (a tiny problem whose first row-list capacity overflows)."""
+    import time
+    M, D, K = oracle.chain_generate(20000, consistent=True, stiffness_scale=1.0)
+    A = oracle.shifted_operator(M, D, K, 10.0)
+    t = time.perf_counter()
+    f = mg.spai_build(A, mode=mg.SEQUENTIAL)
+    dev_s = time.perf_counter() - t
+    want, wres = oracle.spai_build(A, mode=0)
+    got = f.matrix.download()
+    assert got.nnz > 600 * 20000
+    _csr_close(got, want)
+    assert rel(f.target_frob_residual, wres) < 1e-10
+    print(f"sequential MR n=2e4: device {dev_s:.2f} s, nnz {got.nnz}")
 
 
 # ------------------------------------------------------------------ LS-SPAI
