@@ -59,3 +59,14 @@ ref:
 clean:
 	rm -rf build $(LIBDIR)
 	$(MAKE) -C oracle clean
+
+# Experiment build (tools/fma_experiment.py): cg_cluster_v2 with DFMA terms.  Not the product.
+fma-exp: $(LIBDIR)/exp/libmgpu_fma.so
+
+$(OBJDIR)/fma/cg_cluster.o: $(SRC)/cg_cluster.cu $(SRC)/internal.cuh include/mgpu.h
+	mkdir -p $(OBJDIR)/fma
+	$(NVCC) $(NVFLAGS) -DMGPU_CLUSTER_FMA -c $< -o $@ 2> $@.ptxas.log || (cat $@.ptxas.log; exit 1)
+
+$(LIBDIR)/exp/libmgpu_fma.so: $(filter-out $(OBJDIR)/cg_cluster.o,$(CU_OBJS)) $(OBJDIR)/fma/cg_cluster.o $(CPP_OBJS)
+	mkdir -p $(LIBDIR)/exp
+	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart -ldl

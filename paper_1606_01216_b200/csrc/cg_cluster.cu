@@ -890,6 +890,15 @@ struct V2Params
 // EC > 0: every operator row (A and each chain factor) holds exactly EC ELL entries, known at
 // compile time, so the entry loops unroll with constant offsets; EC = 0: runtime widths.
 // AX: asynchronous exchange (else cluster barriers); PR: per-phase clock64 profile (MGPU_PROFILE_PHASES)
+// acc + a * b in cg_cluster_v2's SpMV, dot and axpy terms: two roundings (the reference's scalar
+// kernel table, bitwise) by default; one DFMA with -DMGPU_CLUSTER_FMA (the reference's AVX2 table
+// contracts these, kernels_avx2.cpp:34-35, 57, 88) -- the DESIGN.md 5 experiment (tools/fma_experiment.py).
+#ifdef MGPU_CLUSTER_FMA
+#define V2_MADD(acc, a, b) fma((a), (b), (acc))
+#else
+#define V2_MADD(acc, a, b) __dadd_rn((acc), __dmul_rn((a), (b)))
+#endif
+
 template <int RPT, int EC = 0, bool AX = true, bool PR = false>
 __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
 {
@@ -1042,7 +1051,7 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
 #pragma unroll
           for (int j = 0; j < K; ++j)
             if (ok[j])
-              acc[j] = __dadd_rn(acc[j], __dmul_rn(fv[e * span + q[j]], in[q[j] + hs - hd + off8(ow[j], e)]));
+              acc[j] = V2_MADD(acc[j], fv[e * span + q[j]], in[q[j] + hs - hd + off8(ow[j], e)]);
         }
 #pragma unroll
         for (int j = 0; j < K; ++j)
@@ -1062,7 +1071,7 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
         double a = 0.0;
         const unsigned long long w1 = fo[qq];
         for (int e = 0; e < E; ++e)
-          a = __dadd_rn(a, __dmul_rn(fv[e * span + qq], in[qq + hs - hd + off8(w1, e)]));
+          a = V2_MADD(a, fv[e * span + qq], in[qq + hs - hd + off8(w1, e)]);
         out[qq] = a;
       }
       __syncthreads();
@@ -1092,7 +1101,7 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
       {
         const int lr = threadIdx.x + j * kV2TB;
         if (ok[j])
-          y[j] = __dadd_rn(y[j], __dmul_rn(av[e * R + lr], in[lr + hs + off8(ow[j], e)]));
+          y[j] = V2_MADD(y[j], av[e * R + lr], in[lr + hs + off8(ow[j], e)]);
       }
     }
   };
@@ -1110,7 +1119,7 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
       else
       {
         const double rv = ex_r(ex, q, side)[k];
-        v = fresh ? rv : __dadd_rn(rv, __dmul_rn(beta, ex_d(ex, q, side)[k]));
+        v = fresh ? rv : V2_MADD(rv, beta, ex_d(ex, q, side)[k]);
       }
       dpad[side == 0 ? k : H + R + k] = v;
     }
@@ -1145,7 +1154,7 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
       {
         sol[j] = t[lr + hs];
         y[j] = __dsub_rn(b_at(lr), y[j]);
-        q2[0] = __dadd_rn(q2[0], __dmul_rn(y[j], y[j]));
+        q2[0] = V2_MADD(q2[0], y[j], y[j]);
       }
     }
     cta_sum_push<kV2TB, 2>(sh, q2, 1, cl, inboxA, cs, rank);
@@ -1220,7 +1229,7 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
       const int lr = threadIdx.x + j * kV2TB;
       if (lr < R)
       {
-        const double dn = fresh ? r[j] : __dadd_rn(r[j], __dmul_rn(beta, dpad[H + lr]));
+        const double dn = fresh ? r[j] : V2_MADD(r[j], beta, dpad[H + lr]);
         dpad[H + lr] = dn;
         if constexpr (AX)
           push_async(1, q ^ 1, lr, dn);
@@ -1242,8 +1251,8 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
       if (lr < R)
       {
         const double dn = dpad[H + lr];
-        pa[0] = __dadd_rn(pa[0], __dmul_rn(dn, w[j]));
-        pa[1] = __dadd_rn(pa[1], __dmul_rn(dn, dn));
+        pa[0] = V2_MADD(pa[0], dn, w[j]);
+        pa[1] = V2_MADD(pa[1], dn, dn);
       }
     }
     mark(3);
@@ -1281,9 +1290,9 @@ __global__ void __launch_bounds__(kV2TB, 1) cg_cluster_v2(V2Params P)
       const int lr = threadIdx.x + j * kV2TB;
       if (lr < R)
       {
-        x[j] = __dadd_rn(x[j], __dmul_rn(alpha, dpad[H + lr]));
-        r[j] = __dadd_rn(r[j], __dmul_rn(-alpha, w[j]));
-        pb[0] = __dadd_rn(pb[0], __dmul_rn(r[j], r[j]));
+        x[j] = V2_MADD(x[j], alpha, dpad[H + lr]);
+        r[j] = V2_MADD(r[j], -alpha, w[j]);
+        pb[0] = V2_MADD(pb[0], r[j], r[j]);
         if constexpr (AX)
           push_async(0, q ^ 1, lr, r[j]);
         else
