@@ -27,6 +27,8 @@ lib: $(LIBDIR)/libmgpu.so
 $(OBJDIR) $(LIBDIR):
 	mkdir -p $@
 
+$(OBJDIR)/cg.o $(OBJDIR)/cg_stream.o: $(SRC)/cg_common.cuh
+
 $(OBJDIR)/%.o: $(SRC)/%.cu $(SRC)/internal.cuh include/mgpu.h | $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $@.ptxas.log || (cat $@.ptxas.log; exit 1)
 

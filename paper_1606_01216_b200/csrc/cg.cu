@@ -26,7 +26,7 @@
 #include <chrono>
 #include <vector>
 
-#include "internal.cuh"
+#include "cg_common.cuh"
 
 namespace cgrp = cooperative_groups;
 
@@ -38,26 +38,16 @@ int cg_cluster_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, cons
                       int64_t *d_bd, double *d_hist, int64_t hist_cap, unsigned long long *d_loop, const DCsr *dA,
                       const DCsr *dF);
 
+// cg_stream.cu
+bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_csr *const *chains, int64_t n,
+                  int m, const double *B_dev, int64_t ldb, const int *halo, int hmax, double rtol, int64_t maxit,
+                  double *X_dev, double *REC_dev, double *TR_dev, int64_t *d_it, int *d_conv, int *d_st, int64_t *d_bd,
+                  double *d_hist, int64_t hist_cap, int64_t *d_loop);
+
 namespace
 {
 
-constexpr int kCgThreads = 256;
-constexpr int kWarps = kCgThreads / 32;
-constexpr int kMaxSys = 128;   // systems (points x columns) per launch (mgpu_cg_solve splits larger batches)
-constexpr int kMaxPoints = 128;
-constexpr int kMaxTiles = 1024; // tiles per point (reduction fan-in)
-constexpr int kMaxM = 8;        // rhs columns per launch
-
-enum SysState : int
-{
-  kRun = 0,
-  kConverged = 1,
-  kBreakdown = 2,
-  kZeroRhs = 3,
-  kMaxed = 4,
-  kPendingConv = 5,
-  kPendingRestart = 6,
-};
+// (batch limits, SysState, Seg, BandShared and the reductions: cg_common.cuh)
 
 struct CgParams
 {
@@ -713,15 +703,6 @@ __global__ void __launch_bounds__(kCgThreads) cg_persistent(CgParams P)
 // after the barrier every block sums the per-block partials in block order.
 // Deterministic for a given grid (one block per SM), no atomics.
 // =====================================================================
-constexpr int kMaxZ = 12; // chain factors (the AIRGA update chain grows by one per outer iteration)
-constexpr int kMaxHalo = 64;
-constexpr int kMaxRpt = 4;
-constexpr int kMaxSeg = 8; // row segments per block
-
-struct Seg
-{
-  int p, rs, re, pad; // rows [rs, re) of point p
-};
 
 struct BandParams
 {
@@ -746,85 +727,6 @@ struct BandParams
   int64_t *loop_iters;
 };
 
-template <int TB>
-struct BandShared
-{
-  double rho[kMaxSys], target[kMaxSys], alpha[kMaxSys], beta[kMaxSys], bnorm[kMaxSys];
-  double tot[kMaxSys * 2];
-  int state[kMaxSys];
-  int fresh[kMaxSys];
-  int pend[kMaxSys]; // cg_stream: x~ += alpha d_old still owed (deferred from phase B)
-  int64_t sit[kMaxSys];
-  int pmask[kMaxPoints];
-  Seg seg[kMaxSeg];
-  int nseg;
-  double wsum[TB / 32][2 * kMaxM];
-  double acc[2 * kMaxM];
-  int flag;
-};
-
-// Iterate this block's row segments [rs, re) of point p (host plan in shared memory).
-template <class PT, class S, class F>
-__device__ __forceinline__ void for_segments(const PT &, const S &sh, F &&fn)
-{
-  for (int q = 0; q < sh.nseg; ++q)
-  {
-    const Seg g = sh.seg[q];
-    if (sh.pmask[g.p])
-      fn(g.p, static_cast<int64_t>(g.rs), static_cast<int64_t>(g.re));
-  }
-}
-
-// Adds this chunk's per-thread values (NV of them, nv used) to the block's
-// running partials in a fixed order.
-template <int TB, int NV>
-__device__ __forceinline__ void chunk_sum(BandShared<TB> &sh, double (&v)[NV], int nv)
-{
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int k = 0; k < NV; ++k)
-  {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1)
-      v[k] = __dadd_rn(v[k], __shfl_xor_sync(0xffffffffu, v[k], off));
-  }
-  if (lane == 0)
-  {
-#pragma unroll
-    for (int k = 0; k < NV; ++k)
-      sh.wsum[warp][k] = v[k];
-  }
-  __syncthreads();
-  if (warp == 0)
-  {
-    for (int k = 0; k < nv; ++k)
-    {
-      double x = lane < TB / 32 ? sh.wsum[lane][k] : 0.0;
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1)
-        x = __dadd_rn(x, __shfl_xor_sync(0xffffffffu, x, off));
-      if (lane == 0)
-        sh.acc[k] = __dadd_rn(sh.acc[k], x);
-    }
-  }
-  __syncthreads();
-}
-
-template <int TB>
-__device__ __forceinline__ void begin_point(BandShared<TB> &sh)
-{
-  if (threadIdx.x < 2 * kMaxM)
-    sh.acc[threadIdx.x] = 0.0;
-  __syncthreads();
-}
-
-template <int TB>
-__device__ __forceinline__ void end_point(double *partial, BandShared<TB> &sh, int p, int nv)
-{
-  if (threadIdx.x < nv)
-    partial[(static_cast<int64_t>(p) * 2 * kMaxM + threadIdx.x) * gridDim.x + blockIdx.x] = sh.acc[threadIdx.x];
-  __syncthreads();
-}
 
 template <int TB>
 __device__ __forceinline__ void end_point(const BandParams &P, BandShared<TB> &sh, int p, int nv)
@@ -832,31 +734,6 @@ __device__ __forceinline__ void end_point(const BandParams &P, BandShared<TB> &s
   end_point(P.partial, sh, p, nv);
 }
 
-// After a barrier: tot = sum over blocks (fixed order) for live points; quantity k < m of
-// system (p, c = k) at tot[p m + c], quantity k >= m at tot[l m + p m + (k - m)].
-template <int TB, class PT>
-__device__ void reduce_blocks(const PT &P, BandShared<TB> &sh, int nk)
-{
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int npairs = P.l * nk;
-  for (int q = warp; q < npairs; q += TB / 32)
-  {
-    const int p = q / nk, k = q % nk;
-    if (!sh.pmask[p])
-      continue;
-    const double *src = P.partial + (static_cast<int64_t>(p) * 2 * kMaxM + k) * gridDim.x;
-    const int2 br = P.pblk[p];
-    double a = 0.0;
-    for (int t = br.x + lane; t < br.y; t += 32)
-      a = __dadd_rn(a, __ldcg(src + t));
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1)
-      a = __dadd_rn(a, __shfl_xor_sync(0xffffffffu, a, off));
-    if (lane == 0)
-      sh.tot[k < P.m ? p * P.m + k : P.l * P.m + p * P.m + (k - P.m)] = a;
-  }
-  __syncthreads();
-}
 
 // Phase A.  kCheck: source = x~, outputs sol (own rows) and res = b - A sol (in w);
 // otherwise source = d_new = fresh ? r : r + beta d_old, output w.
@@ -1358,1343 +1235,6 @@ __global__ void __launch_bounds__(TB, 1) cg_banded(BandParams P)
   }
 }
 
-// =====================================================================
-// Streaming kernel for HBM-resident banded systems (cg_stream).
-//   * operators in PADDED ROW-MAJOR ELL: values [row][Epad] (Epad even) and
-//     the row's int8 column offsets packed in one u64, PADR zero rows at both
-//     ends -> every chunk's operator rows are ONE contiguous, 16B-aligned range
-//     (no row_ptr, no column index stream: 8 Epad + 8 bytes per row);
-//   * vectors interleaved [point][PADR + row][rhs], PADR zero rows per side;
-//   * per phase, each CTA walks its rows in chunks of CH = 512 * RPT rows; the
-//     inputs of chunk i+1 are fetched with cp.async.bulk (TMA bulk copies,
-//     mbarrier transaction counts) into the other half of a double buffer
-//     while the CTA computes chunk i from shared memory -> the copy engine
-//     keeps HBM busy independent of warp occupancy.
-// Control flow, reductions and arithmetic are those of cg_banded.
-// =====================================================================
-constexpr int kPadR = 64;
-constexpr int kEllMax = 64; // widest ELL row the streaming kernel takes (int8 offsets: bandwidth < kPadR)
-constexpr int kStreamNB = 4; // bulk-copy ring depth (maximum; StreamParams::nb is the one in use)
-constexpr int kTabSlots = 16; // operator-descriptor slots: segments per block, or points (serial schedule)
-static_assert(kTabSlots >= kMaxSeg, "descriptor table must cover every segment");
-
-__device__ __forceinline__ uint32_t sm_addr(const void *p)
-{
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
-{
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_addr(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
-{
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sm_addr(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
-{
-  asm volatile("{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
-               "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-               "@!p bra WAIT_%=;\n\t}" ::"r"(sm_addr(bar)),
-               "r"(parity)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
-{
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   sm_addr(dst)),
-               "l"(src), "r"(bytes), "r"(sm_addr(bar))
-               : "memory");
-}
-// Same copy with an L2 eviction-priority policy (createpolicy) attached to its reads.
-__device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t pol)
-{
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
-               "%4;" ::"r"(sm_addr(dst)),
-               "l"(src), "r"(bytes), "r"(sm_addr(bar)), "l"(pol)
-               : "memory");
-}
-__device__ __forceinline__ uint64_t policy_evict_first()
-{
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-// L2-only store with an eviction-priority policy (data not re-read soon).
-__device__ __forceinline__ void stg_hint(double *p, double v, uint64_t pol)
-{
-  asm volatile("st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
-}
-// Drops a 128-byte L2 line without writing it back (its contents become undefined).
-__device__ __forceinline__ void discard_l2(const void *p)
-{
-  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
-{
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm_addr(bar)) : "memory");
-}
-__device__ __forceinline__ void fence_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
-
-struct PEll
-{
-  const double *v;             // logical row 0 (PADR zero rows before / after)
-  const unsigned long long *o; // packed int8 offsets, `ow` words per row
-  int E;                       // values per row (even, <= 16)
-  int ow;                      // offset words per row: ceil(E / 8) (E <= kEllMax)
-};
-
-// eq[p] = 1 iff operator p has point 0's CSR structure (then its ELL offsets equal point 0's,
-// and the kernel streams point 0's copy for every such point: one DRAM read, L2 hits for the
-// rest, since the points advance through the rows together).  eq must be preset to 1.
-__global__ void pattern_eq_kernel(int64_t n, int64_t nnz, const int64_t *__restrict__ rp0,
-                                  const int32_t *__restrict__ ci0, const int64_t *__restrict__ rp,
-                                  const int32_t *__restrict__ ci, int *eq)
-{
-  bool same = true;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i <= n; i += gridDim.x * blockDim.x)
-    same = same && rp[i] == rp0[i];
-  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < nnz; k += gridDim.x * blockDim.x)
-    same = same && ci[k] == ci0[k];
-  if (!__all_sync(0xffffffffu, same) && (threadIdx.x & 31) == 0)
-    *eq = 0;
-}
-
-struct StreamParams
-{
-  int l, m, z, rpt, ch; // ch: rows per chunk (phase A and the check pass)
-  int ch_b;             // rows per chunk in phase B (fewer vectors per row: taller chunks fill the same slot)
-  int fold;             // 1: x~ += alpha d deferred to the next phase A (m = 1), 0: applied in phase B
-  int nb;               // ring depth (2..kStreamNB)
-  int serial;           // 1: points one after another (all blocks on one point's rows; L2 hand-off A -> B)
-  // stage-buffer layout: 0 = row-interleaved [row][c]; > 0 (m == 4) = two planes of double2,
-  // (c0, c1) and (c2, c3) per row, plane stride `pst` doubles.  A thread's row loads are then two
-  // 16-byte loads from consecutive 16-byte slots across the warp (no bank conflicts; the
-  // interleaved 32-byte rows cost two wavefronts per 16-byte load).
-  int pst;
-  int64_t n, ldv; // ldv = (n + 2 PADR) * m: doubles per point block
-  int halo[kMaxZ + 1];
-  int hmax;
-  const PEll *A, *F; // [l], [l * z] newest first
-  const int *eqA;     // [l]: operator p shares point 0's structure (use A[0]'s offsets)
-  const int *eqF;     // [l * z]: factor (p, f) shares factor (0, f)'s structure
-  double rtol;
-  int64_t maxit;
-  // vectors: logical (point p, row i, col c) at base + p * ldv + (PADR + i) * m + c
-  const double *b;
-  double *xt, *r, *dbuf0, *dbuf1, *w, *sol;
-  double *partial;
-  const Seg *seg;
-  const int2 *pblk;
-  double *X, *REC, *TR;
-  int64_t *iters;
-  int *conv, *status;
-  int64_t *bd_iter;
-  double *hist;
-  int64_t hist_cap;
-  int64_t *loop_iters;
-  long long *prof; // optional [16] clock64 totals per phase (block 0, thread 0; MGPU_PROFILE_PHASES)
-  // shared-memory carve-up (bytes): two input buffers (phase A layout and
-  // phase B layout alias) + stage buffers
-  size_t buf_bytes, off_stage0, off_stage1, off_stage2;
-  size_t a_vr, a_vd, a_vx, a_fv[kMaxZ], a_fo[kMaxZ], a_av, a_ao; // phase A offsets inside a buffer
-  size_t b_r, b_w, b_x, b_d;                                      // phase B offsets inside a buffer
-};
-
-__device__ __forceinline__ const double *vrow(const StreamParams &P, const double *base, int p, int64_t i)
-{
-  return base + static_cast<int64_t>(p) * P.ldv + (kPadR + i) * P.m;
-}
-
-// chunk iterator over the block's segments
-struct ChunkIt
-{
-  int seg;
-  int64_t c0;
-};
-
-template <int TB>
-__device__ __forceinline__ bool chunk_next(const BandShared<TB> &sh, int64_t CH, ChunkIt &it, int &p, int64_t &c0,
-                                           int64_t &c1)
-{
-  while (it.seg < sh.nseg)
-  {
-    const Seg g = sh.seg[it.seg];
-    if (!sh.pmask[g.p] || it.c0 >= g.re)
-    {
-      ++it.seg;
-      it.c0 = it.seg < sh.nseg ? sh.seg[it.seg].rs : 0;
-      continue;
-    }
-    p = g.p;
-    c0 = it.c0;
-    c1 = min(static_cast<int64_t>(g.re), c0 + CH);
-    it.c0 = c1;
-    return true;
-  }
-  return false;
-}
-
-__device__ __forceinline__ int64_t even_up(int64_t x) { return (x + 1) & ~static_cast<int64_t>(1); }
-
-// Producer: issue the bulk copies of one chunk's inputs into buffer `buf`.
-// kind 0: phase A step (r, d_old over the halo; x~ on own rows for the deferred
-// update), 1: phase A check (x~ and d_old over the halo), 2: phase B (r, w).
-//
-// Serial schedule (P.serial): every read that is the last one before the data's next use
-// two or more passes later is tagged L2 evict_first (operators, d_old, x~, everything phase B
-// reads), so the lines phase B re-reads (r, d_new, w of the same point, written or read by
-// phase A just before) are the ones that stay in L2.
-template <int TB>
-__device__ void stream_issue(const StreamParams &P, const PEll *tab, unsigned char *buf, uint64_t *bar, int kind, int p,
-                             int64_t c0, int64_t c1, const double *dold, const double *dnew)
-{
-  const int m = P.m;
-  uint32_t bytes = 0;
-  const uint64_t pol = policy_evict_first();
-  auto cp = [&](void *dst, const void *src, uint32_t nbytes, bool last_use) {
-    if (P.serial && last_use)
-      bulk_g2s_hint(dst, src, nbytes, bar, pol);
-    else
-      bulk_g2s(dst, src, nbytes, bar);
-  };
-  if (kind == 2)
-  {
-    const int64_t rows = even_up(c1 - c0);
-    const uint32_t vb = static_cast<uint32_t>(rows * m * 8);
-    bytes = (P.fold ? 2 : 4) * vb;
-    mbar_expect_tx(bar, bytes);
-    cp(buf + P.b_r, vrow(P, P.r, p, c0), vb, true);
-    cp(buf + P.b_w, vrow(P, P.w, p, c0), vb, true);
-    if (!P.fold)
-    {
-      cp(buf + P.b_x, vrow(P, P.xt, p, c0), vb, true);
-      cp(buf + P.b_d, vrow(P, dnew, p, c0), vb, true);
-    }
-    return;
-  }
-  const int H0 = P.hmax;
-  const int64_t vrows = even_up(c1 - c0 + 2 * H0);
-  const uint32_t vb = static_cast<uint32_t>(vrows * m * 8);
-  const uint32_t xb = static_cast<uint32_t>(even_up(c1 - c0) * m * 8);
-  const bool need_d = kind == 0 || P.fold; // the check pass reads d_old only for the deferred update
-  uint32_t total = (need_d ? 2 * vb : vb) + (kind == 0 && P.fold ? xb : 0u);
-  for (int st = 0; st < P.z; ++st)
-  {
-    const int hd = P.halo[st + 1];
-    const PEll F = tab[1 + st];
-    const int64_t rows = even_up(c1 - c0 + 2 * hd);
-    total += static_cast<uint32_t>(rows * F.E * 8 + rows * F.ow * 8);
-  }
-  {
-    const PEll A = tab[0];
-    const int64_t rows = even_up(c1 - c0);
-    total += static_cast<uint32_t>(rows * A.E * 8 + rows * A.ow * 8);
-  }
-  mbar_expect_tx(bar, total);
-  cp(buf + P.a_vr, vrow(P, kind == 0 ? P.r : P.xt, p, c0 - H0), vb, kind != 0); // phase B re-reads r
-  if (need_d)
-    cp(buf + P.a_vd, vrow(P, dold, p, c0 - H0), vb, true);
-  if (kind == 0 && P.fold)
-    cp(buf + P.a_vx, vrow(P, P.xt, p, c0), xb, true);
-  for (int st = 0; st < P.z; ++st)
-  {
-    const int hd = P.halo[st + 1];
-    const PEll F = tab[1 + st];
-    const int64_t rows = even_up(c1 - c0 + 2 * hd);
-    cp(buf + P.a_fv[st], F.v + (c0 - hd) * F.E, static_cast<uint32_t>(rows * F.E * 8), true);
-    cp(buf + P.a_fo[st], F.o + (c0 - hd) * F.ow, static_cast<uint32_t>(rows * F.ow * 8), true);
-  }
-  const PEll A = tab[0];
-  const int64_t rows = even_up(c1 - c0);
-  cp(buf + P.a_av, A.v + c0 * A.E, static_cast<uint32_t>(rows * A.E * 8), true);
-  cp(buf + P.a_ao, A.o + c0 * A.ow, static_cast<uint32_t>(rows * A.ow * 8), true);
-}
-
-__device__ __forceinline__ int off8s(unsigned long long w, int t)
-{
-  return static_cast<int>(static_cast<signed char>((w >> (8 * t)) & 0xffull));
-}
-__device__ __forceinline__ int off16(unsigned long long w0, unsigned long long w1, int t)
-{
-  return t < 8 ? off8s(w0, t) : off8s(w1, t - 8);
-}
-// offset t of a row with ow words (the first two held in registers)
-__device__ __forceinline__ int off_any(const unsigned long long *offs, unsigned long long w0, unsigned long long w1,
-                                       int t)
-{
-  return t < 16 ? off16(w0, w1, t) : off8s(offs[t >> 3], t & 7);
-}
-
-// Column of element e of a row-interleaved block with m columns (MT: compile-time bound, a power of two).
-template <int MT>
-__device__ __forceinline__ int col_of(int e, int m)
-{
-  if constexpr (MT == 1)
-    return 0;
-  else
-    return m == MT ? (e & (MT - 1)) : e % m;
-}
-// acc[c] += v without dynamic register indexing.
-template <int MT>
-__device__ __forceinline__ void acc_add(double *acc, int c, double v)
-{
-#pragma unroll
-  for (int k = 0; k < MT; ++k)
-    if (k == c)
-      acc[k] = __dadd_rn(acc[k], v);
-}
-// m doubles of one row (shared memory); 16-byte vector loads when m == MT >= 2.
-template <int MT>
-__device__ __forceinline__ void ld_row(const double *x, double (&v)[MT], int m)
-{
-  if (MT >= 2 && m == MT)
-  {
-#pragma unroll
-    for (int h = 0; h < MT / 2; ++h)
-    {
-      const double2 t = reinterpret_cast<const double2 *>(x)[h];
-      v[2 * h] = t.x;
-      v[2 * h + 1] = t.y;
-    }
-  }
-  else
-  {
-#pragma unroll
-    for (int c = 0; c < MT; ++c)
-      v[c] = c < m ? x[c] : 0.0;
-  }
-}
-template <int MT>
-__device__ __forceinline__ void st_row(double *x, const double (&v)[MT], int m)
-{
-  if (MT >= 2 && m == MT)
-  {
-#pragma unroll
-    for (int h = 0; h < MT / 2; ++h)
-      reinterpret_cast<double2 *>(x)[h] = make_double2(v[2 * h], v[2 * h + 1]);
-  }
-  else
-  {
-#pragma unroll
-    for (int c = 0; c < MT; ++c)
-      if (c < m)
-        x[c] = v[c];
-  }
-}
-// Streaming (L2-only) global store of one row.
-template <int MT>
-__device__ __forceinline__ void stg_row(double *x, const double (&v)[MT], int m)
-{
-  if (MT >= 2 && m == MT)
-  {
-#pragma unroll
-    for (int h = 0; h < MT / 2; ++h)
-      __stcg(reinterpret_cast<double2 *>(x) + h, make_double2(v[2 * h], v[2 * h + 1]));
-  }
-  else
-  {
-#pragma unroll
-    for (int c = 0; c < MT; ++c)
-      if (c < m)
-        __stcg(x + c, v[c]);
-  }
-}
-// One padded-ELL row (E even, values 16-byte aligned) times a row-interleaved
-// shared-memory block: a2[c] = sum_e val_e * src[(in0 + off_e) * m + c], e ascending.
-template <int MT>
-__device__ __forceinline__ void ell_row(const double *vals, const unsigned long long *offs, int E, int ow,
-                                        const double *src, int in0, int m, double (&a2)[MT])
-{
-#pragma unroll
-  for (int c = 0; c < MT; ++c)
-    a2[c] = 0.0;
-  const unsigned long long w0 = offs[0];
-  const unsigned long long w1 = ow > 1 ? offs[1] : 0ull;
-  const double2 *v2 = reinterpret_cast<const double2 *>(vals);
-  if (ow > 2) // wide rows (collapsed update chains): offsets beyond the first two words read per term
-  {
-    for (int e = 0; e < E; ++e)
-    {
-      double x[MT];
-      ld_row<MT>(src + (in0 + off_any(offs, w0, w1, e)) * m, x, m);
-#pragma unroll
-      for (int c = 0; c < MT; ++c)
-        if (c < m)
-          a2[c] = __dadd_rn(a2[c], __dmul_rn(vals[e], x[c]));
-    }
-    return;
-  }
-  auto term = [&](double a, int e) {
-    double x[MT];
-    ld_row<MT>(src + (in0 + off16(w0, w1, e)) * m, x, m);
-#pragma unroll
-    for (int c = 0; c < MT; ++c)
-      if (c < m)
-        a2[c] = __dadd_rn(a2[c], __dmul_rn(a, x[c]));
-  };
-  // single right-hand side: the Hermite operators and their A-pattern LS factors (5 entries)
-  // unrolled with constant shifts (configs[2] shape 31.1 -> 27.6 us per iteration; with m = 4
-  // the preloaded values cost registers and it measured 2% slower, so MT > 1 keeps the loop)
-  if (MT == 1 && E == 5)
-  {
-    double a5[5];
-#pragma unroll
-    for (int e = 0; e < 5; ++e)
-      a5[e] = vals[e];
-#pragma unroll
-    for (int e = 0; e < 5; ++e)
-      term(a5[e], e);
-    return;
-  }
-  if (E & 1) // odd width (no padding entry): rows are 8-byte aligned only
-  {
-    for (int e = 0; e < E; ++e)
-      term(vals[e], e);
-    return;
-  }
-  for (int h = 0; h < E / 2; ++h)
-  {
-    const double2 f = v2[h];
-    term(f.x, 2 * h);
-    term(f.y, 2 * h + 1);
-  }
-}
-
-// The same row with the width EC and the column count MT known at compile time (m == MT): the
-// offsets are byte extracts at constant positions, the loads vectorised, no per-column guards.
-// Same terms in the same order as ell_row (bitwise equal).
-template <int MT, int EC, bool PL = false>
-__device__ __forceinline__ void ell_row_fixed(const double *vals, const unsigned long long *offs, const double *src,
-                                              int in0, double (&a2)[MT], int pst = 0)
-{
-#pragma unroll
-  for (int c = 0; c < MT; ++c)
-    a2[c] = 0.0;
-  const unsigned long long w0 = offs[0];
-  const unsigned long long w1 = EC > 8 ? offs[1] : 0ull;
-#pragma unroll
-  for (int e = 0; e < EC; ++e)
-  {
-    const double ae = vals[e];
-    const int off = e < 8 ? off8s(w0, e) : off8s(w1, e - 8);
-    double x[MT];
-    if constexpr (PL && MT == 4)
-    {
-      const double2 t0 = reinterpret_cast<const double2 *>(src)[in0 + off];
-      const double2 t1 = reinterpret_cast<const double2 *>(src + pst)[in0 + off];
-      x[0] = t0.x;
-      x[1] = t0.y;
-      x[2] = t1.x;
-      x[3] = t1.y;
-    }
-    else if constexpr (MT >= 2)
-    {
-#pragma unroll
-      for (int h = 0; h < MT / 2; ++h)
-      {
-        const double2 t = reinterpret_cast<const double2 *>(src + (in0 + off) * MT)[h];
-        x[2 * h] = t.x;
-        x[2 * h + 1] = t.y;
-      }
-    }
-    else
-      x[0] = src[in0 + off];
-#pragma unroll
-    for (int c = 0; c < MT; ++c)
-      a2[c] = __dadd_rn(a2[c], __dmul_rn(ae, x[c]));
-  }
-}
-
-// Planar (m == 4) row of any width: ell_row's terms in ell_row's order.
-__device__ __forceinline__ void ell_row_planar(const double *vals, const unsigned long long *offs, int E, int ow,
-                                               const double *src, int in0, int pst, double (&a2)[4])
-{
-#pragma unroll
-  for (int c = 0; c < 4; ++c)
-    a2[c] = 0.0;
-  const unsigned long long w0 = offs[0];
-  const unsigned long long w1 = ow > 1 ? offs[1] : 0ull;
-  for (int e = 0; e < E; ++e)
-  {
-    const int r = in0 + off_any(offs, w0, w1, e);
-    const double a = vals[e];
-    const double2 t0 = reinterpret_cast<const double2 *>(src)[r];
-    const double2 t1 = reinterpret_cast<const double2 *>(src + pst)[r];
-    a2[0] = __dadd_rn(a2[0], __dmul_rn(a, t0.x));
-    a2[1] = __dadd_rn(a2[1], __dmul_rn(a, t0.y));
-    a2[2] = __dadd_rn(a2[2], __dmul_rn(a, t1.x));
-    a2[3] = __dadd_rn(a2[3], __dmul_rn(a, t1.y));
-  }
-}
-
-// Stage-buffer row access in the P.pst layout.
-template <int MT>
-__device__ __forceinline__ void ld_stage(const double *buf, int row, double (&v)[MT], int m, int pst)
-{
-  if constexpr (MT == 4)
-  {
-    if (pst > 0)
-    {
-      const double2 t0 = reinterpret_cast<const double2 *>(buf)[row];
-      const double2 t1 = reinterpret_cast<const double2 *>(buf + pst)[row];
-      v[0] = t0.x;
-      v[1] = t0.y;
-      v[2] = t1.x;
-      v[3] = t1.y;
-      return;
-    }
-  }
-  ld_row<MT>(buf + row * m, v, m);
-}
-template <int MT>
-__device__ __forceinline__ void st_stage(double *buf, int row, const double (&v)[MT], int m, int pst)
-{
-  if constexpr (MT == 4)
-  {
-    if (pst > 0)
-    {
-      reinterpret_cast<double2 *>(buf)[row] = make_double2(v[0], v[1]);
-      reinterpret_cast<double2 *>(buf + pst)[row] = make_double2(v[2], v[3]);
-      return;
-    }
-  }
-  st_row<MT>(buf + row * m, v, m);
-}
-// Index of element e (= row * m + c) of a stage buffer.
-__device__ __forceinline__ int stage_idx(int e, int m, int pst)
-{
-  if (pst > 0) // m == 4
-    return ((e & 2) ? pst : 0) + ((e >> 2) << 1) + (e & 1);
-  return e;
-}
-
-// ell_row with the common widths (the Hermite operators: 5; their A^2-pattern factors: 10) and
-// m == MT dispatched to ell_row_fixed.
-// EF: the width this call site expects (the A^2-pattern factors: 10; the Hermite operators: 5),
-// unrolled; any other width takes the loop.  One unrolled width per call site keeps the kernel
-// inside its 128 registers (two unrolled widths per site pushed the parameters to local memory).
-template <int MT, int EF>
-__device__ __forceinline__ void ell_row_any(const double *vals, const unsigned long long *offs, int E, int ow,
-                                            const double *src, int in0, int m, double (&a2)[MT], int pst)
-{
-  if constexpr (MT == 4)
-  {
-    if (pst > 0)
-    {
-      if (E == EF)
-        ell_row_fixed<4, EF, true>(vals, offs, src, in0, a2, pst);
-      else
-        ell_row_planar(vals, offs, E, ow, src, in0, pst, a2);
-      return;
-    }
-  }
-  ell_row<MT>(vals, offs, E, ow, src, in0, m, a2);
-}
-
-// Per-phase clock64 totals (MGPU_PROFILE_PHASES); the ON = false instantiation compiles away.
-template <bool ON>
-struct PhaseClock
-{
-  bool on;
-  long long t, acc[16];
-  __device__ void mark(int k)
-  {
-    if constexpr (ON)
-    {
-      if (on)
-      {
-        const long long now = clock64();
-        acc[k] += now - t;
-        t = now;
-      }
-    }
-  }
-};
-
-// Barrier among the TB consumer threads only (the producer warp streams on).
-template <int TB>
-__device__ __forceinline__ void consumer_sync()
-{
-  asm volatile("bar.sync 1, %0;" ::"n"(TB) : "memory");
-}
-
-// Producer-side state of the bulk-copy ring (lane 0 of the producer warp).
-struct RingProducer
-{
-  uint32_t filled; // bit b: buffer b has been filled at least once
-  uint32_t epar;   // bit b: parity of the next empty-barrier phase to wait for
-};
-
-// One pass over the block's chunks.  kind: 0 phase A (step), 1 phase A
-// (true-residual check), 2 phase B.  Warp-specialised: lane 0 of warp TB/32
-// streams chunk inputs into an NB-deep ring of shared buffers (full barrier:
-// bulk-copy bytes; empty barrier: consumers done), the TB consumer threads
-// compute.  Dot-product partials accumulate per consumer thread over all
-// chunks of a point (row order) and are reduced once per point.
-template <int TB, int MT, int NB, class PC>
-__device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, const PEll *tab, unsigned char *smem,
-                            uint64_t *full, uint64_t *empty, uint32_t &phase_bits, RingProducer &rp, int kind,
-                            const double *dold, double *dnew, PC &pc)
-{
-  const int64_t CH = kind == 2 ? P.ch_b : P.ch;
-  const int m = P.m;
-  const int nv = kind == 0 ? 2 * m : m;
-  ChunkIt cons{0, sh.nseg > 0 ? static_cast<int64_t>(sh.seg[0].rs) : 0};
-  __syncthreads();
-  if (threadIdx.x >= TB)
-  {
-    // ---- producer
-    if (threadIdx.x == TB)
-    {
-      fence_async_global(); // generic stores of the previous phase -> async-proxy (bulk copy) reads
-      ChunkIt prod = cons;
-      int pp;
-      int64_t pc0, pc1;
-      int k = 0;
-      while (chunk_next(sh, CH, prod, pp, pc0, pc1))
-      {
-        const int b = k % P.nb;
-        if ((rp.filled >> b) & 1u)
-        {
-          mbar_wait(&empty[b], (rp.epar >> b) & 1u);
-          rp.epar ^= 1u << b;
-        }
-        rp.filled |= 1u << b;
-        stream_issue<TB>(P, tab + prod.seg * (kMaxZ + 1), smem + b * P.buf_bytes, &full[b], kind, pp, pc0, pc1, dold,
-                         dnew);
-        ++k;
-      }
-    }
-    __syncthreads();
-    return;
-  }
-  // ---- consumers
-  int cp;
-  int64_t cc0, cc1;
-  pc.mark(0);
-  double acc[2 * MT];
-#pragma unroll
-  for (int q = 0; q < 2 * MT; ++q)
-    acc[q] = 0.0;
-  int k = 0;
-  int cur_p = -1;
-  // TB % m == 0 (every m <= 8 but 7): a consumer thread's elements e = tid + k TB all belong to
-  // column c = tid % m, so the element loops hoist the system's scalars, and phase B keeps its
-  // (r, r) partial in one register (the other columns' partials of this thread stay zero).
-  const bool cfix = (TB % m) == 0;
-  const int cth = threadIdx.x % m;
-  double accb = 0.0;
-  auto flush = [&](int pnt) {
-    if (kind == 2 && cfix && !P.serial)
-    {
-#pragma unroll
-      for (int q = 0; q < MT; ++q)
-        acc[q] = q == cth ? accb : 0.0;
-      accb = 0.0;
-    }
-    double pv[2 * MT];
-#pragma unroll
-    for (int q = 0; q < 2 * MT; ++q)
-      pv[q] = 0.0;
-#pragma unroll
-    for (int c = 0; c < MT; ++c)
-      if (c < m)
-      {
-        pv[c] = acc[c];
-        if (kind == 0)
-          pv[m + c] = acc[MT + c];
-      }
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int q = 0; q < 2 * MT; ++q)
-    {
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1)
-        pv[q] = __dadd_rn(pv[q], __shfl_xor_sync(0xffffffffu, pv[q], off));
-    }
-    if (lane == 0)
-    {
-#pragma unroll
-      for (int q = 0; q < 2 * MT; ++q)
-        sh.wsum[warp][q] = pv[q];
-    }
-    consumer_sync<TB>();
-    if (warp == 0)
-    {
-      for (int q = 0; q < nv; ++q)
-      {
-        double x = lane < TB / 32 ? sh.wsum[lane][q] : 0.0;
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1)
-          x = __dadd_rn(x, __shfl_xor_sync(0xffffffffu, x, off));
-        if (lane == 0)
-          P.partial[(static_cast<int64_t>(pnt) * 2 * kMaxM + q) * gridDim.x + blockIdx.x] = x;
-      }
-    }
-    consumer_sync<TB>();
-#pragma unroll
-    for (int q = 0; q < 2 * MT; ++q)
-      acc[q] = 0.0;
-  };
-  while (chunk_next(sh, CH, cons, cp, cc0, cc1))
-  {
-    const int bi = k % P.nb;
-    pc.mark(1);
-    if (cp != cur_p)
-    {
-      if (cur_p >= 0)
-        flush(cur_p);
-      cur_p = cp;
-    }
-    pc.mark(2);
-    mbar_wait(&full[bi], (phase_bits >> bi) & 1u);
-    phase_bits ^= 1u << bi;
-    pc.mark(3);
-    unsigned char *buf = smem + bi * P.buf_bytes;
-    const int64_t base_i = cc0;
-    const int R = static_cast<int>(cc1 - cc0);
-    const int sb = cp * m; // first system of the point
-    if (kind == 2)
-    {
-      // r -= alpha w, partial (r, r): one element (row, column) per thread.  x~ += alpha d
-      // (krylov.cpp:113) is deferred to the next phase A, which streams d anyway.
-      const double *rs = reinterpret_cast<const double *>(buf + P.b_r);
-      const double *ws = reinterpret_cast<const double *>(buf + P.b_w);
-      const double *xs = reinterpret_cast<const double *>(buf + P.b_x);
-      const double *ds = reinterpret_cast<const double *>(buf + P.b_d);
-      double *rg = const_cast<double *>(vrow(P, P.r, cp, base_i));
-      double *xg = const_cast<double *>(vrow(P, P.xt, cp, base_i));
-      const int ne = R * m;
-      if (P.serial)
-      {
-        // w is dead once in shared memory: drop its L2 lines (no write-back to HBM), only
-        // lines that lie wholly inside this chunk's rows
-        const uintptr_t wa = reinterpret_cast<uintptr_t>(vrow(P, P.w, cp, base_i));
-        const uintptr_t l0 = (wa + 127) & ~static_cast<uintptr_t>(127);
-        const uintptr_t l1 = (wa + static_cast<uintptr_t>(ne) * 8) & ~static_cast<uintptr_t>(127);
-        for (uintptr_t a = l0 + static_cast<uintptr_t>(threadIdx.x) * 128; a < l1; a += static_cast<uintptr_t>(TB) * 128)
-          discard_l2(reinterpret_cast<const void *>(a));
-        const uint64_t pol = policy_evict_first();
-        for (int e = threadIdx.x; e < ne; e += TB)
-        {
-          const int c = col_of<MT>(e, m);
-          if (sh.state[sb + c] != kRun)
-            continue;
-          const double al = sh.alpha[sb + c];
-          if (!P.fold)
-            stg_hint(xg + e, __dadd_rn(xs[e], __dmul_rn(al, ds[e])), pol);
-          const double rn = __dadd_rn(rs[e], __dmul_rn(-al, ws[e]));
-          stg_hint(rg + e, rn, pol);
-          acc_add<MT>(acc, c, __dmul_rn(rn, rn));
-        }
-      }
-      else if (cfix)
-      {
-        if (sh.state[sb + cth] == kRun)
-        {
-          const double al = sh.alpha[sb + cth];
-          for (int e = threadIdx.x; e < ne; e += TB)
-          {
-            if (!P.fold)
-              __stcg(xg + e, __dadd_rn(xs[e], __dmul_rn(al, ds[e])));
-            const double rn = __dadd_rn(rs[e], __dmul_rn(-al, ws[e]));
-            __stcg(rg + e, rn);
-            accb = __dadd_rn(accb, __dmul_rn(rn, rn));
-          }
-        }
-      }
-      else
-      for (int e = threadIdx.x; e < ne; e += TB)
-      {
-        const int c = col_of<MT>(e, m);
-        if (sh.state[sb + c] != kRun)
-          continue;
-        const double al = sh.alpha[sb + c];
-        if (!P.fold)
-          __stcg(xg + e, __dadd_rn(xs[e], __dmul_rn(al, ds[e])));
-        const double rn = __dadd_rn(rs[e], __dmul_rn(-al, ws[e]));
-        __stcg(rg + e, rn);
-        acc_add<MT>(acc, c, __dmul_rn(rn, rn));
-      }
-    }
-    else
-    {
-      const int H0 = P.hmax;
-      const double *vr = reinterpret_cast<const double *>(buf + P.a_vr);
-      const double *vd = reinterpret_cast<const double *>(buf + P.a_vd);
-      double *s0 = reinterpret_cast<double *>(smem + P.off_stage0);
-      double *sA = reinterpret_cast<double *>(smem + P.off_stage1);
-      double *sB = reinterpret_cast<double *>(smem + P.off_stage2);
-      // stage 0: d = fresh ? r : r + beta d_old over the halo-extended chunk; the deferred
-      // x~ += alpha_prev d_old on own rows.  Check pass: source x~ + alpha_prev d_old (not
-      // written back: neighbours read the same x~ rows as halo during this pass).
-      const double *vx = reinterpret_cast<const double *>(buf + P.a_vx);
-      const int ne0 = (R + 2 * H0) * m;
-      const int lo = H0 * m, hi = (H0 + R) * m;
-      double *dg = kind == 0 ? const_cast<double *>(vrow(P, dnew, cp, base_i - H0)) : nullptr;
-      double *xg = kind == 0 ? const_cast<double *>(vrow(P, P.xt, cp, base_i - H0)) : nullptr;
-      if (cfix)
-      {
-        const int sys = sb + cth;
-        const bool fr = sh.fresh[sys] != 0, pd = sh.pend[sys] != 0, run = sh.state[sys] == kRun;
-        const double be = sh.beta[sys], al = sh.alpha[sys];
-        if (kind == 1)
-          for (int e = threadIdx.x; e < ne0; e += TB)
-            s0[stage_idx(e, m, P.pst)] = pd ? __dadd_rn(vr[e], __dmul_rn(al, vd[e])) : vr[e];
-        else
-          for (int e = threadIdx.x; e < ne0; e += TB)
-          {
-            const double v = fr ? vr[e] : __dadd_rn(vr[e], __dmul_rn(be, vd[e]));
-            if (e >= lo && e < hi)
-            {
-              __stcg(dg + e, v);
-              if (pd && run)
-                __stcg(xg + e, __dadd_rn(vx[e - lo], __dmul_rn(al, vd[e])));
-            }
-            s0[stage_idx(e, m, P.pst)] = v;
-          }
-      }
-      else
-      for (int e = threadIdx.x; e < ne0; e += TB)
-      {
-        const int c = col_of<MT>(e, m);
-        const int sys = sb + c;
-        double v;
-        if (kind == 1)
-          v = sh.pend[sys] ? __dadd_rn(vr[e], __dmul_rn(sh.alpha[sys], vd[e])) : vr[e];
-        else
-        {
-          v = sh.fresh[sys] ? vr[e] : __dadd_rn(vr[e], __dmul_rn(sh.beta[sys], vd[e]));
-          if (e >= lo && e < hi)
-          {
-            __stcg(dg + e, v);
-            if (sh.pend[sys] && sh.state[sys] == kRun)
-              __stcg(xg + e, __dadd_rn(vx[e - lo], __dmul_rn(sh.alpha[sys], vd[e])));
-          }
-        }
-        s0[stage_idx(e, m, P.pst)] = v;
-      }
-      consumer_sync<TB>();
-      pc.mark(4);
-      const double *src = s0;
-      int hs = H0;
-      for (int st = 0; st < P.z; ++st)
-      {
-        const int hd = P.halo[st + 1];
-        const PEll F = tab[cons.seg * (kMaxZ + 1) + 1 + st];
-        const double *fv = reinterpret_cast<const double *>(buf + P.a_fv[st]);
-        const unsigned long long *fo = reinterpret_cast<const unsigned long long *>(buf + P.a_fo[st]);
-        double *dst = (st & 1) ? sB : sA;
-        const int span = R + 2 * hd;
-        for (int q = threadIdx.x; q < span; q += TB)
-        {
-          double a2[MT];
-          ell_row_any<MT, 10>(fv + q * F.E, fo + q * F.ow, F.E, F.ow, src, q + hs - hd, m, a2, P.pst);
-          st_stage<MT>(dst, q, a2, m, P.pst);
-        }
-        consumer_sync<TB>();
-        src = dst;
-        hs = hd;
-      }
-      pc.mark(5);
-      const PEll A = tab[cons.seg * (kMaxZ + 1)];
-      const double *av = reinterpret_cast<const double *>(buf + P.a_av);
-      const unsigned long long *ao = reinterpret_cast<const unsigned long long *>(buf + P.a_ao);
-      double *wg = const_cast<double *>(vrow(P, P.w, cp, base_i));
-      for (int lr = threadIdx.x; lr < R; lr += TB)
-      {
-        double a2[MT];
-        ell_row_any<MT, 5>(av + lr * A.E, ao + lr * A.ow, A.E, A.ow, src, lr + hs, m, a2, P.pst);
-        if (kind == 1)
-        {
-          const int64_t i = base_i + lr;
-#pragma unroll
-          for (int c = 0; c < MT; ++c)
-          {
-            if (c >= m)
-              break;
-            const double res = __dsub_rn(__ldg(vrow(P, P.b, cp, i) + c), a2[c]);
-            __stcg(wg + lr * m + c, res);
-            __stcg(const_cast<double *>(vrow(P, P.sol, cp, i)) + c, src[stage_idx((lr + hs) * m + c, m, P.pst)]);
-            acc[c] = __dadd_rn(acc[c], __dmul_rn(res, res));
-          }
-        }
-        else
-        {
-          double dn[MT];
-          ld_stage<MT>(s0, H0 + lr, dn, m, P.pst);
-          stg_row<MT>(wg + lr * m, a2, m);
-#pragma unroll
-          for (int c = 0; c < MT; ++c)
-            if (c < m)
-            {
-              acc[c] = __dadd_rn(acc[c], __dmul_rn(dn[c], a2[c]));
-              acc[MT + c] = __dadd_rn(acc[MT + c], __dmul_rn(dn[c], dn[c]));
-            }
-        }
-      }
-    }
-    pc.mark(kind == 2 ? 7 : 6);
-    consumer_sync<TB>(); // buffer bi and the stage buffers are free again
-    if (threadIdx.x == 0)
-      mbar_arrive(&empty[bi]);
-    pc.mark(8);
-    ++k;
-  }
-  if (cur_p >= 0)
-    flush(cur_p);
-  __syncthreads();
-  pc.mark(2);
-}
-
-template <int TB, int MT, bool PR = false>
-__global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
-{
-  constexpr int TBX = TB + 32; // TB consumer threads + one producer warp
-  cgrp::grid_group grid = cgrp::this_grid();
-  extern __shared__ __align__(128) unsigned char smem_s[];
-  __shared__ BandShared<TBX> sh;
-  __shared__ __align__(8) uint64_t bars[2 * kStreamNB]; // full[NB], empty[NB]
-  // operator descriptors per segment (serial schedule: per point): A, then stage factors
-  __shared__ PEll tab[kTabSlots * (kMaxZ + 1)];
-  __shared__ int64_t ser_rows[2]; // serial schedule: this block's row slab, the same for every point
-  const int m = P.m;
-  const int S = P.l * m;
-  uint32_t phase_bits = 0;
-  RingProducer rp{0u, 0u};
-  PhaseClock<PR> pc{PR && P.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0, clock64(), {}};
-  if (threadIdx.x == 0)
-  {
-    int q = 0;
-    while (q < kMaxSeg && P.seg[blockIdx.x * kMaxSeg + q].p >= 0)
-    {
-      sh.seg[q] = P.seg[blockIdx.x * kMaxSeg + q];
-      ++q;
-    }
-    sh.nseg = q;
-    ser_rows[0] = q > 0 ? sh.seg[0].rs : 0;
-    ser_rows[1] = q > 0 ? sh.seg[0].re : 0;
-    const int ntab = P.serial ? P.l : q;
-    for (int g = 0; g < ntab; ++g)
-    {
-      const int p = P.serial ? g : sh.seg[g].p;
-      PEll a = P.A[p];
-      if (P.eqA[p])
-        a.o = P.A[0].o;
-      tab[g * (kMaxZ + 1)] = a;
-      for (int st = 0; st < P.z; ++st)
-      {
-        const int f = P.z - 1 - st;
-        PEll fe = P.F[p * P.z + f];
-        if (P.eqF[p * P.z + f])
-          fe.o = P.F[f].o;
-        tab[g * (kMaxZ + 1) + 1 + st] = fe;
-      }
-    }
-    for (int b = 0; b < 2 * kStreamNB; ++b)
-      mbar_init(&bars[b], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  for (int p = threadIdx.x; p < P.l; p += TBX)
-    sh.pmask[p] = 1;
-  __syncthreads();
-  // rows of every masked point this block owns (serial schedule: the block's slab of each point)
-  auto for_rows = [&](auto &&fn) {
-    if (P.serial)
-    {
-      for (int p = 0; p < P.l; ++p)
-        if (sh.pmask[p])
-          fn(p, ser_rows[0], ser_rows[1]);
-    }
-    else
-      for_segments(P, sh, fn);
-  };
-  // serial schedule: make point p the block's only segment (and the only masked point)
-  auto pick_point = [&](int p) {
-    __syncthreads();
-    for (int q = threadIdx.x; q < P.l; q += TBX)
-      sh.pmask[q] = q == p;
-    if (threadIdx.x == 0)
-    {
-      sh.seg[0] = Seg{p, static_cast<int>(ser_rows[0]), static_cast<int>(ser_rows[1]), 0};
-      sh.nseg = 1;
-    }
-    __syncthreads();
-  };
-  auto point_live = [&](int p) {
-    bool live = false;
-    for (int c = 0; c < m; ++c)
-      live |= sh.state[p * m + c] == kRun;
-    return live;
-  };
-  // ---- phase 0: ||b||^2 (one pass, plain loads)
-  for_rows([&](int p, int64_t rs, int64_t re) {
-    begin_point(sh);
-    for (int64_t c0 = rs; c0 < re; c0 += TBX)
-    {
-      const int64_t i = c0 + threadIdx.x;
-      double pk[MT];
-#pragma unroll
-      for (int c = 0; c < MT; ++c)
-      {
-        pk[c] = 0.0;
-        if (c < m && i < re)
-        {
-          const double bv = __ldg(vrow(P, P.b, p, i) + c);
-          pk[c] = __dmul_rn(bv, bv);
-        }
-      }
-      chunk_sum<TBX, MT>(sh, pk, m);
-    }
-    end_point(P.partial, sh, p, m);
-  });
-  grid.sync();
-  reduce_blocks<TBX, StreamParams>(P, sh, m);
-  for (int s = threadIdx.x; s < S; s += TBX)
-  {
-    const double bb = sh.tot[s];
-    const double bn = sqrt(bb);
-    sh.bnorm[s] = bn;
-    sh.rho[s] = bb;
-    sh.target[s] = P.rtol * bn;
-    sh.state[s] = bn == 0.0 ? kZeroRhs : kRun;
-    sh.fresh[s] = 1;
-    sh.pend[s] = 0;
-    sh.beta[s] = 0.0;
-    sh.sit[s] = 0;
-  }
-  __syncthreads();
-
-  auto copy_finish = [&]() {
-    for_rows([&](int p, int64_t rs, int64_t re) {
-      for (int64_t i = rs + threadIdx.x; i < re; i += TBX)
-        for (int c = 0; c < m; ++c)
-        {
-          const int s = p * m + c;
-          const int64_t o = static_cast<int64_t>(s) * P.n + i;
-          if (sh.state[s] == kPendingConv || sh.state[s] == kMaxed)
-          {
-            if (P.X)
-              P.X[o] = __ldcg(vrow(P, P.sol, p, i) + c);
-            if (P.TR)
-              P.TR[o] = __ldcg(vrow(P, P.w, p, i) + c);
-          }
-          else if (sh.state[s] == kPendingRestart)
-            __stcg(const_cast<double *>(vrow(P, P.r, p, i)) + c, __ldcg(vrow(P, P.w, p, i) + c));
-        }
-    });
-    fence_async_global();
-  };
-
-  // true-residual check pass over the masked points (serial schedule: one point at a time,
-  // no barrier in between -- the passes are independent); leaves pmask as it found it
-  auto check_pass = [&](const double *dcur) {
-    if (!P.serial)
-    {
-      stream_pass<TB, MT, kStreamNB, PhaseClock<PR>>(P, sh, tab, smem_s, bars, bars + kStreamNB, phase_bits, rp, 1, dcur, nullptr, pc);
-      return;
-    }
-    uint32_t msk = 0;
-    for (int p = 0; p < P.l; ++p)
-      msk |= sh.pmask[p] ? 1u << p : 0u;
-    for (int p = 0; p < P.l; ++p)
-      if ((msk >> p) & 1u)
-      {
-        pick_point(p);
-        stream_pass<TB, MT, kStreamNB, PhaseClock<PR>>(P, sh, tab + p * (kMaxZ + 1), smem_s, bars, bars + kStreamNB, phase_bits, rp, 1,
-                                       dcur, nullptr, pc);
-      }
-    __syncthreads();
-    for (int p = threadIdx.x; p < P.l; p += TBX)
-      sh.pmask[p] = (msk >> p) & 1u;
-    __syncthreads();
-  };
-  // after phase A's reduction: alpha or breakdown for the running systems of masked points
-  auto after_a = [&](int64_t itn) {
-    for (int s = threadIdx.x; s < S; s += TBX)
-    {
-      if (!sh.pmask[s / m])
-        continue;
-      sh.pend[s] = 0; // phase A applied the deferred x~ update
-      if (sh.state[s] != kRun)
-        continue;
-      const int p = s / m, c = s % m;
-      const double curv = sh.tot[p * m + c];
-      const double dd = sh.tot[S + p * m + c];
-      if (!(curv > 1e-30 * dd))
-      {
-        sh.state[s] = kBreakdown;
-        sh.sit[s] = itn;
-      }
-      else
-        sh.alpha[s] = sh.rho[s] / curv;
-    }
-    __syncthreads();
-  };
-  // after phase B's reduction: beta, rho for the running systems of masked points (itn: the
-  // iteration just completed, 0-based)
-  auto after_b = [&](int64_t itn) {
-    for (int s = threadIdx.x; s < S; s += TBX)
-    {
-      if (!sh.pmask[s / m] || sh.state[s] != kRun)
-        continue;
-      const double rn = sh.tot[s];
-      if (P.hist && blockIdx.x == 0 && itn < P.hist_cap)
-        P.hist[static_cast<int64_t>(s) * P.hist_cap + itn] = sqrt(rn) / sh.bnorm[s];
-      sh.beta[s] = rn / sh.rho[s];
-      sh.rho[s] = rn;
-      sh.fresh[s] = 0;
-      sh.pend[s] = P.fold; // x~ += alpha d owed to the next phase A / check pass
-    }
-    __syncthreads();
-  };
-
-  int cur = 0;
-  int64_t it = 0;
-  for (;;)
-  {
-    if (it >= P.maxit)
-      break;
-    if (threadIdx.x == 0)
-      sh.flag = 0;
-    __syncthreads();
-    for (int p = threadIdx.x; p < P.l; p += TBX)
-    {
-      int need = 0;
-      for (int c = 0; c < m; ++c)
-      {
-        const int s = p * m + c;
-        need |= sh.state[s] == kRun && sqrt(sh.rho[s]) <= sh.target[s];
-      }
-      sh.pmask[p] = need;
-      if (need)
-        atomicOr(&sh.flag, 1);
-    }
-    __syncthreads();
-    if (sh.flag)
-    {
-      check_pass(cur ? P.dbuf1 : P.dbuf0);
-      fence_async_global();
-      grid.sync();
-      reduce_blocks<TBX, StreamParams>(P, sh, m);
-      for (int s = threadIdx.x; s < S; s += TBX)
-      {
-        if (!(sh.state[s] == kRun && sqrt(sh.rho[s]) <= sh.target[s]))
-          continue;
-        const double tt = sh.tot[s];
-        if (sqrt(tt) <= sh.target[s])
-        {
-          sh.state[s] = kPendingConv;
-          sh.sit[s] = it;
-        }
-        else
-        {
-          sh.rho[s] = tt;
-          if (sqrt(tt) <= sh.target[s])
-          {
-            sh.state[s] = kPendingConv;
-            sh.sit[s] = it;
-          }
-          else
-          {
-            sh.state[s] = kPendingRestart;
-            sh.fresh[s] = 1;
-          }
-        }
-      }
-      __syncthreads();
-      copy_finish();
-      grid.sync();
-      for (int s = threadIdx.x; s < S; s += TBX)
-      {
-        if (sh.state[s] == kPendingConv)
-          sh.state[s] = kConverged;
-        else if (sh.state[s] == kPendingRestart)
-          sh.state[s] = kRun;
-      }
-      __syncthreads();
-    }
-    if (threadIdx.x == 0)
-      sh.flag = 0;
-    __syncthreads();
-    for (int p = threadIdx.x; p < P.l; p += TBX)
-    {
-      int live = 0;
-      for (int c = 0; c < m; ++c)
-        live |= sh.state[p * m + c] == kRun;
-      sh.pmask[p] = live;
-      if (live)
-        atomicOr(&sh.flag, 1);
-    }
-    __syncthreads();
-    if (!sh.flag)
-      break;
-    double *d_old = cur ? P.dbuf1 : P.dbuf0;
-    double *d_new = cur ? P.dbuf0 : P.dbuf1;
-    if (P.serial)
-    {
-      // one point at a time on every block: phase A writes d_new and w and phase B re-reads
-      // them (and r) straight from L2, two grid barriers per point
-      uint32_t live = 0;
-      for (int p = 0; p < P.l; ++p)
-        live |= sh.pmask[p] ? 1u << p : 0u;
-      for (int p = 0; p < P.l; ++p)
-      {
-        if (!((live >> p) & 1u))
-          continue;
-        pick_point(p);
-        const PEll *tp = tab + p * (kMaxZ + 1);
-        pc.mark(9);
-        stream_pass<TB, MT, kStreamNB, PhaseClock<PR>>(P, sh, tp, smem_s, bars, bars + kStreamNB, phase_bits, rp, 0, d_old, d_new, pc);
-        fence_async_global();
-        grid.sync();
-        pc.mark(10);
-        reduce_blocks<TBX, StreamParams>(P, sh, 2 * m);
-        after_a(it);
-        pc.mark(11);
-        stream_pass<TB, MT, kStreamNB, PhaseClock<PR>>(P, sh, tp, smem_s, bars, bars + kStreamNB, phase_bits, rp, 2, d_old, d_new, pc);
-        fence_async_global();
-        grid.sync();
-        pc.mark(10);
-        reduce_blocks<TBX, StreamParams>(P, sh, m);
-        after_b(it);
-        pc.mark(11);
-      }
-      ++it;
-      cur ^= 1;
-      continue;
-    }
-    pc.mark(9);
-    stream_pass<TB, MT, kStreamNB, PhaseClock<PR>>(P, sh, tab, smem_s, bars, bars + kStreamNB, phase_bits, rp, 0, d_old, d_new, pc);
-    fence_async_global();
-    grid.sync();
-    pc.mark(10);
-    reduce_blocks<TBX, StreamParams>(P, sh, 2 * m);
-    pc.mark(11);
-    after_a(it);
-    pc.mark(9);
-    stream_pass<TB, MT, kStreamNB, PhaseClock<PR>>(P, sh, tab, smem_s, bars, bars + kStreamNB, phase_bits, rp, 2, d_old, d_new, pc);
-    fence_async_global();
-    grid.sync();
-    pc.mark(10);
-    reduce_blocks<TBX, StreamParams>(P, sh, m);
-    pc.mark(11);
-    after_b(it);
-    ++it;
-    cur ^= 1;
-  }
-  // ---- budget exhausted: final true-residual check
-  if (threadIdx.x == 0)
-    sh.flag = 0;
-  __syncthreads();
-  for (int p = threadIdx.x; p < P.l; p += TBX)
-  {
-    int need = 0;
-    for (int c = 0; c < m; ++c)
-      need |= sh.state[p * m + c] == kRun;
-    sh.pmask[p] = need;
-    if (need)
-      atomicOr(&sh.flag, 1);
-  }
-  __syncthreads();
-  if (sh.flag)
-  {
-    check_pass(cur ? P.dbuf1 : P.dbuf0);
-    fence_async_global();
-    grid.sync();
-    reduce_blocks<TBX, StreamParams>(P, sh, m);
-    for (int s = threadIdx.x; s < S; s += TBX)
-    {
-      if (sh.state[s] != kRun)
-        continue;
-      const double tt = sh.tot[s];
-      sh.state[s] = sqrt(tt) <= sh.target[s] ? kPendingConv : kMaxed;
-      sh.sit[s] = it;
-    }
-    __syncthreads();
-    copy_finish();
-    for (int s = threadIdx.x; s < S; s += TBX)
-      if (sh.state[s] == kPendingConv)
-        sh.state[s] = kConverged;
-    __syncthreads();
-  }
-  for (int p = threadIdx.x; p < P.l; p += TBX)
-    sh.pmask[p] = 1;
-  __syncthreads();
-  for_rows([&](int p, int64_t rs, int64_t re) {
-    for (int64_t i = rs + threadIdx.x; i < re; i += TBX)
-      for (int c = 0; c < m; ++c)
-      {
-        const int s = p * m + c;
-        const int64_t o = static_cast<int64_t>(s) * P.n + i;
-        if (sh.state[s] == kZeroRhs)
-        {
-          if (P.X)
-            P.X[o] = 0.0;
-          if (P.TR)
-            P.TR[o] = 0.0;
-          if (P.REC)
-            P.REC[o] = 0.0;
-        }
-        else if (sh.state[s] != kBreakdown && P.REC)
-          P.REC[o] = __ldcg(vrow(P, P.r, p, i) + c);
-      }
-  });
-  if constexpr (PR)
-    if (pc.on)
-      for (int k = 0; k < 12; ++k)
-        P.prof[k] = pc.acc[k];
-  if (blockIdx.x == 0)
-  {
-    for (int s = threadIdx.x; s < S; s += TBX)
-    {
-      const int st = sh.state[s];
-      P.iters[s] = sh.sit[s];
-      P.conv[s] = (st == kConverged || st == kZeroRhs) ? 1 : 0;
-      P.status[s] = st == kBreakdown ? MGPU_ERR_BREAKDOWN : MGPU_OK;
-      P.bd_iter[s] = st == kBreakdown ? sh.sit[s] : -1;
-    }
-    if (threadIdx.x == 0)
-      *P.loop_iters = it;
-  }
-}
-
-// CSR -> padded row-major ELL (values [row][E], int8 offsets packed in ow u64 words)
-__global__ void csr_to_pell(int64_t n, DCsr M, int E, int ow, double *vals, unsigned long long *offs)
-{
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n)
-    return;
-  const int64_t k0 = M.rp[i], k1 = M.rp[i + 1];
-  unsigned long long w[kEllMax / 8] = {};
-  for (int t = 0; t < E; ++t)
-  {
-    const bool has = k0 + t < k1;
-    vals[i * E + t] = has ? M.v[k0 + t] : 0.0; // padding adds +0 after the row's entries
-    if (has)
-      w[t >> 3] |=
-          static_cast<unsigned long long>(static_cast<unsigned char>(static_cast<signed char>(M.ci[k0 + t] - i)))
-          << (8 * (t & 7));
-  }
-  for (int q = 0; q < ow; ++q)
-    offs[i * ow + q] = w[q];
-}
-
-__global__ void stream_init(int l, int m, int64_t n, int64_t ldv, const double *__restrict__ B, int64_t ldb,
-                            double *b, double *r, double *d, double *xt)
-{
-  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t per = n * m;
-  if (g >= per * l)
-    return;
-  const int64_t p = g / per, rem = g - p * per, i = rem / m, c = rem - i * m;
-  const double v = B[p * ldb + c * n + i];
-  const int64_t o = p * ldv + (kPadR + i) * m + c;
-  b[o] = v;
-  r[o] = v;
-  d[o] = v;
-  xt[o] = 0.0;
-}
 
 // B [p][c][row] (column-major per point; ldb between points) -> interleaved
 // b, r = b, d = b, x~ = 0.
@@ -2806,341 +1346,6 @@ bool band_plan(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu
   return h <= kMaxHalo;
 }
 
-// Host side of cg_stream.  Returns false if the chunk buffers do not fit.
-bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_csr *const *chains, int64_t n,
-                  int m, const double *B_dev, int64_t ldb, const int *halo, int hmax, double rtol, int64_t maxit,
-                  double *X_dev, double *REC_dev, double *TR_dev, int64_t *d_it, int *d_conv, int *d_st, int64_t *d_bd,
-                  double *d_hist, int64_t hist_cap, int64_t *d_loop)
-{
-  constexpr int TB = 480; // consumer threads; + one producer warp = 512
-  cudaStream_t s = ctx->stream;
-  // even halos keep every bulk copy 16-byte aligned; rebuilt inside-out so that
-  // hal[st] >= hal[st + 1] + bw(factor of stage st) still holds
-  std::vector<int> hal(static_cast<size_t>(z + 1));
-  hal[z] = (halo[z] + 1) & ~1;
-  for (int st = z - 1; st >= 0; --st)
-    hal[st] = (hal[st + 1] + (halo[st] - halo[st + 1]) + 1) & ~1;
-  const int H0 = hal[0];
-  (void)hmax;
-  if (H0 >= kPadR || // even_up(c1 - c0 + 2 H0) may reach one row past the kPadR padding when H0 == kPadR
-       l > kMaxPoints || static_cast<int64_t>(l) * m > kMaxSys || l > ctx->num_sms * kMaxSeg)
-    return false;
-  // ---- padded ELL operators
-  auto ell_of = [&](const mgpu_csr *M, std::vector<DBuf> &keep) {
-    // exact row width (odd widths allowed: a 5-entry row streams 40 bytes, not 48); bulk
-    // copies stay 16-byte multiples because chunk row counts are even
-    const int E = static_cast<int>(csr_max_row(ctx, const_cast<mgpu_csr *>(M)));
-    const int Ee = E < 1 ? 1 : E;
-    const int ow = (Ee + 7) / 8;
-    const int64_t rows = n + 2 * kPadR;
-    keep.emplace_back(sizeof(double) * rows * Ee, s);
-    DBuf &v = keep.back();
-    keep.emplace_back(sizeof(unsigned long long) * rows * ow, s);
-    DBuf &o = keep.back();
-    MG_CUDA(cudaMemsetAsync(v.ptr, 0, sizeof(double) * rows * Ee, s));
-    MG_CUDA(cudaMemsetAsync(o.ptr, 0, sizeof(unsigned long long) * rows * ow, s));
-    double *v0 = v.as<double>() + kPadR * Ee;
-    unsigned long long *o0 = o.as<unsigned long long>() + kPadR * ow;
-    csr_to_pell<<<blocks_for(n), kThreads, 0, s>>>(n, M->view(), Ee, ow, v0, o0);
-    check_launch(ctx, "csr_to_pell");
-    return PEll{v0, o0, Ee, ow};
-  };
-  std::vector<DBuf> keep;
-  keep.reserve(static_cast<size_t>(2 * l * (z + 1) + 16));
-  for (int p = 0; p < l; ++p)
-  {
-    // rows of up to kEllMax entries (collapsed update chains widen with every product)
-    if (csr_max_row(ctx, const_cast<mgpu_csr *>(A[p])) > kEllMax)
-      return false;
-    for (int f = 0; f < z; ++f)
-      if (csr_max_row(ctx, const_cast<mgpu_csr *>(chains[static_cast<size_t>(p) * z + f])) > kEllMax)
-        return false;
-  }
-  std::vector<PEll> hA(static_cast<size_t>(l)), hF(static_cast<size_t>(l) * (z > 0 ? z : 1));
-  int EA = 0;
-  std::vector<int> EF(static_cast<size_t>(z > 0 ? z : 1), 0);
-  std::vector<int> OWF(static_cast<size_t>(z > 0 ? z : 1), 1); // offset words per row (1: <= 8 entries)
-  int OWA = 1;
-  for (int p = 0; p < l; ++p)
-  {
-    hA[p] = ell_of(A[p], keep);
-    EA = std::max(EA, hA[p].E);
-    for (int f = 0; f < z; ++f)
-    {
-      hF[static_cast<size_t>(p) * z + f] = ell_of(chains[static_cast<size_t>(p) * z + f], keep);
-      const int st = z - 1 - f;
-      EF[st] = std::max(EF[st], hF[static_cast<size_t>(p) * z + f].E);
-      OWF[st] = std::max(OWF[st], hF[static_cast<size_t>(p) * z + f].ow);
-    }
-    OWA = std::max(OWA, hA[p].ow);
-  }
-  // x~ update placement: deferred into phase A, which streams d_old anyway (one vector pass
-  // fewer).  Measured on B200 once the kernel dropped to 107 registers: configs[3] (m = 4, P = I)
-  // 1029 -> 1005 us/iter, configs[4] share 5025 -> 4891, configs[2] shape (m = 1, one factor)
-  // 36.9 -> 36.1; earlier (122 registers) phase A was latency-bound and m = 4 / chains lost.
-  // MGPU_OPT_STREAM_FOLD = 0 overrides (diagnostics).
-  const bool fold = ctx->opt[MGPU_OPT_STREAM_FOLD] != 0;
-  // ---- shared-memory plan: the largest chunk height whose double buffer fits
-  StreamParams P{};
-  size_t dyn = 0;
-  int64_t CH = 0;
-  int optin = 0;
-  MG_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
-  const size_t stat = sizeof(BandShared<TB + 32>) + sizeof(PEll) * kTabSlots * (kMaxZ + 1) + 128;
-  // (chunk rows, ring depth) in order of preference; MGPU_STREAM_CFG="rows,depth" forces one (diagnostics)
-  // largest chunk first (per-chunk barriers and pipeline bookkeeping amortise over its rows), 3-deep ring
-  // before 2-deep at equal height.  With m >= 4 the height is capped at 448 rows and multiples of
-  // 128 rows are skipped: with every block striding through HBM in lock step, 512 / 640 rows
-  // measured 872 / 876 us per iteration on configs[3] against 843 / 836 for 576 / 448, and 448
-  // (2-deep) against the 576 default gave configs[3] 847 -> 837, configs[4] 4152 -> 4085.  m = 1
-  // (configs[2] shape) measured best on its largest chunk.
-  std::vector<std::pair<int64_t, int>> cands;
-  for (int64_t ch = 1024; ch >= 128; ch -= 64)
-  {
-    if (m >= 4 && (ch % 128 == 0 || ch > 448))
-      continue;
-    if (m < 4) // m >= 4: 2-deep only (448 rows 3-deep measured 924 us against 837 2-deep)
-      cands.push_back({ch, 3});
-    cands.push_back({ch, 2});
-  }
-  cands.push_back({128, 3});
-  cands.push_back({128, 2});
-  if (ctx->opt[MGPU_OPT_STREAM_CHUNK] > 0) // forced plan (diagnostics)
-  {
-    const int fd = ctx->opt[MGPU_OPT_STREAM_RING] ? static_cast<int>(ctx->opt[MGPU_OPT_STREAM_RING]) : 2;
-    cands.insert(cands.begin(), {ctx->opt[MGPU_OPT_STREAM_CHUNK], fd});
-  }
-  for (const auto &cand : cands)
-  {
-    const int64_t ch = cand.first;
-    const int nb = cand.second;
-    size_t off = 0;
-    auto take = [&](size_t bytes) {
-      const size_t o2 = off;
-      off += (bytes + 127) & ~static_cast<size_t>(127);
-      return o2;
-    };
-    const int64_t vrows = (ch + 2 * H0 + 1) & ~1ll;
-    P.a_vr = take(sizeof(double) * vrows * m);
-    P.a_vd = take(sizeof(double) * vrows * m);
-    P.a_vx = fold ? take(sizeof(double) * ch * m) : 0;
-    for (int st = 0; st < z; ++st)
-    {
-      const int64_t rows = (ch + 2 * hal[st + 1] + 1) & ~1ll;
-      P.a_fv[st] = take(sizeof(double) * rows * EF[st]);
-      P.a_fo[st] = take(sizeof(unsigned long long) * rows * OWF[st]);
-    }
-    P.a_av = take(sizeof(double) * ch * EA);
-    P.a_ao = take(sizeof(unsigned long long) * ch * OWA);
-    const size_t a_bytes = off;
-    off = 0;
-    const size_t b_bytes = sizeof(double) * ch * m * (fold ? 2 : 4);
-    P.buf_bytes = (std::max(a_bytes, b_bytes) + 127) & ~static_cast<size_t>(127);
-    off = nb * P.buf_bytes;
-    // m == 4 with a chain: planar stage buffers, one plane stride (the widest buffer's rows) for all
-    const int64_t srows0 = ch + 2 * H0;
-    P.pst = (m == 4 && z >= 1) ? static_cast<int>(2 * srows0) : 0; // (P = I measured 842 -> 859 us planar)
-    P.off_stage0 = take(sizeof(double) * srows0 * m);
-    P.off_stage1 = z >= 1 ? take(sizeof(double) * (P.pst ? srows0 : ch + 2 * hal[1]) * m) : 0; // chain stages
-    P.off_stage2 = z >= 2 ? take(sizeof(double) * (P.pst ? srows0 : ch + 2 * hal[2]) * m) : 0;
-    if (off + stat <= static_cast<size_t>(optin))
-    {
-      dyn = off;
-      CH = ch;
-      P.nb = nb;
-      break;
-    }
-  }
-  if (CH == 0)
-    return false;
-#ifdef MGPU_HOST_TRACE
-  {
-    char msg[128];
-    std::snprintf(msg, sizeof msg, "cg_stream plan: %lld-row chunks, %d-deep ring, %zu B per slot",
-                  static_cast<long long>(CH), P.nb, P.buf_bytes);
-    host_mark(msg);
-  }
-#endif
-  // ---- vectors (padded) and the per-point block plan
-  const int64_t ldv = (n + 2 * kPadR) * m;
-  const size_t vb = sizeof(double) * static_cast<size_t>(l) * ldv;
-  DBuf b(vb, s), xt(vb, s), r(vb, s), d0(vb, s), d1(vb, s), w(vb, s), sol(vb, s);
-  for (DBuf *q : {&b, &xt, &r, &d0, &d1, &w, &sol})
-    MG_CUDA(cudaMemsetAsync(q->ptr, 0, vb, s));
-  stream_init<<<blocks_for(static_cast<int64_t>(l) * n * m), kThreads, 0, s>>>(
-      l, m, n, ldv, B_dev, ldb, b.as<double>(), r.as<double>(), d0.as<double>(), xt.as<double>());
-  check_launch(ctx, "stream_init");
-  const int G = ctx->num_sms;
-  // Serial schedule (opt-in, MGPU_STREAM_SERIAL=1): the points run one after another on every
-  // block, so phase B re-reads phase A's outputs (r, d_new, w: 24 n m bytes) from L2 and w never
-  // reaches HBM (its lines are discarded once read).  Measured on configs[3] (n = 1e6, m = 4,
-  // 16 points): DRAM traffic 6.15 -> 4.70 GB per batched iteration, but 1072 -> 1415 us per
-  // iteration -- two grid barriers, two block reductions, two flushes and two pipeline fills
-  // per point (~10 us per pass, 32 passes) cost more than the bytes saved.  Off by default.
-  const bool serial = ctx->opt[MGPU_OPT_STREAM_SERIAL] != 0 && l <= kTabSlots;
-  std::vector<Seg> hseg(static_cast<size_t>(G) * kMaxSeg, Seg{-1, 0, 0, 0});
-  std::vector<int2> hpb(static_cast<size_t>(l));
-  if (serial)
-  {
-    // every block: the same row slab of every point (32-row groups, no row-less block inside
-    // the reduction range)
-    const int64_t groups = (n + 31) / 32;
-    const int nb = static_cast<int>(std::min<int64_t>(G, groups));
-    for (int bk = 0; bk < G; ++bk)
-    {
-      const int64_t g0 = bk < nb ? groups * bk / nb : 0, g1 = bk < nb ? groups * (bk + 1) / nb : 0;
-      hseg[static_cast<size_t>(bk) * kMaxSeg] =
-          Seg{0, static_cast<int>(g0 * 32), static_cast<int>(std::min<int64_t>(n, g1 * 32)), 0};
-    }
-    for (int p = 0; p < l; ++p)
-      hpb[p] = make_int2(0, nb);
-  }
-  else if (l <= G)
-  {
-    for (int p = 0; p < l; ++p)
-    {
-      const int b0 = static_cast<int>(static_cast<int64_t>(p) * G / l);
-      const int b1 = static_cast<int>(static_cast<int64_t>(p + 1) * G / l);
-      const int64_t groups = (n + 31) / 32;
-      // a point spans at most one block per 32-row group: every block in [b0, b0 + nb) owns
-      // rows, so every partial-sum slot the reduction reads is written (a block without rows
-      // would never flush its slot)
-      const int nb = static_cast<int>(std::min<int64_t>(b1 - b0, groups));
-      for (int k = 0; k < nb; ++k)
-      {
-        const int64_t g0 = groups * k / nb, g1 = groups * (k + 1) / nb;
-        hseg[static_cast<size_t>(b0 + k) * kMaxSeg] =
-            Seg{p, static_cast<int>(g0 * 32), static_cast<int>(std::min<int64_t>(n, g1 * 32)), 0};
-      }
-      hpb[p] = make_int2(b0, b0 + nb);
-    }
-  }
-  else
-  {
-    for (int bk = 0; bk < G; ++bk)
-    {
-      const int p0 = static_cast<int>(static_cast<int64_t>(bk) * l / G);
-      const int p1 = static_cast<int>(static_cast<int64_t>(bk + 1) * l / G);
-      for (int p = p0; p < p1; ++p)
-      {
-        hseg[static_cast<size_t>(bk) * kMaxSeg + (p - p0)] = Seg{p, 0, static_cast<int>(n), 0};
-        hpb[p] = make_int2(bk, bk + 1);
-      }
-    }
-  }
-  DBuf segs(sizeof(Seg) * hseg.size(), s), pblk(sizeof(int2) * hpb.size(), s);
-  DBuf dA(sizeof(PEll) * hA.size(), s), dF(sizeof(PEll) * hF.size(), s);
-  // structure-equality flags against point 0 (no host round trip: the kernel reads them)
-  DBuf eqA(sizeof(int) * static_cast<size_t>(l), s), eqF(sizeof(int) * static_cast<size_t>(l) * (z > 0 ? z : 1), s);
-  {
-    std::vector<int> ones(static_cast<size_t>(l) * (z > 0 ? z : 1), 1);
-    MG_CUDA(cudaMemcpyAsync(eqA.ptr, ones.data(), sizeof(int) * l, cudaMemcpyHostToDevice, s));
-    MG_CUDA(cudaMemcpyAsync(eqF.ptr, ones.data(), sizeof(int) * ones.size(), cudaMemcpyHostToDevice, s));
-    auto compare = [&](const mgpu_csr *X, const mgpu_csr *X0, int *flag) {
-      if (X == X0 || (X->row_ptr == X0->row_ptr && X->col_idx == X0->col_idx))
-        return; // stays 1
-      if (X->nnz != X0->nnz)
-      {
-        MG_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
-        return;
-      }
-      pattern_eq_kernel<<<std::max(1, std::min(ctx->num_sms * 4, static_cast<int>((n + 255) / 256))), 256, 0, s>>>(
-          n, X->nnz, X0->row_ptr, X0->col_idx, X->row_ptr, X->col_idx, flag);
-      check_launch(ctx, "pattern_eq_kernel");
-    };
-    for (int p = 1; p < l; ++p)
-    {
-      compare(A[p], A[0], eqA.as<int>() + p);
-      for (int f = 0; f < z; ++f)
-        compare(chains[static_cast<size_t>(p) * z + f], chains[f], eqF.as<int>() + static_cast<size_t>(p) * z + f);
-    }
-  }
-  DBuf partial(sizeof(double) * static_cast<size_t>(l) * 2 * kMaxM * G, s);
-  MG_CUDA(cudaMemcpyAsync(segs.ptr, hseg.data(), sizeof(Seg) * hseg.size(), cudaMemcpyHostToDevice, s));
-  MG_CUDA(cudaMemcpyAsync(pblk.ptr, hpb.data(), sizeof(int2) * hpb.size(), cudaMemcpyHostToDevice, s));
-  MG_CUDA(cudaMemcpyAsync(dA.ptr, hA.data(), sizeof(PEll) * hA.size(), cudaMemcpyHostToDevice, s));
-  MG_CUDA(cudaMemcpyAsync(dF.ptr, hF.data(), sizeof(PEll) * hF.size(), cudaMemcpyHostToDevice, s));
-  P.l = l;
-  P.m = m;
-  P.z = z;
-  P.rpt = 1;
-  P.serial = serial ? 1 : 0;
-  P.ch = static_cast<int>(CH);
-  {
-    // phase B: r, w (+ x~, d unfolded) -> the tallest chunk (multiple of 64 rows, <= 8192) that fits one slot
-    const int nvec = fold ? 2 : 4;
-    int64_t chb = static_cast<int64_t>(P.buf_bytes / (nvec * sizeof(double) * static_cast<size_t>(m))) & ~63ll;
-    chb = std::min<int64_t>(std::max<int64_t>(chb, CH), 8192);
-    if (ctx->opt[MGPU_OPT_STREAM_SAME_CHB]) // diagnostics: phase B on the phase A chunk height
-      chb = CH;
-    P.ch_b = static_cast<int>(chb);
-    const size_t vb = static_cast<size_t>(chb) * m * sizeof(double); // multiple of 512 B
-    P.b_r = 0;
-    P.b_w = vb;
-    P.b_x = 2 * vb;
-    P.b_d = 3 * vb;
-    P.fold = fold ? 1 : 0;
-  }
-  P.n = n;
-  P.ldv = ldv;
-  for (int q = 0; q <= z; ++q)
-    P.halo[q] = hal[q];
-  P.hmax = H0;
-  P.A = dA.as<PEll>();
-  P.F = dF.as<PEll>();
-  P.eqA = eqA.as<int>();
-  P.eqF = eqF.as<int>();
-  P.rtol = rtol;
-  P.maxit = maxit;
-  P.b = b.as<double>();
-  P.xt = xt.as<double>();
-  P.r = r.as<double>();
-  P.dbuf0 = d0.as<double>();
-  P.dbuf1 = d1.as<double>();
-  P.w = w.as<double>();
-  P.sol = sol.as<double>();
-  P.partial = partial.as<double>();
-  P.seg = segs.as<Seg>();
-  P.pblk = pblk.as<int2>();
-  P.X = X_dev;
-  P.REC = REC_dev;
-  P.TR = TR_dev;
-  P.iters = d_it;
-  P.conv = d_conv;
-  P.status = d_st;
-  P.bd_iter = d_bd;
-  P.hist = d_hist;
-  P.hist_cap = hist_cap;
-  P.loop_iters = d_loop;
-  P.prof = ctx->prof_dev;
-  auto launch = [&](auto kern) {
-    MG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
-    int per_sm = 0;
-    MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TB + 32, dyn));
-    if (per_sm < 1)
-      return false;
-    void *args[] = {&P};
-    MG_CUDA(cudaEventRecord(ctx->ev0, s));
-    MG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void *>(kern), dim3(static_cast<unsigned>(G)), dim3(TB + 32), args,
-                                        dyn, s));
-    check_launch(ctx, "cg_stream");
-    MG_CUDA(cudaEventRecord(ctx->ev1, s));
-    return true;
-  };
-  bool ok;
-  const bool pr = P.prof != nullptr;
-  if (m == 1)
-    ok = pr ? launch(cg_stream<TB, 1, true>) : launch(cg_stream<TB, 1>);
-  else if (m == 2) // (phase profile instantiated for m = 1 and m <= 4 only)
-    ok = launch(cg_stream<TB, 2>);
-  else if (m <= 4)
-    ok = pr ? launch(cg_stream<TB, 4, true>) : launch(cg_stream<TB, 4>);
-  else
-    ok = launch(cg_stream<TB, 8>);
-  if (ok)
-    MG_CUDA(cudaStreamSynchronize(s)); // keep the padded buffers alive until the kernel is done
-  return ok;
-}
 
 // One sub-batch: l points (all columns m <= kMaxM).
 void cg_batch(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const mgpu_csr *const *chains, int64_t n,
