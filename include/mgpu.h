@@ -97,8 +97,8 @@ int mgpu_last_cg_path(const mgpu_ctx *ctx);
  * Defaults are the measured best choices; the others exist for the A/B experiments in DESIGN.md. */
 typedef enum mgpu_option
 {
-  MGPU_OPT_STREAM_FOLD = 0,     /* cg_stream: x~ update deferred into the next phase A (default 1) */
-  MGPU_OPT_STREAM_SERIAL = 1,   /* cg_stream: point-serial schedule with the L2 hand-off (default 0) */
+  MGPU_OPT_RETIRED0 = 0,        /* (was the x~ update placement; the deferred update is the only schedule now) */
+  MGPU_OPT_RETIRED1 = 1,        /* (was the point-serial schedule; measured slower, removed -- DESIGN.md 5) */
   MGPU_OPT_STREAM_CHUNK = 2,    /* cg_stream: forced chunk rows (0 = planner, default) */
   MGPU_OPT_STREAM_RING = 3,     /* cg_stream: forced ring depth with MGPU_OPT_STREAM_CHUNK (2..4) */
   MGPU_OPT_STREAM_SAME_CHB = 4, /* cg_stream: phase B on phase A's chunk height (default 0) */
@@ -107,7 +107,9 @@ typedef enum mgpu_option
   MGPU_OPT_PROFILE_PHASES = 7,  /* clock64 per-phase totals of the CG kernels (default 0; read with mgpu_phase_profile) */
   MGPU_OPT_QR_UNBLOCKED = 8,    /* thin_qr: column-at-a-time schedule instead of compact WY (default 0) */
   MGPU_OPT_LS_GROUP = 9,        /* LS-SPAI: skip the lane-per-column kernels (default 0) */
-  MGPU_OPT_COUNT = 10,
+  MGPU_OPT_STREAM_TILES = 10,   /* cg_stream: row-slab x point tiles, the points of a slab processed at the same time (default 1: where a tile holds >= 16 chunks; 2: always; 0: one contiguous row range per block) */
+  MGPU_OPT_STREAM_EXP = 11,     /* experiments (default 0) */
+  MGPU_OPT_COUNT = 12,
 } mgpu_option;
 int mgpu_ctx_set_option(mgpu_ctx *ctx, int option, int64_t value);
 int mgpu_ctx_get_option(const mgpu_ctx *ctx, int option, int64_t *value);

@@ -36,7 +36,7 @@ namespace
 constexpr int kPadR = 64;
 constexpr int kEllMax = 64; // widest ELL row the streaming kernel takes (int8 offsets: bandwidth < kPadR)
 constexpr int kStreamNB = 4; // bulk-copy ring depth (maximum; StreamParams::nb is the one in use)
-constexpr int kTabSlots = 16; // operator-descriptor slots: segments per block, or points (serial schedule)
+constexpr int kTabSlots = 16; // operator-descriptor slots: segments per block
 static_assert(kTabSlots >= kMaxSeg, "descriptor table must cover every segment");
 
 __device__ __forceinline__ uint32_t sm_addr(const void *p)
@@ -124,15 +124,14 @@ struct StreamParams
 {
   int l, m, z, rpt, ch; // ch: rows per chunk (phase A and the check pass)
   int ch_b;             // rows per chunk in phase B (fewer vectors per row: taller chunks fill the same slot)
-  int fold;             // 1: x~ += alpha d deferred to the next phase A (m = 1), 0: applied in phase B
   int nb;               // ring depth (2..kStreamNB)
-  int serial;           // 1: points one after another (all blocks on one point's rows; L2 hand-off A -> B)
+  int exp;              // MGPU_OPT_STREAM_EXP bits (experiments; 0 in production)
   // stage-buffer layout: 0 = row-interleaved [row][c]; > 0 (m == 4) = two planes of double2,
   // (c0, c1) and (c2, c3) per row, plane stride `pst` doubles.  A thread's row loads are then two
   // 16-byte loads from consecutive 16-byte slots across the warp (no bank conflicts; the
   // interleaved 32-byte rows cost two wavefronts per 16-byte load).
   int pst;
-  int64_t n, ldv; // ldv = (n + 2 PADR) * m: doubles per point block
+  int64_t n, ldv; // ldv = (n + 2 PADR) * m rounded up to even: doubles per point block (16-byte aligned)
   int halo[kMaxZ + 1];
   int hmax;
   const PEll *A, *F; // [l], [l * z] newest first
@@ -158,7 +157,16 @@ struct StreamParams
   // phase B layout alias) + stage buffers
   size_t buf_bytes, off_stage0, off_stage1, off_stage2;
   size_t a_vr, a_vd, a_vx, a_fv[kMaxZ], a_fo[kMaxZ], a_av, a_ao; // phase A offsets inside a buffer
-  size_t b_r, b_w, b_x, b_d;                                      // phase B offsets inside a buffer
+  size_t b_r, b_w;                                                // phase B offsets inside a buffer
+};
+
+// Per-stage entries of StreamParams, copied to shared memory once: indexing the kernel
+// parameters with a run-time stage number makes ptxas keep a local-memory copy of the whole
+// parameter block (a 700-byte stack frame; configs[3] 1119 -> 1779 us per iteration when it happened).
+struct StageTab
+{
+  int halo[kMaxZ + 1];
+  uint32_t a_fv[kMaxZ], a_fo[kMaxZ];
 };
 
 __device__ __forceinline__ const double *vrow(const StreamParams &P, const double *base, int p, int64_t i)
@@ -166,33 +174,20 @@ __device__ __forceinline__ const double *vrow(const StreamParams &P, const doubl
   return base + static_cast<int64_t>(p) * P.ldv + (kPadR + i) * P.m;
 }
 
-// chunk iterator over the block's segments
-struct ChunkIt
+// The block's chunks in order: its segments (one point each, masked points skipped), then
+// CH-row chunks of the segment.  fn(segment index, point, c0, c1); the producer and the
+// consumers walk the same sequence.  Rows are 32-bit (Seg), the loop carries no 64-bit state.
+template <int TB, class F>
+__device__ __forceinline__ void for_chunks(const BandShared<TB> &sh, int CH, F &&fn)
 {
-  int seg;
-  int64_t c0;
-};
-
-template <int TB>
-__device__ __forceinline__ bool chunk_next(const BandShared<TB> &sh, int64_t CH, ChunkIt &it, int &p, int64_t &c0,
-                                           int64_t &c1)
-{
-  while (it.seg < sh.nseg)
+  for (int sg = 0; sg < sh.nseg; ++sg)
   {
-    const Seg g = sh.seg[it.seg];
-    if (!sh.pmask[g.p] || it.c0 >= g.re)
-    {
-      ++it.seg;
-      it.c0 = it.seg < sh.nseg ? sh.seg[it.seg].rs : 0;
+    const Seg g = sh.seg[sg];
+    if (!sh.pmask[g.p])
       continue;
-    }
-    p = g.p;
-    c0 = it.c0;
-    c1 = min(static_cast<int64_t>(g.re), c0 + CH);
-    it.c0 = c1;
-    return true;
+    for (int c0 = g.rs; c0 < g.re; c0 += CH)
+      fn(sg, g.p, c0, min(g.re, c0 + CH));
   }
-  return false;
 }
 
 __device__ __forceinline__ int64_t even_up(int64_t x) { return (x + 1) & ~static_cast<int64_t>(1); }
@@ -200,48 +195,28 @@ __device__ __forceinline__ int64_t even_up(int64_t x) { return (x + 1) & ~static
 // Producer: issue the bulk copies of one chunk's inputs into buffer `buf`.
 // kind 0: phase A step (r, d_old over the halo; x~ on own rows for the deferred
 // update), 1: phase A check (x~ and d_old over the halo), 2: phase B (r, w).
-//
-// Serial schedule (P.serial): every read that is the last one before the data's next use
-// two or more passes later is tagged L2 evict_first (operators, d_old, x~, everything phase B
-// reads), so the lines phase B re-reads (r, d_new, w of the same point, written or read by
-// phase A just before) are the ones that stay in L2.
 template <int TB>
-__device__ void stream_issue(const StreamParams &P, const PEll *tab, unsigned char *buf, uint64_t *bar, int kind, int p,
-                             int64_t c0, int64_t c1, const double *dold, const double *dnew)
+__device__ __forceinline__ void stream_issue(const StreamParams &P, const StageTab &stg, const PEll *tab, unsigned char *buf,
+                             uint64_t *bar, int kind, int p, int64_t c0, int64_t c1, const double *dold)
 {
   const int m = P.m;
-  uint32_t bytes = 0;
-  const uint64_t pol = policy_evict_first();
-  auto cp = [&](void *dst, const void *src, uint32_t nbytes, bool last_use) {
-    if (P.serial && last_use)
-      bulk_g2s_hint(dst, src, nbytes, bar, pol);
-    else
-      bulk_g2s(dst, src, nbytes, bar);
-  };
   if (kind == 2)
   {
     const int64_t rows = even_up(c1 - c0);
     const uint32_t vb = static_cast<uint32_t>(rows * m * 8);
-    bytes = (P.fold ? 2 : 4) * vb;
-    mbar_expect_tx(bar, bytes);
-    cp(buf + P.b_r, vrow(P, P.r, p, c0), vb, true);
-    cp(buf + P.b_w, vrow(P, P.w, p, c0), vb, true);
-    if (!P.fold)
-    {
-      cp(buf + P.b_x, vrow(P, P.xt, p, c0), vb, true);
-      cp(buf + P.b_d, vrow(P, dnew, p, c0), vb, true);
-    }
+    mbar_expect_tx(bar, 2 * vb);
+    bulk_g2s(buf + P.b_r, vrow(P, P.r, p, c0), vb, bar);
+    bulk_g2s(buf + P.b_w, vrow(P, P.w, p, c0), vb, bar);
     return;
   }
   const int H0 = P.hmax;
   const int64_t vrows = even_up(c1 - c0 + 2 * H0);
   const uint32_t vb = static_cast<uint32_t>(vrows * m * 8);
   const uint32_t xb = static_cast<uint32_t>(even_up(c1 - c0) * m * 8);
-  const bool need_d = kind == 0 || P.fold; // the check pass reads d_old only for the deferred update
-  uint32_t total = (need_d ? 2 * vb : vb) + (kind == 0 && P.fold ? xb : 0u);
+  uint32_t total = 2 * vb + (kind == 0 ? xb : 0u);
   for (int st = 0; st < P.z; ++st)
   {
-    const int hd = P.halo[st + 1];
+    const int hd = stg.halo[st + 1];
     const PEll F = tab[1 + st];
     const int64_t rows = even_up(c1 - c0 + 2 * hd);
     total += static_cast<uint32_t>(rows * F.E * 8 + rows * F.ow * 8);
@@ -252,23 +227,22 @@ __device__ void stream_issue(const StreamParams &P, const PEll *tab, unsigned ch
     total += static_cast<uint32_t>(rows * A.E * 8 + rows * A.ow * 8);
   }
   mbar_expect_tx(bar, total);
-  cp(buf + P.a_vr, vrow(P, kind == 0 ? P.r : P.xt, p, c0 - H0), vb, kind != 0); // phase B re-reads r
-  if (need_d)
-    cp(buf + P.a_vd, vrow(P, dold, p, c0 - H0), vb, true);
-  if (kind == 0 && P.fold)
-    cp(buf + P.a_vx, vrow(P, P.xt, p, c0), xb, true);
+  bulk_g2s(buf + P.a_vr, vrow(P, kind == 0 ? P.r : P.xt, p, c0 - H0), vb, bar);
+  bulk_g2s(buf + P.a_vd, vrow(P, dold, p, c0 - H0), vb, bar); // the check pass reads d_old for the deferred update
+  if (kind == 0)
+    bulk_g2s(buf + P.a_vx, vrow(P, P.xt, p, c0), xb, bar);
   for (int st = 0; st < P.z; ++st)
   {
-    const int hd = P.halo[st + 1];
+    const int hd = stg.halo[st + 1];
     const PEll F = tab[1 + st];
     const int64_t rows = even_up(c1 - c0 + 2 * hd);
-    cp(buf + P.a_fv[st], F.v + (c0 - hd) * F.E, static_cast<uint32_t>(rows * F.E * 8), true);
-    cp(buf + P.a_fo[st], F.o + (c0 - hd) * F.ow, static_cast<uint32_t>(rows * F.ow * 8), true);
+    bulk_g2s(buf + stg.a_fv[st], F.v + (c0 - hd) * F.E, static_cast<uint32_t>(rows * F.E * 8), bar);
+    bulk_g2s(buf + stg.a_fo[st], F.o + (c0 - hd) * F.ow, static_cast<uint32_t>(rows * F.ow * 8), bar);
   }
   const PEll A = tab[0];
   const int64_t rows = even_up(c1 - c0);
-  cp(buf + P.a_av, A.v + c0 * A.E, static_cast<uint32_t>(rows * A.E * 8), true);
-  cp(buf + P.a_ao, A.o + c0 * A.ow, static_cast<uint32_t>(rows * A.ow * 8), true);
+  bulk_g2s(buf + P.a_av, A.v + c0 * A.E, static_cast<uint32_t>(rows * A.E * 8), bar);
+  bulk_g2s(buf + P.a_ao, A.o + c0 * A.ow, static_cast<uint32_t>(rows * A.ow * 8), bar);
 }
 
 __device__ __forceinline__ int off8s(unsigned long long w, int t)
@@ -436,10 +410,29 @@ __device__ __forceinline__ void ell_row_fixed(const double *vals, const unsigned
     a2[c] = 0.0;
   const unsigned long long w0 = offs[0];
   const unsigned long long w1 = EC > 8 ? offs[1] : 0ull;
+  // even widths: rows are 16-byte aligned, values read as double2 (a quarter warp's 16-byte
+  // loads at the 8 EC-byte row stride hit distinct banks; the 8-byte loads conflicted two-way)
+  double av[EC];
+  if constexpr ((EC & 1) == 0)
+  {
+#pragma unroll
+    for (int h = 0; h < EC / 2; ++h)
+    {
+      const double2 t = reinterpret_cast<const double2 *>(vals)[h];
+      av[2 * h] = t.x;
+      av[2 * h + 1] = t.y;
+    }
+  }
+  else
+  {
+#pragma unroll
+    for (int e = 0; e < EC; ++e)
+      av[e] = vals[e];
+  }
 #pragma unroll
   for (int e = 0; e < EC; ++e)
   {
-    const double ae = vals[e];
+    const double ae = av[e];
     const int off = e < 8 ? off8s(w0, e) : off8s(w1, e - 8);
     double x[MT];
     if constexpr (PL && MT == 4)
@@ -596,15 +589,22 @@ struct RingProducer
 // bulk-copy bytes; empty barrier: consumers done), the TB consumer threads
 // compute.  Dot-product partials accumulate per consumer thread over all
 // chunks of a point (row order) and are reduced once per point.
+//
+// Element loops (stage 0, phase B) run on pairs of doubles when m == MT: pair u holds elements
+// 2u, 2u + 1 of the row-interleaved block, i.e. columns (2u) % m and (2u + 1) % m (the same
+// column twice for m = 1).  2 TB % m == 0 for every MT, so a thread's two columns are fixed
+// and their system scalars are read once per chunk.
+// (forceinline: as a real call the pass takes the kernel parameters by address, which costs a
+// local-memory copy of the parameter block and turns `kind` into run-time branches)
 template <int TB, int MT, int NB, class PC, bool WIDE>
-__device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, const PEll *tab, unsigned char *smem,
+__device__ __forceinline__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, const StageTab &stg, const PEll *tab,
+                            unsigned char *smem,
                             uint64_t *full, uint64_t *empty, uint32_t &phase_bits, RingProducer &rp, int kind,
                             const double *dold, double *dnew, PC &pc)
 {
-  const int64_t CH = kind == 2 ? P.ch_b : P.ch;
+  const int CH = kind == 2 ? P.ch_b : P.ch;
   const int m = P.m;
   const int nv = kind == 0 ? 2 * m : m;
-  ChunkIt cons{0, sh.nseg > 0 ? static_cast<int64_t>(sh.seg[0].rs) : 0};
   __syncthreads();
   if (threadIdx.x >= TB)
   {
@@ -612,50 +612,55 @@ __device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, cons
     if (threadIdx.x == TB)
     {
       fence_async_global(); // generic stores of the previous phase -> async-proxy (bulk copy) reads
-      ChunkIt prod = cons;
-      int pp;
-      int64_t pc0, pc1;
-      int k = 0;
-      while (chunk_next(sh, CH, prod, pp, pc0, pc1))
-      {
-        const int b = k % P.nb;
+      int b = 0;
+      for_chunks(sh, CH, [&](int sg, int pp, int c0, int c1) {
         if ((rp.filled >> b) & 1u)
         {
           mbar_wait(&empty[b], (rp.epar >> b) & 1u);
           rp.epar ^= 1u << b;
         }
         rp.filled |= 1u << b;
-        stream_issue<TB>(P, tab + prod.seg * (kMaxZ + 1), smem + b * P.buf_bytes, &full[b], kind, pp, pc0, pc1, dold,
-                         dnew);
-        ++k;
-      }
+        stream_issue<TB>(P, stg, tab + sg * (kMaxZ + 1), smem + b * P.buf_bytes, &full[b], kind, pp, c0, c1, dold);
+        b = b + 1 == P.nb ? 0 : b + 1;
+      });
     }
     __syncthreads();
     return;
   }
   // ---- consumers
-  int cp;
-  int64_t cc0, cc1;
   pc.mark(0);
   double acc[2 * MT];
 #pragma unroll
   for (int q = 0; q < 2 * MT; ++q)
     acc[q] = 0.0;
-  int k = 0;
+  int bi = 0;
   int cur_p = -1;
-  // TB % m == 0 (every m <= 8 but 7): a consumer thread's elements e = tid + k TB all belong to
-  // column c = tid % m, so the element loops hoist the system's scalars, and phase B keeps its
-  // (r, r) partial in one register (the other columns' partials of this thread stay zero).
+  const bool full_m = m == MT;
+  // pairs: this thread's two columns (fixed, see above); scalar fallback (m < MT): TB % m == 0
+  // (every m <= 8 but 7) fixes the column of element e = tid + k TB
+  const int cA = (2 * static_cast<int>(threadIdx.x)) % m, cB = (2 * static_cast<int>(threadIdx.x) + 1) % m;
   const bool cfix = (TB % m) == 0;
   const int cth = threadIdx.x % m;
-  double accb = 0.0;
+  double accA = 0.0, accB = 0.0; // phase B: (r, r) partials of columns cA, cB (pairs) / accA of cth (scalar)
   auto flush = [&](int pnt) {
-    if (kind == 2 && cfix && !P.serial)
+    if (kind == 2 && (full_m || cfix))
     {
 #pragma unroll
       for (int q = 0; q < MT; ++q)
-        acc[q] = q == cth ? accb : 0.0;
-      accb = 0.0;
+      {
+        double v = 0.0;
+        if (full_m)
+        {
+          if (q == cA)
+            v = accA;
+          if (q == cB)
+            v = cB == cA ? __dadd_rn(accA, accB) : accB;
+        }
+        else if (q == cth)
+          v = accA;
+        acc[q] = v;
+      }
+      accA = accB = 0.0;
     }
     double pv[2 * MT];
 #pragma unroll
@@ -701,9 +706,7 @@ __device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, cons
     for (int q = 0; q < 2 * MT; ++q)
       acc[q] = 0.0;
   };
-  while (chunk_next(sh, CH, cons, cp, cc0, cc1))
-  {
-    const int bi = k % P.nb;
+  for_chunks(sh, CH, [&](int sg, int cp, int cc0, int cc1) {
     pc.mark(1);
     if (cp != cur_p)
     {
@@ -717,40 +720,44 @@ __device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, cons
     pc.mark(3);
     unsigned char *buf = smem + bi * P.buf_bytes;
     const int64_t base_i = cc0;
-    const int R = static_cast<int>(cc1 - cc0);
+    const int R = cc1 - cc0;
     const int sb = cp * m; // first system of the point
     if (kind == 2)
     {
-      // r -= alpha w, partial (r, r): one element (row, column) per thread.  x~ += alpha d
-      // (krylov.cpp:113) is deferred to the next phase A, which streams d anyway.
+      // r -= alpha w, partial (r, r).  x~ += alpha d (krylov.cpp:113) is deferred to the next
+      // phase A, which streams d anyway.
       const double *rs = reinterpret_cast<const double *>(buf + P.b_r);
       const double *ws = reinterpret_cast<const double *>(buf + P.b_w);
-      const double *xs = reinterpret_cast<const double *>(buf + P.b_x);
-      const double *ds = reinterpret_cast<const double *>(buf + P.b_d);
       double *rg = const_cast<double *>(vrow(P, P.r, cp, base_i));
-      double *xg = const_cast<double *>(vrow(P, P.xt, cp, base_i));
       const int ne = R * m;
-      if (P.serial)
+      if (full_m)
       {
-        // w is dead once in shared memory: drop its L2 lines (no write-back to HBM), only
-        // lines that lie wholly inside this chunk's rows
-        const uintptr_t wa = reinterpret_cast<uintptr_t>(vrow(P, P.w, cp, base_i));
-        const uintptr_t l0 = (wa + 127) & ~static_cast<uintptr_t>(127);
-        const uintptr_t l1 = (wa + static_cast<uintptr_t>(ne) * 8) & ~static_cast<uintptr_t>(127);
-        for (uintptr_t a = l0 + static_cast<uintptr_t>(threadIdx.x) * 128; a < l1; a += static_cast<uintptr_t>(TB) * 128)
-          discard_l2(reinterpret_cast<const void *>(a));
-        const uint64_t pol = policy_evict_first();
-        for (int e = threadIdx.x; e < ne; e += TB)
+        const bool runA = sh.state[sb + cA] == kRun, runB = sh.state[sb + cB] == kRun;
+        const double alA = sh.alpha[sb + cA], alB = sh.alpha[sb + cB];
+        if (runA || runB)
         {
-          const int c = col_of<MT>(e, m);
-          if (sh.state[sb + c] != kRun)
-            continue;
-          const double al = sh.alpha[sb + c];
-          if (!P.fold)
-            stg_hint(xg + e, __dadd_rn(xs[e], __dmul_rn(al, ds[e])), pol);
-          const double rn = __dadd_rn(rs[e], __dmul_rn(-al, ws[e]));
-          stg_hint(rg + e, rn, pol);
-          acc_add<MT>(acc, c, __dmul_rn(rn, rn));
+          const int nu = (ne + 1) >> 1;
+          for (int u = threadIdx.x; u < nu; u += TB)
+          {
+            const double2 r2 = reinterpret_cast<const double2 *>(rs)[u];
+            const double2 w2 = reinterpret_cast<const double2 *>(ws)[u];
+            const double ra = __dadd_rn(r2.x, __dmul_rn(-alA, w2.x));
+            const double rb = __dadd_rn(r2.y, __dmul_rn(-alB, w2.y));
+            const bool hasB = 2 * u + 1 < ne; // (m = 1, odd row count: the last pair is half empty)
+            if (runA && runB && hasB)
+              __stcg(reinterpret_cast<double2 *>(rg) + u, make_double2(ra, rb));
+            else
+            {
+              if (runA)
+                __stcg(rg + 2 * u, ra);
+              if (runB && hasB)
+                __stcg(rg + 2 * u + 1, rb);
+            }
+            if (runA)
+              accA = __dadd_rn(accA, __dmul_rn(ra, ra));
+            if (runB && hasB)
+              accB = __dadd_rn(accB, __dmul_rn(rb, rb));
+          }
         }
       }
       else if (cfix)
@@ -760,27 +767,23 @@ __device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, cons
           const double al = sh.alpha[sb + cth];
           for (int e = threadIdx.x; e < ne; e += TB)
           {
-            if (!P.fold)
-              __stcg(xg + e, __dadd_rn(xs[e], __dmul_rn(al, ds[e])));
             const double rn = __dadd_rn(rs[e], __dmul_rn(-al, ws[e]));
             __stcg(rg + e, rn);
-            accb = __dadd_rn(accb, __dmul_rn(rn, rn));
+            accA = __dadd_rn(accA, __dmul_rn(rn, rn));
           }
         }
       }
       else
-      for (int e = threadIdx.x; e < ne; e += TB)
-      {
-        const int c = col_of<MT>(e, m);
-        if (sh.state[sb + c] != kRun)
-          continue;
-        const double al = sh.alpha[sb + c];
-        if (!P.fold)
-          __stcg(xg + e, __dadd_rn(xs[e], __dmul_rn(al, ds[e])));
-        const double rn = __dadd_rn(rs[e], __dmul_rn(-al, ws[e]));
-        __stcg(rg + e, rn);
-        acc_add<MT>(acc, c, __dmul_rn(rn, rn));
-      }
+        for (int e = threadIdx.x; e < ne; e += TB)
+        {
+          const int c = col_of<MT>(e, m);
+          if (sh.state[sb + c] != kRun)
+            continue;
+          const double al = sh.alpha[sb + c];
+          const double rn = __dadd_rn(rs[e], __dmul_rn(-al, ws[e]));
+          __stcg(rg + e, rn);
+          acc_add<MT>(acc, c, __dmul_rn(rn, rn));
+        }
     }
     else
     {
@@ -795,10 +798,71 @@ __device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, cons
       // written back: neighbours read the same x~ rows as halo during this pass).
       const double *vx = reinterpret_cast<const double *>(buf + P.a_vx);
       const int ne0 = (R + 2 * H0) * m;
-      const int lo = H0 * m, hi = (H0 + R) * m;
+      const int lo = H0 * m, hi = (H0 + R) * m; // lo is even (even halos)
       double *dg = kind == 0 ? const_cast<double *>(vrow(P, dnew, cp, base_i - H0)) : nullptr;
       double *xg = kind == 0 ? const_cast<double *>(vrow(P, P.xt, cp, base_i - H0)) : nullptr;
-      if (cfix)
+      if (full_m)
+      {
+        const int sysA = sb + cA, sysB = sb + cB;
+        const bool frA = sh.fresh[sysA] != 0, frB = sh.fresh[sysB] != 0;
+        const bool pdA = sh.pend[sysA] != 0, pdB = sh.pend[sysB] != 0;
+        const bool upA = pdA && sh.state[sysA] == kRun, upB = pdB && sh.state[sysB] == kRun;
+        const double beA = sh.beta[sysA], beB = sh.beta[sysB], alA = sh.alpha[sysA], alB = sh.alpha[sysB];
+        const int nu = (ne0 + 1) >> 1;
+        // pair u -> stage slot: planar (m == 4): plane (u & 1), row u >> 1; else element pair u
+        auto st0 = [&](int u, double a, double b) {
+          if (MT == 4 && P.pst > 0)
+            reinterpret_cast<double2 *>(s0 + ((u & 1) ? P.pst : 0))[u >> 1] = make_double2(a, b);
+          else
+            reinterpret_cast<double2 *>(s0)[u] = make_double2(a, b);
+        };
+        if (kind == 1)
+          for (int u = threadIdx.x; u < nu; u += TB)
+          {
+            const double2 r2 = reinterpret_cast<const double2 *>(vr)[u];
+            const double2 d2 = reinterpret_cast<const double2 *>(vd)[u];
+            st0(u, pdA ? __dadd_rn(r2.x, __dmul_rn(alA, d2.x)) : r2.x, pdB ? __dadd_rn(r2.y, __dmul_rn(alB, d2.y)) : r2.y);
+          }
+        else
+          for (int u = threadIdx.x; u < nu; u += TB)
+          {
+            const double2 r2 = reinterpret_cast<const double2 *>(vr)[u];
+            const double2 d2 = reinterpret_cast<const double2 *>(vd)[u];
+            const double va = frA ? r2.x : __dadd_rn(r2.x, __dmul_rn(beA, d2.x));
+            const double vb = frB ? r2.y : __dadd_rn(r2.y, __dmul_rn(beB, d2.y));
+            const int e = 2 * u;
+            const bool ownA = e >= lo && e < hi, ownB = e + 1 >= lo && e + 1 < hi;
+            if (ownA && ownB)
+            {
+              __stcg(reinterpret_cast<double2 *>(dg) + u, make_double2(va, vb));
+              if (upA || upB)
+              {
+                const double2 x2 = reinterpret_cast<const double2 *>(vx)[u - (lo >> 1)];
+                const double xa = __dadd_rn(x2.x, __dmul_rn(alA, d2.x)), xb = __dadd_rn(x2.y, __dmul_rn(alB, d2.y));
+                if (upA && upB)
+                  __stcg(reinterpret_cast<double2 *>(xg) + u, make_double2(xa, xb));
+                else if (upA)
+                  __stcg(xg + e, xa);
+                else
+                  __stcg(xg + e + 1, xb);
+              }
+            }
+            else if (ownA) // (m = 1, odd row count: the chunk's last row shares its pair with a halo row)
+            {
+              __stcg(dg + e, va);
+              if (upA)
+                __stcg(xg + e, __dadd_rn(vx[e - lo], __dmul_rn(alA, d2.x)));
+            }
+            else if (ownB)
+            {
+              __stcg(dg + e + 1, vb);
+              if (upB)
+                __stcg(xg + e + 1, __dadd_rn(vx[e + 1 - lo], __dmul_rn(alB, d2.y)));
+            }
+            st0(u, va, vb);
+          }
+      }
+      else if (cfix)
       {
         const int sys = sb + cth;
         const bool fr = sh.fresh[sys] != 0, pd = sh.pend[sys] != 0, run = sh.state[sys] == kRun;
@@ -820,35 +884,35 @@ __device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, cons
           }
       }
       else
-      for (int e = threadIdx.x; e < ne0; e += TB)
-      {
-        const int c = col_of<MT>(e, m);
-        const int sys = sb + c;
-        double v;
-        if (kind == 1)
-          v = sh.pend[sys] ? __dadd_rn(vr[e], __dmul_rn(sh.alpha[sys], vd[e])) : vr[e];
-        else
+        for (int e = threadIdx.x; e < ne0; e += TB)
         {
-          v = sh.fresh[sys] ? vr[e] : __dadd_rn(vr[e], __dmul_rn(sh.beta[sys], vd[e]));
-          if (e >= lo && e < hi)
+          const int c = col_of<MT>(e, m);
+          const int sys = sb + c;
+          double v;
+          if (kind == 1)
+            v = sh.pend[sys] ? __dadd_rn(vr[e], __dmul_rn(sh.alpha[sys], vd[e])) : vr[e];
+          else
           {
-            __stcg(dg + e, v);
-            if (sh.pend[sys] && sh.state[sys] == kRun)
-              __stcg(xg + e, __dadd_rn(vx[e - lo], __dmul_rn(sh.alpha[sys], vd[e])));
+            v = sh.fresh[sys] ? vr[e] : __dadd_rn(vr[e], __dmul_rn(sh.beta[sys], vd[e]));
+            if (e >= lo && e < hi)
+            {
+              __stcg(dg + e, v);
+              if (sh.pend[sys] && sh.state[sys] == kRun)
+                __stcg(xg + e, __dadd_rn(vx[e - lo], __dmul_rn(sh.alpha[sys], vd[e])));
+            }
           }
+          s0[stage_idx(e, m, P.pst)] = v;
         }
-        s0[stage_idx(e, m, P.pst)] = v;
-      }
       consumer_sync<TB>();
       pc.mark(4);
       const double *src = s0;
       int hs = H0;
       for (int st = 0; st < P.z; ++st)
       {
-        const int hd = P.halo[st + 1];
-        const PEll F = tab[cons.seg * (kMaxZ + 1) + 1 + st];
-        const double *fv = reinterpret_cast<const double *>(buf + P.a_fv[st]);
-        const unsigned long long *fo = reinterpret_cast<const unsigned long long *>(buf + P.a_fo[st]);
+        const int hd = stg.halo[st + 1];
+        const PEll F = tab[sg * (kMaxZ + 1) + 1 + st];
+        const double *fv = reinterpret_cast<const double *>(buf + stg.a_fv[st]);
+        const unsigned long long *fo = reinterpret_cast<const unsigned long long *>(buf + stg.a_fo[st]);
         double *dst = (st & 1) ? sB : sA;
         const int span = R + 2 * hd;
         for (int q = threadIdx.x; q < span; q += TB)
@@ -862,7 +926,7 @@ __device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, cons
         hs = hd;
       }
       pc.mark(5);
-      const PEll A = tab[cons.seg * (kMaxZ + 1)];
+      const PEll A = tab[sg * (kMaxZ + 1)];
       const double *av = reinterpret_cast<const double *>(buf + P.a_av);
       const unsigned long long *ao = reinterpret_cast<const unsigned long long *>(buf + P.a_ao);
       double *wg = const_cast<double *>(vrow(P, P.w, cp, base_i));
@@ -889,13 +953,25 @@ __device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, cons
           double dn[MT];
           ld_stage<MT>(s0, H0 + lr, dn, m, P.pst);
           stg_row<MT>(wg + lr * m, a2, m);
+          if (full_m)
+          {
 #pragma unroll
-          for (int c = 0; c < MT; ++c)
-            if (c < m)
+            for (int c = 0; c < MT; ++c)
             {
               acc[c] = __dadd_rn(acc[c], __dmul_rn(dn[c], a2[c]));
               acc[MT + c] = __dadd_rn(acc[MT + c], __dmul_rn(dn[c], dn[c]));
             }
+          }
+          else
+          {
+#pragma unroll
+            for (int c = 0; c < MT; ++c)
+              if (c < m)
+              {
+                acc[c] = __dadd_rn(acc[c], __dmul_rn(dn[c], a2[c]));
+                acc[MT + c] = __dadd_rn(acc[MT + c], __dmul_rn(dn[c], dn[c]));
+              }
+          }
         }
       }
     }
@@ -904,8 +980,8 @@ __device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, cons
     if (threadIdx.x == 0)
       mbar_arrive(&empty[bi]);
     pc.mark(8);
-    ++k;
-  }
+    bi = bi + 1 == P.nb ? 0 : bi + 1;
+  });
   if (cur_p >= 0)
     flush(cur_p);
   __syncthreads();
@@ -913,16 +989,16 @@ __device__ void stream_pass(const StreamParams &P, BandShared<TB + 32> &sh, cons
 }
 
 template <int TB, int MT, bool PR = false, bool WIDE = false>
-__global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
+__global__ void __launch_bounds__(TB + 32, 1) cg_stream(const __grid_constant__ StreamParams P)
 {
   constexpr int TBX = TB + 32; // TB consumer threads + one producer warp
   cgrp::grid_group grid = cgrp::this_grid();
   extern __shared__ __align__(128) unsigned char smem_s[];
   __shared__ BandShared<TBX> sh;
   __shared__ __align__(8) uint64_t bars[2 * kStreamNB]; // full[NB], empty[NB]
-  // operator descriptors per segment (serial schedule: per point): A, then stage factors
+  // operator descriptors per segment: A, then stage factors
   __shared__ PEll tab[kTabSlots * (kMaxZ + 1)];
-  __shared__ int64_t ser_rows[2]; // serial schedule: this block's row slab, the same for every point
+  __shared__ StageTab stg;
   const int m = P.m;
   const int S = P.l * m;
   uint32_t phase_bits = 0;
@@ -937,15 +1013,14 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
       ++q;
     }
     sh.nseg = q;
-    ser_rows[0] = q > 0 ? sh.seg[0].rs : 0;
-    ser_rows[1] = q > 0 ? sh.seg[0].re : 0;
-    const int ntab = P.serial ? P.l : q;
-    for (int g = 0; g < ntab; ++g)
+    for (int g = 0; g < q; ++g)
     {
-      const int p = P.serial ? g : sh.seg[g].p;
+      const int p = sh.seg[g].p;
       PEll a = P.A[p];
       if (P.eqA[p])
         a.o = P.A[0].o;
+      if (P.exp & 1) // experiment: every point streams point 0's operator values (wrong results; L2-sharing bound)
+        a.v = P.A[0].v;
       tab[g * (kMaxZ + 1)] = a;
       for (int st = 0; st < P.z; ++st)
       {
@@ -953,8 +1028,19 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
         PEll fe = P.F[p * P.z + f];
         if (P.eqF[p * P.z + f])
           fe.o = P.F[f].o;
+        if (P.exp & 2)
+          fe.v = P.F[f].v;
         tab[g * (kMaxZ + 1) + 1 + st] = fe;
       }
+    }
+#pragma unroll
+    for (int st = 0; st <= kMaxZ; ++st)
+      stg.halo[st] = P.halo[st];
+#pragma unroll
+    for (int st = 0; st < kMaxZ; ++st)
+    {
+      stg.a_fv[st] = static_cast<uint32_t>(P.a_fv[st]);
+      stg.a_fo[st] = static_cast<uint32_t>(P.a_fo[st]);
     }
     for (int b = 0; b < 2 * kStreamNB; ++b)
       mbar_init(&bars[b], 1);
@@ -963,35 +1049,8 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
   for (int p = threadIdx.x; p < P.l; p += TBX)
     sh.pmask[p] = 1;
   __syncthreads();
-  // rows of every masked point this block owns (serial schedule: the block's slab of each point)
-  auto for_rows = [&](auto &&fn) {
-    if (P.serial)
-    {
-      for (int p = 0; p < P.l; ++p)
-        if (sh.pmask[p])
-          fn(p, ser_rows[0], ser_rows[1]);
-    }
-    else
-      for_segments(P, sh, fn);
-  };
-  // serial schedule: make point p the block's only segment (and the only masked point)
-  auto pick_point = [&](int p) {
-    __syncthreads();
-    for (int q = threadIdx.x; q < P.l; q += TBX)
-      sh.pmask[q] = q == p;
-    if (threadIdx.x == 0)
-    {
-      sh.seg[0] = Seg{p, static_cast<int>(ser_rows[0]), static_cast<int>(ser_rows[1]), 0};
-      sh.nseg = 1;
-    }
-    __syncthreads();
-  };
-  auto point_live = [&](int p) {
-    bool live = false;
-    for (int c = 0; c < m; ++c)
-      live |= sh.state[p * m + c] == kRun;
-    return live;
-  };
+  // rows of every masked point this block owns
+  auto for_rows = [&](auto &&fn) { for_segments(P, sh, fn); };
   // ---- phase 0: ||b||^2 (one pass, plain loads)
   for_rows([&](int p, int64_t rs, int64_t re) {
     begin_point(sh);
@@ -1051,28 +1110,10 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
     fence_async_global();
   };
 
-  // true-residual check pass over the masked points (serial schedule: one point at a time,
-  // no barrier in between -- the passes are independent); leaves pmask as it found it
+  // true-residual check pass over the masked points
   auto check_pass = [&](const double *dcur) {
-    if (!P.serial)
-    {
-      stream_pass<TB, MT, kStreamNB, PhaseClock<PR>, WIDE>(P, sh, tab, smem_s, bars, bars + kStreamNB, phase_bits, rp, 1, dcur, nullptr, pc);
-      return;
-    }
-    uint32_t msk = 0;
-    for (int p = 0; p < P.l; ++p)
-      msk |= sh.pmask[p] ? 1u << p : 0u;
-    for (int p = 0; p < P.l; ++p)
-      if ((msk >> p) & 1u)
-      {
-        pick_point(p);
-        stream_pass<TB, MT, kStreamNB, PhaseClock<PR>, WIDE>(P, sh, tab + p * (kMaxZ + 1), smem_s, bars, bars + kStreamNB, phase_bits, rp, 1,
-                                       dcur, nullptr, pc);
-      }
-    __syncthreads();
-    for (int p = threadIdx.x; p < P.l; p += TBX)
-      sh.pmask[p] = (msk >> p) & 1u;
-    __syncthreads();
+    stream_pass<TB, MT, kStreamNB, PhaseClock<PR>, WIDE>(P, sh, stg, tab, smem_s, bars, bars + kStreamNB, phase_bits, rp, 1, dcur,
+                                                         nullptr, pc);
   };
   // after phase A's reduction: alpha or breakdown for the running systems of masked points
   auto after_a = [&](int64_t itn) {
@@ -1109,7 +1150,7 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
       sh.beta[s] = rn / sh.rho[s];
       sh.rho[s] = rn;
       sh.fresh[s] = 0;
-      sh.pend[s] = P.fold; // x~ += alpha d owed to the next phase A / check pass
+      sh.pend[s] = 1; // x~ += alpha d owed to the next phase A / check pass
     }
     __syncthreads();
   };
@@ -1196,41 +1237,8 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
       break;
     double *d_old = cur ? P.dbuf1 : P.dbuf0;
     double *d_new = cur ? P.dbuf0 : P.dbuf1;
-    if (P.serial)
-    {
-      // one point at a time on every block: phase A writes d_new and w and phase B re-reads
-      // them (and r) straight from L2, two grid barriers per point
-      uint32_t live = 0;
-      for (int p = 0; p < P.l; ++p)
-        live |= sh.pmask[p] ? 1u << p : 0u;
-      for (int p = 0; p < P.l; ++p)
-      {
-        if (!((live >> p) & 1u))
-          continue;
-        pick_point(p);
-        const PEll *tp = tab + p * (kMaxZ + 1);
-        pc.mark(9);
-        stream_pass<TB, MT, kStreamNB, PhaseClock<PR>, WIDE>(P, sh, tp, smem_s, bars, bars + kStreamNB, phase_bits, rp, 0, d_old, d_new, pc);
-        fence_async_global();
-        grid.sync();
-        pc.mark(10);
-        reduce_blocks<TBX, StreamParams>(P, sh, 2 * m);
-        after_a(it);
-        pc.mark(11);
-        stream_pass<TB, MT, kStreamNB, PhaseClock<PR>, WIDE>(P, sh, tp, smem_s, bars, bars + kStreamNB, phase_bits, rp, 2, d_old, d_new, pc);
-        fence_async_global();
-        grid.sync();
-        pc.mark(10);
-        reduce_blocks<TBX, StreamParams>(P, sh, m);
-        after_b(it);
-        pc.mark(11);
-      }
-      ++it;
-      cur ^= 1;
-      continue;
-    }
     pc.mark(9);
-    stream_pass<TB, MT, kStreamNB, PhaseClock<PR>, WIDE>(P, sh, tab, smem_s, bars, bars + kStreamNB, phase_bits, rp, 0, d_old, d_new, pc);
+    stream_pass<TB, MT, kStreamNB, PhaseClock<PR>, WIDE>(P, sh, stg, tab, smem_s, bars, bars + kStreamNB, phase_bits, rp, 0, d_old, d_new, pc);
     fence_async_global();
     grid.sync();
     pc.mark(10);
@@ -1238,7 +1246,7 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(StreamParams P)
     pc.mark(11);
     after_a(it);
     pc.mark(9);
-    stream_pass<TB, MT, kStreamNB, PhaseClock<PR>, WIDE>(P, sh, tab, smem_s, bars, bars + kStreamNB, phase_bits, rp, 2, d_old, d_new, pc);
+    stream_pass<TB, MT, kStreamNB, PhaseClock<PR>, WIDE>(P, sh, stg, tab, smem_s, bars, bars + kStreamNB, phase_bits, rp, 2, d_old, d_new, pc);
     fence_async_global();
     grid.sync();
     pc.mark(10);
@@ -1431,12 +1439,9 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
     }
     OWA = std::max(OWA, hA[p].ow);
   }
-  // x~ update placement: deferred into phase A, which streams d_old anyway (one vector pass
-  // fewer).  Measured on B200 once the kernel dropped to 107 registers: configs[3] (m = 4, P = I)
-  // 1029 -> 1005 us/iter, configs[4] share 5025 -> 4891, configs[2] shape (m = 1, one factor)
-  // 36.9 -> 36.1; earlier (122 registers) phase A was latency-bound and m = 4 / chains lost.
-  // MGPU_OPT_STREAM_FOLD = 0 overrides (diagnostics).
-  const bool fold = ctx->opt[MGPU_OPT_STREAM_FOLD] != 0;
+  // The x~ update is deferred into the next phase A, which streams d_old anyway (one vector pass
+  // fewer; configs[3] P = I 1029 -> 1005 us per iteration, configs[4] share 5025 -> 4891,
+  // configs[2] shape 36.9 -> 36.1 when it was introduced).
   // ---- shared-memory plan: the largest chunk height whose double buffer fits
   StreamParams P{};
   size_t dyn = 0;
@@ -1480,7 +1485,7 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
     const int64_t vrows = (ch + 2 * H0 + 1) & ~1ll;
     P.a_vr = take(sizeof(double) * vrows * m);
     P.a_vd = take(sizeof(double) * vrows * m);
-    P.a_vx = fold ? take(sizeof(double) * ch * m) : 0;
+    P.a_vx = take(sizeof(double) * ch * m);
     for (int st = 0; st < z; ++st)
     {
       const int64_t rows = (ch + 2 * hal[st + 1] + 1) & ~1ll;
@@ -1491,7 +1496,7 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
     P.a_ao = take(sizeof(unsigned long long) * ch * OWA);
     const size_t a_bytes = off;
     off = 0;
-    const size_t b_bytes = sizeof(double) * ch * m * (fold ? 2 : 4);
+    const size_t b_bytes = sizeof(double) * ch * m * 2;
     P.buf_bytes = (std::max(a_bytes, b_bytes) + 127) & ~static_cast<size_t>(127);
     off = nb * P.buf_bytes;
     // m == 4 with a chain: planar stage buffers, one plane stride (the widest buffer's rows) for all
@@ -1519,7 +1524,7 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
   }
 #endif
   // ---- vectors (padded) and the per-point block plan
-  const int64_t ldv = (n + 2 * kPadR) * m;
+  const int64_t ldv = ((n + 2 * kPadR) * m + 1) & ~1ll; // even: every point block starts 16-byte aligned
   const size_t vb = sizeof(double) * static_cast<size_t>(l) * ldv;
   DBuf b(vb, s), xt(vb, s), r(vb, s), d0(vb, s), d1(vb, s), w(vb, s), sol(vb, s);
   for (DBuf *q : {&b, &xt, &r, &d0, &d1, &w, &sol})
@@ -1528,29 +1533,51 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
       l, m, n, ldv, B_dev, ldb, b.as<double>(), r.as<double>(), d0.as<double>(), xt.as<double>());
   check_launch(ctx, "stream_init");
   const int G = ctx->num_sms;
-  // Serial schedule (opt-in, MGPU_STREAM_SERIAL=1): the points run one after another on every
-  // block, so phase B re-reads phase A's outputs (r, d_new, w: 24 n m bytes) from L2 and w never
-  // reaches HBM (its lines are discarded once read).  Measured on configs[3] (n = 1e6, m = 4,
-  // 16 points): DRAM traffic 6.15 -> 4.70 GB per batched iteration, but 1072 -> 1415 us per
-  // iteration -- two grid barriers, two block reductions, two flushes and two pipeline fills
-  // per point (~10 us per pass, 32 passes) cost more than the bytes saved.  Off by default.
-  const bool serial = ctx->opt[MGPU_OPT_STREAM_SERIAL] != 0 && l <= kTabSlots;
   std::vector<Seg> hseg(static_cast<size_t>(G) * kMaxSeg, Seg{-1, 0, 0, 0});
   std::vector<int2> hpb(static_cast<size_t>(l));
-  if (serial)
+  // tile plan: slabs = G / gcd(G, l) (so that slabs * l tiles = tile_seg * G), when a block's
+  // tile_seg = l / gcd(G, l) segments fit its table and every slab has rows
+  int tile_slabs = 0, tile_seg = 0;
   {
-    // every block: the same row slab of every point (32-row groups, no row-less block inside
-    // the reduction range)
-    const int64_t groups = (n + 31) / 32;
-    const int nb = static_cast<int>(std::min<int64_t>(G, groups));
-    for (int bk = 0; bk < G; ++bk)
+    int a = G, c = l;
+    while (c)
     {
-      const int64_t g0 = bk < nb ? groups * bk / nb : 0, g1 = bk < nb ? groups * (bk + 1) / nb : 0;
-      hseg[static_cast<size_t>(bk) * kMaxSeg] =
-          Seg{0, static_cast<int>(g0 * 32), static_cast<int>(std::min<int64_t>(n, g1 * 32)), 0};
+      const int t = a % c;
+      a = c;
+      c = t;
     }
+    tile_slabs = G / a;
+    tile_seg = l / a;
+  }
+  // (worth it from about 16 chunks per tile: more segments per block mean more per-point flushes,
+  // configs[2] shape measured 26.8 us per iteration contiguous against 29.2 tiled, configs[3] 1106 / 1097)
+  const bool tiled = ctx->opt[MGPU_OPT_STREAM_TILES] != 0 && l > 1 && tile_seg <= kMaxSeg &&
+                     (ctx->opt[MGPU_OPT_STREAM_TILES] > 1 || n / tile_slabs >= 16 * CH) &&
+                     (n + 31) / 32 >= 4 * static_cast<int64_t>(tile_slabs);
+  if (tiled)
+  {
+    // Row-slab x point tiles.  Tile T = (slab T / l, point T % l); block bk takes tiles bk, bk + G,
+    // bk + 2 G, ... in that order, so at any time the G blocks work on G consecutive tiles:
+    // G / l whole slabs, every point of a slab at the same time.  Whatever the points of a slab
+    // share (the ELL offsets; operator values formed from shared M, D, K) is then read from
+    // HBM by the first block to get there and from L2 by the others.  (The contiguous plan below
+    // puts point p on blocks [p G / l, (p + 1) G / l): with G / l = 9.25 only every fourth
+    // point passes the same rows at the same time.)  Every block owns at most one tile of a
+    // point (tile_seg * G tiles, G | tile_slabs * l), so one partial-sum slot per (point, block).
+    const int64_t groups = (n + 31) / 32;
+    for (int bk = 0; bk < G; ++bk)
+      for (int t = 0; t < tile_seg; ++t)
+      {
+        const int64_t T = static_cast<int64_t>(t) * G + bk;
+        const int64_t slab = T / l;
+        const int p = static_cast<int>(T % l);
+        const int64_t g0 = groups * slab / tile_slabs, g1 = groups * (slab + 1) / tile_slabs;
+        hseg[static_cast<size_t>(bk) * kMaxSeg + t] =
+            Seg{p, static_cast<int>(g0 * 32), static_cast<int>(std::min<int64_t>(n, g1 * 32)), 0};
+      }
+    // slots of blocks without a tile of the point stay zero (the buffer is cleared below)
     for (int p = 0; p < l; ++p)
-      hpb[p] = make_int2(0, nb);
+      hpb[p] = make_int2(0, G);
   }
   else if (l <= G)
   {
@@ -1613,6 +1640,7 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
     }
   }
   DBuf partial(sizeof(double) * static_cast<size_t>(l) * 2 * kMaxM * G, s);
+  MG_CUDA(cudaMemsetAsync(partial.ptr, 0, partial.bytes, s));
   MG_CUDA(cudaMemcpyAsync(segs.ptr, hseg.data(), sizeof(Seg) * hseg.size(), cudaMemcpyHostToDevice, s));
   MG_CUDA(cudaMemcpyAsync(pblk.ptr, hpb.data(), sizeof(int2) * hpb.size(), cudaMemcpyHostToDevice, s));
   MG_CUDA(cudaMemcpyAsync(dA.ptr, hA.data(), sizeof(PEll) * hA.size(), cudaMemcpyHostToDevice, s));
@@ -1621,22 +1649,17 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
   P.m = m;
   P.z = z;
   P.rpt = 1;
-  P.serial = serial ? 1 : 0;
+  P.exp = static_cast<int>(ctx->opt[MGPU_OPT_STREAM_EXP]);
   P.ch = static_cast<int>(CH);
   {
-    // phase B: r, w (+ x~, d unfolded) -> the tallest chunk (multiple of 64 rows, <= 8192) that fits one slot
-    const int nvec = fold ? 2 : 4;
-    int64_t chb = static_cast<int64_t>(P.buf_bytes / (nvec * sizeof(double) * static_cast<size_t>(m))) & ~63ll;
+    // phase B: r, w -> the tallest chunk (multiple of 64 rows, <= 8192) that fits one slot
+    int64_t chb = static_cast<int64_t>(P.buf_bytes / (2 * sizeof(double) * static_cast<size_t>(m))) & ~63ll;
     chb = std::min<int64_t>(std::max<int64_t>(chb, CH), 8192);
     if (ctx->opt[MGPU_OPT_STREAM_SAME_CHB]) // diagnostics: phase B on the phase A chunk height
       chb = CH;
     P.ch_b = static_cast<int>(chb);
-    const size_t vb = static_cast<size_t>(chb) * m * sizeof(double); // multiple of 512 B
     P.b_r = 0;
-    P.b_w = vb;
-    P.b_x = 2 * vb;
-    P.b_d = 3 * vb;
-    P.fold = fold ? 1 : 0;
+    P.b_w = static_cast<size_t>(chb) * m * sizeof(double); // multiple of 512 B
   }
   P.n = n;
   P.ldv = ldv;

@@ -37,12 +37,12 @@ def _oracle_case():
     return (M, D, K), ops, facs, b, sols
 
 
-@pytest.mark.parametrize("path", ["auto", "stream", "stream_serial", "banded"])
+@pytest.mark.parametrize("path", ["auto", "stream", "stream_flat", "banded"])
 def test_bench_workload_iterate_parity(mg, path):
     (M, D, K), ops, facs, b, want = _oracle_case()
     ctx = mg.default_context()
-    ctx.set_option("stream_serial", 1 if path == "stream_serial" else 0)
-    ctx.set_cg_path("stream" if path == "stream_serial" else path)
+    ctx.set_option("stream_tiles", 0 if path == "stream_flat" else 2)
+    ctx.set_cg_path("stream" if path == "stream_flat" else path)
     try:
         # the bench's device pipeline: assembly + batched LS-SPAI + one batched solve
         dops = mg.shifted_operators(M, D, K, SHIFTS, ctx=ctx)
@@ -60,14 +60,14 @@ def test_bench_workload_iterate_parity(mg, path):
             assert rel(r.X[:, 0], w["solution"]) < 1e-8
     finally:
         ctx.set_cg_path("auto")
-        ctx.set_option("stream_serial", 0)
+        ctx.set_option("stream_tiles", 1)
 
 
-def test_config3_serial_schedule_matches_batched(mg):
+def test_config3_tile_plan_matches_contiguous_plan(mg):
     """BASELINE configs[3] shape (n = 1e6, m = 4, 16 shifts, P = I) through the streaming
-    kernel: the point-serial schedule (L2 hand-off between the phases, w discarded from L2)
-    against the batched schedule after 40 iterations.  Same arithmetic per element; only the
-    dot-product trees differ (block slabs), so the iterates agree to rounding noise."""
+    kernel: the slab x point tile plan (four tiles per block, the 16 points of a slab in flight
+    together) against one contiguous row range per block, after 40 iterations.  Same arithmetic
+    per element; only the dot-product trees differ, so the iterates agree to rounding noise."""
     ne, m, k = 500000, 4, 40
     shifts = [10.0 ** (1 + 3 * i / 15) for i in range(16)]
     ctx = mg.default_context()
@@ -79,13 +79,13 @@ def test_config3_serial_schedule_matches_batched(mg):
     ops = mg.shifted_operators(M, D, K, shifts, ctx=ctx)
     ctx.set_cg_path("stream")
     try:
-        ctx.set_option("stream_serial", 0)
+        ctx.set_option("stream_tiles", 0)
         ref = mg.cg_solve_batched(ops, [[] for _ in ops], B, rtol=1e-10, maxit=k, ctx=ctx)
-        ctx.set_option("stream_serial", 1)
+        ctx.set_option("stream_tiles", 1)
         got = mg.cg_solve_batched(ops, [[] for _ in ops], B, rtol=1e-10, maxit=k, ctx=ctx)
     finally:
         ctx.set_cg_path("auto")
-        ctx.set_option("stream_serial", 0)
+        ctx.set_option("stream_tiles", 1)
     for g, r in zip(got, ref):
         np.testing.assert_array_equal(g.iterations, r.iterations)
         assert rel(g.X, r.X) < 1e-10

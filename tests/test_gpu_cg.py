@@ -13,20 +13,22 @@ from conftest import rel
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True, params=["auto", "cluster_v1", "stream", "stream_serial", "banded", "general"])
+@pytest.fixture(autouse=True, params=["auto", "cluster_v1", "stream", "stream_flat", "banded", "general"])
 def cg_path(request, mg):
     """Every parity case runs through every CG kernel: cluster-resident (auto on these
-    on-chip sizes), the streaming kernel (batched and point-serial schedules), the banded
+    on-chip sizes), the streaming kernel (slab x point tile plan and one contiguous row range per block), the banded
     grid kernel and the general CSR kernel."""
     ctx = mg.default_context()
-    if request.param == "stream_serial":
-        ctx.set_option("stream_serial", 1)
+    if request.param == "stream_flat":
+        ctx.set_option("stream_tiles", 0)
         ctx.set_cg_path("stream")
     else:
+        if request.param == "stream":
+            ctx.set_option("stream_tiles", 2)  # the tile plan wherever its shape allows, whatever the size
         ctx.set_cg_path(request.param)
     yield request.param
     ctx.set_cg_path("auto")
-    ctx.set_option("stream_serial", 0)
+    ctx.set_option("stream_tiles", 1)
 
 
 def test_path_selection(mg, oracle, cg_path):
@@ -36,7 +38,7 @@ def test_path_selection(mg, oracle, cg_path):
     mg.pcg_solve(A, [P], np.ones(600), maxit=5)
     # A^2-pattern factor: 10 entries per row -> the shared-memory cluster kernel (v1); v2 packs <= 8
     assert mg.default_context().last_cg_path == {"auto": "cluster_v1", "cluster_v1": "cluster_v1", "stream": "stream",
-                                                  "stream_serial": "stream", "banded": "banded",
+                                                  "stream_flat": "stream", "banded": "banded",
                                                   "general": "general"}[cg_path]
     if cg_path == "auto":
         P1 = oracle.spai_ls(A, None, 0)
