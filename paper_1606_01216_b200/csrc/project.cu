@@ -14,8 +14,9 @@
 // trees (deterministic, ~1e-16 relative).  Every scalar update is an
 // unfused multiply then add, like the scalar kernel table.
 //
-// project_reduce: S V as an SpMM in CSR row order (spmv_into's order), then
-// the dense products V^T W, V^T F, Cp V, Cv V are plain GEMMs (cuBLAS DGEMM).
+// project_reduce: V^T (S V) for M, D, K in one fused kernel (proj_fused below: the S V tiles are
+// formed in shared memory in CSR row order, spmv_into's order, and never written to HBM); V^T F,
+// Cp V, Cv V are hand-written FP64 GEMMs (dense_gemm.cu).  No cuBLAS.
 #include <cooperative_groups.h>
 
 #include <algorithm>
