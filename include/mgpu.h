@@ -109,7 +109,8 @@ typedef enum mgpu_option
   MGPU_OPT_LS_GROUP = 9,        /* LS-SPAI: skip the lane-per-column kernels (default 0) */
   MGPU_OPT_STREAM_TILES = 10,   /* cg_stream: row-slab x point tiles, the points of a slab processed at the same time (default 1: where a tile holds >= 16 chunks; 2: always; 0: one contiguous row range per block) */
   MGPU_OPT_STREAM_EXP = 11,     /* experiments (default 0) */
-  MGPU_OPT_COUNT = 12,
+  MGPU_OPT_SEQ_SPARSE = 12,     /* sequential MR-SPAI: sparse row-list kernel at every size (default 0: dense-factor kernel up to n = 4096) */
+  MGPU_OPT_COUNT = 13,
 } mgpu_option;
 int mgpu_ctx_set_option(mgpu_ctx *ctx, int option, int64_t value);
 int mgpu_ctx_get_option(const mgpu_ctx *ctx, int option, int64_t *value);

@@ -136,7 +136,7 @@ struct mgpu_ctx
   int last_cg_path = 1; // 0 banded (grid), 1 general, 2 cluster v2 (m = 1), 3 cluster v1
   int cg_path = 0;      // 0 auto, 1 force general, 2 force banded grid kernel, 3 cluster v1 only, 4 stream (no cluster)
   long long *prof_dev = nullptr; // diagnostics: per-phase clock64 totals of the CG kernels (MGPU_OPT_PROFILE_PHASES)
-  int64_t opt[MGPU_OPT_COUNT] = {0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 1, 0}; // mgpu_ctx_set_option
+  int64_t opt[MGPU_OPT_COUNT] = {0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0}; // mgpu_ctx_set_option
   void *nccl = nullptr;          // ncclComm_t (mgpu_comm_init), one rank per context
   int nranks = 1, rank = 0;
   cudaEvent_t phase_ev[4] = {nullptr, nullptr, nullptr, nullptr}; // mgpu_shifted_solve phase timing (lazy)

@@ -11,6 +11,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <thread>
+#include <vector>
 #include <string>
 
 #include "mgpu.h"
@@ -692,12 +693,38 @@ bool CudaCgBackend::cached(std::int64_t point_index, const DenseMatrix &rhs) con
   return rhs.nrows == st_->n && cached(point_index, rhs.values.data(), rhs.ncols);
 }
 
+namespace
+{
+// memcmp == 0 over several host threads: the exact "is this sys.F" test reads 2 x 8 n m bytes per
+// solve(i, F) call (configs[3]: 16 calls x 32 MB, ~3 ms each on one thread).
+bool same_bytes(const void *a, const void *b, std::size_t bytes)
+{
+  constexpr std::size_t kPerThread = std::size_t(4) << 20;
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const std::size_t parts = std::min<std::size_t>({std::size_t(8), std::size_t(hw), bytes / kPerThread + 1});
+  if (parts <= 1)
+    return std::memcmp(a, b, bytes) == 0;
+  std::vector<int> eq(parts, 1);
+  std::vector<std::thread> th;
+  const auto *pa = static_cast<const unsigned char *>(a);
+  const auto *pb = static_cast<const unsigned char *>(b);
+  for (std::size_t t = 0; t < parts; ++t)
+  {
+    const std::size_t o0 = bytes * t / parts, o1 = bytes * (t + 1) / parts;
+    th.emplace_back([=, &eq] { eq[t] = std::memcmp(pa + o0, pb + o0, o1 - o0) == 0; });
+  }
+  for (auto &x : th)
+    x.join();
+  return std::all_of(eq.begin(), eq.end(), [](int v) { return v != 0; });
+}
+} // namespace
+
 bool CudaCgBackend::cached(std::int64_t point_index, const double *rhs, std::int64_t m) const
 {
   const State &s = *st_;
   const std::size_t pi = static_cast<std::size_t>(point_index);
   return point_index >= 0 && pi < s.spec_ready.size() && s.spec_ready[pi] && m == s.spec_m &&
-         std::memcmp(rhs, s.spec_rhs.data(), sizeof(double) * s.spec_rhs.size()) == 0;
+         same_bytes(rhs, s.spec_rhs.data(), sizeof(double) * s.spec_rhs.size());
 }
 
 void CudaCgBackend::take_cached(std::int64_t point_index, double *X, double *REC, double *TR, std::int64_t *iterations,

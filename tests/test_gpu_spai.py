@@ -101,9 +101,19 @@ def test_mr_stagnation_column_and_message(mg, oracle):
 
 
 # --------------------------------------------- MR-SPAI, sequential mode (the reference default)
+@pytest.fixture(params=["dense", "sparse"])
+def seq_kernel(request, mg):
+    """Both device kernels of sequential mode: the dense-factor grid kernel (n <= 4096) and the
+    sparse row-list chain (every size; forced here with the seq_sparse context option)."""
+    ctx = mg.default_context()
+    ctx.set_option("seq_sparse", 1 if request.param == "sparse" else 0)
+    yield request.param
+    ctx.set_option("seq_sparse", 0)
+
+
 @pytest.mark.parametrize("n,kscale,s", [(300, 0.01, 1.0), (300, 1.0, 10.0), (300, 100.0, 10.0), (500, 1.0, 10.0),
                                         (2000, 1.0, 100.0)])
-def test_mr_sequential_build_t1(mg, oracle, n, kscale, s):
+def test_mr_sequential_build_t1(mg, oracle, seq_kernel, n, kscale, s):
     """d = P r over the columns built so far (spai.cpp:138-158): heavy fill (200-700 nnz/column)."""
     M, D, K = oracle.chain_generate(n, consistent=True, stiffness_scale=kscale)
     A = oracle.shifted_operator(M, D, K, s)
@@ -113,7 +123,7 @@ def test_mr_sequential_build_t1(mg, oracle, n, kscale, s):
     assert rel(f.target_frob_residual, wres) < 1e-10
 
 
-def test_mr_sequential_update_t1(mg, oracle):
+def test_mr_sequential_update_t1(mg, oracle, seq_kernel):
     """s = 10 -> 10.5 at n = 100, sequential mode."""
     M, D, K = oracle.chain_generate(100, consistent=True, stiffness_scale=1.0)
     A1 = oracle.shifted_operator(M, D, K, 10.0)
@@ -126,7 +136,7 @@ def test_mr_sequential_update_t1(mg, oracle):
     np.testing.assert_array_equal(Q.todense(), np.eye(100))
 
 
-def test_mr_sequential_kats(mg):
+def test_mr_sequential_kats(mg, seq_kernel):
     from oracle import Csr
     P = mg.spai_build(Csr.from_dense(np.eye(5)), mode=mg.SEQUENTIAL).matrix.download()
     np.testing.assert_array_equal(P.todense(), np.eye(5))
@@ -134,7 +144,7 @@ def test_mr_sequential_kats(mg):
     assert rel(P.todense(), np.diag([0.5, 0.25])) < 1e-12
 
 
-def test_mr_sequential_stagnation(mg, oracle):
+def test_mr_sequential_stagnation(mg, oracle, seq_kernel):
     from oracle import OracleError
     M, D, K = oracle.hermite_generate(1000)
     A = oracle.shifted_operator(M, D, K, 100.0)
