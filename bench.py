@@ -47,6 +47,36 @@ PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM = 6650.0
 
 
+def ncu_traffic(workload_key: str, loops: int):
+    """(bytes per launch, note): dram__bytes_read + dram__bytes_write of the CG kernel from the
+    committed ncu capture of this workload, scaled from the capture's iteration count to this
+    launch's (the kernel streams the same bytes every iteration); (None, why) when there is no
+    capture of this workload or the kernel source changed since."""
+    import hashlib
+    path = os.path.join(ROOT, "profiles", "r02_ncu_summary.json")
+    try:
+        with open(path) as f:
+            summ = json.load(f)
+    except (OSError, ValueError):
+        return None, "null: no ncu summary under profiles/"
+    for key, ent in summ.items():
+        if ent.get("workload_key") != workload_key or "dram_bytes_per_cg_iteration" not in ent:
+            continue
+        h = hashlib.sha256()
+        try:
+            for rel in ent.get("source_files", []):
+                with open(os.path.join(ROOT, rel), "rb") as f:
+                    h.update(f.read())
+        except OSError:
+            return None, "null: kernel source not found"
+        if h.hexdigest()[:16] != ent.get("source_sha16"):
+            return None, f"null: profiles/r02_ncu_summary.json[{key}] was captured on an older kernel source"
+        return float(ent["dram_bytes_per_cg_iteration"]) * loops, (
+            f"ncu --set full capture profiles/r02_ncu_summary.json[{key}] (dram__bytes_read.sum + "
+            f"dram__bytes_write.sum per CG iteration x {loops} iterations of this launch; source hash checked)")
+    return None, "null: no ncu capture of this workload under profiles/"
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -437,10 +467,12 @@ def run_mgpu(args, rank, world, local_rank):
     e2e_call_value = solves / (e2e_call_ms / 1e3)
     peak, peak_kind = peak_hbm()
     achieved = sum(r["bytes"] for r in recs) / (sum(cg_ms) / 1e3) / 1e9
-    # DRAM traffic is not measurable inside this process (ncu replays kernels); the per-launch
-    # dram__bytes of this command's top kernel are in profiles/ (DESIGN.md 5), not copied here.
-    traffic = None
+    # DRAM traffic is not measurable inside this process (ncu replays kernels).  It comes from the
+    # committed ncu --set full capture of this command (profiles/r02_ncu_summary.json), per launch
+    # like `achieved`, and ONLY while the kernel's source is the one that was captured: the summary
+    # records a hash of the kernel's source files, and a mismatch reports null instead of a stale number.
     loops = recs[-1]["loops"]
+    traffic, traffic_note = ncu_traffic(args.workload, loops)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -487,7 +519,7 @@ def run_mgpu(args, rank, world, local_rank):
             "cg_ms": statistics.median(cg_ms), "cg_us_per_iteration": 1e3 * statistics.median(cg_ms) / max(loops, 1),
             "cg_iterations": loops, "breakdowns": recs[-1]["breakdowns"], "cg_kernel": ctx.last_cg_path,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "traffic_note": "null: measured per launch by ncu, see profiles/",
+                         "traffic": traffic, "traffic_note": traffic_note,
                          "peak_source": peak_kind, "kernel": "cg_" + ctx.last_cg_path,
                          "regime": ("working set on chip (shared memory / L2): latency- and barrier-bound; the HBM "
                                     "fraction is reported for the contract" if args.workload in ("config0", "config1")
