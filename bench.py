@@ -529,6 +529,7 @@ def run_mgpu(args, rank, world, local_rank):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d_bytes,
                     "d2h_bytes_per_step": d2h_bytes,
                     "step_ms_min_med_max": [1e3 * min(plug_recs), 1e3 * statistics.median(plug_recs), 1e3 * max(plug_recs)],
+                    "slowest_step": int(np.argmax(plug_recs)),
                     "prepare_ms": 1e3 * statistics.median(p for p, _ in plug_split),
                     "solves_ms": 1e3 * statistics.median(q for _, q in plug_split),
                     "path": "plugin: mor::CudaCgBackend via include/mor_cuda.h -- prepare(sys, shifts, 1) (upload "

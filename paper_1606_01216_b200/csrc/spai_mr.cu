@@ -6,7 +6,9 @@
 // Here a column's vectors p, r, d, w live in a dense WINDOW of shared memory:
 // with K of lower/upper bandwidth (bl, bu), r's support after k steps lies in
 // [j - (k+1) bu, j + (k+1) bl], so a window of W = 512 slots covers 50 steps
-// of a bandwidth-5 operator.  Entries outside a Spa's support are exact zeros
+// of a bandwidth-5 operator.  Wider operators (or slowly converging columns) get a wider window:
+// the build starts at 512 slots with 4 columns per block and, when a column outgrows its
+// window, reruns at 2048 slots (2 columns per block) and then 6144 (1 column per block, 192 KB).  Entries outside a Spa's support are exact zeros
 // in the window, so every sum over a support equals the sum over the window
 // (zero terms add exactly nothing).  Arithmetic per entry matches spai.cpp:
 // w_i accumulates K_ik d_k in ascending k without FMA, p += a d, r += (-a) w.
@@ -34,9 +36,10 @@ void trace_inner_dev(mgpu_ctx *ctx, const mgpu_csr *A, const mgpu_csr *B, double
 namespace
 {
 
-constexpr int kW = 512;       // window slots per column
-constexpr int kMrWarps = 4;   // columns per block
-constexpr size_t kMrSmem = sizeof(double) * 4 * kW * kMrWarps;
+// window ladder: slots per column, columns (warps) per block
+constexpr int kMrLevels = 3;
+constexpr int kMrW[kMrLevels] = {512, 2048, 6144};
+constexpr int kMrWpb[kMrLevels] = {4, 2, 1};
 
 enum MrFail : int
 {
@@ -77,6 +80,7 @@ struct MrArgs
   double alpha, tol_sq;
   int64_t max_iters;
   int bl, bu; // K's lower / upper bandwidth
+  int W;      // window slots per column
   int *bw;               // pass 1: bandwidth bound of the factor
   int64_t *count;        // pass 1: nonzeros of column j
   double *residual;      // pass 1: final ||r|| (or ||r|| at failure)
@@ -87,7 +91,7 @@ struct MrArgs
   double *out_vals;      // pass 2
 };
 
-template <bool kFill>
+template <bool kFill, int kMrWarps>
 __global__ void __launch_bounds__(kMrWarps * 32) mr_columns(MrArgs a)
 {
   extern __shared__ double smem[];
@@ -95,6 +99,7 @@ __global__ void __launch_bounds__(kMrWarps * 32) mr_columns(MrArgs a)
   const int64_t j = static_cast<int64_t>(blockIdx.x) * kMrWarps + warp;
   if (j >= a.n)
     return;
+  const int kW = a.W;
   double *p = smem + static_cast<size_t>(warp) * 4 * kW;
   double *r = p + kW, *d = r + kW, *w = d + kW;
   const int64_t base = j - kW / 2; // slot(i) = i - base
@@ -304,20 +309,43 @@ mgpu_csr *mr_build(mgpu_ctx *ctx, const mgpu_csr *K, const mgpu_csr *rhs_src, do
   a.residual = resid.as<double>();
   a.fail_iters = fit.as<int64_t>();
   a.err = err.as<unsigned long long>();
-  const unsigned grid = static_cast<unsigned>((n + kMrWarps - 1) / kMrWarps);
-  MG_CUDA(cudaFuncSetAttribute(mr_columns<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMrSmem));
-  MG_CUDA(cudaFuncSetAttribute(mr_columns<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMrSmem));
+  // one pass (count or fill) at window level lv
+  int lv = 0;
+  auto launch = [&](bool fill) {
+    a.W = kMrW[lv];
+    const int wpb = kMrWpb[lv];
+    const size_t smem = sizeof(double) * 4 * static_cast<size_t>(a.W) * wpb;
+    const unsigned grid = static_cast<unsigned>((n + wpb - 1) / wpb);
+    auto go = [&](auto kern) {
+      MG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      kern<<<grid, wpb * 32, smem, s>>>(a);
+    };
+    if (wpb == 4)
+      fill ? go(mr_columns<true, 4>) : go(mr_columns<false, 4>);
+    else if (wpb == 2)
+      fill ? go(mr_columns<true, 2>) : go(mr_columns<false, 2>);
+    else
+      fill ? go(mr_columns<true, 1>) : go(mr_columns<false, 1>);
+    check_launch(ctx, fill ? "mr_columns<fill>" : "mr_columns<count>");
+  };
   mgpu_csr *P = nullptr;
   try
   {
-    if (n > 0)
+    unsigned long long h = ULLONG_MAX;
+    for (;; ++lv)
     {
-      mr_columns<false><<<grid, kMrWarps * 32, kMrSmem, s>>>(a);
-      check_launch(ctx, "mr_columns<count>");
+      if (n > 0)
+        launch(false);
+      MG_CUDA(cudaMemcpyAsync(&h, err.ptr, sizeof(h), cudaMemcpyDeviceToHost, s));
+      MG_CUDA(cudaStreamSynchronize(s));
+      // the lowest failing column outgrew its window: rerun the count pass with the next wider one
+      // (any other failure at a lower column would have been reported instead of it)
+      if (h == ULLONG_MAX || static_cast<int>(h & 0xff) != kWindow || lv + 1 >= kMrLevels)
+        break;
+      MG_CUDA(cudaMemsetAsync(err.ptr, 0xff, sizeof(unsigned long long), s));
+      MG_CUDA(cudaMemsetAsync(count.ptr, 0, sizeof(int64_t) * (n + 1), s));
+      MG_CUDA(cudaMemsetAsync(pbw.ptr, 0, sizeof(int), s));
     }
-    unsigned long long h = 0;
-    MG_CUDA(cudaMemcpyAsync(&h, err.ptr, sizeof(h), cudaMemcpyDeviceToHost, s));
-    MG_CUDA(cudaStreamSynchronize(s));
     if (h != ULLONG_MAX)
     {
       const int64_t col = static_cast<int64_t>(h >> 8);
@@ -342,7 +370,7 @@ mgpu_csr *mr_build(mgpu_ctx *ctx, const mgpu_csr *K, const mgpu_csr *rhs_src, do
         throw Error(MGPU_ERR_NUMERICAL, "spai: non-finite step in column " + c, col);
       default:
         throw Error(MGPU_ERR_UNSUPPORTED,
-                    "spai: column " + c + " outgrew the device window (" + std::to_string(kW) +
+                    "spai: column " + c + " outgrew the device window (" + std::to_string(kMrW[kMrLevels - 1]) +
                         " slots; operator bandwidth " + std::to_string(hbw[0]) + "/" + std::to_string(hbw[1]) + ")",
                     col);
       }
@@ -375,10 +403,7 @@ mgpu_csr *mr_build(mgpu_ctx *ctx, const mgpu_csr *K, const mgpu_csr *rhs_src, do
     a.out_rows = PT->col_idx;
     a.out_vals = PT->values;
     if (n > 0)
-    {
-      mr_columns<true><<<grid, kMrWarps * 32, kMrSmem, s>>>(a);
-      check_launch(ctx, "mr_columns<fill>");
-    }
+      launch(true);
     if (col_residual && n > 0)
       MG_CUDA(cudaMemcpyAsync(col_residual, resid.ptr, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
     P = transpose_csr(ctx, PT);

@@ -100,6 +100,41 @@ def test_mr_stagnation_column_and_message(mg, oracle):
     assert str(eg.value).split(" stalled")[0] == eo.value.msg.split(" stalled")[0]
 
 
+# --------------------------------------------- frozen MR-SPAI beyond the 512-slot column window
+def _banded(n, off, c=-0.5):
+    """SPD, diagonally dominant: 4 on the diagonal, -1 at +-1, c at +-off (CSR built directly)."""
+    from oracle import Csr
+    rows, cols, vals = [], [], []
+    for d, v in ((-off, c), (-1, -1.0), (0, 4.0), (1, -1.0), (off, c)):
+        i = np.arange(max(0, -d), min(n, n - d))
+        rows.append(i)
+        cols.append(i + d)
+        vals.append(np.full(i.shape, v))
+    rows, cols, vals = (np.concatenate(x) for x in (rows, cols, vals))
+    order = np.lexsort((cols, rows))
+    rp = np.zeros(n + 1, np.int64)
+    np.add.at(rp, rows + 1, 1)
+    return Csr(n, n, np.cumsum(rp).astype(np.int64), cols[order].astype(np.int32), vals[order].astype(np.float64))
+
+
+@pytest.mark.parametrize("n,off,tol", [(3000, 40, 1e-2), (6000, 100, 1e-3)])
+def test_mr_frozen_wide_columns(mg, oracle, n, off, tol):
+    """Columns whose residual support outgrows 512 slots (about 800 and 3400 wide here) rerun on the
+    2048- and 6144-slot windows: same factor as the reference."""
+    K = _banded(n, off)
+    want, wres = oracle.spai_build(K, tol=tol, mode=1)
+    f = mg.spai_build(K, tol=tol, mode=mg.FROZEN)
+    _csr_close(f.matrix.download(), want)
+    assert rel(f.target_frob_residual, wres) < 1e-10
+
+
+def test_mr_frozen_window_limit_is_reported(mg):
+    """Beyond the widest window the build refuses (no fallback), naming the column."""
+    K = _banded(40000, 3000)
+    with pytest.raises(mg.UnsupportedError, match="outgrew the device window"):
+        mg.spai_build(K, tol=1e-6, mode=mg.FROZEN)
+
+
 # --------------------------------------------- MR-SPAI, sequential mode (the reference default)
 @pytest.fixture(params=["dense", "sparse"])
 def seq_kernel(request, mg):
