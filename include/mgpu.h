@@ -108,7 +108,7 @@ typedef enum mgpu_option
   MGPU_OPT_QR_UNBLOCKED = 8,    /* thin_qr: column-at-a-time schedule instead of compact WY (default 0) */
   MGPU_OPT_LS_GROUP = 9,        /* LS-SPAI: skip the lane-per-column kernels (default 0) */
   MGPU_OPT_STREAM_TILES = 10,   /* cg_stream: row-slab x point tiles, the points of a slab processed at the same time (default 1: where a tile holds >= 16 chunks; 2: always; 0: one contiguous row range per block) */
-  MGPU_OPT_STREAM_EXP = 11,     /* experiments (default 0) */
+  MGPU_OPT_RETIRED2 = 11,       /* (was a traffic experiment switch of cg_stream; removed) */
   MGPU_OPT_SEQ_SPARSE = 12,     /* sequential MR-SPAI: sparse row-list kernel at every size (default 0: dense-factor kernel up to n = 4096) */
   MGPU_OPT_COUNT = 13,
 } mgpu_option;

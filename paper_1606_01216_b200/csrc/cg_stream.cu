@@ -125,12 +125,12 @@ struct StreamParams
   int l, m, z, rpt, ch; // ch: rows per chunk (phase A and the check pass)
   int ch_b;             // rows per chunk in phase B (fewer vectors per row: taller chunks fill the same slot)
   int nb;               // ring depth (2..kStreamNB)
-  int exp;              // MGPU_OPT_STREAM_EXP bits (experiments; 0 in production)
   // stage-buffer layout: 0 = row-interleaved [row][c]; > 0 (m == 4) = two planes of double2,
   // (c0, c1) and (c2, c3) per row, plane stride `pst` doubles.  A thread's row loads are then two
   // 16-byte loads from consecutive 16-byte slots across the warp (no bank conflicts; the
   // interleaved 32-byte rows cost two wavefronts per 16-byte load).
   int pst;
+  int s0_double; // 1: two stage-0 buffers (chunk parity), no block-wide barrier at the end of a chunk
   int64_t n, ldv; // ldv = (n + 2 PADR) * m rounded up to even: doubles per point block (16-byte aligned)
   int halo[kMaxZ + 1];
   int hmax;
@@ -155,7 +155,7 @@ struct StreamParams
   long long *prof; // optional [16] clock64 totals per phase (block 0, thread 0; MGPU_PROFILE_PHASES)
   // shared-memory carve-up (bytes): two input buffers (phase A layout and
   // phase B layout alias) + stage buffers
-  size_t buf_bytes, off_stage0, off_stage1, off_stage2;
+  size_t buf_bytes, off_stage0, off_stage0b, off_stage1, off_stage2; // stage 0 is double-buffered (chunk parity)
   size_t a_vr, a_vd, a_vx, a_fv[kMaxZ], a_fo[kMaxZ], a_av, a_ao; // phase A offsets inside a buffer
   size_t b_r, b_w;                                                // phase B offsets inside a buffer
 };
@@ -634,6 +634,7 @@ __device__ __forceinline__ void stream_pass(const StreamParams &P, BandShared<TB
   for (int q = 0; q < 2 * MT; ++q)
     acc[q] = 0.0;
   int bi = 0;
+  int step = 0;
   int cur_p = -1;
   const bool full_m = m == MT;
   // pairs: this thread's two columns (fixed, see above); scalar fallback (m < MT): TB % m == 0
@@ -790,7 +791,9 @@ __device__ __forceinline__ void stream_pass(const StreamParams &P, BandShared<TB
       const int H0 = P.hmax;
       const double *vr = reinterpret_cast<const double *>(buf + P.a_vr);
       const double *vd = reinterpret_cast<const double *>(buf + P.a_vd);
-      double *s0 = reinterpret_cast<double *>(smem + P.off_stage0);
+      // stage 0 alternates between two buffers: a warp that is done with this chunk starts the next
+      // one's stage 0 while slower warps still read this chunk's d_new for their dot products
+      double *s0 = reinterpret_cast<double *>(smem + ((step & 1) ? P.off_stage0b : P.off_stage0));
       double *sA = reinterpret_cast<double *>(smem + P.off_stage1);
       double *sB = reinterpret_cast<double *>(smem + P.off_stage2);
       // stage 0: d = fresh ? r : r + beta d_old over the halo-extended chunk; the deferred
@@ -976,11 +979,19 @@ __device__ __forceinline__ void stream_pass(const StreamParams &P, BandShared<TB
       }
     }
     pc.mark(kind == 2 ? 7 : 6);
-    consumer_sync<TB>(); // buffer bi and the stage buffers are free again
-    if (threadIdx.x == 0)
+    // this warp is done with buffer bi (the empty barrier counts the consumer warps); no block-wide
+    // barrier here: the next chunk's stage 0 writes the other stage-0 buffer, and the chain-stage
+    // buffers are next written after that chunk's first barrier, which every warp reaches only
+    // after finishing this chunk
+    if (P.s0_double || kind == 2)
+      __syncwarp();
+    else
+      consumer_sync<TB>(); // single stage-0 buffer: nobody may start the next chunk's stage 0 yet
+    if ((threadIdx.x & 31) == 0)
       mbar_arrive(&empty[bi]);
     pc.mark(8);
     bi = bi + 1 == P.nb ? 0 : bi + 1;
+    ++step;
   });
   if (cur_p >= 0)
     flush(cur_p);
@@ -1019,8 +1030,6 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(const __grid_constant__ 
       PEll a = P.A[p];
       if (P.eqA[p])
         a.o = P.A[0].o;
-      if (P.exp & 1) // experiment: every point streams point 0's operator values (wrong results; L2-sharing bound)
-        a.v = P.A[0].v;
       tab[g * (kMaxZ + 1)] = a;
       for (int st = 0; st < P.z; ++st)
       {
@@ -1028,8 +1037,6 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(const __grid_constant__ 
         PEll fe = P.F[p * P.z + f];
         if (P.eqF[p * P.z + f])
           fe.o = P.F[f].o;
-        if (P.exp & 2)
-          fe.v = P.F[f].v;
         tab[g * (kMaxZ + 1) + 1 + st] = fe;
       }
     }
@@ -1042,8 +1049,11 @@ __global__ void __launch_bounds__(TB + 32, 1) cg_stream(const __grid_constant__ 
       stg.a_fv[st] = static_cast<uint32_t>(P.a_fv[st]);
       stg.a_fo[st] = static_cast<uint32_t>(P.a_fo[st]);
     }
-    for (int b = 0; b < 2 * kStreamNB; ++b)
-      mbar_init(&bars[b], 1);
+    for (int b = 0; b < kStreamNB; ++b)
+    {
+      mbar_init(&bars[b], 1);                   // full: the producer's arrive.expect_tx
+      mbar_init(&bars[kStreamNB + b], TB / 32); // empty: one arrival per consumer warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int p = threadIdx.x; p < P.l; p += TBX)
@@ -1472,8 +1482,13 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
     const int fd = ctx->opt[MGPU_OPT_STREAM_RING] ? static_cast<int>(ctx->opt[MGPU_OPT_STREAM_RING]) : 2;
     cands.insert(cands.begin(), {ctx->opt[MGPU_OPT_STREAM_CHUNK], fd});
   }
-  for (const auto &cand : cands)
+  // every candidate first with the double-buffered stage 0 (no block-wide barrier at the end of a
+  // chunk), then with a single one: the chunk height comes first (configs[4] share: 448-row chunks
+  // with one stage-0 buffer 4841 us per iteration, 320-row chunks with two 5150)
+  for (size_t ci = 0; ci < 2 * cands.size() && CH == 0; ++ci)
   {
+    const auto &cand = cands[ci / 2];
+    const bool dbl = (ci & 1) == 0;
     const int64_t ch = cand.first;
     const int nb = cand.second;
     size_t off = 0;
@@ -1503,6 +1518,8 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
     const int64_t srows0 = ch + 2 * H0;
     P.pst = (m == 4 && z >= 1) ? static_cast<int>(2 * srows0) : 0; // (P = I measured 842 -> 859 us planar)
     P.off_stage0 = take(sizeof(double) * srows0 * m);
+    P.off_stage0b = dbl ? take(sizeof(double) * srows0 * m) : P.off_stage0;
+    P.s0_double = dbl ? 1 : 0;
     P.off_stage1 = z >= 1 ? take(sizeof(double) * (P.pst ? srows0 : ch + 2 * hal[1]) * m) : 0; // chain stages
     P.off_stage2 = z >= 2 ? take(sizeof(double) * (P.pst ? srows0 : ch + 2 * hal[2]) * m) : 0;
     if (off + stat <= static_cast<size_t>(optin))
@@ -1510,7 +1527,6 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
       dyn = off;
       CH = ch;
       P.nb = nb;
-      break;
     }
   }
   if (CH == 0)
@@ -1649,7 +1665,6 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
   P.m = m;
   P.z = z;
   P.rpt = 1;
-  P.exp = static_cast<int>(ctx->opt[MGPU_OPT_STREAM_EXP]);
   P.ch = static_cast<int>(CH);
   {
     // phase B: r, w -> the tallest chunk (multiple of 64 rows, <= 8192) that fits one slot

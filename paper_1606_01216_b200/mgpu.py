@@ -44,7 +44,7 @@ EXPORTED = [
 # mgpu.h mgpu_option
 OPTIONS = {"stream_chunk": 2, "stream_ring": 3, "stream_same_chb": 4,
            "cluster_cs": 5, "cluster_async": 6, "profile_phases": 7, "qr_unblocked": 8, "ls_group": 9,
-           "stream_tiles": 10, "stream_exp": 11, "seq_sparse": 12}
+           "stream_tiles": 10, "seq_sparse": 12}
 
 
 # ---------------------------------------------------------------- errors
