@@ -202,3 +202,34 @@ def test_full_size_preconditioned_matches_oracle(mg, oracle, ne, m, pattern, nsh
         want = oracle.block_solve(A, [P], B, rtol=1e-10, maxit=k)
         np.testing.assert_array_equal(it[p * m:(p + 1) * m], want["iterations"])
         assert rel(X[p].T, want["X"]) < 1e-8
+
+
+@pytest.mark.parametrize("ne,m,l,pattern,k", [(6000, 4, 4, 0x11, 40), (50000, 1, 8, 0, 60), (200000, 4, 16, 0x11, 12)])
+def test_stream_kernel_reruns_are_bitwise_identical(mg, ne, m, l, pattern, k):
+    """The streaming kernel has no floating-point atomics and fixed reduction trees, and its warps
+    run ahead of each other between the stage barriers (per-warp buffer release, double-buffered
+    stage 0): a missing barrier would show up as run-to-run differences.  Five runs of the same
+    solve (the last shape with the tile plan and several tiles per block), every output array
+    compared bitwise."""
+    ctx = mg.default_context()
+    M, D, K = mg.model_hermite_device(ne, ctx=ctx)
+    shifts = [10.0 ** (1 + 3 * i / (l - 1)) for i in range(l)]
+    ops = mg.shifted_operators(M, D, K, shifts, ctx=ctx)
+    chains = [[f.matrix] for f in mg.spai_ls_batched(ops, None, pattern, ctx=ctx)]
+    n = 2 * ne
+    B = np.zeros((n, m))
+    for c in range(m):
+        B[2 * ((c + 1) * ne // m) - 2, c] = 1.0
+    ctx.set_cg_path("stream")
+    ctx.set_option("stream_tiles", 2)
+    try:
+        runs = [mg.cg_solve_batched(ops, chains, B, rtol=1e-10, maxit=k, ctx=ctx) for _ in range(5)]
+        assert ctx.last_cg_path == "stream"
+    finally:
+        ctx.set_cg_path("auto")
+        ctx.set_option("stream_tiles", 1)
+    for other in runs[1:]:
+        for a, b in zip(runs[0], other):
+            np.testing.assert_array_equal(a.X, b.X)
+            np.testing.assert_array_equal(a.iterations, b.iterations)
+    assert np.all(np.isfinite(runs[0][0].X)) and np.max(np.abs(runs[0][0].X)) > 0
