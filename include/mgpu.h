@@ -291,6 +291,11 @@ int mgpu_model_chain(int64_t n, double alpha, double beta, double stiffness_scal
 int mgpu_model_hermite(int64_t ne, double E, double I, double rho, double area, double L, double alpha, double beta,
                        mgpu_host_csr *M, mgpu_host_csr *D, mgpu_host_csr *K);
 void mgpu_host_free(mgpu_host_csr *a);
+/* Page-locks / releases a host range the caller keeps alive (cudaHostRegister): uploads from it
+ * then run as DMA at the link rate instead of through the driver's staging buffers.  The
+ * drop-in backend's C entry points pin their copy of M, D, K (re-uploaded on every prepare). */
+int mgpu_host_pin(mgpu_ctx *ctx, void *ptr, size_t bytes);
+int mgpu_host_unpin(mgpu_ctx *ctx, void *ptr);
 /* Device-side generation of the same Hermite cantilever: M, D, K assembled in HBM,
  * bitwise equal to mgpu_model_hermite (row-parallel element sums in element order, exact zeros dropped). */
 int mgpu_model_hermite_device(mgpu_ctx *ctx, int64_t ne, double E, double I, double rho, double area, double L,

@@ -634,6 +634,23 @@ int mgpu_csr_device_view(const mgpu_csr *a, int64_t *nrows, int64_t *nnz, const 
   return MGPU_OK;
 }
 
+int mgpu_host_pin(mgpu_ctx *ctx, void *ptr, size_t bytes)
+{
+  return guard(ctx, [&] {
+    MG_ARG(ptr != nullptr || bytes == 0, "mgpu_host_pin: null range");
+    if (bytes > 0)
+      MG_CUDA(cudaHostRegister(ptr, bytes, cudaHostRegisterDefault));
+  });
+}
+
+int mgpu_host_unpin(mgpu_ctx *ctx, void *ptr)
+{
+  return guard(ctx, [&] {
+    if (ptr != nullptr)
+      MG_CUDA(cudaHostUnregister(ptr));
+  });
+}
+
 int mgpu_csr_free(mgpu_csr *a)
 {
   if (a == nullptr)

@@ -20,6 +20,16 @@ struct mor_cuda_backend
   mor::SolveBackend &backend() { return multi ? static_cast<mor::SolveBackend &>(*multi) : *impl; }
   mor::SecondOrderSystem sys;
   int64_t n = 0;
+  // host ranges of `sys` that are page-locked (mgpu_host_pin): prepare() re-uploads M, D, K every
+  // time, from pinned memory that is a DMA at the link rate
+  std::vector<void *> pinned;
+  void unpin()
+  {
+    for (void *p : pinned)
+      mgpu_host_unpin(nullptr, p);
+    pinned.clear();
+  }
+  ~mor_cuda_backend() { unpin(); }
 };
 
 namespace
@@ -155,9 +165,20 @@ int mor_cuda_backend_set_system(mor_cuda_backend *b, int64_t n, int64_t nnz_m, c
   return guarded(msg, cap, [&] {
     if (!b || n < 0 || m < 0 || (m > 0 && !F))
       throw mor::ArgumentError("mor_cuda_backend_set_system: bad argument");
+    b->unpin(); // the old arrays go away with the assignments below
     b->sys.M = csr(n, nnz_m, m_rp, m_ci, m_v);
     b->sys.D = csr(n, nnz_d, d_rp, d_ci, d_v);
     b->sys.K = csr(n, nnz_k, k_rp, k_ci, k_v);
+    for (mor::SparseMatrix *A : {&b->sys.M, &b->sys.D, &b->sys.K})
+    {
+      auto pin = [&](void *p, size_t bytes) {
+        if (bytes >= (size_t(1) << 20) && mgpu_host_pin(nullptr, p, bytes) == MGPU_OK) // (small systems: not worth a registration)
+          b->pinned.push_back(p);
+      };
+      pin(A->row_ptr.data(), sizeof(A->row_ptr[0]) * A->row_ptr.size());
+      pin(A->col_idx.data(), sizeof(A->col_idx[0]) * A->col_idx.size());
+      pin(A->values.data(), sizeof(A->values[0]) * A->values.size());
+    }
     b->sys.F = mor::DenseMatrix(n, m);
     if (m > 0)
       std::memcpy(b->sys.F.values.data(), F, sizeof(double) * static_cast<size_t>(n * m));

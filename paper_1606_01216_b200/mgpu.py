@@ -38,7 +38,7 @@ EXPORTED = [
     "mgpu_csr_upload_batch", "mgpu_ctx_set_option", "mgpu_ctx_get_option", "mgpu_phase_profile",
     "mgpu_buffer_alloc", "mgpu_buffer_free", "mgpu_memcpy_d2h", "mgpu_memcpy_h2d",
     "mgpu_comm_unique_id", "mgpu_comm_init", "mgpu_comm_destroy", "mgpu_comm_allreduce_sum", "mgpu_comm_rows",
-    "mgpu_comm_columns_to_rows", "mgpu_comm_project_reduce", "mgpu_csr_bandwidth",
+    "mgpu_comm_columns_to_rows", "mgpu_comm_project_reduce", "mgpu_csr_bandwidth", "mgpu_host_pin", "mgpu_host_unpin",
 ]
 
 # mgpu.h mgpu_option
