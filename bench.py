@@ -422,8 +422,11 @@ def run_mgpu(args, rank, world, local_rank):
             plug_split.append((tp - t0, t1 - tp))
 
     def timed(fn):
+        import gc
         for _ in range(args.warmup):
             fn(None)
+        gc.collect()
+        gc.disable()  # no collector pauses inside the timed steps (host wall clock in the plugin leg)
         stream.synchronize()
         if dist:
             dist.barrier()
@@ -438,6 +441,7 @@ def run_mgpu(args, rank, world, local_rank):
         stream.synchronize()
         sampler.mark("t1")
         launches = ctx.launches - launches0
+        gc.enable()
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
