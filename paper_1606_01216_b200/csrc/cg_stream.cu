@@ -66,30 +66,6 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
                "l"(src), "r"(bytes), "r"(sm_addr(bar))
                : "memory");
 }
-// Same copy with an L2 eviction-priority policy (createpolicy) attached to its reads.
-__device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t pol)
-{
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
-               "%4;" ::"r"(sm_addr(dst)),
-               "l"(src), "r"(bytes), "r"(sm_addr(bar)), "l"(pol)
-               : "memory");
-}
-__device__ __forceinline__ uint64_t policy_evict_first()
-{
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-// L2-only store with an eviction-priority policy (data not re-read soon).
-__device__ __forceinline__ void stg_hint(double *p, double v, uint64_t pol)
-{
-  asm volatile("st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
-}
-// Drops a 128-byte L2 line without writing it back (its contents become undefined).
-__device__ __forceinline__ void discard_l2(const void *p)
-{
-  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
-}
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar)
 {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm_addr(bar)) : "memory");
