@@ -233,3 +233,38 @@ def test_stream_kernel_reruns_are_bitwise_identical(mg, ne, m, l, pattern, k):
             np.testing.assert_array_equal(a.X, b.X)
             np.testing.assert_array_equal(a.iterations, b.iterations)
     assert np.all(np.isfinite(runs[0][0].X)) and np.max(np.abs(runs[0][0].X)) > 0
+
+
+@pytest.mark.parametrize("n,m,l", [(2001, 1, 3), (4999, 3, 2), (20011, 1, 3), (20011, 4, 3), (6007, 7, 2), (6007, 5, 2)])
+def test_stream_kernel_ragged_shapes_match_oracle(mg, oracle, n, m, l):
+    """Odd orders (chunks whose element counts are odd: the pair loops' half-empty last pair and the
+    point blocks' 16-byte alignment), right-hand-side counts that are not the kernel's template
+    width (3 and 5 take the per-column scalar loops, 7 the generic ones) and, at n = 20011 with 3
+    shifts, the tile plan with three tiles per block: the reference chain model (T1, converges in a
+    few iterations) through the streaming kernel against the oracle's block_solve."""
+    M, D, K = oracle.chain_generate(n, consistent=True, stiffness_scale=1.0)
+    shifts = [10.0, 31.0, 100.0][:l]
+    ops = [oracle.shifted_operator(M, D, K, s) for s in shifts]
+    facs = [oracle.spai_build(A, mode=1)[0] for A in ops]
+    rng = np.random.default_rng(n + m)
+    B = rng.standard_normal((n, m))
+    B[:, 0] = 0.0
+    B[n // 3, 0] = 1.0
+    if m > 2:
+        B[:, 2] = 0.0  # a zero column: converged in 0 iterations, zeros out (krylov.cpp:44-51)
+    ctx = mg.default_context()
+    ctx.set_cg_path("stream")
+    ctx.set_option("stream_tiles", 2)
+    try:
+        got = mg.cg_solve_batched(ops, [[f] for f in facs], B, rtol=1e-10, ctx=ctx)
+        assert ctx.last_cg_path == "stream"
+    finally:
+        ctx.set_cg_path("auto")
+        ctx.set_option("stream_tiles", 1)
+    for A, P, g in zip(ops, facs, got):
+        want = oracle.block_solve(A, [P], B, rtol=1e-10)
+        assert np.all(np.abs(g.iterations - want["iterations"]) <= 2), (g.iterations, want["iterations"])
+        assert bool(np.all(g.converged)) == bool(want["all_converged"])
+        assert rel(g.X, want["X"]) < 1e-8
+        if m > 2:
+            assert not g.X[:, 2].any() and int(g.iterations[2]) == 0
