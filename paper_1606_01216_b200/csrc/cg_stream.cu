@@ -1435,38 +1435,9 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
   int optin = 0;
   MG_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
   const size_t stat = sizeof(BandShared<TB + 32>) + sizeof(PEll) * kTabSlots * (kMaxZ + 1) + 128;
-  // (chunk rows, ring depth) in order of preference; MGPU_STREAM_CFG="rows,depth" forces one (diagnostics)
-  // largest chunk first (per-chunk barriers and pipeline bookkeeping amortise over its rows), 3-deep ring
-  // before 2-deep at equal height.  With m >= 4 the height is capped at 448 rows and multiples of
-  // 128 rows are skipped: with every block striding through HBM in lock step, 512 / 640 rows
-  // measured 872 / 876 us per iteration on configs[3] against 843 / 836 for 576 / 448, and 448
-  // (2-deep) against the 576 default gave configs[3] 847 -> 837, configs[4] 4152 -> 4085.  m = 1
-  // (configs[2] shape) measured best on its largest chunk.
-  std::vector<std::pair<int64_t, int>> cands;
-  for (int64_t ch = 1024; ch >= 128; ch -= 64)
-  {
-    if (m >= 4 && (ch % 128 == 0 || ch > 448))
-      continue;
-    if (m < 4) // m >= 4: 2-deep only (448 rows 3-deep measured 924 us against 837 2-deep)
-      cands.push_back({ch, 3});
-    cands.push_back({ch, 2});
-  }
-  cands.push_back({128, 3});
-  cands.push_back({128, 2});
-  if (ctx->opt[MGPU_OPT_STREAM_CHUNK] > 0) // forced plan (diagnostics)
-  {
-    const int fd = ctx->opt[MGPU_OPT_STREAM_RING] ? static_cast<int>(ctx->opt[MGPU_OPT_STREAM_RING]) : 2;
-    cands.insert(cands.begin(), {ctx->opt[MGPU_OPT_STREAM_CHUNK], fd});
-  }
-  // every candidate first with the double-buffered stage 0 (no block-wide barrier at the end of a
-  // chunk), then with a single one: the chunk height comes first (configs[4] share: 448-row chunks
-  // with one stage-0 buffer 4841 us per iteration, 320-row chunks with two 5150)
-  for (size_t ci = 0; ci < 2 * cands.size() && CH == 0; ++ci)
-  {
-    const auto &cand = cands[ci / 2];
-    const bool dbl = (ci & 1) == 0;
-    const int64_t ch = cand.first;
-    const int nb = cand.second;
+  // One plan: fills P's shared-memory layout for (chunk rows, ring depth, stage 0 double-buffered);
+  // false when it does not fit.
+  auto plan = [&](int64_t ch, int nb, bool dbl) {
     size_t off = 0;
     auto take = [&](size_t bytes) {
       const size_t o2 = off;
@@ -1498,12 +1469,58 @@ bool stream_solve(mgpu_ctx *ctx, int l, const mgpu_csr *const *A, int z, const m
     P.s0_double = dbl ? 1 : 0;
     P.off_stage1 = z >= 1 ? take(sizeof(double) * (P.pst ? srows0 : ch + 2 * hal[1]) * m) : 0; // chain stages
     P.off_stage2 = z >= 2 ? take(sizeof(double) * (P.pst ? srows0 : ch + 2 * hal[2]) * m) : 0;
-    if (off + stat <= static_cast<size_t>(optin))
+    if (off + stat > static_cast<size_t>(optin))
+      return false;
+    dyn = off;
+    CH = ch;
+    P.nb = nb;
+    return true;
+  };
+  // Chunk height: as tall as shared memory allows (per-chunk barriers and pipeline bookkeeping
+  // amortise over its rows), with the double-buffered stage 0 (no block-wide barrier at the end of a
+  // chunk) unless that costs more than a tenth of the height.
+  //  * m >= 4: 2-deep ring (448 rows 3-deep measured 924 us against 837 2-deep), at most 448 rows,
+  //    no multiples of 128 rows (with every block striding through HBM in lock step 512 / 640 rows
+  //    measured 872 / 876 us per iteration on configs[3] against 843 / 836 for 576 / 448), in steps
+  //    of 16 rows: configs[3] with its factor 1083 us at 320 rows, 1069 at 336, 1060 at 352 (the
+  //    tallest with two stage-0 buffers), 1065 at 368 with one.  configs[4] share: 448 rows with one
+  //    stage-0 buffer 4841 us, 320 rows with two 5150.
+  //  * m < 4 (configs[2] shape): tallest chunk, 3-deep before 2-deep, measured best (26.8 us at
+  //    1024 rows, 30.7 at 512 / 3-deep, 39.9 at 256).
+  if (ctx->opt[MGPU_OPT_STREAM_CHUNK] > 0) // forced plan (diagnostics)
+  {
+    const int fd = ctx->opt[MGPU_OPT_STREAM_RING] ? static_cast<int>(ctx->opt[MGPU_OPT_STREAM_RING]) : 2;
+    if (!plan(ctx->opt[MGPU_OPT_STREAM_CHUNK], fd, true))
+      plan(ctx->opt[MGPU_OPT_STREAM_CHUNK], fd, false);
+  }
+  if (CH == 0 && m >= 4)
+  {
+    int64_t ch_single = 0, ch_double = 0;
+    for (int64_t ch = 448; ch >= 128 && (ch_single == 0 || ch_double == 0); ch -= 16)
     {
-      dyn = off;
-      CH = ch;
-      P.nb = nb;
+      if (ch % 128 == 0)
+        continue;
+      if (ch_single == 0 && plan(ch, 2, false))
+        ch_single = ch;
+      if (ch_double == 0 && plan(ch, 2, true))
+        ch_double = ch;
     }
+    CH = 0;
+    if (ch_double > 0 && 10 * ch_double >= 9 * ch_single)
+      plan(ch_double, 2, true);
+    else if (ch_single > 0)
+      plan(ch_single, 2, false);
+  }
+  if (CH == 0)
+  {
+    for (int64_t ch = 1024; ch >= 128 && CH == 0; ch -= 64)
+      for (int nb : {3, 2})
+      {
+        if (m >= 4 && nb == 3)
+          continue;
+        if (CH == 0 && !plan(ch, nb, true))
+          plan(ch, nb, false);
+      }
   }
   if (CH == 0)
     return false;

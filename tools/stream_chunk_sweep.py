@@ -15,7 +15,7 @@ B = np.zeros((2 * ne, m))
 for c in range(m):
     B[2 * ((c + 1) * ne // m) - 2, c] = 1.0
 ctx.set_cg_path("stream")
-for ch, ring in [(0, 0), (1024, 2), (768, 3), (512, 3), (512, 4), (384, 4), (256, 4), (256, 3), (128, 4), (320, 2), (320, 3), (192, 3)]:
+for ch, ring in [(0, 0)] + [(int(c), int(r)) for c, r in (x.split(":") for x in os.environ.get("SWEEP", "1024:2,768:3,512:3,512:4,384:4,256:4,256:3,320:2,192:3").split(","))]:
     ctx.set_option("stream_chunk", ch)
     if ch:
         ctx.set_option("stream_ring", ring)
